@@ -1,0 +1,210 @@
+/*
+ * krr_b200.h — C-ABI of the B200-native sketch-preconditioned KRR hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ operator / preconditioner /
+ * solver interfaces (reference = /root/reference/proj, a CPU-only Eigen library).
+ * Every entry point below names the reference interface it replaces (file:line).
+ * Plain pointers and sizes only; no torch, no Eigen, no C++ types.
+ *
+ * Conventions (mirroring the reference):
+ *   - All matrices are ROW-MAJOR fp64 (reference types.hpp:11-13: Matrix is
+ *     Eigen::RowMajor).  Multi-column vectors (n x t) are row-major too.
+ *   - Host pointers in, host pointers out, unless the function name ends in
+ *     `_device` (then all array pointers are device pointers on the context's GPU).
+ *   - Every function returns a krr_status.  On failure, krr_last_error() returns a
+ *     thread-local message.  Status codes map 1:1 onto the reference's exception
+ *     types (types.hpp:18-64); the Python / C++ mirrors rethrow the matching type.
+ *   - Calls are synchronous at return (the reference's pure-function semantics).
+ *     A context is used by one host thread at a time.
+ *   - There is no CPU fallback: every compute entry point runs CUDA kernels on the
+ *     context's device and fails with KRR_ERR_CUDA if the device is unusable.
+ */
+#ifndef KRR_B200_H
+#define KRR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KRR_B200_ABI_VERSION 1
+
+typedef enum krr_status {
+    KRR_OK = 0,
+    KRR_ERR_DIMENSION_MISMATCH = 1,    /* types.hpp:18  DimensionMismatch   (std::invalid_argument) */
+    KRR_ERR_NOT_POSITIVE_DEFINITE = 2, /* types.hpp:22  NotPositiveDefinite (std::runtime_error)   */
+    KRR_ERR_SINGULAR_TRIANGULAR = 3,   /* types.hpp:26  SingularTriangular  (std::runtime_error)   */
+    KRR_ERR_BREAKDOWN = 4,             /* types.hpp:48  BreakdownDetected   (std::runtime_error)   */
+    KRR_ERR_NON_POSITIVE_LAMBDA = 5,   /* types.hpp:38  NonPositiveLambda   (std::invalid_argument) */
+    KRR_ERR_INVALID_ARGUMENT = 6,      /* std::invalid_argument thrown by validate()/pcg_solve      */
+    KRR_ERR_CUDA = 7,                  /* device error (no reference equivalent)                   */
+    KRR_ERR_NCCL = 8,                  /* collective error (no reference equivalent)               */
+    KRR_ERR_STATE = 9,                 /* call out of order (e.g. matvec before krr_set_data)      */
+    KRR_ERR_CALLBACK = 10              /* a user operator callback reported failure                */
+} krr_status;
+
+typedef struct krr_ctx krr_ctx;
+
+/* Per-right-hand-side PCG statistics: reference solver.hpp:29-34 (RhsStats).
+ * residual_history is returned through a separate caller buffer. */
+typedef struct krr_rhs_stats {
+    int32_t iterations;
+    int32_t converged;
+    double final_residual;
+} krr_rhs_stats;
+
+/* ---------------------------------------------------------------- misc */
+const char* krr_last_error(void);
+int krr_abi_version(void);
+/* Number of CUDA devices visible (0 on a CPU-only host; never an error). */
+int krr_device_count(void);
+
+/* ---------------------------------------------------------------- context */
+/* Single-GPU context on `device`. */
+int krr_ctx_create(int device, krr_ctx** out);
+/* Rank `rank` of `world` (one process per GPU).  `nccl_id` is the 128-byte
+ * ncclUniqueId produced by krr_nccl_unique_id on rank 0 and broadcast by the
+ * caller (bench.py uses torch.distributed for that broadcast only). */
+int krr_nccl_unique_id(void* out_128_bytes);
+int krr_ctx_create_dist(int device, int rank, int world, const void* nccl_id, krr_ctx** out);
+int krr_ctx_destroy(krr_ctx* ctx);
+/* Number of kernels this context launched so far (bench.py's gpu_launches claim). */
+int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
+
+/* ---------------------------------------------------------------- data + kernel operator */
+/* Uploads X (n x d, row-major) to the device (replicated on every rank) and
+ * precomputes the row norms.  Replaces the data half of gram_matrix
+ * (kernels.cpp:72-77).  sigma > 0 (KernelSpec::validate, kernels.cpp:37-38). */
+int krr_set_data(krr_ctx* ctx, const double* X, int64_t n, int64_t d, double sigma);
+
+/* out = (K + lambda I) V for the Gaussian kernel, K never stored.  V and out are
+ * n x t row-major host buffers.  Replaces the dense `apply_a` lambda of
+ * solve_regularized (solver.cpp:75-77) applied to gram_matrix (kernels.cpp:72-88):
+ * K_ij = exp(-max(0, |x_i|^2 + |x_j|^2 - 2 x_i.x_j) / (2 sigma^2)), K_ii = 1,
+ * exact symmetry.  This is the LinearOperator adapter (solver.hpp:15). */
+int krr_kernel_matvec(krr_ctx* ctx, double lambda, const double* V, int64_t t, double* out);
+/* Same with device-resident V/out (n x t, row-major, on the context's device). */
+int krr_kernel_matvec_device(krr_ctx* ctx, double lambda, const double* dV, int64_t t,
+                             double* dOut);
+
+/* Rectangular K(A, X)·C with A = Xq (m x d host), the support set being the data
+ * already set on the context: cross_gram(Xq, X)·C (kernels.cpp:103-121,
+ * solver.cpp:135-139, predict_scores).  No diagonal forcing.  C is n x t. */
+int krr_predict_scores(krr_ctx* ctx, const double* Xq, int64_t m, const double* C, int64_t t,
+                       double* out);
+
+/* ---------------------------------------------------------------- random Fourier features */
+/* Host-side, reference-identical draw of the RFF tables: RffMap ctor
+ * (sketches.cpp:24-35) seeded with stage_seed(master, 0) (sketches.cpp:18-20):
+ * mt19937_64(master + 0x9E3779B97F4A7C15); W (s x d) row by row from
+ * normal_distribution(0, 1/sigma), then b (s) from uniform_real_distribution(0, 2pi).
+ * Pure host RNG (libstdc++), no device needed. */
+int krr_rff_realize(uint64_t master_seed, int64_t d, int64_t s, double sigma, double* W,
+                    double* b);
+/* Z = sqrt(2/s) cos(X W^T + b) on the device for the context's data
+ * (RffMap::apply + SketchChain::apply_rows, sketches.cpp:37-41,207-211).
+ * Z stays on the device (row-sharded across ranks). */
+int krr_rff_build(krr_ctx* ctx, const double* W, const double* b, int64_t s);
+/* Download the device Z (n x s row-major) — test/inspection helper. */
+int krr_rff_download(krr_ctx* ctx, double* Z);
+/* Upload an explicit Z (n x s) instead of building it from W, b — lets
+ * build_preconditioner(z, lambda_p) (precond.hpp:28) take any sketch. */
+int krr_sketch_upload(krr_ctx* ctx, const double* Z, int64_t n, int64_t s);
+
+/* ---------------------------------------------------------------- preconditioner */
+/* build_preconditioner (precond.cpp:20-40): G = Z^T Z + lambda_p I; Cholesky;
+ * on failure retry ONCE with 1e-12 trace(G)/s added to the diagonal, then
+ * KRR_ERR_NOT_POSITIVE_DEFINITE; U = L^-1 Z^T (stored in place of Z).
+ * lambda_p <= 0 -> KRR_ERR_NON_POSITIVE_LAMBDA.  *jitter_used (nullable)
+ * reports whether the retry fired. */
+int krr_precond_build(krr_ctx* ctx, double lambda_p, int* jitter_used);
+/* Preconditioner::apply / apply_columns (precond.cpp:10-18):
+ * out = (R - U^T (U R)) / lambda_p, R and out n x t row-major host buffers. */
+int krr_precond_apply(krr_ctx* ctx, const double* R, int64_t t, double* out);
+/* Download U (s x n row-major, the reference's Preconditioner::u) — test helper. */
+int krr_precond_download_u(krr_ctx* ctx, double* U);
+int krr_precond_drop(krr_ctx* ctx);
+
+/* ---------------------------------------------------------------- PCG */
+/* Device-resident PCG on (K + lambda I) C = Y for the context's data
+ * (solve_regularized, solver.cpp:69-94, per-column semantics of pcg_solve,
+ * solver.cpp:22-67: x0 = 0, recursive residual, stop when |r|/|y| <= tau,
+ * BreakdownDetected if p'Ap <= 0).  use_precond != 0 uses the built
+ * preconditioner, else plain CG (null M, solver.cpp:37,60).
+ * Y, C: n x t row-major host buffers.  stats: t entries.  residual_history
+ * (nullable): t x max_iter row-major, entries past stats[j].iterations untouched.
+ * total_matvecs (nullable) = sum of iterations (solver.cpp:88). */
+int krr_pcg_solve(krr_ctx* ctx, double lambda, const double* Y, int64_t t, double tau,
+                  int max_iter, int use_precond, double* C, krr_rhs_stats* stats,
+                  double* residual_history, int64_t* total_matvecs);
+
+/* Generic pcg_solve (solver.hpp:55-57) over caller operators: the PCG vector
+ * algebra runs on the device; apply_a / apply_m are host callbacks
+ * (in, out are host arrays of length n; return 0 on success).  apply_m may be
+ * NULL (plain CG).  observer (nullable) sees (it, x) after each update
+ * (solver.cpp:54).  Used by the drop-in LinearOperator form of the API. */
+typedef int (*krr_operator_cb)(void* user, const double* in, double* out, int64_t n);
+typedef void (*krr_observer_cb)(void* user, int it, const double* x, int64_t n);
+int krr_pcg_solve_operator(krr_ctx* ctx, int64_t n, krr_operator_cb apply_a, void* user_a,
+                           krr_operator_cb apply_m, void* user_m, const double* y, double tau,
+                           int max_iter, krr_observer_cb observer, void* user_obs, double* x,
+                           krr_rhs_stats* stats, double* residual_history);
+
+/* ---------------------------------------------------------------- end-to-end train */
+/* train (solver.cpp:96-133) for the Gaussian kernel with a single RFF stage
+ * (ChainSpec{RandomFourier, s1 = s}): set data, realize the chain with
+ * master_seed, build Z on the device, build the preconditioner (lambda_p <= 0
+ * means "defaults to lambda", solver.cpp:102), solve every column.
+ * X n x d, Y n x t, C out n x t (host).  phase_ms (nullable, 4 doubles):
+ * rff build, precond build, solve, total — CUDA-event timed. */
+int krr_train(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const double* Y, int64_t t,
+              double sigma, double lambda, double lambda_p, int64_t s, uint64_t master_seed,
+              double tau, int max_iter, double* C, krr_rhs_stats* stats,
+              double* residual_history, int64_t* total_matvecs, double* phase_ms);
+
+/* ---------------------------------------------------------------- schedule (host only) */
+/* The symmetric super-tile schedule of the fused kernel mat-vec, exported so the
+ * multi-rank partition can be checked on a CPU-only host.  For n points and
+ * `world` ranks: *super_rows receives the super-tile edge (rows), *num_super the
+ * number of super-rows NS, and (if tiles != NULL, capacity max_tiles) the
+ * (a, b) pairs (a <= b) owned by `rank`, flattened.  *num_tiles = count. */
+int krr_schedule(int64_t n, int world, int rank, int64_t* super_rows, int64_t* num_super,
+                 int32_t* tiles, int64_t max_tiles, int64_t* num_tiles);
+
+/* Row shard [*row_begin, *row_end) of the n sketch rows (Z / U) owned by `rank`:
+ * contiguous equal blocks of ceil(n / world) rows. */
+int krr_shard_rows(int64_t n, int world, int rank, int64_t* row_begin, int64_t* row_end);
+
+/* ---------------------------------------------------------------- synthetic configs */
+/* Deterministic generators for BASELINE.json configs 1-5.
+ * cfg in 1..5; X n x d, Y n x t (host).  Pure host code (libstdc++ RNG). */
+int krr_generate_config(int cfg, int64_t n, int64_t d, int64_t t, uint64_t seed, double* X,
+                        double* Y);
+/* rlsc_encode (solver.cpp:152-161): +1 for the true class, -1 otherwise. */
+int krr_rlsc_encode(const int32_t* classes, int64_t n, int32_t num_classes, double* Y);
+
+/* ---------------------------------------------------------------- measurement */
+/* Runs `steps` device-resident (K + lambda I) v mat-vecs (K1 + finish + the
+ * all-reduce when world > 1) back to back on the context's stream over a
+ * seeded N(0,1) vector and CUDA-event-times them: *total_ms = whole span,
+ * *k1_ms = mean duration of the fused K1 kernel launch alone (per step). */
+int krr_bench_matvec(krr_ctx* ctx, double lambda, int steps, double* total_ms, double* k1_ms);
+
+/* ---------------------------------------------------------------- diagnostics */
+/* Micro-benchmarks run on the context's device: FP64 DMMA and DFMA issue rates,
+ * and the Gaussian-epilogue throughput (results in the 8-double array:
+ * [dmma_tflops, dfma_tflops, dmma+dfma concurrent tflops, exp_libdevice_geval,
+ *  exp_table_geval, sm_count, clock_mhz, reserved]). */
+int krr_microbench(krr_ctx* ctx, double* results);
+/* Evaluate the device Gaussian epilogue exp(-max(0,d2)*scale) for n host values
+ * (mode 0 = libdevice exp, 1 = table exp used by the mat-vec) — accuracy tests. */
+int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale, int mode,
+                        double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KRR_B200_H */

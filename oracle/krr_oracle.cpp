@@ -1,0 +1,548 @@
+// =============================================================================
+// oracle/krr_oracle.cpp — CPU RESTATEMENT of the reference KRR hot path.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs may load this library, and only as the
+// checker or the timed CPU baseline — never as part of the product path.
+//
+// What it restates (all citations are /root/reference/proj/core/... file:line):
+//   * kernels.cpp:72-88   gram_matrix (Gaussian): sq = rowwise |x|^2, P = X X^T,
+//                         K_ij = exp(-max(0, sq_i + sq_j - 2 P_ij) * scale),
+//                         scale = 1/(2 sigma^2), K_ii = 1, upper triangle mirrored.
+//   * solver.cpp:75-77    apply_a(v) = K v + lambda v  (dense, and an on-the-fly
+//                         variant with the identical per-entry formula).
+//   * sketches.cpp:18-41  stage_seed, RffMap ctor (mt19937_64, normal(0,1/sigma)
+//                         for W row by row, THEN uniform(0, 2pi) for b), apply.
+//   * sketches.cpp:207-211 apply_rows (row by row).
+//   * numerics.cpp:49-79  cholesky (lower LLT, NotPositiveDefinite), triangular_solve
+//                         (SingularTriangular when min |diag| < 1e-300).
+//   * precond.cpp:10-40   build_preconditioner (G = Z^T Z + lambda_p I, one jitter
+//                         retry of 1e-12 trace/s, U = L^-1 Z^T), apply (x - U^T U x)/lambda_p.
+//   * solver.cpp:22-67    pcg_solve (x0 = 0, recursive residual, breakdown check).
+//   * solver.cpp:69-94    solve_regularized (sequential per-column PCG).
+//   * solver.cpp:96-133   train (non-adaptive RFF chain).
+//
+// Why C++ and not plain C: the reference draws its RFF tables with libstdc++'s
+// std::normal_distribution / std::uniform_real_distribution, whose algorithms are
+// implementation-defined.  Using the same libstdc++ (GCC 13.3 here and on the GPU
+// box image) reproduces W and b bit for bit.
+//
+// Why not the reference itself: it needs Eigen3 (core/CMakeLists.txt:1,17), which is
+// absent from this image, so it is unbuildable here.  Eigen's
+// internal summation orders (GEMM/GEMV/LLT blocking) therefore cannot be reproduced
+// bit for bit; the restatement uses plain forward-order loops and the parity bar is
+// the tolerance-based one the reference's own tests use.  `sum_order` = 1 switches
+// every reduction to reverse order, which measures the self-consistency floor (two
+// legitimate summation orders of the same algorithm).
+//
+// Compile: see oracle/Makefile (g++ -O2 -ffp-contract=off -fopenmp; no -march, so,
+// like the reference's default Release build, no FMA contraction).
+// =============================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numbers>
+#include <random>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace {
+
+// Status codes: identical numbering to include/krr_b200.h.
+enum {
+    OK = 0,
+    DIMENSION_MISMATCH = 1,
+    NOT_POSITIVE_DEFINITE = 2,
+    SINGULAR_TRIANGULAR = 3,
+    BREAKDOWN = 4,
+    NON_POSITIVE_LAMBDA = 5,
+    INVALID_ARGUMENT = 6,
+};
+
+constexpr std::uint64_t kStageSeedStride = 0x9E3779B97F4A7C15ULL;  // sketches.hpp:14
+
+// sketches.cpp:18-20
+std::uint64_t stage_seed(std::uint64_t master, int stage) {
+    return master + std::uint64_t(stage + 1) * kStageSeedStride;
+}
+
+double dot(const double* a, const double* b, std::int64_t n, int order) {
+    double s = 0.0;
+    if (order == 0) {
+        for (std::int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+    } else {
+        for (std::int64_t i = n - 1; i >= 0; --i) s += a[i] * b[i];
+    }
+    return s;
+}
+
+double dot_strided(const double* a, std::int64_t sa, const double* b, std::int64_t sb,
+                   std::int64_t n, int order) {
+    double s = 0.0;
+    if (order == 0) {
+        for (std::int64_t i = 0; i < n; ++i) s += a[i * sa] * b[i * sb];
+    } else {
+        for (std::int64_t i = n - 1; i >= 0; --i) s += a[i * sa] * b[i * sb];
+    }
+    return s;
+}
+
+// One Gaussian kernel entry, kernels.cpp:79-84 (pair ordered a < b as in the
+// reference's upper-triangle loop, so K(i,j) and K(j,i) are bitwise equal).
+inline double gauss_entry(const double* x, std::int64_t d, const double* sq, std::int64_t i,
+                          std::int64_t j, double scale, int order) {
+    if (i == j) return 1.0;  // kernels.cpp:81
+    const std::int64_t a = std::min(i, j), b = std::max(i, j);
+    const double p = dot(x + a * d, x + b * d, d, order);
+    const double d2 = std::max(0.0, sq[a] + sq[b] - 2.0 * p);
+    return std::exp(-d2 * scale);
+}
+
+std::vector<double> row_sq_norms(const double* x, std::int64_t n, std::int64_t d, int order) {
+    std::vector<double> sq(static_cast<std::size_t>(n));
+    for (std::int64_t i = 0; i < n; ++i) sq[std::size_t(i)] = dot(x + i * d, x + i * d, d, order);
+    return sq;
+}
+
+// Lower Cholesky A = L L^T (numerics.cpp:49-55).  Row-major s x s.  Returns
+// NOT_POSITIVE_DEFINITE on a non-positive (or non-finite) pivot.
+int cholesky_inplace(std::vector<double>& a, std::int64_t s) {
+    for (std::int64_t j = 0; j < s; ++j) {
+        double x = a[std::size_t(j * s + j)];
+        for (std::int64_t k = 0; k < j; ++k) {
+            const double l = a[std::size_t(j * s + k)];
+            x -= l * l;
+        }
+        if (!(x > 0.0) || !std::isfinite(x)) return NOT_POSITIVE_DEFINITE;
+        const double ljj = std::sqrt(x);
+        a[std::size_t(j * s + j)] = ljj;
+        for (std::int64_t i = j + 1; i < s; ++i) {
+            double v = a[std::size_t(i * s + j)];
+            for (std::int64_t k = 0; k < j; ++k)
+                v -= a[std::size_t(i * s + k)] * a[std::size_t(j * s + k)];
+            a[std::size_t(i * s + j)] = v / ljj;
+        }
+    }
+    for (std::int64_t i = 0; i < s; ++i)
+        for (std::int64_t j = i + 1; j < s; ++j) a[std::size_t(i * s + j)] = 0.0;
+    return OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int oracle_abi_version(void) { return 1; }
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
+// ---------------------------------------------------------------- test-support RNG
+// Restates tests/support/oracles.cpp:87-102 (random_matrix / random_vector): mt19937_64
+// + normal_distribution(0, scale), row-major — so the ported known-answer tests feed
+// exactly the inputs the reference's own tests use.
+void oracle_random_matrix(std::int64_t rows, std::int64_t cols, std::uint64_t seed, double scale,
+                          double* out) {
+    std::mt19937_64 gen(seed);
+    std::normal_distribution<double> normal(0.0, scale);
+    for (std::int64_t i = 0; i < rows * cols; ++i) out[i] = normal(gen);
+}
+
+// acceptance.cpp:157-159 style uniform draws (mt19937_64 + uniform_real(lo, hi)).
+void oracle_random_uniform(std::int64_t count, std::uint64_t seed, double lo, double hi,
+                           double* out) {
+    std::mt19937_64 gen(seed);
+    std::uniform_real_distribution<double> u(lo, hi);
+    for (std::int64_t i = 0; i < count; ++i) out[i] = u(gen);
+}
+
+// ---------------------------------------------------------------- RFF (sketches.cpp:24-41)
+int oracle_rff_realize(std::uint64_t master_seed, std::int64_t d, std::int64_t s, double sigma,
+                       double* w, double* b) {
+    if (s < 1) return INVALID_ARGUMENT;
+    if (!(sigma > 0.0)) return INVALID_ARGUMENT;
+    std::mt19937_64 gen(stage_seed(master_seed, 0));
+    std::normal_distribution<double> freq(0.0, 1.0 / sigma);
+    std::uniform_real_distribution<double> phase(0.0, 2.0 * std::numbers::pi);
+    for (std::int64_t i = 0; i < s; ++i)
+        for (std::int64_t j = 0; j < d; ++j) w[i * d + j] = freq(gen);
+    for (std::int64_t i = 0; i < s; ++i) b[i] = phase(gen);
+    return OK;
+}
+
+// apply_rows: z_i = sqrt(2/s) cos(W x_i + b)
+int oracle_rff_apply_rows(const double* x, std::int64_t n, std::int64_t d, const double* w,
+                          const double* b, std::int64_t s, double* z, int order) {
+    const double scale = std::sqrt(2.0 / double(s));
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t k = 0; k < s; ++k)
+            z[i * s + k] = scale * std::cos(dot(w + k * d, x + i * d, d, order) + b[k]);
+    return OK;
+}
+
+// ---------------------------------------------------------------- kernels (kernels.cpp:72-88)
+int oracle_gram_matrix(const double* x, std::int64_t n, std::int64_t d, double sigma, double* k,
+                       int order) {
+    if (!(sigma > 0.0)) return INVALID_ARGUMENT;
+    const std::vector<double> sq = row_sq_norms(x, n, d, order);
+    const double scale = 1.0 / (2.0 * sigma * sigma);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (std::int64_t i = 0; i < n; ++i) {
+        k[i * n + i] = 1.0;
+        for (std::int64_t j = i + 1; j < n; ++j) {
+            const double v = gauss_entry(x, d, sq.data(), i, j, scale, order);
+            k[i * n + j] = v;
+            k[j * n + i] = v;
+        }
+    }
+    return OK;
+}
+
+// cross_gram (kernels.cpp:103-121): no diagonal forcing.
+int oracle_cross_gram(const double* a, std::int64_t m, const double* b, std::int64_t n,
+                      std::int64_t d, double sigma, double* k, int order) {
+    if (!(sigma > 0.0)) return INVALID_ARGUMENT;
+    const std::vector<double> sqa = row_sq_norms(a, m, d, order);
+    const std::vector<double> sqb = row_sq_norms(b, n, d, order);
+    const double scale = 1.0 / (2.0 * sigma * sigma);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < m; ++i)
+        for (std::int64_t j = 0; j < n; ++j) {
+            const double p = dot(a + i * d, b + j * d, d, order);
+            k[i * n + j] = std::exp(-std::max(0.0, sqa[std::size_t(i)] + sqb[std::size_t(j)] - 2.0 * p) * scale);
+        }
+    return OK;
+}
+
+// out[r, :] = ((K + lambda I) V)[r, :] for r in [row_begin, row_end), K on the fly.
+// V is n x t row-major; out is (row_end - row_begin) x t.
+int oracle_kernel_matvec(const double* x, std::int64_t n, std::int64_t d, double sigma,
+                         double lambda, const double* v, std::int64_t t, double* out,
+                         std::int64_t row_begin, std::int64_t row_end, int order) {
+    if (!(sigma > 0.0)) return INVALID_ARGUMENT;
+    if (row_begin < 0 || row_end > n || row_begin > row_end) return DIMENSION_MISMATCH;
+    const std::vector<double> sq = row_sq_norms(x, n, d, order);
+    const double scale = 1.0 / (2.0 * sigma * sigma);
+#pragma omp parallel
+    {
+        std::vector<double> acc(static_cast<std::size_t>(t));
+        std::vector<double> krow(static_cast<std::size_t>(n));
+#pragma omp for schedule(dynamic, 4)
+        for (std::int64_t i = row_begin; i < row_end; ++i) {
+            for (std::int64_t j = 0; j < n; ++j)
+                krow[std::size_t(j)] = gauss_entry(x, d, sq.data(), i, j, scale, order);
+            for (std::int64_t c = 0; c < t; ++c) {
+                const double kv = dot_strided(krow.data(), 1, v + c, t, n, order);
+                out[(i - row_begin) * t + c] = kv + lambda * v[i * t + c];
+            }
+        }
+    }
+    return OK;
+}
+
+// Dense (K + lambda I) V with K given (solver.cpp:75-77).
+int oracle_dense_matvec(const double* k, std::int64_t n, double lambda, const double* v,
+                        std::int64_t t, double* out, int order) {
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t c = 0; c < t; ++c)
+            out[i * t + c] = dot_strided(k + i * n, 1, v + c, t, n, order) + lambda * v[i * t + c];
+    return OK;
+}
+
+// ---------------------------------------------------------------- numerics (numerics.cpp:49-79)
+int oracle_cholesky(const double* a, std::int64_t s, double* l) {
+    std::vector<double> m(a, a + s * s);
+    const int st = cholesky_inplace(m, s);
+    if (st != OK) return st;
+    std::memcpy(l, m.data(), sizeof(double) * std::size_t(s * s));
+    return OK;
+}
+
+// side 0 = Left (L X = B, B is s x m), 1 = Right (X L = B, B is m x s); transpose
+// replaces L by L^T.  Row-major everywhere.
+int oracle_triangular_solve(const double* l, std::int64_t s, const double* bmat, std::int64_t m,
+                            int side, int transpose, double* xout) {
+    for (std::int64_t i = 0; i < s; ++i)
+        if (std::abs(l[i * s + i]) < 1e-300) return SINGULAR_TRIANGULAR;  // numerics.cpp:62-63
+    auto L = [&](std::int64_t i, std::int64_t j) { return transpose ? l[j * s + i] : l[i * s + j]; };
+    const bool lower = !transpose;  // effective triangle of op(L)
+    if (side == 0) {
+        // op(L) X = B, X is s x m: solve column by column.
+        std::memcpy(xout, bmat, sizeof(double) * std::size_t(s * m));
+        for (std::int64_t c = 0; c < m; ++c) {
+            if (lower) {
+                for (std::int64_t i = 0; i < s; ++i) {
+                    double v = xout[i * m + c];
+                    for (std::int64_t k = 0; k < i; ++k) v -= L(i, k) * xout[k * m + c];
+                    xout[i * m + c] = v / L(i, i);
+                }
+            } else {
+                for (std::int64_t i = s - 1; i >= 0; --i) {
+                    double v = xout[i * m + c];
+                    for (std::int64_t k = i + 1; k < s; ++k) v -= L(i, k) * xout[k * m + c];
+                    xout[i * m + c] = v / L(i, i);
+                }
+            }
+        }
+    } else {
+        // X op(L) = B  <=>  op(L)^T X^T = B^T; X is m x s.
+        std::memcpy(xout, bmat, sizeof(double) * std::size_t(s * m));
+        for (std::int64_t r = 0; r < m; ++r) {
+            double* row = xout + r * s;
+            if (lower) {  // op(L)^T upper: back substitution over columns of op(L)
+                for (std::int64_t j = s - 1; j >= 0; --j) {
+                    double v = row[j];
+                    for (std::int64_t k = j + 1; k < s; ++k) v -= row[k] * L(k, j);
+                    row[j] = v / L(j, j);
+                }
+            } else {
+                for (std::int64_t j = 0; j < s; ++j) {
+                    double v = row[j];
+                    for (std::int64_t k = 0; k < j; ++k) v -= row[k] * L(k, j);
+                    row[j] = v / L(j, j);
+                }
+            }
+        }
+    }
+    return OK;
+}
+
+// ---------------------------------------------------------------- precond (precond.cpp:10-40)
+// Z n x s row-major -> U s x n row-major.  jitter_used (nullable).
+int oracle_build_preconditioner(const double* z, std::int64_t n, std::int64_t s, double lambda_p,
+                                double* u, int* jitter_used, int order) {
+    if (!(lambda_p > 0.0)) return NON_POSITIVE_LAMBDA;
+    std::vector<double> g(static_cast<std::size_t>(s * s));
+#pragma omp parallel for schedule(dynamic, 8)
+    for (std::int64_t a = 0; a < s; ++a)
+        for (std::int64_t b = 0; b <= a; ++b) {
+            const double v = dot_strided(z + a, s, z + b, s, n, order);
+            g[std::size_t(a * s + b)] = v;
+            g[std::size_t(b * s + a)] = v;
+        }
+    for (std::int64_t a = 0; a < s; ++a) g[std::size_t(a * s + a)] += lambda_p;
+
+    std::vector<double> l = g;
+    int st = cholesky_inplace(l, s);
+    if (jitter_used) *jitter_used = 0;
+    if (st == NOT_POSITIVE_DEFINITE) {
+        double trace = 0.0;
+        for (std::int64_t a = 0; a < s; ++a) trace += g[std::size_t(a * s + a)];
+        for (std::int64_t a = 0; a < s; ++a) g[std::size_t(a * s + a)] += 1e-12 * trace / double(s);
+        l = g;
+        st = cholesky_inplace(l, s);
+        if (jitter_used) *jitter_used = 1;
+    }
+    if (st != OK) return st;
+    for (std::int64_t i = 0; i < s; ++i)
+        if (std::abs(l[std::size_t(i * s + i)]) < 1e-300) return SINGULAR_TRIANGULAR;
+    // U = L^-1 Z^T: forward substitution, one column (data point) at a time.
+#pragma omp parallel for schedule(static)
+    for (std::int64_t c = 0; c < n; ++c) {
+        for (std::int64_t i = 0; i < s; ++i) {
+            double v = z[c * s + i];
+            if (order == 0) {
+                for (std::int64_t k = 0; k < i; ++k) v -= l[std::size_t(i * s + k)] * u[k * n + c];
+            } else {
+                for (std::int64_t k = i - 1; k >= 0; --k) v -= l[std::size_t(i * s + k)] * u[k * n + c];
+            }
+            u[i * n + c] = v / l[std::size_t(i * s + i)];
+        }
+    }
+    return OK;
+}
+
+// (X - U^T (U X)) / lambda_p, X and out n x t row-major.
+int oracle_precond_apply(const double* u, std::int64_t s, std::int64_t n, double lambda_p,
+                         const double* xin, std::int64_t t, double* out, int order) {
+    std::vector<double> w(static_cast<std::size_t>(s * t));
+#pragma omp parallel for schedule(static)
+    for (std::int64_t k = 0; k < s; ++k)
+        for (std::int64_t c = 0; c < t; ++c)
+            w[std::size_t(k * t + c)] = dot_strided(u + k * n, 1, xin + c, t, n, order);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t c = 0; c < t; ++c) {
+            const double utw = dot_strided(u + i, n, w.data() + c, t, s, order);
+            out[i * t + c] = (xin[i * t + c] - utw) / lambda_p;
+        }
+    return OK;
+}
+
+// ---------------------------------------------------------------- PCG (solver.cpp:22-67)
+typedef int (*oracle_op)(void* user, const double* in, double* out, std::int64_t n);
+typedef void (*oracle_observer)(void* user, int it, const double* x, std::int64_t n);
+
+int oracle_pcg_solve(std::int64_t n, oracle_op apply_a, void* ua, oracle_op apply_m, void* um,
+                     const double* y, double tau, int max_iter, oracle_observer obs, void* uo,
+                     double* x, int* iterations, int* converged, double* final_residual,
+                     double* history, int order) {
+    if (!(tau > 0.0)) return INVALID_ARGUMENT;
+    if (max_iter < 1) return INVALID_ARGUMENT;
+    std::vector<double> r(y, y + n), z(static_cast<std::size_t>(n)), p(static_cast<std::size_t>(n)), ap(static_cast<std::size_t>(n));
+    std::fill(x, x + n, 0.0);
+    *iterations = 0;
+    *converged = 0;
+    *final_residual = 0.0;
+    const double norm_y = std::sqrt(dot(y, y, n, order));
+    if (norm_y == 0.0) {
+        *converged = 1;
+        return OK;
+    }
+    if (apply_m) {
+        if (apply_m(um, r.data(), z.data(), n) != 0) return INVALID_ARGUMENT;
+    } else {
+        z = r;
+    }
+    p = z;
+    double rz = dot(r.data(), z.data(), n, order);
+    for (int it = 1; it <= max_iter; ++it) {
+        if (apply_a(ua, p.data(), ap.data(), n) != 0) return INVALID_ARGUMENT;
+        const double pap = dot(p.data(), ap.data(), n, order);
+        if (!(pap > 0.0)) return BREAKDOWN;
+        const double alpha = rz / pap;
+        for (std::int64_t i = 0; i < n; ++i) x[i] += alpha * p[std::size_t(i)];
+        for (std::int64_t i = 0; i < n; ++i) r[std::size_t(i)] -= alpha * ap[std::size_t(i)];
+        const double rel = std::sqrt(dot(r.data(), r.data(), n, order)) / norm_y;
+        *iterations = it;
+        *final_residual = rel;
+        if (history) history[it - 1] = rel;
+        if (obs) obs(uo, it, x, n);
+        if (rel <= tau) {
+            *converged = 1;
+            return OK;
+        }
+        if (apply_m) {
+            if (apply_m(um, r.data(), z.data(), n) != 0) return INVALID_ARGUMENT;
+        } else {
+            z = r;
+        }
+        const double rz_next = dot(r.data(), z.data(), n, order);
+        const double beta = rz_next / rz;
+        for (std::int64_t i = 0; i < n; ++i) p[std::size_t(i)] = z[std::size_t(i)] + beta * p[std::size_t(i)];
+        rz = rz_next;
+    }
+    *converged = 0;
+    return OK;
+}
+
+// ---------------------------------------------------------------- train (solver.cpp:96-133)
+namespace {
+struct DenseOp {
+    const double* k;
+    std::int64_t n;
+    double lambda;
+    int order;
+};
+int dense_op(void* u, const double* in, double* out, std::int64_t n) {
+    const auto* o = static_cast<const DenseOp*>(u);
+    (void)n;
+    return oracle_dense_matvec(o->k, o->n, o->lambda, in, 1, out, o->order);
+}
+struct OtfOp {
+    const double* x;
+    std::int64_t n, d;
+    double sigma, lambda;
+    int order;
+};
+int otf_op(void* u, const double* in, double* out, std::int64_t n) {
+    const auto* o = static_cast<const OtfOp*>(u);
+    (void)n;
+    return oracle_kernel_matvec(o->x, o->n, o->d, o->sigma, o->lambda, in, 1, out, 0, o->n, o->order);
+}
+struct PrecOp {
+    const double* u;
+    std::int64_t s, n;
+    double lambda_p;
+    int order;
+};
+int prec_op(void* u, const double* in, double* out, std::int64_t n) {
+    const auto* o = static_cast<const PrecOp*>(u);
+    (void)n;
+    return oracle_precond_apply(o->u, o->s, o->n, o->lambda_p, in, 1, out, o->order);
+}
+}  // namespace
+
+// solve_regularized with the Gaussian operator: dense_k != 0 materialises K like the
+// reference (solver.cpp:101); dense_k == 0 computes it on the fly (same entries).
+// u == NULL -> plain CG.  Y, C n x t row-major; iterations/converged/final_residual
+// arrays of t; history t x max_iter (nullable).
+int oracle_solve_gaussian(const double* x, std::int64_t n, std::int64_t d, double sigma,
+                          double lambda, const double* u, std::int64_t s, double lambda_p,
+                          const double* ymat, std::int64_t t, double tau, int max_iter,
+                          int dense_k, double* c, int* iterations, int* converged,
+                          double* final_residual, double* history, long long* total_matvecs,
+                          int order) {
+    if (!(lambda > 0.0)) return NON_POSITIVE_LAMBDA;
+    std::vector<double> k;
+    DenseOp dop{nullptr, n, lambda, order};
+    OtfOp oop{x, n, d, sigma, lambda, order};
+    if (dense_k) {
+        k.resize(std::size_t(n * n));
+        const int st = oracle_gram_matrix(x, n, d, sigma, k.data(), order);
+        if (st != OK) return st;
+        dop.k = k.data();
+    }
+    PrecOp pop{u, s, n, lambda_p, order};
+    std::vector<double> ycol(static_cast<std::size_t>(n)), xcol(static_cast<std::size_t>(n));
+    long long total = 0;
+    for (std::int64_t j = 0; j < t; ++j) {
+        for (std::int64_t i = 0; i < n; ++i) ycol[std::size_t(i)] = ymat[i * t + j];
+        const int st = oracle_pcg_solve(n, dense_k ? dense_op : otf_op,
+                                        dense_k ? static_cast<void*>(&dop) : static_cast<void*>(&oop),
+                                        u ? prec_op : nullptr, &pop, ycol.data(), tau, max_iter,
+                                        nullptr, nullptr, xcol.data(), &iterations[j], &converged[j],
+                                        &final_residual[j],
+                                        history ? history + j * max_iter : nullptr, order);
+        if (st != OK) return st;
+        for (std::int64_t i = 0; i < n; ++i) c[i * t + j] = xcol[std::size_t(i)];
+        total += iterations[j];
+    }
+    if (total_matvecs) *total_matvecs = total;
+    return OK;
+}
+
+// Full train: lambda_p <= 0 means "defaults to lambda" (solver.cpp:102).
+int oracle_train(const double* x, std::int64_t n, std::int64_t d, const double* ymat,
+                 std::int64_t t, double sigma, double lambda, double lambda_p, std::int64_t s,
+                 std::uint64_t seed, double tau, int max_iter, int dense_k, double* c,
+                 int* iterations, int* converged, double* final_residual, double* history,
+                 long long* total_matvecs, int order) {
+    if (n < 1) return INVALID_ARGUMENT;                   // solver.cpp:97
+    if (!(lambda > 0.0)) return NON_POSITIVE_LAMBDA;      // solver.cpp:98
+    if (!(sigma > 0.0)) return INVALID_ARGUMENT;          // KernelSpec::validate
+    if (s < 1) return INVALID_ARGUMENT;                   // ChainSpec::validate
+    const double lp = lambda_p > 0.0 ? lambda_p : lambda;
+    std::vector<double> w(static_cast<std::size_t>(s * d)), b(static_cast<std::size_t>(s)), z(static_cast<std::size_t>(n * s)),
+        u(static_cast<std::size_t>(s * n));
+    int st = oracle_rff_realize(seed, d, s, sigma, w.data(), b.data());
+    if (st != OK) return st;
+    st = oracle_rff_apply_rows(x, n, d, w.data(), b.data(), s, z.data(), order);
+    if (st != OK) return st;
+    st = oracle_build_preconditioner(z.data(), n, s, lp, u.data(), nullptr, order);
+    if (st != OK) return st;
+    return oracle_solve_gaussian(x, n, d, sigma, lambda, u.data(), s, lp, ymat, t, tau, max_iter,
+                                 dense_k, c, iterations, converged, final_residual, history,
+                                 total_matvecs, order);
+}
+
+}  // extern "C"

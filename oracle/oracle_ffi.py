@@ -1,0 +1,285 @@
+"""ctypes binding of oracle/liboracle.so — the CPU restatement of the reference path.
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+CPU-baseline legs (cpu_baseline and --impl reference), never by the product package.
+Every function cites the reference code it restates (see krr_oracle.cpp's header).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "liboracle.so"
+
+OK, DIMENSION_MISMATCH, NOT_POSITIVE_DEFINITE, SINGULAR_TRIANGULAR, BREAKDOWN, \
+    NON_POSITIVE_LAMBDA, INVALID_ARGUMENT = range(7)
+
+
+class OracleError(Exception):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: oracle status {status}")
+        self.status = status
+
+
+def build() -> Path:
+    subprocess.run(["make", "-C", str(HERE)], check=True, capture_output=True)
+    return LIB_PATH
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        build()
+    return C.CDLL(str(LIB_PATH))
+
+
+_L = None
+_vp, _i64, _d, _i = C.c_void_p, C.c_int64, C.c_double, C.c_int
+OP_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+OBS_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_int64)
+
+
+def lib() -> C.CDLL:
+    global _L
+    if _L is None:
+        L = _load()
+        sigs = {
+            "oracle_num_threads": ([], _i),
+            "oracle_set_num_threads": ([_i], None),
+            "oracle_random_matrix": ([_i64, _i64, C.c_uint64, _d, _vp], None),
+            "oracle_random_uniform": ([_i64, C.c_uint64, _d, _d, _vp], None),
+            "oracle_rff_realize": ([C.c_uint64, _i64, _i64, _d, _vp, _vp], _i),
+            "oracle_rff_apply_rows": ([_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i], _i),
+            "oracle_gram_matrix": ([_vp, _i64, _i64, _d, _vp, _i], _i),
+            "oracle_cross_gram": ([_vp, _i64, _vp, _i64, _i64, _d, _vp, _i], _i),
+            "oracle_kernel_matvec": ([_vp, _i64, _i64, _d, _d, _vp, _i64, _vp, _i64, _i64, _i], _i),
+            "oracle_dense_matvec": ([_vp, _i64, _d, _vp, _i64, _vp, _i], _i),
+            "oracle_cholesky": ([_vp, _i64, _vp], _i),
+            "oracle_triangular_solve": ([_vp, _i64, _vp, _i64, _i, _i, _vp], _i),
+            "oracle_build_preconditioner": ([_vp, _i64, _i64, _d, _vp, C.POINTER(_i), _i], _i),
+            "oracle_precond_apply": ([_vp, _i64, _i64, _d, _vp, _i64, _vp, _i], _i),
+            "oracle_pcg_solve": ([_i64, OP_CB, _vp, OP_CB, _vp, _vp, _d, _i, OBS_CB, _vp, _vp,
+                                  C.POINTER(_i), C.POINTER(_i), C.POINTER(_d), _vp, _i], _i),
+            "oracle_solve_gaussian": ([_vp, _i64, _i64, _d, _d, _vp, _i64, _d, _vp, _i64, _d, _i, _i,
+                                       _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_longlong), _i], _i),
+            "oracle_train": ([_vp, _i64, _i64, _vp, _i64, _d, _d, _d, _i64, C.c_uint64, _d, _i, _i,
+                              _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_longlong), _i], _i),
+        }
+        for name, (args, res) in sigs.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _L = L
+    return _L
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _chk(st: int, what: str) -> None:
+    if st != OK:
+        raise OracleError(st, what)
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_num_threads(int(n))
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+def random_matrix(rows: int, cols: int, seed: int, scale: float = 1.0) -> np.ndarray:
+    out = np.empty((rows, cols))
+    lib().oracle_random_matrix(rows, cols, seed, scale, _p(out))
+    return out
+
+
+def random_vector(n: int, seed: int, scale: float = 1.0) -> np.ndarray:
+    return random_matrix(n, 1, seed, scale)[:, 0].copy()
+
+
+def random_uniform(count: int, seed: int, lo: float, hi: float) -> np.ndarray:
+    out = np.empty(count)
+    lib().oracle_random_uniform(count, seed, lo, hi, _p(out))
+    return out
+
+
+def rff_realize(master_seed: int, d: int, s: int, sigma: float):
+    w, b = np.empty((s, d)), np.empty(s)
+    _chk(lib().oracle_rff_realize(master_seed, d, s, sigma, _p(w), _p(b)), "rff_realize")
+    return w, b
+
+
+def rff_apply_rows(x, w, b, order: int = 0) -> np.ndarray:
+    x, w, b = f64(x), f64(w), f64(b)
+    z = np.empty((x.shape[0], w.shape[0]))
+    _chk(lib().oracle_rff_apply_rows(_p(x), x.shape[0], x.shape[1], _p(w), _p(b), w.shape[0], _p(z),
+                                     order), "rff_apply_rows")
+    return z
+
+
+def gram_matrix(x, sigma: float, order: int = 0) -> np.ndarray:
+    x = f64(x)
+    k = np.empty((x.shape[0], x.shape[0]))
+    _chk(lib().oracle_gram_matrix(_p(x), x.shape[0], x.shape[1], sigma, _p(k), order), "gram")
+    return k
+
+
+def cross_gram(a, b, sigma: float, order: int = 0) -> np.ndarray:
+    a, b = f64(a), f64(b)
+    k = np.empty((a.shape[0], b.shape[0]))
+    _chk(lib().oracle_cross_gram(_p(a), a.shape[0], _p(b), b.shape[0], a.shape[1], sigma, _p(k), order),
+         "cross_gram")
+    return k
+
+
+def kernel_matvec(x, sigma: float, lam: float, v, rows=None, order: int = 0) -> np.ndarray:
+    """((K + lam I) V)[rows] with K on the fly (V n or n x t)."""
+    x = f64(x)
+    v = f64(v)
+    vec = v.ndim == 1
+    v2 = v[:, None] if vec else v
+    n = x.shape[0]
+    r0, r1 = (0, n) if rows is None else rows
+    out = np.empty((r1 - r0, v2.shape[1]))
+    _chk(lib().oracle_kernel_matvec(_p(x), n, x.shape[1], sigma, lam, _p(f64(v2)), v2.shape[1], _p(out),
+                                    r0, r1, order), "kernel_matvec")
+    return out[:, 0] if vec else out
+
+
+def cholesky(a) -> np.ndarray:
+    a = f64(a)
+    out = np.empty_like(a)
+    _chk(lib().oracle_cholesky(_p(a), a.shape[0], _p(out)), "cholesky")
+    return out
+
+
+def triangular_solve(l, b, side: str = "left", transpose: bool = False) -> np.ndarray:
+    l, b = f64(l), f64(b)
+    s = l.shape[0]
+    m = b.shape[1] if side == "left" else b.shape[0]
+    out = np.empty_like(b)
+    _chk(lib().oracle_triangular_solve(_p(l), s, _p(b), m, 0 if side == "left" else 1, int(transpose),
+                                       _p(out)), "triangular_solve")
+    return out
+
+
+def build_preconditioner(z, lambda_p: float, order: int = 0):
+    """Returns (U s x n, jitter_used)."""
+    z = f64(z)
+    n, s = z.shape
+    u = np.empty((s, n))
+    jit = C.c_int(0)
+    _chk(lib().oracle_build_preconditioner(_p(z), n, s, lambda_p, _p(u), C.byref(jit), order),
+         "build_preconditioner")
+    return u, bool(jit.value)
+
+
+def precond_apply(u, lambda_p: float, x, order: int = 0) -> np.ndarray:
+    u, x = f64(u), f64(x)
+    vec = x.ndim == 1
+    x2 = x[:, None] if vec else x
+    out = np.empty_like(x2)
+    _chk(lib().oracle_precond_apply(_p(u), u.shape[0], u.shape[1], lambda_p, _p(f64(x2)), x2.shape[1],
+                                    _p(out), order), "precond_apply")
+    return out[:, 0] if vec else out
+
+
+@dataclass
+class PcgOut:
+    solution: np.ndarray
+    iterations: int
+    converged: bool
+    final_residual: float
+    residual_history: list = field(default_factory=list)
+
+
+def pcg_solve(apply_a, apply_m, y, tau: float, max_iter: int, observer=None, order: int = 0) -> PcgOut:
+    """solver.cpp:22-67 with Python operators."""
+    y = f64(y)
+    n = y.shape[0]
+    errs = []
+
+    def wrap(fn):
+        def cb(_u, inp, out, nn):
+            try:
+                v = np.ctypeslib.as_array(inp, shape=(nn,)).copy()
+                np.ctypeslib.as_array(out, shape=(nn,))[:] = np.asarray(fn(v), dtype=np.float64)
+                return 0
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+                return 1
+        return OP_CB(cb)
+
+    ca = wrap(apply_a)
+    cm = wrap(apply_m) if apply_m is not None else OP_CB()
+
+    def ob(_u, it, xp, nn):
+        observer(int(it), np.ctypeslib.as_array(xp, shape=(nn,)).copy())
+
+    co = OBS_CB(ob) if observer is not None else OBS_CB()
+    x = np.zeros(n)
+    it, cv, fr = C.c_int(0), C.c_int(0), C.c_double(0)
+    hist = np.zeros(max(1, max_iter))
+    st = lib().oracle_pcg_solve(n, ca, None, cm, None, _p(y), tau, max_iter, co, None, _p(x),
+                                C.byref(it), C.byref(cv), C.byref(fr), _p(hist), order)
+    if errs:
+        raise errs[0]
+    _chk(st, "pcg_solve")
+    return PcgOut(x, it.value, bool(cv.value), fr.value, list(hist[: it.value]))
+
+
+@dataclass
+class SolveOut:
+    c: np.ndarray
+    iterations: list
+    converged: list
+    final_residual: list
+    residual_history: np.ndarray
+    total_matvecs: int
+
+
+def solve_gaussian(x, sigma, lam, u, lambda_p, y, tau, max_iter, dense_k=True, order=0) -> SolveOut:
+    x, y = f64(x), f64(y)
+    y2 = y[:, None] if y.ndim == 1 else y
+    n, t = y2.shape
+    c = np.empty((n, t))
+    its = np.zeros(t, dtype=np.int32)
+    cvs = np.zeros(t, dtype=np.int32)
+    frs = np.zeros(t)
+    hist = np.zeros((t, max(1, max_iter)))
+    tot = C.c_longlong(0)
+    uptr = None if u is None else _p(f64(u))
+    s = 0 if u is None else u.shape[0]
+    _chk(lib().oracle_solve_gaussian(_p(x), n, x.shape[1], sigma, lam, uptr, s, lambda_p, _p(f64(y2)), t,
+                                     tau, max_iter, int(dense_k), _p(c), _p(its), _p(cvs), _p(frs),
+                                     _p(hist), C.byref(tot), order), "solve_gaussian")
+    return SolveOut(c, its.tolist(), [bool(v) for v in cvs], frs.tolist(), hist, int(tot.value))
+
+
+def train(x, y, sigma, lam, s, seed, tau, max_iter, lambda_p=None, dense_k=True, order=0) -> SolveOut:
+    """solver.cpp:96-133, non-adaptive RFF chain."""
+    x, y = f64(x), f64(y)
+    y2 = y[:, None] if y.ndim == 1 else y
+    n, t = y2.shape
+    c = np.empty((n, t))
+    its = np.zeros(t, dtype=np.int32)
+    cvs = np.zeros(t, dtype=np.int32)
+    frs = np.zeros(t)
+    hist = np.zeros((t, max(1, max_iter)))
+    tot = C.c_longlong(0)
+    lp = -1.0 if lambda_p is None else lambda_p
+    _chk(lib().oracle_train(_p(x), n, x.shape[1], _p(f64(y2)), t, sigma, lam, lp, s, seed, tau, max_iter,
+                            int(dense_k), _p(c), _p(its), _p(cvs), _p(frs), _p(hist), C.byref(tot), order),
+         "train")
+    return SolveOut(c, its.tolist(), [bool(v) for v in cvs], frs.tolist(), hist, int(tot.value))

@@ -1,0 +1,588 @@
+"""B200-native sketch-preconditioned kernel ridge regression (arXiv 1611.03220 hot path).
+
+Host-side mirror of the reference's C++ operator / preconditioner / solver API
+(/root/reference/proj/core/include/krr/{kernels,sketches,precond,solver}.hpp), backed
+by the CUDA library libkrr_b200.so through its C-ABI (include/krr_b200.h).  Same names,
+same argument meaning, same error behaviour (exceptions map 1:1 onto types.hpp).
+All compute runs on the GPU; there is no CPU fallback.
+
+Reference -> here
+  krr::kernels::KernelSpec::gaussian          KernelSpec.gaussian
+  krr::kernels::Dataset                       Dataset
+  krr::sketches::RffMap / ChainSpec / realize_chain / SketchChain::apply_rows
+  krr::precond::build_preconditioner / Preconditioner::{apply, apply_columns}
+  krr::solver::pcg_solve(LinearOperator...)   pcg_solve  (device vector algebra, host operators)
+  krr::solver::solve_regularized(K, ...)      solve_regularized(x, kernel, ...)  (K on the fly)
+  krr::solver::train / predict_scores / predict_labels / rlsc_encode / rlsc_decode
+  apply_a lambda over gram_matrix             GaussianOperator (fused on-the-fly K1 kernel)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import (  # noqa: F401  (re-exported exception types)
+    BreakdownDetected,
+    CallbackError,
+    Context,
+    CudaError,
+    DimensionMismatch,
+    InvalidArgument,
+    KrrError,
+    NcclError,
+    NonPositiveLambda,
+    NotPositiveDefinite,
+    SingularTriangular,
+    StateError,
+    device_count,
+    nccl_unique_id,
+)
+
+__all__ = [
+    "KernelSpec", "Dataset", "RffMap", "ChainSpec", "SketchChain", "realize_chain",
+    "Preconditioner", "build_preconditioner", "GaussianOperator", "SolverConfig", "RhsStats",
+    "PcgReport", "PcgResult", "KrrModel", "TrainResult", "pcg_solve", "solve_regularized",
+    "train", "predict_scores", "predict_labels", "rlsc_encode", "rlsc_decode",
+    "generate_config", "schedule", "Context", "device_count",
+]
+
+K_STAGE_SEED_STRIDE = 0x9E3779B97F4A7C15  # sketches.hpp:14
+
+
+# ----------------------------------------------------------------------------- kernels.hpp
+@dataclass
+class KernelSpec:
+    """Gaussian kernel k(x,z) = exp(-|x-z|^2 / 2 sigma^2) (kernels.hpp:15-27)."""
+
+    family: str = "gaussian"
+    sigma: float = 1.0
+
+    @staticmethod
+    def gaussian(sigma: float) -> "KernelSpec":
+        spec = KernelSpec("gaussian", float(sigma))
+        spec.validate()
+        return spec
+
+    def validate(self) -> None:
+        if self.family != "gaussian":
+            raise InvalidArgument("only the Gaussian kernel is on the B200 hot path")
+        if not (self.sigma > 0.0):  # kernels.cpp:37-38
+            raise InvalidArgument("KernelSpec: sigma must be positive")
+
+
+@dataclass
+class Dataset:
+    """kernels.hpp:33-43: x n x d, y n x t (RLSC +/-1 for classification)."""
+
+    x: np.ndarray
+    y: np.ndarray
+    labels: list = field(default_factory=list)
+    label_map: list = field(default_factory=list)
+
+    def classification(self) -> bool:
+        return len(self.label_map) > 0
+
+    def n(self) -> int:
+        return int(np.asarray(self.x).shape[0])
+
+    def dim(self) -> int:
+        return int(np.asarray(self.x).shape[1])
+
+    def targets(self) -> int:
+        y = np.asarray(self.y)
+        return 1 if y.ndim == 1 else int(y.shape[1])
+
+
+# ----------------------------------------------------------------------------- sketches.hpp
+class RffMap:
+    """Random Fourier features (sketches.hpp:21-31).  W, b drawn on the host with the
+    reference's libstdc++ RNG (sketches.cpp:24-35), so they are bitwise identical."""
+
+    def __init__(self, input_dim: int, features: int, sigma: float, seed: int):
+        if features < 1:
+            raise InvalidArgument("RffMap: need at least one feature")
+        if not (sigma > 0.0):
+            raise InvalidArgument("RffMap: sigma must be positive")
+        self.w = np.empty((features, input_dim))
+        self.b = np.empty(features)
+        self.seed = int(seed)
+        self.sigma = float(sigma)
+        # krr_rff_realize applies stage_seed(master, 0) = master + stride; pass seed - stride.
+        master = (int(seed) - K_STAGE_SEED_STRIDE) % (1 << 64)
+        _lib.check(_lib.LIB.krr_rff_realize(master, input_dim, features, sigma,
+                                            _lib.ptr(self.w), _lib.ptr(self.b)))
+
+    def input_dim(self) -> int:
+        return self.w.shape[1]
+
+    def output_dim(self) -> int:
+        return self.w.shape[0]
+
+    def apply_rows(self, x: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
+        """Z with row i = sqrt(2/s) cos(W x_i + b), built on the device (K2)."""
+        x = _lib.f64(x)
+        if x.ndim != 2 or x.shape[1] != self.input_dim():
+            raise DimensionMismatch("RffMap: input dimension mismatch")
+        n, s = x.shape[0], self.output_dim()
+        if n == 0:
+            return np.zeros((0, s))
+        own = ctx is None
+        ctx = ctx or Context()
+        try:
+            _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, x.shape[1], self.sigma))
+            _lib.check(_lib.LIB.krr_rff_build(ctx.handle, _lib.ptr(self.w), _lib.ptr(self.b), s))
+            z = np.empty((n, s))
+            _lib.check(_lib.LIB.krr_rff_download(ctx.handle, _lib.ptr(z)))
+            return z
+        finally:
+            if own:
+                ctx.close()
+
+    def apply(self, x: np.ndarray) -> np.ndarray:
+        x = _lib.f64(x)
+        if x.ndim != 1 or x.shape[0] != self.input_dim():
+            raise DimensionMismatch("RffMap: input dimension mismatch")
+        return self.apply_rows(x[None, :])[0]
+
+
+@dataclass
+class ChainSpec:
+    """sketches.hpp:96-107.  The B200 path implements the RFF-only chain (s2 = s3 = 0)."""
+
+    first: str = "RandomFourier"
+    s1: int = 0
+    s2: int = 0
+    s3: int = 0
+
+    def validate(self) -> None:
+        if self.s1 < 1:
+            raise InvalidArgument("ChainSpec: s1 must be at least 1")
+        if self.s2 < 0 or self.s3 < 0:
+            raise InvalidArgument("ChainSpec: stage sizes must be non-negative")
+        if self.s2 or self.s3 or self.first != "RandomFourier":
+            raise InvalidArgument("ChainSpec: only the RandomFourier single-stage chain is on the hot path")
+
+    def output_dim(self) -> int:
+        return self.s3 or self.s2 or self.s1
+
+
+@dataclass
+class SketchChain:
+    kernel: KernelSpec
+    in_dim: int
+    out_dim: int
+    rff: RffMap
+
+    def input_dim(self) -> int:
+        return self.in_dim
+
+    def output_dim(self) -> int:
+        return self.out_dim
+
+    def apply_rows(self, x: np.ndarray) -> np.ndarray:
+        return self.rff.apply_rows(x)
+
+    def apply(self, x: np.ndarray) -> np.ndarray:
+        return self.rff.apply(x)
+
+
+def realize_chain(spec: ChainSpec, kernel: KernelSpec, input_dim: int, master_seed: int) -> SketchChain:
+    """sketches.cpp:213-242 (RFF stage 0 seeded with stage_seed(master, 0))."""
+    spec.validate()
+    kernel.validate()
+    seed = (int(master_seed) + K_STAGE_SEED_STRIDE) % (1 << 64)
+    return SketchChain(kernel, input_dim, spec.s1, RffMap(input_dim, spec.s1, kernel.sigma, seed))
+
+
+# ----------------------------------------------------------------------------- precond.hpp
+class Preconditioner:
+    """Woodbury (Z Z^T + lambda_p I)^-1 = (I - U^T U)/lambda_p, U = L^-1 Z^T s x n, resident
+    on the device (precond.hpp:15-23)."""
+
+    def __init__(self, ctx: Context, n: int, s: int, lambda_p: float, jitter_used: bool, owns: bool):
+        self._ctx, self._n, self._s = ctx, n, s
+        self.lambda_p = float(lambda_p)
+        self.jitter_used = bool(jitter_used)
+        self._owns = owns
+
+    def sketch_size(self) -> int:
+        return self._s
+
+    def dim(self) -> int:
+        return self._n
+
+    @property
+    def u(self) -> np.ndarray:
+        out = np.empty((self._s, self._n))
+        _lib.check(_lib.LIB.krr_precond_download_u(self._ctx.handle, _lib.ptr(out)))
+        return out
+
+    def apply_columns(self, x: np.ndarray) -> np.ndarray:
+        x = _lib.f64(x)
+        if x.ndim != 2 or x.shape[0] != self._n:
+            raise DimensionMismatch("Preconditioner: dimension mismatch")
+        out = np.empty_like(x)
+        _lib.check(_lib.LIB.krr_precond_apply(self._ctx.handle, _lib.ptr(x), x.shape[1], _lib.ptr(out)))
+        return out
+
+    def apply(self, x: np.ndarray) -> np.ndarray:
+        x = _lib.f64(x)
+        if x.ndim != 1 or x.shape[0] != self._n:
+            raise DimensionMismatch("Preconditioner: dimension mismatch")
+        return self.apply_columns(x[:, None])[:, 0]
+
+    __call__ = apply
+
+    def close(self):
+        if self._owns:
+            self._ctx.close()
+
+
+def build_preconditioner(z: np.ndarray, lambda_p: float, ctx: Optional[Context] = None) -> Preconditioner:
+    """precond.cpp:20-40 on the device (SYRK, Cholesky with one jitter retry, TRSM)."""
+    if not (lambda_p > 0.0):
+        raise NonPositiveLambda("build_preconditioner: lambda_p must be positive")
+    z = _lib.f64(z)
+    if z.ndim != 2:
+        raise DimensionMismatch("build_preconditioner: Z must be a matrix")
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        _lib.check(_lib.LIB.krr_sketch_upload(ctx.handle, _lib.ptr(z), z.shape[0], z.shape[1]))
+        jit = C.c_int(0)
+        _lib.check(_lib.LIB.krr_precond_build(ctx.handle, float(lambda_p), C.byref(jit)))
+    except Exception:
+        if own:
+            ctx.close()
+        raise
+    return Preconditioner(ctx, z.shape[0], z.shape[1], lambda_p, bool(jit.value), own)
+
+
+# ----------------------------------------------------------------------------- operator
+class GaussianOperator:
+    """v -> (K + lambda I) v for the Gaussian kernel with K never stored: the fused
+    sm_100a K1 kernel.  Callable like the reference's LinearOperator (solver.hpp:15)."""
+
+    def __init__(self, x: np.ndarray, kernel: KernelSpec, lambda_: float = 0.0,
+                 ctx: Optional[Context] = None):
+        kernel.validate()
+        x = _lib.f64(x)
+        if x.ndim != 2 or x.shape[0] < 1:
+            raise DimensionMismatch("GaussianOperator: x must be a non-empty n x d matrix")
+        self._own = ctx is None
+        self.ctx = ctx or Context()
+        self.n, self.d = x.shape
+        self.lambda_ = float(lambda_)
+        self.kernel = kernel
+        _lib.check(_lib.LIB.krr_set_data(self.ctx.handle, _lib.ptr(x), self.n, self.d, kernel.sigma))
+
+    def matmat(self, v: np.ndarray) -> np.ndarray:
+        v = _lib.f64(v)
+        if v.ndim != 2 or v.shape[0] != self.n:
+            raise DimensionMismatch("GaussianOperator: dimension mismatch")
+        out = np.empty_like(v)
+        _lib.check(_lib.LIB.krr_kernel_matvec(self.ctx.handle, self.lambda_, _lib.ptr(v), v.shape[1],
+                                              _lib.ptr(out)))
+        return out
+
+    def __call__(self, v: np.ndarray) -> np.ndarray:
+        v = _lib.f64(v)
+        if v.ndim != 1:
+            raise DimensionMismatch("GaussianOperator: expected a vector")
+        return self.matmat(v[:, None])[:, 0]
+
+    def close(self):
+        if self._own:
+            self.ctx.close()
+
+
+# ----------------------------------------------------------------------------- solver.hpp
+@dataclass
+class SolverConfig:
+    """solver.hpp:17-27 (`lambda` is spelled `lambda_`)."""
+
+    tau: float = 1e-5
+    max_iter: int = 1000
+    lambda_: float = 1e-2
+    lambda_p: Optional[float] = None
+    chain: ChainSpec = field(default_factory=ChainSpec)
+    adaptive: bool = False
+    s0: int = 0
+    s_max: int = 0
+    seed: int = 0
+
+
+@dataclass
+class RhsStats:
+    iterations: int = 0
+    final_residual: float = 0.0
+    converged: bool = False
+    residual_history: list = field(default_factory=list)
+
+
+@dataclass
+class PcgReport:
+    per_rhs: list = field(default_factory=list)
+    total_matvecs: int = 0
+    wall_time_sec: float = 0.0
+    phase_ms: dict = field(default_factory=dict)
+
+    def all_converged(self) -> bool:
+        return all(s.converged for s in self.per_rhs)
+
+    def max_iterations(self) -> int:
+        return max((s.iterations for s in self.per_rhs), default=0)
+
+
+@dataclass
+class PcgResult:
+    solution: np.ndarray
+    stats: RhsStats
+
+
+@dataclass
+class KrrModel:
+    kernel: KernelSpec
+    x: np.ndarray
+    c: np.ndarray
+    label_map: list = field(default_factory=list)
+    lambda_: float = 0.0
+    seed: int = 0
+
+    def classification(self) -> bool:
+        return len(self.label_map) > 0
+
+
+@dataclass
+class TrainResult:
+    model: KrrModel
+    report: PcgReport
+    sketch_size: int = 0
+    quality_passed: bool = True
+    quality_history: list = field(default_factory=list)
+
+
+def _stats_from(c_stats, hist: Optional[np.ndarray], j: int) -> RhsStats:
+    s = c_stats[j]
+    h = [] if hist is None else [float(v) for v in hist[j, : s.iterations]]
+    return RhsStats(int(s.iterations), float(s.final_residual), bool(s.converged), h)
+
+
+def pcg_solve(apply_a: Callable[[np.ndarray], np.ndarray],
+              preconditioner: Optional[Callable[[np.ndarray], np.ndarray]],
+              y: np.ndarray, tau: float, max_iter: int,
+              observer: Optional[Callable[[int, np.ndarray], None]] = None,
+              ctx: Optional[Context] = None) -> PcgResult:
+    """solver.hpp:55-57 / solver.cpp:22-67.  The PCG vector algebra runs on the device;
+    apply_a / preconditioner are caller operators (host callables), exactly as the
+    reference's LinearOperator.  Throws BreakdownDetected when p'Ap <= 0."""
+    y = _lib.f64(y)
+    if y.ndim != 1:
+        raise DimensionMismatch("pcg_solve: y must be a vector")
+    n = y.shape[0]
+    errors: list = []
+
+    def wrap(fn):
+        def cb(_user, inp, out, nn):
+            try:
+                v = np.ctypeslib.as_array(inp, shape=(nn,)).copy()
+                r = np.asarray(fn(v), dtype=np.float64).reshape(-1)
+                if r.shape[0] != nn:
+                    raise DimensionMismatch("operator returned a vector of the wrong length")
+                np.ctypeslib.as_array(out, shape=(nn,))[:] = r
+                return 0
+            except BaseException as e:  # noqa: BLE001 - propagated after the C call
+                errors.append(e)
+                return 1
+        return _lib.OPERATOR_CB(cb)
+
+    cb_a = wrap(apply_a)
+    cb_m = wrap(preconditioner) if preconditioner is not None else _lib.OPERATOR_CB()
+
+    def obs(_user, it, xptr, nn):
+        try:
+            observer(int(it), np.ctypeslib.as_array(xptr, shape=(nn,)).copy())
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    cb_o = _lib.OBSERVER_CB(obs) if observer is not None else _lib.OBSERVER_CB()
+    x = np.zeros(n)
+    st = (_lib.RhsStatsC * 1)()
+    hist = np.zeros((1, max(1, int(max_iter))))
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        status = _lib.LIB.krr_pcg_solve_operator(ctx.handle, n, cb_a, None, cb_m, None, _lib.ptr(y),
+                                                 float(tau), int(max_iter), cb_o, None, _lib.ptr(x),
+                                                 st, _lib.ptr(hist))
+    finally:
+        if own:
+            ctx.close()
+    if errors:
+        raise errors[0]
+    _lib.check(status)
+    return PcgResult(x, _stats_from(st, hist, 0))
+
+
+def solve_regularized(x: np.ndarray, kernel: KernelSpec, y: np.ndarray, lambda_: float,
+                      preconditioner: Optional[Preconditioner], tau: float, max_iter: int,
+                      ctx: Optional[Context] = None):
+    """solver.cpp:69-94 with the Gaussian operator computed on the fly (the reference
+    takes a dense K; here K is never stored).  `preconditioner` must have been built
+    on the same context (pass ctx), or be None for plain CG."""
+    kernel.validate()
+    x = _lib.f64(x)
+    y = _lib.f64(y)
+    y2 = y[:, None] if y.ndim == 1 else y
+    if x.ndim != 2 or y2.shape[0] != x.shape[0]:
+        raise DimensionMismatch("solve_regularized: K and Y dimensions do not match")
+    own = ctx is None
+    if preconditioner is not None:
+        ctx = preconditioner._ctx
+        own = False
+    ctx = ctx or Context()
+    try:
+        n, t = y2.shape
+        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, x.shape[1], kernel.sigma))
+        c = np.empty((n, t))
+        st = (_lib.RhsStatsC * t)()
+        hist = np.zeros((t, max(1, int(max_iter))))
+        tot = C.c_int64()
+        t0 = time.perf_counter()
+        _lib.check(_lib.LIB.krr_pcg_solve(ctx.handle, float(lambda_), _lib.ptr(_lib.f64(y2)), t,
+                                          float(tau), int(max_iter),
+                                          1 if preconditioner is not None else 0, _lib.ptr(c), st,
+                                          _lib.ptr(hist), C.byref(tot)))
+        wall = time.perf_counter() - t0
+    finally:
+        if own:
+            ctx.close()
+    report = PcgReport([_stats_from(st, hist, j) for j in range(t)], int(tot.value), wall)
+    return c, report
+
+
+def train(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Context] = None) -> TrainResult:
+    """solver.cpp:96-133 (non-adaptive RFF chain) — the whole hot path on the device."""
+    if data.n() < 1:
+        raise InvalidArgument("train: dataset is empty")
+    if not (cfg.lambda_ > 0.0):
+        raise NonPositiveLambda("train: lambda must be positive")
+    if cfg.adaptive:
+        raise InvalidArgument("adaptive sketch sizing (precond.cpp:107) is out of the hot-path scope")
+    kernel.validate()
+    cfg.chain.validate()
+    x = _lib.f64(data.x)
+    y = _lib.f64(data.y)
+    y2 = y[:, None] if y.ndim == 1 else y
+    n, d = x.shape
+    t = y2.shape[1]
+    s = cfg.chain.s1
+    c = np.empty((n, t))
+    st = (_lib.RhsStatsC * t)()
+    hist = np.zeros((t, max(1, int(cfg.max_iter))))
+    tot = C.c_int64()
+    phase = np.zeros(4)
+    lp = cfg.lambda_p if cfg.lambda_p is not None else -1.0
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        t0 = time.perf_counter()
+        _lib.check(_lib.LIB.krr_train(ctx.handle, _lib.ptr(x), n, d, _lib.ptr(_lib.f64(y2)), t,
+                                      kernel.sigma, float(cfg.lambda_), float(lp), s, int(cfg.seed),
+                                      float(cfg.tau), int(cfg.max_iter), _lib.ptr(c), st,
+                                      _lib.ptr(hist), C.byref(tot), _lib.ptr(phase)))
+        wall = time.perf_counter() - t0
+    finally:
+        if own:
+            ctx.close()
+    report = PcgReport([_stats_from(st, hist, j) for j in range(t)], int(tot.value), wall,
+                       {"rff_build": phase[0], "precond_build": phase[1], "solve": phase[2],
+                        "total": phase[3]})
+    model = KrrModel(kernel, x.copy(), c, list(data.label_map), float(cfg.lambda_), int(cfg.seed))
+    return TrainResult(model, report, s)
+
+
+def predict_scores(model: KrrModel, xq: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
+    """solver.cpp:135-139: cross_gram(Xq, X) C on the device (no diagonal forcing)."""
+    xq = _lib.f64(xq)
+    if xq.ndim != 2 or xq.shape[1] != model.x.shape[1]:
+        raise DimensionMismatch("predict: query dimension does not match the model")
+    c = _lib.f64(model.c)
+    c2 = c[:, None] if c.ndim == 1 else c
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        x = _lib.f64(model.x)
+        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], model.kernel.sigma))
+        out = np.empty((xq.shape[0], c2.shape[1]))
+        _lib.check(_lib.LIB.krr_predict_scores(ctx.handle, _lib.ptr(xq), xq.shape[0], _lib.ptr(c2),
+                                               c2.shape[1], _lib.ptr(out)))
+    finally:
+        if own:
+            ctx.close()
+    return out
+
+
+def rlsc_encode(class_indices, num_classes: int) -> np.ndarray:
+    """solver.cpp:152-161."""
+    cls = np.ascontiguousarray(class_indices, dtype=np.int32)
+    y = np.empty((cls.shape[0], num_classes))
+    _lib.check(_lib.LIB.krr_rlsc_encode(_lib.ptr(cls), cls.shape[0], int(num_classes), _lib.ptr(y)))
+    return y
+
+
+def rlsc_decode(scores: np.ndarray) -> list:
+    """solver.cpp:163-173: row-wise argmax, ties to the lowest index (host bookkeeping)."""
+    s = np.asarray(scores)
+    return [int(np.argmax(row)) for row in s]  # np.argmax returns the first maximum
+
+
+def predict_labels(model: KrrModel, xq: np.ndarray) -> list:
+    if not model.classification():
+        raise KrrError("predict_labels: model has no label map")
+    scores = predict_scores(model, xq)
+    if scores.shape[1] != len(model.label_map):
+        raise KrrError("predict_labels: score width does not match the label map")
+    return [model.label_map[i] for i in rlsc_decode(scores)]
+
+
+# ----------------------------------------------------------------------------- synthetic data
+def generate_config(cfg: int, n: int, d: int, t: int = 1, seed: int = 0):
+    """BASELINE.json configs 1-5 generators, host C++ in the library."""
+    x = np.empty((n, d))
+    y = np.empty((n, t))
+    _lib.check(_lib.LIB.krr_generate_config(int(cfg), n, d, t, int(seed), _lib.ptr(x), _lib.ptr(y)))
+    return x, y
+
+
+def schedule(n: int, world: int = 1, rank: int = 0):
+    """Symmetric super-tile schedule of K1 (host only): (st, ns, tiles[(a, b)])."""
+    st, ns, nt = C.c_int64(), C.c_int64(), C.c_int64()
+    _lib.check(_lib.LIB.krr_schedule(n, world, rank, C.byref(st), C.byref(ns), None, 0, C.byref(nt)))
+    tiles = np.empty((max(1, nt.value), 2), dtype=np.int32)
+    _lib.check(_lib.LIB.krr_schedule(n, world, rank, C.byref(st), C.byref(ns), _lib.ptr(tiles),
+                                     nt.value, C.byref(nt)))
+    return int(st.value), int(ns.value), tiles[: nt.value].copy()
+
+
+def shard_rows(n: int, world: int, rank: int):
+    """Rows [begin, end) of the sketch owned by `rank` (host only)."""
+    a, b = C.c_int64(), C.c_int64()
+    _lib.check(_lib.LIB.krr_shard_rows(n, world, rank, C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
+
+
+CONFIGS = {
+    # cfg: (n, d, t, sigma, lambda, s)  -- BASELINE.json configs[0..4]
+    1: (8192, 16, 1, 4.0, 1e-3, 1024),
+    2: (65536, 54, 1, 3.0, 1e-4, 2048),
+    3: (262144, 90, 1, 6.0, 1e-5, 4096),
+    4: (1048576, 90, 1, 6.0, 1e-6, 8192),
+    5: (524288, 440, 16, 20.0, 1e-5, 16384),
+}

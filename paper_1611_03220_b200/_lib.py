@@ -1,0 +1,225 @@
+"""ctypes binding of libkrr_b200.so (the C-ABI in include/krr_b200.h).
+
+The product path is the CUDA library; there is no Python/NumPy compute fallback.
+If the shared library is missing, importing the binding raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("KRR_B200_LIB", _HERE / "libkrr_b200.so"))
+
+# Status codes (include/krr_b200.h)
+OK = 0
+ERR_DIMENSION_MISMATCH = 1
+ERR_NOT_POSITIVE_DEFINITE = 2
+ERR_SINGULAR_TRIANGULAR = 3
+ERR_BREAKDOWN = 4
+ERR_NON_POSITIVE_LAMBDA = 5
+ERR_INVALID_ARGUMENT = 6
+ERR_CUDA = 7
+ERR_NCCL = 8
+ERR_STATE = 9
+ERR_CALLBACK = 10
+
+
+class KrrError(Exception):
+    """Base of every error raised through the C-ABI."""
+
+
+# Exception types mirror reference types.hpp:18-64 (invalid_argument-derived ones
+# also derive from ValueError, runtime_error-derived ones from RuntimeError).
+class DimensionMismatch(KrrError, ValueError):
+    pass
+
+
+class NotPositiveDefinite(KrrError, RuntimeError):
+    pass
+
+
+class SingularTriangular(KrrError, RuntimeError):
+    pass
+
+
+class BreakdownDetected(KrrError, RuntimeError):
+    pass
+
+
+class NonPositiveLambda(KrrError, ValueError):
+    pass
+
+
+class InvalidArgument(KrrError, ValueError):
+    pass
+
+
+class CudaError(KrrError, RuntimeError):
+    pass
+
+
+class NcclError(KrrError, RuntimeError):
+    pass
+
+
+class StateError(KrrError, RuntimeError):
+    pass
+
+
+class CallbackError(KrrError, RuntimeError):
+    pass
+
+
+_EXC = {
+    ERR_DIMENSION_MISMATCH: DimensionMismatch,
+    ERR_NOT_POSITIVE_DEFINITE: NotPositiveDefinite,
+    ERR_SINGULAR_TRIANGULAR: SingularTriangular,
+    ERR_BREAKDOWN: BreakdownDetected,
+    ERR_NON_POSITIVE_LAMBDA: NonPositiveLambda,
+    ERR_INVALID_ARGUMENT: InvalidArgument,
+    ERR_CUDA: CudaError,
+    ERR_NCCL: NcclError,
+    ERR_STATE: StateError,
+    ERR_CALLBACK: CallbackError,
+}
+
+
+class RhsStatsC(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("final_residual", C.c_double)]
+
+
+OPERATOR_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+OBSERVER_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_int64)
+
+_vp = C.c_void_p
+_i64 = C.c_int64
+_d = C.c_double
+_i = C.c_int
+
+# name -> argtypes (restype int unless stated)
+_SIGS = {
+    "krr_abi_version": [],
+    "krr_device_count": [],
+    "krr_ctx_create": [_i, C.POINTER(_vp)],
+    "krr_nccl_unique_id": [_vp],
+    "krr_ctx_create_dist": [_i, _i, _i, _vp, C.POINTER(_vp)],
+    "krr_ctx_destroy": [_vp],
+    "krr_ctx_launch_count": [_vp, C.POINTER(_i64)],
+    "krr_set_data": [_vp, _vp, _i64, _i64, _d],
+    "krr_kernel_matvec": [_vp, _d, _vp, _i64, _vp],
+    "krr_kernel_matvec_device": [_vp, _d, _vp, _i64, _vp],
+    "krr_predict_scores": [_vp, _vp, _i64, _vp, _i64, _vp],
+    "krr_rff_realize": [C.c_uint64, _i64, _i64, _d, _vp, _vp],
+    "krr_rff_build": [_vp, _vp, _vp, _i64],
+    "krr_rff_download": [_vp, _vp],
+    "krr_sketch_upload": [_vp, _vp, _i64, _i64],
+    "krr_precond_build": [_vp, _d, C.POINTER(_i)],
+    "krr_precond_apply": [_vp, _vp, _i64, _vp],
+    "krr_precond_download_u": [_vp, _vp],
+    "krr_precond_drop": [_vp],
+    "krr_pcg_solve": [_vp, _d, _vp, _i64, _d, _i, _i, _vp, _vp, _vp, C.POINTER(_i64)],
+    "krr_pcg_solve_operator": [_vp, _i64, OPERATOR_CB, _vp, OPERATOR_CB, _vp, _vp, _d, _i,
+                               OBSERVER_CB, _vp, _vp, _vp, _vp],
+    "krr_train": [_vp, _vp, _i64, _i64, _vp, _i64, _d, _d, _d, _i64, C.c_uint64, _d, _i, _vp,
+                  _vp, _vp, C.POINTER(_i64), _vp],
+    "krr_schedule": [_i64, _i, _i, C.POINTER(_i64), C.POINTER(_i64), _vp, _i64, C.POINTER(_i64)],
+    "krr_shard_rows": [_i64, _i, _i, C.POINTER(_i64), C.POINTER(_i64)],
+    "krr_generate_config": [_i, _i64, _i64, _i64, C.c_uint64, _vp, _vp],
+    "krr_rlsc_encode": [_vp, _i64, C.c_int32, _vp],
+    "krr_bench_matvec": [_vp, _d, _i, C.POINTER(_d), C.POINTER(_d)],
+    "krr_microbench": [_vp, _vp],
+    "krr_debug_gauss_exp": [_vp, _vp, _i64, _d, _i, _vp],
+}
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python paper_1611_03220_b200/_build.py` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    lib.krr_last_error.restype = C.c_char_p
+    lib.krr_last_error.argtypes = []
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    return lib
+
+
+LIB = _load()
+
+
+def declared_symbols() -> list[str]:
+    return ["krr_last_error"] + list(_SIGS)
+
+
+def check(status: int) -> None:
+    if status != OK:
+        msg = LIB.krr_last_error().decode(errors="replace")
+        raise _EXC.get(status, KrrError)(msg)
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def f64(a, shape=None) -> np.ndarray:
+    """Contiguous row-major float64 view/copy (reference Matrix is RowMajor fp64)."""
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        out = out.reshape(shape)
+    return out
+
+
+def device_count() -> int:
+    return int(LIB.krr_device_count())
+
+
+class Context:
+    """One device context (one GPU, one stream; NCCL comm when world > 1)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        h = C.c_void_p()
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise InvalidArgument("a 128-byte NCCL unique id is required when world > 1")
+            buf = C.create_string_buffer(nccl_id, 128)
+            check(LIB.krr_ctx_create_dist(device, rank, world, buf, C.byref(h)))
+        else:
+            check(LIB.krr_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device, self.rank, self.world = device, rank, world
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) and self.handle.value:
+            LIB.krr_ctx_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def launches(self) -> int:
+        v = C.c_int64()
+        check(LIB.krr_ctx_launch_count(self.handle, C.byref(v)))
+        return int(v.value)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(LIB.krr_nccl_unique_id(buf))
+    return buf.raw

@@ -1,0 +1,216 @@
+// Auxiliary kernels: epilogue constants, rectangular predict kernel, accuracy probe
+// of the device exp, and the FP64 pipe micro-benchmarks used for the roofline.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace krr {
+
+ExpConsts make_exp_consts(double scale) {
+    ExpConsts c{};
+    const long double ln2 = 0.693147180559945309417232121458176568L;
+    const long double l = ln2 / 64.0L;
+    c.kscale = double(-(long double)scale * 64.0L / ln2);
+    c.neg_scale = -scale;
+    long double term = 1.0L;
+    double a[6];
+    for (int m = 1; m <= 5; ++m) {
+        term = term * l / (long double)m;
+        a[m] = double(term);
+    }
+    c.a1 = a[1];
+    c.a2 = a[2];
+    c.a3 = a[3];
+    c.a4 = a[4];
+    c.a5 = a[5];
+    // exp(-d2 scale) >= 2^-1020 <=> d2 <= 1020 ln2 / scale
+    const double d2max = double(1020.0L * ln2 / (long double)scale);
+    int64_t bits;
+    std::memcpy(&bits, &d2max, sizeof(bits));
+    c.hi_under = int(bits >> 32);
+    c.pad_ = 0;
+    return c;
+}
+
+void make_exp_table(double* tab64) {
+    for (int j = 0; j < 64; ++j) tab64[j] = double(exp2l((long double)j / 64.0L));
+}
+
+namespace {
+
+__global__ void cross_matvec_kernel(const double* __restrict__ Xq, int64_t m,
+                                    const double* __restrict__ X, int64_t n, int64_t d,
+                                    const double* __restrict__ c, int64_t t, double scale,
+                                    double* __restrict__ out) {
+    __shared__ double scr[32];
+    const int64_t q = blockIdx.x;
+    if (q >= m) return;
+    const double* a = Xq + q * d;
+    double sqa = 0.0;
+    for (int64_t k = 0; k < d; ++k) sqa = fma(a[k], a[k], sqa);
+    for (int64_t col = 0; col < t; ++col) {
+        double acc = 0.0;
+        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+            const double* xj = X + j * d;
+            double dot = 0.0, sqj = 0.0;
+            for (int64_t k = 0; k < d; ++k) {
+                dot = fma(a[k], xj[k], dot);
+                sqj = fma(xj[k], xj[k], sqj);
+            }
+            const double e = exp(-fmax(0.0, sqa + sqj - 2.0 * dot) * scale);
+            acc = fma(e, c[j * t + col], acc);
+        }
+        acc = block_sum(acc, scr);
+        if (threadIdx.x == 0) out[q * t + col] = acc;
+    }
+}
+
+__global__ void debug_exp_kernel(const double* __restrict__ d2, int64_t n, ExpConsts ec,
+                                 const double* __restrict__ tab_g, int mode,
+                                 double* __restrict__ out) {
+    __shared__ double tab[64];
+    if (threadIdx.x < 64) tab[threadIdx.x] = tab_g[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = mode == 0 ? gauss_exp<0>(d2[i], ec, tab) : gauss_exp<1>(d2[i], ec, tab);
+}
+
+// ---- micro-benchmarks
+constexpr int MB_ITERS = 4096;
+
+__global__ void mb_dmma_kernel(double* sink, double a, double b) {
+    double acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int it = 0; it < MB_ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma884(acc[i][0], acc[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+    if (s == 12345.678) sink[0] = s;
+}
+
+__global__ void mb_dfma_kernel(double* sink, double a, double b) {
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = double(i) * 1e-3;
+    for (int it = 0; it < MB_ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+    if (s == 12345.678) sink[0] = s;
+}
+
+// Interleaved: per iteration 8 DMMA (8 x 256 MAC per warp) and 8 x 8 DFMA per thread.
+__global__ void mb_mixed_kernel(double* sink, double a, double b) {
+    double acc[8][2], f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        acc[i][0] = acc[i][1] = 0.0;
+        f[i] = double(i) * 1e-3;
+    }
+    for (int it = 0; it < MB_ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            dmma884(acc[i][0], acc[i][1], a, b);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = fma(f[j], a, b);
+        }
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1] + f[i];
+    if (s == 12345.678) sink[0] = s;
+}
+
+template <int MODE>
+__global__ void mb_exp_kernel(double* sink, ExpConsts ec, const double* __restrict__ tab_g) {
+    __shared__ double tab[64];
+    if (threadIdx.x < 64) tab[threadIdx.x] = tab_g[threadIdx.x];
+    __syncthreads();
+    double x[8], acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = 1.0 + 0.37 * i + 1e-3 * threadIdx.x;
+    for (int it = 0; it < MB_ITERS / 8; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double e = gauss_exp<MODE>(x[i], ec, tab);
+            acc = fma(e, 0.5, acc);
+            x[i] += 1e-7;
+        }
+    }
+    if (acc == 12345.678) sink[0] = acc;
+}
+
+}  // namespace
+
+void cross_matvec_launch(const double* Xq, int64_t m, const double* X, int64_t n, int64_t d,
+                         const double* c, int64_t t, double scale, double* out,
+                         cudaStream_t stream) {
+    if (m == 0) return;
+    cross_matvec_kernel<<<unsigned(m), 256, 0, stream>>>(Xq, m, X, n, d, c, t, scale, out);
+    KRR_LAUNCH_CHECK();
+}
+
+void debug_exp_launch(const double* d2, int64_t n, const ExpConsts& ec, const double* tab,
+                      int mode, double* out, cudaStream_t stream) {
+    const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1184)));
+    debug_exp_kernel<<<blocks, 256, 0, stream>>>(d2, n, ec, tab, mode, out);
+    KRR_LAUNCH_CHECK();
+}
+
+void microbench_run(const ExpConsts& ec, const double* tab, double* results, cudaStream_t stream) {
+    int dev = 0, sms = 0, clk_khz = 0;
+    KRR_CUDA(cudaGetDevice(&dev));
+    KRR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    KRR_CUDA(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev));
+    double* sink = nullptr;
+    KRR_CUDA(cudaMalloc(&sink, 64));
+    cudaEvent_t e0, e1;
+    KRR_CUDA(cudaEventCreate(&e0));
+    KRR_CUDA(cudaEventCreate(&e1));
+    const unsigned blocks = unsigned(sms * 4);
+    const unsigned threads = 256;
+    const double warps = double(blocks) * threads / 32.0;
+    auto time_it = [&](auto&& launch) {
+        launch();  // warm-up
+        KRR_CUDA(cudaEventRecord(e0, stream));
+        for (int r = 0; r < 5; ++r) launch();
+        KRR_CUDA(cudaEventRecord(e1, stream));
+        KRR_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        KRR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        return double(ms) / 5.0 * 1e-3;
+    };
+    const double t_dmma = time_it([&] { mb_dmma_kernel<<<blocks, threads, 0, stream>>>(sink, 1.0, 1e-9); });
+    const double t_dfma = time_it([&] { mb_dfma_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
+    const double t_mixed = time_it([&] { mb_mixed_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
+    const double t_exp0 = time_it([&] { mb_exp_kernel<0><<<blocks, threads, 0, stream>>>(sink, ec, tab); });
+    const double t_exp1 = time_it([&] { mb_exp_kernel<1><<<blocks, threads, 0, stream>>>(sink, ec, tab); });
+    KRR_LAUNCH_CHECK();
+    const double dmma_flop = warps * MB_ITERS * 8 * 512.0;
+    const double dfma_flop = double(blocks) * threads * MB_ITERS * 8 * 2.0;
+    const double mixed_flop = dmma_flop + dfma_flop * 8.0;
+    const double evals = double(blocks) * threads * (MB_ITERS / 8) * 8;
+    results[0] = dmma_flop / t_dmma * 1e-12;
+    results[1] = dfma_flop / t_dfma * 1e-12;
+    results[2] = mixed_flop / t_mixed * 1e-12;
+    results[3] = evals / t_exp0 * 1e-9;
+    results[4] = evals / t_exp1 * 1e-9;
+    results[5] = sms;
+    results[6] = clk_khz / 1000.0;
+    results[7] = 0.0;
+    KRR_CUDA(cudaEventDestroy(e0));
+    KRR_CUDA(cudaEventDestroy(e1));
+    KRR_CUDA(cudaFree(sink));
+}
+
+}  // namespace krr

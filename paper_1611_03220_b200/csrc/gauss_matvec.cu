@@ -1,0 +1,315 @@
+// K1 — fused, symmetric, on-the-fly Gaussian kernel mat-vec (K never stored).
+//
+// Replaces gram_matrix (reference kernels.cpp:72-88) + the dense apply_a GEMV
+// (solver.cpp:75-77).  Per unordered pair {i, j} (i < j) it computes
+//     d2  = |x_i|^2 + |x_j|^2 - 2 x_i.x_j      (ONE FP64 tensor-core contraction:
+//           L_i . R_j with L_i = [x_i, |x_i|^2, 1], R_j = [-2 x_j, 1, |x_j|^2]),
+//     e   = exp(-max(0, d2) / (2 sigma^2))    (register epilogue, gauss_exp.cuh),
+//     out_i += e v_j  and  out_j += e v_i     (both halves of the symmetric matrix
+//                                               from one evaluation => K_ij == K_ji
+//                                               bitwise, as in kernels.cpp:85-86).
+// The diagonal K_ii = 1 (kernels.cpp:81) and +lambda v_i are added by the finish
+// kernel.
+//
+// Work decomposition (deterministic, no atomics):
+//   rows are padded to n_pad (multiple of the super-tile edge ST, itself a multiple
+//   of 128); super-tile (a, b), a <= b, covers rows [a ST, (a+1) ST) x cols
+//   [b ST, (b+1) ST).  One CTA per super-tile.  Inside, 128 x 128 tiles are visited
+//   column-tile-major (J outer, I inner); diagonal super-tiles visit only I <= J and
+//   the I == J tile only strictly above its diagonal.
+//   Row sums of a super-tile accumulate in shared memory (ST doubles) and are
+//   written once to part[b][rows of a]; column sums of each J tile are reduced in
+//   registers over the whole I sweep and written once to part[a][rows of b].  Every
+//   slot part[x][rows of y] therefore has exactly one writer (for x == y the two
+//   halves are combined in shared memory first), and the finish kernel sums the NS
+//   slots of a row in a fixed order.
+//
+// Mainloop: 256 threads = 8 warps as 2 (M) x 4 (N), warp tile 64 x 32 =
+// 8 x 4 DMMA.8x8x4 accumulators (64 doubles per thread).  Operands stream through a
+// 3-stage cp.async pipeline in k-chunks of 16 doubles (smem row stride 20 doubles
+// => conflict-free fragment loads); the pipeline runs across tile boundaries so
+// the epilogue of tile q overlaps the loads of tile q+1.
+#include "common.cuh"
+#include "gauss_exp.cuh"
+#include "kernels.cuh"
+
+namespace krr {
+
+namespace {
+
+constexpr int BM = 128;           // tile edge (rows and cols)
+constexpr int KC = 16;            // k-chunk (doubles)
+constexpr int KS = 20;            // smem row stride (doubles), 20 = 4 mod 16
+constexpr int NSTAGE = 3;
+constexpr int NTHREADS = 256;
+constexpr int STAGE_DOUBLES = 2 * BM * KS;  // L chunk + R chunk
+
+struct MatvecArgs {
+    const double* __restrict__ L;
+    const double* __restrict__ R;
+    const double* __restrict__ v;
+    double* __restrict__ part;
+    const int2* __restrict__ tiles;
+    const double* __restrict__ exp_tab;
+    int64_t n_pad;
+    int dp;
+    int st;
+    ExpConsts ec;
+};
+
+template <int EXPMODE>
+__global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecArgs A) {
+    extern __shared__ __align__(16) double smem[];
+    double* stages = smem;                                  // NSTAGE * STAGE_DOUBLES
+    double* rowacc = smem + NSTAGE * STAGE_DOUBLES;         // st
+    double* scr_row = rowacc + A.st;                        // 4 x 128
+    double* scr_col = scr_row + 4 * BM;                     // 2 x 128
+    double* tab = scr_col + 2 * BM;                         // 64
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int g = lane >> 2, t4 = lane & 3;
+
+    const int2 tile = A.tiles[blockIdx.x];
+    const int sa = tile.x, sb = tile.y;
+    const bool diag = (sa == sb);
+    const int nT = A.st / BM;
+    const int64_t rowBase = int64_t(sa) * A.st;
+    const int64_t colBase = int64_t(sb) * A.st;
+    const int nk = (A.dp + KC - 1) / KC;
+    const int ntiles = diag ? nT * (nT + 1) / 2 : nT * nT;
+    const int total = ntiles * nk;
+
+    for (int i = tid; i < A.st; i += NTHREADS) rowacc[i] = 0.0;
+    if (EXPMODE == 1 && tid < 64) tab[tid] = A.exp_tab[tid];
+
+    // ---- producer cursor over (jt, it, kc)
+    int p_it = 0, p_jt = 0, p_kc = 0;
+    auto issue = [&](int slot) {
+        double* sL = stages + slot * STAGE_DOUBLES;
+        double* sR = sL + BM * KS;
+        const int k0 = p_kc * KC;
+        const int pieces = min(KC, A.dp - k0) >> 1;  // 16-byte pieces per row
+        const double* gL = A.L + (rowBase + int64_t(p_it) * BM) * A.dp + k0;
+        const double* gR = A.R + (colBase + int64_t(p_jt) * BM) * A.dp + k0;
+#pragma unroll
+        for (int q = 0; q < (2 * BM * (KC / 2)) / NTHREADS; ++q) {
+            const int idx = tid + q * NTHREADS;
+            const int op = idx / (BM * (KC / 2));
+            const int rem = idx % (BM * (KC / 2));
+            const int row = rem / (KC / 2), pc = rem % (KC / 2);
+            if (pc < pieces) {
+                const double* gp = (op ? gR : gL) + int64_t(row) * A.dp + pc * 2;
+                double* sp = (op ? sR : sL) + row * KS + pc * 2;
+                cp_async16(sp, gp);
+            }
+        }
+    };
+    auto advance = [&]() {
+        if (++p_kc == nk) {
+            p_kc = 0;
+            ++p_it;
+            if (p_it > (diag ? p_jt : nT - 1)) {
+                p_it = 0;
+                ++p_jt;
+            }
+        }
+    };
+
+    int ps = 0;  // next stage index to issue
+#pragma unroll
+    for (int s = 0; s < NSTAGE - 1; ++s) {
+        if (ps < total) {
+            issue(ps % NSTAGE);
+            advance();
+        }
+        cp_async_commit();
+        ++ps;
+    }
+    __syncthreads();  // rowacc / tab initialised
+
+    int cs = 0;  // consumer stage index
+    for (int jt = 0; jt < nT; ++jt) {
+        const int64_t J0 = colBase + int64_t(jt) * BM;
+        double vj[4][2];
+#pragma unroll
+        for (int ns = 0; ns < 4; ++ns)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) vj[ns][h] = A.v[J0 + wn * 32 + ns * 8 + 2 * t4 + h];
+        double colacc[4][2];
+#pragma unroll
+        for (int ns = 0; ns < 4; ++ns) colacc[ns][0] = colacc[ns][1] = 0.0;
+
+        const int itEnd = diag ? jt : nT - 1;
+        for (int it = 0; it <= itEnd; ++it) {
+            const int64_t I0 = rowBase + int64_t(it) * BM;
+            double vi[8];
+#pragma unroll
+            for (int ms = 0; ms < 8; ++ms) vi[ms] = A.v[I0 + wm * 64 + ms * 8 + g];
+
+            double acc[8][4][2];
+#pragma unroll
+            for (int ms = 0; ms < 8; ++ms)
+#pragma unroll
+                for (int ns = 0; ns < 4; ++ns) acc[ms][ns][0] = acc[ms][ns][1] = 0.0;
+
+            for (int kc = 0; kc < nk; ++kc, ++cs) {
+                cp_async_wait<NSTAGE - 2>();
+                __syncthreads();
+                if (ps < total) {
+                    issue(ps % NSTAGE);
+                    advance();
+                }
+                cp_async_commit();
+                ++ps;
+
+                const double* sL = stages + (cs % NSTAGE) * STAGE_DOUBLES;
+                const double* sR = sL + BM * KS;
+                const int nks = (min(KC, A.dp - kc * KC)) >> 2;
+                const double* aBase = sL + (wm * 64 + g) * KS + t4;
+                const double* bBase = sR + (wn * 32 + g) * KS + t4;
+#pragma unroll
+                for (int ks = 0; ks < KC / 4; ++ks) {
+                    if (ks < nks) {
+                        double af[8], bf[4];
+#pragma unroll
+                        for (int ms = 0; ms < 8; ++ms) af[ms] = aBase[ms * 8 * KS + ks * 4];
+#pragma unroll
+                        for (int ns = 0; ns < 4; ++ns) bf[ns] = bBase[ns * 8 * KS + ks * 4];
+#pragma unroll
+                        for (int ms = 0; ms < 8; ++ms)
+#pragma unroll
+                            for (int ns = 0; ns < 4; ++ns)
+                                dmma884(acc[ms][ns][0], acc[ms][ns][1], af[ms], bf[ns]);
+                    }
+                }
+            }
+
+            // ---- epilogue: exp, row sums, column sums
+            const bool dtile = diag && (it == jt);
+            double rowp[8];
+#pragma unroll
+            for (int ms = 0; ms < 8; ++ms) {
+                rowp[ms] = 0.0;
+                const int il = wm * 64 + ms * 8 + g;
+#pragma unroll
+                for (int ns = 0; ns < 4; ++ns)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        double e = gauss_exp<EXPMODE>(acc[ms][ns][h], A.ec, tab);
+                        if (dtile) {
+                            const int jl = wn * 32 + ns * 8 + 2 * t4 + h;
+                            e = (jl > il) ? e : 0.0;
+                        }
+                        rowp[ms] = fma(e, vj[ns][h], rowp[ms]);
+                        colacc[ns][h] = fma(e, vi[ms], colacc[ns][h]);
+                    }
+            }
+#pragma unroll
+            for (int ms = 0; ms < 8; ++ms) {
+                double r = rowp[ms];
+                r += __shfl_xor_sync(0xffffffffu, r, 1);
+                r += __shfl_xor_sync(0xffffffffu, r, 2);
+                if (t4 == 0) scr_row[wn * BM + wm * 64 + ms * 8 + g] = r;
+            }
+            __syncthreads();
+            if (tid < BM) {
+                rowacc[it * BM + tid] += ((scr_row[tid] + scr_row[BM + tid]) + scr_row[2 * BM + tid]) +
+                                         scr_row[3 * BM + tid];
+            }
+            // scr_row is rewritten only after the next tile's mainloop barriers.
+        }
+
+        // ---- column sums of this J tile: reduce over g, then over the two M warps
+#pragma unroll
+        for (int ns = 0; ns < 4; ++ns)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double c = colacc[ns][h];
+                c += __shfl_xor_sync(0xffffffffu, c, 4);
+                c += __shfl_xor_sync(0xffffffffu, c, 8);
+                c += __shfl_xor_sync(0xffffffffu, c, 16);
+                if (g == 0) scr_col[wm * BM + wn * 32 + ns * 8 + 2 * t4 + h] = c;
+            }
+        __syncthreads();
+        if (tid < BM) {
+            const double c = scr_col[tid] + scr_col[BM + tid];
+            if (diag) {
+                rowacc[jt * BM + tid] += c;
+            } else {
+                A.part[int64_t(sa) * A.n_pad + J0 + tid] = c;
+            }
+        }
+        // scr_col is rewritten only after the next J's mainloop barriers.
+    }
+    __syncthreads();
+    double* dst = A.part + int64_t(sb) * A.n_pad + rowBase;
+    for (int i = tid; i < A.st; i += NTHREADS) dst[i] = rowacc[i];
+}
+
+// out_i = sum_x part[x][i] (owned slots only) + (1 + lambda) v_i  (diag, rank 0)
+__global__ void matvec_finish_kernel(const double* __restrict__ part, int ns_count, int64_t n_pad,
+                                     int64_t n, int st, const uint8_t* __restrict__ owned,
+                                     const double* __restrict__ v, double lambda, int add_diag,
+                                     double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_pad;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        if (i >= n) {
+            out[i] = 0.0;
+            continue;
+        }
+        const int y = int(i / st);
+        double s = 0.0;
+        for (int x = 0; x < ns_count; ++x)
+            if (!owned || owned[int64_t(x) * ns_count + y]) s += part[int64_t(x) * n_pad + i];
+        if (add_diag) {
+            const double vi = v[i];
+            s = (s + vi) + lambda * vi;
+        }
+        out[i] = s;
+    }
+}
+
+}  // namespace
+
+size_t gauss_matvec_smem_bytes(int st) {
+    return sizeof(double) * (size_t(NSTAGE) * STAGE_DOUBLES + st + 4 * BM + 2 * BM + 64);
+}
+
+void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part, int exp_mode,
+                         cudaStream_t stream) {
+    if (p.num_tiles == 0) return;
+    MatvecArgs a;
+    a.L = p.L;
+    a.R = p.R;
+    a.v = v;
+    a.part = part;
+    a.tiles = p.tiles;
+    a.exp_tab = p.exp_tab;
+    a.n_pad = p.n_pad;
+    a.dp = p.dp;
+    a.st = p.st;
+    a.ec = p.ec;
+    const size_t smem = gauss_matvec_smem_bytes(p.st);
+    if (exp_mode == 0) {
+        KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_kernel<0>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        gauss_matvec_kernel<0><<<unsigned(p.num_tiles), NTHREADS, smem, stream>>>(a);
+    } else {
+        KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_kernel<1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        gauss_matvec_kernel<1><<<unsigned(p.num_tiles), NTHREADS, smem, stream>>>(a);
+    }
+    KRR_LAUNCH_CHECK();
+}
+
+void matvec_finish_launch(const GaussMatvecPlan& p, const double* part, const double* v,
+                          double lambda, int add_diag, double* out, cudaStream_t stream) {
+    const int64_t blocks = std::min<int64_t>((p.n_pad + 255) / 256, 148 * 8);
+    matvec_finish_kernel<<<unsigned(blocks), 256, 0, stream>>>(part, p.ns, p.n_pad, p.n, p.st,
+                                                                p.owned, v, lambda, add_diag, out);
+    KRR_LAUNCH_CHECK();
+}
+
+}  // namespace krr

@@ -1,0 +1,90 @@
+// Host-side launch interface of every CUDA kernel in the library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "gauss_exp.cuh"
+
+namespace krr {
+
+// ---------------------------------------------------------------- K1 Gaussian mat-vec
+struct GaussMatvecPlan {
+    const double* L = nullptr;     // n_pad x dp, [x, |x|^2, 1, 0...]
+    const double* R = nullptr;     // n_pad x dp, [-2x, 1, |x|^2, 0...]
+    const int2* tiles = nullptr;   // owned super-tiles (a <= b)
+    int64_t num_tiles = 0;
+    const uint8_t* owned = nullptr;  // NS x NS ownership (nullptr: all owned)
+    const double* exp_tab = nullptr; // 64 doubles
+    int64_t n = 0, n_pad = 0;
+    int dp = 0, st = 0, ns = 0;
+    ExpConsts ec{};
+};
+size_t gauss_matvec_smem_bytes(int st);
+void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part, int exp_mode,
+                         cudaStream_t stream);
+void matvec_finish_launch(const GaussMatvecPlan& p, const double* part, const double* v,
+                          double lambda, int add_diag, double* out, cudaStream_t stream);
+
+// Build L / R operands from X (n x d) on the device; rows >= n and cols >= d+2 zeroed.
+void build_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, int dp,
+                           double* L, double* R, cudaStream_t stream);
+
+// Rectangular cross kernel: out[m] = sum_j exp(-max(0,|a|^2+|x_j|^2-2 a.x_j) scale) c_j
+// (predict_scores, solver.cpp:135-139; no diagonal forcing).  Simple DMMA-free
+// reference-speed kernel (not on the PCG hot path).
+void cross_matvec_launch(const double* Xq, int64_t m, const double* X, int64_t n, int64_t d,
+                         const double* c, int64_t t, double scale, double* out,
+                         cudaStream_t stream);
+
+// ---------------------------------------------------------------- vector algebra (K7)
+// All reductions are deterministic: `nb` fixed block partials then a fixed-order sum.
+int vec_blocks(int64_t n);
+void dot_partial_launch(const double* a, const double* b, int64_t n, double* partial, int nb,
+                        cudaStream_t stream);
+void sum_partials_launch(const double* partial, int nb, double* out, cudaStream_t stream);
+// alpha = rz / pap (pap summed from pap_part), x += alpha p, r -= alpha ap, rr partials.
+// scal[0] <- pap, scal[1] <- alpha (written by block 0).
+void pcg_update_xr_launch(const double* pap_part, int nb, const double* rz, double* x, double* r,
+                          const double* p, const double* ap, int64_t n, double* rr_part,
+                          double* scal, cudaStream_t stream);
+// rz_new = sum(rz_part); beta = rz_new / rz_old; p = z + beta p; *rz_out = rz_new.
+void pcg_update_p_launch(const double* rz_part, int nb, const double* rz_old, double* rz_out,
+                         double* p, const double* z, int64_t n, cudaStream_t stream);
+void copy_launch(double* dst, const double* src, int64_t n, cudaStream_t stream);
+// Gather column c of an n x t row-major matrix into a contiguous vector (and back).
+void gather_col_launch(const double* M, int64_t n, int64_t t, int64_t c, double* out,
+                       cudaStream_t stream);
+void scatter_col_launch(const double* v, int64_t n, int64_t t, int64_t c, double* M,
+                        cudaStream_t stream);
+
+// ---------------------------------------------------------------- RFF (K2)
+// Z[i][k] = sqrt(2/s) * cos(Z[i][k] + b[k]), in place, Z n x s row-major.
+void rff_cos_launch(double* Z, int64_t n, int64_t s, const double* b, cudaStream_t stream);
+
+// ---------------------------------------------------------------- preconditioner (K3-K6)
+// G (s x s, col-major) diag += add; trace -> *trace (nullable)
+void diag_add_launch(double* G, int64_t s, double add, cudaStream_t stream);
+void trace_launch(const double* G, int64_t s, double* out, cudaStream_t stream);
+// min |L_kk| and a finiteness flag: out[0] = min |diag|, out[1] = 1 if any non-finite entry on diag
+void diag_check_launch(const double* G, int64_t s, double* out, cudaStream_t stream);
+// B = U^T stored n x s row-major.  Wpart[chunk][k] = sum_{i in chunk} B[i][k] r_i.
+int gemvT_chunks(int64_t n, int64_t s);
+void gemvT_partial_launch(const double* B, int64_t n, int64_t s, const double* r, double* Wpart,
+                          int nchunks, cudaStream_t stream);
+void reduce_rows_launch(const double* Wpart, int nchunks, int64_t s, double* W,
+                        cudaStream_t stream);
+// z_i = (r_i - B[i] . W) / lambda_p, rz partials (nb blocks).
+int zrow_blocks(int64_t n);
+void precond_z_launch(const double* B, int64_t n, int64_t s, const double* W, const double* r,
+                      double lambda_p, double* z, double* rz_part, int nb, cudaStream_t stream);
+
+// ---------------------------------------------------------------- diagnostics
+void debug_exp_launch(const double* d2, int64_t n, const ExpConsts& ec, const double* tab,
+                      int mode, double* out, cudaStream_t stream);
+// results: see krr_microbench in include/krr_b200.h
+void microbench_run(const ExpConsts& ec, const double* tab, double* results, cudaStream_t stream);
+
+}  // namespace krr

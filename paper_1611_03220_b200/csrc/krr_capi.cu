@@ -1,0 +1,952 @@
+// C-ABI implementation: device context, the device-resident PCG engine, the
+// preconditioner build, and the NCCL plumbing.  See include/krr_b200.h for the
+// reference interface each entry point replaces.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host.hpp"
+#include "kernels.cuh"
+
+namespace krr {
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void cublas_check(cublasStatus_t st, const char* what) {
+    if (st != CUBLAS_STATUS_SUCCESS)
+        fail(KRR_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(int(st)));
+}
+void cusolver_check(cusolverStatus_t st, const char* what) {
+    if (st != CUSOLVER_STATUS_SUCCESS)
+        fail(KRR_ERR_CUDA, std::string(what) + ": cuSOLVER status " + std::to_string(int(st)));
+}
+void nccl_check(ncclResult_t st, const char* what) {
+    if (st != ncclSuccess)
+        fail(KRR_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(st));
+}
+
+template <class T>
+struct DevMem {
+    T* p = nullptr;
+    size_t count = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+    void ensure(size_t n) {
+        if (n <= count && p) return;
+        release();
+        if (n == 0) return;
+        KRR_CUDA(cudaMalloc(&p, n * sizeof(T)));
+        count = n;
+    }
+    T* get() const { return p; }
+};
+
+struct PinnedScalars {
+    double* p = nullptr;
+    PinnedScalars() { KRR_CUDA(cudaMallocHost(&p, 16 * sizeof(double))); }
+    ~PinnedScalars() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+}  // namespace
+
+struct Ctx {
+    int device = 0, rank = 0, world = 1;
+    cudaStream_t stream = nullptr;
+    cublasHandle_t blas = nullptr;
+    cusolverDnHandle_t sol = nullptr;
+    ncclComm_t comm = nullptr;
+    int exp_mode = 1;
+
+    // data
+    bool has_data = false;
+    int64_t n = 0, d = 0;
+    double sigma = 1.0, scale = 0.5;
+    Schedule sched;
+    GaussMatvecPlan plan;
+    DevMem<double> X, L, R, part, exp_tab;
+    DevMem<int2> tiles;
+    DevMem<uint8_t> owned;
+
+    // PCG vectors (n_pad each) and reduction scratch
+    DevMem<double> vin, vout, vx, vr, vz, vp, vap, vy, red, scal, mat_a, mat_b;
+    std::unique_ptr<PinnedScalars> hscal;
+
+    // preconditioner (row shard [z0, z1) of the n rows; world == 1 => all rows)
+    bool has_sketch = false, has_pre = false;
+    int64_t pn = 0, s = 0, z0 = 0, z1 = 0;
+    double lambda_p = 1.0;
+    DevMem<double> Z, G, Gcopy, W, Wpart, work, brff, wrff, chk;
+    DevMem<int> info;
+
+    int nb = 1;  // vector reduction blocks
+
+    void set_device() const { KRR_CUDA(cudaSetDevice(device)); }
+    void sync() const { KRR_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+namespace {
+
+void require_data(const Ctx& c) {
+    if (!c.has_data) fail(KRR_ERR_STATE, "no data set on the context (call krr_set_data first)");
+}
+
+void allreduce_sum(Ctx& c, double* buf, int64_t count) {
+    if (c.world <= 1) return;
+    nccl_check(ncclAllReduce(buf, buf, size_t(count), ncclDouble, ncclSum, c.comm, c.stream),
+               "ncclAllReduce");
+}
+
+// out (n_pad) = (K + lambda I) v, v zero-padded to n_pad.  Replicated on all ranks.
+void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t k1a = nullptr,
+                cudaEvent_t k1b = nullptr) {
+    if (k1a) KRR_CUDA(cudaEventRecord(k1a, c.stream));
+    gauss_matvec_launch(c.plan, v, c.part.get(), c.exp_mode, c.stream);
+    if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
+    matvec_finish_launch(c.plan, c.part.get(), v, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
+    allreduce_sum(c, out, c.plan.n_pad);
+}
+
+void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
+    if (n < 1 || d < 1) fail(KRR_ERR_INVALID_ARGUMENT, "krr_set_data: n and d must be positive");
+    if (!(sigma > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: sigma must be positive");
+    c.set_device();
+    c.has_data = false;
+    c.n = n;
+    c.d = d;
+    c.sigma = sigma;
+    c.scale = 1.0 / (2.0 * sigma * sigma);  // kernels.cpp:79
+    c.sched = make_schedule(n, c.world, c.rank);
+    const int dp = int(((d + 2) + 3) / 4 * 4);
+    const int64_t n_pad = c.sched.n_pad;
+    c.X.ensure(size_t(n * d));
+    KRR_CUDA(cudaMemcpyAsync(c.X.get(), X, sizeof(double) * size_t(n * d), cudaMemcpyHostToDevice,
+                             c.stream));
+    c.L.ensure(size_t(n_pad * dp));
+    c.R.ensure(size_t(n_pad * dp));
+    build_operands_launch(c.X.get(), n, d, n_pad, dp, c.L.get(), c.R.get(), c.stream);
+    const int64_t ntiles = int64_t(c.sched.tiles.size() / 2);
+    c.tiles.ensure(size_t(std::max<int64_t>(1, ntiles)));
+    if (ntiles)
+        KRR_CUDA(cudaMemcpyAsync(c.tiles.get(), c.sched.tiles.data(), sizeof(int2) * size_t(ntiles),
+                                 cudaMemcpyHostToDevice, c.stream));
+    if (c.world > 1) {
+        c.owned.ensure(c.sched.owned.size());
+        KRR_CUDA(cudaMemcpyAsync(c.owned.get(), c.sched.owned.data(), c.sched.owned.size(),
+                                 cudaMemcpyHostToDevice, c.stream));
+    }
+    double tab[64];
+    make_exp_table(tab);
+    c.exp_tab.ensure(64);
+    KRR_CUDA(cudaMemcpyAsync(c.exp_tab.get(), tab, sizeof(tab), cudaMemcpyHostToDevice, c.stream));
+    c.part.ensure(size_t(c.sched.ns * n_pad));
+    for (auto* v : {&c.vin, &c.vout, &c.vx, &c.vr, &c.vz, &c.vp, &c.vap, &c.vy}) {
+        v->ensure(size_t(n_pad));
+        KRR_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(double) * size_t(n_pad), c.stream));
+    }
+    c.nb = vec_blocks(n);
+    c.red.ensure(size_t(4 * 1024));
+    c.scal.ensure(16);
+    KRR_CUDA(cudaMemsetAsync(c.scal.get(), 0, 16 * sizeof(double), c.stream));
+
+    GaussMatvecPlan& p = c.plan;
+    p.L = c.L.get();
+    p.R = c.R.get();
+    p.tiles = c.tiles.get();
+    p.num_tiles = ntiles;
+    p.owned = c.world > 1 ? c.owned.get() : nullptr;
+    p.exp_tab = c.exp_tab.get();
+    p.n = n;
+    p.n_pad = n_pad;
+    p.dp = dp;
+    p.st = int(c.sched.st);
+    p.ns = int(c.sched.ns);
+    p.ec = make_exp_consts(c.scale);
+    c.sync();
+    c.has_data = true;
+}
+
+// ---------------------------------------------------------------- preconditioner
+void sketch_alloc(Ctx& c, int64_t n, int64_t s) {
+    c.pn = n;
+    c.s = s;
+    shard_rows(n, c.world, c.rank, &c.z0, &c.z1);  // contiguous equal blocks
+    c.Z.ensure(size_t(std::max<int64_t>(1, (c.z1 - c.z0) * s)));
+    c.has_sketch = false;
+    c.has_pre = false;
+}
+
+void rff_build(Ctx& c, const double* W, const double* b, int64_t s) {
+    require_data(c);
+    if (s < 1) fail(KRR_ERR_INVALID_ARGUMENT, "ChainSpec: s1 must be at least 1");
+    c.set_device();
+    sketch_alloc(c, c.n, s);
+    c.wrff.ensure(size_t(s * c.d));
+    c.brff.ensure(size_t(s));
+    KRR_CUDA(cudaMemcpyAsync(c.wrff.get(), W, sizeof(double) * size_t(s * c.d),
+                             cudaMemcpyHostToDevice, c.stream));
+    KRR_CUDA(cudaMemcpyAsync(c.brff.get(), b, sizeof(double) * size_t(s), cudaMemcpyHostToDevice,
+                             c.stream));
+    const int64_t rows = c.z1 - c.z0;
+    if (rows > 0) {
+        // Z (rows x s, row-major) = X[z0:z1] W^T  <=>  col-major Z^T (s x rows) = W (X)^T
+        const double one = 1.0, zero = 0.0;
+        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, int(s), int(rows), int(c.d), &one,
+                                 c.wrff.get(), int(c.d), c.X.get() + c.z0 * c.d, int(c.d), &zero,
+                                 c.Z.get(), int(s)),
+                     "cublasDgemm(X W^T)");
+        rff_cos_launch(c.Z.get(), rows, s, c.brff.get(), c.stream);
+    }
+    c.sync();
+    c.has_sketch = true;
+}
+
+void sketch_upload(Ctx& c, const double* Z, int64_t n, int64_t s) {
+    if (n < 1 || s < 1) fail(KRR_ERR_INVALID_ARGUMENT, "krr_sketch_upload: empty sketch");
+    c.set_device();
+    sketch_alloc(c, n, s);
+    const int64_t rows = c.z1 - c.z0;
+    if (rows > 0)
+        KRR_CUDA(cudaMemcpyAsync(c.Z.get(), Z + c.z0 * s, sizeof(double) * size_t(rows * s),
+                                 cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+    c.has_sketch = true;
+}
+
+// Returns true when the factorisation succeeded (finite, positive pivots).
+bool try_potrf(Ctx& c, int64_t s) {
+    // Non-finite input (e.g. Z'Z overflowed to inf) can slip through potrf's pivot test.
+    diag_check_launch(c.G.get(), s, c.chk.get(), c.stream);
+    double h[2];
+    KRR_CUDA(cudaMemcpyAsync(h, c.chk.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (h[1] != 0.0) return false;
+    int lwork = 0;
+    cusolver_check(cusolverDnDpotrf_bufferSize(c.sol, CUBLAS_FILL_MODE_LOWER, int(s), c.G.get(),
+                                               int(s), &lwork),
+                   "potrf_bufferSize");
+    c.work.ensure(size_t(std::max(1, lwork)));
+    cusolver_check(cusolverDnDpotrf(c.sol, CUBLAS_FILL_MODE_LOWER, int(s), c.G.get(), int(s),
+                                    c.work.get(), lwork, c.info.get()),
+                   "cusolverDnDpotrf");
+    int hinfo = 0;
+    KRR_CUDA(cudaMemcpyAsync(&hinfo, c.info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    diag_check_launch(c.G.get(), s, c.chk.get(), c.stream);
+    KRR_CUDA(cudaMemcpyAsync(h, c.chk.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return hinfo == 0 && h[1] == 0.0;
+}
+
+// build_preconditioner, precond.cpp:20-40.
+void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
+    if (!(lambda_p > 0.0))
+        fail(KRR_ERR_NON_POSITIVE_LAMBDA, "build_preconditioner: lambda_p must be positive");
+    if (!c.has_sketch) fail(KRR_ERR_STATE, "no sketch on the context (krr_rff_build / krr_sketch_upload)");
+    c.set_device();
+    const int64_t s = c.s;
+    const int64_t rows = c.z1 - c.z0;
+    c.G.ensure(size_t(s * s));
+    c.Gcopy.ensure(size_t(s * s));
+    c.chk.ensure(4);
+    c.info.ensure(1);
+    const double one = 1.0, zero = 0.0;
+    if (rows > 0) {
+        // G = Z^T Z (lower): Z row-major rows x s == col-major A = Z^T (s x rows); G = A A^T.
+        cublas_check(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(s), int(rows), &one,
+                                 c.Z.get(), int(s), &zero, c.G.get(), int(s)),
+                     "cublasDsyrk(Z^T Z)");
+    } else {
+        KRR_CUDA(cudaMemsetAsync(c.G.get(), 0, sizeof(double) * size_t(s * s), c.stream));
+    }
+    allreduce_sum(c, c.G.get(), s * s);
+    diag_add_launch(c.G.get(), s, lambda_p, c.stream);  // precond.cpp:24
+    KRR_CUDA(cudaMemcpyAsync(c.Gcopy.get(), c.G.get(), sizeof(double) * size_t(s * s),
+                             cudaMemcpyDeviceToDevice, c.stream));
+    if (jitter_used) *jitter_used = 0;
+    if (!try_potrf(c, s)) {
+        // precond.cpp:29-33: one retry with 1e-12 trace / s on the diagonal.
+        KRR_CUDA(cudaMemcpyAsync(c.G.get(), c.Gcopy.get(), sizeof(double) * size_t(s * s),
+                                 cudaMemcpyDeviceToDevice, c.stream));
+        trace_launch(c.G.get(), s, c.chk.get() + 2, c.stream);
+        double tr = 0.0;
+        KRR_CUDA(cudaMemcpyAsync(&tr, c.chk.get() + 2, sizeof(double), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+        diag_add_launch(c.G.get(), s, 1e-12 * tr / double(s), c.stream);
+        if (jitter_used) *jitter_used = 1;
+        if (!try_potrf(c, s))
+            fail(KRR_ERR_NOT_POSITIVE_DEFINITE, "cholesky: non-positive pivot encountered");
+    }
+    // numerics.cpp:62-63
+    double h[2];
+    diag_check_launch(c.G.get(), s, c.chk.get(), c.stream);
+    KRR_CUDA(cudaMemcpyAsync(h, c.chk.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (h[0] < 1e-300) fail(KRR_ERR_SINGULAR_TRIANGULAR, "triangular_solve: diagonal entry below 1e-300");
+    if (rows > 0) {
+        // U = L^-1 Z^T in place: col-major s x rows, ld = s  (precond.cpp:38)
+        cublas_check(cublasDtrsm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                                 CUBLAS_DIAG_NON_UNIT, int(s), int(rows), &one, c.G.get(), int(s),
+                                 c.Z.get(), int(s)),
+                     "cublasDtrsm(L^-1 Z^T)");
+    }
+    c.lambda_p = lambda_p;
+    c.sync();
+    c.has_pre = true;
+}
+
+// z (full length pn, zero-padded beyond) = (r - U^T U r) / lambda_p
+void precond_apply_dev(Ctx& c, const double* r, double* z) {
+    if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
+    const int64_t s = c.s;
+    const int64_t rows = c.z1 - c.z0;
+    const int nchunks = gemvT_chunks(std::max<int64_t>(1, rows), s);
+    c.W.ensure(size_t(s));
+    c.Wpart.ensure(size_t(nchunks) * size_t(s));
+    if (rows > 0) {
+        gemvT_partial_launch(c.Z.get(), rows, s, r + c.z0, c.Wpart.get(), nchunks, c.stream);
+        reduce_rows_launch(c.Wpart.get(), nchunks, s, c.W.get(), c.stream);
+    } else {
+        KRR_CUDA(cudaMemsetAsync(c.W.get(), 0, sizeof(double) * size_t(s), c.stream));
+    }
+    allreduce_sum(c, c.W.get(), s);
+    const int nbz = zrow_blocks(std::max<int64_t>(1, rows));
+    c.red.ensure(size_t(4 * 1024));
+    if (rows > 0)
+        precond_z_launch(c.Z.get(), rows, s, c.W.get(), r + c.z0, c.lambda_p, z + c.z0,
+                         c.red.get() + 3 * 1024, nbz, c.stream);
+    if (c.world > 1) {
+        // Every rank owns an equal block `per` of rows (the last one possibly short);
+        // zero the non-owned rows and sum — an all-gather expressed as an all-reduce,
+        // valid for any n.
+        if (c.z0 > 0) KRR_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * size_t(c.z0), c.stream));
+        if (c.z1 < c.pn)
+            KRR_CUDA(cudaMemsetAsync(z + c.z1, 0, sizeof(double) * size_t(c.pn - c.z1), c.stream));
+        allreduce_sum(c, z, c.pn);
+    }
+}
+
+// ---------------------------------------------------------------- PCG core (solver.cpp:22-67)
+using DevOp = std::function<void(const double* din, double* dout)>;
+using HostObserver = std::function<void(int, const double* dx)>;
+
+struct PcgOut {
+    int iterations = 0;
+    int converged = 0;
+    double final_residual = 0.0;
+};
+
+// Vectors live in c.vx/vr/vz/vp/vap (length >= n, zero beyond n).  y is a device
+// vector of length n (zero-padded to the buffer length).  The solution is left in c.vx.
+PcgOut pcg_core(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, const double* y, double tau,
+                int max_iter, double* hist, const HostObserver* obs) {
+    if (!(tau > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "pcg_solve: tau must be positive");
+    if (max_iter < 1) fail(KRR_ERR_INVALID_ARGUMENT, "pcg_solve: max_iter must be at least 1");
+    const int nb = vec_blocks(n);
+    double* red = c.red.get();
+    double* pap_part = red;
+    double* rr_part = red + 1024;
+    double* rz_part = red + 2048;
+    double* scal = c.scal.get();  // [0] pap [1] alpha [2] rz(even) [3] rz(odd) [4] rr [5] yy
+    double* hs = c.hscal->p;
+    PcgOut out;
+    KRR_CUDA(cudaMemsetAsync(c.vx.get(), 0, sizeof(double) * size_t(n), c.stream));
+    dot_partial_launch(y, y, n, rr_part, nb, c.stream);
+    sum_partials_launch(rr_part, nb, scal + 5, c.stream);
+    KRR_CUDA(cudaMemcpyAsync(hs + 5, scal + 5, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const double norm_y = std::sqrt(hs[5]);
+    if (norm_y == 0.0) {  // solver.cpp:30-34
+        out.converged = 1;
+        return out;
+    }
+    copy_launch(c.vr.get(), y, n, c.stream);  // r = y
+    double* z = c.vz.get();
+    if (M) {
+        (*M)(c.vr.get(), z);
+    } else {
+        z = c.vr.get();
+    }
+    copy_launch(c.vp.get(), z, n, c.stream);  // p = z
+    dot_partial_launch(c.vr.get(), z, n, rz_part, nb, c.stream);
+    sum_partials_launch(rz_part, nb, scal + 2, c.stream);
+    int cur = 0;
+    for (int it = 1; it <= max_iter; ++it) {
+        A(c.vp.get(), c.vap.get());
+        dot_partial_launch(c.vp.get(), c.vap.get(), n, pap_part, nb, c.stream);
+        pcg_update_xr_launch(pap_part, nb, scal + 2 + cur, c.vx.get(), c.vr.get(), c.vp.get(),
+                             c.vap.get(), n, rr_part, scal, c.stream);
+        sum_partials_launch(rr_part, nb, scal + 4, c.stream);
+        KRR_CUDA(cudaMemcpyAsync(hs, scal, 5 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        const double pap = hs[0];
+        if (!(pap > 0.0))
+            fail(KRR_ERR_BREAKDOWN, "pcg_solve: p'Ap <= 0, operator is not positive definite");
+        const double rel = std::sqrt(hs[4]) / norm_y;
+        out.iterations = it;
+        out.final_residual = rel;
+        if (hist) hist[it - 1] = rel;
+        if (obs) (*obs)(it, c.vx.get());
+        if (rel <= tau) {
+            out.converged = 1;
+            return out;
+        }
+        if (M) (*M)(c.vr.get(), z);
+        dot_partial_launch(c.vr.get(), z, n, rz_part, nb, c.stream);
+        pcg_update_p_launch(rz_part, nb, scal + 2 + cur, scal + 2 + (cur ^ 1), c.vp.get(), z, n,
+                            c.stream);
+        cur ^= 1;
+    }
+    out.converged = 0;
+    return out;
+}
+
+DevOp gaussian_op(Ctx& c, double lambda) {
+    return [&c, lambda](const double* din, double* dout) { matvec_dev(c, din, dout, lambda); };
+}
+
+DevOp precond_op(Ctx& c) {
+    return [&c](const double* din, double* dout) { precond_apply_dev(c, din, dout); };
+}
+
+// solve_regularized (solver.cpp:69-94): per-column sequential PCG.
+void solve_gaussian(Ctx& c, double lambda, const double* Y, int64_t t, double tau, int max_iter,
+                    int use_precond, double* C, krr_rhs_stats* stats, double* hist,
+                    int64_t* total_matvecs) {
+    require_data(c);
+    if (!(lambda > 0.0)) fail(KRR_ERR_NON_POSITIVE_LAMBDA, "train: lambda must be positive");
+    if (t < 1) fail(KRR_ERR_DIMENSION_MISMATCH, "solve_regularized: Y needs at least one column");
+    if (use_precond) {
+        if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
+        if (c.pn != c.n)
+            fail(KRR_ERR_DIMENSION_MISMATCH, "Preconditioner: dimension mismatch");
+    }
+    c.set_device();
+    const int64_t n = c.n;
+    c.mat_a.ensure(size_t(n * t));
+    c.mat_b.ensure(size_t(n * t));
+    KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), Y, sizeof(double) * size_t(n * t), cudaMemcpyHostToDevice,
+                             c.stream));
+    const DevOp A = gaussian_op(c, lambda);
+    const DevOp M = precond_op(c);
+    int64_t total = 0;
+    for (int64_t j = 0; j < t; ++j) {
+        // K1 reads the padded tail of p: keep every PCG vector zero beyond n.
+        for (auto* v : {&c.vx, &c.vr, &c.vz, &c.vp, &c.vap, &c.vy})
+            KRR_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(double) * v->count, c.stream));
+        gather_col_launch(c.mat_a.get(), n, t, j, c.vy.get(), c.stream);
+        const PcgOut o = pcg_core(c, n, A, use_precond ? &M : nullptr, c.vy.get(), tau, max_iter,
+                                  hist ? hist + j * max_iter : nullptr, nullptr);
+        scatter_col_launch(c.vx.get(), n, t, j, c.mat_b.get(), c.stream);
+        stats[j].iterations = o.iterations;
+        stats[j].converged = o.converged;
+        stats[j].final_residual = o.final_residual;
+        total += o.iterations;
+    }
+    KRR_CUDA(cudaMemcpyAsync(C, c.mat_b.get(), sizeof(double) * size_t(n * t), cudaMemcpyDeviceToHost,
+                             c.stream));
+    c.sync();
+    if (total_matvecs) *total_matvecs = total;
+}
+
+void ctx_init_common(Ctx& c) {
+    c.set_device();
+    KRR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    cublas_check(cublasCreate(&c.blas), "cublasCreate");
+    cublas_check(cublasSetStream(c.blas, c.stream), "cublasSetStream");
+    cublas_check(cublasSetMathMode(c.blas, CUBLAS_DEFAULT_MATH), "cublasSetMathMode");
+    cusolver_check(cusolverDnCreate(&c.sol), "cusolverDnCreate");
+    cusolver_check(cusolverDnSetStream(c.sol, c.stream), "cusolverDnSetStream");
+    c.hscal = std::make_unique<PinnedScalars>();
+    c.red.ensure(size_t(4 * 1024));
+    c.scal.ensure(16);
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return KRR_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return KRR_ERR_INVALID_ARGUMENT;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("host allocation failed: ") + e.what();
+        return KRR_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return KRR_ERR_CUDA;
+    }
+}
+
+Ctx* as_ctx(krr_ctx* p) {
+    if (!p) fail(KRR_ERR_INVALID_ARGUMENT, "null context");
+    return reinterpret_cast<Ctx*>(p);
+}
+
+}  // namespace
+}  // namespace krr
+
+using krr::Ctx;
+using krr::fail;
+using krr::guard;
+
+extern "C" {
+
+const char* krr_last_error(void) { return krr::g_last_error.c_str(); }
+int krr_abi_version(void) { return KRR_B200_ABI_VERSION; }
+
+int krr_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int krr_ctx_create(int device, krr_ctx** out) {
+    return guard([&] {
+        if (!out) fail(KRR_ERR_INVALID_ARGUMENT, "null output pointer");
+        *out = nullptr;
+        if (krr_device_count() <= device || device < 0)
+            fail(KRR_ERR_CUDA, "CUDA device " + std::to_string(device) + " not available");
+        auto c = std::make_unique<Ctx>();
+        c->device = device;
+        krr::ctx_init_common(*c);
+        *out = reinterpret_cast<krr_ctx*>(c.release());
+    });
+}
+
+int krr_nccl_unique_id(void* out_128_bytes) {
+    return guard([&] {
+        ncclUniqueId id;
+        krr::nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(out_128_bytes, &id, sizeof(id));
+    });
+}
+
+int krr_ctx_create_dist(int device, int rank, int world, const void* nccl_id, krr_ctx** out) {
+    return guard([&] {
+        if (!out || !nccl_id) fail(KRR_ERR_INVALID_ARGUMENT, "null pointer");
+        *out = nullptr;
+        if (world < 1 || rank < 0 || rank >= world) fail(KRR_ERR_INVALID_ARGUMENT, "bad rank/world");
+        if (krr_device_count() <= device || device < 0)
+            fail(KRR_ERR_CUDA, "CUDA device " + std::to_string(device) + " not available");
+        auto c = std::make_unique<Ctx>();
+        c->device = device;
+        c->rank = rank;
+        c->world = world;
+        krr::ctx_init_common(*c);
+        if (world > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            krr::nccl_check(ncclCommInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
+        }
+        *out = reinterpret_cast<krr_ctx*>(c.release());
+    });
+}
+
+int krr_ctx_destroy(krr_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        Ctx* c = krr::as_ctx(ctx);
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        if (c->comm) ncclCommDestroy(c->comm);
+        if (c->sol) cusolverDnDestroy(c->sol);
+        if (c->blas) cublasDestroy(c->blas);
+        cudaStream_t st = c->stream;
+        delete c;  // frees device buffers
+        if (st) cudaStreamDestroy(st);
+    });
+}
+
+int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out) {
+    return guard([&] {
+        (void)krr::as_ctx(ctx);
+        *out = krr::g_launches.load();
+    });
+}
+
+int krr_set_data(krr_ctx* ctx, const double* X, int64_t n, int64_t d, double sigma) {
+    return guard([&] { krr::set_data(*krr::as_ctx(ctx), X, n, d, sigma); });
+}
+
+int krr_kernel_matvec_device(krr_ctx* ctx, double lambda, const double* dV, int64_t t,
+                             double* dOut) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (t < 1) fail(KRR_ERR_DIMENSION_MISMATCH, "matvec: V needs at least one column");
+        c.set_device();
+        const int64_t n = c.n;
+        for (int64_t j = 0; j < t; ++j) {
+            if (t == 1) {
+                KRR_CUDA(cudaMemcpyAsync(c.vin.get(), dV, sizeof(double) * size_t(n),
+                                         cudaMemcpyDeviceToDevice, c.stream));
+            } else {
+                krr::gather_col_launch(dV, n, t, j, c.vin.get(), c.stream);
+            }
+            krr::matvec_dev(c, c.vin.get(), c.vout.get(), lambda);
+            if (t == 1) {
+                KRR_CUDA(cudaMemcpyAsync(dOut, c.vout.get(), sizeof(double) * size_t(n),
+                                         cudaMemcpyDeviceToDevice, c.stream));
+            } else {
+                krr::scatter_col_launch(c.vout.get(), n, t, j, dOut, c.stream);
+            }
+        }
+        c.sync();
+    });
+}
+
+int krr_kernel_matvec(krr_ctx* ctx, double lambda, const double* V, int64_t t, double* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (t < 1) fail(KRR_ERR_DIMENSION_MISMATCH, "matvec: V needs at least one column");
+        c.set_device();
+        const int64_t n = c.n;
+        c.mat_a.ensure(size_t(n * t));
+        c.mat_b.ensure(size_t(n * t));
+        KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), V, sizeof(double) * size_t(n * t),
+                                 cudaMemcpyHostToDevice, c.stream));
+        for (int64_t j = 0; j < t; ++j) {
+            krr::gather_col_launch(c.mat_a.get(), n, t, j, c.vin.get(), c.stream);
+            krr::matvec_dev(c, c.vin.get(), c.vout.get(), lambda);
+            krr::scatter_col_launch(c.vout.get(), n, t, j, c.mat_b.get(), c.stream);
+        }
+        KRR_CUDA(cudaMemcpyAsync(out, c.mat_b.get(), sizeof(double) * size_t(n * t),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
+int krr_predict_scores(krr_ctx* ctx, const double* Xq, int64_t m, const double* C, int64_t t,
+                       double* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (t < 1 || m < 0) fail(KRR_ERR_DIMENSION_MISMATCH, "predict: bad shapes");
+        c.set_device();
+        if (m == 0) return;
+        krr::DevMem<double> q, cc, o;
+        q.ensure(size_t(m * c.d));
+        cc.ensure(size_t(c.n * t));
+        o.ensure(size_t(m * t));
+        KRR_CUDA(cudaMemcpyAsync(q.get(), Xq, sizeof(double) * size_t(m * c.d), cudaMemcpyHostToDevice,
+                                 c.stream));
+        KRR_CUDA(cudaMemcpyAsync(cc.get(), C, sizeof(double) * size_t(c.n * t), cudaMemcpyHostToDevice,
+                                 c.stream));
+        krr::cross_matvec_launch(q.get(), m, c.X.get(), c.n, c.d, cc.get(), t, c.scale, o.get(),
+                                 c.stream);
+        KRR_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * size_t(m * t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+    });
+}
+
+int krr_rff_realize(uint64_t master_seed, int64_t d, int64_t s, double sigma, double* W,
+                    double* b) {
+    return guard([&] { krr::rff_realize(master_seed, d, s, sigma, W, b); });
+}
+
+int krr_rff_build(krr_ctx* ctx, const double* W, const double* b, int64_t s) {
+    return guard([&] { krr::rff_build(*krr::as_ctx(ctx), W, b, s); });
+}
+
+int krr_rff_download(krr_ctx* ctx, double* Zout) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (!c.has_sketch || c.has_pre) fail(KRR_ERR_STATE, "no raw sketch on the device");
+        if (c.world != 1) fail(KRR_ERR_STATE, "krr_rff_download is single-rank only");
+        c.set_device();
+        KRR_CUDA(cudaMemcpyAsync(Zout, c.Z.get(), sizeof(double) * size_t(c.pn * c.s),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
+int krr_sketch_upload(krr_ctx* ctx, const double* Z, int64_t n, int64_t s) {
+    return guard([&] { krr::sketch_upload(*krr::as_ctx(ctx), Z, n, s); });
+}
+
+int krr_precond_build(krr_ctx* ctx, double lambda_p, int* jitter_used) {
+    return guard([&] { krr::precond_build(*krr::as_ctx(ctx), lambda_p, jitter_used); });
+}
+
+int krr_precond_apply(krr_ctx* ctx, const double* Rm, int64_t t, double* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
+        if (t < 1) fail(KRR_ERR_DIMENSION_MISMATCH, "Preconditioner: dimension mismatch");
+        c.set_device();
+        const int64_t n = c.pn;
+        krr::DevMem<double> a, b, vi, vo;
+        a.ensure(size_t(n * t));
+        b.ensure(size_t(n * t));
+        vi.ensure(size_t(n));
+        vo.ensure(size_t(n));
+        KRR_CUDA(cudaMemcpyAsync(a.get(), Rm, sizeof(double) * size_t(n * t), cudaMemcpyHostToDevice,
+                                 c.stream));
+        for (int64_t j = 0; j < t; ++j) {
+            krr::gather_col_launch(a.get(), n, t, j, vi.get(), c.stream);
+            krr::precond_apply_dev(c, vi.get(), vo.get());
+            krr::scatter_col_launch(vo.get(), n, t, j, b.get(), c.stream);
+        }
+        KRR_CUDA(cudaMemcpyAsync(out, b.get(), sizeof(double) * size_t(n * t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+    });
+}
+
+int krr_precond_download_u(krr_ctx* ctx, double* U) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
+        if (c.world != 1) fail(KRR_ERR_STATE, "krr_precond_download_u is single-rank only");
+        c.set_device();
+        std::vector<double> b(static_cast<size_t>(c.pn * c.s));
+        KRR_CUDA(cudaMemcpyAsync(b.data(), c.Z.get(), sizeof(double) * b.size(), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+        for (int64_t i = 0; i < c.pn; ++i)
+            for (int64_t k = 0; k < c.s; ++k) U[k * c.pn + i] = b[size_t(i * c.s + k)];
+    });
+}
+
+int krr_precond_drop(krr_ctx* ctx) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        c.has_pre = false;
+        c.has_sketch = false;
+        c.Z.release();
+        c.G.release();
+        c.Gcopy.release();
+    });
+}
+
+int krr_pcg_solve(krr_ctx* ctx, double lambda, const double* Y, int64_t t, double tau, int max_iter,
+                  int use_precond, double* C, krr_rhs_stats* stats, double* residual_history,
+                  int64_t* total_matvecs) {
+    return guard([&] {
+        krr::solve_gaussian(*krr::as_ctx(ctx), lambda, Y, t, tau, max_iter, use_precond, C, stats,
+                            residual_history, total_matvecs);
+    });
+}
+
+int krr_pcg_solve_operator(krr_ctx* ctx, int64_t n, krr_operator_cb apply_a, void* user_a,
+                           krr_operator_cb apply_m, void* user_m, const double* y, double tau,
+                           int max_iter, krr_observer_cb observer, void* user_obs, double* x,
+                           krr_rhs_stats* stats, double* residual_history) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (n < 1) fail(KRR_ERR_DIMENSION_MISMATCH, "pcg_solve: empty system");
+        if (!apply_a) fail(KRR_ERR_INVALID_ARGUMENT, "pcg_solve: null operator");
+        c.set_device();
+        // Use private vectors sized n (independent of any data on the context).
+        for (auto* v : {&c.vx, &c.vr, &c.vz, &c.vp, &c.vap, &c.vy})
+            if (v->count < size_t(n)) {
+                v->ensure(size_t(n));
+                KRR_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(double) * size_t(n), c.stream));
+            }
+        std::vector<double> hin(static_cast<size_t>(n)), hout(static_cast<size_t>(n));
+        auto host_op = [&](krr_operator_cb cb, void* user) {
+            return krr::DevOp([&, cb, user](const double* din, double* dout) {
+                KRR_CUDA(cudaMemcpyAsync(hin.data(), din, sizeof(double) * size_t(n),
+                                         cudaMemcpyDeviceToHost, c.stream));
+                c.sync();
+                if (cb(user, hin.data(), hout.data(), n) != 0)
+                    fail(KRR_ERR_CALLBACK, "operator callback failed");
+                KRR_CUDA(cudaMemcpyAsync(dout, hout.data(), sizeof(double) * size_t(n),
+                                         cudaMemcpyHostToDevice, c.stream));
+                c.sync();
+            });
+        };
+        const krr::DevOp A = host_op(apply_a, user_a);
+        const krr::DevOp M = apply_m ? host_op(apply_m, user_m) : krr::DevOp();
+        std::vector<double> hx(static_cast<size_t>(n));
+        const krr::HostObserver obs = [&](int it, const double* dx) {
+            KRR_CUDA(cudaMemcpyAsync(hx.data(), dx, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
+                                     c.stream));
+            c.sync();
+            observer(user_obs, it, hx.data(), n);
+        };
+        KRR_CUDA(cudaMemcpyAsync(c.vy.get(), y, sizeof(double) * size_t(n), cudaMemcpyHostToDevice,
+                                 c.stream));
+        const krr::PcgOut o = krr::pcg_core(c, n, A, apply_m ? &M : nullptr, c.vy.get(), tau, max_iter,
+                                            residual_history, observer ? &obs : nullptr);
+        KRR_CUDA(cudaMemcpyAsync(x, c.vx.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+        stats->iterations = o.iterations;
+        stats->converged = o.converged;
+        stats->final_residual = o.final_residual;
+    });
+}
+
+int krr_train(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const double* Y, int64_t t,
+              double sigma, double lambda, double lambda_p, int64_t s, uint64_t master_seed, double tau,
+              int max_iter, double* C, krr_rhs_stats* stats, double* residual_history,
+              int64_t* total_matvecs, double* phase_ms) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (n < 1) fail(KRR_ERR_INVALID_ARGUMENT, "train: dataset is empty");          // solver.cpp:97
+        if (!(lambda > 0.0)) fail(KRR_ERR_NON_POSITIVE_LAMBDA, "train: lambda must be positive");
+        if (s < 1) fail(KRR_ERR_INVALID_ARGUMENT, "ChainSpec: s1 must be at least 1");
+        const double lp = lambda_p > 0.0 ? lambda_p : lambda;                           // solver.cpp:102
+        krr::set_data(c, X, n, d, sigma);
+        std::vector<double> W(static_cast<size_t>(s * d)), b(static_cast<size_t>(s));
+        krr::rff_realize(master_seed, d, s, sigma, W.data(), b.data());
+        cudaEvent_t ev[4];
+        for (auto& e : ev) KRR_CUDA(cudaEventCreate(&e));
+        KRR_CUDA(cudaEventRecord(ev[0], c.stream));
+        krr::rff_build(c, W.data(), b.data(), s);
+        KRR_CUDA(cudaEventRecord(ev[1], c.stream));
+        krr::precond_build(c, lp, nullptr);
+        KRR_CUDA(cudaEventRecord(ev[2], c.stream));
+        krr::solve_gaussian(c, lambda, Y, t, tau, max_iter, 1, C, stats, residual_history,
+                            total_matvecs);
+        KRR_CUDA(cudaEventRecord(ev[3], c.stream));
+        KRR_CUDA(cudaEventSynchronize(ev[3]));
+        if (phase_ms) {
+            float a = 0, b2 = 0, c3 = 0, tot = 0;
+            KRR_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+            KRR_CUDA(cudaEventElapsedTime(&b2, ev[1], ev[2]));
+            KRR_CUDA(cudaEventElapsedTime(&c3, ev[2], ev[3]));
+            KRR_CUDA(cudaEventElapsedTime(&tot, ev[0], ev[3]));
+            phase_ms[0] = a;
+            phase_ms[1] = b2;
+            phase_ms[2] = c3;
+            phase_ms[3] = tot;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int krr_schedule(int64_t n, int world, int rank, int64_t* super_rows, int64_t* num_super,
+                 int32_t* tiles, int64_t max_tiles, int64_t* num_tiles) {
+    return guard([&] {
+        const krr::Schedule s = krr::make_schedule(n, world, rank);
+        if (super_rows) *super_rows = s.st;
+        if (num_super) *num_super = s.ns;
+        const int64_t nt = int64_t(s.tiles.size() / 2);
+        if (num_tiles) *num_tiles = nt;
+        if (tiles) {
+            if (max_tiles < nt) fail(KRR_ERR_DIMENSION_MISMATCH, "krr_schedule: tile buffer too small");
+            std::memcpy(tiles, s.tiles.data(), sizeof(int32_t) * s.tiles.size());
+        }
+    });
+}
+
+int krr_shard_rows(int64_t n, int world, int rank, int64_t* row_begin, int64_t* row_end) {
+    return guard([&] { krr::shard_rows(n, world, rank, row_begin, row_end); });
+}
+
+int krr_generate_config(int cfg, int64_t n, int64_t d, int64_t t, uint64_t seed, double* X,
+                        double* Y) {
+    return guard([&] { krr::generate_config(cfg, n, d, t, seed, X, Y); });
+}
+
+int krr_rlsc_encode(const int32_t* classes, int64_t n, int32_t num_classes, double* Y) {
+    return guard([&] { krr::rlsc_encode(classes, n, num_classes, Y); });
+}
+
+int krr_bench_matvec(krr_ctx* ctx, double lambda, int steps, double* total_ms, double* k1_ms) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (steps < 1) fail(KRR_ERR_INVALID_ARGUMENT, "steps must be positive");
+        c.set_device();
+        {
+            std::vector<double> v(size_t(c.plan.n_pad), 0.0);
+            std::mt19937_64 gen(12345);
+            std::normal_distribution<double> nd(0.0, 1.0);
+            for (int64_t i = 0; i < c.n; ++i) v[size_t(i)] = nd(gen);
+            KRR_CUDA(cudaMemcpyAsync(c.vin.get(), v.data(), sizeof(double) * v.size(),
+                                     cudaMemcpyHostToDevice, c.stream));
+            c.sync();
+        }
+        std::vector<cudaEvent_t> ev(size_t(2 * steps + 2));
+        for (auto& e : ev) KRR_CUDA(cudaEventCreate(&e));
+        KRR_CUDA(cudaEventRecord(ev[0], c.stream));
+        for (int k = 0; k < steps; ++k)
+            krr::matvec_dev(c, c.vin.get(), c.vout.get(), lambda, ev[size_t(2 + 2 * k)],
+                            ev[size_t(3 + 2 * k)]);
+        KRR_CUDA(cudaEventRecord(ev[1], c.stream));
+        KRR_CUDA(cudaEventSynchronize(ev[1]));
+        float tot = 0.f;
+        KRR_CUDA(cudaEventElapsedTime(&tot, ev[0], ev[1]));
+        double k1 = 0.0;
+        for (int k = 0; k < steps; ++k) {
+            float ms = 0.f;
+            KRR_CUDA(cudaEventElapsedTime(&ms, ev[size_t(2 + 2 * k)], ev[size_t(3 + 2 * k)]));
+            k1 += ms;
+        }
+        *total_ms = tot;
+        *k1_ms = k1 / steps;
+        for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int krr_microbench(krr_ctx* ctx, double* results) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        c.set_device();
+        double tab[64];
+        krr::make_exp_table(tab);
+        krr::DevMem<double> dt;
+        dt.ensure(64);
+        KRR_CUDA(cudaMemcpy(dt.get(), tab, sizeof(tab), cudaMemcpyHostToDevice));
+        const krr::ExpConsts ec = krr::make_exp_consts(1.0 / 72.0);
+        krr::microbench_run(ec, dt.get(), results, c.stream);
+    });
+}
+
+int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale, int mode,
+                        double* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        c.set_device();
+        double tab[64];
+        krr::make_exp_table(tab);
+        krr::DevMem<double> dt, din, dout;
+        dt.ensure(64);
+        din.ensure(size_t(std::max<int64_t>(1, n)));
+        dout.ensure(size_t(std::max<int64_t>(1, n)));
+        KRR_CUDA(cudaMemcpyAsync(dt.get(), tab, sizeof(tab), cudaMemcpyHostToDevice, c.stream));
+        KRR_CUDA(cudaMemcpyAsync(din.get(), d2, sizeof(double) * size_t(n), cudaMemcpyHostToDevice,
+                                 c.stream));
+        krr::debug_exp_launch(din.get(), n, krr::make_exp_consts(scale), dt.get(), mode, dout.get(),
+                              c.stream);
+        KRR_CUDA(cudaMemcpyAsync(out, dout.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+    });
+}
+
+}  // extern "C"

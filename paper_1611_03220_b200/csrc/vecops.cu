@@ -1,0 +1,198 @@
+// K7 — PCG vector algebra (HBM-bound, deterministic reductions) and operand prep.
+//
+// Reference: pcg_solve (solver.cpp:41-63).  Per iteration:
+//   pap = p.ap ; alpha = rz/pap ; x += alpha p ; r -= alpha ap ; |r|^2
+//   rz' = r.z  ; p = z + (rz'/rz) p
+// Scalars stay on the device (alpha/beta are recomputed inside the kernels from the
+// fixed-order block partials), so the host only reads pap and |r|^2 once per
+// iteration for the stopping / breakdown decision.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace krr {
+
+namespace {
+
+__global__ void build_operands_kernel(const double* __restrict__ X, int64_t n, int64_t d,
+                                      int64_t n_pad, int dp, double* __restrict__ L,
+                                      double* __restrict__ R) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_pad;
+         i += warps) {
+        double* li = L + i * dp;
+        double* ri = R + i * dp;
+        if (i >= n) {
+            for (int k = lane; k < dp; k += 32) li[k] = ri[k] = 0.0;
+            continue;
+        }
+        const double* xi = X + i * d;
+        double sq = 0.0;
+        for (int64_t k = lane; k < d; k += 32) {
+            const double x = xi[k];
+            sq = fma(x, x, sq);
+            li[k] = x;
+            ri[k] = -2.0 * x;
+        }
+        sq = warp_sum(sq);
+        for (int k = int(d) + lane; k < dp; k += 32) {
+            double lv = 0.0, rv = 0.0;
+            if (k == d) {
+                lv = sq;
+                rv = 1.0;
+            } else if (k == d + 1) {
+                lv = 1.0;
+                rv = sq;
+            }
+            li[k] = lv;
+            ri[k] = rv;
+        }
+    }
+}
+
+__global__ void dot_partial_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                   int64_t n, double* __restrict__ partial) {
+    __shared__ double scr[32];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        s = fma(a[i], b[i], s);
+    s = block_sum(s, scr);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// Fixed-order sum of nb partials, executed identically by every calling block.
+__device__ __forceinline__ double sum_fixed(const double* __restrict__ part, int nb, double* scr) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s += part[i];
+    s = block_sum(s, scr);
+    __shared__ double bcast;
+    if (threadIdx.x == 0) bcast = s;
+    __syncthreads();
+    return bcast;
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int nb,
+                                    double* __restrict__ out) {
+    __shared__ double scr[32];
+    const double s = sum_fixed(partial, nb, scr);
+    if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void pcg_update_xr_kernel(const double* __restrict__ pap_part, int nb,
+                                     const double* __restrict__ rz, double* __restrict__ x,
+                                     double* __restrict__ r, const double* __restrict__ p,
+                                     const double* __restrict__ ap, int64_t n,
+                                     double* __restrict__ rr_part, double* __restrict__ scal) {
+    __shared__ double scr[32];
+    const double pap = sum_fixed(pap_part, nb, scr);
+    const double alpha = *rz / pap;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scal[0] = pap;
+        scal[1] = alpha;
+    }
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * ap[i];
+        r[i] = ri;
+        s = fma(ri, ri, s);
+    }
+    s = block_sum(s, scr);
+    if (threadIdx.x == 0) rr_part[blockIdx.x] = s;
+}
+
+__global__ void pcg_update_p_kernel(const double* __restrict__ rz_part, int nb,
+                                    const double* __restrict__ rz_old, double* __restrict__ rz_out,
+                                    double* __restrict__ p, const double* __restrict__ z,
+                                    int64_t n) {
+    __shared__ double scr[32];
+    const double rz_new = sum_fixed(rz_part, nb, scr);
+    const double beta = rz_new / *rz_old;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *rz_out = rz_new;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        p[i] = z[i] + beta * p[i];
+}
+
+__global__ void copy_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
+__global__ void gather_col_kernel(const double* __restrict__ M, int64_t n, int64_t t, int64_t c,
+                                  double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = M[i * t + c];
+}
+
+__global__ void scatter_col_kernel(const double* __restrict__ v, int64_t n, int64_t t, int64_t c,
+                                   double* __restrict__ M) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        M[i * t + c] = v[i];
+}
+
+unsigned grid_for(int64_t n) {
+    return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
+}
+
+}  // namespace
+
+void build_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, int dp,
+                           double* L, double* R, cudaStream_t stream) {
+    const unsigned blocks = unsigned(std::min<int64_t>((n_pad + 7) / 8, 148 * 16));
+    build_operands_kernel<<<blocks, 256, 0, stream>>>(X, n, d, n_pad, dp, L, R);
+    KRR_LAUNCH_CHECK();
+}
+
+int vec_blocks(int64_t n) {
+    return int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 4)));
+}
+
+void dot_partial_launch(const double* a, const double* b, int64_t n, double* partial, int nb,
+                        cudaStream_t stream) {
+    dot_partial_kernel<<<nb, kVecThreads, 0, stream>>>(a, b, n, partial);
+    KRR_LAUNCH_CHECK();
+}
+
+void sum_partials_launch(const double* partial, int nb, double* out, cudaStream_t stream) {
+    sum_partials_kernel<<<1, kVecThreads, 0, stream>>>(partial, nb, out);
+    KRR_LAUNCH_CHECK();
+}
+
+void pcg_update_xr_launch(const double* pap_part, int nb, const double* rz, double* x, double* r,
+                          const double* p, const double* ap, int64_t n, double* rr_part,
+                          double* scal, cudaStream_t stream) {
+    pcg_update_xr_kernel<<<nb, kVecThreads, 0, stream>>>(pap_part, nb, rz, x, r, p, ap, n, rr_part,
+                                                         scal);
+    KRR_LAUNCH_CHECK();
+}
+
+void pcg_update_p_launch(const double* rz_part, int nb, const double* rz_old, double* rz_out,
+                         double* p, const double* z, int64_t n, cudaStream_t stream) {
+    pcg_update_p_kernel<<<nb, kVecThreads, 0, stream>>>(rz_part, nb, rz_old, rz_out, p, z, n);
+    KRR_LAUNCH_CHECK();
+}
+
+void copy_launch(double* dst, const double* src, int64_t n, cudaStream_t stream) {
+    copy_kernel<<<grid_for(n), 256, 0, stream>>>(dst, src, n);
+    KRR_LAUNCH_CHECK();
+}
+
+void gather_col_launch(const double* M, int64_t n, int64_t t, int64_t c, double* out,
+                       cudaStream_t stream) {
+    gather_col_kernel<<<grid_for(n), 256, 0, stream>>>(M, n, t, c, out);
+    KRR_LAUNCH_CHECK();
+}
+
+void scatter_col_launch(const double* v, int64_t n, int64_t t, int64_t c, double* M,
+                        cudaStream_t stream) {
+    scatter_col_kernel<<<grid_for(n), 256, 0, stream>>>(v, n, t, c, M);
+    KRR_LAUNCH_CHECK();
+}
+
+}  // namespace krr

@@ -1,0 +1,237 @@
+"""RFF build, Woodbury preconditioner and PCG on the B200 vs the CPU oracle, plus the
+reference's own known-answer tests ported onto the device path.
+
+Reference tests mirrored (file:line under /root/reference/proj/tests):
+  test_precond.cpp:16-72, test_solver.cpp:25-147, test_sketches.cpp:13-24,195-207.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+# ----------------------------------------------------------------------------- RFF (K2)
+def test_rff_rows_match_oracle(krr, oracle, ctx):
+    n, d, s, sigma = 1000, 16, 300, 4.0
+    x = oracle.random_matrix(n, d, 4)
+    chain = krr.realize_chain(krr.ChainSpec(s1=s), krr.KernelSpec.gaussian(sigma), d, 0)
+    w, b = oracle.rff_realize(0, d, s, sigma)
+    assert np.array_equal(chain.rff.w, w) and np.array_equal(chain.rff.b, b)  # bitwise draws
+    z = chain.rff.apply_rows(x, ctx=ctx)
+    want = oracle.rff_apply_rows(x, w, b)
+    assert np.max(np.abs(z - want)) <= 1e-14
+
+
+def test_rff_chain_rows_and_determinism(krr, oracle):
+    """test_sketches.cpp:13-24 (same seed -> same output) and :195-207 (rows stack)."""
+    kernel = krr.KernelSpec.gaussian(1.1)
+    chain = krr.realize_chain(krr.ChainSpec(s1=16), kernel, 5, 99)
+    x = oracle.random_matrix(9, 5, 6)
+    z = chain.apply_rows(x)
+    assert z.shape == (9, 16)
+    again = krr.realize_chain(krr.ChainSpec(s1=16), kernel, 5, 99).apply_rows(x)
+    assert np.array_equal(z, again)
+    for i in range(9):
+        assert np.array_equal(z[i], chain.apply(x[i]))
+
+
+# ----------------------------------------------------------------------------- precond
+def test_zero_sketch_scaled_identity(krr, oracle):
+    p = krr.build_preconditioner(np.zeros((10, 3)), 0.5)
+    x = oracle.random_vector(10, 1)
+    assert np.max(np.abs(p.apply(x) - x / 0.5)) <= 1e-14
+
+
+def test_identity_sketch_halves(krr, oracle):
+    p = krr.build_preconditioner(np.eye(8), 1.0)
+    x = oracle.random_vector(8, 2)
+    assert np.max(np.abs(p.apply(x) - x / 2.0)) <= 1e-12
+
+
+def test_precond_matches_dense_inverse(krr, oracle):
+    z = oracle.random_matrix(300, 50, 7)
+    lp = 0.1
+    dense = z @ z.T + lp * np.eye(300)
+    inv = np.linalg.inv(dense)
+    p = krr.build_preconditioner(z, lp)
+    for t in range(5):
+        x = oracle.random_vector(300, 100 + t)
+        assert rel(p.apply(x), inv @ x) <= 1e-10
+
+
+def test_precond_matches_oracle_u_and_apply(krr, oracle):
+    z = oracle.random_matrix(1200, 96, 3)
+    lp = 0.05
+    u_ref, jit = oracle.build_preconditioner(z, lp)
+    p = krr.build_preconditioner(z, lp)
+    assert p.jitter_used == jit
+    assert rel(p.u, u_ref) <= 1e-11
+    x = oracle.random_matrix(1200, 3, 4)
+    assert rel(p.apply_columns(x), oracle.precond_apply(u_ref, lp, x)) <= 1e-11
+
+
+def test_woodbury_round_trips(krr, oracle):
+    for trial in range(0, 50, 7):
+        n = 100 + (trial % 4) * 100
+        s = 10 + (trial % 7) * 5
+        lp = [1e-3, 1e-1, 10.0][trial % 3]
+        z = oracle.random_matrix(n, s, 200 + trial)
+        p = krr.build_preconditioner(z, lp)
+        x = oracle.random_vector(n, 300 + trial)
+        px = p.apply(x)
+        rt = z @ (z.T @ px) + lp * px
+        assert rel(rt, x) <= 1e-8
+
+
+def test_apply_columns_equals_apply(krr, oracle):
+    z = oracle.random_matrix(60, 12, 3)
+    p = krr.build_preconditioner(z, 0.2)
+    x = oracle.random_matrix(60, 4, 4)
+    cols = p.apply_columns(x)
+    for j in range(4):
+        assert np.max(np.abs(cols[:, j] - p.apply(x[:, j]))) <= 1e-14
+
+
+def test_precond_errors(krr, oracle):
+    z = oracle.random_matrix(10, 3, 5)
+    with pytest.raises(krr.NonPositiveLambda):
+        krr.build_preconditioner(z, 0.0)
+    with pytest.raises(krr.NotPositiveDefinite):
+        krr.build_preconditioner(np.full((4, 2), 1e200), 1.0)
+
+
+# ----------------------------------------------------------------------------- PCG (generic operators)
+def mat_op(a):
+    return lambda v: a @ v
+
+
+def test_pcg_2x2_diagonal(krr):
+    a = np.diag([3.0, 2.0])
+    r = krr.pcg_solve(mat_op(a), None, np.array([3.0, 2.0]), 1e-10, 50)
+    assert r.stats.converged and r.stats.iterations <= 2
+    assert np.max(np.abs(r.solution - 1.0)) <= 1e-9
+
+
+def test_pcg_exact_inverse_one_iteration(krr, oracle):
+    m = oracle.random_matrix(20, 20, 1)
+    a = m @ m.T + np.eye(20)
+    inv = np.linalg.inv(a)
+    r = krr.pcg_solve(mat_op(a), mat_op(inv), oracle.random_vector(20, 2), 1e-10, 50)
+    assert r.stats.converged and r.stats.iterations == 1
+
+
+def test_pcg_random_spd_dense_solve(krr, oracle):
+    m = oracle.random_matrix(50, 50, 3)
+    a = m @ m.T + 5.0 * np.eye(50)
+    y = oracle.random_vector(50, 4)
+    want = np.linalg.solve(a, y)
+    r = krr.pcg_solve(mat_op(a), None, y, 1e-12, 500)
+    assert r.stats.converged
+    assert rel(r.solution, want) <= 1e-8
+    ref = oracle.pcg_solve(mat_op(a), None, y, 1e-12, 500)
+    assert abs(r.stats.iterations - ref.iterations) <= 1
+
+
+def test_pcg_zero_rhs(krr):
+    r = krr.pcg_solve(mat_op(np.eye(5)), None, np.zeros(5), 1e-8, 10)
+    assert r.stats.converged and r.stats.iterations == 0 and np.linalg.norm(r.solution) == 0.0
+
+
+def test_pcg_breakdown(krr):
+    with pytest.raises(krr.BreakdownDetected):
+        krr.pcg_solve(mat_op(-np.eye(4)), None, np.ones(4), 1e-8, 10)
+
+
+def test_pcg_invalid_args(krr):
+    with pytest.raises(ValueError):
+        krr.pcg_solve(mat_op(np.eye(3)), None, np.ones(3), 0.0, 10)
+    with pytest.raises(ValueError):
+        krr.pcg_solve(mat_op(np.eye(3)), None, np.ones(3), 1e-8, 0)
+
+
+def test_pcg_energy_norm_non_increasing(krr, oracle):
+    m = oracle.random_matrix(30, 30, 8)
+    a = m @ m.T + np.eye(30)
+    y = oracle.random_vector(30, 9)
+    exact = np.linalg.solve(a, y)
+
+    def en(c):
+        d = c - exact
+        return float(np.sqrt(max(0.0, d @ (a @ d))))
+
+    errors = [en(np.zeros(30))]
+    krr.pcg_solve(mat_op(a), None, y, 1e-12, 200, observer=lambda it, c: errors.append(en(c)))
+    for i in range(1, len(errors)):
+        assert errors[i] <= errors[i - 1] + 1e-12 * errors[0]
+
+
+# ----------------------------------------------------------------------------- train
+def test_train_single_point(krr):
+    data = krr.Dataset(np.zeros((1, 1)), np.full((1, 1), 2.0))
+    cfg = krr.SolverConfig(lambda_=1.0, tau=1e-12, chain=krr.ChainSpec(s1=1))
+    res = krr.train(data, krr.KernelSpec.gaussian(1.0), cfg)
+    assert abs(res.model.c[0, 0] - 1.0) <= 1e-12
+
+
+def test_train_regularizer_dominated(krr, oracle):
+    x = oracle.random_matrix(30, 2, 1)
+    y = oracle.random_matrix(30, 1, 2)
+    cfg = krr.SolverConfig(lambda_=1e12, tau=1e-10, chain=krr.ChainSpec(s1=4))
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(1.0), cfg)
+    assert rel(res.model.c, y / 1e12) <= 1e-6
+
+
+def test_train_matches_dense_solve_within_tau_bound(krr, oracle):
+    """test_solver.cpp:126-147."""
+    kernel = krr.KernelSpec.gaussian(1.5)
+    x = oracle.random_matrix(200, 3, 5)
+    y = oracle.random_matrix(200, 2, 6)
+    cfg = krr.SolverConfig(lambda_=0.1, tau=1e-8, chain=krr.ChainSpec(s1=64), seed=3)
+    res = krr.train(krr.Dataset(x, y), kernel, cfg)
+    assert res.report.all_converged()
+    a = oracle.gram_matrix(x, 1.5) + 0.1 * np.eye(200)
+    want = np.linalg.solve(a, y)
+    for j in range(2):
+        bound = 1e-8 * np.linalg.norm(y[:, j]) / 0.1
+        assert np.linalg.norm(res.model.c[:, j] - want[:, j]) <= 2.0 * bound
+
+
+@pytest.mark.parametrize("n,d,sigma,lam,s,tau", [
+    (500, 4, 1.0, 1e-2, 64, 1e-8),
+    (2000, 16, 4.0, 1e-3, 256, 1e-6),
+    (3000, 54, 3.0, 1e-4, 512, 1e-6),
+])
+def test_train_parity_with_oracle(krr, oracle, n, d, sigma, lam, s, tau):
+    """Same seeded inputs, same RFF draws: iterations +-1 and alpha rel-err <= 1e-8."""
+    x = oracle.random_matrix(n, d, 11)
+    y = oracle.random_matrix(n, 1, 12)
+    ref = oracle.train(x, y, sigma, lam, s, 0, tau, 500)
+    cfg = krr.SolverConfig(lambda_=lam, tau=tau, max_iter=500, chain=krr.ChainSpec(s1=s), seed=0)
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), cfg)
+    assert abs(res.report.per_rhs[0].iterations - ref.iterations[0]) <= 1
+    assert res.report.per_rhs[0].converged == ref.converged[0]
+    assert rel(res.model.c, ref.c) <= 1e-8, rel(res.model.c, ref.c)
+
+
+def test_plain_cg_parity(krr, oracle):
+    n, d, sigma, lam = 800, 5, 1.5, 1e-1
+    x = oracle.random_matrix(n, d, 21)
+    y = oracle.random_matrix(n, 1, 22)
+    ref = oracle.solve_gaussian(x, sigma, lam, None, 1.0, y, 1e-8, 500)
+    c, rep = krr.solve_regularized(x, krr.KernelSpec.gaussian(sigma), y, lam, None, 1e-8, 500)
+    assert abs(rep.per_rhs[0].iterations - ref.iterations[0]) <= 1
+    assert rel(c, ref.c) <= 1e-8
+
+
+def test_predict_scores(krr, oracle):
+    x = oracle.random_matrix(25, 3, 7)
+    y = oracle.random_matrix(25, 1, 8)
+    cfg = krr.SolverConfig(lambda_=0.5, chain=krr.ChainSpec(s1=8))
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(1.0), cfg)
+    scores = krr.predict_scores(res.model, x)
+    want = oracle.gram_matrix(x, 1.0) @ res.model.c
+    assert rel(scores, want) <= 1e-10
+    xq = oracle.random_matrix(11, 3, 9)
+    assert rel(krr.predict_scores(res.model, xq), oracle.cross_gram(xq, x, 1.0) @ res.model.c) <= 1e-12
