@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark: kernel-matvec Gevals/s at n = 1M (BASELINE.json config 4) on N B200s.
+
+One "step" = one (K + lambda I) v product over the full n = 1,048,576 x d = 90 Gaussian
+kernel (sigma = 6, lambda = 1e-6), K never stored: the fused symmetric K1 kernel, its
+finish pass, and (N > 1) the NCCL all-reduce of the result — the PCG hot loop's
+dominant operation (reference solver.cpp:75-77 over kernels.cpp:72-88).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--n N] [--time-to-tol CFG]
+
+value   = whole-job Gevals/s = n^2 * K / (max-over-ranks device time of the K steps);
+          inputs resident in HBM; X (755 MB) and the partial-sum buffer (2 GB) exceed the
+          126 MB L2, so no explicit flush between steps.
+e2e     = same metric through the reference-facing C-ABI call krr_kernel_matvec with
+          pinned HOST buffers (H2D of v and D2H of the result inside the timed region).
+roofline: dominant kernel = K1; achieved = algorithmic FP64 tensor FLOPs per launch
+          (unique pairs owned by the rank x 2d) / mean K1 launch time
+          (CUDA events on the launching stream); peak = FP64 DMMA rate measured live on
+          this GPU by krr_microbench (not in MEASURED_PEAKS.json).
+--impl reference: the CPU restatement (oracle/, all host threads) on a bounded row
+          sample of the same workload — the reference itself (CPU-only, Eigen) cannot be
+          built in this image.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG4 = dict(n=1048576, d=90, sigma=6.0, lam=1e-6, s=8192, cfg=4)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=CFG4["n"], help="override n (debug only)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--time-to-tol", type=int, default=0, metavar="CFG",
+                    help="also run the full train (RFF + precond + PCG) of BASELINE config CFG")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- plumbing
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+class Dist:
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.dist:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes | None) -> bytes:
+        if not self.dist:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/krr_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.index)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                rows.append(f)
+        try:
+            self.path.unlink()
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_baseline(x, sigma, lam, budget_s: float) -> dict:
+    """The oracle's on-the-fly mat-vec (CPU restatement, all host threads) on a bounded
+    row sample of the same workload: Gevals/s = rows * n / seconds."""
+    from oracle import oracle_ffi as oracle
+    threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
+    n = x.shape[0]
+    v = np.random.default_rng(12345).standard_normal(n)
+    rows = max(1, threads)
+    t0 = time.perf_counter()
+    oracle.kernel_matvec(x, sigma, lam, v, rows=(0, rows))
+    dt = time.perf_counter() - t0
+    rows2 = int(min(n, max(rows, rows * budget_s / max(dt, 1e-6))))
+    rows2 = max(threads, (rows2 // threads) * threads)
+    t0 = time.perf_counter()
+    oracle.kernel_matvec(x, sigma, lam, v, rows=(0, rows2))
+    dt2 = time.perf_counter() - t0
+    return {"value": rows2 * n / dt2 / 1e9, "unit": "Gevals/s", "cores": threads, "kind": "port",
+            "seconds": dt2,
+            "sample": f"rows 0..{rows2} of the n={n} (K + lambda I) v product ({rows2 * n:.3e} kernel "
+                      f"evaluations, each row over all n columns), oracle/krr_oracle.cpp on {threads} threads"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0  # the CPU reference arm runs on rank 0 only
+    import paper_1611_03220_b200 as krr  # host-only generator (no GPU work)
+    n = args.n
+    x, _ = krr.generate_config(4, n, CFG4["d"], 1, 0)
+    from oracle import oracle_ffi as oracle
+    threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
+    v = np.random.default_rng(12345).standard_normal(n)
+    # size each step to ~budget / (steps + warmup)
+    per_step = max(2.0, min(30.0, 150.0 / max(1, args.steps + args.warmup)))
+    t0 = time.perf_counter()
+    oracle.kernel_matvec(x, CFG4["sigma"], CFG4["lam"], v, rows=(0, threads))
+    dt = time.perf_counter() - t0
+    rows = max(threads, int(threads * per_step / max(dt, 1e-6)) // threads * threads)
+    rows = min(rows, n)
+    for _ in range(args.warmup):
+        oracle.kernel_matvec(x, CFG4["sigma"], CFG4["lam"], v, rows=(0, min(rows, threads)))
+    times = []
+    for k in range(args.steps):
+        r0 = (k * rows) % max(1, n - rows + 1)
+        t0 = time.perf_counter()
+        oracle.kernel_matvec(x, CFG4["sigma"], CFG4["lam"], v, rows=(r0, r0 + rows))
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = rows * n / (ms * 1e-3) / 1e9
+    sample = (f"{rows} rows x {n} columns of (K + lambda I) v per step (config 4), "
+              f"oracle/krr_oracle.cpp on {threads} threads")
+    line = {
+        "impl": "reference", "metric": "kernel-matvec Gevals/s (n=1M, fp64)", "value": value,
+        "unit": "Gevals/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 4 generator, seed 0)",
+        "config": {"workload": "config4 kernel mat-vec", "n": n, "d": CFG4["d"], "sigma": CFG4["sigma"],
+                   "lambda": CFG4["lam"], "rows_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": "Gevals/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "Gevals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (CPU-only C++/Eigen) is unbuildable here (Eigen3 absent); this arm "
+                "times its restatement oracle/krr_oracle.cpp with the same per-entry formula",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    world, rank, local = dist_env()
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    D = Dist(world, rank)
+    import paper_1611_03220_b200 as krr
+    from paper_1611_03220_b200 import _lib
+
+    nccl_id = krr.nccl_unique_id() if (world > 1 and rank == 0) else None
+    nccl_id = D.bcast_bytes(nccl_id)
+    ctx = krr.Context(local, rank, world, nccl_id)
+    n, d, sigma, lam = args.n, CFG4["d"], CFG4["sigma"], CFG4["lam"]
+    x, _ = krr.generate_config(4, n, d, 1, 0)
+    _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, sigma))
+
+    mb = np.zeros(8)
+    _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(mb)))
+    peak_dmma = float(mb[0])
+
+    tot, k1 = C.c_double(), C.c_double()
+    if args.warmup > 0:
+        _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, lam, args.warmup, C.byref(tot), C.byref(k1)))
+    D.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launches
+    _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, lam, args.steps, C.byref(tot), C.byref(k1)))
+    launches = ctx.launches - launches0
+    clk = clocks.stop()
+    D.barrier()
+    total_ms = D.max(tot.value)
+    k1_ms = k1.value
+
+    # ---- e2e through the reference-facing C-ABI call with pinned host buffers
+    import torch
+    hv = torch.from_numpy(np.random.default_rng(7).standard_normal(n)).pin_memory()
+    ho = torch.empty(n, dtype=torch.float64).pin_memory()
+    _lib.check(_lib.LIB.krr_kernel_matvec(ctx.handle, lam, hv.data_ptr(), 1, ho.data_ptr()))  # warm
+    D.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _lib.check(_lib.LIB.krr_kernel_matvec(ctx.handle, lam, hv.data_ptr(), 1, ho.data_ptr()))
+    e2e_s = D.max(time.perf_counter() - t0)
+
+    # ---- optional time-to-tolerance (full train on the device)
+    ttt = None
+    if args.time_to_tol:
+        ttt = time_to_tol(krr, ctx, args.time_to_tol)
+
+    # ---- roofline bookkeeping
+    st, ns, tiles = krr.schedule(n, world, rank)
+    pairs_rank = 0
+    for a, b in tiles:
+        ra = min(st, max(0, n - a * st))
+        rb = min(st, max(0, n - b * st))
+        pairs_rank += ra * (ra - 1) // 2 if a == b else ra * rb
+    flops = pairs_rank * 2.0 * d
+    achieved = flops / (k1_ms * 1e-3) / 1e12
+    dp = (d + 2 + 3) // 4 * 4
+    pipe_ops = pairs_rank * 2.0 * (dp + 12)  # DMMA MACs (dp) + 10 exp + 2 accumulate FP64 ops
+    traffic = None
+    tf = ROOT / "profiles" / "k1_ncu_summary.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(x, sigma, lam, args.cpu_seconds)
+
+    steps = args.steps
+    value = float(n) * n * steps / (total_ms * 1e-3) / 1e9
+    line = {
+        "metric": "kernel-matvec Gevals/s (n=1M, fp64)",
+        "value": value,
+        "unit": "Gevals/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE config 4 generator: AR(1) features rho=0.5, standardised, seed 0)",
+        "config": {"workload": "config4 (K + lambda I) v, K on the fly", "n": n, "d": d, "sigma": sigma,
+                   "lambda": lam, "parallelism": f"row/tile-sharded x{world} + NCCL all-reduce",
+                   "l2": "no flush: X (755 MB) and partials (2 GB) exceed the 126 MB L2",
+                   "kernel_evals_per_step": float(n) * n, "unique_pairs_per_step": n * (n - 1) / 2},
+        "e2e": {"value": float(n) * n * steps / e2e_s / 1e9, "unit": "Gevals/s",
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
+                     "frac": achieved / peak_dmma, "traffic": traffic,
+                     "kernel": "gauss_matvec_kernel (K1)",
+                     "flops_per_launch": flops, "k1_ms": k1_ms,
+                     "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU "
+                                    "(krr_microbench; MEASURED_PEAKS.json has no FP64 entry)",
+                     "fp64_pipe": {"ops_per_pair": dp + 12, "achieved_tflops_equiv":
+                                   pipe_ops / (k1_ms * 1e-3) / 1e12,
+                                   "frac": pipe_ops / (k1_ms * 1e-3) / 1e12 / peak_dmma}},
+        "microbench": {"dmma_tflops": mb[0], "dfma_tflops": mb[1], "dmma_dfma_mixed_tflops": mb[2],
+                       "exp_libdevice_gevals": mb[3], "exp_table_gevals": mb[4]},
+        "clocks": clk,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if ttt:
+        line["time_to_tol"] = ttt
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    D.close()
+    return 0
+
+
+def time_to_tol(krr, ctx, cfg: int) -> dict:
+    n, d, t, sigma, lam, s = krr.CONFIGS[cfg]
+    x, y = krr.generate_config(cfg, n, d, t, 0)
+    sc = krr.SolverConfig(tau=1e-6, max_iter=500, lambda_=lam, chain=krr.ChainSpec(s1=s), seed=0)
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), sc, ctx=ctx)
+    st = res.report.per_rhs
+    return {"config": cfg, "n": n, "d": d, "s": s, "t": t, "phase_ms": res.report.phase_ms,
+            "iterations": [r.iterations for r in st], "converged": [r.converged for r in st],
+            "final_residual": [r.final_residual for r in st], "wall_s": res.report.wall_time_sec}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

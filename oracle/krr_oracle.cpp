@@ -70,25 +70,72 @@ std::uint64_t stage_seed(std::uint64_t master, int stage) {
     return master + std::uint64_t(stage + 1) * kStageSeedStride;
 }
 
+// Summation orders (the `order` argument of every exported function):
+//   0  forward sequential sums everywhere;
+//   1  reverse sequential sums everywhere (the self-consistency floor partner of 0);
+//   2  "Eigen-like": what Eigen 3.x emits for the reference's calls in a default
+//      x86-64 build (SSE2 packets of 2 doubles, no FMA) — vector reductions
+//      (dot, squaredNorm) use two packet accumulators = 4 interleaved partial sums
+//      combined as (s0+s2)+(s1+s3); row-major GEMV rows use one packet accumulator =
+//      even/odd partial sums; GEMM inner products (X X^T, Z^T Z) stay sequential.
+
+// Vector reduction sum_i a[i] b[i]  (Eigen: redux over cwiseProduct)
 double dot(const double* a, const double* b, std::int64_t n, int order) {
     double s = 0.0;
     if (order == 0) {
         for (std::int64_t i = 0; i < n; ++i) s += a[i] * b[i];
-    } else {
+    } else if (order == 1) {
         for (std::int64_t i = n - 1; i >= 0; --i) s += a[i] * b[i];
+    } else {
+        double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+        std::int64_t i = 0;
+        for (; i + 4 <= n; i += 4) {
+            p0 += a[i] * b[i];
+            p1 += a[i + 1] * b[i + 1];
+            q0 += a[i + 2] * b[i + 2];
+            q1 += a[i + 3] * b[i + 3];
+        }
+        if (i + 2 <= n) {
+            p0 += a[i] * b[i];
+            p1 += a[i + 1] * b[i + 1];
+            i += 2;
+        }
+        s = (p0 + q0) + (p1 + q1);
+        for (; i < n; ++i) s += a[i] * b[i];
     }
     return s;
 }
 
+// Inner product of a GEMM (sequential over k in every order but 1).
+double gemm_dot(const double* a, const double* b, std::int64_t n, int order) {
+    return dot(a, b, n, order == 2 ? 0 : order);
+}
+
+// One row of a row-major GEMV (stride sa on the matrix row, sb on the vector).
 double dot_strided(const double* a, std::int64_t sa, const double* b, std::int64_t sb,
                    std::int64_t n, int order) {
     double s = 0.0;
     if (order == 0) {
         for (std::int64_t i = 0; i < n; ++i) s += a[i * sa] * b[i * sb];
-    } else {
+    } else if (order == 1) {
         for (std::int64_t i = n - 1; i >= 0; --i) s += a[i * sa] * b[i * sb];
+    } else {
+        double e = 0.0, o = 0.0;
+        std::int64_t i = 0;
+        for (; i + 2 <= n; i += 2) {
+            e += a[i * sa] * b[i * sb];
+            o += a[(i + 1) * sa] * b[(i + 1) * sb];
+        }
+        s = e + o;
+        for (; i < n; ++i) s += a[i * sa] * b[i * sb];
     }
     return s;
+}
+
+// Column-major GEMV / TRSM-style accumulation: sequential over k.
+double colmajor_dot(const double* a, std::int64_t sa, const double* b, std::int64_t sb,
+                    std::int64_t n, int order) {
+    return dot_strided(a, sa, b, sb, n, order == 2 ? 0 : order);
 }
 
 // One Gaussian kernel entry, kernels.cpp:79-84 (pair ordered a < b as in the
@@ -97,7 +144,7 @@ inline double gauss_entry(const double* x, std::int64_t d, const double* sq, std
                           std::int64_t j, double scale, int order) {
     if (i == j) return 1.0;  // kernels.cpp:81
     const std::int64_t a = std::min(i, j), b = std::max(i, j);
-    const double p = dot(x + a * d, x + b * d, d, order);
+    const double p = gemm_dot(x + a * d, x + b * d, d, order);
     const double d2 = std::max(0.0, sq[a] + sq[b] - 2.0 * p);
     return std::exp(-d2 * scale);
 }
@@ -194,7 +241,7 @@ int oracle_rff_apply_rows(const double* x, std::int64_t n, std::int64_t d, const
 #pragma omp parallel for schedule(static)
     for (std::int64_t i = 0; i < n; ++i)
         for (std::int64_t k = 0; k < s; ++k)
-            z[i * s + k] = scale * std::cos(dot(w + k * d, x + i * d, d, order) + b[k]);
+            z[i * s + k] = scale * std::cos(dot_strided(w + k * d, 1, x + i * d, 1, d, order) + b[k]);
     return OK;
 }
 
@@ -226,7 +273,7 @@ int oracle_cross_gram(const double* a, std::int64_t m, const double* b, std::int
 #pragma omp parallel for schedule(static)
     for (std::int64_t i = 0; i < m; ++i)
         for (std::int64_t j = 0; j < n; ++j) {
-            const double p = dot(a + i * d, b + j * d, d, order);
+            const double p = gemm_dot(a + i * d, b + j * d, d, order);
             k[i * n + j] = std::exp(-std::max(0.0, sqa[std::size_t(i)] + sqb[std::size_t(j)] - 2.0 * p) * scale);
         }
     return OK;
@@ -335,7 +382,7 @@ int oracle_build_preconditioner(const double* z, std::int64_t n, std::int64_t s,
 #pragma omp parallel for schedule(dynamic, 8)
     for (std::int64_t a = 0; a < s; ++a)
         for (std::int64_t b = 0; b <= a; ++b) {
-            const double v = dot_strided(z + a, s, z + b, s, n, order);
+            const double v = colmajor_dot(z + a, s, z + b, s, n, order);
             g[std::size_t(a * s + b)] = v;
             g[std::size_t(b * s + a)] = v;
         }
@@ -382,7 +429,7 @@ int oracle_precond_apply(const double* u, std::int64_t s, std::int64_t n, double
 #pragma omp parallel for schedule(static)
     for (std::int64_t i = 0; i < n; ++i)
         for (std::int64_t c = 0; c < t; ++c) {
-            const double utw = dot_strided(u + i, n, w.data() + c, t, s, order);
+            const double utw = colmajor_dot(u + i, n, w.data() + c, t, s, order);
             out[i * t + c] = (xin[i * t + c] - utw) / lambda_p;
         }
     return OK;

@@ -1,5 +1,9 @@
 """ctypes binding of oracle/liboracle.so — the CPU restatement of the reference path.
 
+`order` selects the summation order (krr_oracle.cpp): 2 = Eigen-like (the default,
+closest to the reference's SSE2/Eigen arithmetic), 0 = forward sequential,
+1 = reverse sequential.
+
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
 CPU-baseline legs (cpu_baseline and --impl reference), never by the product package.
 Every function cites the reference code it restates (see krr_oracle.cpp's header).
@@ -15,6 +19,8 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "liboracle.so"
+
+DEFAULT_ORDER = 2
 
 OK, DIMENSION_MISMATCH, NOT_POSITIVE_DEFINITE, SINGULAR_TRIANGULAR, BREAKDOWN, \
     NON_POSITIVE_LAMBDA, INVALID_ARGUMENT = range(7)
@@ -120,7 +126,7 @@ def rff_realize(master_seed: int, d: int, s: int, sigma: float):
     return w, b
 
 
-def rff_apply_rows(x, w, b, order: int = 0) -> np.ndarray:
+def rff_apply_rows(x, w, b, order: int = DEFAULT_ORDER) -> np.ndarray:
     x, w, b = f64(x), f64(w), f64(b)
     z = np.empty((x.shape[0], w.shape[0]))
     _chk(lib().oracle_rff_apply_rows(_p(x), x.shape[0], x.shape[1], _p(w), _p(b), w.shape[0], _p(z),
@@ -128,14 +134,14 @@ def rff_apply_rows(x, w, b, order: int = 0) -> np.ndarray:
     return z
 
 
-def gram_matrix(x, sigma: float, order: int = 0) -> np.ndarray:
+def gram_matrix(x, sigma: float, order: int = DEFAULT_ORDER) -> np.ndarray:
     x = f64(x)
     k = np.empty((x.shape[0], x.shape[0]))
     _chk(lib().oracle_gram_matrix(_p(x), x.shape[0], x.shape[1], sigma, _p(k), order), "gram")
     return k
 
 
-def cross_gram(a, b, sigma: float, order: int = 0) -> np.ndarray:
+def cross_gram(a, b, sigma: float, order: int = DEFAULT_ORDER) -> np.ndarray:
     a, b = f64(a), f64(b)
     k = np.empty((a.shape[0], b.shape[0]))
     _chk(lib().oracle_cross_gram(_p(a), a.shape[0], _p(b), b.shape[0], a.shape[1], sigma, _p(k), order),
@@ -143,7 +149,7 @@ def cross_gram(a, b, sigma: float, order: int = 0) -> np.ndarray:
     return k
 
 
-def kernel_matvec(x, sigma: float, lam: float, v, rows=None, order: int = 0) -> np.ndarray:
+def kernel_matvec(x, sigma: float, lam: float, v, rows=None, order: int = DEFAULT_ORDER) -> np.ndarray:
     """((K + lam I) V)[rows] with K on the fly (V n or n x t)."""
     x = f64(x)
     v = f64(v)
@@ -174,7 +180,7 @@ def triangular_solve(l, b, side: str = "left", transpose: bool = False) -> np.nd
     return out
 
 
-def build_preconditioner(z, lambda_p: float, order: int = 0):
+def build_preconditioner(z, lambda_p: float, order: int = DEFAULT_ORDER):
     """Returns (U s x n, jitter_used)."""
     z = f64(z)
     n, s = z.shape
@@ -185,7 +191,7 @@ def build_preconditioner(z, lambda_p: float, order: int = 0):
     return u, bool(jit.value)
 
 
-def precond_apply(u, lambda_p: float, x, order: int = 0) -> np.ndarray:
+def precond_apply(u, lambda_p: float, x, order: int = DEFAULT_ORDER) -> np.ndarray:
     u, x = f64(u), f64(x)
     vec = x.ndim == 1
     x2 = x[:, None] if vec else x
@@ -204,7 +210,7 @@ class PcgOut:
     residual_history: list = field(default_factory=list)
 
 
-def pcg_solve(apply_a, apply_m, y, tau: float, max_iter: int, observer=None, order: int = 0) -> PcgOut:
+def pcg_solve(apply_a, apply_m, y, tau: float, max_iter: int, observer=None, order: int = DEFAULT_ORDER) -> PcgOut:
     """solver.cpp:22-67 with Python operators."""
     y = f64(y)
     n = y.shape[0]
@@ -249,7 +255,7 @@ class SolveOut:
     total_matvecs: int
 
 
-def solve_gaussian(x, sigma, lam, u, lambda_p, y, tau, max_iter, dense_k=True, order=0) -> SolveOut:
+def solve_gaussian(x, sigma, lam, u, lambda_p, y, tau, max_iter, dense_k=True, order=DEFAULT_ORDER) -> SolveOut:
     x, y = f64(x), f64(y)
     y2 = y[:, None] if y.ndim == 1 else y
     n, t = y2.shape
@@ -267,7 +273,7 @@ def solve_gaussian(x, sigma, lam, u, lambda_p, y, tau, max_iter, dense_k=True, o
     return SolveOut(c, its.tolist(), [bool(v) for v in cvs], frs.tolist(), hist, int(tot.value))
 
 
-def train(x, y, sigma, lam, s, seed, tau, max_iter, lambda_p=None, dense_k=True, order=0) -> SolveOut:
+def train(x, y, sigma, lam, s, seed, tau, max_iter, lambda_p=None, dense_k=True, order=DEFAULT_ORDER) -> SolveOut:
     """solver.cpp:96-133, non-adaptive RFF chain."""
     x, y = f64(x), f64(y)
     y2 = y[:, None] if y.ndim == 1 else y

@@ -61,6 +61,12 @@ void scatter_col_launch(const double* v, int64_t n, int64_t t, int64_t c, double
                         cudaStream_t stream);
 
 // ---------------------------------------------------------------- RFF (K2)
+// Wp (s_pad x dp) = W (s x d) zero-padded.
+void rff_pad_w_launch(const double* W, int64_t s, int64_t d, int64_t s_pad, int dp, double* Wp,
+                      cudaStream_t stream);
+// Z (rows x s, row-major) = sqrt(2/s) cos(L[rows] Wp^T + b), L the K1 operand (dp columns).
+void rff_features_launch(const double* L, const double* Wp, const double* b, double* Z, int64_t rows,
+                         int64_t s, int dp, cudaStream_t stream);
 // Z[i][k] = sqrt(2/s) * cos(Z[i][k] + b[k]), in place, Z n x s row-major.
 void rff_cos_launch(double* Z, int64_t n, int64_t s, const double* b, cudaStream_t stream);
 

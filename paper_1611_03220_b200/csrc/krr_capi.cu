@@ -96,7 +96,7 @@ struct Ctx {
     bool has_sketch = false, has_pre = false;
     int64_t pn = 0, s = 0, z0 = 0, z1 = 0;
     double lambda_p = 1.0;
-    DevMem<double> Z, G, Gcopy, W, Wpart, work, brff, wrff, chk;
+    DevMem<double> Z, G, Gcopy, W, Wpart, work, brff, wrff, wpad, chk;
     DevMem<int> info;
 
     int nb = 1;  // vector reduction blocks
@@ -208,15 +208,11 @@ void rff_build(Ctx& c, const double* W, const double* b, int64_t s) {
     KRR_CUDA(cudaMemcpyAsync(c.brff.get(), b, sizeof(double) * size_t(s), cudaMemcpyHostToDevice,
                              c.stream));
     const int64_t rows = c.z1 - c.z0;
-    if (rows > 0) {
-        // Z (rows x s, row-major) = X[z0:z1] W^T  <=>  col-major Z^T (s x rows) = W (X)^T
-        const double one = 1.0, zero = 0.0;
-        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, int(s), int(rows), int(c.d), &one,
-                                 c.wrff.get(), int(c.d), c.X.get() + c.z0 * c.d, int(c.d), &zero,
-                                 c.Z.get(), int(s)),
-                     "cublasDgemm(X W^T)");
-        rff_cos_launch(c.Z.get(), rows, s, c.brff.get(), c.stream);
-    }
+    const int64_t s_pad = (s + 127) / 128 * 128;
+    c.wpad.ensure(size_t(s_pad * c.plan.dp));
+    rff_pad_w_launch(c.wrff.get(), s, c.d, s_pad, c.plan.dp, c.wpad.get(), c.stream);
+    rff_features_launch(c.L.get() + c.z0 * c.plan.dp, c.wpad.get(), c.brff.get(), c.Z.get(), rows, s,
+                        c.plan.dp, c.stream);
     c.sync();
     c.has_sketch = true;
 }
