@@ -34,6 +34,7 @@ import time
 from pathlib import Path
 
 import numpy as np
+import torch  # noqa: F401  (import before the CUDA library so torch's NCCL is the one loaded)
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))

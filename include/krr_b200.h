@@ -73,6 +73,11 @@ int krr_ctx_destroy(krr_ctx* ctx);
 /* Number of kernels this context launched so far (bench.py's gpu_launches claim). */
 int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
 
+/* Tuning / diagnostic knobs (no reference equivalent):
+ *   "k1_resident" 1|0  keep the column tile of the fused mat-vec in shared memory (default 1)
+ *   "exp_mode"    1|0  table exp (default) | libdevice exp in the Gaussian epilogue */
+int krr_set_option(krr_ctx* ctx, const char* key, double value);
+
 /* ---------------------------------------------------------------- data + kernel operator */
 /* Uploads X (n x d, row-major) to the device (replicated on every rank) and
  * precomputes the row norms.  Replaces the data half of gram_matrix

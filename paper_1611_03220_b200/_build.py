@@ -31,9 +31,8 @@ NVCC_FLAGS = ARCH + [
 ]
 LINK_LIBS = [
     "-L", str(CUDA_HOME / "lib64"), "-lcublas", "-lcusolver", "-lcudart",
-    "-L", "/usr/lib/x86_64-linux-gnu", "-lnccl",
+    "-ldl",
     "-Xlinker", "-rpath," + str(CUDA_HOME / "lib64"),
-    "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu",
 ]
 
 

@@ -109,6 +109,7 @@ _SIGS = {
     "krr_ctx_create_dist": [_i, _i, _i, _vp, C.POINTER(_vp)],
     "krr_ctx_destroy": [_vp],
     "krr_ctx_launch_count": [_vp, C.POINTER(_i64)],
+    "krr_set_option": [_vp, C.c_char_p, _d],
     "krr_set_data": [_vp, _vp, _i64, _i64, _d],
     "krr_kernel_matvec": [_vp, _d, _vp, _i64, _vp],
     "krr_kernel_matvec_device": [_vp, _d, _vp, _i64, _vp],
@@ -211,6 +212,9 @@ class Context:
 
     def __exit__(self, *exc):
         self.close()
+
+    def set_option(self, key: str, value: float) -> None:
+        check(LIB.krr_set_option(self.handle, key.encode(), float(value)))
 
     @property
     def launches(self) -> int:

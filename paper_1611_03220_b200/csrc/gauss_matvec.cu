@@ -40,9 +40,18 @@ namespace {
 constexpr int BM = 128;           // tile edge (rows and cols)
 constexpr int KC = 16;            // k-chunk (doubles)
 constexpr int KS = 20;            // smem row stride (doubles), 20 = 4 mod 16
-constexpr int NSTAGE = 3;
 constexpr int NTHREADS = 256;
-constexpr int STAGE_DOUBLES = 2 * BM * KS;  // L chunk + R chunk
+constexpr int MAX_SMEM = 227 * 1024;
+
+// Two pipeline shapes:
+//  streaming (RES = false): each stage holds a k-chunk of both L_I and R_J (3 stages);
+//  resident  (RES = true):  R_J (128 x dp) stays in shared memory for the whole I sweep
+//                           and only L_I chunks stream (4 stages) — half the copy work.
+template <bool RES>
+struct Shape {
+    static constexpr int NSTAGE = RES ? 4 : 3;
+    static constexpr int STAGE_DOUBLES = (RES ? 1 : 2) * BM * KS;
+};
 
 struct MatvecArgs {
     const double* __restrict__ L;
@@ -54,17 +63,22 @@ struct MatvecArgs {
     int64_t n_pad;
     int dp;
     int st;
+    int ksr;  // resident R_J row stride (doubles), = 4 or 12 mod 16
     ExpConsts ec;
 };
 
-template <int EXPMODE>
+template <int EXPMODE, bool RES>
 __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecArgs A) {
+    constexpr int NSTAGE = Shape<RES>::NSTAGE;
+    constexpr int STAGE_DOUBLES = Shape<RES>::STAGE_DOUBLES;
     extern __shared__ __align__(16) double smem[];
-    double* stages = smem;                                  // NSTAGE * STAGE_DOUBLES
-    double* rowacc = smem + NSTAGE * STAGE_DOUBLES;         // st
+    double* rres = smem;                                    // RES: BM * ksr
+    double* stages = smem + (RES ? BM * A.ksr : 0);          // NSTAGE * STAGE_DOUBLES
+    double* rowacc = stages + NSTAGE * STAGE_DOUBLES;       // st
     double* scr_row = rowacc + A.st;                        // 4 x 128
     double* scr_col = scr_row + 4 * BM;                     // 2 x 128
     double* tab = scr_col + 2 * BM;                         // 64
+    double* vjs = tab + 64;                                 // 128: v of the current J tile
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -94,9 +108,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
         const double* gL = A.L + (rowBase + int64_t(p_it) * BM) * A.dp + k0;
         const double* gR = A.R + (colBase + int64_t(p_jt) * BM) * A.dp + k0;
 #pragma unroll
-        for (int q = 0; q < (2 * BM * (KC / 2)) / NTHREADS; ++q) {
+        for (int q = 0; q < ((RES ? 1 : 2) * BM * (KC / 2)) / NTHREADS; ++q) {
             const int idx = tid + q * NTHREADS;
-            const int op = idx / (BM * (KC / 2));
+            const int op = RES ? 0 : idx / (BM * (KC / 2));
             const int rem = idx % (BM * (KC / 2));
             const int row = rem / (KC / 2), pc = rem % (KC / 2);
             if (pc < pieces) {
@@ -132,11 +146,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
     int cs = 0;  // consumer stage index
     for (int jt = 0; jt < nT; ++jt) {
         const int64_t J0 = colBase + int64_t(jt) * BM;
-        double vj[4][2];
-#pragma unroll
-        for (int ns = 0; ns < 4; ++ns)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) vj[ns][h] = A.v[J0 + wn * 32 + ns * 8 + 2 * t4 + h];
+        if constexpr (RES) {
+            // R_J for the whole I sweep: drain the pipeline, load, publish.
+            __syncthreads();
+            const int pieces = A.dp >> 1;
+            const double* gR = A.R + J0 * A.dp;
+            for (int idx = tid; idx < BM * pieces; idx += NTHREADS) {
+                const int row = idx / pieces, pc = idx % pieces;
+                cp_async16(rres + row * A.ksr + pc * 2, gR + int64_t(row) * A.dp + pc * 2);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncthreads();
+        }
+        if (!RES) __syncthreads();  // previous J's epilogue is done with vjs
+        if (tid < BM) vjs[tid] = A.v[J0 + tid];
+        // published by the first mainloop barrier of this J
         double colacc[4][2];
 #pragma unroll
         for (int ns = 0; ns < 4; ++ns) colacc[ns][0] = colacc[ns][1] = 0.0;
@@ -144,10 +169,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
         const int itEnd = diag ? jt : nT - 1;
         for (int it = 0; it <= itEnd; ++it) {
             const int64_t I0 = rowBase + int64_t(it) * BM;
-            double vi[8];
-#pragma unroll
-            for (int ms = 0; ms < 8; ++ms) vi[ms] = A.v[I0 + wm * 64 + ms * 8 + g];
-
             double acc[8][4][2];
 #pragma unroll
             for (int ms = 0; ms < 8; ++ms)
@@ -165,10 +186,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
                 ++ps;
 
                 const double* sL = stages + (cs % NSTAGE) * STAGE_DOUBLES;
-                const double* sR = sL + BM * KS;
                 const int nks = (min(KC, A.dp - kc * KC)) >> 2;
                 const double* aBase = sL + (wm * 64 + g) * KS + t4;
-                const double* bBase = sR + (wn * 32 + g) * KS + t4;
+                const int bstride = RES ? A.ksr : KS;
+                const double* bBase = RES ? rres + (wn * 32 + g) * A.ksr + t4 + kc * KC
+                                          : sL + BM * KS + (wn * 32 + g) * KS + t4;
 #pragma unroll
                 for (int ks = 0; ks < KC / 4; ++ks) {
                     if (ks < nks) {
@@ -176,7 +198,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
 #pragma unroll
                         for (int ms = 0; ms < 8; ++ms) af[ms] = aBase[ms * 8 * KS + ks * 4];
 #pragma unroll
-                        for (int ns = 0; ns < 4; ++ns) bf[ns] = bBase[ns * 8 * KS + ks * 4];
+                        for (int ns = 0; ns < 4; ++ns) bf[ns] = bBase[ns * 8 * bstride + ks * 4];
 #pragma unroll
                         for (int ms = 0; ms < 8; ++ms)
 #pragma unroll
@@ -188,6 +210,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
 
             // ---- epilogue: exp, row sums, column sums
             const bool dtile = diag && (it == jt);
+            double vi[8];
+#pragma unroll
+            for (int ms = 0; ms < 8; ++ms) vi[ms] = A.v[I0 + wm * 64 + ms * 8 + g];
+            double vj[4][2];
+#pragma unroll
+            for (int ns = 0; ns < 4; ++ns) {
+                const double2 p2 = *reinterpret_cast<const double2*>(vjs + wn * 32 + ns * 8 + 2 * t4);
+                vj[ns][0] = p2.x;
+                vj[ns][1] = p2.y;
+            }
             double rowp[8];
 #pragma unroll
             for (int ms = 0; ms < 8; ++ms) {
@@ -271,11 +303,32 @@ __global__ void matvec_finish_kernel(const double* __restrict__ part, int ns_cou
     }
 }
 
+int resident_stride(int dp) {
+    int k = dp;
+    while (k % 16 != 4 && k % 16 != 12) k += 4;
+    return k;
+}
+
+template <bool RES>
+size_t smem_bytes(int st, int dp) {
+    return sizeof(double) * (size_t(RES ? BM * resident_stride(dp) : 0) +
+                             size_t(Shape<RES>::NSTAGE) * Shape<RES>::STAGE_DOUBLES + st + 4 * BM +
+                             2 * BM + 64 + BM);
+}
+
+template <int EXPMODE, bool RES>
+void launch_variant(const MatvecArgs& a, int64_t ntiles, cudaStream_t stream) {
+    const size_t smem = smem_bytes<RES>(a.st, a.dp);
+    KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_kernel<EXPMODE, RES>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    gauss_matvec_kernel<EXPMODE, RES><<<unsigned(ntiles), NTHREADS, smem, stream>>>(a);
+}
+
 }  // namespace
 
-size_t gauss_matvec_smem_bytes(int st) {
-    return sizeof(double) * (size_t(NSTAGE) * STAGE_DOUBLES + st + 4 * BM + 2 * BM + 64);
-}
+size_t gauss_matvec_smem_bytes(int st) { return smem_bytes<false>(st, 0); }
+
+bool gauss_matvec_resident_ok(int st, int dp) { return smem_bytes<true>(st, dp) <= size_t(MAX_SMEM); }
 
 void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part, int exp_mode,
                          cudaStream_t stream) {
@@ -290,16 +343,13 @@ void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part
     a.n_pad = p.n_pad;
     a.dp = p.dp;
     a.st = p.st;
+    a.ksr = resident_stride(p.dp);
     a.ec = p.ec;
-    const size_t smem = gauss_matvec_smem_bytes(p.st);
+    const bool res = p.resident && gauss_matvec_resident_ok(p.st, p.dp);
     if (exp_mode == 0) {
-        KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_kernel<0>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        gauss_matvec_kernel<0><<<unsigned(p.num_tiles), NTHREADS, smem, stream>>>(a);
+        res ? launch_variant<0, true>(a, p.num_tiles, stream) : launch_variant<0, false>(a, p.num_tiles, stream);
     } else {
-        KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_kernel<1>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        gauss_matvec_kernel<1><<<unsigned(p.num_tiles), NTHREADS, smem, stream>>>(a);
+        res ? launch_variant<1, true>(a, p.num_tiles, stream) : launch_variant<1, false>(a, p.num_tiles, stream);
     }
     KRR_LAUNCH_CHECK();
 }

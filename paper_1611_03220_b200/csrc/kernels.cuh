@@ -20,9 +20,11 @@ struct GaussMatvecPlan {
     const double* exp_tab = nullptr; // 64 doubles
     int64_t n = 0, n_pad = 0;
     int dp = 0, st = 0, ns = 0;
+    bool resident = true;            // keep R_J in shared memory when it fits
     ExpConsts ec{};
 };
 size_t gauss_matvec_smem_bytes(int st);
+bool gauss_matvec_resident_ok(int st, int dp);
 void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part, int exp_mode,
                          cudaStream_t stream);
 void matvec_finish_launch(const GaussMatvecPlan& p, const double* part, const double* v,

@@ -3,6 +3,7 @@
 // reference interface each entry point replaces.
 #include <cublas_v2.h>
 #include <cusolverDn.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <chrono>
@@ -32,9 +33,40 @@ void cusolver_check(cusolverStatus_t st, const char* what) {
     if (st != CUSOLVER_STATUS_SUCCESS)
         fail(KRR_ERR_CUDA, std::string(what) + ": cuSOLVER status " + std::to_string(int(st)));
 }
+// NCCL is resolved lazily with dlopen("libnccl.so.2") and only when world > 1, so a
+// single-GPU process never loads it and a process that already loaded an NCCL (e.g.
+// torch's bundled one) shares that copy instead of mixing two versions.
+struct NcclApi {
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(h, "ncclAllReduce"));
+        a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+        return a;
+    }();
+    if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
+        fail(KRR_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    return api;
+}
+
 void nccl_check(ncclResult_t st, const char* what) {
     if (st != ncclSuccess)
-        fail(KRR_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(st));
+        fail(KRR_ERR_NCCL, std::string(what) + ": " +
+                               (nccl().getErrorString ? nccl().getErrorString(st) : "nccl error"));
 }
 
 template <class T>
@@ -77,6 +109,7 @@ struct Ctx {
     cusolverDnHandle_t sol = nullptr;
     ncclComm_t comm = nullptr;
     int exp_mode = 1;
+    bool k1_resident = true;
 
     // data
     bool has_data = false;
@@ -113,7 +146,7 @@ void require_data(const Ctx& c) {
 
 void allreduce_sum(Ctx& c, double* buf, int64_t count) {
     if (c.world <= 1) return;
-    nccl_check(ncclAllReduce(buf, buf, size_t(count), ncclDouble, ncclSum, c.comm, c.stream),
+    nccl_check(nccl().allReduce(buf, buf, size_t(count), ncclDouble, ncclSum, c.comm, c.stream),
                "ncclAllReduce");
 }
 
@@ -182,6 +215,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
     p.st = int(c.sched.st);
     p.ns = int(c.sched.ns);
     p.ec = make_exp_consts(c.scale);
+    p.resident = c.k1_resident;
     c.sync();
     c.has_data = true;
 }
@@ -540,7 +574,7 @@ int krr_ctx_create(int device, krr_ctx** out) {
 int krr_nccl_unique_id(void* out_128_bytes) {
     return guard([&] {
         ncclUniqueId id;
-        krr::nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        krr::nccl_check(krr::nccl().getUniqueId(&id), "ncclGetUniqueId");
         static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
         std::memcpy(out_128_bytes, &id, sizeof(id));
     });
@@ -561,7 +595,7 @@ int krr_ctx_create_dist(int device, int rank, int world, const void* nccl_id, kr
         if (world > 1) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
-            krr::nccl_check(ncclCommInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
+            krr::nccl_check(krr::nccl().commInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
         }
         *out = reinterpret_cast<krr_ctx*>(c.release());
     });
@@ -573,7 +607,7 @@ int krr_ctx_destroy(krr_ctx* ctx) {
         Ctx* c = krr::as_ctx(ctx);
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
-        if (c->comm) ncclCommDestroy(c->comm);
+        if (c->comm) krr::nccl().commDestroy(c->comm);
         if (c->sol) cusolverDnDestroy(c->sol);
         if (c->blas) cublasDestroy(c->blas);
         cudaStream_t st = c->stream;
@@ -586,6 +620,21 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out) {
     return guard([&] {
         (void)krr::as_ctx(ctx);
         *out = krr::g_launches.load();
+    });
+}
+
+int krr_set_option(krr_ctx* ctx, const char* key, double value) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        const std::string k = key ? key : "";
+        if (k == "k1_resident") {
+            c.k1_resident = value != 0.0;
+            c.plan.resident = c.k1_resident;
+        } else if (k == "exp_mode") {
+            c.exp_mode = value != 0.0 ? 1 : 0;
+        } else {
+            fail(KRR_ERR_INVALID_ARGUMENT, "unknown option '" + k + "'");
+        }
     });
 }
 

@@ -128,3 +128,26 @@ def test_device_matvec_entry_and_launch_count(krr, oracle, ctx):
     _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 0.1, 3, C.byref(tot), C.byref(k1)))
     assert ctx.launches - before == 3 * 2  # K1 + finish per mat-vec
     assert tot.value > 0 and 0 < k1.value <= tot.value
+
+
+@pytest.mark.parametrize("n,d", [(1000, 16), (3000, 90), (700, 54)])
+def test_resident_and_streaming_variants_bitwise_equal(krr, oracle, ctx, n, d):
+    """The two K1 pipeline shapes do the same arithmetic in the same order."""
+    x = oracle.random_matrix(n, d, 31)
+    v = oracle.random_vector(n, 32)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(5.0), 1e-4, ctx=ctx)
+    a = op(v)
+    ctx.set_option("k1_resident", 0)
+    b = op(v)
+    ctx.set_option("exp_mode", 0)
+    c = op(v)
+    ctx.set_option("k1_resident", 1)
+    ctx.set_option("exp_mode", 1)
+    assert np.array_equal(a, b)
+    assert rel(c, a) <= 1e-14
+    assert np.array_equal(op(v), a)  # deterministic run to run
+
+
+def test_set_option_rejects_unknown(krr, ctx):
+    with pytest.raises(ValueError):
+        ctx.set_option("no_such_knob", 1)
