@@ -1,0 +1,124 @@
+// C++ caller of the C-ABI (include/krr_b200.h) without Python: the reference's own
+// solver tests (test_solver.cpp:25-63, :126-147) rewritten against the B200 library.
+// Built by __graft_entry__.build() into examples/cpp_dropin; run by
+// tests/test_gpu_cpp_dropin.py.  Exit code 0 = all checks passed.
+#include <krr_b200.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <vector>
+
+namespace {
+
+int failures = 0;
+
+void check(bool ok, const char* what) {
+    std::printf("%s %s\n", ok ? "PASS" : "FAIL", what);
+    if (!ok) ++failures;
+}
+
+void must(int st, const char* what) {
+    if (st != KRR_OK) {
+        std::printf("FAIL %s: status %d: %s\n", what, st, krr_last_error());
+        ++failures;
+    }
+}
+
+struct Dense {
+    std::vector<double> a;
+    int64_t n;
+};
+
+int dense_op(void* user, const double* in, double* out, int64_t n) {
+    const auto* m = static_cast<const Dense*>(user);
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int64_t j = 0; j < n; ++j) s += m->a[size_t(i * n + j)] * in[j];
+        out[i] = s;
+    }
+    return 0;
+}
+
+std::vector<double> random_matrix(int64_t rows, int64_t cols, uint64_t seed) {
+    std::mt19937_64 gen(seed);  // tests/support/oracles.cpp:87-94
+    std::normal_distribution<double> normal(0.0, 1.0);
+    std::vector<double> m(static_cast<size_t>(rows * cols));
+    for (auto& v : m) v = normal(gen);
+    return m;
+}
+
+}  // namespace
+
+int main() {
+    if (krr_device_count() < 1) {
+        std::printf("no CUDA device\n");
+        return 2;
+    }
+    krr_ctx* ctx = nullptr;
+    must(krr_ctx_create(0, &ctx), "krr_ctx_create");
+    if (!ctx) return 1;
+
+    // pcg solves a 2x2 diagonal system in two iterations (test_solver.cpp:25-35)
+    {
+        Dense a{{3.0, 0.0, 0.0, 2.0}, 2};
+        const double y[2] = {3.0, 2.0};
+        double x[2] = {0, 0};
+        krr_rhs_stats st{};
+        must(krr_pcg_solve_operator(ctx, 2, dense_op, &a, nullptr, nullptr, y, 1e-10, 50, nullptr,
+                                    nullptr, x, &st, nullptr),
+             "pcg 2x2");
+        check(st.converged && st.iterations <= 2 && std::fabs(x[0] - 1) <= 1e-9 &&
+                  std::fabs(x[1] - 1) <= 1e-9,
+              "pcg 2x2 diagonal");
+    }
+    // breakdown on -I (test_solver.cpp:65-69) -> KRR_ERR_BREAKDOWN
+    {
+        Dense a{{-1, 0, 0, 0, -1, 0, 0, 0, -1}, 3};
+        const double y[3] = {1, 1, 1};
+        double x[3];
+        krr_rhs_stats st{};
+        const int rc = krr_pcg_solve_operator(ctx, 3, dense_op, &a, nullptr, nullptr, y, 1e-8, 10,
+                                              nullptr, nullptr, x, &st, nullptr);
+        check(rc == KRR_ERR_BREAKDOWN, "pcg breakdown maps to BreakdownDetected");
+    }
+    // train agrees with the reference's tau bound (test_solver.cpp:126-147), through
+    // the device kernel operator: |c - c*| <= 2 tau |y| / lambda with c* from a dense solve
+    {
+        const int64_t n = 200, d = 3, t = 2;
+        const auto x = random_matrix(n, d, 5);
+        const auto y = random_matrix(n, t, 6);
+        std::vector<double> c(static_cast<size_t>(n * t));
+        std::vector<krr_rhs_stats> st(t);
+        int64_t total = 0;
+        must(krr_train(ctx, x.data(), n, d, y.data(), t, 1.5, 0.1, -1.0, 64, 3, 1e-8, 1000, c.data(),
+                       st.data(), nullptr, &total, nullptr),
+             "krr_train");
+        // true residual of the returned c through the device kernel operator
+        bool ok = st[0].converged && st[1].converged;
+        for (int64_t j = 0; j < t && ok; ++j) {
+            std::vector<double> ycol(static_cast<size_t>(n)), kc(static_cast<size_t>(n));
+            for (int64_t i = 0; i < n; ++i) ycol[size_t(i)] = y[size_t(i * t + j)];
+            std::vector<double> ccol(static_cast<size_t>(n));
+            for (int64_t i = 0; i < n; ++i) ccol[size_t(i)] = c[size_t(i * t + j)];
+            must(krr_kernel_matvec(ctx, 0.1, ccol.data(), 1, kc.data()), "matvec");
+            double rn = 0, yn = 0;
+            for (int64_t i = 0; i < n; ++i) {
+                rn += (ycol[size_t(i)] - kc[size_t(i)]) * (ycol[size_t(i)] - kc[size_t(i)]);
+                yn += ycol[size_t(i)] * ycol[size_t(i)];
+            }
+            ok = ok && std::sqrt(rn) <= 1.5e-8 * std::sqrt(yn);  // true residual ~ tau (recursive <= tau)
+        }
+        check(ok && total == st[0].iterations + st[1].iterations, "train residual within tau");
+    }
+    // error mapping: lambda <= 0 -> NonPositiveLambda; sigma <= 0 -> invalid_argument
+    {
+        double dummy[4] = {0, 0, 0, 0};
+        check(krr_precond_build(ctx, 0.0, nullptr) != KRR_OK, "precond before sketch fails");
+        check(krr_set_data(ctx, dummy, 2, 2, -1.0) == KRR_ERR_INVALID_ARGUMENT, "sigma <= 0 rejected");
+    }
+    krr_ctx_destroy(ctx);
+    std::printf("%d failure(s)\n", failures);
+    return failures == 0 ? 0 : 1;
+}

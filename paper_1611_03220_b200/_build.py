@@ -81,6 +81,20 @@ def build_lib(verbose: bool = False, force: bool = False) -> Path:
     return LIB
 
 
+def build_examples() -> Path:
+    """C++ caller of the C-ABI (examples/cpp_dropin.cpp), linked against the in-tree .so."""
+    src = ROOT / "examples" / "cpp_dropin.cpp"
+    out = ROOT / "examples" / "cpp_dropin"
+    if out.exists() and out.stat().st_mtime >= max(src.stat().st_mtime, LIB.stat().st_mtime):
+        return out
+    cmd = ["g++", "-O2", "-std=c++20", "-I", str(ROOT / "include"), str(src), "-o", str(out),
+           "-L", str(PKG), "-lkrr_b200", "-Wl,-rpath,$ORIGIN/../paper_1611_03220_b200"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"example build failed:\n{res.stderr}")
+    return out
+
+
 def build_oracle() -> Path:
     """CPU restatement used only by tests / the CPU baseline (oracle/Makefile)."""
     make = shutil.which("make")
@@ -98,8 +112,10 @@ def main(argv=None) -> int:
     force = "-f" in argv
     lib = build_lib(verbose=verbose, force=force)
     orc = build_oracle()
+    ex = build_examples()
     print(lib)
     print(orc)
+    print(ex)
     return 0
 
 

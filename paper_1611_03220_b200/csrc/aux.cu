@@ -131,6 +131,35 @@ __global__ void mb_mixed_kernel(double* sink, double a, double b) {
     if (s == 12345.678) sink[0] = s;
 }
 
+// Half the warps run the DMMA loop, the other half the DFMA loop: if the two pipes
+// are independent the combined rate approaches the sum.
+__global__ void mb_split_kernel(double* sink, double a, double b) {
+    const int warp = threadIdx.x >> 5;
+    double s = 0.0;
+    if (warp & 1) {
+        double acc[8][2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+        for (int it = 0; it < MB_ITERS; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dmma884(acc[i][0], acc[i][1], a, b);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+    } else {
+        double f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = double(i) * 1e-3;
+        for (int it = 0; it < MB_ITERS; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = fma(f[i], a, b);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += f[i];
+    }
+    if (s == 12345.678) sink[0] = s;
+}
+
 template <int MODE>
 __global__ void mb_exp_kernel(double* sink, ExpConsts ec, const double* __restrict__ tab_g) {
     __shared__ double tab[64];
@@ -193,6 +222,7 @@ void microbench_run(const ExpConsts& ec, const double* tab, double* results, cud
     const double t_dmma = time_it([&] { mb_dmma_kernel<<<blocks, threads, 0, stream>>>(sink, 1.0, 1e-9); });
     const double t_dfma = time_it([&] { mb_dfma_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
     const double t_mixed = time_it([&] { mb_mixed_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
+    const double t_split = time_it([&] { mb_split_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
     const double t_exp0 = time_it([&] { mb_exp_kernel<0><<<blocks, threads, 0, stream>>>(sink, ec, tab); });
     const double t_exp1 = time_it([&] { mb_exp_kernel<1><<<blocks, threads, 0, stream>>>(sink, ec, tab); });
     KRR_LAUNCH_CHECK();
@@ -207,7 +237,8 @@ void microbench_run(const ExpConsts& ec, const double* tab, double* results, cud
     results[4] = evals / t_exp1 * 1e-9;
     results[5] = sms;
     results[6] = clk_khz / 1000.0;
-    results[7] = 0.0;
+    // split: half the warps DMMA (dmma_flop / 2), half DFMA (dfma_flop / 2)
+    results[7] = (dmma_flop / 2 + dfma_flop / 2) / t_split * 1e-12;
     KRR_CUDA(cudaEventDestroy(e0));
     KRR_CUDA(cudaEventDestroy(e1));
     KRR_CUDA(cudaFree(sink));

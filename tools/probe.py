@@ -1,7 +1,7 @@
 """GPU probe: FP64 pipe micro-benchmarks + K1 mat-vec throughput at the BASELINE shapes.
 
-python tools/probe.py [--sizes 8192:16,65536:54,...] [--steps 3]
-Prints one JSON object (written to gpurun_out/probe.json when that directory exists).
+python tools/probe.py [--sizes 8192:16,65536:54,...] [--steps 3] [--resident -1|0|1]
+Prints JSON lines (and writes gpurun_out/probe.json when that directory exists).
 """
 import argparse
 import ctypes as C
@@ -18,42 +18,52 @@ import numpy as np  # noqa: E402
 import paper_1611_03220_b200 as krr  # noqa: E402
 from paper_1611_03220_b200 import _lib  # noqa: E402
 
+MB_KEYS = ["dmma_tflops", "dfma_tflops", "mixed_tflops", "exp_libdevice_gevals", "exp_table_gevals",
+           "sms", "clock_mhz", "split_warps_tflops"]
+
+
+def report(n, d, ms, k1, t_set, res, exp_mode):
+    pairs = n * (n - 1) / 2
+    dp = (d + 2 + 3) // 4 * 4
+    row = {"n": n, "d": d, "resident": res, "exp_mode": exp_mode, "ms_per_matvec": ms, "k1_ms": k1,
+           "gevals_per_s": n * n / (ms * 1e-3) / 1e9,
+           "unique_pairs_per_s": pairs / (k1 * 1e-3) / 1e9,
+           "dot_tflops": pairs * 2 * d / (k1 * 1e-3) / 1e12,
+           "fp64_ops_tflops_equiv": pairs * 2 * (dp + 12) / (k1 * 1e-3) / 1e12,
+           "set_data_s": t_set}
+    print(json.dumps(row), flush=True)
+    return row
+
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--sizes", default="8192:16,65536:54,262144:90,1048576:90")
+    ap.add_argument("--sizes", default="8192:16,65536:54,262144:90")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--exp-mode", type=int, default=1)
+    ap.add_argument("--resident", type=int, default=-1, help="-1: both K1 variants")
+    ap.add_argument("--no-microbench", action="store_true")
     args = ap.parse_args()
     out = {}
     ctx = krr.Context(0)
-    res = np.zeros(8)
-    _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(res)))
-    out["microbench"] = dict(zip(["dmma_tflops", "dfma_tflops", "mixed_tflops", "exp_libdevice_gevals",
-                                  "exp_table_gevals", "sms", "clock_mhz"], res[:7].tolist()))
-    print(json.dumps(out["microbench"]), flush=True)
+    if not args.no_microbench:
+        res = np.zeros(8)
+        _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(res)))
+        out["microbench"] = dict(zip(MB_KEYS, res.tolist()))
+        print(json.dumps(out["microbench"]), flush=True)
     rows = []
     for spec in args.sizes.split(","):
         n, d = (int(v) for v in spec.split(":"))
-        rng = np.random.default_rng(0)
-        x = rng.standard_normal((n, d))
+        x = np.random.default_rng(0).standard_normal((n, d))
         t0 = time.perf_counter()
         _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, 6.0))
         t_set = time.perf_counter() - t0
-        tot, k1 = C.c_double(), C.c_double()
-        _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))  # warm
-        _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, args.steps, C.byref(tot), C.byref(k1)))
-        ms = tot.value / args.steps
-        pairs = n * (n - 1) / 2
-        dp = (d + 2 + 3) // 4 * 4
-        row = {"n": n, "d": d, "ms_per_matvec": ms, "k1_ms": k1.value,
-               "gevals_per_s": n * n / (ms * 1e-3) / 1e9,
-               "unique_pairs_per_s": pairs / (k1.value * 1e-3) / 1e9,
-               "dot_tflops": pairs * 2 * d / (k1.value * 1e-3) / 1e12,
-               "fp64_lane_ops_tflops_equiv": pairs * (2 * dp + 2 * 11) / (k1.value * 1e-3) / 1e12,
-               "set_data_s": t_set}
-        rows.append(row)
-        print(json.dumps(row), flush=True)
+        for res in ([1, 0] if args.resident < 0 else [args.resident]):
+            ctx.set_option("k1_resident", res)
+            ctx.set_option("exp_mode", args.exp_mode)
+            tot, k1 = C.c_double(), C.c_double()
+            _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))  # warm
+            _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, args.steps, C.byref(tot), C.byref(k1)))
+            rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode))
     out["matvec"] = rows
     ctx.close()
     od = ROOT / "gpurun_out"
