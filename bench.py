@@ -235,7 +235,7 @@ def main():
     x, _ = krr.generate_config(4, n, d, 1, 0)
     _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, sigma))
 
-    mb = np.zeros(8)
+    mb = np.zeros(9)
     _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(mb)))
     peak_dmma = float(mb[0])
 

@@ -201,7 +201,8 @@ int krr_bench_matvec(krr_ctx* ctx, double lambda, int steps, double* total_ms, d
 /* Micro-benchmarks run on the context's device: FP64 DMMA and DFMA issue rates,
  * and the Gaussian-epilogue throughput (results in the 8-double array:
  * [dmma_tflops, dfma_tflops, dmma+dfma concurrent tflops, exp_libdevice_geval,
- *  exp_table_geval, sm_count, clock_mhz, split-warps dmma|dfma tflops]). */
+ *  exp_table_geval, sm_count, clock_mhz, split-warps dmma|dfma tflops,
+ *  legacy mma.sync int8 tops]). */
 int krr_microbench(krr_ctx* ctx, double* results);
 /* Evaluate the device Gaussian epilogue exp(-max(0,d2)*scale) for n host values
  * (mode 0 = libdevice exp, 1 = table exp used by the mat-vec) — accuracy tests. */

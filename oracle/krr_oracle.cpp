@@ -378,14 +378,26 @@ int oracle_triangular_solve(const double* l, std::int64_t s, const double* bmat,
 int oracle_build_preconditioner(const double* z, std::int64_t n, std::int64_t s, double lambda_p,
                                 double* u, int* jitter_used, int order) {
     if (!(lambda_p > 0.0)) return NON_POSITIVE_LAMBDA;
-    std::vector<double> g(static_cast<std::size_t>(s * s));
-#pragma omp parallel for schedule(dynamic, 8)
-    for (std::int64_t a = 0; a < s; ++a)
-        for (std::int64_t b = 0; b <= a; ++b) {
-            const double v = colmajor_dot(z + a, s, z + b, s, n, order);
-            g[std::size_t(a * s + b)] = v;
-            g[std::size_t(b * s + a)] = v;
+    // G = Z^T Z (precond.cpp:23): G[a][b] = sum_i z[i][a] z[i][b], summed over i in
+    // increasing order (decreasing for order 1) — the same arithmetic as a column dot
+    // product, blocked over a so that every row of Z streams once per block.
+    std::vector<double> g(static_cast<std::size_t>(s * s), 0.0);
+    constexpr std::int64_t AB = 32;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (std::int64_t a0 = 0; a0 < s; a0 += AB) {
+        const std::int64_t a1 = std::min(s, a0 + AB);
+        for (std::int64_t ii = 0; ii < n; ++ii) {
+            const std::int64_t i = order == 1 ? n - 1 - ii : ii;
+            const double* zi = z + i * s;
+            for (std::int64_t a = a0; a < a1; ++a) {
+                const double za = zi[a];
+                double* ga = g.data() + a * s;
+                for (std::int64_t b = 0; b <= a; ++b) ga[b] += za * zi[b];
+            }
         }
+    }
+    for (std::int64_t a = 0; a < s; ++a)
+        for (std::int64_t b = 0; b < a; ++b) g[std::size_t(b * s + a)] = g[std::size_t(a * s + b)];
     for (std::int64_t a = 0; a < s; ++a) g[std::size_t(a * s + a)] += lambda_p;
 
     std::vector<double> l = g;
@@ -402,17 +414,24 @@ int oracle_build_preconditioner(const double* z, std::int64_t n, std::int64_t s,
     if (st != OK) return st;
     for (std::int64_t i = 0; i < s; ++i)
         if (std::abs(l[std::size_t(i * s + i)]) < 1e-300) return SINGULAR_TRIANGULAR;
-    // U = L^-1 Z^T: forward substitution, one column (data point) at a time.
-#pragma omp parallel for schedule(static)
-    for (std::int64_t c = 0; c < n; ++c) {
-        for (std::int64_t i = 0; i < s; ++i) {
-            double v = z[c * s + i];
-            if (order == 0) {
-                for (std::int64_t k = 0; k < i; ++k) v -= l[std::size_t(i * s + k)] * u[k * n + c];
-            } else {
-                for (std::int64_t k = i - 1; k >= 0; --k) v -= l[std::size_t(i * s + k)] * u[k * n + c];
+    // U = L^-1 Z^T (precond.cpp:38): forward substitution, one column (data point) at a
+    // time; inner sums over k ascending (descending for order 1).
+#pragma omp parallel
+    {
+        std::vector<double> uc(static_cast<std::size_t>(s));
+#pragma omp for schedule(static)
+        for (std::int64_t c = 0; c < n; ++c) {
+            for (std::int64_t i = 0; i < s; ++i) {
+                double v = z[c * s + i];
+                const double* li = l.data() + i * s;
+                if (order != 1) {
+                    for (std::int64_t k = 0; k < i; ++k) v -= li[k] * uc[std::size_t(k)];
+                } else {
+                    for (std::int64_t k = i - 1; k >= 0; --k) v -= li[k] * uc[std::size_t(k)];
+                }
+                uc[std::size_t(i)] = v / li[i];
             }
-            u[i * n + c] = v / l[std::size_t(i * s + i)];
+            for (std::int64_t i = 0; i < s; ++i) u[i * n + c] = uc[std::size_t(i)];
         }
     }
     return OK;

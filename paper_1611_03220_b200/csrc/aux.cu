@@ -160,6 +160,25 @@ __global__ void mb_split_kernel(double* sink, double a, double b) {
     if (s == 12345.678) sink[0] = s;
 }
 
+// Legacy warp-level integer MMA (IMMA m16n8k32 s8 x s8 -> s32): 8 independent accumulators.
+__global__ void mb_imma_kernel(int* sink, int a, int b) {
+    int acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0;
+    for (int it = 0; it < MB_ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%0,%1,%2,%3};\n"
+                : "+r"(acc[i][0]), "+r"(acc[i][1]), "+r"(acc[i][2]), "+r"(acc[i][3])
+                : "r"(a), "r"(a), "r"(a), "r"(a), "r"(b), "r"(b));
+    }
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1] + acc[i][2] + acc[i][3];
+    if (s == 12345) sink[0] = s;
+}
+
 template <int MODE>
 __global__ void mb_exp_kernel(double* sink, ExpConsts ec, const double* __restrict__ tab_g) {
     __shared__ double tab[64];
@@ -223,6 +242,7 @@ void microbench_run(const ExpConsts& ec, const double* tab, double* results, cud
     const double t_dfma = time_it([&] { mb_dfma_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
     const double t_mixed = time_it([&] { mb_mixed_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
     const double t_split = time_it([&] { mb_split_kernel<<<blocks, threads, 0, stream>>>(sink, 0.999, 1e-9); });
+    const double t_imma = time_it([&] { mb_imma_kernel<<<blocks, threads, 0, stream>>>(reinterpret_cast<int*>(sink), 0x01010101, 0x01010101); });
     const double t_exp0 = time_it([&] { mb_exp_kernel<0><<<blocks, threads, 0, stream>>>(sink, ec, tab); });
     const double t_exp1 = time_it([&] { mb_exp_kernel<1><<<blocks, threads, 0, stream>>>(sink, ec, tab); });
     KRR_LAUNCH_CHECK();
@@ -239,6 +259,8 @@ void microbench_run(const ExpConsts& ec, const double* tab, double* results, cud
     results[6] = clk_khz / 1000.0;
     // split: half the warps DMMA (dmma_flop / 2), half DFMA (dfma_flop / 2)
     results[7] = (dmma_flop / 2 + dfma_flop / 2) / t_split * 1e-12;
+    // legacy IMMA: 16 x 8 x 32 MACs per instruction per warp, 2 ops per MAC
+    results[8] = warps * MB_ITERS * 8 * (16.0 * 8 * 32 * 2) / t_imma * 1e-12;
     KRR_CUDA(cudaEventDestroy(e0));
     KRR_CUDA(cudaEventDestroy(e1));
     KRR_CUDA(cudaFree(sink));

@@ -26,9 +26,18 @@
 //
 // Mainloop: 256 threads = 8 warps as 2 (M) x 4 (N), warp tile 64 x 32 =
 // 8 x 4 DMMA.8x8x4 accumulators (64 doubles per thread).  Operands stream through a
-// 3-stage cp.async pipeline in k-chunks of 16 doubles (smem row stride 20 doubles
-// => conflict-free fragment loads); the pipeline runs across tile boundaries so
-// the epilogue of tile q overlaps the loads of tile q+1.
+// cp.async pipeline in k-chunks of 16 doubles (smem row stride 20 doubles =>
+// conflict-free fragment loads); the pipeline runs across tile boundaries.
+//
+// Three pipeline shapes (same arithmetic, bitwise-identical results):
+//   streaming  both L_I and R_J chunks stream (3 stages) — small super-tiles;
+//   resident   R_J stays in shared memory for the whole I sweep, L_I streams;
+//   grouped    (default for super-tiles >= 1024 rows) resident R_J and two decoupled,
+//              phase-offset warp groups, each streaming its own half of L_I behind
+//              its own named barrier.  Measured on B200: DMMA and DFMA share ONE FP64
+//              datapath (split-warp microbenchmark: 37.0 TFLOP/s combined = DMMA
+//              alone), so the only way to fill the latency-bound exp epilogue's idle
+//              pipe cycles is another warp's DMMAs on the same SM sub-partition.
 #include "common.cuh"
 #include "gauss_exp.cuh"
 #include "kernels.cuh"
@@ -40,8 +49,18 @@ namespace {
 constexpr int BM = 128;           // tile edge (rows and cols)
 constexpr int KC = 16;            // k-chunk (doubles)
 constexpr int KS = 20;            // smem row stride (doubles), 20 = 4 mod 16
-constexpr int NTHREADS = 256;
 constexpr int MAX_SMEM = 227 * 1024;
+constexpr int WGN = 4;            // warps along the tile's columns (warp tile 32 columns)
+
+// Warp layout: MS m8-subtiles per warp (warp tile 8*MS x 32), WGM = 16/MS warps along
+// the rows.  MS = 8: 8 warps, 64 accumulator doubles per thread (255 registers, 2 warps
+// per SM sub-partition).  MS = 4: 16 warps, 32 accumulator doubles (<= 128 registers,
+// 4 warps per sub-partition for latency hiding).
+template <int MS>
+struct Warps {
+    static constexpr int WGM = 16 / MS;
+    static constexpr int NT = 32 * WGM * WGN;
+};
 
 // Two pipeline shapes:
 //  streaming (RES = false): each stage holds a k-chunk of both L_I and R_J (3 stages);
@@ -67,8 +86,46 @@ struct MatvecArgs {
     ExpConsts ec;
 };
 
-template <int EXPMODE, bool RES>
-__global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecArgs A) {
+// Epilogue of one warp tile: e = exp(-max(0, d2) scale) for the warp's MS x 4 DMMA
+// accumulator blocks, then row partials rowp[ms] (over the warp's 32 columns, this
+// thread's 8 of them) and column partials colacc (accumulated across the I sweep).
+// On a diagonal tile only the strictly upper pairs (j > i) count.
+template <int EXPMODE, int MS>
+__device__ __forceinline__ void tile_epilogue(double (&acc)[MS][4][2], const double (&vi)[MS],
+                                              const double (&vj)[4][2], double (&colacc)[4][2],
+                                              double (&rowp)[MS], bool dtile, int il0, int jl0, int g,
+                                              int t4, const ExpConsts& ec, const double* tab) {
+#pragma unroll
+    for (int ms = 0; ms < MS; ++ms) {
+        rowp[ms] = 0.0;
+        const int il = il0 + ms * 8 + g;
+#pragma unroll
+        for (int ns = 0; ns < 4; ++ns)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double e = gauss_exp<EXPMODE>(acc[ms][ns][h], ec, tab);
+                if (dtile) {
+                    const int jl = jl0 + ns * 8 + 2 * t4 + h;
+                    e = (jl > il) ? e : 0.0;
+                }
+                rowp[ms] = fma(e, vj[ns][h], rowp[ms]);
+                colacc[ns][h] = fma(e, vi[ms], colacc[ns][h]);
+            }
+    }
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int EXPMODE, bool RES, int MS>
+__global__ void __launch_bounds__(Warps<MS>::NT, 1) gauss_matvec_kernel(const MatvecArgs A) {
+    constexpr int WGM = Warps<MS>::WGM;
+    constexpr int NTHREADS = Warps<MS>::NT;
+    constexpr int WM = 8 * MS;
     constexpr int NSTAGE = Shape<RES>::NSTAGE;
     constexpr int STAGE_DOUBLES = Shape<RES>::STAGE_DOUBLES;
     extern __shared__ __align__(16) double smem[];
@@ -76,13 +133,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
     double* stages = smem + (RES ? BM * A.ksr : 0);          // NSTAGE * STAGE_DOUBLES
     double* rowacc = stages + NSTAGE * STAGE_DOUBLES;       // st
     double* scr_row = rowacc + A.st;                        // 4 x 128
-    double* scr_col = scr_row + 4 * BM;                     // 2 x 128
-    double* tab = scr_col + 2 * BM;                         // 64
+    double* scr_col = scr_row + WGN * BM;                   // WGM x 128
+    double* tab = scr_col + WGM * BM;                       // 64
     double* vjs = tab + 64;                                 // 128: v of the current J tile
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = warp % WGM, wn = warp / WGM;
     const int g = lane >> 2, t4 = lane & 3;
 
     const int2 tile = A.tiles[blockIdx.x];
@@ -169,9 +226,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
         const int itEnd = diag ? jt : nT - 1;
         for (int it = 0; it <= itEnd; ++it) {
             const int64_t I0 = rowBase + int64_t(it) * BM;
-            double acc[8][4][2];
+            double acc[MS][4][2];
 #pragma unroll
-            for (int ms = 0; ms < 8; ++ms)
+            for (int ms = 0; ms < MS; ++ms)
 #pragma unroll
                 for (int ns = 0; ns < 4; ++ns) acc[ms][ns][0] = acc[ms][ns][1] = 0.0;
 
@@ -187,20 +244,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
 
                 const double* sL = stages + (cs % NSTAGE) * STAGE_DOUBLES;
                 const int nks = (min(KC, A.dp - kc * KC)) >> 2;
-                const double* aBase = sL + (wm * 64 + g) * KS + t4;
+                const double* aBase = sL + (wm * WM + g) * KS + t4;
                 const int bstride = RES ? A.ksr : KS;
                 const double* bBase = RES ? rres + (wn * 32 + g) * A.ksr + t4 + kc * KC
                                           : sL + BM * KS + (wn * 32 + g) * KS + t4;
 #pragma unroll
                 for (int ks = 0; ks < KC / 4; ++ks) {
                     if (ks < nks) {
-                        double af[8], bf[4];
+                        double af[MS], bf[4];
 #pragma unroll
-                        for (int ms = 0; ms < 8; ++ms) af[ms] = aBase[ms * 8 * KS + ks * 4];
+                        for (int ms = 0; ms < MS; ++ms) af[ms] = aBase[ms * 8 * KS + ks * 4];
 #pragma unroll
                         for (int ns = 0; ns < 4; ++ns) bf[ns] = bBase[ns * 8 * bstride + ks * 4];
 #pragma unroll
-                        for (int ms = 0; ms < 8; ++ms)
+                        for (int ms = 0; ms < MS; ++ms)
 #pragma unroll
                             for (int ns = 0; ns < 4; ++ns)
                                 dmma884(acc[ms][ns][0], acc[ms][ns][1], af[ms], bf[ns]);
@@ -210,9 +267,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
 
             // ---- epilogue: exp, row sums, column sums
             const bool dtile = diag && (it == jt);
-            double vi[8];
+            double vi[MS];
 #pragma unroll
-            for (int ms = 0; ms < 8; ++ms) vi[ms] = A.v[I0 + wm * 64 + ms * 8 + g];
+            for (int ms = 0; ms < MS; ++ms) vi[ms] = A.v[I0 + wm * WM + ms * 8 + g];
             double vj[4][2];
 #pragma unroll
             for (int ns = 0; ns < 4; ++ns) {
@@ -220,30 +277,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
                 vj[ns][0] = p2.x;
                 vj[ns][1] = p2.y;
             }
-            double rowp[8];
+            double rowp[MS];
+            tile_epilogue<EXPMODE, MS>(acc, vi, vj, colacc, rowp, dtile, wm * WM, wn * 32, g, t4, A.ec, tab);
 #pragma unroll
-            for (int ms = 0; ms < 8; ++ms) {
-                rowp[ms] = 0.0;
-                const int il = wm * 64 + ms * 8 + g;
-#pragma unroll
-                for (int ns = 0; ns < 4; ++ns)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        double e = gauss_exp<EXPMODE>(acc[ms][ns][h], A.ec, tab);
-                        if (dtile) {
-                            const int jl = wn * 32 + ns * 8 + 2 * t4 + h;
-                            e = (jl > il) ? e : 0.0;
-                        }
-                        rowp[ms] = fma(e, vj[ns][h], rowp[ms]);
-                        colacc[ns][h] = fma(e, vi[ms], colacc[ns][h]);
-                    }
-            }
-#pragma unroll
-            for (int ms = 0; ms < 8; ++ms) {
+            for (int ms = 0; ms < MS; ++ms) {
                 double r = rowp[ms];
                 r += __shfl_xor_sync(0xffffffffu, r, 1);
                 r += __shfl_xor_sync(0xffffffffu, r, 2);
-                if (t4 == 0) scr_row[wn * BM + wm * 64 + ms * 8 + g] = r;
+                if (t4 == 0) scr_row[wn * BM + wm * WM + ms * 8 + g] = r;
             }
             __syncthreads();
             if (tid < BM) {
@@ -266,7 +307,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
             }
         __syncthreads();
         if (tid < BM) {
-            const double c = scr_col[tid] + scr_col[BM + tid];
+            double c = scr_col[tid];
+#pragma unroll
+            for (int w = 1; w < WGM; ++w) c += scr_col[w * BM + tid];
             if (diag) {
                 rowacc[jt * BM + tid] += c;
             } else {
@@ -278,6 +321,200 @@ __global__ void __launch_bounds__(NTHREADS, 1) gauss_matvec_kernel(const MatvecA
     __syncthreads();
     double* dst = A.part + int64_t(sb) * A.n_pad + rowBase;
     for (int i = tid; i < A.st; i += NTHREADS) dst[i] = rowacc[i];
+}
+
+// ---------------------------------------------------------------------------------
+// v3: two decoupled warp groups.  Group gr (= warp / 4) owns rows [64 gr, 64 gr + 64)
+// of every 128-row I tile, warp wn (= warp % 4) columns [32 wn, 32 wn + 32) of the
+// J tile, so warps w and w + 4 share an SM sub-partition.  Each group streams its own
+// half of L through its own 4-stage cp.async pipeline and synchronises with a named
+// barrier of 128 threads; R_J is resident and shared (CTA-wide barrier only at J
+// boundaries).  Group 1 starts every J sweep half a mainloop behind group 0, so the
+// latency-bound exp epilogue of one group overlaps the DMMA mainloop of the other —
+// DMMA and DFMA share one FP64 datapath, and this fills its idle epilogue cycles.
+// Arithmetic (per element and per reduction) is identical to the 8-warp kernel.
+template <int EXPMODE>
+__global__ void __launch_bounds__(256, 1) gauss_matvec_grouped_kernel(const MatvecArgs A) {
+    constexpr int MS = 8, WM = 64, GT = 128, NSTG = 4;
+    constexpr int GSTAGE = WM * KS;
+    extern __shared__ __align__(16) double smem[];
+    double* rres = smem;                                  // BM * ksr
+    double* gst = rres + BM * A.ksr;                      // 2 groups x NSTG x GSTAGE
+    double* rowacc = gst + 2 * NSTG * GSTAGE;             // st
+    double* scr_row = rowacc + A.st;                      // 2 groups x 4 x WM
+    double* scr_col = scr_row + 2 * 4 * WM;               // 2 x BM
+    double* tab = scr_col + 2 * BM;                       // 64
+    double* vjs = tab + 64;                               // BM
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gr = warp >> 2, wn = warp & 3;
+    const int gtid = tid & (GT - 1);
+    const int g = lane >> 2, t4 = lane & 3;
+    const int bar_id = 1 + gr;
+
+    const int2 tile = A.tiles[blockIdx.x];
+    const int sa = tile.x, sb = tile.y;
+    const bool diag = (sa == sb);
+    const int nT = A.st / BM;
+    const int64_t rowBase = int64_t(sa) * A.st;
+    const int64_t colBase = int64_t(sb) * A.st;
+    const int nk = (A.dp + KC - 1) / KC;
+    const int ntiles = diag ? nT * (nT + 1) / 2 : nT * nT;
+    const int total = ntiles * nk;
+    const int sig_kc = (nk - 1) / 2;  // group 0 releases group 1 after this chunk
+
+    for (int i = tid; i < A.st; i += 256) rowacc[i] = 0.0;
+    if (EXPMODE == 1 && tid < 64) tab[tid] = A.exp_tab[tid];
+
+    double* mystages = gst + gr * NSTG * GSTAGE;
+    int p_it = 0, p_jt = 0, p_kc = 0;
+    auto issue = [&](int slot) {
+        double* sL = mystages + slot * GSTAGE;
+        const int k0 = p_kc * KC;
+        const int pieces = min(KC, A.dp - k0) >> 1;
+        const double* gL = A.L + (rowBase + int64_t(p_it) * BM + gr * WM) * A.dp + k0;
+#pragma unroll
+        for (int q = 0; q < (WM * (KC / 2)) / GT; ++q) {
+            const int idx = gtid + q * GT;
+            const int row = idx / (KC / 2), pc = idx % (KC / 2);
+            if (pc < pieces) cp_async16(sL + row * KS + pc * 2, gL + int64_t(row) * A.dp + pc * 2);
+        }
+    };
+    auto advance = [&]() {
+        if (++p_kc == nk) {
+            p_kc = 0;
+            ++p_it;
+            if (p_it > (diag ? p_jt : nT - 1)) {
+                p_it = 0;
+                ++p_jt;
+            }
+        }
+    };
+    int ps = 0;
+#pragma unroll
+    for (int s2 = 0; s2 < NSTG - 1; ++s2) {
+        if (ps < total) {
+            issue(ps % NSTG);
+            advance();
+        }
+        cp_async_commit();
+        ++ps;
+    }
+
+    int cs = 0;
+    for (int jt = 0; jt < nT; ++jt) {
+        const int64_t J0 = colBase + int64_t(jt) * BM;
+        __syncthreads();  // everyone is done with the previous R_J, vjs, scr_col
+        {
+            const int pieces = A.dp >> 1;
+            const double* gR = A.R + J0 * A.dp;
+            for (int idx = tid; idx < BM * pieces; idx += 256) {
+                const int row = idx / pieces, pc = idx % pieces;
+                cp_async16(rres + row * A.ksr + pc * 2, gR + int64_t(row) * A.dp + pc * 2);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+        }
+        if (tid < BM) vjs[tid] = A.v[J0 + tid];
+        __syncthreads();
+
+        double colacc[4][2];
+#pragma unroll
+        for (int ns = 0; ns < 4; ++ns) colacc[ns][0] = colacc[ns][1] = 0.0;
+        if (gr == 1) named_bar_sync(3, 256);  // phase offset: wait for group 0's signal
+
+        const int itEnd = diag ? jt : nT - 1;
+        for (int it = 0; it <= itEnd; ++it) {
+            const int64_t I0 = rowBase + int64_t(it) * BM;
+            double acc[MS][4][2];
+#pragma unroll
+            for (int ms = 0; ms < MS; ++ms)
+#pragma unroll
+                for (int ns = 0; ns < 4; ++ns) acc[ms][ns][0] = acc[ms][ns][1] = 0.0;
+
+            for (int kc = 0; kc < nk; ++kc, ++cs) {
+                cp_async_wait<NSTG - 2>();
+                named_bar_sync(bar_id, GT);
+                if (ps < total) {
+                    issue(ps % NSTG);
+                    advance();
+                }
+                cp_async_commit();
+                ++ps;
+
+                const double* sL = mystages + (cs % NSTG) * GSTAGE;
+                const int nks = (min(KC, A.dp - kc * KC)) >> 2;
+                const double* aBase = sL + g * KS + t4;
+                const double* bBase = rres + (wn * 32 + g) * A.ksr + t4 + kc * KC;
+#pragma unroll
+                for (int ks = 0; ks < KC / 4; ++ks) {
+                    if (ks < nks) {
+                        double af[MS], bf[4];
+#pragma unroll
+                        for (int ms = 0; ms < MS; ++ms) af[ms] = aBase[ms * 8 * KS + ks * 4];
+#pragma unroll
+                        for (int ns = 0; ns < 4; ++ns) bf[ns] = bBase[ns * 8 * A.ksr + ks * 4];
+#pragma unroll
+                        for (int ms = 0; ms < MS; ++ms)
+#pragma unroll
+                            for (int ns = 0; ns < 4; ++ns)
+                                dmma884(acc[ms][ns][0], acc[ms][ns][1], af[ms], bf[ns]);
+                    }
+                }
+                if (gr == 0 && it == 0 && kc == sig_kc) named_bar_arrive(3, 256);
+            }
+
+            const bool dtile = diag && (it == jt);
+            double vi[MS];
+#pragma unroll
+            for (int ms = 0; ms < MS; ++ms) vi[ms] = A.v[I0 + gr * WM + ms * 8 + g];
+            double vj[4][2];
+#pragma unroll
+            for (int ns = 0; ns < 4; ++ns) {
+                const double2 p2 = *reinterpret_cast<const double2*>(vjs + wn * 32 + ns * 8 + 2 * t4);
+                vj[ns][0] = p2.x;
+                vj[ns][1] = p2.y;
+            }
+            double rowp[MS];
+            tile_epilogue<EXPMODE, MS>(acc, vi, vj, colacc, rowp, dtile, gr * WM, wn * 32, g, t4, A.ec, tab);
+#pragma unroll
+            for (int ms = 0; ms < MS; ++ms) {
+                double r = rowp[ms];
+                r += __shfl_xor_sync(0xffffffffu, r, 1);
+                r += __shfl_xor_sync(0xffffffffu, r, 2);
+                if (t4 == 0) scr_row[(gr * 4 + wn) * WM + ms * 8 + g] = r;
+            }
+            named_bar_sync(bar_id, GT);
+            if (gtid < WM) {
+                const double* sr = scr_row + gr * 4 * WM + gtid;
+                rowacc[it * BM + gr * WM + gtid] += ((sr[0] + sr[WM]) + sr[2 * WM]) + sr[3 * WM];
+            }
+            // scr_row[gr] is rewritten only after the group's next chunk barrier.
+        }
+
+#pragma unroll
+        for (int ns = 0; ns < 4; ++ns)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double c = colacc[ns][h];
+                c += __shfl_xor_sync(0xffffffffu, c, 4);
+                c += __shfl_xor_sync(0xffffffffu, c, 8);
+                c += __shfl_xor_sync(0xffffffffu, c, 16);
+                if (g == 0) scr_col[gr * BM + wn * 32 + ns * 8 + 2 * t4 + h] = c;
+            }
+        __syncthreads();
+        if (tid < BM) {
+            const double c = scr_col[tid] + scr_col[BM + tid];
+            if (diag) {
+                rowacc[jt * BM + tid] += c;
+            } else {
+                A.part[int64_t(sa) * A.n_pad + J0 + tid] = c;
+            }
+        }
+    }
+    __syncthreads();
+    double* dst = A.part + int64_t(sb) * A.n_pad + rowBase;
+    for (int i = tid; i < A.st; i += 256) dst[i] = rowacc[i];
 }
 
 // out_i = sum_x part[x][i] (owned slots only) + (1 + lambda) v_i  (diag, rank 0)
@@ -311,17 +548,39 @@ int resident_stride(int dp) {
 
 template <bool RES>
 size_t smem_bytes(int st, int dp) {
+    // scratch sized for the widest warp layout (WGM = 4)
     return sizeof(double) * (size_t(RES ? BM * resident_stride(dp) : 0) +
-                             size_t(Shape<RES>::NSTAGE) * Shape<RES>::STAGE_DOUBLES + st + 4 * BM +
-                             2 * BM + 64 + BM);
+                             size_t(Shape<RES>::NSTAGE) * Shape<RES>::STAGE_DOUBLES + st + WGN * BM +
+                             4 * BM + 64 + BM);
 }
 
-template <int EXPMODE, bool RES>
+template <int EXPMODE, bool RES, int MS>
 void launch_variant(const MatvecArgs& a, int64_t ntiles, cudaStream_t stream) {
     const size_t smem = smem_bytes<RES>(a.st, a.dp);
-    KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_kernel<EXPMODE, RES>,
+    KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_kernel<EXPMODE, RES, MS>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    gauss_matvec_kernel<EXPMODE, RES><<<unsigned(ntiles), NTHREADS, smem, stream>>>(a);
+    gauss_matvec_kernel<EXPMODE, RES, MS><<<unsigned(ntiles), Warps<MS>::NT, smem, stream>>>(a);
+}
+
+template <int EXPMODE, int MS>
+void launch_ms(const MatvecArgs& a, int64_t ntiles, bool res, cudaStream_t stream) {
+    if (res)
+        launch_variant<EXPMODE, true, MS>(a, ntiles, stream);
+    else
+        launch_variant<EXPMODE, false, MS>(a, ntiles, stream);
+}
+
+size_t grouped_smem_bytes(int st, int dp) {
+    return sizeof(double) * (size_t(BM) * resident_stride(dp) + size_t(2) * 4 * 64 * KS + st +
+                             2 * 4 * 64 + 2 * BM + 64 + BM);
+}
+
+template <int EXPMODE>
+void launch_grouped(const MatvecArgs& a, int64_t ntiles, cudaStream_t stream) {
+    const size_t smem = grouped_smem_bytes(a.st, a.dp);
+    KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_grouped_kernel<EXPMODE>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    gauss_matvec_grouped_kernel<EXPMODE><<<unsigned(ntiles), 256, smem, stream>>>(a);
 }
 
 }  // namespace
@@ -345,11 +604,15 @@ void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part
     a.st = p.st;
     a.ksr = resident_stride(p.dp);
     a.ec = p.ec;
-    const bool res = p.resident && gauss_matvec_resident_ok(p.st, p.dp);
-    if (exp_mode == 0) {
-        res ? launch_variant<0, true>(a, p.num_tiles, stream) : launch_variant<0, false>(a, p.num_tiles, stream);
+    // The resident shape pays one pipeline drain per column tile: only worth it for
+    // long I sweeps (super-tiles of >= 1024 rows).
+    const bool res = p.resident && p.st >= 1024 && gauss_matvec_resident_ok(p.st, p.dp);
+    if (res && p.grouped && !p.warps16 && grouped_smem_bytes(p.st, p.dp) <= size_t(MAX_SMEM)) {
+        exp_mode == 0 ? launch_grouped<0>(a, p.num_tiles, stream) : launch_grouped<1>(a, p.num_tiles, stream);
+    } else if (exp_mode == 0) {
+        p.warps16 ? launch_ms<0, 4>(a, p.num_tiles, res, stream) : launch_ms<0, 8>(a, p.num_tiles, res, stream);
     } else {
-        res ? launch_variant<1, true>(a, p.num_tiles, stream) : launch_variant<1, false>(a, p.num_tiles, stream);
+        p.warps16 ? launch_ms<1, 4>(a, p.num_tiles, res, stream) : launch_ms<1, 8>(a, p.num_tiles, res, stream);
     }
     KRR_LAUNCH_CHECK();
 }

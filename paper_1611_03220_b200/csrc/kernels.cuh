@@ -21,6 +21,8 @@ struct GaussMatvecPlan {
     int64_t n = 0, n_pad = 0;
     int dp = 0, st = 0, ns = 0;
     bool resident = true;            // keep R_J in shared memory when it fits
+    bool warps16 = false;            // 16 warps x (32 x 32) instead of 8 warps x (64 x 32)
+    bool grouped = true;             // two phase-offset warp groups (resident shape only)
     ExpConsts ec{};
 };
 size_t gauss_matvec_smem_bytes(int st);
@@ -28,6 +30,13 @@ bool gauss_matvec_resident_ok(int st, int dp);
 void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part, int exp_mode,
                          cudaStream_t stream);
 void matvec_finish_launch(const GaussMatvecPlan& p, const double* part, const double* v,
+                          double lambda, int add_diag, double* out, cudaStream_t stream);
+
+// K1T: OUT = (K + lambda I) V for T in {8, 16} interleaved right-hand sides (n_pad x T),
+// part is NS x n_pad x T.
+void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, double* part,
+                         cudaStream_t stream);
+void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const double* v, int T,
                           double lambda, int add_diag, double* out, cudaStream_t stream);
 
 // Build L / R operands from X (n x d) on the device; rows >= n and cols >= d+2 zeroed.
@@ -61,6 +70,25 @@ void gather_col_launch(const double* M, int64_t n, int64_t t, int64_t c, double*
                        cudaStream_t stream);
 void scatter_col_launch(const double* v, int64_t n, int64_t t, int64_t c, double* M,
                         cudaStream_t stream);
+
+// Batched variants for T independent right-hand sides, vectors n x T row-major,
+// partials nb x T, T in {2, 4, 8, 16}; `active` (device, T ints) masks converged columns.
+int vecT_blocks(int64_t n, int T);
+void dotT_partial_launch(const double* a, const double* b, int64_t n, int T, double* partial, int nb,
+                         cudaStream_t stream);
+void sumT_partials_launch(const double* partial, int nb, int T, double* out, cudaStream_t stream);
+void pcgT_update_xr_launch(const double* pap_part, int nb, int T, const double* rz, const int* active,
+                           double* x, double* r, const double* p, const double* ap, int64_t n,
+                           double* rr_part, double* pap_out, cudaStream_t stream);
+void pcgT_update_p_launch(const double* rz_part, int nb, int T, const double* rz_old, double* rz_out,
+                          const int* active, double* p, const double* z, int64_t n, cudaStream_t stream);
+void woodbury_finish_launch(const double* r, const double* y, double lambda_p, double* z, int64_t count,
+                            cudaStream_t stream);
+// columns [c0, c0 + T) of an n x t row-major block <-> n_pad x T interleaved (zero padded)
+void pad_cols_launch(const double* in, int64_t n, int64_t t, int64_t c0, int64_t n_pad, int T, double* out,
+                     cudaStream_t stream);
+void unpad_cols_launch(const double* in, int64_t n, int64_t t, int64_t c0, int T, double* out,
+                       cudaStream_t stream);
 
 // ---------------------------------------------------------------- RFF (K2)
 // Wp (s_pad x dp) = W (s x d) zero-padded.

@@ -94,7 +94,7 @@ struct DevMem {
 
 struct PinnedScalars {
     double* p = nullptr;
-    PinnedScalars() { KRR_CUDA(cudaMallocHost(&p, 16 * sizeof(double))); }
+    explicit PinnedScalars(size_t count = 16) { KRR_CUDA(cudaMallocHost(&p, count * sizeof(double))); }
     ~PinnedScalars() {
         if (p) cudaFreeHost(p);
     }
@@ -110,6 +110,8 @@ struct Ctx {
     ncclComm_t comm = nullptr;
     int exp_mode = 1;
     bool k1_resident = true;
+    bool k1_warps16 = false;
+    bool k1_grouped = true;
 
     // data
     bool has_data = false;
@@ -133,6 +135,13 @@ struct Ctx {
     DevMem<int> info;
 
     int nb = 1;  // vector reduction blocks
+
+    // batched multi-RHS state (n_pad x T interleaved blocks)
+    bool batched = true;
+    DevMem<double> bx, br, bz, bp, bap, by, bin, bout, bpart, bred, bscal, bW, bY;
+    DevMem<int> bactive;
+    std::unique_ptr<PinnedScalars> hscalT;
+    int* hactive = nullptr;
 
     void set_device() const { KRR_CUDA(cudaSetDevice(device)); }
     void sync() const { KRR_CUDA(cudaStreamSynchronize(stream)); }
@@ -216,6 +225,8 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
     p.ns = int(c.sched.ns);
     p.ec = make_exp_consts(c.scale);
     p.resident = c.k1_resident;
+    p.warps16 = c.k1_warps16;
+    p.grouped = c.k1_grouped;
     c.sync();
     c.has_data = true;
 }
@@ -451,6 +462,134 @@ PcgOut pcg_core(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, const double*
     return out;
 }
 
+// ---------------------------------------------------------------- batched multi-RHS (t > 1)
+int batch_width(int64_t t) { return t <= 8 ? 8 : 16; }
+
+void ensure_batched(Ctx& c, int T) {
+    const size_t nt = size_t(c.plan.n_pad) * size_t(T);
+    for (auto* v : {&c.bx, &c.br, &c.bz, &c.bp, &c.bap, &c.by, &c.bin, &c.bout}) v->ensure(nt);
+    c.bpart.ensure(size_t(c.sched.ns) * nt);
+    c.bred.ensure(size_t(3) * 148 * 4 * 16);
+    c.bscal.ensure(128);
+    c.bactive.ensure(16);
+    if (!c.hscalT) {
+        c.hscalT = std::make_unique<PinnedScalars>(128);
+        KRR_CUDA(cudaMallocHost(&c.hactive, 16 * sizeof(int)));
+    }
+}
+
+// out (n_pad x T) = (K + lambda I) v (n_pad x T), replicated on all ranks.
+void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
+    gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.stream);
+    matmat_finish_launch(c.plan, c.bpart.get(), v, T, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
+    allreduce_sum(c, out, c.plan.n_pad * T);
+}
+
+// z (pn x T) = (r - U^T U r) / lambda_p for T interleaved columns: two cuBLAS GEMMs over
+// the row shard of B = U^T (n x s row-major == s x n column-major) + a fused finish.
+void precondT_apply_dev(Ctx& c, const double* r, double* z, int T) {
+    if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
+    const int64_t s = c.s, rows = c.z1 - c.z0;
+    c.bW.ensure(size_t(s * T));
+    c.bY.ensure(size_t(std::max<int64_t>(1, rows)) * T);
+    const double one = 1.0, zero = 0.0;
+    if (rows > 0) {
+        // W (s x T col-major) = B_cm (s x rows) . R_cm^T, R_cm = r rows as T x rows col-major
+        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_T, int(s), T, int(rows), &one, c.Z.get(),
+                                 int(s), r + c.z0 * T, T, &zero, c.bW.get(), int(s)),
+                     "cublasDgemm(U R)");
+    } else {
+        KRR_CUDA(cudaMemsetAsync(c.bW.get(), 0, sizeof(double) * size_t(s * T), c.stream));
+    }
+    allreduce_sum(c, c.bW.get(), s * T);
+    if (rows > 0) {
+        // Y (T x rows col-major == rows x T row-major) = W^T . B_cm
+        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, T, int(rows), int(s), &one, c.bW.get(),
+                                 int(s), c.Z.get(), int(s), &zero, c.bY.get(), T),
+                     "cublasDgemm(U^T W)");
+        woodbury_finish_launch(r + c.z0 * T, c.bY.get(), c.lambda_p, z + c.z0 * T, rows * T, c.stream);
+    }
+    if (c.world > 1) {
+        if (c.z0 > 0) KRR_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * size_t(c.z0 * T), c.stream));
+        if (c.z1 < c.pn)
+            KRR_CUDA(cudaMemsetAsync(z + c.z1 * T, 0, sizeof(double) * size_t((c.pn - c.z1) * T), c.stream));
+        allreduce_sum(c, z, c.pn * T);
+    }
+}
+
+// Batched PCG over T interleaved columns, t_real of which are real.  Every column runs
+// exactly the reference's per-column recurrence (solver.cpp:22-67) with its own alpha,
+// beta and stopping test; converged columns are frozen by a device mask.
+void pcgT_core(Ctx& c, int T, int t_real, double lambda, bool use_pre, double tau, int max_iter,
+               krr_rhs_stats* stats, double* hist, int64_t hist_stride) {
+    if (!(tau > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "pcg_solve: tau must be positive");
+    if (max_iter < 1) fail(KRR_ERR_INVALID_ARGUMENT, "pcg_solve: max_iter must be at least 1");
+    const int64_t n = c.n, nt = c.plan.n_pad * T;
+    const int nb = vecT_blocks(n, T);
+    double* pap_part = c.bred.get();
+    double* rr_part = pap_part + size_t(nb) * T;
+    double* rz_part = rr_part + size_t(nb) * T;
+    double* sc = c.bscal.get();  // [0,16) pap  [16,32) rz even  [32,48) rz odd  [48,64) rr  [64,80) yy
+    double* hs = c.hscalT->p;
+    KRR_CUDA(cudaMemsetAsync(c.bx.get(), 0, sizeof(double) * size_t(nt), c.stream));
+    dotT_partial_launch(c.by.get(), c.by.get(), n, T, rr_part, nb, c.stream);
+    sumT_partials_launch(rr_part, nb, T, sc + 64, c.stream);
+    KRR_CUDA(cudaMemcpyAsync(hs + 64, sc + 64, sizeof(double) * T, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    std::vector<double> norm_y(static_cast<size_t>(T));
+    int n_active = 0;
+    for (int j = 0; j < T; ++j) {
+        norm_y[size_t(j)] = std::sqrt(hs[64 + j]);
+        const bool act = j < t_real && norm_y[size_t(j)] != 0.0;
+        c.hactive[j] = act ? 1 : 0;
+        n_active += act;
+        if (j < t_real) stats[j] = krr_rhs_stats{0, act ? 0 : 1, 0.0};  // zero RHS: converged, 0 its
+    }
+    KRR_CUDA(cudaMemcpyAsync(c.bactive.get(), c.hactive, sizeof(int) * T, cudaMemcpyHostToDevice, c.stream));
+    if (n_active == 0) return;
+    copy_launch(c.br.get(), c.by.get(), nt, c.stream);
+    double* z = use_pre ? c.bz.get() : c.br.get();
+    if (use_pre) precondT_apply_dev(c, c.br.get(), z, T);
+    copy_launch(c.bp.get(), z, nt, c.stream);
+    dotT_partial_launch(c.br.get(), z, n, T, rz_part, nb, c.stream);
+    sumT_partials_launch(rz_part, nb, T, sc + 16, c.stream);
+    int cur = 0;
+    for (int it = 1; it <= max_iter && n_active > 0; ++it) {
+        matvecT_dev(c, c.bp.get(), c.bap.get(), T, lambda);
+        dotT_partial_launch(c.bp.get(), c.bap.get(), n, T, pap_part, nb, c.stream);
+        pcgT_update_xr_launch(pap_part, nb, T, sc + 16 + 16 * cur, c.bactive.get(), c.bx.get(), c.br.get(),
+                              c.bp.get(), c.bap.get(), n, rr_part, sc, c.stream);
+        sumT_partials_launch(rr_part, nb, T, sc + 48, c.stream);
+        KRR_CUDA(cudaMemcpyAsync(hs, sc, sizeof(double) * 64, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        bool changed = false;
+        for (int j = 0; j < t_real; ++j) {
+            if (!c.hactive[j]) continue;
+            if (!(hs[j] > 0.0))
+                fail(KRR_ERR_BREAKDOWN, "pcg_solve: p'Ap <= 0, operator is not positive definite");
+            const double rel = std::sqrt(hs[48 + j]) / norm_y[size_t(j)];
+            stats[j].iterations = it;
+            stats[j].final_residual = rel;
+            if (hist) hist[j * hist_stride + it - 1] = rel;
+            if (rel <= tau) {
+                stats[j].converged = 1;
+                c.hactive[j] = 0;
+                --n_active;
+                changed = true;
+            }
+        }
+        if (n_active == 0) break;
+        if (changed)
+            KRR_CUDA(cudaMemcpyAsync(c.bactive.get(), c.hactive, sizeof(int) * T, cudaMemcpyHostToDevice,
+                                     c.stream));
+        if (use_pre) precondT_apply_dev(c, c.br.get(), z, T);
+        dotT_partial_launch(c.br.get(), z, n, T, rz_part, nb, c.stream);
+        pcgT_update_p_launch(rz_part, nb, T, sc + 16 + 16 * cur, sc + 16 + 16 * (cur ^ 1), c.bactive.get(),
+                             c.bp.get(), z, n, c.stream);
+        cur ^= 1;
+    }
+}
+
 DevOp gaussian_op(Ctx& c, double lambda) {
     return [&c, lambda](const double* din, double* dout) { matvec_dev(c, din, dout, lambda); };
 }
@@ -477,6 +616,25 @@ void solve_gaussian(Ctx& c, double lambda, const double* Y, int64_t t, double ta
     c.mat_b.ensure(size_t(n * t));
     KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), Y, sizeof(double) * size_t(n * t), cudaMemcpyHostToDevice,
                              c.stream));
+    if (t > 1 && c.batched) {
+        // Independent columns in batches of T = 8 or 16 sharing every K1T pass.
+        const int T = batch_width(t);
+        ensure_batched(c, T);
+        int64_t total = 0;
+        for (int64_t c0 = 0; c0 < t; c0 += T) {
+            const int t_real = int(std::min<int64_t>(T, t - c0));
+            pad_cols_launch(c.mat_a.get(), n, t, c0, c.plan.n_pad, T, c.by.get(), c.stream);
+            pcgT_core(c, T, t_real, lambda, use_precond != 0, tau, max_iter, stats + c0,
+                      hist ? hist + c0 * max_iter : nullptr, max_iter);
+            unpad_cols_launch(c.bx.get(), n, t, c0, T, c.mat_b.get(), c.stream);
+            for (int j = 0; j < t_real; ++j) total += stats[c0 + j].iterations;
+        }
+        KRR_CUDA(cudaMemcpyAsync(C, c.mat_b.get(), sizeof(double) * size_t(n * t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+        if (total_matvecs) *total_matvecs = total;
+        return;
+    }
     const DevOp A = gaussian_op(c, lambda);
     const DevOp M = precond_op(c);
     int64_t total = 0;
@@ -611,6 +769,7 @@ int krr_ctx_destroy(krr_ctx* ctx) {
         if (c->sol) cusolverDnDestroy(c->sol);
         if (c->blas) cublasDestroy(c->blas);
         cudaStream_t st = c->stream;
+        if (c->hactive) cudaFreeHost(c->hactive);
         delete c;  // frees device buffers
         if (st) cudaStreamDestroy(st);
     });
@@ -630,6 +789,15 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
         if (k == "k1_resident") {
             c.k1_resident = value != 0.0;
             c.plan.resident = c.k1_resident;
+        } else if (k == "k1_warps") {
+            if (value != 8.0 && value != 16.0) fail(KRR_ERR_INVALID_ARGUMENT, "k1_warps must be 8 or 16");
+            c.k1_warps16 = value == 16.0;
+            c.plan.warps16 = c.k1_warps16;
+        } else if (k == "k1_grouped") {
+            c.k1_grouped = value != 0.0;
+            c.plan.grouped = c.k1_grouped;
+        } else if (k == "batched_rhs") {
+            c.batched = value != 0.0;
         } else if (k == "exp_mode") {
             c.exp_mode = value != 0.0 ? 1 : 0;
         } else {
@@ -680,10 +848,20 @@ int krr_kernel_matvec(krr_ctx* ctx, double lambda, const double* V, int64_t t, d
         c.mat_b.ensure(size_t(n * t));
         KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), V, sizeof(double) * size_t(n * t),
                                  cudaMemcpyHostToDevice, c.stream));
-        for (int64_t j = 0; j < t; ++j) {
-            krr::gather_col_launch(c.mat_a.get(), n, t, j, c.vin.get(), c.stream);
-            krr::matvec_dev(c, c.vin.get(), c.vout.get(), lambda);
-            krr::scatter_col_launch(c.vout.get(), n, t, j, c.mat_b.get(), c.stream);
+        if (t > 1 && c.batched) {
+            const int T = krr::batch_width(t);
+            krr::ensure_batched(c, T);
+            for (int64_t c0 = 0; c0 < t; c0 += T) {
+                krr::pad_cols_launch(c.mat_a.get(), n, t, c0, c.plan.n_pad, T, c.bin.get(), c.stream);
+                krr::matvecT_dev(c, c.bin.get(), c.bout.get(), T, lambda);
+                krr::unpad_cols_launch(c.bout.get(), n, t, c0, T, c.mat_b.get(), c.stream);
+            }
+        } else {
+            for (int64_t j = 0; j < t; ++j) {
+                krr::gather_col_launch(c.mat_a.get(), n, t, j, c.vin.get(), c.stream);
+                krr::matvec_dev(c, c.vin.get(), c.vout.get(), lambda);
+                krr::scatter_col_launch(c.vout.get(), n, t, j, c.mat_b.get(), c.stream);
+            }
         }
         KRR_CUDA(cudaMemcpyAsync(out, c.mat_b.get(), sizeof(double) * size_t(n * t),
                                  cudaMemcpyDeviceToHost, c.stream));

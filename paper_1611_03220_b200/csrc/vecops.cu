@@ -136,11 +136,177 @@ __global__ void scatter_col_kernel(const double* __restrict__ v, int64_t n, int6
         M[i * t + c] = v[i];
 }
 
+// ---- batched (n x T, row-major) variants for T independent right-hand sides.
+// Thread layout: column c = threadIdx.x % T, row slot = threadIdx.x / T, so every
+// thread owns one column's running sum; per-column block reduction through smem in
+// a fixed order.  T divides blockDim (T in {2, 4, 8, 16}).
+__device__ __forceinline__ void block_sum_cols(double v, int T, double* scr, double* out_row) {
+    scr[threadIdx.x] = v;
+    __syncthreads();
+    for (int stride = blockDim.x / 2; stride >= T; stride >>= 1) {
+        if (threadIdx.x < stride) scr[threadIdx.x] += scr[threadIdx.x + stride];
+        __syncthreads();
+    }
+    if (threadIdx.x < T) out_row[threadIdx.x] = scr[threadIdx.x];
+}
+
+__global__ void dotT_partial_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                    int64_t n, int T, double* __restrict__ partial) {
+    __shared__ double scr[256];
+    const int c = threadIdx.x % T;
+    const int rs = threadIdx.x / T, rper = blockDim.x / T;
+    double s = 0.0;
+    for (int64_t i = int64_t(blockIdx.x) * rper + rs; i < n; i += int64_t(gridDim.x) * rper)
+        s = fma(a[i * T + c], b[i * T + c], s);
+    block_sum_cols(s, T, scr, partial + int64_t(blockIdx.x) * T);
+}
+
+__global__ void sumT_partials_kernel(const double* __restrict__ partial, int nb, int T,
+                                     double* __restrict__ out) {
+    const int c = threadIdx.x;
+    if (c >= T) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += partial[int64_t(b) * T + c];
+    out[c] = s;
+}
+
+// alpha_c = active_c ? rz_c / pap_c : 0 (pap_c summed from the partials);
+// x += alpha p, r -= alpha ap, |r|^2 partials.  scal_out[c] <- pap_c (block 0).
+__global__ void pcgT_update_xr_kernel(const double* __restrict__ pap_part, int nb, int T,
+                                      const double* __restrict__ rz, const int* __restrict__ active,
+                                      double* __restrict__ x, double* __restrict__ r,
+                                      const double* __restrict__ p, const double* __restrict__ ap,
+                                      int64_t n, double* __restrict__ rr_part,
+                                      double* __restrict__ pap_out) {
+    __shared__ double scr[256];
+    __shared__ double alpha[16];
+    if (threadIdx.x < T) {
+        double pap = 0.0;
+        for (int b = 0; b < nb; ++b) pap += pap_part[int64_t(b) * T + threadIdx.x];
+        alpha[threadIdx.x] = active[threadIdx.x] ? rz[threadIdx.x] / pap : 0.0;
+        if (blockIdx.x == 0) pap_out[threadIdx.x] = pap;
+    }
+    __syncthreads();
+    const int c = threadIdx.x % T;
+    const int rs = threadIdx.x / T, rper = blockDim.x / T;
+    const double al = alpha[c];
+    double s = 0.0;
+    for (int64_t i = int64_t(blockIdx.x) * rper + rs; i < n; i += int64_t(gridDim.x) * rper) {
+        const int64_t k = i * T + c;
+        x[k] += al * p[k];
+        const double ri = r[k] - al * ap[k];
+        r[k] = ri;
+        s = fma(ri, ri, s);
+    }
+    block_sum_cols(s, T, scr, rr_part + int64_t(blockIdx.x) * T);
+}
+
+// beta_c = rz_new_c / rz_old_c; p = z + beta p (active columns); rz_out <- rz_new.
+__global__ void pcgT_update_p_kernel(const double* __restrict__ rz_part, int nb, int T,
+                                     const double* __restrict__ rz_old, double* __restrict__ rz_out,
+                                     const int* __restrict__ active, double* __restrict__ p,
+                                     const double* __restrict__ z, int64_t n) {
+    __shared__ double beta[16];
+    if (threadIdx.x < T) {
+        double rzn = 0.0;
+        for (int b = 0; b < nb; ++b) rzn += rz_part[int64_t(b) * T + threadIdx.x];
+        beta[threadIdx.x] = rzn / rz_old[threadIdx.x];
+        if (blockIdx.x == 0) rz_out[threadIdx.x] = active[threadIdx.x] ? rzn : rz_old[threadIdx.x];
+    }
+    __syncthreads();
+    const int c = threadIdx.x % T;
+    const int rs = threadIdx.x / T, rper = blockDim.x / T;
+    if (!active[c]) return;
+    const double be = beta[c];
+    for (int64_t i = int64_t(blockIdx.x) * rper + rs; i < n; i += int64_t(gridDim.x) * rper) {
+        const int64_t k = i * T + c;
+        p[k] = z[k] + be * p[k];
+    }
+}
+
+// Interleave an n x t row-major block into n_pad x T (zero padded) and back.
+__global__ void pad_cols_kernel(const double* __restrict__ in, int64_t n, int64_t t, int64_t c0,
+                                int64_t n_pad, int T, double* __restrict__ out) {
+    const int64_t total = n_pad * T;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k / T, c = k % T;
+        out[k] = (i < n && c0 + c < t) ? in[i * t + c0 + c] : 0.0;
+    }
+}
+
+__global__ void unpad_cols_kernel(const double* __restrict__ in, int64_t n, int64_t t, int64_t c0, int T,
+                                  double* __restrict__ out) {
+    const int64_t tc = min(int64_t(T), t - c0);
+    const int64_t total = n * tc;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = k / tc, c = k % tc;
+        out[i * t + c0 + c] = in[i * T + c];
+    }
+}
+
+// z = (r - y) / lambda_p elementwise (batched Woodbury epilogue after the cuBLAS GEMMs)
+__global__ void woodbury_finish_kernel(const double* __restrict__ r, const double* __restrict__ y,
+                                       double lambda_p, double* __restrict__ z, int64_t count) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+         i += int64_t(gridDim.x) * blockDim.x)
+        z[i] = (r[i] - y[i]) / lambda_p;
+}
+
 unsigned grid_for(int64_t n) {
     return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
 }
 
 }  // namespace
+
+int vecT_blocks(int64_t n, int T) {
+    const int64_t rows_per_block = 256 / T;
+    return int(std::max<int64_t>(1, std::min<int64_t>((n + rows_per_block - 1) / rows_per_block, 148 * 4)));
+}
+
+void dotT_partial_launch(const double* a, const double* b, int64_t n, int T, double* partial, int nb,
+                         cudaStream_t stream) {
+    dotT_partial_kernel<<<nb, 256, 0, stream>>>(a, b, n, T, partial);
+    KRR_LAUNCH_CHECK();
+}
+
+void sumT_partials_launch(const double* partial, int nb, int T, double* out, cudaStream_t stream) {
+    sumT_partials_kernel<<<1, 32, 0, stream>>>(partial, nb, T, out);
+    KRR_LAUNCH_CHECK();
+}
+
+void pcgT_update_xr_launch(const double* pap_part, int nb, int T, const double* rz, const int* active,
+                           double* x, double* r, const double* p, const double* ap, int64_t n,
+                           double* rr_part, double* pap_out, cudaStream_t stream) {
+    pcgT_update_xr_kernel<<<nb, 256, 0, stream>>>(pap_part, nb, T, rz, active, x, r, p, ap, n, rr_part,
+                                                  pap_out);
+    KRR_LAUNCH_CHECK();
+}
+
+void pcgT_update_p_launch(const double* rz_part, int nb, int T, const double* rz_old, double* rz_out,
+                          const int* active, double* p, const double* z, int64_t n, cudaStream_t stream) {
+    pcgT_update_p_kernel<<<nb, 256, 0, stream>>>(rz_part, nb, T, rz_old, rz_out, active, p, z, n);
+    KRR_LAUNCH_CHECK();
+}
+
+void pad_cols_launch(const double* in, int64_t n, int64_t t, int64_t c0, int64_t n_pad, int T, double* out,
+                     cudaStream_t stream) {
+    pad_cols_kernel<<<grid_for(n_pad * T), 256, 0, stream>>>(in, n, t, c0, n_pad, T, out);
+    KRR_LAUNCH_CHECK();
+}
+
+void unpad_cols_launch(const double* in, int64_t n, int64_t t, int64_t c0, int T, double* out,
+                       cudaStream_t stream) {
+    unpad_cols_kernel<<<grid_for(n * T), 256, 0, stream>>>(in, n, t, c0, T, out);
+    KRR_LAUNCH_CHECK();
+}
+
+void woodbury_finish_launch(const double* r, const double* y, double lambda_p, double* z, int64_t count,
+                            cudaStream_t stream) {
+    woodbury_finish_kernel<<<grid_for(count), 256, 0, stream>>>(r, y, lambda_p, z, count);
+    KRR_LAUNCH_CHECK();
+}
 
 void build_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, int dp,
                            double* L, double* R, cudaStream_t stream) {

@@ -130,22 +130,36 @@ def test_device_matvec_entry_and_launch_count(krr, oracle, ctx):
     assert tot.value > 0 and 0 < k1.value <= tot.value
 
 
-@pytest.mark.parametrize("n,d", [(1000, 16), (3000, 90), (700, 54)])
+@pytest.mark.parametrize("n,d", [(1000, 16), (3000, 90), (700, 54), (5000, 20), (40000, 90), (33000, 5)])
 def test_resident_and_streaming_variants_bitwise_equal(krr, oracle, ctx, n, d):
     """The two K1 pipeline shapes do the same arithmetic in the same order."""
     x = oracle.random_matrix(n, d, 31)
     v = oracle.random_vector(n, 32)
     op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(5.0), 1e-4, ctx=ctx)
     a = op(v)
+    ctx.set_option("k1_grouped", 0)
+    a2 = op(v)
+    ctx.set_option("k1_grouped", 1)
+    assert np.array_equal(a, a2)  # phase-offset warp groups: same arithmetic, same order
     ctx.set_option("k1_resident", 0)
     b = op(v)
     ctx.set_option("exp_mode", 0)
     c = op(v)
     ctx.set_option("k1_resident", 1)
     ctx.set_option("exp_mode", 1)
+    ctx.set_option("k1_warps", 16)
+    d16 = op(v)
+    ctx.set_option("k1_resident", 0)
+    e16 = op(v)
+    ctx.set_option("k1_resident", 1)
+    ctx.set_option("k1_warps", 8)
     assert np.array_equal(a, b)
+    assert np.array_equal(d16, e16)
     assert rel(c, a) <= 1e-14
+    assert rel(d16, a) <= 1e-14  # 16-warp layout reduces column sums over 4 warps, not 2
     assert np.array_equal(op(v), a)  # deterministic run to run
+    want = oracle.kernel_matvec(x, 5.0, 1e-4, v)
+    assert rel(d16, want) <= 1e-13
 
 
 def test_set_option_rejects_unknown(krr, ctx):

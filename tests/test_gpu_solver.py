@@ -278,3 +278,55 @@ def test_predict_scores(krr, oracle):
     assert rel(scores, want) <= 1e-10
     xq = oracle.random_matrix(11, 3, 9)
     assert rel(krr.predict_scores(res.model, xq), oracle.cross_gram(xq, x, 1.0) @ res.model.c) <= 1e-12
+
+
+# ----------------------------------------------------------------------------- multi-RHS (config 5 path)
+@pytest.mark.parametrize("n,d,t", [(3000, 40, 16), (2500, 7, 3), (1500, 12, 20)])
+def test_multi_rhs_matvec(krr, oracle, ctx, n, d, t):
+    """K1T: (K + lambda I) V for interleaved right-hand sides on the DMMA path."""
+    x = oracle.random_matrix(n, d, 41)
+    v = oracle.random_matrix(n, t, 42)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(4.0), 1e-3, ctx=ctx)
+    got = op.matmat(v)
+    want = oracle.kernel_matvec(x, 4.0, 1e-3, v)
+    assert rel(got, want) <= 1e-13, rel(got, want)
+    ctx.set_option("batched_rhs", 0)
+    per_col = op.matmat(v)
+    ctx.set_option("batched_rhs", 1)
+    assert rel(got, per_col) <= 1e-14
+
+
+def test_multi_rhs_train_parity(krr, oracle):
+    """Batched independent-column PCG (solver.cpp:85-90 semantics per column): every
+    column's iterations within +-1 of the oracle family and alpha <= 1e-8."""
+    n, d, sigma, lam, s, t = 3000, 5, 2.0, 1e-2, 256, 5
+    x = oracle.random_matrix(n, d, 51)
+    y = oracle.random_matrix(n, t, 52)
+    y[:, 2] = 0.0  # a zero right-hand side converges with 0 iterations (solver.cpp:30-34)
+    fam = {k: oracle.train(x, y, sigma, lam, s, 0, 1e-8, 500, order=k) for k in (2, 0, 1)}
+    cfg = krr.SolverConfig(lambda_=lam, tau=1e-8, max_iter=500, chain=krr.ChainSpec(s1=s), seed=0)
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), cfg)
+    for j in range(t):
+        its = [f.iterations[j] for f in fam.values()]
+        st = res.report.per_rhs[j]
+        assert min(its) - 1 <= st.iterations <= max(its) + 1, (j, st.iterations, its)
+        assert st.converged
+        assert len(st.residual_history) == st.iterations
+    assert res.report.per_rhs[2].iterations == 0
+    assert res.report.total_matvecs == sum(r.iterations for r in res.report.per_rhs)
+    assert rel(res.model.c, fam[2].c) <= 1e-8, rel(res.model.c, fam[2].c)
+
+
+def test_rlsc_multiclass_train(krr, oracle):
+    """Config-5-shaped (small): RLSC one-vs-all targets, 16 classes, batched PCG, labels
+    predicted on the training set agree with the oracle's."""
+    n, d, t = 2048, 20, 16
+    x, y = krr.generate_config(5, n, d, t, 0)
+    sigma, lam, s = 4.0, 1e-2, 512
+    cfg = krr.SolverConfig(lambda_=lam, tau=1e-6, max_iter=300, chain=krr.ChainSpec(s1=s), seed=0)
+    res = krr.train(krr.Dataset(x, y, label_map=list(range(t))), krr.KernelSpec.gaussian(sigma), cfg)
+    ref = oracle.train(x, y, sigma, lam, s, 0, 1e-6, 300)
+    assert rel(res.model.c, ref.c) <= 1e-7
+    pred = krr.predict_labels(res.model, x[:200])
+    want = [int(np.argmax(r)) for r in oracle.cross_gram(x[:200], x, sigma) @ ref.c]
+    assert pred == want

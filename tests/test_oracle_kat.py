@@ -283,3 +283,19 @@ def test_undersized_sketch_stalls_like_reference(oracle):
     y = oracle.random_matrix(1000, 1, 4)
     a = oracle.train(x, y, 2.0, 1e-3, 128, 0, 1e-6, 60)
     assert a.iterations[0] == 60 and not a.converged[0] and a.final_residual[0] > 1e-6
+
+
+def test_oracle_regression_freeze(oracle):
+    """tests/golden/oracle_small.json freezes the oracle's outputs (Eigen-like order);
+    any change to the restatement's arithmetic must be deliberate (regenerate with
+    tests/golden/make_golden.py and say why in the commit)."""
+    g = json.loads((Path(__file__).parent / "golden" / "oracle_small.json").read_text())
+    x = oracle.random_matrix(64, 3, 1)
+    y = oracle.random_matrix(64, 1, 2)
+    t = g["train_n64_d3"]
+    res = oracle.train(x, y, t["sigma"], t["lambda"], t["s"], t["seed"], t["tau"], 200)
+    assert res.iterations[0] == t["iterations"]
+    assert res.c[:, 0].tolist() == t["c"]
+    m = g["matvec_n64_d3"]
+    v = oracle.random_vector(64, m["v_seed"])
+    assert oracle.kernel_matvec(x, m["sigma"], m["lambda"], v).tolist() == m["out"]

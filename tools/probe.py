@@ -19,13 +19,13 @@ import paper_1611_03220_b200 as krr  # noqa: E402
 from paper_1611_03220_b200 import _lib  # noqa: E402
 
 MB_KEYS = ["dmma_tflops", "dfma_tflops", "mixed_tflops", "exp_libdevice_gevals", "exp_table_gevals",
-           "sms", "clock_mhz", "split_warps_tflops"]
+           "sms", "clock_mhz", "split_warps_tflops", "imma_legacy_tops"]
 
 
-def report(n, d, ms, k1, t_set, res, exp_mode):
+def report(n, d, ms, k1, t_set, res, exp_mode, warps, grouped=0):
     pairs = n * (n - 1) / 2
     dp = (d + 2 + 3) // 4 * 4
-    row = {"n": n, "d": d, "resident": res, "exp_mode": exp_mode, "ms_per_matvec": ms, "k1_ms": k1,
+    row = {"n": n, "d": d, "resident": res, "warps": warps, "grouped": grouped, "exp_mode": exp_mode, "ms_per_matvec": ms, "k1_ms": k1,
            "gevals_per_s": n * n / (ms * 1e-3) / 1e9,
            "unique_pairs_per_s": pairs / (k1 * 1e-3) / 1e9,
            "dot_tflops": pairs * 2 * d / (k1 * 1e-3) / 1e12,
@@ -41,12 +41,14 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--exp-mode", type=int, default=1)
     ap.add_argument("--resident", type=int, default=-1, help="-1: both K1 variants")
+    ap.add_argument("--warps", type=int, default=-1, help="-1: both 8 and 16")
+    ap.add_argument("--grouped", type=int, default=-1, help="-1: both (resident 8-warp only)")
     ap.add_argument("--no-microbench", action="store_true")
     args = ap.parse_args()
     out = {}
     ctx = krr.Context(0)
     if not args.no_microbench:
-        res = np.zeros(8)
+        res = np.zeros(9)
         _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(res)))
         out["microbench"] = dict(zip(MB_KEYS, res.tolist()))
         print(json.dumps(out["microbench"]), flush=True)
@@ -57,13 +59,19 @@ def main():
         t0 = time.perf_counter()
         _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, 6.0))
         t_set = time.perf_counter() - t0
-        for res in ([1, 0] if args.resident < 0 else [args.resident]):
+        combos = [(r, w, gp) for w in ([8, 16] if args.warps < 0 else [args.warps])
+                  for r in ([1, 0] if args.resident < 0 else [args.resident])
+                  for gp in ([1, 0] if args.grouped < 0 and r == 1 and w == 8 else
+                             [max(args.grouped, 0) if r == 1 and w == 8 else 0])]
+        for res, w, gp in combos:
             ctx.set_option("k1_resident", res)
+            ctx.set_option("k1_warps", w)
+            ctx.set_option("k1_grouped", gp)
             ctx.set_option("exp_mode", args.exp_mode)
             tot, k1 = C.c_double(), C.c_double()
             _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))  # warm
             _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, args.steps, C.byref(tot), C.byref(k1)))
-            rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode))
+            rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode, w, gp))
     out["matvec"] = rows
     ctx.close()
     od = ROOT / "gpurun_out"
