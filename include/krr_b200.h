@@ -209,6 +209,13 @@ int krr_microbench(krr_ctx* ctx, double* results);
 int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale, int mode,
                         double* out);
 
+/* tcgen05 kind::i8 probe: C (128 x N int32) = A (128 x K int8) . B (N x K int8)^T on
+ * one CTA (K % 32 == 0, K <= 256, N in {32, 64}); host buffers, row-major. */
+int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int K, int N);
+/* cycles per back-to-back tcgen05.mma kind::i8 (M = 128, N in {32, 64, 128, 256}, K = 32),
+ * operands in the no-swizzle K-major layout with `kbytes` bytes per row. */
+int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, double* cycles_per_mma);
+
 #ifdef __cplusplus
 }
 #endif

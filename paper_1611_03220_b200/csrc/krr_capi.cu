@@ -122,6 +122,13 @@ struct Ctx {
     DevMem<double> X, L, R, part, exp_tab;
     DevMem<int2> tiles;
     DevMem<uint8_t> owned;
+    // K1-I8 operands (int8 slices, row exponents, |x|^2)
+    int k1_path = 0;  // 0 = FP64 DMMA, 1 = tcgen05 INT8 slices
+    bool i8_ready = false;
+    int kp8 = 0;
+    DevMem<uint8_t> S8;
+    DevMem<int> ex8;
+    DevMem<double> sq8;
 
     // PCG vectors (n_pad each) and reduction scratch
     DevMem<double> vin, vout, vx, vr, vz, vp, vap, vy, red, scal, mat_a, mat_b;
@@ -163,7 +170,10 @@ void allreduce_sum(Ctx& c, double* buf, int64_t count) {
 void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t k1a = nullptr,
                 cudaEvent_t k1b = nullptr) {
     if (k1a) KRR_CUDA(cudaEventRecord(k1a, c.stream));
-    gauss_matvec_launch(c.plan, v, c.part.get(), c.exp_mode, c.stream);
+    if (c.k1_path == 1 && c.i8_ready)
+        gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.sq8.get(), v, c.part.get(), c.kp8, c.stream);
+    else
+        gauss_matvec_launch(c.plan, v, c.part.get(), c.exp_mode, c.stream);
     if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
     matvec_finish_launch(c.plan, c.part.get(), v, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad);
@@ -224,6 +234,15 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
     p.st = int(c.sched.st);
     p.ns = int(c.sched.ns);
     p.ec = make_exp_consts(c.scale);
+    c.i8_ready = false;
+    if (i8_supported(d, int(c.sched.st))) {
+        c.kp8 = i8_kp(d);
+        c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
+        c.ex8.ensure(size_t(n_pad));
+        c.sq8.ensure(size_t(n_pad));
+        i8_prepare_launch(c.X.get(), n, d, n_pad, c.L.get(), dp, c.S8.get(), c.ex8.get(), c.sq8.get(), c.stream);
+        c.i8_ready = true;
+    }
     p.resident = c.k1_resident;
     p.warps16 = c.k1_warps16;
     p.grouped = c.k1_grouped;
@@ -796,6 +815,9 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
         } else if (k == "k1_grouped") {
             c.k1_grouped = value != 0.0;
             c.plan.grouped = c.k1_grouped;
+        } else if (k == "k1_path") {
+            if (value != 0.0 && value != 1.0) fail(KRR_ERR_INVALID_ARGUMENT, "k1_path must be 0 (dmma) or 1 (i8)");
+            c.k1_path = int(value);
         } else if (k == "batched_rhs") {
             c.batched = value != 0.0;
         } else if (k == "exp_mode") {
@@ -1169,6 +1191,35 @@ int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale,
         KRR_CUDA(cudaMemcpyAsync(out, dout.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
                                  c.stream));
         c.sync();
+    });
+}
+
+int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int K, int N) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (K <= 0 || K % 32 != 0 || K > 256) fail(KRR_ERR_INVALID_ARGUMENT, "K must be a multiple of 32 <= 256");
+        c.set_device();
+        krr::DevMem<int8_t> a, b;
+        krr::DevMem<int32_t> o;
+        a.ensure(size_t(128 * K));
+        b.ensure(size_t(N * K));
+        o.ensure(size_t(128 * N));
+        KRR_CUDA(cudaMemcpyAsync(a.get(), A, size_t(128 * K), cudaMemcpyHostToDevice, c.stream));
+        KRR_CUDA(cudaMemcpyAsync(b.get(), B, size_t(N * K), cudaMemcpyHostToDevice, c.stream));
+        krr::i8_probe_launch(a.get(), b.get(), o.get(), K, N, c.stream);
+        KRR_CUDA(cudaMemcpyAsync(C, o.get(), sizeof(int32_t) * size_t(128 * N), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
+int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, double* cycles_per_mma) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (N != 16 && N != 32 && N != 64 && N != 128 && N != 256)
+            fail(KRR_ERR_INVALID_ARGUMENT, "N must be 16/32/64/128/256");
+        if (kbytes < 32 || kbytes % 32 != 0) fail(KRR_ERR_INVALID_ARGUMENT, "kbytes must be a multiple of 32");
+        c.set_device();
+        *cycles_per_mma = krr::i8_mma_rate(N, reps, kbytes, c.stream);
     });
 }
 

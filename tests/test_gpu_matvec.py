@@ -165,3 +165,46 @@ def test_resident_and_streaming_variants_bitwise_equal(krr, oracle, ctx, n, d):
 def test_set_option_rejects_unknown(krr, ctx):
     with pytest.raises(ValueError):
         ctx.set_option("no_such_knob", 1)
+
+
+I8_CASES = [(1, 1, 1.0), (5, 4, 0.7), (127, 3, 1.5), (300, 4, 1.7), (1000, 90, 6.0), (4097, 16, 4.0),
+            (5000, 54, 3.0), (40000, 90, 6.0), (9000, 96, 8.0)]
+
+
+@pytest.mark.parametrize("n,d,sigma", I8_CASES)
+def test_i8_slice_matvec_matches_oracle(krr, oracle, ctx, n, d, sigma):
+    """K1-I8 (tcgen05 kind::i8 Ozaki slices): same bar as the FP64 DMMA kernel."""
+    x = oracle.random_matrix(n, d, 5 + n)
+    v = oracle.random_vector(n, 7 + n)
+    ctx.set_option("k1_path", 1)
+    try:
+        op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(sigma), 1e-3, ctx=ctx)
+        got = op(v)
+    finally:
+        ctx.set_option("k1_path", 0)
+    dmma = op(v)
+    want = oracle.kernel_matvec(x, sigma, 1e-3, v)
+    assert rel(got, want) <= 1e-13, rel(got, want)
+    assert rel(got, dmma) <= 1e-13
+
+
+def test_i8_symmetry_diagonal_and_scaled_rows(krr, oracle, ctx):
+    """Exact symmetry / unit diagonal on the I8 path, with rows of very different scale
+    (per-row exponents) and duplicated rows (d2 clamp)."""
+    n, d = 300, 6
+    x = oracle.random_matrix(n, d, 2)
+    x[::7] *= 1e-3
+    x[1::11] *= 40.0
+    x[5] = x[6]
+    ctx.set_option("k1_path", 1)
+    try:
+        op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(2.0), 0.0, ctx=ctx)
+        kk = op.matmat(np.eye(n))
+        kk1 = np.column_stack([op(np.eye(n)[:, j]) for j in range(0, n, 37)])
+    finally:
+        ctx.set_option("k1_path", 0)
+    assert np.array_equal(np.diag(kk), np.ones(n))
+    assert np.array_equal(kk, kk.T)
+    want = oracle.gram_matrix(x, 2.0)
+    assert np.max(np.abs(kk - want)) <= 2e-15
+    assert kk[5, 6] == 1.0

@@ -22,10 +22,10 @@ MB_KEYS = ["dmma_tflops", "dfma_tflops", "mixed_tflops", "exp_libdevice_gevals",
            "sms", "clock_mhz", "split_warps_tflops", "imma_legacy_tops"]
 
 
-def report(n, d, ms, k1, t_set, res, exp_mode, warps, grouped=0):
+def report(n, d, ms, k1, t_set, res, exp_mode, warps, grouped=0, path=0):
     pairs = n * (n - 1) / 2
     dp = (d + 2 + 3) // 4 * 4
-    row = {"n": n, "d": d, "resident": res, "warps": warps, "grouped": grouped, "exp_mode": exp_mode, "ms_per_matvec": ms, "k1_ms": k1,
+    row = {"n": n, "d": d, "path": ["dmma", "i8"][path], "resident": res, "warps": warps, "grouped": grouped, "exp_mode": exp_mode, "ms_per_matvec": ms, "k1_ms": k1,
            "gevals_per_s": n * n / (ms * 1e-3) / 1e9,
            "unique_pairs_per_s": pairs / (k1 * 1e-3) / 1e9,
            "dot_tflops": pairs * 2 * d / (k1 * 1e-3) / 1e12,
@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--resident", type=int, default=-1, help="-1: both K1 variants")
     ap.add_argument("--warps", type=int, default=-1, help="-1: both 8 and 16")
     ap.add_argument("--grouped", type=int, default=-1, help="-1: both (resident 8-warp only)")
+    ap.add_argument("--path", type=int, default=0, help="K1 path: 0 = FP64 DMMA, 1 = tcgen05 INT8 slices, -1 both")
     ap.add_argument("--no-microbench", action="store_true")
     args = ap.parse_args()
     out = {}
@@ -63,7 +64,10 @@ def main():
                   for r in ([1, 0] if args.resident < 0 else [args.resident])
                   for gp in ([1, 0] if args.grouped < 0 and r == 1 and w == 8 else
                              [max(args.grouped, 0) if r == 1 and w == 8 else 0])]
-        for res, w, gp in combos:
+        paths = [0, 1] if args.path < 0 else [args.path]
+        combos = [(r, w, gp, pa) for pa in paths for (r, w, gp) in (combos if pa == 0 else [(1, 8, 1)])]
+        for res, w, gp, pa in combos:
+            ctx.set_option("k1_path", pa)
             ctx.set_option("k1_resident", res)
             ctx.set_option("k1_warps", w)
             ctx.set_option("k1_grouped", gp)
@@ -71,7 +75,7 @@ def main():
             tot, k1 = C.c_double(), C.c_double()
             _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))  # warm
             _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, args.steps, C.byref(tot), C.byref(k1)))
-            rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode, w, gp))
+            rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode, w, gp, pa))
     out["matvec"] = rows
     ctx.close()
     od = ROOT / "gpurun_out"
