@@ -212,9 +212,17 @@ int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale,
 /* tcgen05 kind::i8 probe: C (128 x N int32) = A (128 x K int8) . B (N x K int8)^T on
  * one CTA (K % 32 == 0, K <= 256, N in {32, 64}); host buffers, row-major. */
 int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int K, int N);
-/* cycles per back-to-back tcgen05.mma kind::i8 (M = 128, N in {32, 64, 128, 256}, K = 32),
- * operands in the no-swizzle K-major layout with `kbytes` bytes per row. */
-int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, double* cycles_per_mma);
+/* cycles per back-to-back tcgen05.mma kind::i8 (M = 128, N in {16, 32, 64, 128, 256}, K = 32),
+ * operands in the no-swizzle K-major layout with `kbytes` bytes per row.  mode: 0 SS with
+ * per-MMA descriptors, 1 SS hoisted, 2 SS hoisted + rotating accumulators, 3 TS (A in
+ * TMEM), 4 TS hoisted + rotating, 5 SS hoisted + rotating + distinct smem tiles, 6 / 7 the
+ * K1-I8 tile (N = 64, kp = 96, 36 products in 8 groups) in group-major / A-major order with
+ * reps = tiles (N, kbytes ignored); 8-11: FP64 lane-ops / clk / SM of DADD, DADD beside
+ * back-to-back MMAs, DFMA, DFMA beside MMAs (reps = iterations). */
+int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, double* cycles_per_mma);
+/* TMEM read throughput (tcgen05.ld.32x32b.x16 + wait in a loop), `warps` warps on every
+ * SM; returns bytes per clock per SM. */
+int krr_debug_tmem_ld_rate(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk);
 
 #ifdef __cplusplus
 }

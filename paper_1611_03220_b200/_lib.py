@@ -135,7 +135,8 @@ _SIGS = {
     "krr_microbench": [_vp, _vp],
     "krr_debug_gauss_exp": [_vp, _vp, _i64, _d, _i, _vp],
     "krr_debug_i8_gemm": [_vp, _vp, _vp, _vp, _i, _i],
-    "krr_debug_i8_mma_rate": [_vp, _i, _i, _i, C.POINTER(_d)],
+    "krr_debug_i8_mma_rate": [_vp, _i, _i, _i, _i, C.POINTER(_d)],
+    "krr_debug_tmem_ld_rate": [_vp, _i, _i, C.POINTER(_d)],
 }
 
 

@@ -9,28 +9,40 @@
 // Decomposition (per row i, e_i = ilogb(max_k |x_ik|) + 1, u_i = x_i 2^-e_i in (-1, 1)):
 //     u_i = sum_{p<8} A_i^(p) 2^(-7(p+1)) + r_i,   A^(p) in [-127, 127],  |r_i| < 2^-56
 // (truncation, all steps exact in fp64).  Then
-//     x_i . x_j = 2^(e_i + e_j) sum_{p,q} 2^(-7(p+q+2)) (A_i^(p) . A_j^(q))
-// keeping p + q <= 7: 36 int8 GEMM products accumulated exactly in int32 into 8 TMEM
-// groups c = p + q.  The epilogue recombines the groups in fp64 (pairs fused in int32,
-// 4 exact int->fp64 conversions, 3 FMAs), forms d2 = |x_i|^2 + |x_j|^2 - 2 x_i.x_j,
-// and continues exactly like K1 (table exp, row sums, column sums).  Dot-product error
-// <= ~2^-52 * d * 2^(e_i + e_j), the same order as an fp64 dot product's bound.
+//     x_i . x_j = 2^(e_i + e_j - 14) sum_c 2^(-7c) G_c,   G_c = sum_{p+q=c} A_i^(p) . A_j^(q)
+// keeping c = p + q <= 7: 36 int8 products accumulated exactly in int32 into 8 TMEM
+// groups.  The epilogue fuses the groups in integer arithmetic and converts twice:
+//     b_k = 128 G_2k + G_2k+1 (int32),  H = 2^14 b_0 + b_1,  Lo = 2^14 b_2 + b_3 (int64, exact)
+//     T = H + 2^-28 Lo  (one rounding)  =  2^21 sum_c 2^(-7c) G_c
+// via the 1.5 * 2^52 bit trick (IMAD.WIDE into the mantissa field + one DADD / DFMA), so
+// -2 x_i.x_j = -2^(e_i + e_j - 34) T.  The exp argument is formed directly,
+//     y = kscale d2 = sq'_i + sq'_j + |kscale| 2^(e_i - 34) 2^(e_j) T,   sq' = kscale |x|^2,
+// (the per-column power of two is an integer add on the high word), clamped to
+// [-1022 * 64, 0] and fed to the same 64-entry table exp as K1.  Dot-product error
+// <= ~2^-52 * d * 2^(e_i + e_j), the order of an fp64 dot product's own bound.
 //
-// Structure (one CTA per symmetric super-tile, 10 warps):
-//   warp 0     producer: 1-D bulk async copies (TMA engine) of the slice tiles into
-//              shared memory — the I tile (128 rows x 8 slices, resident per I) and a
-//              3-stage ring of J tiles (32 rows x 8 slices) — on mbarrier tx counts;
-//   warp 1     MMA issuer: one thread issues 36 x (kp/32) tcgen05.mma (M = 128, N = 32,
-//              K = 32) per 128 x 32 tile into one of two TMEM accumulator buffers
-//              (2 x 8 groups x 32 columns = all 512 columns) and commits to mbarriers;
-//   warps 2-9  epilogue: each thread owns one row (its TMEM lane) and 16 of the 32
-//              columns; tcgen05.ld of the 8 groups, fp64 recombination + exp, row sums
-//              in registers, column sums by a deterministic butterfly + fixed-order
-//              shared-memory reduction.  Tile q's epilogue overlaps tile q+1's MMAs.
-// Slots in `part` follow exactly the K1 rules (gauss_matvec.cu), so the finish kernel
-// is shared.  Operand layout in global memory: slice p, 8-row group, 16-byte K chunk
+// Structure (one CTA per symmetric super-tile, 10 warps, M = 128 rows x N = 64 columns):
+//   warp 0     producer: 1-D bulk async copies (TMA engine) of the slice tiles — the I
+//              tile (128 rows x 8 slices, resident per I) and a ring of J tiles
+//              (64 rows x 8 slices) — plus a ring of per-column data (sq', v, e_j << 20);
+//   warp 1     MMA issuer: one thread issues the 36 x (kp/32) tcgen05.mma of a tile group
+//              by group, c = 7 down to 0, each group into its own 64 TMEM columns
+//              (8 x 64 = all 512), committing one mbarrier per group;
+//   warps 2-9  epilogue: each thread owns one row (its TMEM lane) and 32 of the 64
+//              columns.  It drains the groups in completion order (tcgen05.ld x32) and
+//              releases each at once, so the next tile's MMAs for group c overlap this
+//              tile's remaining drain and its whole exp phase — a single TMEM buffer,
+//              pipelined per group.  Row sums stay in registers; column sums go through a
+//              per-warp shared-memory transpose and a fixed-order 4-way combine.
+// Slots in `part` follow exactly the K1 rules (gauss_matvec.cu) — one writer per
+// (slot, index) — so the finish kernel is shared; column sums are accumulated in the
+// CTA's own slot in global memory (owner thread per column, program order), which
+// frees the shared memory the 96-byte-row tiles need.
+// Operand layout in global memory: slice p, 8-row group, 16-byte K chunk
 // ([p][n_pad/8][kp/16][8][16]), so any 8-aligned row range is one contiguous block that
 // is directly the canonical no-swizzle K-major UMMA layout (LBO = 128 B, SBO = 8 kp B).
+#include <vector>
+
 #include "common.cuh"
 #include "gauss_exp.cuh"
 #include "kernels.cuh"
@@ -43,57 +55,147 @@ namespace {
 constexpr int P = 8;      // slices
 constexpr int NGRP = 8;   // groups c = p + q in [0, 7]
 constexpr int TI = 128;   // I tile rows (MMA M)
-constexpr int TJ = 32;    // J tile columns (MMA N)
-constexpr int NST = 3;    // J-tile stages
-constexpr int NEPI = 8;   // epilogue warps
+constexpr int TJ = 64;    // J tile columns (MMA N)
+constexpr int NCD = 4;    // column-data stages
+constexpr int NEPI = 8;   // epilogue warps (2 per TMEM lane quarter)
+constexpr int CPT = 32;   // columns per epilogue thread
 constexpr int NTHR = 32 * (2 + NEPI);
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int KP_MAX = 96;
+constexpr int SCR_LD = 34;  // transpose scratch row stride (doubles): conflict-free both ways
+constexpr int CD_BYTES = TJ * 8 * 3;  // sq', v, 2^e_j
+
+template <int KPT>
+struct Cfg {
+    static constexpr int NSTB = KPT >= 96 ? 2 : 3;  // J-tile stages
+    static constexpr int CH = KPT >= 96 ? 8 : 16;   // transpose chunk (columns)
+    static constexpr size_t A_BYTES = size_t(P) * TI * KPT;
+    static constexpr size_t B_BYTES = size_t(P) * TJ * KPT;
+    static constexpr size_t OFF_B = A_BYTES;
+    static constexpr size_t OFF_CD = OFF_B + NSTB * B_BYTES;
+    static constexpr size_t OFF_SCR = OFF_CD + NCD * CD_BYTES;
+    static constexpr size_t OFF_COLSCR = OFF_SCR + size_t(NEPI) * CH * SCR_LD * 8;
+    static constexpr size_t OFF_ROWBUF = OFF_COLSCR + 2 * 4 * TJ * 8;
+    static constexpr size_t OFF_TAB = OFF_ROWBUF + 2 * TI * 8;
+    static constexpr size_t OFF_BARS = OFF_TAB + 64 * 8;
+    static constexpr int NBARS = 2 + 2 * NSTB + 2 * NCD + 2 * NGRP;
+    static constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
+};
 
 struct I8Args {
     const uint8_t* __restrict__ S;
-    const int* __restrict__ ex;
-    const double* __restrict__ sq;
+    const int* __restrict__ ex;      // e_i
+    const double* __restrict__ cpow; // 2^e_j
+    const double* __restrict__ sqs;  // kscale |x_j|^2
     const double* __restrict__ v;
     double* __restrict__ part;
     const int2* __restrict__ tiles;
     const double* __restrict__ exp_tab;
     int64_t n_pad;
-    int kp;
     int st;
+    int debug;  // profiling only: bit 0 skips the MMAs, bit 1 the exp phase (results invalid)
     ExpConsts ec;
 };
 
-__device__ __forceinline__ double i2d_exact(int32_t b) {
-    // 1.5 * 2^52 + (b + 2^31) built bitwise, minus the same constant: exact for all int32
-    return __hiloint2double(0x43380000, int(uint32_t(b) ^ 0x80000000u)) - 6755401588539392.0;
-}
-
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NEPI * 32) : "memory"); }
 
-size_t i8_smem_bytes(int kp, int st) {
-    return size_t(P) * TI * kp + size_t(NST) * P * TJ * kp + sizeof(double) * (size_t(st) + 2 * TI + 2 * 2 * 4 * 16 + 64) +
-           sizeof(uint64_t) * 16 + 16;
+// 64-bit pattern {lo = b ^ 2^31, hi = 0x43380000} + a * 2^14 (signed): the bits of the
+// double 1.5 * 2^52 + 2^31 + (2^14 a + b), exact for |2^14 a + b| < 2^51.
+__device__ __forceinline__ double magic_pack(int32_t a, int32_t b) {
+    double r;
+    asm("{\n\t.reg .b64 base, prod;\n\t"
+        "mov.b64 base, {%2, %3};\n\t"
+        "mad.wide.s32 prod, %1, 16384, base;\n\t"
+        "mov.b64 %0, prod;\n\t}\n"
+        : "=d"(r)
+        : "r"(a), "r"(int(uint32_t(b) ^ 0x80000000u)), "r"(0x43380000));
+    return r;
+}
+// 1.5 * 2^52 + 2^31 and that constant times (1 + 2^-28), both exact integers < 2^53
+constexpr double M2 = 6755401588539392.0 + 25165832.0;  // M1 = 1.5 * 2^52 + 2^31, M2 = M1 (1 + 2^-28)
+
+template <int KPT, bool MASK>
+__device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Args& A, const double* __restrict__ tab,
+                                          const double* __restrict__ cd_sq, const double* __restrict__ cd_v,
+                                          const double* __restrict__ cd_c, double* __restrict__ scr,
+                                          double* __restrict__ colscr_q, double nsi, double sqs_i,
+                                          double v_i, double& rowacc, int lane, int colOff, int mask_row) {
+    using C = Cfg<KPT>;
+    constexpr int CH = C::CH;
+    const ExpConsts& ec = A.ec;
+    const double shifter = 6755399441055744.0;  // 1.5 * 2^52
+#pragma unroll
+    for (int ch = 0; ch < CPT / CH; ++ch) {
+        double colv[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const int cl = colOff + ch * CH + k;  // column within the 64-wide tile
+            const double sqj = cd_sq[cl];
+            const double vj = cd_v[cl];
+            double y = fma(T[ch * CH + k], nsi * cd_c[cl], sqs_i + sqj);
+            // y <= 0 (d2 >= 0): y > 0 (rounding, near-duplicate rows) has a non-negative
+            // high word; clamping it to 0 leaves a positive denormal, whose exp is 1 exactly.
+            y = __hiloint2double(min(__double2hiint(y), 0), __double2loint(y));
+            const double t2 = y + shifter;
+            const double kd = t2 - shifter;
+            const double f = y - kd;
+            double q = fma(f, ec.a5, ec.a4);
+            q = fma(q, f, ec.a3);
+            q = fma(q, f, ec.a2);
+            q = fma(q, f, ec.a1);
+            q = q * f;
+            // k >= -1022 * 64 keeps 2^(k/64) normal (e >= ~2^-1022 instead of underflowing)
+            const int kk = max(__double2loint(t2), -65408);
+            const double tj = tab[kk & 63];
+            const double ts = __hiloint2double(__double2hiint(tj) + (kk >> 6) * (1 << 20), __double2loint(tj));
+            double e = fma(ts, q, ts);
+            if constexpr (MASK) e = (cl > mask_row) ? e : 0.0;
+            rowacc = fma(e, vj, rowacc);
+            colv[k] = e * v_i;
+        }
+        // column sums over the warp's 32 rows: transpose through shared memory
+#pragma unroll
+        for (int k = 0; k < CH; ++k) scr[k * SCR_LD + lane] = colv[k];
+        __syncwarp();
+        const int c = lane % CH, rb = (lane / CH) * CH;
+        const double* src = scr + c * SCR_LD + rb;
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < CH; m += 2) {
+            const double2 pr = *reinterpret_cast<const double2*>(src + m);
+            acc += pr.x;
+            acc += pr.y;
+        }
+#pragma unroll
+        for (int o = CH; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane < CH) colscr_q[colOff + ch * CH + lane] = acc;
+        __syncwarp();
+    }
 }
 
 template <int KPT>
 __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A) {
-    extern __shared__ __align__(1024) uint8_t smem[];
+    using C = Cfg<KPT>;
     constexpr int kp = KPT;
+    constexpr int NSTB = C::NSTB;
+    extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
-    uint8_t* sB = sA + P * TI * kp;
-    double* colacc = reinterpret_cast<double*>(sB + NST * P * TJ * kp);
-    double* rowbuf = colacc + A.st;
-    double* colscr = rowbuf + 2 * TI;        // [2 buffers][2 halves][4 quarters][16]
-    double* tab = colscr + 2 * 2 * 4 * 16;  // 64
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 64);
+    uint8_t* sB = smem + C::OFF_B;
+    uint8_t* sCD = smem + C::OFF_CD;
+    double* scr_all = reinterpret_cast<double*>(smem + C::OFF_SCR);
+    double* colscr = reinterpret_cast<double*>(smem + C::OFF_COLSCR);  // [2][4 quarters][64]
+    double* rowbuf = reinterpret_cast<double*>(smem + C::OFF_ROWBUF);  // [2 halves][128]
+    double* tab = reinterpret_cast<double*>(smem + C::OFF_TAB);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BARS);
     uint64_t* a_full = bars;
     uint64_t* a_empty = bars + 1;
     uint64_t* b_full = bars + 2;
-    uint64_t* b_empty = b_full + NST;
-    uint64_t* t_full = b_empty + NST;
-    uint64_t* t_empty = t_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+    uint64_t* b_empty = b_full + NSTB;
+    uint64_t* cd_full = b_empty + NSTB;
+    uint64_t* cd_empty = cd_full + NCD;
+    uint64_t* g_full = cd_empty + NCD;
+    uint64_t* g_empty = g_full + NGRP;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_empty + NGRP);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int2 tile = A.tiles[blockIdx.x];
@@ -108,17 +210,20 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
     if (tid == 0) {
         tc::mbar_init(a_full, 1);
         tc::mbar_init(a_empty, 1);
-        for (int s = 0; s < NST; ++s) {
+        for (int s = 0; s < NSTB; ++s) {
             tc::mbar_init(b_full + s, 1);
             tc::mbar_init(b_empty + s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(t_full + b, 1);
-            tc::mbar_init(t_empty + b, NEPI);
+        for (int s = 0; s < NCD; ++s) {
+            tc::mbar_init(cd_full + s, 1);
+            tc::mbar_init(cd_empty + s, NEPI);
+        }
+        for (int g = 0; g < NGRP; ++g) {
+            tc::mbar_init(g_full + g, 1);
+            tc::mbar_init(g_empty + g, NEPI);
         }
         tc::mbar_fence_init();
     }
-    for (int i = tid; i < A.st; i += NTHR) colacc[i] = 0.0;
     if (tid < 64) tab[tid] = A.exp_tab[tid];
     if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
     tc::fence_before();
@@ -131,19 +236,26 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         if (lane == 0) {
             int bq = 0;
             for (int it = 0; it < nTI; ++it) {
-                if (it > 0) tc::mbar_wait(a_empty, uint32_t((it - 1) & 1));
-                tc::mbar_arrive_expect_tx(a_full, uint32_t(P * TI * kp));
+                if (it > 0) tc::mbar_wait_sleep(a_empty, uint32_t((it - 1) & 1));
+                tc::mbar_arrive_expect_tx(a_full, uint32_t(C::A_BYTES));
                 const int64_t r0 = rowBase + int64_t(it) * TI;
                 for (int p = 0; p < P; ++p)
                     tc::bulk_g2s(sA + p * TI * kp, A.S + int64_t(p) * A.n_pad * kp + r0 * kp, uint32_t(TI * kp), a_full);
                 for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
-                    const int s = bq % NST;
-                    if (bq >= NST) tc::mbar_wait(b_empty + s, uint32_t(((bq / NST) - 1) & 1));
-                    tc::mbar_arrive_expect_tx(b_full + s, uint32_t(P * TJ * kp));
+                    const int s = bq % NSTB;
+                    if (bq >= NSTB) tc::mbar_wait_sleep(b_empty + s, uint32_t(((bq / NSTB) - 1) & 1));
+                    tc::mbar_arrive_expect_tx(b_full + s, uint32_t(C::B_BYTES));
                     const int64_t c0 = colBase + int64_t(jt) * TJ;
                     for (int q = 0; q < P; ++q)
-                        tc::bulk_g2s(sB + (s * P + q) * TJ * kp, A.S + int64_t(q) * A.n_pad * kp + c0 * kp,
+                        tc::bulk_g2s(sB + s * C::B_BYTES + q * TJ * kp, A.S + int64_t(q) * A.n_pad * kp + c0 * kp,
                                      uint32_t(TJ * kp), b_full + s);
+                    const int cs = bq % NCD;
+                    if (bq >= NCD) tc::mbar_wait_sleep(cd_empty + cs, uint32_t(((bq / NCD) - 1) & 1));
+                    tc::mbar_arrive_expect_tx(cd_full + cs, uint32_t(CD_BYTES));
+                    uint8_t* cd = sCD + cs * CD_BYTES;
+                    tc::bulk_g2s(cd, A.sqs + c0, TJ * 8, cd_full + cs);
+                    tc::bulk_g2s(cd + TJ * 8, A.v + c0, TJ * 8, cd_full + cs);
+                    tc::bulk_g2s(cd + TJ * 16, A.cpow + c0, TJ * 8, cd_full + cs);
                 }
             }
         }
@@ -152,33 +264,36 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_i8(TI, TJ);
             const uint32_t aBase = tc::smem_u32(sA);
-            int bq = 0, tq = 0;
+            int bq = 0;
             for (int it = 0; it < nTI; ++it) {
-                tc::mbar_wait(a_full, uint32_t(it & 1));
+                tc::mbar_wait_sleep(a_full, uint32_t(it & 1));
                 tc::fence_after();
-                for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq, ++tq) {
-                    const int s = bq % NST, buf = tq & 1;
-                    if (tq >= 2) tc::mbar_wait(t_empty + buf, uint32_t(((tq >> 1) - 1) & 1));
-                    tc::mbar_wait(b_full + s, uint32_t((bq / NST) & 1));
+                for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
+                    const int s = bq % NSTB;
+                    tc::mbar_wait_sleep(b_full + s, uint32_t((bq / NSTB) & 1));
                     tc::fence_after();
                     // Descriptors differ only in the start-address field (16-byte units):
-                    // build the two bases once and add compile-time offsets, so the
-                    // fully unrolled 36 x ksteps issue sequence is pure uniform adds.
+                    // two bases plus compile-time offsets in the fully unrolled sequence.
                     const uint64_t dA0 = tc::smem_desc(aBase, 128, sbo);
-                    const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB + s * P * TJ * kp), 128, sbo);
-                    const uint32_t dcol0 = tmem_base + uint32_t(buf * NGRP * TJ);
+                    const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB + s * C::B_BYTES), 128, sbo);
 #pragma unroll
-                    for (int p = 0; p < P; ++p)
+                    for (int c = NGRP - 1; c >= 0; --c) {
+                        if (bq > 0) {
+                            tc::mbar_wait_sleep(g_empty + c, uint32_t((bq - 1) & 1));
+                            tc::fence_after();
+                        }
+                        if (!(A.debug & 1))
 #pragma unroll
-                        for (int q = 0; q + p < NGRP; ++q)
+                        for (int p = 0; p <= c; ++p)
 #pragma unroll
                             for (int ks = 0; ks < ksteps; ++ks)
-                                tc::mma_i8(dcol0 + uint32_t((p + q) * TJ),
+                                tc::mma_i8(tmem_base + uint32_t(c * TJ),
                                            dA0 + uint64_t((p * TI * kp + ks * 256) >> 4),
-                                           dB0 + uint64_t((q * TJ * kp + ks * 256) >> 4), idesc,
+                                           dB0 + uint64_t(((c - p) * TJ * kp + ks * 256) >> 4), idesc,
                                            (p == 0 && ks == 0) ? 0u : 1u);
+                        tc::mma_commit(g_full + c);
+                    }
                     tc::mma_commit(b_empty + s);
-                    tc::mma_commit(t_full + buf);
                 }
                 tc::mma_commit(a_empty);
             }
@@ -187,125 +302,117 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         // ------------------------------------------------------------ epilogue
         const int ew = warp - 2;            // 0..7
         const int quarter = warp & 3;       // TMEM lane quarter this warp may access
-        const int half = ew >> 2;           // which 16 of the 32 columns
+        const int half = ew >> 2;           // which 32 of the 64 columns
         const int etid = ew * 32 + lane;    // 0..255
         const int row = quarter * 32 + lane;
-        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+        const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(half * CPT);
+        double* scr = scr_all + ew * C::CH * SCR_LD;
+        const double kabs = -A.ec.kscale;
         int tq = 0;
         for (int it = 0; it < nTI; ++it) {
             const int64_t gi = rowBase + int64_t(it) * TI + row;
-            const int ei = A.ex[gi];
-            const double sqi = A.sq[gi];
-            const double vi = A.v[gi];
+            const double sqs_i = A.sqs[gi];
+            const double v_i = A.v[gi];
+            const double nsi = scalbn(kabs, A.ex[gi] - 34);  // |kscale| 2^(e_i - 34)
             double rowacc = 0.0;
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++tq) {
-                const int buf = tq & 1;
-                const bool dmask = diag && jt < (it + 1) * (TI / TJ);
-                tc::mbar_wait(t_full + buf, uint32_t((tq >> 1) & 1));
-                tc::fence_after();
-                const int64_t jbase = colBase + int64_t(jt) * TJ + half * 16;
-                double colv[16];
+                const uint32_t ph = uint32_t(tq & 1);
+                // prefetch this column's running sum (owner threads; same thread every pass)
+                double* cdst = A.part + int64_t(sa) * A.n_pad + colBase + int64_t(jt) * TJ + etid;
+                double cprev = 0.0;
+                if (etid < TJ && it > 0) cprev = *cdst;
+
+                // ---- drain the 8 groups in MMA completion order (7 -> 0) two at a time,
+                // 16 columns per tcgen05.ld (register pressure), releasing each pair at once
+                int32_t bint[CPT];
+                double lo[CPT], T[CPT];
+                auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
+                    tc::mbar_wait(g_full + ca + 1, ph);
+                    tc::mbar_wait(g_full + ca, ph);
+                    tc::fence_after();
 #pragma unroll
-                for (int hb = 0; hb < 2; ++hb) {
-                    uint32_t acc[NGRP][8];
+                    for (int hh = 0; hh < CPT / 16; ++hh) {
+                        uint32_t gl[16], gh[16];
+                        tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ + hh * 16), gl);
+                        tc::tmem_ld16(taddr + uint32_t(ca * TJ + hh * 16), gh);
+                        tc::tmem_wait_ld();
 #pragma unroll
-                    for (int c = 0; c < NGRP; ++c)
-                        tc::tmem_ld8(tmem_base + lane_addr + uint32_t(buf * NGRP * TJ + c * TJ + half * 16 + hb * 8),
-                                     acc[c]);
-                    tc::tmem_wait_ld();
-                    if (hb == 1) {
-                        // both halves of this thread's columns are in registers: release TMEM
-                        tc::fence_before();
-                        __syncwarp();
-                        if (lane == 0) tc::mbar_arrive(t_empty + buf);
+                        for (int k = 0; k < 16; ++k) fn(hh * 16 + k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
                     }
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        const int64_t j = jbase + hb * 8 + jj;
-                        const int32_t b0 = int32_t(acc[0][jj]) * 128 + int32_t(acc[1][jj]);
-                        const int32_t b1 = int32_t(acc[2][jj]) * 128 + int32_t(acc[3][jj]);
-                        const int32_t b2 = int32_t(acc[4][jj]) * 128 + int32_t(acc[5][jj]);
-                        const int32_t b3 = int32_t(acc[6][jj]) * 128 + int32_t(acc[7][jj]);
-                        double t = i2d_exact(b3);
-                        t = fma(t, 0x1p-14, i2d_exact(b2));
-                        t = fma(t, 0x1p-14, i2d_exact(b1));
-                        t = fma(t, 0x1p-14, i2d_exact(b0));
-                        // -2 x_i.x_j = t * (-2^(e_i + e_j - 20))
-                        const int be = ei + A.ex[j] + (1023 - 20);
-                        const double nscale = __hiloint2double(int(0x80000000u | (uint32_t(be) << 20)), 0);
-                        const double d2 = fma(t, nscale, sqi + A.sq[j]);
-                        double e = gauss_exp_table(d2, A.ec, tab);
-                        if (dmask && j <= gi) e = 0.0;
-                        rowacc = fma(e, A.v[j], rowacc);
-                        colv[hb * 8 + jj] = e * vi;
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc::mbar_arrive(g_empty + ca + 1);
+                        tc::mbar_arrive(g_empty + ca);
                     }
-                }
-                // column sums over the warp's 32 rows: butterfly reduce-scatter, then lanes
-                // (2c, 2c+1) hold column c's sum.
-                double w8[8];
+                };
+                stage(6, [&](int k, int32_t b) { bint[k] = b; });                    // b3
+                stage(4, [&](int k, int32_t b) { lo[k] = magic_pack(b, bint[k]); });  // M1 + Lo
+                stage(2, [&](int k, int32_t b) { bint[k] = b; });                    // b1
+                stage(0, [&](int k, int32_t b) {
+                    T[k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
+                });
+
+                // ---- exp, row sums, column sums
+                const int cs = tq % NCD;
+                tc::mbar_wait(cd_full + cs, uint32_t((tq / NCD) & 1));
+                const uint8_t* cd = sCD + cs * CD_BYTES;
+                const double* cd_sq = reinterpret_cast<const double*>(cd);
+                const double* cd_v = reinterpret_cast<const double*>(cd + TJ * 8);
+                const double* cd_c = reinterpret_cast<const double*>(cd + TJ * 16);
+                double* colscr_q = colscr + ((tq & 1) * 4 + quarter) * TJ;
+                const int colOff = half * CPT;
+                const bool masked = diag && jt < (it + 1) * (TI / TJ);
+                if (A.debug & 2) {
+                    double z = 0.0;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double mine = (lane & 16) ? colv[8 + k] : colv[k];
-                    const double other = (lane & 16) ? colv[k] : colv[8 + k];
-                    w8[k] = mine + __shfl_xor_sync(0xffffffffu, other, 16);
+                    for (int k = 0; k < CPT; ++k) z += T[k];
+                    rowacc += z;
+                } else if (masked) {
+                    // diagonal block: keep j > i (local column index vs local row index)
+                    const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
+                    exp_phase<KPT, true>(T, A, tab, cd_sq, cd_v, cd_c, scr, colscr_q, nsi, sqs_i, v_i,
+                                         rowacc, lane, colOff, mask_row);
+                } else {
+                    exp_phase<KPT, false>(T, A, tab, cd_sq, cd_v, cd_c, scr, colscr_q, nsi, sqs_i, v_i,
+                                          rowacc, lane, colOff, 0);
                 }
-                double w4[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const double mine = (lane & 8) ? w8[4 + k] : w8[k];
-                    const double other = (lane & 8) ? w8[k] : w8[4 + k];
-                    w4[k] = mine + __shfl_xor_sync(0xffffffffu, other, 8);
-                }
-                double w2[2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const double mine = (lane & 4) ? w4[2 + k] : w4[k];
-                    const double other = (lane & 4) ? w4[k] : w4[2 + k];
-                    w2[k] = mine + __shfl_xor_sync(0xffffffffu, other, 4);
-                }
-                double w1;
-                {
-                    const double mine = (lane & 2) ? w2[1] : w2[0];
-                    const double other = (lane & 2) ? w2[0] : w2[1];
-                    w1 = mine + __shfl_xor_sync(0xffffffffu, other, 2);
-                }
-                w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
-                const int cb = tq & 1;
-                if ((lane & 1) == 0) colscr[((cb * 2 + half) * 4 + quarter) * 16 + (lane >> 1)] = w1;
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(cd_empty + cs);
                 epi_bar();
                 if (etid < TJ) {
-                    const int h = etid >> 4, c16 = etid & 15;
-                    const double* cs = colscr + (cb * 2 + h) * 4 * 16 + c16;
-                    colacc[jt * TJ + etid] += ((cs[0] + cs[16]) + cs[32]) + cs[48];
+                    const double* q4 = colscr + (tq & 1) * 4 * TJ + etid;
+                    const double s4 = ((q4[0] + q4[TJ]) + q4[2 * TJ]) + q4[3 * TJ];
+                    *cdst = cprev + s4;
                 }
             }
             // row partials of this I tile: combine the two column halves in fixed order
             rowbuf[half * TI + row] = rowacc;
             epi_bar();
-            if (etid < TI) {
-                const double r = rowbuf[etid] + rowbuf[TI + etid];
-                if (diag) {
-                    colacc[it * TI + etid] += r;
-                } else {
-                    A.part[int64_t(sb) * A.n_pad + rowBase + int64_t(it) * TI + etid] = r;
+            if (diag) {
+                // same slot and index range as the column sums: the column owner adds
+                if (etid < TJ) {
+#pragma unroll
+                    for (int h = 0; h < TI / TJ; ++h) {
+                        const int r = h * TJ + etid;
+                        double* dst = A.part + int64_t(sa) * A.n_pad + rowBase + int64_t(it) * TI + r;
+                        *dst = *dst + (rowbuf[r] + rowbuf[TI + r]);
+                    }
                 }
+            } else if (etid < TI) {
+                A.part[int64_t(sb) * A.n_pad + rowBase + int64_t(it) * TI + etid] = rowbuf[etid] + rowbuf[TI + etid];
             }
-            epi_bar();
         }
     }
 
     tc::fence_before();
     __syncthreads();
-    tc::fence_after();
-    // column sums (diag: combined row + column sums) -> this CTA's slot
-    double* dst = A.part + int64_t(sa) * A.n_pad + (diag ? rowBase : colBase);
-    for (int i = tid; i < A.st; i += NTHR) dst[i] = colacc[i];
     if (warp == 1) tc::tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
 // ---- operand preparation
 __global__ void row_exponent_kernel(const double* __restrict__ X, int64_t n, int64_t d, int64_t n_pad,
-                                    int* __restrict__ ex) {
+                                    int* __restrict__ ex, double* __restrict__ cpow) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_pad; i += warps) {
@@ -314,7 +421,11 @@ __global__ void row_exponent_kernel(const double* __restrict__ X, int64_t n, int
             for (int64_t k = lane; k < d; k += 32) m = fmax(m, fabs(X[i * d + k]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) ex[i] = m > 0.0 ? ilogb(m) + 1 : 0;
+        if (lane == 0) {
+            const int e = m > 0.0 ? ilogb(m) + 1 : 0;
+            ex[i] = e;
+            cpow[i] = scalbn(1.0, e);
+        }
     }
 }
 
@@ -337,58 +448,80 @@ __global__ void slice_kernel(const double* __restrict__ X, int64_t n, int64_t d,
     }
 }
 
-__global__ void copy_sq_kernel(const double* __restrict__ L, int64_t n_pad, int dp, int d, double* __restrict__ sq) {
+// sq'_i = kscale |x_i|^2 (|x_i|^2 from the L operand's column d)
+__global__ void scaled_sq_kernel(const double* __restrict__ L, int64_t n_pad, int dp, int d, double kscale,
+                                 double* __restrict__ sqs) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_pad; i += int64_t(gridDim.x) * blockDim.x)
-        sq[i] = L[i * dp + d];
+        sqs[i] = kscale * L[i * dp + d];
+}
+
+template <int KPT>
+void launch_kp(const I8Args& a, int64_t num_tiles, cudaStream_t stream) {
+    constexpr size_t smem = Cfg<KPT>::SMEM;
+    static_assert(smem <= 227 * 1024, "K1-I8 shared memory");
+    KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_i8_kernel<KPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
+    gauss_matvec_i8_kernel<KPT><<<unsigned(num_tiles), NTHR, smem, stream>>>(a);
 }
 
 }  // namespace
 
 bool i8_supported(int64_t d, int st) {
     const int kp = int((d + 31) / 32 * 32);
-    return kp <= KP_MAX && st % TI == 0 && i8_smem_bytes(kp, st) <= 227 * 1024;
+    return kp <= KP_MAX && st % TI == 0 && st >= TI;
 }
 
 int i8_kp(int64_t d) { return int((d + 31) / 32 * 32); }
 
-void i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp, uint8_t* S,
-                       int* ex, double* sq, cudaStream_t stream) {
+bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp,
+                       double kscale, uint8_t* S, int* ex, double* cpow, double* sqs, cudaStream_t stream) {
     const int kp = i8_kp(d);
     const unsigned wblocks = unsigned(std::min<int64_t>((n_pad + 7) / 8, 148 * 16));
-    row_exponent_kernel<<<wblocks, 256, 0, stream>>>(X, n, d, n_pad, ex);
+    row_exponent_kernel<<<wblocks, 256, 0, stream>>>(X, n, d, n_pad, ex, cpow);
     KRR_LAUNCH_CHECK();
     const int64_t total = n_pad * kp;
     slice_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(X, n, d, n_pad, kp,
                                                                                                  ex, S);
     KRR_LAUNCH_CHECK();
-    copy_sq_kernel<<<unsigned(std::min<int64_t>((n_pad + 255) / 256, 148 * 8)), 256, 0, stream>>>(L, n_pad, dp,
-                                                                                                  int(d), sq);
+    scaled_sq_kernel<<<unsigned(std::min<int64_t>((n_pad + 255) / 256, 148 * 8)), 256, 0, stream>>>(
+        L, n_pad, dp, int(d), kscale, sqs);
     KRR_LAUNCH_CHECK();
+    // exponent range: |kscale| 2^(e_i + e_j - 34) must stay a normal double
+    std::vector<int> h(static_cast<size_t>(n_pad));
+    KRR_CUDA(cudaMemcpyAsync(h.data(), ex, sizeof(int) * size_t(n_pad), cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaStreamSynchronize(stream));
+    int lo = 0, hi = 0;
+    for (int e : h) {
+        lo = std::min(lo, e);
+        hi = std::max(hi, e);
+    }
+    // (1) |kscale| 2^(e_i + e_j - 34) stays a normal double;
+    // (2) |y| = |kscale| d2 <= |kscale| 4 d 2^(2 e_max) < 2^50 (the 1.5 * 2^52 rounding shifter)
+    const int ek = std::ilogb(-kscale);
+    const double ymax = -kscale * 4.0 * double(d) * std::ldexp(1.0, 2 * hi);
+    return ek + 2 * lo - 34 > -1000 && ek + 2 * hi - 34 < 1000 && ymax < std::ldexp(1.0, 50);
 }
 
-void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const double* sq,
-                            const double* v, double* part, int kp, cudaStream_t stream) {
+void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const double* cpow,
+                            const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
+                            int debug) {
     if (p.num_tiles == 0) return;
     I8Args a;
     a.S = S;
     a.ex = ex;
-    a.sq = sq;
+    a.cpow = cpow;
+    a.sqs = sqs;
     a.v = v;
     a.part = part;
     a.tiles = p.tiles;
     a.exp_tab = p.exp_tab;
     a.n_pad = p.n_pad;
-    a.kp = kp;
     a.st = p.st;
     a.ec = p.ec;
-    const size_t smem = i8_smem_bytes(kp, p.st);
-    auto run = [&](auto kern) {
-        KRR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<unsigned(p.num_tiles), NTHR, smem, stream>>>(a);
-    };
-    if (kp == 32) run(gauss_matvec_i8_kernel<32>);
-    else if (kp == 64) run(gauss_matvec_i8_kernel<64>);
-    else if (kp == 96) run(gauss_matvec_i8_kernel<96>);
+    a.debug = debug;
+    if (kp == 32) launch_kp<32>(a, p.num_tiles, stream);
+    else if (kp == 64) launch_kp<64>(a, p.num_tiles, stream);
+    else if (kp == 96) launch_kp<96>(a, p.num_tiles, stream);
     else fail(KRR_ERR_INVALID_ARGUMENT, "K1-I8: kp must be 32, 64 or 96");
     KRR_LAUNCH_CHECK();
 }

@@ -42,10 +42,13 @@ void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const do
 // K1-I8: tcgen05 kind::i8 slice path (gauss_matvec_i8.cu).  Supported for d <= 96.
 bool i8_supported(int64_t d, int st);
 int i8_kp(int64_t d);
-void i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp, uint8_t* S,
-                       int* ex, double* sq, cudaStream_t stream);
-void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const double* sq,
-                            const double* v, double* part, int kp, cudaStream_t stream);
+// Builds the slices S, row exponents ex (and 2^ex), sq' = kscale |x|^2; returns false
+// when the data's exponent range would leave the range the fused epilogue handles.
+bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp,
+                       double kscale, uint8_t* S, int* ex, double* cpow, double* sqs, cudaStream_t stream);
+void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const double* cpow,
+                            const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
+                            int debug = 0);
 
 // Build L / R operands from X (n x d) on the device; rows >= n and cols >= d+2 zeroed.
 void build_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, int dp,
@@ -129,7 +132,10 @@ void precond_z_launch(const double* B, int64_t n, int64_t s, const double* W, co
 // one-CTA tcgen05 kind::i8 GEMM probe: C (128 x N) = A (128 x K) B (N x K)^T, K % 32 == 0
 void i8_probe_launch(const int8_t* A, const int8_t* B, int32_t* C, int K, int N, cudaStream_t stream);
 // cycles per tcgen05.mma kind::i8 (M = 128, N, K = 32), one CTA per SM, back-to-back
-double i8_mma_rate(int N, int reps, int kbytes, cudaStream_t stream);
+double i8_mma_rate(int N, int reps, int kbytes, int mode, cudaStream_t stream);
+double tmem_ld_rate(int warps, int reps, cudaStream_t stream);
+double i8_tile_order_rate(int order, int tiles, cudaStream_t stream);
+double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream);
 void debug_exp_launch(const double* d2, int64_t n, const ExpConsts& ec, const double* tab,
                       int mode, double* out, cudaStream_t stream);
 // results: see krr_microbench in include/krr_b200.h

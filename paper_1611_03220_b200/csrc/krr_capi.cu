@@ -124,11 +124,12 @@ struct Ctx {
     DevMem<uint8_t> owned;
     // K1-I8 operands (int8 slices, row exponents, |x|^2)
     int k1_path = 0;  // 0 = FP64 DMMA, 1 = tcgen05 INT8 slices
+    int i8_debug = 0; // profiling knob for K1-I8 (bit 0: skip MMAs, bit 1: skip exp phase)
     bool i8_ready = false;
     int kp8 = 0;
     DevMem<uint8_t> S8;
     DevMem<int> ex8;
-    DevMem<double> sq8;
+    DevMem<double> sq8, cpow8;
 
     // PCG vectors (n_pad each) and reduction scratch
     DevMem<double> vin, vout, vx, vr, vz, vp, vap, vy, red, scal, mat_a, mat_b;
@@ -171,7 +172,8 @@ void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t
                 cudaEvent_t k1b = nullptr) {
     if (k1a) KRR_CUDA(cudaEventRecord(k1a, c.stream));
     if (c.k1_path == 1 && c.i8_ready)
-        gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.sq8.get(), v, c.part.get(), c.kp8, c.stream);
+        gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.cpow8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
+                               c.stream, c.i8_debug);
     else
         gauss_matvec_launch(c.plan, v, c.part.get(), c.exp_mode, c.stream);
     if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
@@ -239,9 +241,10 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
         c.kp8 = i8_kp(d);
         c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
         c.ex8.ensure(size_t(n_pad));
+        c.cpow8.ensure(size_t(n_pad));
         c.sq8.ensure(size_t(n_pad));
-        i8_prepare_launch(c.X.get(), n, d, n_pad, c.L.get(), dp, c.S8.get(), c.ex8.get(), c.sq8.get(), c.stream);
-        c.i8_ready = true;
+        c.i8_ready = i8_prepare_launch(c.X.get(), n, d, n_pad, c.L.get(), dp, p.ec.kscale, c.S8.get(), c.ex8.get(),
+                                       c.cpow8.get(), c.sq8.get(), c.stream);
     }
     p.resident = c.k1_resident;
     p.warps16 = c.k1_warps16;
@@ -815,6 +818,8 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
         } else if (k == "k1_grouped") {
             c.k1_grouped = value != 0.0;
             c.plan.grouped = c.k1_grouped;
+        } else if (k == "i8_debug") {
+            c.i8_debug = int(value);
         } else if (k == "k1_path") {
             if (value != 0.0 && value != 1.0) fail(KRR_ERR_INVALID_ARGUMENT, "k1_path must be 0 (dmma) or 1 (i8)");
             c.k1_path = int(value);
@@ -1212,14 +1217,35 @@ int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C
     });
 }
 
-int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, double* cycles_per_mma) {
+int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, double* cycles_per_mma) {
     return guard([&] {
         Ctx& c = *krr::as_ctx(ctx);
         if (N != 16 && N != 32 && N != 64 && N != 128 && N != 256)
             fail(KRR_ERR_INVALID_ARGUMENT, "N must be 16/32/64/128/256");
         if (kbytes < 32 || kbytes % 32 != 0) fail(KRR_ERR_INVALID_ARGUMENT, "kbytes must be a multiple of 32");
+        if (mode >= 8 && mode <= 11) {  // FP64 ops/clk/SM: 8 DADD, 9 DADD + MMA, 10 DFMA, 11 DFMA + MMA
+            c.set_device();
+            *cycles_per_mma = krr::fp64_under_mma((mode - 8) >> 1, (mode - 8) & 1, std::max(64, reps), c.stream);
+            return;
+        }
+        if (mode == 6 || mode == 7) {  // in-situ K1-I8 tile order (N = 64, kp = 96), reps = tiles
+            c.set_device();
+            *cycles_per_mma = krr::i8_tile_order_rate(mode - 6, std::max(1, reps), c.stream);
+            return;
+        }
+        if (reps < 8 || mode < 0 || mode > 5) fail(KRR_ERR_INVALID_ARGUMENT, "reps >= 8, mode in [0, 7]");
+        if (size_t(128 + N) * size_t(kbytes) > 200 * 1024) fail(KRR_ERR_INVALID_ARGUMENT, "operands exceed smem");
         c.set_device();
-        *cycles_per_mma = krr::i8_mma_rate(N, reps, kbytes, c.stream);
+        *cycles_per_mma = krr::i8_mma_rate(N, reps, kbytes, mode, c.stream);
+    });
+}
+
+int krr_debug_tmem_ld_rate(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (warps < 1 || warps > 32 || reps < 1) fail(KRR_ERR_INVALID_ARGUMENT, "warps in [1, 32], reps >= 1");
+        c.set_device();
+        *bytes_per_clk = krr::tmem_ld_rate(warps, reps, c.stream);
     });
 }
 

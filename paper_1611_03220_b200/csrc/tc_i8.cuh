@@ -94,6 +94,19 @@ __device__ __forceinline__ void mbar_wait(void* mbar, uint32_t parity) {
         : "memory");
 }
 
+// Same wait, but lets the hardware suspend the thread until the phase completes (up to
+// ~1 ms per try) instead of spinning: keeps single-thread producer / MMA roles off the
+// issue slots their SM sub-partition shares with the epilogue warps.
+__device__ __forceinline__ void mbar_wait_sleep(void* mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
+
 // 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
@@ -110,6 +123,19 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 //   LBO = rows * 16 bytes (next 16-wide K chunk), SBO = 128 bytes (next 8-row group).
 __host__ __device__ __forceinline__ uint32_t kmajor_offset(int row, int k, int rows) {
     return uint32_t((k >> 4) * rows * 16 + (row >> 3) * 128 + (row & 7) * 16 + (k & 15));
+}
+
+// 32 lanes x 32 bit, 32 consecutive columns -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
 }
 
 }  // namespace tc

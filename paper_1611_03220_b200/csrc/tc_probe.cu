@@ -1,6 +1,8 @@
 // Diagnostic: one-CTA tcgen05 kind::i8 GEMM  C (128 x N, s32) = A (128 x K) . B (N x K)^T
 // through the helpers in tc_i8.cuh — validates the descriptor / TMEM mechanics the
 // INT8-slice mat-vec relies on (tests/test_gpu_tc.py).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_i8.cuh"
@@ -54,8 +56,14 @@ __global__ void __launch_bounds__(128) i8_probe_kernel(const int8_t* __restrict_
 
 // MMA throughput: one CTA per SM issues `reps` back-to-back tcgen05.mma (M = 128, N, K = 32)
 // on zero operands (no swizzle, K-major) into TMEM; cycles per MMA -> out[blockIdx.x].
-template <int N>
-__global__ void __launch_bounds__(128) i8_mma_rate_kernel(int reps, int kbytes, long long* out, int naccum) {
+// mode 0: SS, descriptors rebuilt per MMA, one accumulator
+//      1: SS, hoisted descriptors, one accumulator
+//      2: SS, hoisted, 8 MMAs per iteration into rotating accumulators
+//      3: TS (A in TMEM), descriptors rebuilt per MMA
+//      4: TS, hoisted, rotating accumulators
+//      5: SS, hoisted, rotating accumulators and distinct A/B smem tiles per MMA
+template <int N, int MODE>
+__global__ void __launch_bounds__(128) i8_mma_rate_kernel(int reps, int kbytes, long long* out) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t tbase;
@@ -71,21 +79,34 @@ __global__ void __launch_bounds__(128) i8_mma_rate_kernel(int reps, int kbytes, 
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = tbase;
+    // accumulators: D at columns [0, 256) for TS (A at 256..), [0, 512) otherwise
+    constexpr int NACC_SS = (512 / N) < 8 ? (512 / N) : 8;
+    constexpr int NACC_TS = (256 / N) < 8 ? ((256 / N) < 1 ? 1 : (256 / N)) : 8;
+    constexpr int KB = 96;  // hoisted modes: 96 bytes per row
     if (tid == 0) {
         const uint32_t idesc = tc::idesc_i8(128, N);
         const uint32_t a = tc::smem_u32(sm), b = tc::smem_u32(sm + 128 * kbytes);
         const long long t0 = clock64();
-        if (naccum == -2) {
-            // SS mode, descriptors hoisted, 8 MMAs per iteration (pure issue rate)
-            const uint64_t da = tc::smem_desc(a, 128, uint32_t(kbytes) * 8);
-            const uint64_t db = tc::smem_desc(b, 128, uint32_t(kbytes) * 8);
+        if constexpr (MODE == 1 || MODE == 2 || MODE == 5) {
+            const uint64_t da = tc::smem_desc(a, 128, uint32_t(KB) * 8);
+            const uint64_t db = tc::smem_desc(b, 128, uint32_t(KB) * 8);
             tc::mma_i8(tmem, da, db, idesc, 0u);
             for (int r = 0; r < reps / 8; ++r) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) tc::mma_i8(tmem, da, db, idesc, 1u);
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t d = MODE == 1 ? tmem : tmem + uint32_t((u % NACC_SS) * N);
+                    const uint64_t off = MODE == 5 ? uint64_t((u % (KB / 32)) * 16) : 0;
+                    tc::mma_i8(d, da + off, db + off, idesc, 1u);
+                }
             }
-        } else if (naccum < 0) {
-            // TS mode: A (128 x 32 int8 = 8 TMEM columns) at TMEM column 256, D at column 0
+        } else if constexpr (MODE == 4) {
+            const uint64_t db = tc::smem_desc(b, 128, uint32_t(KB) * 8);
+            for (int r = 0; r < reps / 8; ++r) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    tc::mma_i8_ts(tmem + uint32_t((u % NACC_TS) * N), tmem + 256u + uint32_t(u * 8), db, idesc, 1u);
+            }
+        } else if constexpr (MODE == 3) {
             for (int r = 0; r < reps; ++r) {
                 const int ks = r % (kbytes / 32);
                 const uint64_t db = tc::smem_desc(b + ks * 256, 128, uint32_t(kbytes) * 8);
@@ -96,8 +117,7 @@ __global__ void __launch_bounds__(128) i8_mma_rate_kernel(int reps, int kbytes, 
                 const int ks = r % (kbytes / 32);
                 const uint64_t da = tc::smem_desc(a + ks * 256, 128, uint32_t(kbytes) * 8);
                 const uint64_t db = tc::smem_desc(b + ks * 256, 128, uint32_t(kbytes) * 8);
-                const int slot = r % naccum;
-                tc::mma_i8(tmem + uint32_t(slot * N), da, db, idesc, r >= naccum ? 1u : 0u);
+                tc::mma_i8(tmem, da, db, idesc, r > 0 ? 1u : 0u);
             }
         }
         tc::mma_commit(&mbar);
@@ -110,31 +130,186 @@ __global__ void __launch_bounds__(128) i8_mma_rate_kernel(int reps, int kbytes, 
     if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
+// In-situ order of the K1-I8 tile: M = 128, N = 64, kp = 96 (3 K steps), 8 A slices and
+// 8 B slices resident, 36 products accumulated into 8 TMEM groups of 64 columns.
+// ORDER 0: group-major (c = 7..0, p = 0..c) as the kernel issues them; ORDER 1: A-slice
+// major (p outer, q inner: consecutive MMAs share the A operand).  Cycles per MMA.
+template <int ORDER>
+__global__ void __launch_bounds__(128) i8_tile_order_kernel(int tiles, long long* out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tbase;
+    constexpr int KP = 96, TI = 128, TJ = 64;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 8 * (TI + TJ) * KP; i += 128) sm[i] = uint8_t(i * 7);
+    tc::fence_proxy_async();
+    if (tid == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::mbar_fence_init();
+    }
+    if (warp == 0) tc::tmem_alloc(&tbase, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tbase;
+    if (tid == 0) {
+        const uint32_t idesc = tc::idesc_i8(TI, TJ);
+        const uint64_t dA0 = tc::smem_desc(tc::smem_u32(sm), 128, KP * 8);
+        const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sm + 8 * TI * KP), 128, KP * 8);
+        const long long t0 = clock64();
+        for (int t = 0; t < tiles; ++t) {
+            if constexpr (ORDER == 0) {
+#pragma unroll
+                for (int c = 7; c >= 0; --c)
+#pragma unroll
+                    for (int p = 0; p <= c; ++p)
+#pragma unroll
+                        for (int ks = 0; ks < 3; ++ks)
+                            tc::mma_i8(tmem + uint32_t(c * TJ), dA0 + uint64_t((p * TI * KP + ks * 256) >> 4),
+                                       dB0 + uint64_t(((c - p) * TJ * KP + ks * 256) >> 4), idesc,
+                                       (p == 0 && ks == 0) ? 0u : 1u);
+            } else {
+#pragma unroll
+                for (int p = 0; p < 8; ++p)
+#pragma unroll
+                    for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+                        for (int q = 0; q + p < 8; ++q)
+                            tc::mma_i8(tmem + uint32_t((p + q) * TJ), dA0 + uint64_t((p * TI * KP + ks * 256) >> 4),
+                                       dB0 + uint64_t((q * TJ * KP + ks * 256) >> 4), idesc,
+                                       (q == 0 ? (ks == 0) : (p == 0 && ks == 0)) ? 0u : 1u);
+            }
+        }
+        tc::mma_commit(&mbar);
+        tc::mbar_wait(&mbar, 0);
+        const long long t1 = clock64();
+        out[blockIdx.x] = (t1 - t0);
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+// Does tensor-core INT8 work slow the FP64 pipe?  Warps 4-7 run 8 independent DADD (OP 0)
+// or DFMA (OP 1) chains for `iters` iterations; with MMA != 0, thread 0 meanwhile issues
+// back-to-back tcgen05.mma kind::i8 (M = 128, N = 64, K = 32, SS) until they finish.
+// Returns cycles of the FP64 loop (max over SMs).
+template <int OP, bool MMA>
+__global__ void __launch_bounds__(256) fp64_under_mma_kernel(int iters, long long* out, double* sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tbase;
+    __shared__ volatile int stop;
+    __shared__ long long tmax;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (128 + 64) * 96; i += 256) sm[i] = 0;
+    tc::fence_proxy_async();
+    if (tid == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::mbar_fence_init();
+        stop = 0;
+        tmax = 0;
+    }
+    if (warp == 0) tc::tmem_alloc(&tbase, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tbase;
+    if (MMA && tid == 0) {
+        const uint32_t idesc = tc::idesc_i8(128, 64);
+        const uint64_t da = tc::smem_desc(tc::smem_u32(sm), 128, 96 * 8);
+        const uint64_t db = tc::smem_desc(tc::smem_u32(sm + 128 * 96), 128, 96 * 8);
+        int r = 0;
+        while (!stop && r < (1 << 22)) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) tc::mma_i8(tmem + uint32_t(u * 64), da, db, idesc, 1u);
+            r += 8;
+            if ((r & 63) == 0) {  // keep the queue bounded
+                tc::mma_commit(&mbar);
+                tc::mbar_wait(&mbar, uint32_t(((r >> 6) - 1) & 1));
+            }
+        }
+    } else if (warp >= 4) {
+        double a[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = 1.0 + 1e-3 * (i + tid);
+        const double b = 1e-9, c = 0.999999;
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = OP == 0 ? a[i] + b : fma(a[i], c, b);
+        }
+        const long long t1 = clock64();
+        double s = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += a[i];
+        if (s == 1234.5) sink[0] = s;
+        atomicMax(reinterpret_cast<unsigned long long*>(&tmax), (unsigned long long)(t1 - t0));
+        __syncwarp();
+        if (tid == 128) stop = 1;
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) out[blockIdx.x] = tmax;
+    if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+// TMEM read throughput: `warps` warps per CTA (one CTA per SM) each issue `reps`
+// tcgen05.ld.32x32b.x16 (+ wait) from their lane quarter; cycles -> out[blockIdx.x].
+__global__ void tmem_ld_rate_kernel(int reps, long long* out, unsigned* sink) {
+    __shared__ uint32_t tbase;
+    __shared__ long long tmax;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tc::tmem_alloc(&tbase, 512);
+    if (tid == 0) tmax = 0;
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tbase + (uint32_t((warp & 3) * 32) << 16);
+    unsigned x = 0;
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+        uint32_t v[16];
+        tc::tmem_ld16(tmem + uint32_t(((r * 16) + (warp >> 2) * 128) & 511), v);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x ^= v[j];
+    }
+    const long long t1 = clock64();
+    atomicMax(reinterpret_cast<unsigned long long*>(&tmax), (unsigned long long)(t1 - t0));
+    if (x == 0x12345u) sink[0] = x;
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) out[blockIdx.x] = tmax;
+    if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
 }  // namespace
 
-double i8_mma_rate(int N, int reps, int kbytes, cudaStream_t stream) {
-    int naccum = kbytes >= 1024 ? std::max(1, 512 / N) : 1;  // kbytes >= 1024: rotate accumulators
-    if (kbytes >= 1024) kbytes /= 32;
-    if (reps < 0) {  // TS mode (A in TMEM)
-        reps = -reps;
-        naccum = -1;
-        if (reps >= 1000000) {  // hoisted-descriptor SS variant
-            reps -= 1000000;
-            naccum = -2;
-        }
-    }
+double i8_mma_rate(int N, int reps, int kbytes, int mode, cudaStream_t stream) {
     long long* d = nullptr;
     KRR_CUDA(cudaMalloc(&d, 148 * sizeof(long long)));
     const size_t smem = size_t(128 + N) * kbytes;
     auto run = [&](auto kern) {
         KRR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<148, 128, smem, stream>>>(reps, kbytes, d, naccum);
+        kern<<<148, 128, smem, stream>>>(reps, kbytes, d);
     };
-    if (N == 16) run(i8_mma_rate_kernel<16>);
-    else if (N == 32) run(i8_mma_rate_kernel<32>);
-    else if (N == 64) run(i8_mma_rate_kernel<64>);
-    else if (N == 128) run(i8_mma_rate_kernel<128>);
-    else run(i8_mma_rate_kernel<256>);
+    auto by_mode = [&](auto n) {
+        constexpr int NN = decltype(n)::value;
+        switch (mode) {
+            case 0: run(i8_mma_rate_kernel<NN, 0>); break;
+            case 1: run(i8_mma_rate_kernel<NN, 1>); break;
+            case 2: run(i8_mma_rate_kernel<NN, 2>); break;
+            case 3: run(i8_mma_rate_kernel<NN, 3>); break;
+            case 4: run(i8_mma_rate_kernel<NN, 4>); break;
+            default: run(i8_mma_rate_kernel<NN, 5>); break;
+        }
+    };
+    if (N == 16) by_mode(std::integral_constant<int, 16>{});
+    else if (N == 32) by_mode(std::integral_constant<int, 32>{});
+    else if (N == 64) by_mode(std::integral_constant<int, 64>{});
+    else if (N == 128) by_mode(std::integral_constant<int, 128>{});
+    else by_mode(std::integral_constant<int, 256>{});
     KRR_LAUNCH_CHECK();
     long long h[148];
     KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -143,6 +318,70 @@ double i8_mma_rate(int N, int reps, int kbytes, cudaStream_t stream) {
     double mx = 0;
     for (long long v : h) mx = std::max(mx, double(v));
     return mx / reps;
+}
+
+double i8_tile_order_rate(int order, int tiles, cudaStream_t stream) {
+    long long* d = nullptr;
+    KRR_CUDA(cudaMalloc(&d, 148 * sizeof(long long)));
+    const size_t smem = size_t(8) * (128 + 64) * 96;
+    auto run = [&](auto kern) {
+        KRR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<148, 128, smem, stream>>>(tiles, d);
+    };
+    if (order == 0) run(i8_tile_order_kernel<0>);
+    else run(i8_tile_order_kernel<1>);
+    KRR_LAUNCH_CHECK();
+    long long h[148];
+    KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d);
+    double mx = 0;
+    for (long long v : h) mx = std::max(mx, double(v));
+    return mx / (double(tiles) * 108.0);
+}
+
+double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream) {
+    long long* d = nullptr;
+    double* sink = nullptr;
+    KRR_CUDA(cudaMalloc(&d, 148 * sizeof(long long)));
+    KRR_CUDA(cudaMalloc(&sink, sizeof(double)));
+    const size_t smem = size_t(128 + 64) * 96;
+    auto run = [&](auto kern) {
+        KRR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<148, 256, smem, stream>>>(iters, d, sink);
+    };
+    if (op == 0 && mma) run(fp64_under_mma_kernel<0, true>);
+    else if (op == 0) run(fp64_under_mma_kernel<0, false>);
+    else if (mma) run(fp64_under_mma_kernel<1, true>);
+    else run(fp64_under_mma_kernel<1, false>);
+    KRR_LAUNCH_CHECK();
+    long long h[148];
+    KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d);
+    cudaFree(sink);
+    double mx = 0;
+    for (long long v : h) mx = std::max(mx, double(v));
+    // FP64 lane-ops per clock per SM: 4 warps x 32 lanes x 8 chains x iters / cycles
+    return 4.0 * 32 * 8 * double(iters) / mx;
+}
+
+double tmem_ld_rate(int warps, int reps, cudaStream_t stream) {
+    long long* d = nullptr;
+    unsigned* sink = nullptr;
+    KRR_CUDA(cudaMalloc(&d, 148 * sizeof(long long)));
+    KRR_CUDA(cudaMalloc(&sink, sizeof(unsigned)));
+    tmem_ld_rate_kernel<<<148, 32 * warps, 0, stream>>>(reps, d, sink);
+    KRR_LAUNCH_CHECK();
+    long long h[148];
+    KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d);
+    cudaFree(sink);
+    double mx = 0;
+    for (long long v : h) mx = std::max(mx, double(v));
+    // bytes per clock per SM: warps x reps x (32 lanes x 16 columns x 4 B) / cycles
+    return double(warps) * reps * 2048.0 / mx;
 }
 
 void i8_probe_launch(const int8_t* A, const int8_t* B, int32_t* C, int K, int N, cudaStream_t stream) {

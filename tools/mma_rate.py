@@ -1,4 +1,5 @@
-"""tcgen05 kind::i8 MMA throughput probe: cycles per MMA vs N and K bytes per row."""
+"""tcgen05 kind::i8 MMA throughput probe (cycles per MMA vs N, operand source and
+accumulator rotation) and TMEM read throughput (bytes / clk / SM vs warps)."""
 import ctypes as C
 import json
 import sys
@@ -8,14 +9,31 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1611_03220_b200 as krr  # noqa: E402
 from paper_1611_03220_b200 import _lib  # noqa: E402
 
+MODES = {0: "SS", 1: "SS-hoisted", 2: "SS-hoisted-rot", 3: "TS", 4: "TS-hoisted-rot", 5: "SS-hoisted-rot-tiles"}
+
 ctx = krr.Context(0)
-for kb, reps in ((96, -1004096),):  # hoisted descriptors, 8 MMAs per loop iteration
+kb = 96
+for mode in (1, 2, 4, 5):
     for n in (16, 32, 64, 128, 256):
-        kbb = kb if kb < 1024 else kb // 32
-        if (128 + n) * kbb > 200 * 1024:
+        if (128 + n) * kb > 200 * 1024:
             continue
         cyc = C.c_double()
-        _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, n, reps, kb, C.byref(cyc)))
+        _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, n, 4096, kb, mode, C.byref(cyc)))
         macs = 128 * n * 32
-        print(json.dumps({"N": n, "kbytes": kbb, "mode": "SS-hoisted" if reps <= -1000000 else ("TS" if reps < 0 else "SS"), "cycles_per_mma": cyc.value, "mac_per_clk": macs / cyc.value,
-                          "tops_at_1965MHz_148sm": 2 * macs / cyc.value * 148 * 1.965e9 / 1e12}), flush=True)
+        print(json.dumps({"N": n, "kbytes": kb, "mode": MODES[mode], "cycles_per_mma": round(cyc.value, 2),
+                          "mac_per_clk": round(macs / cyc.value, 1),
+                          "tops_at_1965MHz_148sm": round(2 * macs / cyc.value * 148 * 1.965e9 / 1e12, 1)}),
+              flush=True)
+for mode in (6, 7):
+    cyc = C.c_double()
+    _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, 64, 200, 96, mode, C.byref(cyc)))
+    print(json.dumps({"tile_order": ["group-major", "A-major"][mode - 6], "N": 64, "kp": 96,
+                      "cycles_per_mma": round(cyc.value, 2)}), flush=True)
+for mode, name in ((8, "DADD"), (9, "DADD+MMA"), (10, "DFMA"), (11, "DFMA+MMA")):
+    r = C.c_double()
+    _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, 64, 20000, 96, mode, C.byref(r)))
+    print(json.dumps({"fp64_under_mma": name, "fp64_lane_ops_per_clk_per_sm": round(r.value, 2)}), flush=True)
+for warps in (1, 4, 8, 16):
+    bpc = C.c_double()
+    _lib.check(_lib.LIB.krr_debug_tmem_ld_rate(ctx.handle, warps, 4096, C.byref(bpc)))
+    print(json.dumps({"tmem_ld_warps": warps, "bytes_per_clk_per_sm": round(bpc.value, 1)}), flush=True)

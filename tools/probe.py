@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--grouped", type=int, default=-1, help="-1: both (resident 8-warp only)")
     ap.add_argument("--path", type=int, default=0, help="K1 path: 0 = FP64 DMMA, 1 = tcgen05 INT8 slices, -1 both")
     ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--i8-debug", default="0", help="comma list of K1-I8 profiling modes (1 no MMA, 2 no exp)")
     args = ap.parse_args()
     out = {}
     ctx = krr.Context(0)
@@ -66,8 +67,11 @@ def main():
                              [max(args.grouped, 0) if r == 1 and w == 8 else 0])]
         paths = [0, 1] if args.path < 0 else [args.path]
         combos = [(r, w, gp, pa) for pa in paths for (r, w, gp) in (combos if pa == 0 else [(1, 8, 1)])]
-        for res, w, gp, pa in combos:
+        dbgs = [int(v) for v in args.i8_debug.split(",")]
+        combos = [(r, w, gp, pa, dbg) for (r, w, gp, pa) in combos for dbg in (dbgs if pa == 1 else [0])]
+        for res, w, gp, pa, dbg in combos:
             ctx.set_option("k1_path", pa)
+            ctx.set_option("i8_debug", dbg)
             ctx.set_option("k1_resident", res)
             ctx.set_option("k1_warps", w)
             ctx.set_option("k1_grouped", gp)
@@ -75,7 +79,10 @@ def main():
             tot, k1 = C.c_double(), C.c_double()
             _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))  # warm
             _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, args.steps, C.byref(tot), C.byref(k1)))
+            if dbg:
+                print(json.dumps({"i8_debug": dbg}), flush=True)
             rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode, w, gp, pa))
+        ctx.set_option("i8_debug", 0)
     out["matvec"] = rows
     ctx.close()
     od = ROOT / "gpurun_out"
