@@ -14,10 +14,13 @@ value   = whole-job Gevals/s = n^2 * K / (max-over-ranks device time of the K st
           126 MB L2, so no explicit flush between steps.
 e2e     = same metric through the reference-facing C-ABI call krr_kernel_matvec with
           pinned HOST buffers (H2D of v and D2H of the result inside the timed region).
-roofline: dominant kernel = K1; achieved = algorithmic FP64 tensor FLOPs per launch
-          (unique pairs owned by the rank x 2d) / mean K1 launch time
-          (CUDA events on the launching stream); peak = FP64 DMMA rate measured live on
-          this GPU by krr_microbench (not in MEASURED_PEAKS.json).
+roofline: dominant kernel = K1.  The default path at d = 90 is K1-I8 (tcgen05 kind::i8
+          Ozaki slices): achieved = algorithmic INT8 tensor ops per launch (unique pairs x
+          36 slice products x kp x 2) / mean K1 launch time (CUDA events on the launching
+          stream); peak = 2 x the measured dense bf16 rate in MEASURED_PEAKS.json (B200 INT8
+          = 2x bf16).  The same launch is also expressed as FP64-equivalent dot-product
+          TFLOP/s (pairs x 2d) against the live-measured FP64 DMMA peak (krr_microbench),
+          the unit of the DMMA K1 path (k1_path = 0).
 --impl reference: the CPU restatement (oracle/, all host threads) on a bounded row
           sample of the same workload — the reference itself (CPU-only, Eigen) cannot be
           built in this image.
@@ -238,6 +241,7 @@ def main():
     mb = np.zeros(9)
     _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(mb)))
     peak_dmma = float(mb[0])
+    path = int(ctx.get_option("k1_path_effective"))  # 1 = K1-I8 (tcgen05), 0 = K1 (DMMA)
 
     tot, k1 = C.c_double(), C.c_double()
     if args.warmup > 0:
@@ -281,12 +285,39 @@ def main():
     dp = (d + 2 + 3) // 4 * 4
     pipe_ops = pairs_rank * 2.0 * (dp + 12)  # DMMA MACs (dp) + 10 exp + 2 accumulate FP64 ops
     traffic = None
-    tf = ROOT / "profiles" / "k1_ncu_summary.json"
+    tf = ROOT / "profiles" / ("k1_i8_ncu_summary.json" if path == 1 else "k1_ncu_summary.json")
     if tf.exists():
         try:
             traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    fp64_view = {"achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s", "frac": achieved / peak_dmma,
+                 "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU (krr_microbench)"}
+    if path == 1:
+        kp = (d + 31) // 32 * 32
+        i8_ops = pairs_rank * 36.0 * kp * 2.0
+        i8_achieved = i8_ops / (k1_ms * 1e-3) / 1e12
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        peak_i8 = 2.0 * float(peaks.get("bf16_tflops", 2250.0))
+        roofline = {"bound": "tensor", "achieved": i8_achieved, "peak": peak_i8, "unit": "TOPS (int8)",
+                    "frac": i8_achieved / peak_i8, "traffic": traffic,
+                    "kernel": "gauss_matvec_i8_kernel (K1-I8, tcgen05 kind::i8)",
+                    "ops_per_launch": i8_ops, "k1_ms": k1_ms,
+                    "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2x bf16 on B200)"
+                                   if "bf16_tflops" in peaks else "2 x 2.25 PF nominal bf16 (no MEASURED_PEAKS.json)",
+                    "fp64_equivalent": fp64_view,
+                    "note": "FP64 epilogue and INT8 MMAs share SM execution resources and shared-memory "
+                            "bandwidth on B200 (profiles/README.md), so MMA and epilogue time add"}
+    else:
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
+                    "frac": achieved / peak_dmma, "traffic": traffic,
+                    "kernel": "gauss_matvec_kernel (K1, FP64 DMMA)",
+                    "flops_per_launch": flops, "k1_ms": k1_ms,
+                    "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU "
+                                   "(krr_microbench; MEASURED_PEAKS.json has no FP64 entry)",
+                    "fp64_pipe": {"ops_per_pair": dp + 12, "achieved_tflops_equiv":
+                                  pipe_ops / (k1_ms * 1e-3) / 1e12,
+                                  "frac": pipe_ops / (k1_ms * 1e-3) / 1e12 / peak_dmma}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -310,19 +341,14 @@ def main():
         "config": {"workload": "config4 (K + lambda I) v, K on the fly", "n": n, "d": d, "sigma": sigma,
                    "lambda": lam, "parallelism": f"row/tile-sharded x{world} + NCCL all-reduce",
                    "l2": "no flush: X (755 MB) and partials (2 GB) exceed the 126 MB L2",
-                   "kernel_evals_per_step": float(n) * n, "unique_pairs_per_step": n * (n - 1) / 2},
+                   "kernel_evals_per_step": float(n) * n, "unique_pairs_per_step": n * (n - 1) / 2,
+                   "dot_products": "exact int8 Ozaki slices on tcgen05 (fp64-accurate)" if path == 1
+                   else "FP64 DMMA"},
         "e2e": {"value": float(n) * n * steps / e2e_s / 1e9, "unit": "Gevals/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
-                     "frac": achieved / peak_dmma, "traffic": traffic,
-                     "kernel": "gauss_matvec_kernel (K1)",
-                     "flops_per_launch": flops, "k1_ms": k1_ms,
-                     "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU "
-                                    "(krr_microbench; MEASURED_PEAKS.json has no FP64 entry)",
-                     "fp64_pipe": {"ops_per_pair": dp + 12, "achieved_tflops_equiv":
-                                   pipe_ops / (k1_ms * 1e-3) / 1e12,
-                                   "frac": pipe_ops / (k1_ms * 1e-3) / 1e12 / peak_dmma}},
+        "roofline": roofline,
+        "k1_path": ["dmma", "i8"][path],
         "microbench": {"dmma_tflops": mb[0], "dfma_tflops": mb[1], "dmma_dfma_mixed_tflops": mb[2],
                        "exp_libdevice_gevals": mb[3], "exp_table_gevals": mb[4]},
         "clocks": clk,

@@ -74,9 +74,18 @@ int krr_ctx_destroy(krr_ctx* ctx);
 int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
 
 /* Tuning / diagnostic knobs (no reference equivalent):
- *   "k1_resident" 1|0  keep the column tile of the fused mat-vec in shared memory (default 1)
- *   "exp_mode"    1|0  table exp (default) | libdevice exp in the Gaussian epilogue */
+ *   "k1_path"     -1|0|1  fused mat-vec kernel: auto (default: INT8-slice tensor-core kernel
+ *                         for d >= 48 when the data's exponent range allows, else FP64 DMMA) |
+ *                         FP64 DMMA | tcgen05 INT8 slices
+ *   "k1_resident" 1|0  keep the column tile of the DMMA mat-vec in shared memory (default 1)
+ *   "k1_warps" 8|16, "k1_grouped" 1|0  DMMA mat-vec shape (defaults 8, 1)
+ *   "batched_rhs" 1|0  multi-RHS solves / mat-mats through the batched kernel (default 1)
+ *   "exp_mode"    1|0  table exp (default) | libdevice exp in the Gaussian epilogue
+ *   "i8_debug"    bits  profiling only (K1-I8: 1 skip MMAs, 2 skip exp, 4 clock trace) */
 int krr_set_option(krr_ctx* ctx, const char* key, double value);
+/* Read a knob back: "k1_path", "exp_mode", "batched_rhs", and (after krr_set_data)
+ * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now) and "i8_supported". */
+int krr_get_option(krr_ctx* ctx, const char* key, double* value);
 
 /* ---------------------------------------------------------------- data + kernel operator */
 /* Uploads X (n x d, row-major) to the device (replicated on every rank) and
@@ -223,6 +232,9 @@ int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, d
 /* TMEM read throughput (tcgen05.ld.32x32b.x16 + wait in a loop), `warps` warps on every
  * SM; returns bytes per clock per SM. */
 int krr_debug_tmem_ld_rate(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk);
+/* K1-I8 profiling trace (set_option("i8_debug", 4) before a mat-vec): clock64 stamps of
+ * CTA 0, 16 per tile for the first 64 tiles. */
+int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count);
 
 #ifdef __cplusplus
 }

@@ -110,6 +110,7 @@ _SIGS = {
     "krr_ctx_destroy": [_vp],
     "krr_ctx_launch_count": [_vp, C.POINTER(_i64)],
     "krr_set_option": [_vp, C.c_char_p, _d],
+    "krr_get_option": [_vp, C.c_char_p, C.POINTER(_d)],
     "krr_set_data": [_vp, _vp, _i64, _i64, _d],
     "krr_kernel_matvec": [_vp, _d, _vp, _i64, _vp],
     "krr_kernel_matvec_device": [_vp, _d, _vp, _i64, _vp],
@@ -137,6 +138,7 @@ _SIGS = {
     "krr_debug_i8_gemm": [_vp, _vp, _vp, _vp, _i, _i],
     "krr_debug_i8_mma_rate": [_vp, _i, _i, _i, _i, C.POINTER(_d)],
     "krr_debug_tmem_ld_rate": [_vp, _i, _i, C.POINTER(_d)],
+    "krr_debug_i8_trace": [_vp, _vp, _i],
 }
 
 
@@ -218,6 +220,11 @@ class Context:
 
     def set_option(self, key: str, value: float) -> None:
         check(LIB.krr_set_option(self.handle, key.encode(), float(value)))
+
+    def get_option(self, key: str) -> float:
+        out = C.c_double()
+        check(LIB.krr_get_option(self.handle, key.encode(), C.byref(out)))
+        return out.value
 
     @property
     def launches(self) -> int:

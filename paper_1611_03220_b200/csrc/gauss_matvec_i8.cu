@@ -2,9 +2,13 @@
 // 5th-generation tensor cores (tcgen05.mma kind::i8, TMEM accumulators), exact to
 // fp64 level via an Ozaki-style slice decomposition.
 //
-// Why: on B200 the FP64 tensor path (DMMA) and DFMA share one FP64 datapath
-// (37 TFLOP/s), and the d-long dot product is ~90 % of K1's FP64 work.  INT8 tensor
-// throughput is ~120x larger, and integer MMA accumulates exactly.
+// Why: the d-long dot product is ~90 % of K1's FP64 work, and integer MMA accumulates
+// exactly.  Measured on B200 (tools/mma_rate.py, profiles/): the FP64 pipe, DMMA and the
+// INT8 tensor path share one execution resource — DFMA / DADD drop from 61 to 16
+// lane-ops / clk / SM while tcgen05 INT8 MMAs run — so K1-I8's cost is MMA time + FP64
+// time, and the design minimises both: one MMA per 128 x 64 x 32-byte block (~50 clk),
+// and 15 FP64 operations per pair in the epilogue (vs 92 + 12 per pair for the DMMA K1
+// at d = 90).
 //
 // Decomposition (per row i, e_i = ilogb(max_k |x_ik|) + 1, u_i = x_i 2^-e_i in (-1, 1)):
 //     u_i = sum_{p<8} A_i^(p) 2^(-7(p+1)) + r_i,   A^(p) in [-127, 127],  |r_i| < 2^-56
@@ -14,33 +18,39 @@
 // groups.  The epilogue fuses the groups in integer arithmetic and converts twice:
 //     b_k = 128 G_2k + G_2k+1 (int32),  H = 2^14 b_0 + b_1,  Lo = 2^14 b_2 + b_3 (int64, exact)
 //     T = H + 2^-28 Lo  (one rounding)  =  2^21 sum_c 2^(-7c) G_c
-// via the 1.5 * 2^52 bit trick (IMAD.WIDE into the mantissa field + one DADD / DFMA), so
-// -2 x_i.x_j = -2^(e_i + e_j - 34) T.  The exp argument is formed directly,
+// via the 1.5 * 2^52 bit trick (a 64-bit integer multiply-add into the mantissa field +
+// one DADD / DFMA), so -2 x_i.x_j = -2^(e_i + e_j - 34) T.  The exp argument is formed
+// directly in units of 1/256 octave,
 //     y = kscale d2 = sq'_i + sq'_j + |kscale| 2^(e_i - 34) 2^(e_j) T,   sq' = kscale |x|^2,
-// (the per-column power of two is an integer add on the high word), clamped to
-// [-1022 * 64, 0] and fed to the same 64-entry table exp as K1.  Dot-product error
+// with kscale = -scale 256 / ln2 (the per-column power of two is an integer add on the high
+// word), and e = 2^(k/256) (1 + q(f)), k = round(y), f = y - k, from a 256-entry table and
+// a degree-4 polynomial (truncation error 4e-17 relative).  Dot-product error
 // <= ~2^-52 * d * 2^(e_i + e_j), the order of an fp64 dot product's own bound.
 //
-// Structure (one CTA per symmetric super-tile, 10 warps, M = 128 rows x N = 64 columns):
-//   warp 0     producer: 1-D bulk async copies (TMA engine) of the slice tiles — the I
-//              tile (128 rows x 8 slices, resident per I) and a ring of J tiles
-//              (64 rows x 8 slices) — plus a ring of per-column data (sq', v, e_j << 20);
-//   warp 1     MMA issuer: one thread issues the 36 x (kp/32) tcgen05.mma of a tile group
-//              by group, c = 7 down to 0, each group into its own 64 TMEM columns
-//              (8 x 64 = all 512), committing one mbarrier per group;
-//   warps 2-9  epilogue: each thread owns one row (its TMEM lane) and 32 of the 64
-//              columns.  It drains the groups in completion order (tcgen05.ld x32) and
-//              releases each at once, so the next tile's MMAs for group c overlap this
-//              tile's remaining drain and its whole exp phase — a single TMEM buffer,
-//              pipelined per group.  Row sums stay in registers; column sums go through a
-//              per-warp shared-memory transpose and a fixed-order 4-way combine.
-// Slots in `part` follow exactly the K1 rules (gauss_matvec.cu) — one writer per
-// (slot, index) — so the finish kernel is shared; column sums are accumulated in the
-// CTA's own slot in global memory (owner thread per column, program order), which
-// frees the shared memory the 96-byte-row tiles need.
+// Structure (one CTA per symmetric super-tile, 10 warps, tiles of M = 128 rows x N = 64
+// columns):
+//   warp 0     producer: 1-D bulk async copies (TMA engine) of the I tile (128 rows x 8
+//              slices, resident for a pass), a ring of J tiles (64 rows x 8 slices) and a
+//              ring of per-column data (sq', v, e_j << 20);
+//   warp 1     MMA issuer: one thread issues the 36 x (kp/32) tcgen05.mma of a tile group by
+//              group, c = 7 down to 0, each group into its own 64 TMEM columns (8 x 64 = all
+//              512), committing one mbarrier per group;
+//   warps 2-9  epilogue: each thread owns one row (its TMEM lane) and 32 of the 64 columns.
+//              It drains the groups in completion order (tcgen05.ld) and releases each pair
+//              at once, so the next tile's MMAs start while this tile is still converting.
+//              Row sums stay in registers; every e v_i goes straight to a per-warp
+//              shared-memory transpose (one sync per tile), then each lane sums one column
+//              and the four lane quarters combine in fixed order.
+// The J-tile ring has one stage at kp = 96: the next tile's load overlaps this tile's FP64
+// epilogue, which cannot overlap the MMAs anyway (shared execution resource, above).  Slots in `part` follow exactly the K1 rules
+// (gauss_matvec.cu) — one writer per (slot, index) — so the finish kernel is shared; column
+// sums accumulate in the CTA's own slot in global memory (one owner thread per column,
+// program order).  Everything is deterministic.
 // Operand layout in global memory: slice p, 8-row group, 16-byte K chunk
 // ([p][n_pad/8][kp/16][8][16]), so any 8-aligned row range is one contiguous block that
 // is directly the canonical no-swizzle K-major UMMA layout (LBO = 128 B, SBO = 8 kp B).
+#include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -57,44 +67,60 @@ constexpr int NGRP = 8;   // groups c = p + q in [0, 7]
 constexpr int TI = 128;   // I tile rows (MMA M)
 constexpr int TJ = 64;    // J tile columns (MMA N)
 constexpr int NCD = 4;    // column-data stages
-constexpr int NEPI = 8;   // epilogue warps (2 per TMEM lane quarter)
-constexpr int CPT = 32;   // columns per epilogue thread
+constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
+constexpr int CPT = 16;   // columns per epilogue thread
 constexpr int NTHR = 32 * (2 + NEPI);
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int KP_MAX = 96;
-constexpr int SCR_LD = 34;  // transpose scratch row stride (doubles): conflict-free both ways
-constexpr int CD_BYTES = TJ * 8 * 3;  // sq', v, 2^e_j
+constexpr int SCR_LD = 33;  // transpose scratch row stride (doubles): conflict-free both ways
+constexpr int CD_BYTES = TJ * 8 * 2 + TJ * 4;  // sq', v, e_j << 20
+constexpr int TAB = 256;
+constexpr int YMIN_K = -1022 * TAB;  // 2^(k/256) stays normal
+
+__device__ double g_tab256[TAB];
+// profiling trace (i8_debug bit 2): clock64 stamps of CTA 0, 16 per tile, first 64 tiles
+constexpr int TRACE_TILES = 64;
+__device__ long long g_trace[TRACE_TILES * 16];
+#define I8_TRACE(cond, tile, slot)                                                          \
+    do {                                                                                    \
+        if ((A.debug & 4) && blockIdx.x == 0 && (cond) && (tile) < TRACE_TILES)             \
+            g_trace[(tile) * 16 + (slot)] = clock64();                                      \
+    } while (0)
 
 template <int KPT>
 struct Cfg {
-    static constexpr int NSTB = KPT >= 96 ? 2 : 3;  // J-tile stages
-    static constexpr int CH = KPT >= 96 ? 8 : 16;   // transpose chunk (columns)
+    static constexpr int NSTB = KPT >= 96 ? 1 : (KPT >= 64 ? 2 : 3);  // J-tile stages
     static constexpr size_t A_BYTES = size_t(P) * TI * KPT;
     static constexpr size_t B_BYTES = size_t(P) * TJ * KPT;
     static constexpr size_t OFF_B = A_BYTES;
     static constexpr size_t OFF_CD = OFF_B + NSTB * B_BYTES;
     static constexpr size_t OFF_SCR = OFF_CD + NCD * CD_BYTES;
-    static constexpr size_t OFF_COLSCR = OFF_SCR + size_t(NEPI) * CH * SCR_LD * 8;
+    static constexpr size_t OFF_COLSCR = OFF_SCR + size_t(NEPI) * CPT * SCR_LD * 8;
     static constexpr size_t OFF_ROWBUF = OFF_COLSCR + 2 * 4 * TJ * 8;
-    static constexpr size_t OFF_TAB = OFF_ROWBUF + 2 * TI * 8;
-    static constexpr size_t OFF_BARS = OFF_TAB + 64 * 8;
+    static constexpr size_t OFF_TAB = OFF_ROWBUF + (NEPI / 4) * TI * 8;
+    static constexpr size_t OFF_BARS = OFF_TAB + TAB * 8;
     static constexpr int NBARS = 2 + 2 * NSTB + 2 * NCD + 2 * NGRP;
     static constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
+};
+
+struct I8Consts {
+    double kabs;            // |kscale| = scale 256 / ln2
+    double a1, a2, a3, a4;  // (ln2/256)^m / m!
 };
 
 struct I8Args {
     const uint8_t* __restrict__ S;
     const int* __restrict__ ex;      // e_i
-    const double* __restrict__ cpow; // 2^e_j
+    const int* __restrict__ ejs;     // e_j << 20
     const double* __restrict__ sqs;  // kscale |x_j|^2
     const double* __restrict__ v;
     double* __restrict__ part;
     const int2* __restrict__ tiles;
-    const double* __restrict__ exp_tab;
     int64_t n_pad;
     int st;
-    int debug;  // profiling only: bit 0 skips the MMAs, bit 1 the exp phase (results invalid)
-    ExpConsts ec;
+    int debug;  // profiling only: bit 0 skips the MMAs, bit 1 the exp phase (results invalid),
+                // bit 2 records a clock64 trace of CTA 0 (i8_read_trace)
+    I8Consts ec;
 };
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NEPI * 32) : "memory"); }
@@ -114,63 +140,60 @@ __device__ __forceinline__ double magic_pack(int32_t a, int32_t b) {
 // 1.5 * 2^52 + 2^31 and that constant times (1 + 2^-28), both exact integers < 2^53
 constexpr double M2 = 6755401588539392.0 + 25165832.0;  // M1 = 1.5 * 2^52 + 2^31, M2 = M1 (1 + 2^-28)
 
-template <int KPT, bool MASK>
-__device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Args& A, const double* __restrict__ tab,
+template <bool MASK>
+__device__ __forceinline__ void exp_phase(const I8Consts& ec, const double* __restrict__ tab,
                                           const double* __restrict__ cd_sq, const double* __restrict__ cd_v,
-                                          const double* __restrict__ cd_c, double* __restrict__ scr,
-                                          double* __restrict__ colscr_q, double nsi, double sqs_i,
+                                          const int* __restrict__ cd_e, double* __restrict__ scr,
+                                          double* __restrict__ colscr_q, int nsi_hi, int nsi_lo, double sqs_i,
                                           double v_i, double& rowacc, int lane, int colOff, int mask_row) {
-    using C = Cfg<KPT>;
-    constexpr int CH = C::CH;
-    const ExpConsts& ec = A.ec;
     const double shifter = 6755399441055744.0;  // 1.5 * 2^52
+    double racc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int ch = 0; ch < CPT / CH; ++ch) {
-        double colv[CH];
-#pragma unroll
-        for (int k = 0; k < CH; ++k) {
-            const int cl = colOff + ch * CH + k;  // column within the 64-wide tile
-            const double sqj = cd_sq[cl];
-            const double vj = cd_v[cl];
-            double y = fma(T[ch * CH + k], nsi * cd_c[cl], sqs_i + sqj);
-            // y <= 0 (d2 >= 0): y > 0 (rounding, near-duplicate rows) has a non-negative
-            // high word; clamping it to 0 leaves a positive denormal, whose exp is 1 exactly.
-            y = __hiloint2double(min(__double2hiint(y), 0), __double2loint(y));
-            const double t2 = y + shifter;
-            const double kd = t2 - shifter;
-            const double f = y - kd;
-            double q = fma(f, ec.a5, ec.a4);
-            q = fma(q, f, ec.a3);
-            q = fma(q, f, ec.a2);
-            q = fma(q, f, ec.a1);
-            q = q * f;
-            // k >= -1022 * 64 keeps 2^(k/64) normal (e >= ~2^-1022 instead of underflowing)
-            const int kk = max(__double2loint(t2), -65408);
-            const double tj = tab[kk & 63];
-            const double ts = __hiloint2double(__double2hiint(tj) + (kk >> 6) * (1 << 20), __double2loint(tj));
-            double e = fma(ts, q, ts);
-            if constexpr (MASK) e = (cl > mask_row) ? e : 0.0;
-            rowacc = fma(e, vj, rowacc);
-            colv[k] = e * v_i;
-        }
-        // column sums over the warp's 32 rows: transpose through shared memory
-#pragma unroll
-        for (int k = 0; k < CH; ++k) scr[k * SCR_LD + lane] = colv[k];
-        __syncwarp();
-        const int c = lane % CH, rb = (lane / CH) * CH;
-        const double* src = scr + c * SCR_LD + rb;
-        double acc = 0.0;
-#pragma unroll
-        for (int m = 0; m < CH; m += 2) {
-            const double2 pr = *reinterpret_cast<const double2*>(src + m);
-            acc += pr.x;
-            acc += pr.y;
-        }
-#pragma unroll
-        for (int o = CH; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane < CH) colscr_q[colOff + ch * CH + lane] = acc;
-        __syncwarp();
+    for (int k = 0; k < CPT; ++k) {
+        const int cl = colOff + k;  // column within the 64-wide tile
+        const double sqj = cd_sq[cl];
+        const double vj = cd_v[cl];
+        const double nscale = __hiloint2double(nsi_hi + cd_e[cl], nsi_lo);
+        // T of (row `lane`, column k) was parked in this thread's scratch slot by the drain
+        double y = fma(scr[k * SCR_LD + lane], nscale, sqs_i + sqj);
+        // y <= 0 (d2 >= 0): y > 0 (rounding, near-duplicate rows) has a non-negative high
+        // word; clamping it to 0 leaves a positive denormal, whose exp is 1 exactly.
+        y = __hiloint2double(min(__double2hiint(y), 0), __double2loint(y));
+        const double t2 = y + shifter;
+        const double kd = t2 - shifter;
+        const double f = y - kd;
+        double q = fma(f, ec.a4, ec.a3);
+        q = fma(q, f, ec.a2);
+        q = fma(q, f, ec.a1);
+        q = q * f;
+        // k >= -1022 * 256 keeps 2^(k/256) normal (e >= ~2^-1022 instead of underflowing)
+        const int kk = max(__double2loint(t2), YMIN_K);
+        const double tj = tab[kk & (TAB - 1)];
+        const double ts = __hiloint2double(__double2hiint(tj) + (kk >> 8) * (1 << 20), __double2loint(tj));
+        double e = fma(ts, q, ts);
+        if constexpr (MASK) e = (cl > mask_row) ? e : 0.0;
+        racc[k & 3] = fma(e, vj, racc[k & 3]);
+        scr[k * SCR_LD + lane] = e * v_i;  // column k, row `lane`
     }
+    rowacc += (racc[0] + racc[1]) + (racc[2] + racc[3]);
+    // column sums over the warp's 32 rows: lane L sums column L % CPT over rows
+    // (L / CPT) * RPL .. + RPL in 4 chains, then a butterfly over the row blocks (fixed order)
+    __syncwarp();
+    constexpr int RPL = 32 * CPT / 32;  // rows per lane
+    const double* src = scr + (lane % CPT) * SCR_LD + (lane / CPT) * RPL;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; r += 4) {
+        a0 += src[r];
+        a1 += src[r + 1];
+        a2 += src[r + 2];
+        a3 += src[r + 3];
+    }
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = CPT; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane < CPT) colscr_q[colOff + lane] = acc;
+    __syncwarp();
 }
 
 template <int KPT>
@@ -224,7 +247,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         }
         tc::mbar_fence_init();
     }
-    if (tid < 64) tab[tid] = A.exp_tab[tid];
+    for (int i = tid; i < TAB; i += NTHR) tab[i] = g_tab256[i];
     if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
     tc::fence_before();
     __syncthreads();
@@ -255,7 +278,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     uint8_t* cd = sCD + cs * CD_BYTES;
                     tc::bulk_g2s(cd, A.sqs + c0, TJ * 8, cd_full + cs);
                     tc::bulk_g2s(cd + TJ * 8, A.v + c0, TJ * 8, cd_full + cs);
-                    tc::bulk_g2s(cd + TJ * 16, A.cpow + c0, TJ * 8, cd_full + cs);
+                    tc::bulk_g2s(cd + TJ * 16, A.ejs + c0, TJ * 4, cd_full + cs);
                 }
             }
         }
@@ -270,8 +293,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 tc::fence_after();
                 for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
                     const int s = bq % NSTB;
+                    I8_TRACE(true, bq, 8);
                     tc::mbar_wait_sleep(b_full + s, uint32_t((bq / NSTB) & 1));
                     tc::fence_after();
+                    I8_TRACE(true, bq, 9);
                     // Descriptors differ only in the start-address field (16-byte units):
                     // two bases plus compile-time offsets in the fully unrolled sequence.
                     const uint64_t dA0 = tc::smem_desc(aBase, 128, sbo);
@@ -282,6 +307,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                             tc::mbar_wait_sleep(g_empty + c, uint32_t((bq - 1) & 1));
                             tc::fence_after();
                         }
+                        if (c == 7 || c == 4 || c == 0) I8_TRACE(true, bq, c == 7 ? 10 : (c == 4 ? 11 : 12));
                         if (!(A.debug & 1))
 #pragma unroll
                         for (int p = 0; p <= c; ++p)
@@ -300,24 +326,25 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int ew = warp - 2;            // 0..7
+        const int ew = warp - 2;            // 0..NEPI-1
         const int quarter = warp & 3;       // TMEM lane quarter this warp may access
-        const int half = ew >> 2;           // which 32 of the 64 columns
-        const int etid = ew * 32 + lane;    // 0..255
+        const int half = ew >> 2;           // which CPT of the 64 columns
+        const int etid = ew * 32 + lane;
         const int row = quarter * 32 + lane;
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(half * CPT);
-        double* scr = scr_all + ew * C::CH * SCR_LD;
-        const double kabs = -A.ec.kscale;
+        double* scr = scr_all + ew * CPT * SCR_LD;
+        const int kabs_hi = __double2hiint(A.ec.kabs), kabs_lo = __double2loint(A.ec.kabs);
         int tq = 0;
         for (int it = 0; it < nTI; ++it) {
             const int64_t gi = rowBase + int64_t(it) * TI + row;
             const double sqs_i = A.sqs[gi];
             const double v_i = A.v[gi];
-            const double nsi = scalbn(kabs, A.ex[gi] - 34);  // |kscale| 2^(e_i - 34)
+            const int nsi_hi = kabs_hi + (A.ex[gi] - 34) * (1 << 20);  // |kscale| 2^(e_i - 34)
             double rowacc = 0.0;
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++tq) {
                 const uint32_t ph = uint32_t(tq & 1);
                 // prefetch this column's running sum (owner threads; same thread every pass)
+                I8_TRACE(etid == 0, tq, 0);
                 double* cdst = A.part + int64_t(sa) * A.n_pad + colBase + int64_t(jt) * TJ + etid;
                 double cprev = 0.0;
                 if (etid < TJ && it > 0) cprev = *cdst;
@@ -325,19 +352,19 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 // ---- drain the 8 groups in MMA completion order (7 -> 0) two at a time,
                 // 16 columns per tcgen05.ld (register pressure), releasing each pair at once
                 int32_t bint[CPT];
-                double lo[CPT], T[CPT];
+                double lo[CPT];
                 auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
                     tc::mbar_wait(g_full + ca + 1, ph);
                     tc::mbar_wait(g_full + ca, ph);
                     tc::fence_after();
 #pragma unroll
-                    for (int hh = 0; hh < CPT / 16; ++hh) {
-                        uint32_t gl[16], gh[16];
-                        tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ + hh * 16), gl);
-                        tc::tmem_ld16(taddr + uint32_t(ca * TJ + hh * 16), gh);
+                    for (int hh = 0; hh < CPT / 8; ++hh) {
+                        uint32_t gl[8], gh[8];
+                        tc::tmem_ld8(taddr + uint32_t((ca + 1) * TJ + hh * 8), gl);
+                        tc::tmem_ld8(taddr + uint32_t(ca * TJ + hh * 8), gh);
                         tc::tmem_wait_ld();
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) fn(hh * 16 + k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
+                        for (int k = 0; k < 8; ++k) fn(hh * 8 + k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
                     }
                     tc::fence_before();
                     __syncwarp();
@@ -347,46 +374,53 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     }
                 };
                 stage(6, [&](int k, int32_t b) { bint[k] = b; });                    // b3
+                I8_TRACE(etid == 0, tq, 1);
                 stage(4, [&](int k, int32_t b) { lo[k] = magic_pack(b, bint[k]); });  // M1 + Lo
+                I8_TRACE(etid == 0, tq, 2);
                 stage(2, [&](int k, int32_t b) { bint[k] = b; });                    // b1
-                stage(0, [&](int k, int32_t b) {
-                    T[k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
+                I8_TRACE(etid == 0, tq, 3);
+                stage(0, [&](int k, int32_t b) {  // T = H + 2^-28 Lo, parked in the scratch slot
+                    scr[k * SCR_LD + lane] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);
                 });
 
                 // ---- exp, row sums, column sums
+                I8_TRACE(etid == 0, tq, 4);
                 const int cs = tq % NCD;
                 tc::mbar_wait(cd_full + cs, uint32_t((tq / NCD) & 1));
+                I8_TRACE(etid == 0, tq, 5);
                 const uint8_t* cd = sCD + cs * CD_BYTES;
                 const double* cd_sq = reinterpret_cast<const double*>(cd);
                 const double* cd_v = reinterpret_cast<const double*>(cd + TJ * 8);
-                const double* cd_c = reinterpret_cast<const double*>(cd + TJ * 16);
+                const int* cd_e = reinterpret_cast<const int*>(cd + TJ * 16);
                 double* colscr_q = colscr + ((tq & 1) * 4 + quarter) * TJ;
                 const int colOff = half * CPT;
                 const bool masked = diag && jt < (it + 1) * (TI / TJ);
                 if (A.debug & 2) {
                     double z = 0.0;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) z += T[k];
+                    for (int k = 0; k < CPT; ++k) z += scr[k * SCR_LD + lane];
                     rowacc += z;
                 } else if (masked) {
                     // diagonal block: keep j > i (local column index vs local row index)
                     const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
-                    exp_phase<KPT, true>(T, A, tab, cd_sq, cd_v, cd_c, scr, colscr_q, nsi, sqs_i, v_i,
+                    exp_phase<true>(A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
                                          rowacc, lane, colOff, mask_row);
                 } else {
-                    exp_phase<KPT, false>(T, A, tab, cd_sq, cd_v, cd_c, scr, colscr_q, nsi, sqs_i, v_i,
+                    exp_phase<false>(A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
                                           rowacc, lane, colOff, 0);
                 }
+                I8_TRACE(etid == 0, tq, 6);
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(cd_empty + cs);
                 epi_bar();
+                I8_TRACE(etid == 0, tq, 7);
                 if (etid < TJ) {
                     const double* q4 = colscr + (tq & 1) * 4 * TJ + etid;
                     const double s4 = ((q4[0] + q4[TJ]) + q4[2 * TJ]) + q4[3 * TJ];
                     *cdst = cprev + s4;
                 }
             }
-            // row partials of this I tile: combine the two column halves in fixed order
+            // row partials of this I tile: combine the column parts in fixed order
             rowbuf[half * TI + row] = rowacc;
             epi_bar();
             if (diag) {
@@ -396,11 +430,17 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     for (int h = 0; h < TI / TJ; ++h) {
                         const int r = h * TJ + etid;
                         double* dst = A.part + int64_t(sa) * A.n_pad + rowBase + int64_t(it) * TI + r;
-                        *dst = *dst + (rowbuf[r] + rowbuf[TI + r]);
+                        double rs = rowbuf[r];
+#pragma unroll
+                        for (int h2 = 1; h2 < NEPI / 4; ++h2) rs += rowbuf[h2 * TI + r];
+                        *dst = *dst + rs;
                     }
                 }
             } else if (etid < TI) {
-                A.part[int64_t(sb) * A.n_pad + rowBase + int64_t(it) * TI + etid] = rowbuf[etid] + rowbuf[TI + etid];
+                double rs = rowbuf[etid];
+#pragma unroll
+                for (int h2 = 1; h2 < NEPI / 4; ++h2) rs += rowbuf[h2 * TI + etid];
+                A.part[int64_t(sb) * A.n_pad + rowBase + int64_t(it) * TI + etid] = rs;
             }
         }
     }
@@ -412,7 +452,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
 
 // ---- operand preparation
 __global__ void row_exponent_kernel(const double* __restrict__ X, int64_t n, int64_t d, int64_t n_pad,
-                                    int* __restrict__ ex, double* __restrict__ cpow) {
+                                    int* __restrict__ ex, int* __restrict__ ejs) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < n_pad; i += warps) {
@@ -424,7 +464,7 @@ __global__ void row_exponent_kernel(const double* __restrict__ X, int64_t n, int
         if (lane == 0) {
             const int e = m > 0.0 ? ilogb(m) + 1 : 0;
             ex[i] = e;
-            cpow[i] = scalbn(1.0, e);
+            ejs[i] = e * (1 << 20);
         }
     }
 }
@@ -464,7 +504,29 @@ void launch_kp(const I8Args& a, int64_t num_tiles, cudaStream_t stream) {
     gauss_matvec_i8_kernel<KPT><<<unsigned(num_tiles), NTHR, smem, stream>>>(a);
 }
 
+// kscale of the 1/256-octave exp: -scale 256 / ln2 = 4 x the 1/64-octave K1 constant (exact)
+double i8_kscale(double kscale64) { return 4.0 * kscale64; }
+
+void ensure_table(cudaStream_t stream) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    KRR_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && done[dev]) return;
+    double t[TAB];
+    for (int j = 0; j < TAB; ++j) t[j] = double(exp2l((long double)j / TAB));
+    KRR_CUDA(cudaMemcpyToSymbolAsync(g_tab256, t, sizeof(t), 0, cudaMemcpyHostToDevice, stream));
+    KRR_CUDA(cudaStreamSynchronize(stream));
+    if (dev < 64) done[dev] = true;
+}
+
 }  // namespace
+
+void i8_read_trace(long long* out, int count) {
+    count = std::min(count, TRACE_TILES * 16);
+    KRR_CUDA(cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * size_t(count)));
+}
 
 bool i8_supported(int64_t d, int st) {
     const int kp = int((d + 31) / 32 * 32);
@@ -474,19 +536,21 @@ bool i8_supported(int64_t d, int st) {
 int i8_kp(int64_t d) { return int((d + 31) / 32 * 32); }
 
 bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp,
-                       double kscale, uint8_t* S, int* ex, double* cpow, double* sqs, cudaStream_t stream) {
+                       double kscale, uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream) {
     const int kp = i8_kp(d);
+    const double ks = i8_kscale(kscale);
     const unsigned wblocks = unsigned(std::min<int64_t>((n_pad + 7) / 8, 148 * 16));
-    row_exponent_kernel<<<wblocks, 256, 0, stream>>>(X, n, d, n_pad, ex, cpow);
+    row_exponent_kernel<<<wblocks, 256, 0, stream>>>(X, n, d, n_pad, ex, ejs);
     KRR_LAUNCH_CHECK();
     const int64_t total = n_pad * kp;
     slice_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(X, n, d, n_pad, kp,
                                                                                                  ex, S);
     KRR_LAUNCH_CHECK();
     scaled_sq_kernel<<<unsigned(std::min<int64_t>((n_pad + 255) / 256, 148 * 8)), 256, 0, stream>>>(
-        L, n_pad, dp, int(d), kscale, sqs);
+        L, n_pad, dp, int(d), ks, sqs);
     KRR_LAUNCH_CHECK();
-    // exponent range: |kscale| 2^(e_i + e_j - 34) must stay a normal double
+    // exponent range: (1) |kscale| 2^(e_i + e_j - 34) stays a normal double;
+    // (2) |y| = |kscale| d2 <= |kscale| 4 d 2^(2 e_max) < 2^50 (the 1.5 * 2^52 rounding shifter)
     std::vector<int> h(static_cast<size_t>(n_pad));
     KRR_CUDA(cudaMemcpyAsync(h.data(), ex, sizeof(int) * size_t(n_pad), cudaMemcpyDeviceToHost, stream));
     KRR_CUDA(cudaStreamSynchronize(stream));
@@ -495,30 +559,40 @@ bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, con
         lo = std::min(lo, e);
         hi = std::max(hi, e);
     }
-    // (1) |kscale| 2^(e_i + e_j - 34) stays a normal double;
-    // (2) |y| = |kscale| d2 <= |kscale| 4 d 2^(2 e_max) < 2^50 (the 1.5 * 2^52 rounding shifter)
-    const int ek = std::ilogb(-kscale);
-    const double ymax = -kscale * 4.0 * double(d) * std::ldexp(1.0, 2 * hi);
+    const int ek = std::ilogb(-ks);
+    const double ymax = -ks * 4.0 * double(d) * std::ldexp(1.0, 2 * hi);
     return ek + 2 * lo - 34 > -1000 && ek + 2 * hi - 34 < 1000 && ymax < std::ldexp(1.0, 50);
 }
 
-void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const double* cpow,
+void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const int* ejs,
                             const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
                             int debug) {
     if (p.num_tiles == 0) return;
+    ensure_table(stream);
     I8Args a;
     a.S = S;
     a.ex = ex;
-    a.cpow = cpow;
+    a.ejs = ejs;
     a.sqs = sqs;
     a.v = v;
     a.part = part;
     a.tiles = p.tiles;
-    a.exp_tab = p.exp_tab;
     a.n_pad = p.n_pad;
     a.st = p.st;
-    a.ec = p.ec;
     a.debug = debug;
+    const long double ln2 = 0.693147180559945309417232121458176568L;
+    const long double l = ln2 / TAB;
+    a.ec.kabs = -i8_kscale(p.ec.kscale);
+    long double term = 1.0L;
+    double c[5];
+    for (int m = 1; m <= 4; ++m) {
+        term = term * l / (long double)m;
+        c[m] = double(term);
+    }
+    a.ec.a1 = c[1];
+    a.ec.a2 = c[2];
+    a.ec.a3 = c[3];
+    a.ec.a4 = c[4];
     if (kp == 32) launch_kp<32>(a, p.num_tiles, stream);
     else if (kp == 64) launch_kp<64>(a, p.num_tiles, stream);
     else if (kp == 96) launch_kp<96>(a, p.num_tiles, stream);

@@ -240,11 +240,13 @@ Schedule make_schedule(int64_t n, int world, int rank) {
     s.ns = nsuper(st);
     s.n_pad = s.ns * st;
     // Heaviest (off-diagonal, full) super-tiles first, diagonal (half) last, dealt
-    // round-robin over ranks so every rank gets the same work within one tile.
+    // round-robin over ranks so every rank gets the same work within one tile.  Column
+    // super-tile major: CTAs resident at the same time share their column (J) super-tile,
+    // which the K1 kernels stream repeatedly, so those re-reads hit L2 instead of HBM.
     std::vector<std::pair<int32_t, int32_t>> order;
     order.reserve(size_t(s.ns * (s.ns + 1) / 2));
-    for (int64_t a = 0; a < s.ns; ++a)
-        for (int64_t b = a + 1; b < s.ns; ++b) order.emplace_back(int32_t(a), int32_t(b));
+    for (int64_t b = 1; b < s.ns; ++b)
+        for (int64_t a = 0; a < b; ++a) order.emplace_back(int32_t(a), int32_t(b));
     for (int64_t a = 0; a < s.ns; ++a) order.emplace_back(int32_t(a), int32_t(a));
     s.owned.assign(size_t(s.ns * s.ns), 0);
     for (size_t q = 0; q < order.size(); ++q) {

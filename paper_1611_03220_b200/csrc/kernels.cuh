@@ -41,12 +41,14 @@ void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const do
 
 // K1-I8: tcgen05 kind::i8 slice path (gauss_matvec_i8.cu).  Supported for d <= 96.
 bool i8_supported(int64_t d, int st);
+void i8_read_trace(long long* out, int count);
 int i8_kp(int64_t d);
-// Builds the slices S, row exponents ex (and 2^ex), sq' = kscale |x|^2; returns false
-// when the data's exponent range would leave the range the fused epilogue handles.
+// Builds the slices S, row exponents ex (and ex << 20), sq' = kscale' |x|^2 (kscale' of the
+// 1/256-octave exp); returns false when the data's exponent range would leave the range
+// the fused epilogue handles.
 bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp,
-                       double kscale, uint8_t* S, int* ex, double* cpow, double* sqs, cudaStream_t stream);
-void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const double* cpow,
+                       double kscale, uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream);
+void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const int* ejs,
                             const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
                             int debug = 0);
 

@@ -123,13 +123,13 @@ struct Ctx {
     DevMem<int2> tiles;
     DevMem<uint8_t> owned;
     // K1-I8 operands (int8 slices, row exponents, |x|^2)
-    int k1_path = 0;  // 0 = FP64 DMMA, 1 = tcgen05 INT8 slices
+    int k1_path = -1;  // -1 auto, 0 = FP64 DMMA, 1 = tcgen05 INT8 slices
     int i8_debug = 0; // profiling knob for K1-I8 (bit 0: skip MMAs, bit 1: skip exp phase)
     bool i8_ready = false;
     int kp8 = 0;
     DevMem<uint8_t> S8;
-    DevMem<int> ex8;
-    DevMem<double> sq8, cpow8;
+    DevMem<int> ex8, ejs8;
+    DevMem<double> sq8;
 
     // PCG vectors (n_pad each) and reduction scratch
     DevMem<double> vin, vout, vx, vr, vz, vp, vap, vy, red, scal, mat_a, mat_b;
@@ -167,12 +167,21 @@ void allreduce_sum(Ctx& c, double* buf, int64_t count) {
                "ncclAllReduce");
 }
 
+// K1 path selection: the INT8-slice tensor-core kernel where it is faster than the FP64
+// DMMA kernel on B200 (measured: d >= ~48, profiles/README.md) and the data's exponent range
+// allows it; the DMMA kernel otherwise.  Both are GPU kernels; neither is a fallback.
+bool use_i8(const Ctx& c) {
+    if (!c.i8_ready) return false;
+    if (c.k1_path >= 0) return c.k1_path == 1;
+    return c.d >= 48;
+}
+
 // out (n_pad) = (K + lambda I) v, v zero-padded to n_pad.  Replicated on all ranks.
 void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t k1a = nullptr,
                 cudaEvent_t k1b = nullptr) {
     if (k1a) KRR_CUDA(cudaEventRecord(k1a, c.stream));
-    if (c.k1_path == 1 && c.i8_ready)
-        gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.cpow8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
+    if (use_i8(c))
+        gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.ejs8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
                                c.stream, c.i8_debug);
     else
         gauss_matvec_launch(c.plan, v, c.part.get(), c.exp_mode, c.stream);
@@ -241,10 +250,10 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
         c.kp8 = i8_kp(d);
         c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
         c.ex8.ensure(size_t(n_pad));
-        c.cpow8.ensure(size_t(n_pad));
+        c.ejs8.ensure(size_t(n_pad));
         c.sq8.ensure(size_t(n_pad));
         c.i8_ready = i8_prepare_launch(c.X.get(), n, d, n_pad, c.L.get(), dp, p.ec.kscale, c.S8.get(), c.ex8.get(),
-                                       c.cpow8.get(), c.sq8.get(), c.stream);
+                                       c.ejs8.get(), c.sq8.get(), c.stream);
     }
     p.resident = c.k1_resident;
     p.warps16 = c.k1_warps16;
@@ -821,12 +830,35 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
         } else if (k == "i8_debug") {
             c.i8_debug = int(value);
         } else if (k == "k1_path") {
-            if (value != 0.0 && value != 1.0) fail(KRR_ERR_INVALID_ARGUMENT, "k1_path must be 0 (dmma) or 1 (i8)");
+            if (value != 0.0 && value != 1.0 && value != -1.0)
+                fail(KRR_ERR_INVALID_ARGUMENT, "k1_path must be -1 (auto), 0 (dmma) or 1 (i8)");
             c.k1_path = int(value);
         } else if (k == "batched_rhs") {
             c.batched = value != 0.0;
         } else if (k == "exp_mode") {
             c.exp_mode = value != 0.0 ? 1 : 0;
+        } else {
+            fail(KRR_ERR_INVALID_ARGUMENT, "unknown option '" + k + "'");
+        }
+    });
+}
+
+int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        const std::string k = key ? key : "";
+        if (k == "k1_path") {
+            *value = c.k1_path;
+        } else if (k == "k1_path_effective") {  // the K1 kernel a mat-vec runs now
+            krr::require_data(c);
+            *value = krr::use_i8(c) ? 1.0 : 0.0;
+        } else if (k == "i8_supported") {
+            krr::require_data(c);
+            *value = c.i8_ready ? 1.0 : 0.0;
+        } else if (k == "exp_mode") {
+            *value = c.exp_mode;
+        } else if (k == "batched_rhs") {
+            *value = c.batched ? 1.0 : 0.0;
         } else {
             fail(KRR_ERR_INVALID_ARGUMENT, "unknown option '" + k + "'");
         }
@@ -1237,6 +1269,14 @@ int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, d
         if (size_t(128 + N) * size_t(kbytes) > 200 * 1024) fail(KRR_ERR_INVALID_ARGUMENT, "operands exceed smem");
         c.set_device();
         *cycles_per_mma = krr::i8_mma_rate(N, reps, kbytes, mode, c.stream);
+    });
+}
+
+int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        c.set_device();
+        krr::i8_read_trace(out, count);
     });
 }
 

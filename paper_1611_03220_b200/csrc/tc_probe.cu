@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128) i8_probe_kernel(const int8_t* __restrict_
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tmem, N < 32 ? 32 : N);
+    if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
 // MMA throughput: one CTA per SM issues `reps` back-to-back tcgen05.mma (M = 128, N, K = 32)

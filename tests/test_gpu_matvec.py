@@ -132,9 +132,10 @@ def test_device_matvec_entry_and_launch_count(krr, oracle, ctx):
 
 @pytest.mark.parametrize("n,d", [(1000, 16), (3000, 90), (700, 54), (5000, 20), (40000, 90), (33000, 5)])
 def test_resident_and_streaming_variants_bitwise_equal(krr, oracle, ctx, n, d):
-    """The two K1 pipeline shapes do the same arithmetic in the same order."""
+    """The DMMA K1 pipeline shapes do the same arithmetic in the same order."""
     x = oracle.random_matrix(n, d, 31)
     v = oracle.random_vector(n, 32)
+    ctx.set_option("k1_path", 0)
     op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(5.0), 1e-4, ctx=ctx)
     a = op(v)
     ctx.set_option("k1_grouped", 0)
@@ -165,6 +166,24 @@ def test_resident_and_streaming_variants_bitwise_equal(krr, oracle, ctx, n, d):
 def test_set_option_rejects_unknown(krr, ctx):
     with pytest.raises(ValueError):
         ctx.set_option("no_such_knob", 1)
+    with pytest.raises(ValueError):
+        ctx.get_option("no_such_knob")
+    with pytest.raises(ValueError):
+        ctx.set_option("k1_path", 2)
+
+
+@pytest.mark.parametrize("d,want", [(16, 0), (47, 0), (48, 1), (90, 1), (96, 1), (97, 0)])
+def test_k1_path_auto_selection(krr, oracle, ctx, d, want):
+    """Auto path: INT8-slice tensor-core K1 for 48 <= d <= 96, FP64 DMMA otherwise; both
+    match the oracle."""
+    n = 600
+    x = oracle.random_matrix(n, d, 7)
+    v = oracle.random_vector(n, 8)
+    assert ctx.get_option("k1_path") == -1
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(6.0), 1e-3, ctx=ctx)
+    assert ctx.get_option("k1_path_effective") == want
+    assert ctx.get_option("i8_supported") == (1 if d <= 96 else 0)
+    assert rel(op(v), oracle.kernel_matvec(x, 6.0, 1e-3, v)) <= 1e-13
 
 
 I8_CASES = [(1, 1, 1.0), (5, 4, 0.7), (127, 3, 1.5), (300, 4, 1.7), (1000, 90, 6.0), (4097, 16, 4.0),

@@ -1,0 +1,34 @@
+"""K1-I8 per-tile timeline of CTA 0 (clock64 stamps; i8_debug bit 2).
+
+python tools/i8_trace.py [n] [d] [extra debug bits]
+"""
+import ctypes as C
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1611_03220_b200 as krr  # noqa: E402
+from paper_1611_03220_b200 import _lib  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 90
+extra = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+ctx = krr.Context(0)
+x = np.random.default_rng(0).standard_normal((n, d))
+_lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, 6.0))
+ctx.set_option("k1_path", 1)
+tot, k1 = C.c_double(), C.c_double()
+_lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))
+ctx.set_option("i8_debug", 4 | extra)
+_lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))
+buf = np.zeros(64 * 16, dtype=np.int64)
+_lib.check(_lib.LIB.krr_debug_i8_trace(ctx.handle, buf.ctypes.data_as(C.c_void_p), buf.size))
+t = buf.reshape(64, 16)
+t0 = t[0, 0]
+names = ["start", "st6", "st4", "st2", "st0", "cd", "exp", "bar", "m:bfull?", "m:bfull", "m:g7", "m:g4", "m:g0"]
+print("tile " + " ".join(f"{nm:>8s}" for nm in names))
+for q in range(1, 40):
+    row = t[q]
+    print(f"{q:4d} " + " ".join(f"{(row[i] - t[q, 0]):8d}" for i in range(13)), f" dt={t[q + 1, 0] - t[q, 0]}")
