@@ -20,12 +20,12 @@
 //     T = H + 2^-28 Lo  (one rounding)  =  2^21 sum_c 2^(-7c) G_c
 // via the 1.5 * 2^52 bit trick (a 64-bit integer multiply-add into the mantissa field +
 // one DADD / DFMA), so -2 x_i.x_j = -2^(e_i + e_j - 34) T.  The exp argument is formed
-// directly in units of 1/256 octave,
+// directly in units of 1/64 octave,
 //     y = kscale d2 = sq'_i + sq'_j + |kscale| 2^(e_i - 34) 2^(e_j) T,   sq' = kscale |x|^2,
-// with kscale = -scale 256 / ln2 (the per-column power of two is an integer add on the high
-// word), and e = 2^(k/256) (1 + q(f)), k = round(y), f = y - k, from a 256-entry table and
-// a degree-4 polynomial (truncation error 4e-17 relative).  Dot-product error
-// <= ~2^-52 * d * 2^(e_i + e_j), the order of an fp64 dot product's own bound.
+// with kscale = -scale 64 / ln2 (the per-column power of two is an integer add on the high
+// word), and e = 2^(k/64) (1 + q(f)), k = round(y), f = y - k, from the K1 64-entry table
+// (replicated 16x in shared memory so a warp's lookups are bank-conflict free) and a
+// degree-5 polynomial.  Dot-product error <= ~2^-52 * d * 2^(e_i + e_j), the order of an fp64 dot product's own bound.
 //
 // Structure (one CTA per symmetric super-tile, 10 warps, tiles of M = 128 rows x N = 64
 // columns):
@@ -66,18 +66,19 @@ constexpr int P = 8;      // slices
 constexpr int NGRP = 8;   // groups c = p + q in [0, 7]
 constexpr int TI = 128;   // I tile rows (MMA M)
 constexpr int TJ = 64;    // J tile columns (MMA N)
-constexpr int NCD = 4;    // column-data stages
+constexpr int NCD = 3;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
-constexpr int CPT = 16;   // columns per epilogue thread
+constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int KP_MAX = 96;
 constexpr int SCR_LD = 33;  // transpose scratch row stride (doubles): conflict-free both ways
 constexpr int CD_BYTES = TJ * 8 * 2 + TJ * 4;  // sq', v, e_j << 20
-constexpr int TAB = 256;
-constexpr int YMIN_K = -1022 * TAB;  // 2^(k/256) stays normal
+constexpr int TAB = 64;    // 2^(j/64), replicated per lane pair: conflict-free lookups
+constexpr int TAB_REP = 16;
+constexpr int YMIN_K = -1022 * TAB;  // 2^(k/64) stays normal
 
-__device__ double g_tab256[TAB];
+__device__ double g_tab64[TAB];
 // profiling trace (i8_debug bit 2): clock64 stamps of CTA 0, 16 per tile, first 64 tiles
 constexpr int TRACE_TILES = 64;
 __device__ long long g_trace[TRACE_TILES * 16];
@@ -96,16 +97,15 @@ struct Cfg {
     static constexpr size_t OFF_CD = OFF_B + NSTB * B_BYTES;
     static constexpr size_t OFF_SCR = OFF_CD + NCD * CD_BYTES;
     static constexpr size_t OFF_COLSCR = OFF_SCR + size_t(NEPI) * CPT * SCR_LD * 8;
-    static constexpr size_t OFF_ROWBUF = OFF_COLSCR + 2 * 4 * TJ * 8;
-    static constexpr size_t OFF_TAB = OFF_ROWBUF + (NEPI / 4) * TI * 8;
-    static constexpr size_t OFF_BARS = OFF_TAB + TAB * 8;
+    static constexpr size_t OFF_TAB = OFF_COLSCR + 2 * 4 * TJ * 8;
+    static constexpr size_t OFF_BARS = OFF_TAB + TAB * TAB_REP * 8;
     static constexpr int NBARS = 2 + 2 * NSTB + 2 * NCD + 2 * NGRP;
     static constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
 };
 
 struct I8Consts {
-    double kabs;            // |kscale| = scale 256 / ln2
-    double a1, a2, a3, a4;  // (ln2/256)^m / m!
+    double kabs;                // |kscale| = scale 64 / ln2
+    double a1, a2, a3, a4, a5;  // (ln2/64)^m / m!
 };
 
 struct I8Args {
@@ -141,39 +141,59 @@ __device__ __forceinline__ double magic_pack(int32_t a, int32_t b) {
 constexpr double M2 = 6755401588539392.0 + 25165832.0;  // M1 = 1.5 * 2^52 + 2^31, M2 = M1 (1 + 2^-28)
 
 template <bool MASK>
-__device__ __forceinline__ void exp_phase(const I8Consts& ec, const double* __restrict__ tab,
+__device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts& ec, const double* __restrict__ tab,
                                           const double* __restrict__ cd_sq, const double* __restrict__ cd_v,
                                           const int* __restrict__ cd_e, double* __restrict__ scr,
                                           double* __restrict__ colscr_q, int nsi_hi, int nsi_lo, double sqs_i,
                                           double v_i, double& rowacc, int lane, int colOff, int mask_row) {
     const double shifter = 6755399441055744.0;  // 1.5 * 2^52
     double racc[4] = {0.0, 0.0, 0.0, 0.0};
+    // four columns at a time, each step applied across the batch: independent chains
+    // side by side for the scheduler (the per-pair chain is ~16 dependent FP64 ops)
+    constexpr int BW = 4;
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-        const int cl = colOff + k;  // column within the 64-wide tile
-        const double sqj = cd_sq[cl];
-        const double vj = cd_v[cl];
-        const double nscale = __hiloint2double(nsi_hi + cd_e[cl], nsi_lo);
-        // T of (row `lane`, column k) was parked in this thread's scratch slot by the drain
-        double y = fma(scr[k * SCR_LD + lane], nscale, sqs_i + sqj);
-        // y <= 0 (d2 >= 0): y > 0 (rounding, near-duplicate rows) has a non-negative high
-        // word; clamping it to 0 leaves a positive denormal, whose exp is 1 exactly.
-        y = __hiloint2double(min(__double2hiint(y), 0), __double2loint(y));
-        const double t2 = y + shifter;
-        const double kd = t2 - shifter;
-        const double f = y - kd;
-        double q = fma(f, ec.a4, ec.a3);
-        q = fma(q, f, ec.a2);
-        q = fma(q, f, ec.a1);
-        q = q * f;
-        // k >= -1022 * 256 keeps 2^(k/256) normal (e >= ~2^-1022 instead of underflowing)
-        const int kk = max(__double2loint(t2), YMIN_K);
-        const double tj = tab[kk & (TAB - 1)];
-        const double ts = __hiloint2double(__double2hiint(tj) + (kk >> 8) * (1 << 20), __double2loint(tj));
-        double e = fma(ts, q, ts);
-        if constexpr (MASK) e = (cl > mask_row) ? e : 0.0;
-        racc[k & 3] = fma(e, vj, racc[k & 3]);
-        scr[k * SCR_LD + lane] = e * v_i;  // column k, row `lane`
+    for (int k0 = 0; k0 < CPT; k0 += BW) {
+        double y[BW], t2[BW], f[BW], q[BW], e[BW];
+        int kk[BW];
+#pragma unroll
+        for (int b = 0; b < BW; ++b) {
+            const int cl = colOff + k0 + b;
+            const double nscale = __hiloint2double(nsi_hi + cd_e[cl], nsi_lo);
+            y[b] = fma(T[k0 + b], nscale, sqs_i + cd_sq[cl]);
+            // y <= 0 (d2 >= 0): y > 0 (rounding, near-duplicate rows) has a non-negative high
+            // word; clamping it to 0 leaves a positive denormal, whose exp is 1 exactly.
+            y[b] = __hiloint2double(min(__double2hiint(y[b]), 0), __double2loint(y[b]));
+        }
+#pragma unroll
+        for (int b = 0; b < BW; ++b) t2[b] = y[b] + shifter;
+#pragma unroll
+        for (int b = 0; b < BW; ++b) f[b] = y[b] - (t2[b] - shifter);
+#pragma unroll
+        for (int b = 0; b < BW; ++b) q[b] = fma(f[b], ec.a5, ec.a4);
+#pragma unroll
+        for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a3);
+#pragma unroll
+        for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a2);
+#pragma unroll
+        for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a1);
+#pragma unroll
+        for (int b = 0; b < BW; ++b) {
+            q[b] = q[b] * f[b];
+            // k >= -1022 * 64 keeps 2^(k/64) normal (e >= ~2^-1022 instead of underflowing)
+            kk[b] = max(__double2loint(t2[b]), YMIN_K);
+        }
+#pragma unroll
+        for (int b = 0; b < BW; ++b) {
+            const double tj = tab[(kk[b] & (TAB - 1)) * TAB_REP + (lane & (TAB_REP - 1))];
+            const double ts = __hiloint2double(__double2hiint(tj) + (kk[b] >> 6) * (1 << 20), __double2loint(tj));
+            e[b] = fma(ts, q[b], ts);
+            if constexpr (MASK) e[b] = (colOff + k0 + b > mask_row) ? e[b] : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < BW; ++b) {
+            racc[b] = fma(e[b], cd_v[colOff + k0 + b], racc[b]);
+            scr[(k0 + b) * SCR_LD + lane] = e[b] * v_i;  // column k, row `lane`
+        }
     }
     rowacc += (racc[0] + racc[1]) + (racc[2] + racc[3]);
     // column sums over the warp's 32 rows: lane L sums column L % CPT over rows
@@ -207,7 +227,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
     uint8_t* sCD = smem + C::OFF_CD;
     double* scr_all = reinterpret_cast<double*>(smem + C::OFF_SCR);
     double* colscr = reinterpret_cast<double*>(smem + C::OFF_COLSCR);  // [2][4 quarters][64]
-    double* rowbuf = reinterpret_cast<double*>(smem + C::OFF_ROWBUF);  // [2 halves][128]
+    double* rowbuf = scr_all;  // [NEPI/4 parts][128], only at pass ends (scratch idle)
     double* tab = reinterpret_cast<double*>(smem + C::OFF_TAB);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BARS);
     uint64_t* a_full = bars;
@@ -247,7 +267,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         }
         tc::mbar_fence_init();
     }
-    for (int i = tid; i < TAB; i += NTHR) tab[i] = g_tab256[i];
+    for (int i = tid; i < TAB * TAB_REP; i += NTHR) tab[i] = g_tab64[i / TAB_REP];
     if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
     tc::fence_before();
     __syncthreads();
@@ -352,20 +372,19 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 // ---- drain the 8 groups in MMA completion order (7 -> 0) two at a time,
                 // 16 columns per tcgen05.ld (register pressure), releasing each pair at once
                 int32_t bint[CPT];
-                double lo[CPT];
+                double lo[CPT], T[CPT];
                 auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
                     tc::mbar_wait(g_full + ca + 1, ph);
                     tc::mbar_wait(g_full + ca, ph);
                     tc::fence_after();
+                    // all loads of the stage in flight before one wait (TMEM load latency
+                    // under load is ~250 clk; one round trip per stage, not per 8 columns)
+                    uint32_t gl[CPT], gh[CPT];
+                    tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ), gl);
+                    tc::tmem_ld16(taddr + uint32_t(ca * TJ), gh);
+                    tc::tmem_wait_ld();
 #pragma unroll
-                    for (int hh = 0; hh < CPT / 8; ++hh) {
-                        uint32_t gl[8], gh[8];
-                        tc::tmem_ld8(taddr + uint32_t((ca + 1) * TJ + hh * 8), gl);
-                        tc::tmem_ld8(taddr + uint32_t(ca * TJ + hh * 8), gh);
-                        tc::tmem_wait_ld();
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) fn(hh * 8 + k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
-                    }
+                    for (int k = 0; k < CPT; ++k) fn(k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
                     tc::fence_before();
                     __syncwarp();
                     if (lane == 0) {
@@ -379,8 +398,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 I8_TRACE(etid == 0, tq, 2);
                 stage(2, [&](int k, int32_t b) { bint[k] = b; });                    // b1
                 I8_TRACE(etid == 0, tq, 3);
-                stage(0, [&](int k, int32_t b) {  // T = H + 2^-28 Lo, parked in the scratch slot
-                    scr[k * SCR_LD + lane] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);
+                stage(0, [&](int k, int32_t b) {
+                    T[k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
                 });
 
                 // ---- exp, row sums, column sums
@@ -398,15 +417,15 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 if (A.debug & 2) {
                     double z = 0.0;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) z += scr[k * SCR_LD + lane];
+                    for (int k = 0; k < CPT; ++k) z += T[k];
                     rowacc += z;
                 } else if (masked) {
                     // diagonal block: keep j > i (local column index vs local row index)
                     const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
-                    exp_phase<true>(A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
+                    exp_phase<true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
                                          rowacc, lane, colOff, mask_row);
                 } else {
-                    exp_phase<false>(A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
+                    exp_phase<false>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
                                           rowacc, lane, colOff, 0);
                 }
                 I8_TRACE(etid == 0, tq, 6);
@@ -442,6 +461,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 for (int h2 = 1; h2 < NEPI / 4; ++h2) rs += rowbuf[h2 * TI + etid];
                 A.part[int64_t(sb) * A.n_pad + rowBase + int64_t(it) * TI + etid] = rs;
             }
+            epi_bar();  // the scratch (row buffer) is reused by the next pass
         }
     }
 
@@ -504,8 +524,8 @@ void launch_kp(const I8Args& a, int64_t num_tiles, cudaStream_t stream) {
     gauss_matvec_i8_kernel<KPT><<<unsigned(num_tiles), NTHR, smem, stream>>>(a);
 }
 
-// kscale of the 1/256-octave exp: -scale 256 / ln2 = 4 x the 1/64-octave K1 constant (exact)
-double i8_kscale(double kscale64) { return 4.0 * kscale64; }
+// kscale of the 1/64-octave table exp (the K1 constant, -scale 64 / ln2)
+double i8_kscale(double kscale64) { return kscale64; }
 
 void ensure_table(cudaStream_t stream) {
     static std::mutex mu;
@@ -515,8 +535,8 @@ void ensure_table(cudaStream_t stream) {
     std::lock_guard<std::mutex> lock(mu);
     if (dev < 64 && done[dev]) return;
     double t[TAB];
-    for (int j = 0; j < TAB; ++j) t[j] = double(exp2l((long double)j / TAB));
-    KRR_CUDA(cudaMemcpyToSymbolAsync(g_tab256, t, sizeof(t), 0, cudaMemcpyHostToDevice, stream));
+    make_exp_table(t);  // 2^(j/64), correctly rounded (the K1 table)
+    KRR_CUDA(cudaMemcpyToSymbolAsync(g_tab64, t, sizeof(t), 0, cudaMemcpyHostToDevice, stream));
     KRR_CUDA(cudaStreamSynchronize(stream));
     if (dev < 64) done[dev] = true;
 }
@@ -584,8 +604,8 @@ void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const in
     const long double l = ln2 / TAB;
     a.ec.kabs = -i8_kscale(p.ec.kscale);
     long double term = 1.0L;
-    double c[5];
-    for (int m = 1; m <= 4; ++m) {
+    double c[6];
+    for (int m = 1; m <= 5; ++m) {
         term = term * l / (long double)m;
         c[m] = double(term);
     }
@@ -593,6 +613,7 @@ void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const in
     a.ec.a2 = c[2];
     a.ec.a3 = c[3];
     a.ec.a4 = c[4];
+    a.ec.a5 = c[5];
     if (kp == 32) launch_kp<32>(a, p.num_tiles, stream);
     else if (kp == 64) launch_kp<64>(a, p.num_tiles, stream);
     else if (kp == 96) launch_kp<96>(a, p.num_tiles, stream);
