@@ -32,6 +32,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
+// Same with per-operand signedness (A / B dtype field: 1 = s8, 0 = u8).
+__host__ __device__ constexpr uint32_t idesc_i8s(int M, int N, bool a_signed, bool b_signed) {
+    return (2u << 4) | (a_signed ? (1u << 7) : 0u) | (b_signed ? (1u << 10) : 0u) | (uint32_t(N >> 3) << 17) |
+           (uint32_t(M >> 4) << 24);
+}
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                        uint32_t accumulate) {

@@ -186,6 +186,23 @@ def test_k1_path_auto_selection(krr, oracle, ctx, d, want):
     assert rel(op(v), oracle.kernel_matvec(x, 6.0, 1e-3, v)) <= 1e-13
 
 
+def test_i8_exponent_range_guard(krr, oracle, ctx):
+    """Rows whose magnitudes would push the fused I8 scale factor out of the normal range
+    (or the exp argument past the 1.5*2^52 rounding shifter) switch the auto path to the
+    DMMA kernel at set_data; results stay exact either way."""
+    n, d = 400, 64
+    x = oracle.random_matrix(n, d, 3)
+    x[7] *= 1e150
+    v = oracle.random_vector(n, 4)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(2.0), 1e-3, ctx=ctx)
+    assert ctx.get_option("i8_supported") == 0
+    assert ctx.get_option("k1_path_effective") == 0
+    assert rel(op(v), oracle.kernel_matvec(x, 2.0, 1e-3, v)) <= 1e-13
+    x[7] /= 1e150
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(2.0), 1e-3, ctx=ctx)
+    assert ctx.get_option("k1_path_effective") == 1
+
+
 I8_CASES = [(1, 1, 1.0), (5, 4, 0.7), (127, 3, 1.5), (300, 4, 1.7), (1000, 90, 6.0), (4097, 16, 4.0),
             (5000, 54, 3.0), (40000, 90, 6.0), (9000, 96, 8.0)]
 
