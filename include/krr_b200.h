@@ -227,7 +227,8 @@ int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C
  * TMEM), 4 TS hoisted + rotating, 5 SS hoisted + rotating + distinct smem tiles, 6 / 7 the
  * K1-I8 tile (N = 64, kp = 96, 36 products in 8 groups) in group-major / A-major order with
  * reps = tiles (N, kbytes ignored); 8-11: FP64 lane-ops / clk / SM of DADD, DADD beside
- * back-to-back MMAs, DFMA, DFMA beside MMAs (reps = iterations). */
+ * back-to-back MMAs, DFMA, DFMA beside MMAs (reps = iterations); 12: 2-SM tcgen05.mma
+ * (cta_group::2, M = 256, clusters of 2), N in {64, 128, 256}. */
 int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, double* cycles_per_mma);
 /* TMEM read throughput (tcgen05.ld.32x32b.x16 + wait in a loop), `warps` warps on every
  * SM; returns bytes per clock per SM. */

@@ -138,6 +138,7 @@ double i8_mma_rate(int N, int reps, int kbytes, int mode, cudaStream_t stream);
 double tmem_ld_rate(int warps, int reps, cudaStream_t stream);
 double i8_tile_order_rate(int order, int tiles, cudaStream_t stream);
 double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream);
+double i8_mma_rate_pair(int N, int reps, cudaStream_t stream);
 void debug_exp_launch(const double* d2, int64_t n, const ExpConsts& ec, const double* tab,
                       int mode, double* out, cudaStream_t stream);
 // results: see krr_microbench in include/krr_b200.h

@@ -1255,6 +1255,12 @@ int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, d
         if (N != 16 && N != 32 && N != 64 && N != 128 && N != 256)
             fail(KRR_ERR_INVALID_ARGUMENT, "N must be 16/32/64/128/256");
         if (kbytes < 32 || kbytes % 32 != 0) fail(KRR_ERR_INVALID_ARGUMENT, "kbytes must be a multiple of 32");
+        if (mode == 12) {  // 2-SM (cta_group::2) MMA, M = 256, N in {64, 128, 256}
+            if (N != 64 && N != 128 && N != 256) fail(KRR_ERR_INVALID_ARGUMENT, "pair mode: N in {64, 128, 256}");
+            c.set_device();
+            *cycles_per_mma = krr::i8_mma_rate_pair(N, std::max(8, reps), c.stream);
+            return;
+        }
         if (mode >= 8 && mode <= 11) {  // FP64 ops/clk/SM: 8 DADD, 9 DADD + MMA, 10 DFMA, 11 DFMA + MMA
             c.set_device();
             *cycles_per_mma = krr::fp64_under_mma((mode - 8) >> 1, (mode - 8) & 1, std::max(64, reps), c.stream);

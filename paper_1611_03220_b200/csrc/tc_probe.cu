@@ -254,6 +254,68 @@ __global__ void __launch_bounds__(256) fp64_under_mma_kernel(int iters, long lon
     if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
+// 2-SM MMA rate: clusters of 2 CTAs; the leader issues `reps` tcgen05.mma.cta_group::2
+// kind::i8 (M = 256: 128 rows from each CTA's smem, N columns split N/2 per CTA) into
+// rotating accumulators; cycles per instruction -> out[blockIdx.x] (both CTAs).
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
+    i8_mma_rate_pair_kernel(int reps, long long* out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tbase;
+    constexpr int KB = 96;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+    for (int i = tid; i < (128 + N / 2) * KB; i += 128) sm[i] = uint8_t(i * 7 + rank);
+    tc::fence_proxy_async();
+    if (tid == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::mbar_fence_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&tbase)),
+                     "r"(512u)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    tc::fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    tc::fence_after();
+    const uint32_t tmem = tbase;
+    constexpr int NACC = (512 / N) < 8 ? (512 / N) : 8;
+    long long t0 = clock64();
+    if (rank == 0 && tid == 0) {
+        // M = 256 (two CTAs), idesc M field = M >> 4
+        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+        const uint64_t da = tc::smem_desc(tc::smem_u32(sm), 128, KB * 8);
+        const uint64_t db = tc::smem_desc(tc::smem_u32(sm + 128 * KB), 128, KB * 8);
+        for (int r = 0; r < reps / 8; ++r) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t off = uint64_t((u % 3) * 16);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + uint32_t((u % NACC) * N)),
+                    "l"(da + off), "l"(db + off), "r"(idesc), "r"(1u));
+            }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                tc::smem_u32(&mbar)),
+            "h"((unsigned short)3)
+            : "memory");
+    }
+    if (tid == 0) {
+        tc::mbar_wait(&mbar, 0);
+        const long long t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+    }
+    tc::fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u) : "memory");
+}
+
 // TMEM read throughput: `warps` warps per CTA (one CTA per SM) each issue `reps`
 // tcgen05.ld.32x32b.x16 (+ wait) from their lane quarter; cycles -> out[blockIdx.x].
 __global__ void tmem_ld_rate_kernel(int reps, long long* out, unsigned* sink) {
@@ -364,6 +426,27 @@ double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream) {
     for (long long v : h) mx = std::max(mx, double(v));
     // FP64 lane-ops per clock per SM: 4 warps x 32 lanes x 8 chains x iters / cycles
     return 4.0 * 32 * 8 * double(iters) / mx;
+}
+
+double i8_mma_rate_pair(int N, int reps, cudaStream_t stream) {
+    long long* d = nullptr;
+    KRR_CUDA(cudaMalloc(&d, 148 * sizeof(long long)));
+    const size_t smem = size_t(128 + N / 2) * 96;
+    auto run = [&](auto kern) {
+        KRR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<148, 128, smem, stream>>>(reps, d);
+    };
+    if (N == 64) run(i8_mma_rate_pair_kernel<64>);
+    else if (N == 128) run(i8_mma_rate_pair_kernel<128>);
+    else run(i8_mma_rate_pair_kernel<256>);
+    KRR_LAUNCH_CHECK();
+    long long h[148];
+    KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d);
+    double mx = 0;
+    for (long long v : h) mx = std::max(mx, double(v));
+    return mx / reps;
 }
 
 double tmem_ld_rate(int warps, int reps, cudaStream_t stream) {

@@ -29,6 +29,12 @@ for mode in (6, 7):
     _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, 64, 200, 96, mode, C.byref(cyc)))
     print(json.dumps({"tile_order": ["group-major", "A-major"][mode - 6], "N": 64, "kp": 96,
                       "cycles_per_mma": round(cyc.value, 2)}), flush=True)
+for n in (64, 128, 256):
+    cyc = C.c_double()
+    _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, n, 4096, 96, 12, C.byref(cyc)))
+    macs_per_sm = 128 * n * 32
+    print(json.dumps({"pair_cta_group2": True, "M": 256, "N": n, "cycles_per_mma": round(cyc.value, 2),
+                      "mac_per_clk_per_sm": round(macs_per_sm / cyc.value, 1)}), flush=True)
 for mode, name in ((8, "DADD"), (9, "DADD+MMA"), (10, "DFMA"), (11, "DFMA+MMA")):
     r = C.c_double()
     _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, 64, 20000, 96, mode, C.byref(r)))
