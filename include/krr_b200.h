@@ -83,8 +83,15 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
  *   "exp_mode"    1|0  table exp (default) | libdevice exp in the Gaussian epilogue
  *   "i8_debug"    bits  profiling only (K1-I8: 1 skip MMAs, 2 skip exp, 4 clock trace) */
 int krr_set_option(krr_ctx* ctx, const char* key, double value);
+/* Arithmetic of the fused mat-vec (SURVEY §8b krr_set_precision; north-star "optional fp32
+ * mode, reported separately"): 64 = fp64, oracle-matching (default); 32 = fp32-accuracy K1
+ * (three bf16 parts per value on tcgen05 kind::f16, fp32 epilogue, d <= 128; relative error
+ * of K v ~1e-6).  PCG vectors, dots and the preconditioner stay fp64 in both modes;
+ * multi-RHS solves run column by column in fp32 mode. */
+int krr_set_precision(krr_ctx* ctx, int bits);
 /* Read a knob back: "k1_path", "exp_mode", "batched_rhs", and (after krr_set_data)
- * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now) and "i8_supported". */
+ * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now), "i8_supported",
+ * and "precision" (64 | 32). */
 int krr_get_option(krr_ctx* ctx, const char* key, double* value);
 
 /* ---------------------------------------------------------------- data + kernel operator */
@@ -221,6 +228,9 @@ int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale,
 /* tcgen05 kind::i8 probe: C (128 x N int32) = A (128 x K int8) . B (N x K int8)^T on
  * one CTA (K % 32 == 0, K <= 256, N in {32, 64}); host buffers, row-major. */
 int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int K, int N);
+/* tcgen05 kind::f16 probe: C (128 x N fp32) = A (128 x K bf16) . B (N x K bf16)^T, K % 16 == 0,
+ * K <= 128, N in {32, 64}; bf16 given as uint16 bit patterns. */
+int krr_debug_bf16_gemm(krr_ctx* ctx, const uint16_t* A, const uint16_t* B, float* C, int K, int N);
 /* cycles per back-to-back tcgen05.mma kind::i8 (M = 128, N in {16, 32, 64, 128, 256}, K = 32),
  * operands in the no-swizzle K-major layout with `kbytes` bytes per row.  mode: 0 SS with
  * per-MMA descriptors, 1 SS hoisted, 2 SS hoisted + rotating accumulators, 3 TS (A in

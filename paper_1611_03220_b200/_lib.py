@@ -111,6 +111,7 @@ _SIGS = {
     "krr_ctx_launch_count": [_vp, C.POINTER(_i64)],
     "krr_set_option": [_vp, C.c_char_p, _d],
     "krr_get_option": [_vp, C.c_char_p, C.POINTER(_d)],
+    "krr_set_precision": [_vp, _i],
     "krr_set_data": [_vp, _vp, _i64, _i64, _d],
     "krr_kernel_matvec": [_vp, _d, _vp, _i64, _vp],
     "krr_kernel_matvec_device": [_vp, _d, _vp, _i64, _vp],
@@ -136,6 +137,7 @@ _SIGS = {
     "krr_microbench": [_vp, _vp],
     "krr_debug_gauss_exp": [_vp, _vp, _i64, _d, _i, _vp],
     "krr_debug_i8_gemm": [_vp, _vp, _vp, _vp, _i, _i],
+    "krr_debug_bf16_gemm": [_vp, _vp, _vp, _vp, _i, _i],
     "krr_debug_i8_mma_rate": [_vp, _i, _i, _i, _i, C.POINTER(_d)],
     "krr_debug_tmem_ld_rate": [_vp, _i, _i, C.POINTER(_d)],
     "krr_debug_i8_trace": [_vp, _vp, _i],
@@ -220,6 +222,10 @@ class Context:
 
     def set_option(self, key: str, value: float) -> None:
         check(LIB.krr_set_option(self.handle, key.encode(), float(value)))
+
+    def set_precision(self, bits: int) -> None:
+        """64: fp64 oracle-matching K v (default); 32: the optional fp32-accuracy mode."""
+        check(LIB.krr_set_precision(self.handle, int(bits)))
 
     def get_option(self, key: str) -> float:
         out = C.c_double()

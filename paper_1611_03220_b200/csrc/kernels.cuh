@@ -41,6 +41,14 @@ void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const do
 
 // K1-I8: tcgen05 kind::i8 slice path (gauss_matvec_i8.cu).  Supported for d <= 96.
 bool i8_supported(int64_t d, int st);
+// K1-F32 (optional fp32-accuracy mode, gauss_matvec_f32.cu): three bf16 parts per value on
+// tcgen05 kind::f16, fp32 epilogue.  d <= 128.
+bool f32_supported(int64_t d, int st);
+int f32_kb(int64_t d);
+void f32_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp, double scale,
+                        uint8_t* S, float* s, cudaStream_t stream);
+void gauss_matvec_f32_launch(const GaussMatvecPlan& p, const uint8_t* S, const float* s, const double* v,
+                             float* v32, double* part, int kb, double scale, cudaStream_t stream);
 void i8_read_trace(long long* out, int count);
 int i8_kp(int64_t d);
 // Builds the slices S, row exponents ex (and ex << 20), sq' = kscale' |x|^2 (kscale' of the
@@ -133,6 +141,8 @@ void precond_z_launch(const double* B, int64_t n, int64_t s, const double* W, co
 // ---------------------------------------------------------------- diagnostics
 // one-CTA tcgen05 kind::i8 GEMM probe: C (128 x N) = A (128 x K) B (N x K)^T, K % 32 == 0
 void i8_probe_launch(const int8_t* A, const int8_t* B, int32_t* C, int K, int N, cudaStream_t stream);
+// same with BF16 inputs (kind::f16, fp32 accumulate), K elements per row (K % 16 == 0)
+void bf16_probe_launch(const uint16_t* A, const uint16_t* B, float* C, int K, int N, cudaStream_t stream);
 // cycles per tcgen05.mma kind::i8 (M = 128, N, K = 32), one CTA per SM, back-to-back
 double i8_mma_rate(int N, int reps, int kbytes, int mode, cudaStream_t stream);
 double tmem_ld_rate(int warps, int reps, cudaStream_t stream);

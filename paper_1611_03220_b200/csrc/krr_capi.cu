@@ -130,6 +130,11 @@ struct Ctx {
     DevMem<uint8_t> S8;
     DevMem<int> ex8, ejs8;
     DevMem<double> sq8;
+    // K1-F32 operands (optional fp32 mode; prepared on first use)
+    int precision = 64;  // 64: fp64 (oracle-matching); 32: fp32-accuracy K1
+    bool f32_ready = false;
+    DevMem<uint8_t> S32;
+    DevMem<float> s32, v32;
 
     // PCG vectors (n_pad each) and reduction scratch
     DevMem<double> vin, vout, vx, vr, vz, vp, vap, vy, red, scal, mat_a, mat_b;
@@ -176,11 +181,28 @@ bool use_i8(const Ctx& c) {
     return c.d >= 48;
 }
 
+void f32_ensure(Ctx& c) {
+    if (c.f32_ready) return;
+    if (!f32_supported(c.d, int(c.sched.st)))
+        fail(KRR_ERR_INVALID_ARGUMENT, "fp32 precision mode supports d <= 128 (got d = " + std::to_string(c.d) + ")");
+    const int kb = f32_kb(c.d);
+    c.S32.ensure(size_t(3) * size_t(c.plan.n_pad) * size_t(kb));
+    c.s32.ensure(size_t(c.plan.n_pad));
+    c.v32.ensure(size_t(c.plan.n_pad));
+    f32_prepare_launch(c.X.get(), c.n, c.d, c.plan.n_pad, c.L.get(), c.plan.dp, c.scale, c.S32.get(), c.s32.get(),
+                       c.stream);
+    c.f32_ready = true;
+}
+
 // out (n_pad) = (K + lambda I) v, v zero-padded to n_pad.  Replicated on all ranks.
 void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t k1a = nullptr,
                 cudaEvent_t k1b = nullptr) {
+    if (c.precision == 32) f32_ensure(c);
     if (k1a) KRR_CUDA(cudaEventRecord(k1a, c.stream));
-    if (use_i8(c))
+    if (c.precision == 32)
+        gauss_matvec_f32_launch(c.plan, c.S32.get(), c.s32.get(), v, c.v32.get(), c.part.get(), f32_kb(c.d), c.scale,
+                                c.stream);
+    else if (use_i8(c))
         gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.ejs8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
                                c.stream, c.i8_debug);
     else
@@ -246,6 +268,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
     p.ns = int(c.sched.ns);
     p.ec = make_exp_consts(c.scale);
     c.i8_ready = false;
+    c.f32_ready = false;
     if (i8_supported(d, int(c.sched.st))) {
         c.kp8 = i8_kp(d);
         c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
@@ -647,7 +670,7 @@ void solve_gaussian(Ctx& c, double lambda, const double* Y, int64_t t, double ta
     c.mat_b.ensure(size_t(n * t));
     KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), Y, sizeof(double) * size_t(n * t), cudaMemcpyHostToDevice,
                              c.stream));
-    if (t > 1 && c.batched) {
+    if (t > 1 && c.batched && c.precision == 64) {
         // Independent columns in batches of T = 8 or 16 sharing every K1T pass.
         const int T = batch_width(t);
         ensure_batched(c, T);
@@ -843,12 +866,22 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
     });
 }
 
+int krr_set_precision(krr_ctx* ctx, int bits) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (bits != 64 && bits != 32) fail(KRR_ERR_INVALID_ARGUMENT, "precision must be 64 (fp64) or 32 (fp32 mode)");
+        c.precision = bits;
+    });
+}
+
 int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
     return guard([&] {
         Ctx& c = *krr::as_ctx(ctx);
         const std::string k = key ? key : "";
         if (k == "k1_path") {
             *value = c.k1_path;
+        } else if (k == "precision") {
+            *value = c.precision;
         } else if (k == "k1_path_effective") {  // the K1 kernel a mat-vec runs now
             krr::require_data(c);
             *value = krr::use_i8(c) ? 1.0 : 0.0;
@@ -907,7 +940,7 @@ int krr_kernel_matvec(krr_ctx* ctx, double lambda, const double* V, int64_t t, d
         c.mat_b.ensure(size_t(n * t));
         KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), V, sizeof(double) * size_t(n * t),
                                  cudaMemcpyHostToDevice, c.stream));
-        if (t > 1 && c.batched) {
+        if (t > 1 && c.batched && c.precision == 64) {
             const int T = krr::batch_width(t);
             krr::ensure_batched(c, T);
             for (int64_t c0 = 0; c0 < t; c0 += T) {
@@ -1245,6 +1278,24 @@ int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C
         KRR_CUDA(cudaMemcpyAsync(b.get(), B, size_t(N * K), cudaMemcpyHostToDevice, c.stream));
         krr::i8_probe_launch(a.get(), b.get(), o.get(), K, N, c.stream);
         KRR_CUDA(cudaMemcpyAsync(C, o.get(), sizeof(int32_t) * size_t(128 * N), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
+int krr_debug_bf16_gemm(krr_ctx* ctx, const uint16_t* A, const uint16_t* B, float* C, int K, int N) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (K <= 0 || K % 16 != 0 || K > 128) fail(KRR_ERR_INVALID_ARGUMENT, "K must be a multiple of 16 <= 128");
+        c.set_device();
+        krr::DevMem<uint16_t> a, b;
+        krr::DevMem<float> o;
+        a.ensure(size_t(128 * K));
+        b.ensure(size_t(N * K));
+        o.ensure(size_t(128 * N));
+        KRR_CUDA(cudaMemcpyAsync(a.get(), A, sizeof(uint16_t) * size_t(128 * K), cudaMemcpyHostToDevice, c.stream));
+        KRR_CUDA(cudaMemcpyAsync(b.get(), B, sizeof(uint16_t) * size_t(N * K), cudaMemcpyHostToDevice, c.stream));
+        krr::bf16_probe_launch(a.get(), b.get(), o.get(), K, N, c.stream);
+        KRR_CUDA(cudaMemcpyAsync(C, o.get(), sizeof(float) * size_t(128 * N), cudaMemcpyDeviceToHost, c.stream));
         c.sync();
     });
 }

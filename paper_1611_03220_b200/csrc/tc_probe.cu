@@ -10,7 +10,9 @@
 namespace krr {
 namespace {
 
-template <int N>
+// BF16 = true: A (128 x K/2), B (N x K/2) are bf16 bit patterns (K = bytes per row), the
+// MMA is kind::f16 with an fp32 accumulator and C receives fp32 bit patterns.
+template <int N, bool BF16 = false>
 __global__ void __launch_bounds__(128) i8_probe_kernel(const int8_t* __restrict__ A, const int8_t* __restrict__ B,
                                                        int32_t* __restrict__ C, int K) {
     extern __shared__ __align__(128) uint8_t sm[];
@@ -32,11 +34,12 @@ __global__ void __launch_bounds__(128) i8_probe_kernel(const int8_t* __restrict_
     tc::fence_after();
     const uint32_t tmem = tbase;
     if (tid == 0) {
-        const uint32_t idesc = tc::idesc_i8(128, N);
+        const uint32_t idesc = BF16 ? tc::idesc_bf16(128, N) : tc::idesc_i8(128, N);
         for (int ks = 0; ks < K / 32; ++ks) {
             const uint64_t da = tc::smem_desc(tc::smem_u32(sA) + ks * 2 * (128 * 16), 128 * 16, 128);
             const uint64_t db = tc::smem_desc(tc::smem_u32(sB) + ks * 2 * (N * 16), N * 16, 128);
-            tc::mma_i8(tmem, da, db, idesc, ks > 0 ? 1u : 0u);
+            if constexpr (BF16) tc::mma_f16(tmem, da, db, idesc, ks > 0 ? 1u : 0u);
+            else tc::mma_i8(tmem, da, db, idesc, ks > 0 ? 1u : 0u);
         }
         tc::mma_commit(&mbar);
     }
@@ -465,6 +468,24 @@ double tmem_ld_rate(int warps, int reps, cudaStream_t stream) {
     for (long long v : h) mx = std::max(mx, double(v));
     // bytes per clock per SM: warps x reps x (32 lanes x 16 columns x 4 B) / cycles
     return double(warps) * reps * 2048.0 / mx;
+}
+
+void bf16_probe_launch(const uint16_t* A, const uint16_t* B, float* C, int Kel, int N, cudaStream_t stream) {
+    const int K = 2 * Kel;  // bytes per row
+    const size_t smem = size_t(128 + N) * K;
+    const auto* a = reinterpret_cast<const int8_t*>(A);
+    const auto* b = reinterpret_cast<const int8_t*>(B);
+    auto* c = reinterpret_cast<int32_t*>(C);
+    if (N == 32) {
+        KRR_CUDA(cudaFuncSetAttribute(i8_probe_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        i8_probe_kernel<32, true><<<1, 128, smem, stream>>>(a, b, c, K);
+    } else if (N == 64) {
+        KRR_CUDA(cudaFuncSetAttribute(i8_probe_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        i8_probe_kernel<64, true><<<1, 128, smem, stream>>>(a, b, c, K);
+    } else {
+        fail(KRR_ERR_INVALID_ARGUMENT, "bf16 probe: N must be 32 or 64");
+    }
+    KRR_LAUNCH_CHECK();
 }
 
 void i8_probe_launch(const int8_t* A, const int8_t* B, int32_t* C, int K, int N, cudaStream_t stream) {

@@ -245,3 +245,46 @@ def test_i8_symmetry_diagonal_and_scaled_rows(krr, oracle, ctx):
     assert np.max(np.abs(kk - want)) <= 2e-15
     assert np.max(np.abs(kk1 - want[:, ::37])) <= 2e-15
     assert kk[5, 6] == 1.0
+
+
+F32_CASES = [(1, 1, 1.0), (300, 4, 1.7), (1000, 90, 6.0), (4097, 16, 4.0), (5000, 54, 3.0), (40000, 90, 6.0),
+             (3000, 128, 8.0), (2000, 100, 5.0)]
+
+
+@pytest.mark.parametrize("n,d,sigma", F32_CASES)
+def test_f32_mode_matvec(krr, oracle, ctx, n, d, sigma):
+    """Optional fp32 mode (three bf16 parts on tcgen05 kind::f16, fp32 epilogue): K v within
+    fp32-level error of the fp64 oracle; the default stays fp64."""
+    x = oracle.random_matrix(n, d, 5 + n)
+    v = oracle.random_vector(n, 7 + n)
+    assert ctx.get_option("precision") == 64
+    ctx.set_precision(32)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(sigma), 1e-3, ctx=ctx)
+    got = op(v)
+    assert ctx.get_option("precision") == 32
+    want = oracle.kernel_matvec(x, sigma, 1e-3, v)
+    assert rel(got, want) <= 2e-6, rel(got, want)
+    assert np.array_equal(op(v), got)  # deterministic
+    ctx.set_precision(64)
+    assert rel(op(v), want) <= 1e-13
+
+
+def test_f32_mode_gram_entries(krr, oracle, ctx):
+    n, d = 300, 6
+    x = oracle.random_matrix(n, d, 2)
+    ctx.set_precision(32)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(2.0), 0.0, ctx=ctx)
+    cols = np.column_stack([op(np.eye(n)[:, j]) for j in range(0, n, 29)])
+    want = oracle.gram_matrix(x, 2.0)[:, ::29]
+    assert np.max(np.abs(cols - want)) <= 2e-6
+    assert np.all(np.abs(cols[np.arange(0, n, 29), np.arange(cols.shape[1])] - 1.0) == 0.0)  # K_ii = 1 exactly
+
+
+def test_f32_mode_rejects_wide_d_and_bad_bits(krr, oracle, ctx):
+    with pytest.raises(ValueError):
+        ctx.set_precision(16)
+    x = oracle.random_matrix(200, 129, 1)
+    ctx.set_precision(32)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(5.0), 1e-3, ctx=ctx)
+    with pytest.raises(ValueError):
+        op(np.ones(200))

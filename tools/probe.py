@@ -25,7 +25,7 @@ MB_KEYS = ["dmma_tflops", "dfma_tflops", "mixed_tflops", "exp_libdevice_gevals",
 def report(n, d, ms, k1, t_set, res, exp_mode, warps, grouped=0, path=0):
     pairs = n * (n - 1) / 2
     dp = (d + 2 + 3) // 4 * 4
-    row = {"n": n, "d": d, "path": ["dmma", "i8"][path], "resident": res, "warps": warps, "grouped": grouped, "exp_mode": exp_mode, "ms_per_matvec": ms, "k1_ms": k1,
+    row = {"n": n, "d": d, "path": ["dmma", "i8", "f32"][path], "resident": res, "warps": warps, "grouped": grouped, "exp_mode": exp_mode, "ms_per_matvec": ms, "k1_ms": k1,
            "gevals_per_s": n * n / (ms * 1e-3) / 1e9,
            "unique_pairs_per_s": pairs / (k1 * 1e-3) / 1e9,
            "dot_tflops": pairs * 2 * d / (k1 * 1e-3) / 1e12,
@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--grouped", type=int, default=-1, help="-1: both (resident 8-warp only)")
     ap.add_argument("--path", type=int, default=0, help="K1 path: 0 = FP64 DMMA, 1 = tcgen05 INT8 slices, -1 both")
     ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--precision", type=int, default=64, help="64 (fp64) or 32 (fp32 mode)")
     ap.add_argument("--i8-debug", default="0", help="comma list of K1-I8 profiling modes (1 no MMA, 2 no exp)")
     args = ap.parse_args()
     out = {}
@@ -69,6 +70,7 @@ def main():
         combos = [(r, w, gp, pa) for pa in paths for (r, w, gp) in (combos if pa == 0 else [(1, 8, 1)])]
         dbgs = [int(v) for v in args.i8_debug.split(",")]
         combos = [(r, w, gp, pa, dbg) for (r, w, gp, pa) in combos for dbg in (dbgs if pa == 1 else [0])]
+        ctx.set_precision(args.precision)
         for res, w, gp, pa, dbg in combos:
             ctx.set_option("k1_path", pa)
             ctx.set_option("i8_debug", dbg)
@@ -81,7 +83,8 @@ def main():
             _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, args.steps, C.byref(tot), C.byref(k1)))
             if dbg:
                 print(json.dumps({"i8_debug": dbg}), flush=True)
-            rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode, w, gp, pa))
+            rows.append(report(n, d, tot.value / args.steps, k1.value, t_set, res, args.exp_mode, w, gp,
+                               2 if args.precision == 32 else pa))
         ctx.set_option("i8_debug", 0)
     out["matvec"] = rows
     ctx.close()
