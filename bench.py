@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--n", type=int, default=CFG4["n"], help="override n (debug only)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the optional fp32-mode measurement")
     ap.add_argument("--time-to-tol", type=int, default=0, metavar="CFG",
                     help="also run the full train (RFF + precond + PCG) of BASELINE config CFG")
     return ap.parse_args()
@@ -268,6 +269,25 @@ def main():
         _lib.check(_lib.LIB.krr_kernel_matvec(ctx.handle, lam, hv.data_ptr(), 1, ho.data_ptr()))
     e2e_s = D.max(time.perf_counter() - t0)
 
+    # ---- optional fp32 mode (north star: reported separately), same workload and vector
+    f32 = None
+    if not args.no_fp32:
+        vv = np.random.default_rng(11).standard_normal(n)
+        ref64 = np.empty(n)
+        _lib.check(_lib.LIB.krr_kernel_matvec(ctx.handle, lam, _lib.ptr(vv), 1, _lib.ptr(ref64)))
+        ctx.set_precision(32)
+        out32 = np.empty(n)
+        _lib.check(_lib.LIB.krr_kernel_matvec(ctx.handle, lam, _lib.ptr(vv), 1, _lib.ptr(out32)))  # warm + prep
+        D.barrier()
+        tot32, k132 = C.c_double(), C.c_double()
+        _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, lam, args.steps, C.byref(tot32), C.byref(k132)))
+        t32 = D.max(tot32.value)
+        ctx.set_precision(64)
+        f32 = {"value": float(n) * n * args.steps / (t32 * 1e-3) / 1e9, "unit": "Gevals/s",
+               "ms_per_step": t32 / args.steps, "dtype": "f32 (3 bf16 parts, tcgen05 kind::f16, fp32 exp)",
+               "rel_err_vs_fp64": float(np.linalg.norm(out32 - ref64) / np.linalg.norm(ref64)),
+               "note": "optional fp32-accuracy mode (krr_set_precision 32); not the headline"}
+
     # ---- optional time-to-tolerance (full train on the device)
     ttt = None
     if args.time_to_tol:
@@ -357,6 +377,8 @@ def main():
         line["cpu_baseline"] = cpu
     if ttt:
         line["time_to_tol"] = ttt
+    if f32:
+        line["fp32_mode"] = f32
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--tau", type=float, default=1e-6)
     ap.add_argument("--oracle-iters", type=int, default=0)
     ap.add_argument("--n", type=int, default=0, help="override n (sub-sampled config)")
+    ap.add_argument("--precision", type=int, default=64, help="64 (fp64, default) or 32 (optional fp32 mode)")
     args = ap.parse_args()
     od = ROOT / "gpurun_out"
     od.mkdir(exist_ok=True)
@@ -40,8 +41,9 @@ def main():
         sc = krr.SolverConfig(tau=args.tau, max_iter=args.max_iter, lambda_=lam,
                               chain=krr.ChainSpec(s1=s), seed=0)
         ctx = krr.Context(0)
+        ctx.set_precision(args.precision)
         res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), sc, ctx=ctx)
-        out = {"config": cfg, "n": n, "d": d, "t": t, "sigma": sigma, "lambda": lam, "s": s,
+        out = {"config": cfg, "precision": args.precision, "n": n, "d": d, "t": t, "sigma": sigma, "lambda": lam, "s": s,
                "tau": args.tau, "max_iter": args.max_iter, "gen_s": gen_s,
                "phase_ms": res.report.phase_ms, "wall_s": res.report.wall_time_sec,
                "per_rhs": [{"iterations": r.iterations, "converged": r.converged,
@@ -68,7 +70,8 @@ def main():
         print(json.dumps({k2: v for k2, v in out.items() if k2 != "per_rhs"}), flush=True)
         print(json.dumps({"iterations": [r["iterations"] for r in out["per_rhs"]],
                           "final_residual": [r["final_residual"] for r in out["per_rhs"]]}), flush=True)
-        (od / f"ttt_{cfg}{'_n' + str(n) if args.n else ''}.json").write_text(json.dumps(out, indent=1))
+        tag = ("_n" + str(n) if args.n else "") + ("_fp32" if args.precision == 32 else "")
+        (od / f"ttt_{cfg}{tag}.json").write_text(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":
