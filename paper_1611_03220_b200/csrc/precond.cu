@@ -94,13 +94,29 @@ __global__ void gemvT_partial_kernel(const double* __restrict__ B, int64_t n, in
     }
 }
 
+// W[k] = sum_c Wpart[c][k]: one block per 32 columns, lane <-> column (coalesced rows);
+// warp w sums a contiguous range of chunks in order (loads unrolled ahead of the adds), then
+// the 8 warp sums are combined in order — a blocked forward sum over the rows of U^T:
+// deterministic, close to the reference's sequential order, no long per-thread load chain.
 __global__ void reduce_rows_kernel(const double* __restrict__ Wpart, int nchunks, int64_t s,
                                    double* __restrict__ W) {
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < s;
-         k += int64_t(gridDim.x) * blockDim.x) {
-        double acc = 0.0;
-        for (int c = 0; c < nchunks; ++c) acc += Wpart[int64_t(c) * s + k];
-        W[k] = acc;
+    __shared__ double part[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t k = int64_t(blockIdx.x) * 32 + lane;
+    const int per = (nchunks + 7) / 8;
+    const int c0 = warp * per, c1 = min(nchunks, c0 + per);
+    double acc = 0.0;
+    if (k < s) {
+#pragma unroll 8
+        for (int c = c0; c < c1; ++c) acc += Wpart[int64_t(c) * s + k];
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && k < s) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w][lane];
+        W[k] = t;
     }
 }
 
@@ -184,7 +200,7 @@ void gemvT_partial_launch(const double* B, int64_t n, int64_t s, const double* r
 
 void reduce_rows_launch(const double* Wpart, int nchunks, int64_t s, double* W,
                         cudaStream_t stream) {
-    const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((s + 255) / 256, 148 * 4)));
+    const unsigned blocks = unsigned(std::max<int64_t>(1, (s + 31) / 32));
     reduce_rows_kernel<<<blocks, 256, 0, stream>>>(Wpart, nchunks, s, W);
     KRR_LAUNCH_CHECK();
 }
