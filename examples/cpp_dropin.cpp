@@ -112,6 +112,35 @@ int main() {
         }
         check(ok && total == st[0].iterations + st[1].iterations, "train residual within tau");
     }
+    // mat-vec paths behind the same entry point: auto (K1-I8 tensor cores for d >= 48),
+    // forced DMMA, and the optional fp32 mode, on one problem (the fp64 paths agree to
+    // ~1e-13, the fp32 mode to ~1e-6)
+    {
+        const int64_t n = 700, d = 64;
+        const auto x = random_matrix(n, d, 9);
+        const auto v = random_matrix(n, 1, 10);
+        std::vector<double> a(static_cast<size_t>(n)), b(static_cast<size_t>(n)), f(static_cast<size_t>(n));
+        must(krr_set_data(ctx, x.data(), n, d, 6.0), "set_data");
+        double path = -2;
+        must(krr_get_option(ctx, "k1_path_effective", &path), "get_option");
+        must(krr_kernel_matvec(ctx, 1e-3, v.data(), 1, a.data()), "matvec auto");
+        must(krr_set_option(ctx, "k1_path", 0), "k1_path dmma");
+        must(krr_kernel_matvec(ctx, 1e-3, v.data(), 1, b.data()), "matvec dmma");
+        must(krr_set_option(ctx, "k1_path", -1), "k1_path auto");
+        must(krr_set_precision(ctx, 32), "precision 32");
+        must(krr_kernel_matvec(ctx, 1e-3, v.data(), 1, f.data()), "matvec fp32");
+        must(krr_set_precision(ctx, 64), "precision 64");
+        double dn = 0, fn = 0, nn = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            dn += (a[size_t(i)] - b[size_t(i)]) * (a[size_t(i)] - b[size_t(i)]);
+            fn += (a[size_t(i)] - f[size_t(i)]) * (a[size_t(i)] - f[size_t(i)]);
+            nn += a[size_t(i)] * a[size_t(i)];
+        }
+        check(path == 1.0, "auto path is K1-I8 at d = 64");
+        check(std::sqrt(dn / nn) <= 1e-13, "K1-I8 == K1-DMMA to 1e-13");
+        check(std::sqrt(fn / nn) <= 2e-6, "fp32 mode within 2e-6");
+        check(krr_set_precision(ctx, 16) == KRR_ERR_INVALID_ARGUMENT, "precision 16 rejected");
+    }
     // error mapping: lambda <= 0 -> NonPositiveLambda; sigma <= 0 -> invalid_argument
     {
         double dummy[4] = {0, 0, 0, 0};
