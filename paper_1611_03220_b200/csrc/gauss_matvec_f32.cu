@@ -35,7 +35,8 @@ constexpr int TJ = 64;    // J tile columns (MMA N)
 constexpr int NACC = 4;   // TMEM accumulator buffers
 constexpr int NCD = 4;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps
-constexpr int CPT = 16;   // columns per epilogue thread
+constexpr int CPT = 16;   // columns per epilogue thread per tile
+constexpr int CPP = 2 * CPT;  // per tile pair (the epilogue consumes two tiles per step)
 constexpr int NTHR = 32 * (2 + NEPI);
 constexpr uint32_t TMEM_COLS = 256;
 constexpr int SCR_LD = 33;
@@ -44,15 +45,18 @@ constexpr int KB_MAX = 256;           // bytes per row per part (d <= 128)
 
 template <int KB>
 struct CfgF {
-    static constexpr int NSTB = KB >= 256 ? 1 : (KB >= 160 ? 2 : 3);
     static constexpr size_t A_BYTES = size_t(NPART) * TI * KB;
     static constexpr size_t B_BYTES = size_t(NPART) * TJ * KB;
+    static constexpr size_t SCR_BYTES = size_t(NEPI) * CPP * SCR_LD * 4;
+    static constexpr size_t FIXED = NCD * CD_BYTES + SCR_BYTES + 2 * 4 * 2 * TJ * 4 + 512;
+    static constexpr size_t FIT = (232448 - A_BYTES - FIXED) / B_BYTES;
+    static constexpr int NSTB = FIT >= 3 ? 3 : int(FIT);  // J-tile stages that fit
+    static_assert(NSTB >= 1, "K1-F32: operand tiles do not fit");
     static constexpr size_t OFF_B = A_BYTES;
     static constexpr size_t OFF_CD = OFF_B + NSTB * B_BYTES;
     static constexpr size_t OFF_SCR = OFF_CD + NCD * CD_BYTES;
-    static constexpr size_t SCR_BYTES = size_t(NEPI) * CPT * SCR_LD * 4;
     static constexpr size_t OFF_COLSCR = OFF_SCR + (SCR_BYTES > 4 * TI * 8 ? SCR_BYTES : 4 * TI * 8);
-    static constexpr size_t OFF_BARS = OFF_COLSCR + 2 * 4 * TJ * 4;
+    static constexpr size_t OFF_BARS = OFF_COLSCR + 2 * 4 * 2 * TJ * 4;
     static constexpr int NBARS = 2 + 2 * NSTB + 2 * NCD + 2 * NACC;
     static constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
 };
@@ -193,90 +197,107 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_f32_kernel(const F32Args
         }
     } else {
         // ------------------------------------------------------------ epilogue
+        // Two consecutive 64-column tiles per step (every pass has an even tile count):
+        // one barrier, one transpose and one owner update per 128 columns.
         const int ew = warp - 2;
         const int quarter = warp & 3;
-        const int part = ew >> 2;  // which 16 of the 64 columns
+        const int part = ew >> 2;  // which 16 of each tile's 64 columns
         const int etid = ew * 32 + lane;
         const int row = quarter * 32 + lane;
         const int colOff = part * CPT;
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-        float* scr = scr_all + ew * CPT * SCR_LD;
+        float* scr = scr_all + ew * CPP * SCR_LD;
         int tq = 0;
         for (int it = 0; it < nTI; ++it) {
             const int64_t gi = rowBase + int64_t(it) * TI + row;
             const float s_i = A.s[gi];
             const float v_i = A.v[gi];
             double rowacc = 0.0;
-            for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++tq) {
-                const int buf = tq % NACC;
+            for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; jt += 2, tq += 2) {
+                // owner thread of pair column etid (< 128): the same thread every pass
                 double* cdst = A.part + int64_t(sa) * A.n_pad + colBase + int64_t(jt) * TJ + etid;
                 double cprev = 0.0;
-                if (etid < TJ && it > 0) cprev = *cdst;
-                tc::mbar_wait(t_full + buf, uint32_t((tq / NACC) & 1));
+                if (etid < 2 * TJ && it > 0) cprev = *cdst;
+                uint32_t dr[CPP];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int buf = (tq + h) % NACC;
+                    tc::mbar_wait(t_full + buf, uint32_t(((tq + h) / NACC) & 1));
+                }
                 tc::fence_after();
-                uint32_t dr[CPT];
-                tc::tmem_ld16(tmem_base + lane_addr + uint32_t(buf * TJ + colOff), dr);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t(&d16)[CPT] = *reinterpret_cast<uint32_t(*)[CPT]>(dr + h * CPT);
+                    tc::tmem_ld16(tmem_base + lane_addr + uint32_t(((tq + h) % NACC) * TJ + colOff), d16);
+                }
                 tc::tmem_wait_ld();
                 tc::fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(t_empty + buf);
-
-                const int cs = tq % NCD;
-                tc::mbar_wait(cd_full + cs, uint32_t((tq / NCD) & 1));
-                const float* cd_s = reinterpret_cast<const float*>(sCD + cs * CD_BYTES);
-                const float* cd_v = cd_s + TJ;
-                const bool masked = diag && jt < (it + 1) * (TI / TJ);
-                const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
+                if (lane == 0) {
+                    tc::mbar_arrive(t_empty + tq % NACC);
+                    tc::mbar_arrive(t_empty + (tq + 1) % NACC);
+                }
+                const float* cds[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cs = (tq + h) % NCD;
+                    tc::mbar_wait(cd_full + cs, uint32_t(((tq + h) / NCD) & 1));
+                    cds[h] = reinterpret_cast<const float*>(sCD + cs * CD_BYTES);
+                }
+                // the pair (2it, 2it+1) of a diagonal super-tile is the diagonal block: keep
+                // pair column > row
+                const bool masked = diag && jt == it * (TI / TJ);
                 float rt0 = 0.f, rt1 = 0.f;
 #pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    const int cl = colOff + k;
+                for (int k = 0; k < CPP; ++k) {
+                    const int h = k / CPT, cl = colOff + (k % CPT);
                     // y = log2(e) (-scale) d2 = s_i + s_j + 2c x_i.x_j, clamped at 0 (d2 >= 0)
-                    const float y = fminf(fmaf(__uint_as_float(dr[k]), A.c2, s_i + cd_s[cl]), 0.f);
+                    const float y = fminf(fmaf(__uint_as_float(dr[k]), A.c2, s_i + cds[h][cl]), 0.f);
                     float e = ex2_approx(y);
-                    if (masked) e = (cl > mask_row) ? e : 0.f;
-                    if (k & 1) rt1 = fmaf(e, cd_v[cl], rt1);
-                    else rt0 = fmaf(e, cd_v[cl], rt0);
+                    if (masked) e = (h * TJ + cl > row) ? e : 0.f;
+                    if (k & 1) rt1 = fmaf(e, cds[h][TJ + cl], rt1);
+                    else rt0 = fmaf(e, cds[h][TJ + cl], rt0);
                     scr[k * SCR_LD + lane] = e * v_i;
                 }
                 rowacc += double(rt0 + rt1);
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(cd_empty + cs);
-                // column sums over the warp's 32 rows: lane L sums column L % 16 over 16 rows
+                if (lane == 0) {
+                    tc::mbar_arrive(cd_empty + tq % NCD);
+                    tc::mbar_arrive(cd_empty + (tq + 1) % NCD);
+                }
+                // column sums over the warp's 32 rows: lane k sums its column over all 32 rows
                 {
-                    const float* src = scr + (lane % CPT) * SCR_LD + (lane / CPT) * 16;
-                    float a0 = 0.f, a1 = 0.f;
+                    const float* src = scr + lane * SCR_LD;
+                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-                    for (int r = 0; r < 16; r += 2) {
+                    for (int r = 0; r < 32; r += 4) {
                         a0 += src[r];
                         a1 += src[r + 1];
+                        a2 += src[r + 2];
+                        a3 += src[r + 3];
                     }
-                    float acc = a0 + a1;
-                    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-                    if (lane < CPT) colscr[((tq & 1) * 4 + quarter) * TJ + colOff + lane] = acc;
+                    const int pc = (lane / CPT) * TJ + colOff + (lane % CPT);  // pair column
+                    colscr[((tq >> 1) & 1) * 4 * 2 * TJ + quarter * 2 * TJ + pc] = (a0 + a1) + (a2 + a3);
                 }
                 __syncwarp();
                 epi_bar();
-                if (etid < TJ) {
-                    const float* q4 = colscr + (tq & 1) * 4 * TJ + etid;
-                    *cdst = cprev + double((q4[0] + q4[TJ]) + (q4[2 * TJ] + q4[3 * TJ]));
+                if (etid < 2 * TJ) {
+                    const float* q4 = colscr + ((tq >> 1) & 1) * 4 * 2 * TJ + etid;
+                    *cdst = cprev + double((q4[0] + q4[2 * TJ]) + (q4[4 * TJ] + q4[6 * TJ]));
                 }
             }
-            // pass end: row partials, 4 column parts combined in fixed order
+            // pass end: row partials, 4 column parts combined in fixed order; the pair-column
+            // owner (index mod 128) adds on diagonal super-tiles
             rowbuf[part * TI + row] = rowacc;
             epi_bar();
-            if (diag) {
-                if (etid < TJ) {
-#pragma unroll
-                    for (int h = 0; h < TI / TJ; ++h) {
-                        const int r = h * TJ + etid;
-                        double* dst = A.part + int64_t(sa) * A.n_pad + rowBase + int64_t(it) * TI + r;
-                        *dst = *dst + (((rowbuf[r] + rowbuf[TI + r]) + rowbuf[2 * TI + r]) + rowbuf[3 * TI + r]);
-                    }
+            if (etid < TI) {
+                const double rs = ((rowbuf[etid] + rowbuf[TI + etid]) + rowbuf[2 * TI + etid]) + rowbuf[3 * TI + etid];
+                if (diag) {
+                    double* dst = A.part + int64_t(sa) * A.n_pad + rowBase + int64_t(it) * TI + etid;
+                    *dst = *dst + rs;
+                } else {
+                    A.part[int64_t(sb) * A.n_pad + rowBase + int64_t(it) * TI + etid] = rs;
                 }
-            } else if (etid < TI) {
-                A.part[int64_t(sb) * A.n_pad + rowBase + int64_t(it) * TI + etid] =
-                    ((rowbuf[etid] + rowbuf[TI + etid]) + rowbuf[2 * TI + etid]) + rowbuf[3 * TI + etid];
             }
             epi_bar();
         }
