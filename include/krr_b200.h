@@ -89,6 +89,15 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value);
  * of K v ~1e-6).  PCG vectors, dots and the preconditioner stay fp64 in both modes;
  * multi-RHS solves run column by column in fp32 mode. */
 int krr_set_precision(krr_ctx* ctx, int bits);
+/* the sketch-and-solve random-features baseline of `krr bench`.
+ * train_random_features_baseline (solver.cpp:175-193): w (s x t, row-major) =
+ * (Z^T Z + lambda I)^{-1} Z^T Y with Z = RFF(X of krr_set_data; W s x d, b s from
+ * krr_rff_realize), no jitter (NotPositiveDefinite on failure).  Single-rank. */
+int krr_rf_baseline_train(krr_ctx* ctx, const double* W, const double* b, int64_t s, const double* Y, int64_t t,
+                          double lambda, double* w_out);
+/* baseline_predict_scores (solver.cpp:195-197): out (m x t) = RFF(Xq) w. */
+int krr_rf_baseline_predict(krr_ctx* ctx, const double* Xq, int64_t m, const double* W, const double* b, int64_t s,
+                            const double* w, int64_t t, double* out);
 /* Read a knob back: "k1_path", "exp_mode", "batched_rhs", and (after krr_set_data)
  * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now), "i8_supported",
  * and "precision" (64 | 32). */

@@ -289,3 +289,22 @@ def train(x, y, sigma, lam, s, seed, tau, max_iter, lambda_p=None, dense_k=True,
                             int(dense_k), _p(c), _p(its), _p(cvs), _p(frs), _p(hist), C.byref(tot), order),
          "train")
     return SolveOut(c, its.tolist(), [bool(v) for v in cvs], frs.tolist(), hist, int(tot.value))
+
+
+def rf_baseline(x, y, sigma: float, lam: float, s: int, seed: int, order: int = DEFAULT_ORDER):
+    """train_random_features_baseline (solver.cpp:175-193) composed from the restated pieces:
+    Z = apply_rows (sketches.cpp:207-211), gram = Z^T Z + lambda I, L = cholesky
+    (numerics.cpp:49-55), forward = L^-1 Z^T Y, w = L^-T forward (numerics.cpp:57-79).
+    Returns (w, W, b).  Test infrastructure only."""
+    x = f64(x)
+    y = f64(y)
+    y = y[:, None] if y.ndim == 1 else y
+    w_rff, b_rff = rff_realize(seed, x.shape[1], s, sigma)
+    z = rff_apply_rows(x, w_rff, b_rff, order)
+    gram = z.T @ z
+    gram[np.diag_indices(s)] += lam
+    l = cholesky(gram)
+    rhs = z.T @ y
+    fwd = triangular_solve(l, rhs)
+    w = triangular_solve(l, fwd, side="left", transpose=True)
+    return w, w_rff, b_rff

@@ -50,6 +50,7 @@ __all__ = [
     "PcgReport", "PcgResult", "KrrModel", "TrainResult", "pcg_solve", "solve_regularized",
     "train", "predict_scores", "predict_labels", "rlsc_encode", "rlsc_decode",
     "generate_config", "schedule", "Context", "device_count",
+    "RandomFeaturesModel", "train_random_features_baseline", "baseline_predict_scores", "baseline_predict_labels",
 ]
 
 K_STAGE_SEED_STRIDE = 0x9E3779B97F4A7C15  # sketches.hpp:14
@@ -550,6 +551,78 @@ def predict_labels(model: KrrModel, xq: np.ndarray) -> list:
     if scores.shape[1] != len(model.label_map):
         raise KrrError("predict_labels: score width does not match the label map")
     return [model.label_map[i] for i in rlsc_decode(scores)]
+
+
+# ----------------------------------------------------------------------------- f1: RF baseline
+@dataclass
+class RandomFeaturesModel:
+    """solver.hpp RandomFeaturesModel: the realized RFF chain, weights w (s x t), lambda."""
+    chain: SketchChain
+    w: np.ndarray
+    lambda_: float
+    label_map: list = field(default_factory=list)
+
+    def classification(self) -> bool:
+        return len(self.label_map) > 0
+
+
+def _rff_stage(chain: SketchChain) -> "RffMap":
+    return chain.rff  # realize_chain enforces Gaussian <=> one RandomFourier stage (sketches.cpp:217-218)
+
+
+def train_random_features_baseline(data: Dataset, kernel: KernelSpec, chain: ChainSpec, lambda_: float,
+                                   seed: int = 0, ctx: Optional[Context] = None) -> RandomFeaturesModel:
+    """Sketch-and-solve baseline of `krr bench` (solver.cpp:175-193): Z = RFF(X),
+    w = (Z^T Z + lambda I)^{-1} Z^T Y on the device (K2 features, cuBLAS SYRK/GEMM,
+    cuSOLVER potrf/potrs; no jitter)."""
+    kernel.validate()
+    if not (lambda_ > 0.0):
+        raise NonPositiveLambda("baseline: lambda must be positive")
+    x = _lib.f64(data.x)
+    y = _lib.f64(data.y)
+    y2 = y[:, None] if y.ndim == 1 else y
+    sk = realize_chain(chain, kernel, x.shape[1], seed)
+    st = _rff_stage(sk)
+    s, t = st.output_dim(), y2.shape[1]
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], kernel.sigma))
+        w = np.empty((s, t))
+        _lib.check(_lib.LIB.krr_rf_baseline_train(ctx.handle, _lib.ptr(st.w), _lib.ptr(st.b), s, _lib.ptr(y2), t,
+                                                  float(lambda_), _lib.ptr(w)))
+    finally:
+        if own:
+            ctx.close()
+    return RandomFeaturesModel(sk, w, float(lambda_), list(data.label_map))
+
+
+def baseline_predict_scores(model: RandomFeaturesModel, xq: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
+    """solver.cpp:195-197: RFF(Xq) w."""
+    xq = _lib.f64(xq)
+    st = _rff_stage(model.chain)
+    if xq.ndim != 2 or xq.shape[1] != st.input_dim():
+        raise DimensionMismatch("baseline predict: query dimension mismatch")
+    s, t = model.w.shape
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        # the context needs a data set for d / the operand layout: the queries themselves
+        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(xq), xq.shape[0], xq.shape[1], st.sigma))
+        out = np.empty((xq.shape[0], t))
+        _lib.check(_lib.LIB.krr_rf_baseline_predict(ctx.handle, _lib.ptr(xq), xq.shape[0], _lib.ptr(st.w),
+                                                    _lib.ptr(st.b), s, _lib.ptr(_lib.f64(model.w)), t,
+                                                    _lib.ptr(out)))
+    finally:
+        if own:
+            ctx.close()
+    return out
+
+
+def baseline_predict_labels(model: RandomFeaturesModel, xq: np.ndarray) -> list:
+    if not model.classification():
+        raise KrrError("baseline: model has no label map")
+    return [model.label_map[i] for i in rlsc_decode(baseline_predict_scores(model, xq))]
 
 
 # ----------------------------------------------------------------------------- synthetic data

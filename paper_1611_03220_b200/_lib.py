@@ -112,6 +112,8 @@ _SIGS = {
     "krr_set_option": [_vp, C.c_char_p, _d],
     "krr_get_option": [_vp, C.c_char_p, C.POINTER(_d)],
     "krr_set_precision": [_vp, _i],
+    "krr_rf_baseline_train": [_vp, _vp, _vp, _i64, _vp, _i64, _d, _vp],
+    "krr_rf_baseline_predict": [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp],
     "krr_set_data": [_vp, _vp, _i64, _i64, _d],
     "krr_kernel_matvec": [_vp, _d, _vp, _i64, _vp],
     "krr_kernel_matvec_device": [_vp, _d, _vp, _i64, _vp],

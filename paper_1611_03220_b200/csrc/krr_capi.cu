@@ -985,6 +985,123 @@ int krr_predict_scores(krr_ctx* ctx, const double* Xq, int64_t m, const double* 
     });
 }
 
+// ---------------------------------------------------------------- f1: RF sketch-and-solve baseline
+// train_random_features_baseline (solver.cpp:175-193) and baseline_predict_scores
+// (solver.cpp:195-197): w = (Z^T Z + lambda I)^{-1} Z^T Y with Z the RFF features (K2), LLT
+// with no jitter (numerics::cholesky throws NotPositiveDefinite), then the two triangular
+// solves (potrs).  Single-rank.
+namespace krr {
+namespace {
+void rf_features_dev(Ctx& c, const double* Xdev, int64_t m, const double* W, const double* b, int64_t s,
+                     DevMem<double>& Z) {
+    const int dp = c.plan.dp;
+    const int64_t m_pad = (m + 127) / 128 * 128;
+    DevMem<double> L, R, wdev, bdev, wpad;
+    L.ensure(size_t(m_pad * dp));
+    R.ensure(size_t(m_pad * dp));
+    build_operands_launch(Xdev, m, c.d, m_pad, dp, L.get(), R.get(), c.stream);
+    wdev.ensure(size_t(s * c.d));
+    bdev.ensure(size_t(s));
+    KRR_CUDA(cudaMemcpyAsync(wdev.get(), W, sizeof(double) * size_t(s * c.d), cudaMemcpyHostToDevice, c.stream));
+    KRR_CUDA(cudaMemcpyAsync(bdev.get(), b, sizeof(double) * size_t(s), cudaMemcpyHostToDevice, c.stream));
+    const int64_t s_pad = (s + 127) / 128 * 128;
+    wpad.ensure(size_t(s_pad * dp));
+    rff_pad_w_launch(wdev.get(), s, c.d, s_pad, dp, wpad.get(), c.stream);
+    Z.ensure(size_t(m * s));
+    rff_features_launch(L.get(), wpad.get(), bdev.get(), Z.get(), m, s, dp, c.stream);
+    c.sync();  // temporaries are released on return
+}
+}  // namespace
+}  // namespace krr
+
+int krr_rf_baseline_train(krr_ctx* ctx, const double* W, const double* b, int64_t s, const double* Y, int64_t t,
+                          double lambda, double* w_out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (!(lambda > 0.0)) krr::fail(KRR_ERR_NON_POSITIVE_LAMBDA, "baseline: lambda must be positive");
+        if (s < 1) krr::fail(KRR_ERR_INVALID_ARGUMENT, "ChainSpec: s1 must be at least 1");
+        if (t < 1) krr::fail(KRR_ERR_DIMENSION_MISMATCH, "baseline: Y needs at least one column");
+        if (c.world != 1) krr::fail(KRR_ERR_STATE, "the random-features baseline is single-rank");
+        c.set_device();
+        const int64_t n = c.n;
+        krr::DevMem<double> Z, G, Yd, Rm, work;
+        krr::DevMem<int> info;
+        krr::rf_features_dev(c, c.X.get(), n, W, b, s, Z);
+        // G = Z^T Z + lambda I (lower): Z row-major n x s == col-major Z^T (s x n)
+        G.ensure(size_t(s * s));
+        const double one = 1.0, zero = 0.0;
+        krr::cublas_check(cublasSetStream(c.blas, c.stream), "cublasSetStream");
+        krr::cublas_check(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(s), int(n), &one, Z.get(),
+                                      int(s), &zero, G.get(), int(s)),
+                          "cublasDsyrk(Z^T Z)");
+        krr::diag_add_launch(G.get(), s, lambda, c.stream);
+        int lwork = 0;
+        krr::cusolver_check(cusolverDnSetStream(c.sol, c.stream), "cusolverDnSetStream");
+        krr::cusolver_check(
+            cusolverDnDpotrf_bufferSize(c.sol, CUBLAS_FILL_MODE_LOWER, int(s), G.get(), int(s), &lwork),
+            "potrf_bufferSize");
+        work.ensure(size_t(std::max(1, lwork)));
+        info.ensure(1);
+        krr::cusolver_check(cusolverDnDpotrf(c.sol, CUBLAS_FILL_MODE_LOWER, int(s), G.get(), int(s), work.get(), lwork,
+                                             info.get()),
+                            "potrf");
+        int hinfo = 0;
+        KRR_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (hinfo != 0) krr::fail(KRR_ERR_NOT_POSITIVE_DEFINITE, "cholesky: non-positive pivot encountered");
+        // numerics.cpp:62-63 (triangular_solve's singular check) on the factor's diagonal
+        std::vector<double> dg(static_cast<size_t>(s));
+        KRR_CUDA(cudaMemcpy2DAsync(dg.data(), sizeof(double), G.get(), sizeof(double) * size_t(s + 1), sizeof(double),
+                                   size_t(s), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        for (double v : dg)
+            if (!(std::fabs(v) >= 1e-300)) krr::fail(KRR_ERR_SINGULAR_TRIANGULAR, "triangular_solve: singular matrix");
+        // rhs = Z^T Y (s x t, col-major): Y row-major n x t == col-major Y^T (t x n)
+        Yd.ensure(size_t(n * t));
+        KRR_CUDA(cudaMemcpyAsync(Yd.get(), Y, sizeof(double) * size_t(n * t), cudaMemcpyHostToDevice, c.stream));
+        Rm.ensure(size_t(s * t));
+        krr::cublas_check(cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_T, int(s), int(t), int(n), &one, Z.get(), int(s),
+                                      Yd.get(), int(t), &zero, Rm.get(), int(s)),
+                          "cublasDgemm(Z^T Y)");
+        krr::cusolver_check(cusolverDnDpotrs(c.sol, CUBLAS_FILL_MODE_LOWER, int(s), int(t), G.get(), int(s), Rm.get(),
+                                             int(s), info.get()),
+                            "potrs");
+        std::vector<double> wcm(static_cast<size_t>(s * t));
+        KRR_CUDA(cudaMemcpyAsync(wcm.data(), Rm.get(), sizeof(double) * size_t(s * t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        c.sync();
+        for (int64_t k = 0; k < s; ++k)
+            for (int64_t j = 0; j < t; ++j) w_out[k * t + j] = wcm[size_t(j * s + k)];
+    });
+}
+
+int krr_rf_baseline_predict(krr_ctx* ctx, const double* Xq, int64_t m, const double* W, const double* b, int64_t s,
+                            const double* w, int64_t t, double* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (s < 1 || t < 1 || m < 0) krr::fail(KRR_ERR_DIMENSION_MISMATCH, "baseline predict: bad shapes");
+        c.set_device();
+        if (m == 0) return;
+        krr::DevMem<double> q, Zq, wd, o;
+        q.ensure(size_t(m * c.d));
+        KRR_CUDA(cudaMemcpyAsync(q.get(), Xq, sizeof(double) * size_t(m * c.d), cudaMemcpyHostToDevice, c.stream));
+        krr::rf_features_dev(c, q.get(), m, W, b, s, Zq);
+        wd.ensure(size_t(s * t));
+        KRR_CUDA(cudaMemcpyAsync(wd.get(), w, sizeof(double) * size_t(s * t), cudaMemcpyHostToDevice, c.stream));
+        o.ensure(size_t(m * t));
+        const double one = 1.0, zero = 0.0;
+        krr::cublas_check(cublasSetStream(c.blas, c.stream), "cublasSetStream");
+        // out (m x t row-major) = Zq (m x s) w (s x t): col-major out^T = w^T Zq^T
+        krr::cublas_check(cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, int(t), int(m), int(s), &one, wd.get(), int(t),
+                                      Zq.get(), int(s), &zero, o.get(), int(t)),
+                          "cublasDgemm(Zq w)");
+        KRR_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * size_t(m * t), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
 int krr_rff_realize(uint64_t master_seed, int64_t d, int64_t s, double sigma, double* W,
                     double* b) {
     return guard([&] { krr::rff_realize(master_seed, d, s, sigma, W, b); });

@@ -299,3 +299,14 @@ def test_oracle_regression_freeze(oracle):
     m = g["matvec_n64_d3"]
     v = oracle.random_vector(64, m["v_seed"])
     assert oracle.kernel_matvec(x, m["sigma"], m["lambda"], v).tolist() == m["out"]
+
+
+def test_oracle_rf_baseline_is_the_normal_equations(oracle):
+    """The restated sketch-and-solve baseline (solver.cpp:175-193) solves
+    (Z^T Z + lambda I) w = Z^T Y."""
+    x = oracle.random_matrix(300, 4, 1)
+    y = oracle.random_matrix(300, 2, 2)
+    w, wr, br = oracle.rf_baseline(x, y, 1.5, 1e-2, 40, 7)
+    z = oracle.rff_apply_rows(x, wr, br)
+    want = np.linalg.solve(z.T @ z + 1e-2 * np.eye(40), z.T @ y)
+    assert np.max(np.abs(w - want)) <= 1e-10 * np.max(np.abs(want))
