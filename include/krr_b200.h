@@ -42,7 +42,8 @@ typedef enum krr_status {
     KRR_ERR_CUDA = 7,                  /* device error (no reference equivalent)                   */
     KRR_ERR_NCCL = 8,                  /* collective error (no reference equivalent)               */
     KRR_ERR_STATE = 9,                 /* call out of order (e.g. matvec before krr_set_data)      */
-    KRR_ERR_CALLBACK = 10              /* a user operator callback reported failure                */
+    KRR_ERR_CALLBACK = 10,             /* a user operator callback reported failure                */
+    KRR_ERR_IO = 11                    /* model file I/O or format error (std::runtime_error, io.cpp) */
 } krr_status;
 
 typedef struct krr_ctx krr_ctx;
@@ -98,6 +99,16 @@ int krr_rf_baseline_train(krr_ctx* ctx, const double* W, const double* b, int64_
 /* baseline_predict_scores (solver.cpp:195-197): out (m x t) = RFF(Xq) w. */
 int krr_rf_baseline_predict(krr_ctx* ctx, const double* Xq, int64_t m, const double* W, const double* b, int64_t s,
                             const double* w, int64_t t, double* out);
+/* the reference's KRRM model file (io.cpp:192-261), byte-identical layout
+ * ("KRRM", version 1, metadata JSON as nlohmann dumps it, X n x d, C n x t fp64), so models
+ * trained here feed the reference's `krr predict` / `krr eval`.  Gaussian models only.
+ * Errors (bad magic, unsupported version, truncation, trailing bytes, non-finite entries,
+ * invalid dimensions) -> KRR_ERR_IO with the reference's messages. */
+int krr_model_save(const char* path, double sigma, double lambda, uint64_t seed, const double* label_map,
+                   int64_t nlabels, const double* X, int64_t n, int64_t d, const double* C, int64_t t);
+int krr_model_info(const char* path, int64_t* n, int64_t* d, int64_t* t, int64_t* nlabels, double* sigma,
+                   double* lambda, uint64_t* seed);
+int krr_model_load(const char* path, double* label_map, double* X, double* C);
 /* Read a knob back: "k1_path", "exp_mode", "batched_rhs", and (after krr_set_data)
  * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now), "i8_supported",
  * and "precision" (64 | 32). */

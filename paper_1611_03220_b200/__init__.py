@@ -35,6 +35,7 @@ from ._lib import (  # noqa: F401  (re-exported exception types)
     DimensionMismatch,
     InvalidArgument,
     KrrError,
+    ModelFileError,
     NcclError,
     NonPositiveLambda,
     NotPositiveDefinite,
@@ -50,6 +51,7 @@ __all__ = [
     "PcgReport", "PcgResult", "KrrModel", "TrainResult", "pcg_solve", "solve_regularized",
     "train", "predict_scores", "predict_labels", "rlsc_encode", "rlsc_decode",
     "generate_config", "schedule", "Context", "device_count",
+    "save_model", "load_model", "ModelFileError",
     "RandomFeaturesModel", "train_random_features_baseline", "baseline_predict_scores", "baseline_predict_labels",
 ]
 
@@ -551,6 +553,33 @@ def predict_labels(model: KrrModel, xq: np.ndarray) -> list:
     if scores.shape[1] != len(model.label_map):
         raise KrrError("predict_labels: score width does not match the label map")
     return [model.label_map[i] for i in rlsc_decode(scores)]
+
+
+# ----------------------------------------------------------------------------- f2: KRRM model file
+def save_model(path, model: KrrModel) -> None:
+    """io.cpp:192-215: the reference's KRRM file (byte-identical layout), written by the
+    library's host code; readable by the reference's `krr predict` / `krr eval`."""
+    x = _lib.f64(model.x)
+    c = _lib.f64(model.c)
+    c2 = c[:, None] if c.ndim == 1 else c
+    lm = np.ascontiguousarray(model.label_map, dtype=np.float64)
+    _lib.check(_lib.LIB.krr_model_save(str(path).encode(), float(model.kernel.sigma), float(model.lambda_),
+                                       int(model.seed) % (1 << 64), _lib.ptr(lm) if lm.size else None, lm.size,
+                                       _lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(c2), c2.shape[1]))
+
+
+def load_model(path) -> KrrModel:
+    """io.cpp:217-261 (same checks and messages; Gaussian models)."""
+    n, d, t, nl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    sigma, lam, seed = C.c_double(), C.c_double(), C.c_uint64()
+    p = str(path).encode()
+    _lib.check(_lib.LIB.krr_model_info(p, C.byref(n), C.byref(d), C.byref(t), C.byref(nl), C.byref(sigma),
+                                       C.byref(lam), C.byref(seed)))
+    lm = np.empty(max(1, nl.value))
+    x = np.empty((n.value, d.value))
+    c = np.empty((n.value, t.value))
+    _lib.check(_lib.LIB.krr_model_load(p, _lib.ptr(lm), _lib.ptr(x), _lib.ptr(c)))
+    return KrrModel(KernelSpec.gaussian(sigma.value), x, c, list(lm[:nl.value]), lam.value, int(seed.value))
 
 
 # ----------------------------------------------------------------------------- f1: RF baseline

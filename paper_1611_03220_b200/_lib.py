@@ -26,6 +26,7 @@ ERR_CUDA = 7
 ERR_NCCL = 8
 ERR_STATE = 9
 ERR_CALLBACK = 10
+ERR_IO = 11
 
 
 class KrrError(Exception):
@@ -74,6 +75,10 @@ class CallbackError(KrrError, RuntimeError):
     pass
 
 
+class ModelFileError(KrrError, RuntimeError):
+    """io.cpp model file errors (std::runtime_error in the reference)."""
+
+
 _EXC = {
     ERR_DIMENSION_MISMATCH: DimensionMismatch,
     ERR_NOT_POSITIVE_DEFINITE: NotPositiveDefinite,
@@ -85,6 +90,7 @@ _EXC = {
     ERR_NCCL: NcclError,
     ERR_STATE: StateError,
     ERR_CALLBACK: CallbackError,
+    ERR_IO: ModelFileError,
 }
 
 
@@ -112,6 +118,10 @@ _SIGS = {
     "krr_set_option": [_vp, C.c_char_p, _d],
     "krr_get_option": [_vp, C.c_char_p, C.POINTER(_d)],
     "krr_set_precision": [_vp, _i],
+    "krr_model_save": [C.c_char_p, _d, _d, C.c_uint64, _vp, _i64, _vp, _i64, _i64, _vp, _i64],
+    "krr_model_info": [C.c_char_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
+                       C.POINTER(_d), C.POINTER(_d), C.POINTER(C.c_uint64)],
+    "krr_model_load": [C.c_char_p, _vp, _vp, _vp],
     "krr_rf_baseline_train": [_vp, _vp, _vp, _i64, _vp, _i64, _d, _vp],
     "krr_rf_baseline_predict": [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp],
     "krr_set_data": [_vp, _vp, _i64, _i64, _d],

@@ -9,16 +9,10 @@
 #include <string>
 
 #include "../../include/krr_b200.h"
+#include "error.hpp"
 
 namespace krr {
 
-// Exception used inside the library; converted to a krr_status at the C-ABI.
-struct Error : std::runtime_error {
-    int status;
-    Error(int st, const std::string& msg) : std::runtime_error(msg), status(st) {}
-};
-
-[[noreturn]] inline void fail(int st, const std::string& msg) { throw Error(st, msg); }
 
 inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
     if (e != cudaSuccess)

@@ -29,4 +29,16 @@ Schedule make_schedule(int64_t n, int world, int rank);
 // Row shard of the sketch (Z / U) rows: contiguous blocks of ceil(n / world).
 void shard_rows(int64_t n, int world, int rank, int64_t* z0, int64_t* z1);
 
+// KRRM model file (io.cpp:192-261), model_io.cpp.
+struct ModelMeta {
+    int64_t n = 0, d = 0, t = 0;
+    double sigma = 0, lambda = 0;
+    uint64_t seed = 0;
+    std::vector<double> label_map;
+};
+void model_save(const char* path, double sigma, double lambda, uint64_t seed, const double* label_map,
+                int64_t nlabels, const double* X, int64_t n, int64_t d, const double* C, int64_t t);
+ModelMeta model_info(const char* path);
+void model_load(const char* path, double* label_map, double* X, double* C);
+
 }  // namespace krr

@@ -1304,6 +1304,29 @@ int krr_generate_config(int cfg, int64_t n, int64_t d, int64_t t, uint64_t seed,
     return guard([&] { krr::generate_config(cfg, n, d, t, seed, X, Y); });
 }
 
+int krr_model_save(const char* path, double sigma, double lambda, uint64_t seed, const double* label_map,
+                   int64_t nlabels, const double* X, int64_t n, int64_t d, const double* C, int64_t t) {
+    return guard([&] { krr::model_save(path, sigma, lambda, seed, label_map, nlabels, X, n, d, C, t); });
+}
+
+int krr_model_info(const char* path, int64_t* n, int64_t* d, int64_t* t, int64_t* nlabels, double* sigma,
+                   double* lambda, uint64_t* seed) {
+    return guard([&] {
+        const krr::ModelMeta m = krr::model_info(path);
+        *n = m.n;
+        *d = m.d;
+        *t = m.t;
+        *nlabels = int64_t(m.label_map.size());
+        *sigma = m.sigma;
+        *lambda = m.lambda;
+        *seed = m.seed;
+    });
+}
+
+int krr_model_load(const char* path, double* label_map, double* X, double* C) {
+    return guard([&] { krr::model_load(path, label_map, X, C); });
+}
+
 int krr_rlsc_encode(const int32_t* classes, int64_t n, int32_t num_classes, double* Y) {
     return guard([&] { krr::rlsc_encode(classes, n, num_classes, Y); });
 }

@@ -45,3 +45,22 @@ def test_plain_cg_row_matches_oracle(krr, oracle, ctx):
     ref = oracle.solve_gaussian(x, sigma, lam, None, 0.0, y, 1e-8, 500, dense_k=False)
     assert abs(report.per_rhs[0].iterations - int(ref.iterations[0])) <= 1
     assert rel(c, ref.c) <= 1e-8
+
+
+def test_trained_model_round_trips_through_krrm(krr, oracle, ctx, tmp_path):
+    """a model trained on the device, saved in the reference's KRRM format and
+    loaded back, predicts identically (predict_scores = cross_gram(Xq, X) C on the device)."""
+    x = oracle.random_matrix(800, 6, 31)
+    y = oracle.random_matrix(800, 2, 32)
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(2.0),
+                    krr.SolverConfig(tau=1e-8, max_iter=300, lambda_=1e-2, chain=krr.ChainSpec(s1=128), seed=3),
+                    ctx=ctx)
+    p = tmp_path / "trained.krrm"
+    krr.save_model(p, res.model)
+    back = krr.load_model(p)
+    xq = oracle.random_matrix(100, 6, 33)
+    a = krr.predict_scores(res.model, xq, ctx=ctx)
+    b = krr.predict_scores(back, xq, ctx=ctx)
+    assert np.array_equal(a, b)
+    # coefficients ~1e2 cancel to scores ~1: the comparison bound scales with that cancellation
+    assert rel(a, oracle.cross_gram(xq, x, 2.0) @ res.model.c) <= 1e-11
