@@ -21,6 +21,8 @@
 // K-major UMMA layout (LBO = 128 B, SBO = 8 kb B), byte-identical in structure to K1-I8's.
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_i8.cuh"
@@ -248,17 +250,22 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_f32_kernel(const F32Args
                 // pair column > row
                 const bool masked = diag && jt == it * (TI / TJ);
                 float rt0 = 0.f, rt1 = 0.f;
+                auto exp_cols = [&](auto mask_tag) {
+                    constexpr bool MASK = decltype(mask_tag)::value;
 #pragma unroll
-                for (int k = 0; k < CPP; ++k) {
-                    const int h = k / CPT, cl = colOff + (k % CPT);
-                    // y = log2(e) (-scale) d2 = s_i + s_j + 2c x_i.x_j, clamped at 0 (d2 >= 0)
-                    const float y = fminf(fmaf(__uint_as_float(dr[k]), A.c2, s_i + cds[h][cl]), 0.f);
-                    float e = ex2_approx(y);
-                    if (masked) e = (h * TJ + cl > row) ? e : 0.f;
-                    if (k & 1) rt1 = fmaf(e, cds[h][TJ + cl], rt1);
-                    else rt0 = fmaf(e, cds[h][TJ + cl], rt0);
-                    scr[k * SCR_LD + lane] = e * v_i;
-                }
+                    for (int k = 0; k < CPP; ++k) {
+                        const int h = k / CPT, cl = colOff + (k % CPT);
+                        // y = log2(e) (-scale) d2 = s_i + s_j + 2c x_i.x_j, clamped at 0 (d2 >= 0)
+                        const float y = fminf(fmaf(__uint_as_float(dr[k]), A.c2, s_i + cds[h][cl]), 0.f);
+                        float e = ex2_approx(y);
+                        if constexpr (MASK) e = (h * TJ + cl > row) ? e : 0.f;
+                        if (k & 1) rt1 = fmaf(e, cds[h][TJ + cl], rt1);
+                        else rt0 = fmaf(e, cds[h][TJ + cl], rt0);
+                        scr[k * SCR_LD + lane] = e * v_i;
+                    }
+                };
+                if (masked) exp_cols(std::true_type{});
+                else exp_cols(std::false_type{});
                 rowacc += double(rt0 + rt1);
                 __syncwarp();
                 if (lane == 0) {

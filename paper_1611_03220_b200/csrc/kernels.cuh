@@ -119,7 +119,6 @@ void rff_pad_w_launch(const double* W, int64_t s, int64_t d, int64_t s_pad, int 
 void rff_features_launch(const double* L, const double* Wp, const double* b, double* Z, int64_t rows,
                          int64_t s, int dp, cudaStream_t stream);
 // Z[i][k] = sqrt(2/s) * cos(Z[i][k] + b[k]), in place, Z n x s row-major.
-void rff_cos_launch(double* Z, int64_t n, int64_t s, const double* b, cudaStream_t stream);
 
 // ---------------------------------------------------------------- preconditioner (K3-K6)
 // G (s x s, col-major) diag += add; trace -> *trace (nullable)

@@ -1,4 +1,4 @@
-// K2/K3-K6 support kernels: RFF cos epilogue, Gram diagonal ops, and the two
+// K3-K6 support kernels: Gram diagonal ops, and the two
 // HBM-bound GEMV passes of the Woodbury apply.
 //
 // Reference: RffMap::apply (sketches.cpp:37-41), build_preconditioner
@@ -14,16 +14,6 @@
 namespace krr {
 
 namespace {
-
-__global__ void rff_cos_kernel(double* __restrict__ Z, int64_t n, int64_t s,
-                               const double* __restrict__ b, double scale) {
-    const int64_t total = n * s;
-    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-         idx += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t k = idx % s;
-        Z[idx] = scale * cos(Z[idx] + b[k]);
-    }
-}
 
 __global__ void diag_add_kernel(double* G, int64_t s, double add) {
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < s;
@@ -160,13 +150,6 @@ __global__ void precond_z_kernel(const double* __restrict__ B, int64_t n, int64_
 
 }  // namespace
 
-void rff_cos_launch(double* Z, int64_t n, int64_t s, const double* b, cudaStream_t stream) {
-    const double scale = sqrt(2.0 / double(s));
-    const int64_t total = n * s;
-    const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)));
-    rff_cos_kernel<<<blocks, 256, 0, stream>>>(Z, n, s, b, scale);
-    KRR_LAUNCH_CHECK();
-}
 
 void diag_add_launch(double* G, int64_t s, double add, cudaStream_t stream) {
     diag_add_kernel<<<unsigned((s + 255) / 256), 256, 0, stream>>>(G, s, add);
