@@ -109,6 +109,35 @@ int krr_model_save(const char* path, double sigma, double lambda, uint64_t seed,
 int krr_model_info(const char* path, int64_t* n, int64_t* d, int64_t* t, int64_t* nlabels, double* sigma,
                    double* lambda, uint64_t* seed);
 int krr_model_load(const char* path, double* label_map, double* X, double* C);
+/* QualityReport (precond.hpp:35-47). */
+typedef struct krr_quality_report {
+    int32_t passed;
+    int32_t pad_;
+    double cond1_value;          /* |(I-P) K (I-P)| by power iteration */
+    double cond2_ratio_low;      /* eigenvalue range of Sigma^-1 (B'KB) Sigma^-1 on range(P) */
+    double cond2_ratio_high;
+    int64_t rank_of_p;
+    int64_t sketch_size;
+    double lambda;
+    double cond1_threshold;      /* 0.1 lambda */
+    double spectrum_cut;         /* 0.05 lambda */
+    double ratio_low_threshold;  /* 0.9 */
+    double ratio_high_threshold; /* 1.1 */
+} krr_quality_report;
+/* quality_test (precond.cpp:60-100) of the context's raw sketch (after krr_rff_build /
+ * krr_sketch_upload, before krr_precond_build) against the Gaussian K of krr_set_data:
+ * eig(Z'Z) by cuSOLVER syevd, the retained basis by GEMM, condition 1 by power iteration
+ * through the fused K1 (start vector from mt19937_64(7), tol 1e-4, 500 iterations),
+ * condition 2 through the multi-RHS K1T.  Single-rank. */
+int krr_quality_test(krr_ctx* ctx, double lambda, krr_quality_report* out);
+/* adaptive_build (precond.cpp:107-138) for the Gaussian / RFF chain: s = s0, doubling
+ * until quality_test passes or s reaches s_max; attempt a draws its RFF map with master
+ * seed master_seed + a * 0xD1B54A32D192ED03 (sketches.hpp:16); then builds the Woodbury
+ * preconditioner (lambda_p, jitter retry) from the final sketch on the context.
+ * history (nullable) receives up to max_history reports. */
+int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0, int64_t s_max,
+                       uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
+                       int64_t* final_size, int* passed, int* jitter_used);
 /* Read a knob back: "k1_path", "exp_mode", "batched_rhs", and (after krr_set_data)
  * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now), "i8_supported",
  * and "precision" (64 | 32). */

@@ -308,3 +308,73 @@ def rf_baseline(x, y, sigma: float, lam: float, s: int, seed: int, order: int = 
     fwd = triangular_solve(l, rhs)
     w = triangular_solve(l, fwd, side="left", transpose=True)
     return w, w_rff, b_rff
+
+
+def quality_test(x, sigma: float, z, lam: float, order: int = DEFAULT_ORDER) -> dict:
+    """quality_test (precond.cpp:60-100) restated with the dense oracle K (small n only):
+    retained_left_singular_basis (precond.cpp:42-58) through eig(Z'Z) (Eigen sorts ascending,
+    the reference flips to descending, numerics.cpp:144-154), condition 1 by the reference's
+    power iteration (numerics.cpp:156-190: mt19937_64(7) normal start, tol 1e-4, 500 its) on
+    (I-P)K(I-P), condition 2 from eig(Sigma^-1 (B'KB) Sigma^-1).  Test infrastructure only."""
+    x, z = f64(x), f64(z)
+    n, s = z.shape
+    k = gram_matrix(x, sigma, order)
+    rep = {"lambda": lam, "sketch_size": s, "spectrum_cut": 0.05 * lam, "cond1_threshold": 0.1 * lam,
+           "cond2_ratio_low": 1.0, "cond2_ratio_high": 1.0}
+    ev, vec = np.linalg.eigh(z.T @ z)
+    ev, vec = ev[::-1], vec[:, ::-1]
+    max_ev = max(0.0, ev[0]) if s else 0.0
+    kk = 0
+    while kk < s and ev[kk] > rep["spectrum_cut"] and ev[kk] > 1e-20 * max_ev:
+        kk += 1
+    rep["rank_of_p"] = kk
+    b = z @ vec[:, :kk] / np.sqrt(ev[:kk])
+
+    def deflated(v):
+        w = v - b @ (b.T @ v)
+        w = k @ w
+        return w - b @ (b.T @ w)
+
+    v = random_matrix(n, 1, 7)[:, 0]
+    v = v / np.linalg.norm(v)
+    prev, val = 0.0, 0.0
+    for it in range(1, 501):
+        w = deflated(v)
+        rq = float(v @ w)
+        val = rq
+        nw = float(np.linalg.norm(w))
+        if nw == 0.0:
+            val = 0.0
+            break
+        if it > 1 and abs(rq - prev) <= 1e-4 * abs(rq):
+            break
+        prev = rq
+        v = w / nw
+    rep["cond1_value"] = val
+    if kk > 0:
+        inv = 1.0 / np.sqrt(ev[:kk])
+        m = (b.T @ k @ b) * inv[:, None] * inv[None, :]
+        m = (m + m.T) / 2.0
+        e2 = np.linalg.eigvalsh(m)
+        rep["cond2_ratio_high"], rep["cond2_ratio_low"] = float(e2[-1]), float(e2[0])
+    rep["passed"] = (rep["cond1_value"] <= rep["cond1_threshold"] and rep["cond2_ratio_low"] >= 0.9
+                     and rep["cond2_ratio_high"] <= 1.1)
+    return rep
+
+
+ATTEMPT_SEED_STRIDE = 0xD1B54A32D192ED03  # sketches.hpp:16
+
+
+def adaptive_sizes(x, sigma: float, lam: float, s0: int, s_max: int, master_seed: int) -> list:
+    """adaptive_build's doubling loop (precond.cpp:107-138) with the oracle quality test:
+    returns [(s, report), ...] per attempt."""
+    out, s = [], s0
+    for attempt in range(64):
+        seed = (master_seed + attempt * ATTEMPT_SEED_STRIDE) % (1 << 64)
+        w, b = rff_realize(seed, x.shape[1], s, sigma)
+        rep = quality_test(x, sigma, rff_apply_rows(x, w, b), lam)
+        out.append((s, rep))
+        if rep["passed"] or s >= s_max:
+            break
+        s = min(2 * s, s_max)
+    return out

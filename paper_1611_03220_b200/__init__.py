@@ -52,6 +52,7 @@ __all__ = [
     "train", "predict_scores", "predict_labels", "rlsc_encode", "rlsc_decode",
     "generate_config", "schedule", "Context", "device_count",
     "save_model", "load_model", "ModelFileError",
+    "QualityReport", "quality_test", "AdaptiveResult", "adaptive_build", "default_initial_sketch_size",
     "RandomFeaturesModel", "train_random_features_baseline", "baseline_predict_scores", "baseline_predict_labels",
 ]
 
@@ -477,7 +478,7 @@ def train(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Co
     if not (cfg.lambda_ > 0.0):
         raise NonPositiveLambda("train: lambda must be positive")
     if cfg.adaptive:
-        raise InvalidArgument("adaptive sketch sizing (precond.cpp:107) is out of the hot-path scope")
+        return _train_adaptive(data, kernel, cfg, ctx)
     kernel.validate()
     cfg.chain.validate()
     x = _lib.f64(data.x)
@@ -509,6 +510,29 @@ def train(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Co
                         "total": phase[3]})
     model = KrrModel(kernel, x.copy(), c, list(data.label_map), float(cfg.lambda_), int(cfg.seed))
     return TrainResult(model, report, s)
+
+
+def _train_adaptive(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Context]) -> TrainResult:
+    """solver.cpp:106-116: adaptive sketch size, then the same device PCG."""
+    kernel.validate()
+    cfg.chain.validate()
+    x = _lib.f64(data.x)
+    n = x.shape[0]
+    s0 = cfg.s0 if cfg.s0 > 0 else default_initial_sketch_size(n)
+    s_max = min(cfg.s_max, n) if cfg.s_max > 0 else max(n, s0)
+    lp = cfg.lambda_p if cfg.lambda_p is not None else cfg.lambda_
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        t0 = time.perf_counter()
+        ad = adaptive_build(x, cfg.chain, kernel, cfg.lambda_, lp, min(s0, s_max), s_max, cfg.seed, ctx=ctx)
+        c, rep = solve_regularized(x, kernel, data.y, cfg.lambda_, ad.preconditioner, cfg.tau, cfg.max_iter)
+        rep.wall_time_sec = time.perf_counter() - t0
+    finally:
+        if own:
+            ctx.close()
+    model = KrrModel(kernel, x.copy(), c, list(data.label_map), float(cfg.lambda_), int(cfg.seed))
+    return TrainResult(model, rep, ad.final_size, ad.passed, ad.history)
 
 
 def predict_scores(model: KrrModel, xq: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
@@ -553,6 +577,96 @@ def predict_labels(model: KrrModel, xq: np.ndarray) -> list:
     if scores.shape[1] != len(model.label_map):
         raise KrrError("predict_labels: score width does not match the label map")
     return [model.label_map[i] for i in rlsc_decode(scores)]
+
+
+# ----------------------------------------------------------------------------- f3: quality test / adaptive sizing
+@dataclass
+class QualityReport:
+    """precond.hpp:35-47."""
+    passed: bool = False
+    cond1_value: float = 0.0
+    cond2_ratio_low: float = 1.0
+    cond2_ratio_high: float = 1.0
+    rank_of_p: int = 0
+    sketch_size: int = 0
+    lambda_: float = 0.0
+    cond1_threshold: float = 0.0
+    spectrum_cut: float = 0.0
+    ratio_low_threshold: float = 0.9
+    ratio_high_threshold: float = 1.1
+
+
+def _qr(r) -> QualityReport:
+    return QualityReport(bool(r.passed), r.cond1_value, r.cond2_ratio_low, r.cond2_ratio_high, int(r.rank_of_p),
+                         int(r.sketch_size), r.lambda_, r.cond1_threshold, r.spectrum_cut, r.ratio_low_threshold,
+                         r.ratio_high_threshold)
+
+
+def default_initial_sketch_size(n: int) -> int:
+    """precond.cpp:102-104."""
+    return max(64, (int(n) + 63) // 64)
+
+
+def quality_test(x: np.ndarray, kernel: KernelSpec, z: np.ndarray, lambda_: float,
+                 ctx: Optional[Context] = None) -> QualityReport:
+    """quality_test (precond.cpp:60-100) with K the Gaussian kernel of X (never stored):
+    eig(Z'Z), power iteration on (I-P)K(I-P) through the fused K1, B'KB through K1T."""
+    kernel.validate()
+    x = _lib.f64(x)
+    z = _lib.f64(z)
+    if z.ndim != 2 or z.shape[0] != x.shape[0]:
+        raise DimensionMismatch("quality_test: K and Z dimensions do not match")
+    if not (lambda_ > 0.0):
+        raise NonPositiveLambda("quality_test: lambda must be positive")
+    own = ctx is None
+    ctx = ctx or Context()
+    try:
+        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], kernel.sigma))
+        _lib.check(_lib.LIB.krr_sketch_upload(ctx.handle, _lib.ptr(z), z.shape[0], z.shape[1]))
+        r = _lib.QualityReportC()
+        _lib.check(_lib.LIB.krr_quality_test(ctx.handle, float(lambda_), C.byref(r)))
+    finally:
+        if own:
+            ctx.close()
+    return _qr(r)
+
+
+@dataclass
+class AdaptiveResult:
+    """precond.hpp AdaptiveResult (the sketch itself stays on the device)."""
+    passed: bool
+    preconditioner: "Preconditioner"
+    final_size: int
+    history: list
+
+
+def adaptive_build(x: np.ndarray, chain_template: ChainSpec, kernel: KernelSpec, lambda_: float, lambda_p: float,
+                   s0: int, s_max: int, master_seed: int, ctx: Optional[Context] = None) -> AdaptiveResult:
+    """adaptive_build (precond.cpp:107-138): double s from s0 until quality_test passes or s_max,
+    each attempt re-seeded with master + attempt * 0xD1B54A32D192ED03; the preconditioner from the
+    final sketch stays resident on the device (pass ctx to keep using it)."""
+    kernel.validate()
+    chain_template.validate()
+    if s0 < 1:
+        raise InvalidArgument("adaptive_build: s0 must be at least 1")
+    if s_max < s0:
+        raise InvalidArgument("adaptive_build: s_max must be >= s0")
+    x = _lib.f64(x)
+    own = ctx is None
+    ctx = ctx or Context()
+    hist = (_lib.QualityReportC * 64)()
+    nh, fs, ok, jit = C.c_int(), C.c_int64(), C.c_int(), C.c_int()
+    try:
+        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], kernel.sigma))
+        _lib.check(_lib.LIB.krr_adaptive_build(ctx.handle, float(lambda_), float(lambda_p), int(s0), int(s_max),
+                                               int(master_seed) % (1 << 64), hist, 64, C.byref(nh), C.byref(fs),
+                                               C.byref(ok), C.byref(jit)))
+    except BaseException:
+        if own:
+            ctx.close()
+        raise
+    pre = Preconditioner(ctx, x.shape[0], int(fs.value), float(lambda_p), bool(jit.value), own)
+    return AdaptiveResult(bool(ok.value), pre, int(fs.value), [_qr(hist[i]) for i in range(min(nh.value, 64))])
 
 
 # ----------------------------------------------------------------------------- f2: KRRM model file

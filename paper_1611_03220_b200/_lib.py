@@ -94,6 +94,14 @@ _EXC = {
 }
 
 
+class QualityReportC(C.Structure):
+    _fields_ = [("passed", C.c_int32), ("pad_", C.c_int32), ("cond1_value", C.c_double),
+                ("cond2_ratio_low", C.c_double), ("cond2_ratio_high", C.c_double), ("rank_of_p", C.c_int64),
+                ("sketch_size", C.c_int64), ("lambda_", C.c_double), ("cond1_threshold", C.c_double),
+                ("spectrum_cut", C.c_double), ("ratio_low_threshold", C.c_double),
+                ("ratio_high_threshold", C.c_double)]
+
+
 class RhsStatsC(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("final_residual", C.c_double)]
 
@@ -118,6 +126,9 @@ _SIGS = {
     "krr_set_option": [_vp, C.c_char_p, _d],
     "krr_get_option": [_vp, C.c_char_p, C.POINTER(_d)],
     "krr_set_precision": [_vp, _i],
+    "krr_quality_test": [_vp, _d, C.POINTER(QualityReportC)],
+    "krr_adaptive_build": [_vp, _d, _d, _i64, _i64, C.c_uint64, _vp, _i, C.POINTER(_i), C.POINTER(_i64),
+                           C.POINTER(_i), C.POINTER(_i)],
     "krr_model_save": [C.c_char_p, _d, _d, C.c_uint64, _vp, _i64, _vp, _i64, _i64, _vp, _i64],
     "krr_model_info": [C.c_char_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                        C.POINTER(_d), C.POINTER(_d), C.POINTER(C.c_uint64)],

@@ -260,4 +260,19 @@ Schedule make_schedule(int64_t n, int world, int rank) {
     return s;
 }
 
+void power_iteration_start(uint64_t seed, int64_t n, double* v) {
+    std::mt19937_64 gen(seed);
+    std::normal_distribution<double> normal(0.0, 1.0);
+    double ss = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        v[i] = normal(gen);
+        ss += v[i] * v[i];
+    }
+    const double nrm = std::sqrt(ss);
+    if (nrm > 0.0)
+        for (int64_t i = 0; i < n; ++i) v[i] /= nrm;
+}
+
+int64_t default_initial_sketch_size(int64_t n) { return std::max<int64_t>(64, (n + 63) / 64); }
+
 }  // namespace krr

@@ -29,6 +29,15 @@ Schedule make_schedule(int64_t n, int world, int rank);
 // Row shard of the sketch (Z / U) rows: contiguous blocks of ceil(n / world).
 void shard_rows(int64_t n, int world, int rank, int64_t* z0, int64_t* z1);
 
+// power_iteration_spectral_norm's start vector (numerics.cpp:160-164): mt19937_64(seed)
+// normal(0, 1) draws, normalised.
+void power_iteration_start(uint64_t seed, int64_t n, double* v);
+
+// default_initial_sketch_size (precond.cpp:102-104): max(64, ceil(n / 64)).
+int64_t default_initial_sketch_size(int64_t n);
+// kAttemptSeedStride (sketches.hpp:16): adaptive attempt a uses master + a * stride.
+constexpr uint64_t kAttemptSeedStride = 0xD1B54A32D192ED03ULL;
+
 // KRRM model file (io.cpp:192-261), model_io.cpp.
 struct ModelMeta {
     int64_t n = 0, d = 0, t = 0;

@@ -652,6 +652,184 @@ DevOp precond_op(Ctx& c) {
     return [&c](const double* din, double* dout) { precond_apply_dev(c, din, dout); };
 }
 
+// (K + lambda I) V for V n x t row-major on the device (K1T batches, or column by column).
+void matmat_dev(Ctx& c, const double* V, int64_t t, double lambda, double* Out) {
+    const int64_t n = c.n;
+    if (t > 1 && c.batched && c.precision == 64) {
+        const int T = batch_width(t);
+        ensure_batched(c, T);
+        for (int64_t c0 = 0; c0 < t; c0 += T) {
+            pad_cols_launch(V, n, t, c0, c.plan.n_pad, T, c.bin.get(), c.stream);
+            matvecT_dev(c, c.bin.get(), c.bout.get(), T, lambda);
+            unpad_cols_launch(c.bout.get(), n, t, c0, T, Out, c.stream);
+        }
+    } else {
+        for (int64_t j = 0; j < t; ++j) {
+            gather_col_launch(V, n, t, j, c.vin.get(), c.stream);
+            matvec_dev(c, c.vin.get(), c.vout.get(), lambda);
+            scatter_col_launch(c.vout.get(), n, t, j, Out, c.stream);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- f3: quality test / adaptive sizing
+// symmetric_eigen (numerics.cpp:144-154): eigenvalues descending, eigenvectors as columns (in
+// place of A, col-major s x s); cuSOLVER returns them ascending, the caller reads them reversed.
+void syevd_dev(Ctx& c, double* A, int64_t s, double* evals) {
+    int lwork = 0;
+    cusolver_check(cusolverDnSetStream(c.sol, c.stream), "cusolverDnSetStream");
+    cusolver_check(cusolverDnDsyevd_bufferSize(c.sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, int(s), A,
+                                               int(s), evals, &lwork),
+                   "syevd_bufferSize");
+    DevMem<double> work;
+    DevMem<int> info;
+    work.ensure(size_t(std::max(1, lwork)));
+    info.ensure(1);
+    cusolver_check(cusolverDnDsyevd(c.sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, int(s), A, int(s), evals,
+                                    work.get(), lwork, info.get()),
+                   "syevd");
+    int h = 0;
+    KRR_CUDA(cudaMemcpyAsync(&h, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (h != 0) fail(KRR_ERR_NOT_POSITIVE_DEFINITE, "symmetric_eigen: eigensolver did not converge");
+}
+
+// quality_test (precond.cpp:60-100) of the context's raw sketch Z against its data's K.
+krr_quality_report quality_test_dev(Ctx& c, double lambda) {
+    if (!(lambda > 0.0)) fail(KRR_ERR_NON_POSITIVE_LAMBDA, "quality_test: lambda must be positive");
+    if (!c.has_sketch || c.has_pre) fail(KRR_ERR_STATE, "quality_test needs the raw sketch (before the preconditioner)");
+    if (c.world != 1) fail(KRR_ERR_STATE, "quality_test is single-rank");
+    if (c.pn != c.n) fail(KRR_ERR_DIMENSION_MISMATCH, "quality_test: K and Z dimensions do not match");
+    c.set_device();
+    const int64_t n = c.n, s = c.s;
+    krr_quality_report r{};
+    r.lambda = lambda;
+    r.sketch_size = s;
+    r.spectrum_cut = 0.05 * lambda;
+    r.cond1_threshold = 0.1 * lambda;
+    r.ratio_low_threshold = 0.9;
+    r.ratio_high_threshold = 1.1;
+    r.cond2_ratio_low = 1.0;
+    r.cond2_ratio_high = 1.0;
+    const double one = 1.0, zero = 0.0, mone = -1.0;
+    cublas_check(cublasSetStream(c.blas, c.stream), "cublasSetStream");
+    // retained_left_singular_basis (precond.cpp:42-58): eig(Z^T Z), B = Z V_k / sqrt(ev)
+    DevMem<double> G, ev;
+    G.ensure(size_t(s * s));
+    ev.ensure(size_t(s));
+    cublas_check(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(s), int(n), &one, c.Z.get(), int(s),
+                             &zero, G.get(), int(s)),
+                 "cublasDsyrk(Z^T Z)");
+    syevd_dev(c, G.get(), s, ev.get());
+    std::vector<double> evh(static_cast<size_t>(s));
+    KRR_CUDA(cudaMemcpyAsync(evh.data(), ev.get(), sizeof(double) * size_t(s), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    std::reverse(evh.begin(), evh.end());  // descending
+    const double max_ev = s > 0 ? std::max(0.0, evh[0]) : 0.0;
+    const double zero_floor = 1e-20 * max_ev;
+    int64_t k = 0;
+    while (k < s && evh[size_t(k)] > r.spectrum_cut && evh[size_t(k)] > zero_floor) ++k;
+    r.rank_of_p = k;
+    DevMem<double> Vk, Bt, tk, v, w, w2;
+    if (k > 0) {
+        // V_k scaled: column i = eigenvector of the i-th largest eigenvalue / sqrt(ev_i)
+        // (cuSOLVER's ascending column s-1-i); host-side scale list, device gather
+        std::vector<double> sc(static_cast<size_t>(k));
+        for (int64_t i = 0; i < k; ++i) sc[size_t(i)] = 1.0 / std::sqrt(evh[size_t(i)]);
+        Vk.ensure(size_t(s * k));
+        for (int64_t i = 0; i < k; ++i) {
+            KRR_CUDA(cudaMemcpyAsync(Vk.get() + i * s, G.get() + (s - 1 - i) * s, sizeof(double) * size_t(s),
+                                     cudaMemcpyDeviceToDevice, c.stream));
+            cublas_check(cublasDscal(c.blas, int(s), &sc[size_t(i)], Vk.get() + i * s, 1), "cublasDscal");
+        }
+        // B (n x k row-major) = col-major B^T (k x n) = V_k^T (k x s) . Z^T (s x n)
+        Bt.ensure(size_t(k * n));
+        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, int(k), int(n), int(s), &one, Vk.get(), int(s),
+                                 c.Z.get(), int(s), &zero, Bt.get(), int(k)),
+                     "cublasDgemm(B)");
+        tk.ensure(size_t(k));
+    }
+    // condition 1: power_iteration_spectral_norm (numerics.cpp:156-190) on (I-P) K (I-P),
+    // start vector from mt19937_64(7) normal draws, tol 1e-4, 500 iterations
+    const int64_t n_pad = c.plan.n_pad;
+    v.ensure(size_t(n_pad));
+    w.ensure(size_t(n_pad));
+    w2.ensure(size_t(n_pad));
+    KRR_CUDA(cudaMemsetAsync(v.get(), 0, sizeof(double) * size_t(n_pad), c.stream));
+    KRR_CUDA(cudaMemsetAsync(w.get(), 0, sizeof(double) * size_t(n_pad), c.stream));
+    KRR_CUDA(cudaMemsetAsync(w2.get(), 0, sizeof(double) * size_t(n_pad), c.stream));
+    {
+        std::vector<double> v0(static_cast<size_t>(n));
+        power_iteration_start(7, n, v0.data());
+        KRR_CUDA(cudaMemcpyAsync(v.get(), v0.data(), sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c.stream));
+    }
+    auto deflate = [&](double* x) {  // x -= B (B^T x)
+        if (k == 0) return;
+        cublas_check(cublasDgemv(c.blas, CUBLAS_OP_N, int(k), int(n), &one, Bt.get(), int(k), x, 1, &zero, tk.get(), 1),
+                     "gemv B^T x");
+        cublas_check(cublasDgemv(c.blas, CUBLAS_OP_T, int(k), int(n), &mone, Bt.get(), int(k), tk.get(), 1, &one, x, 1),
+                     "gemv x - B t");
+    };
+    double prev = 0.0;
+    r.cond1_value = 0.0;
+    for (int it = 1; it <= 500; ++it) {
+        KRR_CUDA(cudaMemcpyAsync(w2.get(), v.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, c.stream));
+        deflate(w2.get());
+        matvec_dev(c, w2.get(), w.get(), 0.0);  // K (no diagonal shift)
+        deflate(w.get());
+        double rq = 0.0, nw = 0.0;
+        cublas_check(cublasDdot(c.blas, int(n), v.get(), 1, w.get(), 1, &rq), "dot");
+        cublas_check(cublasDnrm2(c.blas, int(n), w.get(), 1, &nw), "nrm2");
+        r.cond1_value = rq;
+        if (nw == 0.0) {
+            r.cond1_value = 0.0;
+            break;
+        }
+        if (it > 1 && std::abs(rq - prev) <= 1e-4 * std::abs(rq)) break;
+        prev = rq;
+        const double inv = 1.0 / nw;
+        KRR_CUDA(cudaMemcpyAsync(v.get(), w.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, c.stream));
+        cublas_check(cublasDscal(c.blas, int(n), &inv, v.get(), 1), "scal");
+    }
+    // condition 2 on range(P): eigenvalues of Sigma^-1 (B^T K B) Sigma^-1, symmetrised
+    if (k > 0) {
+        DevMem<double> B, KB, M;
+        B.ensure(size_t(n * k));
+        KB.ensure(size_t(n * k));
+        // B row-major n x k is exactly Bt col-major: the same buffer
+        matmat_dev(c, Bt.get(), k, 0.0, KB.get());
+        M.ensure(size_t(k * k));
+        // M (k x k) = B^T (K B): col-major Bt (k x n) . KBt (k x n)^T
+        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_T, int(k), int(k), int(n), &one, Bt.get(), int(k),
+                                 KB.get(), int(k), &zero, M.get(), int(k)),
+                     "cublasDgemm(B^T K B)");
+        std::vector<double> mh(static_cast<size_t>(k * k));
+        KRR_CUDA(cudaMemcpyAsync(mh.data(), M.get(), sizeof(double) * size_t(k * k), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        std::vector<double> inv_sigma(static_cast<size_t>(k));
+        for (int64_t i = 0; i < k; ++i) inv_sigma[size_t(i)] = 1.0 / std::sqrt(evh[size_t(i)]);
+        std::vector<double> sym(static_cast<size_t>(k * k));
+        for (int64_t i = 0; i < k; ++i)
+            for (int64_t j = 0; j < k; ++j) {
+                const double a = inv_sigma[size_t(i)] * mh[size_t(j * k + i)] * inv_sigma[size_t(j)];
+                const double b = inv_sigma[size_t(j)] * mh[size_t(i * k + j)] * inv_sigma[size_t(i)];
+                sym[size_t(j * k + i)] = (a + b) / 2.0;
+            }
+        KRR_CUDA(cudaMemcpyAsync(M.get(), sym.data(), sizeof(double) * size_t(k * k), cudaMemcpyHostToDevice, c.stream));
+        DevMem<double> ev2;
+        ev2.ensure(size_t(k));
+        syevd_dev(c, M.get(), k, ev2.get());
+        std::vector<double> e2(static_cast<size_t>(k));
+        KRR_CUDA(cudaMemcpyAsync(e2.data(), ev2.get(), sizeof(double) * size_t(k), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        r.cond2_ratio_high = e2[size_t(k - 1)];
+        r.cond2_ratio_low = e2[0];
+    }
+    r.passed = r.cond1_value <= r.cond1_threshold && r.cond2_ratio_low >= r.ratio_low_threshold &&
+               r.cond2_ratio_high <= r.ratio_high_threshold;
+    return r;
+}
+
 // solve_regularized (solver.cpp:69-94): per-column sequential PCG.
 void solve_gaussian(Ctx& c, double lambda, const double* Y, int64_t t, double tau, int max_iter,
                     int use_precond, double* C, krr_rhs_stats* stats, double* hist,
@@ -940,21 +1118,7 @@ int krr_kernel_matvec(krr_ctx* ctx, double lambda, const double* V, int64_t t, d
         c.mat_b.ensure(size_t(n * t));
         KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), V, sizeof(double) * size_t(n * t),
                                  cudaMemcpyHostToDevice, c.stream));
-        if (t > 1 && c.batched && c.precision == 64) {
-            const int T = krr::batch_width(t);
-            krr::ensure_batched(c, T);
-            for (int64_t c0 = 0; c0 < t; c0 += T) {
-                krr::pad_cols_launch(c.mat_a.get(), n, t, c0, c.plan.n_pad, T, c.bin.get(), c.stream);
-                krr::matvecT_dev(c, c.bin.get(), c.bout.get(), T, lambda);
-                krr::unpad_cols_launch(c.bout.get(), n, t, c0, T, c.mat_b.get(), c.stream);
-            }
-        } else {
-            for (int64_t j = 0; j < t; ++j) {
-                krr::gather_col_launch(c.mat_a.get(), n, t, j, c.vin.get(), c.stream);
-                krr::matvec_dev(c, c.vin.get(), c.vout.get(), lambda);
-                krr::scatter_col_launch(c.vout.get(), n, t, j, c.mat_b.get(), c.stream);
-            }
-        }
+        krr::matmat_dev(c, c.mat_a.get(), t, lambda, c.mat_b.get());
         KRR_CUDA(cudaMemcpyAsync(out, c.mat_b.get(), sizeof(double) * size_t(n * t),
                                  cudaMemcpyDeviceToHost, c.stream));
         c.sync();
@@ -1302,6 +1466,48 @@ int krr_shard_rows(int64_t n, int world, int rank, int64_t* row_begin, int64_t* 
 int krr_generate_config(int cfg, int64_t n, int64_t d, int64_t t, uint64_t seed, double* X,
                         double* Y) {
     return guard([&] { krr::generate_config(cfg, n, d, t, seed, X, Y); });
+}
+
+int krr_quality_test(krr_ctx* ctx, double lambda, krr_quality_report* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        *out = krr::quality_test_dev(c, lambda);
+    });
+}
+
+int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0, int64_t s_max,
+                       uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
+                       int64_t* final_size, int* passed, int* jitter_used) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (s0 < 1) fail(KRR_ERR_INVALID_ARGUMENT, "adaptive_build: s0 must be at least 1");
+        if (s_max < s0) fail(KRR_ERR_INVALID_ARGUMENT, "adaptive_build: s_max must be >= s0");
+        const double lp = lambda_p > 0.0 ? lambda_p : lambda;
+        int64_t s = s0;
+        int nh = 0;
+        bool ok = false;
+        for (int attempt = 0;; ++attempt) {
+            const uint64_t seed = master_seed + uint64_t(attempt) * krr::kAttemptSeedStride;
+            std::vector<double> W(static_cast<size_t>(s * c.d)), b(static_cast<size_t>(s));
+            krr::rff_realize(seed, c.d, s, c.sigma, W.data(), b.data());
+            krr::rff_build(c, W.data(), b.data(), s);
+            const krr_quality_report rep = krr::quality_test_dev(c, lambda);
+            if (history && nh < max_history) history[nh] = rep;
+            ++nh;
+            if (final_size) *final_size = s;
+            if (rep.passed) {
+                ok = true;
+                break;
+            }
+            if (s >= s_max) break;
+            s = std::min(2 * s, s_max);
+        }
+        if (n_history) *n_history = nh;
+        if (passed) *passed = ok ? 1 : 0;
+        krr::precond_build(c, lp, jitter_used);
+    });
 }
 
 int krr_model_save(const char* path, double sigma, double lambda, uint64_t seed, const double* label_map,
