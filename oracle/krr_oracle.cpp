@@ -40,6 +40,7 @@
 // =============================================================================
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdint>
 #include <cstring>
 #include <numbers>
@@ -609,6 +610,280 @@ int oracle_train(const double* x, std::int64_t n, std::int64_t d, const double* 
     return oracle_solve_gaussian(x, n, d, sigma, lambda, u.data(), s, lp, ymat, t, tau, max_iter,
                                  dense_k, c, iterations, converged, final_residual, history,
                                  total_matvecs, order);
+}
+
+}  // extern "C"
+
+// ============================================================================= SURVEY 8f4
+// Polynomial kernel (kernels.cpp:10-14 ipow, :56-62 augmented_inputs, :89-99 gram,
+// :103-121 cross_gram) and the TensorSketch / SRHT / Gaussian sketch stages
+// (sketches.cpp:43-153), with realize_chain's stage seeds (sketches.cpp:213-242).
+namespace {
+
+// kernels.cpp:10-14: repeated multiplication, base first.
+double ipow_ref(double base, int e) {
+    double r = base;
+    for (int i = 1; i < e; ++i) r *= base;
+    return r;
+}
+
+bool poly_spec_ok(double gamma, double offset, int degree) {  // kernels.cpp:39-43
+    return degree >= 1 && offset >= 0.0 && gamma > 0.0;
+}
+
+// augmented_inputs: [sqrt(gamma) x, sqrt(offset)], n x (d+1) row-major.
+std::vector<double> augment_rows(const double* x, std::int64_t n, std::int64_t d, double gamma,
+                                 double offset) {
+    const std::int64_t da = d + 1;
+    const double sg = std::sqrt(gamma), so = std::sqrt(offset);
+    std::vector<double> a(static_cast<std::size_t>(n * da));
+    for (std::int64_t i = 0; i < n; ++i) {
+        for (std::int64_t k = 0; k < d; ++k) a[std::size_t(i * da + k)] = sg * x[i * d + k];
+        a[std::size_t(i * da + d)] = so;
+    }
+    return a;
+}
+
+// In-place iterative radix-2 FFT (the published Cooley-Tukey form numerics.cpp:20-46
+// restates): bit-reversal permutation, then butterflies whose twiddle advances by one
+// complex multiplication per butterfly; the inverse divides by the length.
+void fft_radix2(std::vector<std::complex<double>>& a, bool inverse) {
+    const std::size_t n = a.size();
+    std::size_t rev = 0;
+    for (std::size_t i = 1; i < n; ++i) {
+        std::size_t bit = n >> 1;
+        while (rev & bit) {
+            rev ^= bit;
+            bit >>= 1;
+        }
+        rev ^= bit;
+        if (i < rev) std::swap(a[i], a[rev]);
+    }
+    for (std::size_t len = 2; len <= n; len <<= 1) {
+        const double ang = (inverse ? 2.0 : -2.0) * std::numbers::pi / double(len);
+        const std::complex<double> step = std::polar(1.0, ang);
+        for (std::size_t base = 0; base < n; base += len) {
+            std::complex<double> w(1.0, 0.0);
+            for (std::size_t j = 0; j < len / 2; ++j) {
+                const std::complex<double> u = a[base + j];
+                const std::complex<double> v = a[base + j + len / 2] * w;
+                a[base + j] = u + v;
+                a[base + j + len / 2] = u - v;
+                w *= step;
+            }
+        }
+    }
+    if (inverse)
+        for (auto& v : a) v /= double(n);
+}
+
+std::int64_t pow2_ceil(std::int64_t m) {
+    std::int64_t p = 1;
+    while (p < m) p <<= 1;
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int oracle_poly_gram(const double* x, std::int64_t n, std::int64_t d, double gamma, double offset,
+                     int degree, double* k, int order) {
+    if (!poly_spec_ok(gamma, offset, degree)) return INVALID_ARGUMENT;
+    const std::int64_t da = d + 1;
+    const std::vector<double> a = augment_rows(x, n, d, gamma, offset);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t j = i; j < n; ++j) {
+            const double v = ipow_ref(gemm_dot(a.data() + i * da, a.data() + j * da, da, order), degree);
+            k[i * n + j] = v;
+            k[j * n + i] = v;
+        }
+    return OK;
+}
+
+int oracle_poly_cross(const double* q, std::int64_t m, const double* x, std::int64_t n, std::int64_t d,
+                      double gamma, double offset, int degree, double* k, int order) {
+    if (!poly_spec_ok(gamma, offset, degree)) return INVALID_ARGUMENT;
+    const std::int64_t da = d + 1;
+    const std::vector<double> aq = augment_rows(q, m, d, gamma, offset);
+    const std::vector<double> ax = augment_rows(x, n, d, gamma, offset);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < m; ++i)
+        for (std::int64_t j = 0; j < n; ++j)
+            k[i * n + j] = ipow_ref(gemm_dot(aq.data() + i * da, ax.data() + j * da, da, order), degree);
+    return OK;
+}
+
+// out = (K + lambda I) V for the polynomial kernel, K on the fly (same entries as the gram).
+int oracle_poly_matvec(const double* x, std::int64_t n, std::int64_t d, double gamma, double offset,
+                       int degree, double lambda, const double* v, std::int64_t t, double* out, int order) {
+    if (!poly_spec_ok(gamma, offset, degree)) return INVALID_ARGUMENT;
+    const std::int64_t da = d + 1;
+    const std::vector<double> a = augment_rows(x, n, d, gamma, offset);
+#pragma omp parallel
+    {
+        std::vector<double> krow(static_cast<std::size_t>(n));
+#pragma omp for schedule(dynamic, 4)
+        for (std::int64_t i = 0; i < n; ++i) {
+            for (std::int64_t j = 0; j < n; ++j) {
+                const std::int64_t lo = std::min(i, j), hi = std::max(i, j);
+                krow[std::size_t(j)] =
+                    ipow_ref(gemm_dot(a.data() + lo * da, a.data() + hi * da, da, order), degree);
+            }
+            for (std::int64_t c = 0; c < t; ++c)
+                out[i * t + c] = dot_strided(krow.data(), 1, v + c, t, n, order) + lambda * v[i * t + c];
+        }
+    }
+    return OK;
+}
+
+// solve_regularized (solver.cpp:69-94) on a given dense K (any kernel family).
+int oracle_solve_dense(const double* k, std::int64_t n, double lambda, const double* u, std::int64_t s,
+                       double lambda_p, const double* ymat, std::int64_t t, double tau, int max_iter,
+                       double* c, int* iterations, int* converged, double* final_residual, double* history,
+                       long long* total_matvecs, int order) {
+    if (!(lambda > 0.0)) return NON_POSITIVE_LAMBDA;
+    DenseOp dop{k, n, lambda, order};
+    PrecOp pop{u, s, n, lambda_p, order};
+    std::vector<double> ycol(static_cast<std::size_t>(n)), xcol(static_cast<std::size_t>(n));
+    long long total = 0;
+    for (std::int64_t j = 0; j < t; ++j) {
+        for (std::int64_t i = 0; i < n; ++i) ycol[std::size_t(i)] = ymat[i * t + j];
+        const int st = oracle_pcg_solve(n, dense_op, &dop, u ? prec_op : nullptr, &pop, ycol.data(), tau,
+                                        max_iter, nullptr, nullptr, xcol.data(), &iterations[j], &converged[j],
+                                        &final_residual[j], history ? history + j * max_iter : nullptr, order);
+        if (st != OK) return st;
+        for (std::int64_t i = 0; i < n; ++i) c[i * t + j] = xcol[std::size_t(i)];
+        total += iterations[j];
+    }
+    if (total_matvecs) *total_matvecs = total;
+    return OK;
+}
+
+// TensorSketchMap ctor (sketches.cpp:51-69): per mode the whole hash table, then the
+// whole sign table.  `seed` is the map's own seed (realize_chain passes stage 0).
+int oracle_tensorsketch_realize(std::uint64_t seed, std::int64_t in_dim, std::int64_t s, int degree,
+                                std::uint32_t* hash, double* sign) {
+    if (s < 1 || degree < 1) return INVALID_ARGUMENT;
+    std::mt19937_64 gen(seed);
+    std::uniform_int_distribution<std::uint32_t> bucket(0, std::uint32_t(s - 1));
+    std::uniform_int_distribution<int> coin(0, 1);
+    for (int q = 0; q < degree; ++q) {
+        for (std::int64_t j = 0; j < in_dim; ++j) hash[q * in_dim + j] = bucket(gen);
+        for (std::int64_t j = 0; j < in_dim; ++j) sign[q * in_dim + j] = coin(gen) ? 1.0 : -1.0;
+    }
+    return OK;
+}
+
+// TensorSketchMap::apply (sketches.cpp:71-93) row by row: count sketches, product of
+// their spectra, inverse transform, wrap mod s.  x rows have in_dim entries (already
+// augmented for the polynomial kernel).
+int oracle_tensorsketch_apply_rows(const std::uint32_t* hash, const double* sign, std::int64_t in_dim,
+                                   std::int64_t s, int degree, const double* x, std::int64_t n, double* z) {
+    if (s < 1 || degree < 1) return INVALID_ARGUMENT;
+    const bool p2 = (s & (s - 1)) == 0;
+    const std::int64_t padded = p2 ? s : pow2_ceil(std::int64_t(degree) * (s - 1) + 1);
+#pragma omp parallel
+    {
+        std::vector<double> cs(static_cast<std::size_t>(s));
+        std::vector<std::complex<double>> spec, f(static_cast<std::size_t>(padded));
+#pragma omp for schedule(static)
+        for (std::int64_t i = 0; i < n; ++i) {
+            const double* xi = x + i * in_dim;
+            double* zi = z + i * s;
+            for (int q = 0; q < degree; ++q) {
+                std::fill(cs.begin(), cs.end(), 0.0);
+                for (std::int64_t j = 0; j < in_dim; ++j)  // countsketch_apply (sketches.cpp:43-49)
+                    cs[hash[q * in_dim + j]] += sign[q * in_dim + j] * xi[j];
+                if (degree == 1) break;
+                std::fill(f.begin(), f.end(), std::complex<double>(0.0, 0.0));
+                for (std::int64_t b = 0; b < s; ++b) f[std::size_t(b)] = {cs[std::size_t(b)], 0.0};
+                fft_radix2(f, false);
+                if (q == 0) {
+                    spec = f;
+                } else {
+                    for (std::int64_t b = 0; b < padded; ++b) spec[std::size_t(b)] *= f[std::size_t(b)];
+                }
+            }
+            if (degree == 1) {
+                std::copy(cs.begin(), cs.end(), zi);
+                continue;
+            }
+            fft_radix2(spec, true);
+            std::fill(zi, zi + s, 0.0);
+            for (std::int64_t b = 0; b < padded; ++b) zi[b % s] += spec[std::size_t(b)].real();
+        }
+    }
+    return OK;
+}
+
+// SrhtMap ctor (sketches.cpp:95-109): signs for the padded length, then the sampled rows.
+int oracle_srht_realize(std::uint64_t seed, std::int64_t in_dim, std::int64_t s, double* sign,
+                        std::int64_t* rows) {
+    if (s < 1 || in_dim < 1) return INVALID_ARGUMENT;
+    const std::int64_t p = pow2_ceil(in_dim);
+    std::mt19937_64 gen(seed);
+    std::uniform_int_distribution<int> coin(0, 1);
+    std::uniform_int_distribution<std::int64_t> row(0, p - 1);
+    for (std::int64_t i = 0; i < p; ++i) sign[i] = coin(gen) ? 1.0 : -1.0;
+    for (std::int64_t i = 0; i < s; ++i) rows[i] = row(gen);
+    return OK;
+}
+
+// SrhtMap::apply (sketches.cpp:111-121): pad, sign flip, Walsh-Hadamard (Sylvester order,
+// numerics.cpp:81-95), sample, scale by 1/sqrt(s).
+int oracle_srht_apply_rows(const double* sign, const std::int64_t* rows, std::int64_t in_dim, std::int64_t s,
+                           const double* x, std::int64_t n, double* z) {
+    if (s < 1 || in_dim < 1) return INVALID_ARGUMENT;
+    const std::int64_t p = pow2_ceil(in_dim);
+    const double scale = 1.0 / std::sqrt(double(s));
+#pragma omp parallel
+    {
+        std::vector<double> h(static_cast<std::size_t>(p));
+#pragma omp for schedule(static)
+        for (std::int64_t i = 0; i < n; ++i) {
+            for (std::int64_t j = 0; j < p; ++j) h[std::size_t(j)] = (j < in_dim ? x[i * in_dim + j] : 0.0) * sign[j];
+            for (std::int64_t half = 1; half < p; half <<= 1)
+                for (std::int64_t b = 0; b < p; b += 2 * half)
+                    for (std::int64_t j = b; j < b + half; ++j) {
+                        const double u = h[std::size_t(j)], v = h[std::size_t(j + half)];
+                        h[std::size_t(j)] = u + v;
+                        h[std::size_t(j + half)] = u - v;
+                    }
+            for (std::int64_t k = 0; k < s; ++k) z[i * s + k] = scale * h[std::size_t(rows[k])];
+        }
+    }
+    return OK;
+}
+
+// GaussianMap ctor (sketches.cpp:128-135): proj s x in_dim, row by row, normal(0, 1).
+int oracle_gaussmap_realize(std::uint64_t seed, std::int64_t in_dim, std::int64_t s, double* proj) {
+    if (s < 1) return INVALID_ARGUMENT;
+    std::mt19937_64 gen(seed);
+    std::normal_distribution<double> normal(0.0, 1.0);
+    for (std::int64_t i = 0; i < s * in_dim; ++i) proj[i] = normal(gen);
+    return OK;
+}
+
+// GaussianMap::apply (sketches.cpp:137-140): (proj x) / sqrt(s).
+int oracle_gaussmap_apply_rows(const double* proj, std::int64_t in_dim, std::int64_t s, const double* x,
+                               std::int64_t n, double* z, int order) {
+    if (s < 1) return INVALID_ARGUMENT;
+    const double root = std::sqrt(double(s));
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t k = 0; k < s; ++k)
+            z[i * s + k] = dot_strided(proj + k * in_dim, 1, x + i * in_dim, 1, in_dim, order) / root;
+    return OK;
+}
+
+// augmented_inputs (kernels.cpp:56-62).
+int oracle_poly_augment(const double* x, std::int64_t n, std::int64_t d, double gamma, double offset,
+                        double* out) {
+    const std::vector<double> a = augment_rows(x, n, d, gamma, offset);
+    std::copy(a.begin(), a.end(), out);
+    return OK;
 }
 
 }  // extern "C"

@@ -74,6 +74,18 @@ def lib() -> C.CDLL:
                                        _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_longlong), _i], _i),
             "oracle_train": ([_vp, _i64, _i64, _vp, _i64, _d, _d, _d, _i64, C.c_uint64, _d, _i, _i,
                               _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_longlong), _i], _i),
+            "oracle_poly_gram": ([_vp, _i64, _i64, _d, _d, _i, _vp, _i], _i),
+            "oracle_poly_cross": ([_vp, _i64, _vp, _i64, _i64, _d, _d, _i, _vp, _i], _i),
+            "oracle_poly_matvec": ([_vp, _i64, _i64, _d, _d, _i, _d, _vp, _i64, _vp, _i], _i),
+            "oracle_poly_augment": ([_vp, _i64, _i64, _d, _d, _vp], _i),
+            "oracle_solve_dense": ([_vp, _i64, _d, _vp, _i64, _d, _vp, _i64, _d, _i, _vp, _vp, _vp, _vp, _vp,
+                                    C.POINTER(C.c_longlong), _i], _i),
+            "oracle_tensorsketch_realize": ([C.c_uint64, _i64, _i64, _i, _vp, _vp], _i),
+            "oracle_tensorsketch_apply_rows": ([_vp, _vp, _i64, _i64, _i, _vp, _i64, _vp], _i),
+            "oracle_srht_realize": ([C.c_uint64, _i64, _i64, _vp, _vp], _i),
+            "oracle_srht_apply_rows": ([_vp, _vp, _i64, _i64, _vp, _i64, _vp], _i),
+            "oracle_gaussmap_realize": ([C.c_uint64, _i64, _i64, _vp], _i),
+            "oracle_gaussmap_apply_rows": ([_vp, _i64, _i64, _vp, _i64, _vp, _i], _i),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -310,7 +322,7 @@ def rf_baseline(x, y, sigma: float, lam: float, s: int, seed: int, order: int = 
     return w, w_rff, b_rff
 
 
-def quality_test(x, sigma: float, z, lam: float, order: int = DEFAULT_ORDER) -> dict:
+def quality_test(x, sigma, z, lam: float, order: int = DEFAULT_ORDER, k=None) -> dict:
     """quality_test (precond.cpp:60-100) restated with the dense oracle K (small n only):
     retained_left_singular_basis (precond.cpp:42-58) through eig(Z'Z) (Eigen sorts ascending,
     the reference flips to descending, numerics.cpp:144-154), condition 1 by the reference's
@@ -318,7 +330,8 @@ def quality_test(x, sigma: float, z, lam: float, order: int = DEFAULT_ORDER) -> 
     (I-P)K(I-P), condition 2 from eig(Sigma^-1 (B'KB) Sigma^-1).  Test infrastructure only."""
     x, z = f64(x), f64(z)
     n, s = z.shape
-    k = gram_matrix(x, sigma, order)
+    if k is None:
+        k = gram_matrix(x, sigma, order)
     rep = {"lambda": lam, "sketch_size": s, "spectrum_cut": 0.05 * lam, "cond1_threshold": 0.1 * lam,
            "cond2_ratio_low": 1.0, "cond2_ratio_high": 1.0}
     ev, vec = np.linalg.eigh(z.T @ z)
@@ -373,6 +386,215 @@ def adaptive_sizes(x, sigma: float, lam: float, s0: int, s_max: int, master_seed
         seed = (master_seed + attempt * ATTEMPT_SEED_STRIDE) % (1 << 64)
         w, b = rff_realize(seed, x.shape[1], s, sigma)
         rep = quality_test(x, sigma, rff_apply_rows(x, w, b), lam)
+        out.append((s, rep))
+        if rep["passed"] or s >= s_max:
+            break
+        s = min(2 * s, s_max)
+    return out
+
+
+# ============================================================================= SURVEY 8f4
+# Polynomial kernel and the TensorSketch / SRHT / Gaussian sketch chain.  Kernels are
+# passed as dicts {"family": "gaussian", "sigma": S} or {"family": "polynomial",
+# "gamma": G, "offset": C, "degree": Q} (kernels.hpp:15-27).
+
+STAGE_SEED_STRIDE = 0x9E3779B97F4A7C15  # sketches.hpp:14
+
+
+def stage_seed(master: int, stage: int) -> int:
+    """sketches.cpp:18-20."""
+    return (int(master) + (stage + 1) * STAGE_SEED_STRIDE) % (1 << 64)
+
+
+def poly_gram(x, gamma: float, offset: float, degree: int, order: int = DEFAULT_ORDER) -> np.ndarray:
+    """kernels.cpp:89-99."""
+    x = f64(x)
+    k = np.empty((x.shape[0], x.shape[0]))
+    _chk(lib().oracle_poly_gram(_p(x), x.shape[0], x.shape[1], gamma, offset, degree, _p(k), order), "poly_gram")
+    return k
+
+
+def poly_cross(q, x, gamma: float, offset: float, degree: int, order: int = DEFAULT_ORDER) -> np.ndarray:
+    """kernels.cpp:103-121 (polynomial branch)."""
+    q, x = f64(q), f64(x)
+    k = np.empty((q.shape[0], x.shape[0]))
+    _chk(lib().oracle_poly_cross(_p(q), q.shape[0], _p(x), x.shape[0], x.shape[1], gamma, offset, degree, _p(k),
+                                 order), "poly_cross")
+    return k
+
+
+def poly_matvec(x, gamma, offset, degree, lam, v, order: int = DEFAULT_ORDER) -> np.ndarray:
+    x, v = f64(x), f64(v)
+    v2 = v[:, None] if v.ndim == 1 else v
+    out = np.empty_like(v2)
+    _chk(lib().oracle_poly_matvec(_p(x), x.shape[0], x.shape[1], gamma, offset, degree, lam, _p(v2), v2.shape[1],
+                                  _p(out), order), "poly_matvec")
+    return out[:, 0].copy() if v.ndim == 1 else out
+
+
+def poly_augment(x, gamma: float, offset: float) -> np.ndarray:
+    """kernels.cpp:56-62."""
+    x = f64(x)
+    out = np.empty((x.shape[0], x.shape[1] + 1))
+    _chk(lib().oracle_poly_augment(_p(x), x.shape[0], x.shape[1], gamma, offset, _p(out)), "poly_augment")
+    return out
+
+
+def kernel_gram(x, kernel: dict, order: int = DEFAULT_ORDER) -> np.ndarray:
+    if kernel["family"] == "gaussian":
+        return gram_matrix(x, kernel["sigma"], order)
+    return poly_gram(x, kernel["gamma"], kernel["offset"], kernel["degree"], order)
+
+
+def tensorsketch_realize(seed: int, in_dim: int, s: int, degree: int):
+    """TensorSketchMap ctor (sketches.cpp:51-69) with the map's own seed."""
+    h = np.empty((degree, in_dim), dtype=np.uint32)
+    g = np.empty((degree, in_dim))
+    _chk(lib().oracle_tensorsketch_realize(seed % (1 << 64), in_dim, s, degree, _p(h), _p(g)), "tensorsketch_realize")
+    return h, g
+
+
+def tensorsketch_apply_rows(h, g, s: int, x) -> np.ndarray:
+    """TensorSketchMap::apply (sketches.cpp:71-93) row by row."""
+    h = np.ascontiguousarray(h, dtype=np.uint32)
+    g, x = f64(g), f64(x)
+    z = np.empty((x.shape[0], s))
+    _chk(lib().oracle_tensorsketch_apply_rows(_p(h), _p(g), h.shape[1], s, h.shape[0], _p(x), x.shape[0], _p(z)),
+         "tensorsketch_apply_rows")
+    return z
+
+
+def srht_realize(seed: int, in_dim: int, s: int):
+    """SrhtMap ctor (sketches.cpp:95-109)."""
+    p = 1
+    while p < in_dim:
+        p <<= 1
+    sign = np.empty(p)
+    rows = np.empty(s, dtype=np.int64)
+    _chk(lib().oracle_srht_realize(seed % (1 << 64), in_dim, s, _p(sign), _p(rows)), "srht_realize")
+    return sign, rows
+
+
+def srht_apply_rows(sign, rows, in_dim: int, x) -> np.ndarray:
+    """SrhtMap::apply (sketches.cpp:111-121)."""
+    sign, x = f64(sign), f64(x)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    z = np.empty((x.shape[0], rows.shape[0]))
+    _chk(lib().oracle_srht_apply_rows(_p(sign), _p(rows), in_dim, rows.shape[0], _p(x), x.shape[0], _p(z)),
+         "srht_apply_rows")
+    return z
+
+
+def gaussmap_realize(seed: int, in_dim: int, s: int) -> np.ndarray:
+    """GaussianMap ctor (sketches.cpp:128-135)."""
+    proj = np.empty((s, in_dim))
+    _chk(lib().oracle_gaussmap_realize(seed % (1 << 64), in_dim, s, _p(proj)), "gaussmap_realize")
+    return proj
+
+
+def gaussmap_apply_rows(proj, x, order: int = DEFAULT_ORDER) -> np.ndarray:
+    """GaussianMap::apply (sketches.cpp:137-140)."""
+    proj, x = f64(proj), f64(x)
+    z = np.empty((x.shape[0], proj.shape[0]))
+    _chk(lib().oracle_gaussmap_apply_rows(_p(proj), proj.shape[1], proj.shape[0], _p(x), x.shape[0], _p(z), order),
+         "gaussmap_apply_rows")
+    return z
+
+
+def chain_realize(first: str, s1: int, s2: int, s3: int, kernel: dict, d: int, master_seed: int) -> dict:
+    """realize_chain (sketches.cpp:213-242): stage 0 RFF (Gaussian) or TensorSketch on the
+    d+1 augmented inputs (polynomial), stage 1 SRHT, stage 2 Gaussian map."""
+    t = {"first": first, "s1": s1, "s2": s2, "s3": s3, "kernel": dict(kernel), "d": d}
+    if first == "RandomFourier":
+        t["w"], t["b"] = rff_realize(master_seed, d, s1, kernel["sigma"])
+    else:
+        t["hash"], t["sign"] = tensorsketch_realize(stage_seed(master_seed, 0), d + 1, s1, kernel["degree"])
+    prev = s1
+    if s2 > 0:
+        t["srht_sign"], t["srht_rows"] = srht_realize(stage_seed(master_seed, 1), prev, s2)
+        t["srht_in"] = prev
+        prev = s2
+    if s3 > 0:
+        t["proj"] = gaussmap_realize(stage_seed(master_seed, 2), prev, s3)
+        prev = s3
+    return t
+
+
+def chain_apply_rows(t: dict, x, order: int = DEFAULT_ORDER) -> np.ndarray:
+    """SketchChain::apply_rows (sketches.cpp:194-211)."""
+    x = f64(x)
+    k = t["kernel"]
+    if t["first"] == "RandomFourier":
+        z = rff_apply_rows(x, t["w"], t["b"], order)
+    else:
+        z = tensorsketch_apply_rows(t["hash"], t["sign"], t["s1"], poly_augment(x, k["gamma"], k["offset"]))
+    if t["s2"] > 0:
+        z = srht_apply_rows(t["srht_sign"], t["srht_rows"], t["srht_in"], z)
+    if t["s3"] > 0:
+        z = gaussmap_apply_rows(t["proj"], z, order)
+    return z
+
+
+def chain_scaled_to(s1: int, s2: int, s3: int, target: int):
+    """ChainSpec::scaled_to (sketches.cpp:173-192)."""
+    import math
+    out_dim = s3 or s2 or s1
+    factor = float(target) / float(out_dim)
+
+    def scale(v):
+        return max(target, int(math.ceil(float(v) * factor)))
+
+    n1 = scale(s1)
+    n2 = scale(s2) if s2 > 0 else 0
+    n3 = scale(s3) if s3 > 0 else 0
+    if n3 > 0:
+        n3 = target
+    elif n2 > 0:
+        n2 = target
+    else:
+        n1 = target
+    return n1, n2, n3
+
+
+def solve_dense(k, lam, u, lambda_p, y, tau, max_iter, order=DEFAULT_ORDER) -> SolveOut:
+    """solve_regularized (solver.cpp:69-94) on a given dense K."""
+    k, y = f64(k), f64(y)
+    y2 = y[:, None] if y.ndim == 1 else y
+    n, t = y2.shape
+    c = np.empty((n, t))
+    its = np.zeros(t, dtype=np.int32)
+    cvs = np.zeros(t, dtype=np.int32)
+    frs = np.zeros(t)
+    hist = np.zeros((t, max(1, max_iter)))
+    tot = C.c_longlong(0)
+    uptr = None if u is None else _p(f64(u))
+    s = 0 if u is None else u.shape[0]
+    _chk(lib().oracle_solve_dense(_p(k), n, lam, uptr, s, lambda_p, _p(f64(y2)), t, tau, max_iter, _p(c), _p(its),
+                                  _p(cvs), _p(frs), _p(hist), C.byref(tot), order), "solve_dense")
+    return SolveOut(c, its.tolist(), [bool(v) for v in cvs], frs.tolist(), hist, int(tot.value))
+
+
+def train_chain(x, y, kernel: dict, first: str, s1: int, s2: int, s3: int, lam: float, seed: int, tau: float,
+                max_iter: int, lambda_p=None, order=DEFAULT_ORDER) -> SolveOut:
+    """train (solver.cpp:96-133) for any kernel family and chain, dense K (small n)."""
+    lp = lam if lambda_p is None else lambda_p
+    t = chain_realize(first, s1, s2, s3, kernel, f64(x).shape[1], seed)
+    z = chain_apply_rows(t, x, order)
+    u, _ = build_preconditioner(z, lp, order)
+    return solve_dense(kernel_gram(x, kernel, order), lam, u, lp, y, tau, max_iter, order)
+
+
+def adaptive_sizes_chain(x, kernel: dict, first: str, s1: int, s2: int, s3: int, lam: float, s0: int, s_max: int,
+                         master_seed: int) -> list:
+    """adaptive_build (precond.cpp:107-138) for any chain template: attempt a realizes
+    chain_template.scaled_to(s) with master + a * kAttemptSeedStride."""
+    k = kernel_gram(x, kernel)
+    out, s = [], s0
+    for attempt in range(64):
+        seed = (master_seed + attempt * ATTEMPT_SEED_STRIDE) % (1 << 64)
+        a1, a2, a3 = chain_scaled_to(s1, s2, s3, s)
+        t = chain_realize(first, a1, a2, a3, kernel, f64(x).shape[1], seed)
+        rep = quality_test(x, None, chain_apply_rows(t, x), lam, k=k)
         out.append((s, rep))
         if rep["passed"] or s >= s_max:
             break
