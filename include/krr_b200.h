@@ -183,6 +183,92 @@ int krr_rff_download(krr_ctx* ctx, double* Z);
  * build_preconditioner(z, lambda_p) (precond.hpp:28) take any sketch. */
 int krr_sketch_upload(krr_ctx* ctx, const double* Z, int64_t n, int64_t s);
 
+/* ---------------------------------------------------------------- kernel families + sketch chains */
+/* KernelSpec (kernels.hpp:15-27).  family 0 = Gaussian (sigma > 0), 1 = polynomial
+ * k(x, z) = (gamma x.z + offset)^degree (gamma > 0, offset >= 0, degree >= 1);
+ * KernelSpec::validate's rules and messages (kernels.cpp:36-44) -> KRR_ERR_INVALID_ARGUMENT. */
+typedef struct krr_kernel_spec {
+    int32_t family;
+    int32_t degree;
+    double sigma;
+    double gamma;
+    double offset;
+} krr_kernel_spec;
+/* krr_set_data for either family.  For the polynomial kernel the fused K1 / K1T kernels
+ * contract the augmented inputs [sqrt(gamma) x, sqrt(offset)] (kernels.cpp:56-62) on the
+ * FP64 tensor path and raise p_ij to the degree in the epilogue (ipow, kernels.cpp:10-14);
+ * K_ii = ipow(|xa_i|^2) is applied by the finish kernel (kernels.cpp:89-99 keeps the
+ * diagonal, unlike the Gaussian K_ii = 1).  The INT8 / fp32 K1 paths serve the Gaussian
+ * kernel only (polynomial: K1 is always the DMMA kernel; precision 32 is rejected). */
+int krr_set_data_kernel(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const krr_kernel_spec* kernel);
+
+/* ChainSpec (sketches.hpp:96-107): first 0 = RandomFourier (Gaussian kernel), 1 =
+ * TensorSketch (polynomial kernel); optional SRHT stage s2 and Gaussian stage s3 (0 = absent),
+ * non-increasing sizes (ChainSpec::validate, sketches.cpp:155-165). */
+typedef struct krr_chain_spec {
+    int32_t first;
+    int32_t pad_;
+    int64_t s1, s2, s3;
+} krr_chain_spec;
+/* A realized SketchChain's tables (sketches.hpp:109-127), caller-owned host arrays.  Unused
+ * stages' pointers may be NULL.  in_dim = d (RFF) or d + 1 (TensorSketch on augmented inputs).
+ *   rff_w s1 x d, rff_b s1                      (RffMap)
+ *   ts_hash degree x in_dim, ts_sign same       (TensorSketchMap)
+ *   srht_sign next_pow2(s1), srht_rows s2       (SrhtMap)
+ *   gauss_proj s3 x (s2 ? s2 : s1)              (GaussianMap) */
+typedef struct krr_chain_tables {
+    int32_t first;
+    int32_t degree;
+    int64_t in_dim, s1, s2, s3;
+    const double* rff_w;
+    const double* rff_b;
+    const uint32_t* ts_hash;
+    const double* ts_sign;
+    const double* srht_sign;
+    const int64_t* srht_rows;
+    const double* gauss_proj;
+} krr_chain_tables;
+/* Host-side, reference-identical stage draws with the map's OWN seed (realize_chain applies
+ * stage_seed(master, k) = master + (k+1) 0x9E3779B97F4A7C15 for stage k = 0, 1, 2):
+ * TensorSketchMap ctor (sketches.cpp:51-69), SrhtMap ctor (:95-109), GaussianMap ctor (:128-135). */
+int krr_tensorsketch_realize(uint64_t seed, int64_t in_dim, int64_t s, int degree, uint32_t* hash, double* sign);
+int krr_srht_realize(uint64_t seed, int64_t in_dim, int64_t s, double* sign, int64_t* rows);
+int krr_gaussmap_realize(uint64_t seed, int64_t in_dim, int64_t s, double* proj);
+/* SketchChain::apply_rows (sketches.cpp:194-211) on the device for m query rows Xq (m x d,
+ * the context's d and kernel): Z (m x out_dim, host).  RFF stage = K2; TensorSketch = count
+ * sketches + radix-2 transforms in shared memory (bitwise the reference algorithm's
+ * operations); SRHT = pad / sign / Walsh-Hadamard / sample (bitwise); Gaussian stage = DGEMM. */
+int krr_chain_apply(krr_ctx* ctx, const krr_chain_tables* tables, const double* Xq, int64_t m, double* Z);
+/* The same for the context's own data, kept on the device as the sketch Z (row-sharded),
+ * ready for krr_precond_build / krr_quality_test (generalises krr_rff_build). */
+int krr_chain_build(krr_ctx* ctx, const krr_chain_tables* tables);
+/* realize_chain (sketches.cpp:213-242) + krr_chain_build: draws every stage on the host from
+ * master_seed and builds Z on the device. */
+int krr_chain_build_seeded(krr_ctx* ctx, const krr_chain_spec* spec, uint64_t master_seed);
+/* ChainSpec::scaled_to (sketches.cpp:173-192). */
+int krr_chain_scaled_to(const krr_chain_spec* spec, int64_t target, krr_chain_spec* out);
+/* train (solver.cpp:96-133) for any kernel family and chain: set data, realize + build the
+ * chain, Woodbury build (lambda_p <= 0 -> lambda), device PCG; arguments otherwise as krr_train. */
+int krr_train_ex(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const double* Y, int64_t t,
+                 const krr_kernel_spec* kernel, const krr_chain_spec* chain, double lambda, double lambda_p,
+                 uint64_t master_seed, double tau, int max_iter, double* C, krr_rhs_stats* stats,
+                 double* residual_history, int64_t* total_matvecs, double* phase_ms);
+/* adaptive_build (precond.cpp:107-138) for any chain template (scaled_to(s) per attempt). */
+int krr_adaptive_build_ex(krr_ctx* ctx, const krr_chain_spec* chain_template, double lambda, double lambda_p,
+                          int64_t s0, int64_t s_max, uint64_t master_seed, krr_quality_report* history,
+                          int max_history, int* n_history, int64_t* final_size, int* passed, int* jitter_used);
+/* train_random_features_baseline (solver.cpp:175-193) / baseline_predict_scores (:195-197)
+ * for any realized chain. */
+int krr_rf_baseline_train_ex(krr_ctx* ctx, const krr_chain_tables* tables, const double* Y, int64_t t,
+                             double lambda, double* w_out);
+int krr_rf_baseline_predict_ex(krr_ctx* ctx, const krr_chain_tables* tables, const double* Xq, int64_t m,
+                               const double* w, int64_t t, double* out);
+/* KRRM model file with the kernel spec (io.cpp:73-89 kernel_to_json / kernel_from_json). */
+int krr_model_save_ex(const char* path, const krr_kernel_spec* kernel, double lambda, uint64_t seed,
+                      const double* label_map, int64_t nlabels, const double* X, int64_t n, int64_t d,
+                      const double* C, int64_t t);
+int krr_model_kernel(const char* path, krr_kernel_spec* kernel);
+
 /* ---------------------------------------------------------------- preconditioner */
 /* build_preconditioner (precond.cpp:20-40): G = Z^T Z + lambda_p I; Cholesky;
  * on failure retry ONCE with 1e-12 trace(G)/s added to the diagonal, then

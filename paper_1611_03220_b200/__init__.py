@@ -46,7 +46,8 @@ from ._lib import (  # noqa: F401  (re-exported exception types)
 )
 
 __all__ = [
-    "KernelSpec", "Dataset", "RffMap", "ChainSpec", "SketchChain", "realize_chain",
+    "KernelSpec", "Dataset", "RffMap", "TensorSketchMap", "SrhtMap", "GaussianMap", "ChainSpec", "SketchChain",
+    "realize_chain", "KernelOperator",
     "Preconditioner", "build_preconditioner", "GaussianOperator", "SolverConfig", "RhsStats",
     "PcgReport", "PcgResult", "KrrModel", "TrainResult", "pcg_solve", "solve_regularized",
     "train", "predict_scores", "predict_labels", "rlsc_encode", "rlsc_decode",
@@ -62,10 +63,14 @@ K_STAGE_SEED_STRIDE = 0x9E3779B97F4A7C15  # sketches.hpp:14
 # ----------------------------------------------------------------------------- kernels.hpp
 @dataclass
 class KernelSpec:
-    """Gaussian kernel k(x,z) = exp(-|x-z|^2 / 2 sigma^2) (kernels.hpp:15-27)."""
+    """KernelSpec (kernels.hpp:15-27): the Gaussian kernel exp(-|x-z|^2 / 2 sigma^2) or the
+    polynomial kernel (gamma x.z + offset)^degree."""
 
     family: str = "gaussian"
     sigma: float = 1.0
+    gamma: float = 1.0
+    offset: float = 0.0
+    degree: int = 2
 
     @staticmethod
     def gaussian(sigma: float) -> "KernelSpec":
@@ -73,11 +78,34 @@ class KernelSpec:
         spec.validate()
         return spec
 
-    def validate(self) -> None:
-        if self.family != "gaussian":
-            raise InvalidArgument("only the Gaussian kernel is on the B200 hot path")
-        if not (self.sigma > 0.0):  # kernels.cpp:37-38
-            raise InvalidArgument("KernelSpec: sigma must be positive")
+    @staticmethod
+    def polynomial(gamma: float, offset: float, degree: int) -> "KernelSpec":
+        spec = KernelSpec("polynomial", 1.0, float(gamma), float(offset), int(degree))
+        spec.validate()
+        return spec
+
+    def validate(self) -> None:  # kernels.cpp:36-44
+        if self.family == "gaussian":
+            if not (self.sigma > 0.0):
+                raise InvalidArgument("KernelSpec: sigma must be positive")
+        elif self.family == "polynomial":
+            if self.degree < 1:
+                raise InvalidArgument("KernelSpec: degree must be at least 1")
+            if self.offset < 0.0:
+                raise InvalidArgument("KernelSpec: offset must be non-negative")
+            if not (self.gamma > 0.0):
+                raise InvalidArgument("KernelSpec: gamma must be positive")
+        else:
+            raise InvalidArgument(f"KernelSpec: unknown kernel family '{self.family}'")
+
+    def _c(self) -> "_lib.KernelSpecC":
+        return _lib.KernelSpecC(0 if self.family == "gaussian" else 1, int(self.degree), float(self.sigma),
+                                float(self.gamma), float(self.offset))
+
+
+def _set_data(ctx: Context, x: np.ndarray, kernel: KernelSpec) -> None:
+    kc = kernel._c()
+    _lib.check(_lib.LIB.krr_set_data_kernel(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], C.byref(kc)))
 
 
 @dataclass
@@ -155,33 +183,119 @@ class RffMap:
         return self.apply_rows(x[None, :])[0]
 
 
+class TensorSketchMap:
+    """TensorSketchMap (sketches.hpp:45-62): per mode a hash table (buckets in [0, s)) and a
+    +-1 sign table, drawn on the host with the reference's libstdc++ distributions in its
+    order (sketches.cpp:51-69).  Tables are public and may be overwritten, as in the
+    reference's tests; the device applies them through SketchChain.apply_rows."""
+
+    def __init__(self, input_dim: int, features: int, degree: int, seed: int):
+        if features < 1:
+            raise InvalidArgument("TensorSketchMap: need at least one feature")
+        if degree < 1:
+            raise InvalidArgument("TensorSketchMap: degree must be >= 1")
+        self.in_dim, self.out_dim, self.degree, self.seed = int(input_dim), int(features), int(degree), int(seed)
+        self.hash = np.empty((degree, input_dim), dtype=np.uint32)
+        self.sign = np.empty((degree, input_dim))
+        _lib.check(_lib.LIB.krr_tensorsketch_realize(int(seed) % (1 << 64), input_dim, features, degree,
+                                                     _lib.ptr(self.hash), _lib.ptr(self.sign)))
+
+
+class SrhtMap:
+    """SrhtMap (sketches.hpp:64-79): sign (next_pow2(in) entries) then sampled rows, drawn
+    as sketches.cpp:95-109 does."""
+
+    def __init__(self, input_dim: int, features: int, seed: int):
+        if features < 1:
+            raise InvalidArgument("SrhtMap: need at least one feature")
+        if input_dim < 1:
+            raise InvalidArgument("SrhtMap: input dimension must be positive")
+        self.in_dim, self.out_dim, self.seed = int(input_dim), int(features), int(seed)
+        self.padded_dim = 1 << max(0, (int(input_dim) - 1).bit_length())
+        self.sign = np.empty(self.padded_dim)
+        self.rows = np.empty(features, dtype=np.int64)
+        _lib.check(_lib.LIB.krr_srht_realize(int(seed) % (1 << 64), input_dim, features, _lib.ptr(self.sign),
+                                             _lib.ptr(self.rows)))
+
+    def dense(self) -> np.ndarray:
+        """SrhtMap::dense (sketches.cpp:123-135)."""
+        i = self.rows[:, None].astype(np.uint64)
+        j = np.arange(self.in_dim, dtype=np.uint64)[None, :]
+        bits = np.unpackbits((i & j).view(np.uint8).reshape(len(self.rows), self.in_dim, 8), axis=2).sum(axis=2)
+        return np.where(bits & 1, -1.0, 1.0) * self.sign[None, :self.in_dim] / math.sqrt(self.out_dim)
+
+
+class GaussianMap:
+    """GaussianMap (sketches.hpp:81-92): proj (s x in) standard normals (sketches.cpp:128-135)."""
+
+    def __init__(self, input_dim: int, features: int, seed: int):
+        if features < 1:
+            raise InvalidArgument("GaussianMap: need at least one feature")
+        self.seed = int(seed)
+        self.proj = np.empty((features, input_dim))
+        _lib.check(_lib.LIB.krr_gaussmap_realize(int(seed) % (1 << 64), input_dim, features, _lib.ptr(self.proj)))
+
+    def dense(self) -> np.ndarray:
+        return self.proj / math.sqrt(self.proj.shape[0])
+
+
+_FIRST = {"RandomFourier": 0, "TensorSketch": 1}
+
+
 @dataclass
 class ChainSpec:
-    """sketches.hpp:96-107.  The B200 path implements the RFF-only chain (s2 = s3 = 0)."""
+    """ChainSpec (sketches.hpp:96-107): first stage RandomFourier (Gaussian kernel) or
+    TensorSketch (polynomial kernel), optional SRHT (s2) and Gaussian (s3) stages."""
 
     first: str = "RandomFourier"
     s1: int = 0
     s2: int = 0
     s3: int = 0
 
-    def validate(self) -> None:
+    def validate(self) -> None:  # sketches.cpp:155-165
+        if self.first not in _FIRST:
+            raise InvalidArgument(f"ChainSpec: unknown first stage '{self.first}'")
         if self.s1 < 1:
             raise InvalidArgument("ChainSpec: s1 must be at least 1")
         if self.s2 < 0 or self.s3 < 0:
             raise InvalidArgument("ChainSpec: stage sizes must be non-negative")
-        if self.s2 or self.s3 or self.first != "RandomFourier":
-            raise InvalidArgument("ChainSpec: only the RandomFourier single-stage chain is on the hot path")
+        prev = self.s1
+        if self.s2 > 0:
+            if self.s2 > prev:
+                raise InvalidArgument("ChainSpec: stage sizes must be non-increasing")
+            prev = self.s2
+        if self.s3 > 0 and self.s3 > prev:
+            raise InvalidArgument("ChainSpec: stage sizes must be non-increasing")
 
     def output_dim(self) -> int:
         return self.s3 or self.s2 or self.s1
 
+    def scaled_to(self, target: int) -> "ChainSpec":
+        """sketches.cpp:173-192."""
+        out = _lib.ChainSpecC()
+        _lib.check(_lib.LIB.krr_chain_scaled_to(C.byref(self._c()), int(target), C.byref(out)))
+        return ChainSpec(self.first, int(out.s1), int(out.s2), int(out.s3))
+
+    def _c(self) -> "_lib.ChainSpecC":
+        if self.first not in _FIRST:
+            raise InvalidArgument(f"ChainSpec: unknown first stage '{self.first}'")
+        return _lib.ChainSpecC(_FIRST[self.first], 0, int(self.s1), int(self.s2), int(self.s3))
+
+    def rff_only(self) -> bool:
+        return self.first == "RandomFourier" and self.s2 == 0 and self.s3 == 0
+
 
 @dataclass
 class SketchChain:
+    """SketchChain (sketches.hpp:109-127): the realized stages; apply_rows runs on the device."""
+
     kernel: KernelSpec
     in_dim: int
     out_dim: int
-    rff: RffMap
+    rff: Optional[RffMap] = None
+    tensor: Optional[TensorSketchMap] = None
+    srht: Optional[SrhtMap] = None
+    gauss: Optional[GaussianMap] = None
 
     def input_dim(self) -> int:
         return self.in_dim
@@ -189,19 +303,77 @@ class SketchChain:
     def output_dim(self) -> int:
         return self.out_dim
 
-    def apply_rows(self, x: np.ndarray) -> np.ndarray:
-        return self.rff.apply_rows(x)
+    def _tables(self):
+        """krr_chain_tables view (the arrays stay referenced by self while the call runs)."""
+        t = _lib.ChainTablesC()
+        if self.rff is not None:
+            t.first, t.in_dim, t.s1 = 0, self.rff.w.shape[1], self.rff.w.shape[0]
+            t.rff_w, t.rff_b = _lib.ptr(self.rff.w), _lib.ptr(self.rff.b)
+        else:
+            ts = self.tensor
+            ts.hash = np.ascontiguousarray(ts.hash, dtype=np.uint32)
+            ts.sign = _lib.f64(ts.sign)
+            t.first, t.degree, t.in_dim, t.s1 = 1, ts.degree, ts.in_dim, ts.out_dim
+            t.ts_hash, t.ts_sign = _lib.ptr(ts.hash), _lib.ptr(ts.sign)
+        if self.srht is not None:
+            self.srht.sign = _lib.f64(self.srht.sign)
+            self.srht.rows = np.ascontiguousarray(self.srht.rows, dtype=np.int64)
+            t.s2, t.srht_sign, t.srht_rows = len(self.srht.rows), _lib.ptr(self.srht.sign), _lib.ptr(self.srht.rows)
+        if self.gauss is not None:
+            self.gauss.proj = _lib.f64(self.gauss.proj)
+            t.s3, t.gauss_proj = self.gauss.proj.shape[0], _lib.ptr(self.gauss.proj)
+        return t
+
+    def apply_rows(self, x: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
+        """SketchChain::apply_rows (sketches.cpp:207-211) on the device."""
+        x = _lib.f64(x)
+        if x.ndim != 2 or x.shape[1] != self.in_dim:
+            raise DimensionMismatch("SketchChain: input dimension mismatch")
+        if x.shape[0] == 0:
+            return np.zeros((0, self.out_dim))
+        own = ctx is None
+        ctx = ctx or Context()
+        try:
+            _set_data(ctx, x, self.kernel)
+            z = np.empty((x.shape[0], self.out_dim))
+            t = self._tables()
+            _lib.check(_lib.LIB.krr_chain_apply(ctx.handle, C.byref(t), _lib.ptr(x), x.shape[0], _lib.ptr(z)))
+            return z
+        finally:
+            if own:
+                ctx.close()
 
     def apply(self, x: np.ndarray) -> np.ndarray:
-        return self.rff.apply(x)
+        x = _lib.f64(x)
+        if x.ndim != 1 or x.shape[0] != self.in_dim:
+            raise DimensionMismatch("SketchChain: input dimension mismatch")
+        return self.apply_rows(x[None, :])[0]
+
+
+def _stage_seed(master: int, stage: int) -> int:
+    return (int(master) + (stage + 1) * K_STAGE_SEED_STRIDE) % (1 << 64)
 
 
 def realize_chain(spec: ChainSpec, kernel: KernelSpec, input_dim: int, master_seed: int) -> SketchChain:
-    """sketches.cpp:213-242 (RFF stage 0 seeded with stage_seed(master, 0))."""
+    """realize_chain (sketches.cpp:213-242): stage k drawn with stage_seed(master, k)."""
     spec.validate()
     kernel.validate()
-    seed = (int(master_seed) + K_STAGE_SEED_STRIDE) % (1 << 64)
-    return SketchChain(kernel, input_dim, spec.s1, RffMap(input_dim, spec.s1, kernel.sigma, seed))
+    if spec.first == "RandomFourier" and kernel.family != "gaussian":
+        raise InvalidArgument("realize_chain: random Fourier features serve the Gaussian kernel")
+    if spec.first == "TensorSketch" and kernel.family != "polynomial":
+        raise InvalidArgument("realize_chain: TensorSketch serves the polynomial kernel")
+    chain = SketchChain(kernel, int(input_dim), spec.output_dim())
+    if spec.first == "RandomFourier":
+        chain.rff = RffMap(input_dim, spec.s1, kernel.sigma, _stage_seed(master_seed, 0))
+    else:
+        chain.tensor = TensorSketchMap(input_dim + 1, spec.s1, kernel.degree, _stage_seed(master_seed, 0))
+    prev = spec.s1
+    if spec.s2 > 0:
+        chain.srht = SrhtMap(prev, spec.s2, _stage_seed(master_seed, 1))
+        prev = spec.s2
+    if spec.s3 > 0:
+        chain.gauss = GaussianMap(prev, spec.s3, _stage_seed(master_seed, 2))
+    return chain
 
 
 # ----------------------------------------------------------------------------- precond.hpp
@@ -270,8 +442,9 @@ def build_preconditioner(z: np.ndarray, lambda_p: float, ctx: Optional[Context] 
 
 # ----------------------------------------------------------------------------- operator
 class GaussianOperator:
-    """v -> (K + lambda I) v for the Gaussian kernel with K never stored: the fused
-    sm_100a K1 kernel.  Callable like the reference's LinearOperator (solver.hpp:15)."""
+    """v -> (K + lambda I) v with K never stored: the fused sm_100a K1 kernel (Gaussian, or
+    the polynomial kernel of SURVEY 8f4 — see KernelOperator).  Callable like the
+    reference's LinearOperator (solver.hpp:15)."""
 
     def __init__(self, x: np.ndarray, kernel: KernelSpec, lambda_: float = 0.0,
                  ctx: Optional[Context] = None):
@@ -284,7 +457,7 @@ class GaussianOperator:
         self.n, self.d = x.shape
         self.lambda_ = float(lambda_)
         self.kernel = kernel
-        _lib.check(_lib.LIB.krr_set_data(self.ctx.handle, _lib.ptr(x), self.n, self.d, kernel.sigma))
+        _set_data(self.ctx, x, kernel)
 
     def matmat(self, v: np.ndarray) -> np.ndarray:
         v = _lib.f64(v)
@@ -304,6 +477,9 @@ class GaussianOperator:
     def close(self):
         if self._own:
             self.ctx.close()
+
+
+KernelOperator = GaussianOperator  # either kernel family
 
 
 # ----------------------------------------------------------------------------- solver.hpp
@@ -453,7 +629,7 @@ def solve_regularized(x: np.ndarray, kernel: KernelSpec, y: np.ndarray, lambda_:
     ctx = ctx or Context()
     try:
         n, t = y2.shape
-        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, x.shape[1], kernel.sigma))
+        _set_data(ctx, x, kernel)
         c = np.empty((n, t))
         st = (_lib.RhsStatsC * t)()
         hist = np.zeros((t, max(1, int(max_iter))))
@@ -472,7 +648,8 @@ def solve_regularized(x: np.ndarray, kernel: KernelSpec, y: np.ndarray, lambda_:
 
 
 def train(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Context] = None) -> TrainResult:
-    """solver.cpp:96-133 (non-adaptive RFF chain) — the whole hot path on the device."""
+    """solver.cpp:96-133 — the whole hot path on the device (RFF chain for the Gaussian kernel,
+    TensorSketch chains for the polynomial kernel, optional SRHT / Gaussian stages)."""
     if data.n() < 1:
         raise InvalidArgument("train: dataset is empty")
     if not (cfg.lambda_ > 0.0):
@@ -486,7 +663,7 @@ def train(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Co
     y2 = y[:, None] if y.ndim == 1 else y
     n, d = x.shape
     t = y2.shape[1]
-    s = cfg.chain.s1
+    s = cfg.chain.output_dim()
     c = np.empty((n, t))
     st = (_lib.RhsStatsC * t)()
     hist = np.zeros((t, max(1, int(cfg.max_iter))))
@@ -497,16 +674,23 @@ def train(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Co
     ctx = ctx or Context()
     try:
         t0 = time.perf_counter()
-        _lib.check(_lib.LIB.krr_train(ctx.handle, _lib.ptr(x), n, d, _lib.ptr(_lib.f64(y2)), t,
-                                      kernel.sigma, float(cfg.lambda_), float(lp), s, int(cfg.seed),
-                                      float(cfg.tau), int(cfg.max_iter), _lib.ptr(c), st,
-                                      _lib.ptr(hist), C.byref(tot), _lib.ptr(phase)))
+        if kernel.family == "gaussian" and cfg.chain.rff_only():
+            _lib.check(_lib.LIB.krr_train(ctx.handle, _lib.ptr(x), n, d, _lib.ptr(_lib.f64(y2)), t,
+                                          kernel.sigma, float(cfg.lambda_), float(lp), s, int(cfg.seed),
+                                          float(cfg.tau), int(cfg.max_iter), _lib.ptr(c), st,
+                                          _lib.ptr(hist), C.byref(tot), _lib.ptr(phase)))
+        else:  # any kernel family / sketch chain
+            kc, cc = kernel._c(), cfg.chain._c()
+            _lib.check(_lib.LIB.krr_train_ex(ctx.handle, _lib.ptr(x), n, d, _lib.ptr(_lib.f64(y2)), t,
+                                             C.byref(kc), C.byref(cc), float(cfg.lambda_), float(lp),
+                                             int(cfg.seed) % (1 << 64), float(cfg.tau), int(cfg.max_iter),
+                                             _lib.ptr(c), st, _lib.ptr(hist), C.byref(tot), _lib.ptr(phase)))
         wall = time.perf_counter() - t0
     finally:
         if own:
             ctx.close()
     report = PcgReport([_stats_from(st, hist, j) for j in range(t)], int(tot.value), wall,
-                       {"rff_build": phase[0], "precond_build": phase[1], "solve": phase[2],
+                       {"sketch_build": phase[0], "rff_build": phase[0], "precond_build": phase[1], "solve": phase[2],
                         "total": phase[3]})
     model = KrrModel(kernel, x.copy(), c, list(data.label_map), float(cfg.lambda_), int(cfg.seed))
     return TrainResult(model, report, s)
@@ -546,7 +730,7 @@ def predict_scores(model: KrrModel, xq: np.ndarray, ctx: Optional[Context] = Non
     ctx = ctx or Context()
     try:
         x = _lib.f64(model.x)
-        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], model.kernel.sigma))
+        _set_data(ctx, x, model.kernel)
         out = np.empty((xq.shape[0], c2.shape[1]))
         _lib.check(_lib.LIB.krr_predict_scores(ctx.handle, _lib.ptr(xq), xq.shape[0], _lib.ptr(c2),
                                                c2.shape[1], _lib.ptr(out)))
@@ -621,7 +805,7 @@ def quality_test(x: np.ndarray, kernel: KernelSpec, z: np.ndarray, lambda_: floa
     own = ctx is None
     ctx = ctx or Context()
     try:
-        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], kernel.sigma))
+        _set_data(ctx, x, kernel)
         _lib.check(_lib.LIB.krr_sketch_upload(ctx.handle, _lib.ptr(z), z.shape[0], z.shape[1]))
         r = _lib.QualityReportC()
         _lib.check(_lib.LIB.krr_quality_test(ctx.handle, float(lambda_), C.byref(r)))
@@ -657,10 +841,11 @@ def adaptive_build(x: np.ndarray, chain_template: ChainSpec, kernel: KernelSpec,
     hist = (_lib.QualityReportC * 64)()
     nh, fs, ok, jit = C.c_int(), C.c_int64(), C.c_int(), C.c_int()
     try:
-        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], kernel.sigma))
-        _lib.check(_lib.LIB.krr_adaptive_build(ctx.handle, float(lambda_), float(lambda_p), int(s0), int(s_max),
-                                               int(master_seed) % (1 << 64), hist, 64, C.byref(nh), C.byref(fs),
-                                               C.byref(ok), C.byref(jit)))
+        _set_data(ctx, x, kernel)
+        cc = chain_template._c()
+        _lib.check(_lib.LIB.krr_adaptive_build_ex(ctx.handle, C.byref(cc), float(lambda_), float(lambda_p), int(s0),
+                                                  int(s_max), int(master_seed) % (1 << 64), hist, 64, C.byref(nh),
+                                                  C.byref(fs), C.byref(ok), C.byref(jit)))
     except BaseException:
         if own:
             ctx.close()
@@ -677,13 +862,14 @@ def save_model(path, model: KrrModel) -> None:
     c = _lib.f64(model.c)
     c2 = c[:, None] if c.ndim == 1 else c
     lm = np.ascontiguousarray(model.label_map, dtype=np.float64)
-    _lib.check(_lib.LIB.krr_model_save(str(path).encode(), float(model.kernel.sigma), float(model.lambda_),
-                                       int(model.seed) % (1 << 64), _lib.ptr(lm) if lm.size else None, lm.size,
-                                       _lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(c2), c2.shape[1]))
+    kc = model.kernel._c()
+    _lib.check(_lib.LIB.krr_model_save_ex(str(path).encode(), C.byref(kc), float(model.lambda_),
+                                          int(model.seed) % (1 << 64), _lib.ptr(lm) if lm.size else None, lm.size,
+                                          _lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(c2), c2.shape[1]))
 
 
 def load_model(path) -> KrrModel:
-    """io.cpp:217-261 (same checks and messages; Gaussian models)."""
+    """io.cpp:217-261 (same checks and messages; Gaussian and polynomial models)."""
     n, d, t, nl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
     sigma, lam, seed = C.c_double(), C.c_double(), C.c_uint64()
     p = str(path).encode()
@@ -693,13 +879,17 @@ def load_model(path) -> KrrModel:
     x = np.empty((n.value, d.value))
     c = np.empty((n.value, t.value))
     _lib.check(_lib.LIB.krr_model_load(p, _lib.ptr(lm), _lib.ptr(x), _lib.ptr(c)))
-    return KrrModel(KernelSpec.gaussian(sigma.value), x, c, list(lm[:nl.value]), lam.value, int(seed.value))
+    kc = _lib.KernelSpecC()
+    _lib.check(_lib.LIB.krr_model_kernel(p, C.byref(kc)))
+    kernel = (KernelSpec.gaussian(kc.sigma) if kc.family == 0
+              else KernelSpec.polynomial(kc.gamma, kc.offset, int(kc.degree)))
+    return KrrModel(kernel, x, c, list(lm[:nl.value]), lam.value, int(seed.value))
 
 
 # ----------------------------------------------------------------------------- f1: RF baseline
 @dataclass
 class RandomFeaturesModel:
-    """solver.hpp RandomFeaturesModel: the realized RFF chain, weights w (s x t), lambda."""
+    """solver.hpp RandomFeaturesModel: the realized sketch chain, weights w (s x t), lambda."""
     chain: SketchChain
     w: np.ndarray
     lambda_: float
@@ -709,15 +899,11 @@ class RandomFeaturesModel:
         return len(self.label_map) > 0
 
 
-def _rff_stage(chain: SketchChain) -> "RffMap":
-    return chain.rff  # realize_chain enforces Gaussian <=> one RandomFourier stage (sketches.cpp:217-218)
-
-
 def train_random_features_baseline(data: Dataset, kernel: KernelSpec, chain: ChainSpec, lambda_: float,
                                    seed: int = 0, ctx: Optional[Context] = None) -> RandomFeaturesModel:
-    """Sketch-and-solve baseline of `krr bench` (solver.cpp:175-193): Z = RFF(X),
-    w = (Z^T Z + lambda I)^{-1} Z^T Y on the device (K2 features, cuBLAS SYRK/GEMM,
-    cuSOLVER potrf/potrs; no jitter)."""
+    """Sketch-and-solve baseline of `krr bench` (solver.cpp:175-193): Z = chain(X),
+    w = (Z^T Z + lambda I)^{-1} Z^T Y on the device (chain stages as SketchChain.apply_rows,
+    cuBLAS SYRK/GEMM, cuSOLVER potrf/potrs; no jitter)."""
     kernel.validate()
     if not (lambda_ > 0.0):
         raise NonPositiveLambda("baseline: lambda must be positive")
@@ -725,15 +911,15 @@ def train_random_features_baseline(data: Dataset, kernel: KernelSpec, chain: Cha
     y = _lib.f64(data.y)
     y2 = y[:, None] if y.ndim == 1 else y
     sk = realize_chain(chain, kernel, x.shape[1], seed)
-    st = _rff_stage(sk)
-    s, t = st.output_dim(), y2.shape[1]
+    s, t = sk.output_dim(), y2.shape[1]
     own = ctx is None
     ctx = ctx or Context()
     try:
-        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), x.shape[0], x.shape[1], kernel.sigma))
+        _set_data(ctx, x, kernel)
         w = np.empty((s, t))
-        _lib.check(_lib.LIB.krr_rf_baseline_train(ctx.handle, _lib.ptr(st.w), _lib.ptr(st.b), s, _lib.ptr(y2), t,
-                                                  float(lambda_), _lib.ptr(w)))
+        tab = sk._tables()
+        _lib.check(_lib.LIB.krr_rf_baseline_train_ex(ctx.handle, C.byref(tab), _lib.ptr(y2), t, float(lambda_),
+                                                     _lib.ptr(w)))
     finally:
         if own:
             ctx.close()
@@ -741,21 +927,20 @@ def train_random_features_baseline(data: Dataset, kernel: KernelSpec, chain: Cha
 
 
 def baseline_predict_scores(model: RandomFeaturesModel, xq: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
-    """solver.cpp:195-197: RFF(Xq) w."""
+    """solver.cpp:195-197: chain(Xq) w."""
     xq = _lib.f64(xq)
-    st = _rff_stage(model.chain)
-    if xq.ndim != 2 or xq.shape[1] != st.input_dim():
+    if xq.ndim != 2 or xq.shape[1] != model.chain.input_dim():
         raise DimensionMismatch("baseline predict: query dimension mismatch")
     s, t = model.w.shape
     own = ctx is None
     ctx = ctx or Context()
     try:
-        # the context needs a data set for d / the operand layout: the queries themselves
-        _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(xq), xq.shape[0], xq.shape[1], st.sigma))
+        # the context needs a data set for d / the kernel: the queries themselves
+        _set_data(ctx, xq, model.chain.kernel)
         out = np.empty((xq.shape[0], t))
-        _lib.check(_lib.LIB.krr_rf_baseline_predict(ctx.handle, _lib.ptr(xq), xq.shape[0], _lib.ptr(st.w),
-                                                    _lib.ptr(st.b), s, _lib.ptr(_lib.f64(model.w)), t,
-                                                    _lib.ptr(out)))
+        tab = model.chain._tables()
+        _lib.check(_lib.LIB.krr_rf_baseline_predict_ex(ctx.handle, C.byref(tab), _lib.ptr(xq), xq.shape[0],
+                                                       _lib.ptr(_lib.f64(model.w)), t, _lib.ptr(out)))
     finally:
         if own:
             ctx.close()

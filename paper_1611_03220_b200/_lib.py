@@ -106,6 +106,23 @@ class RhsStatsC(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("final_residual", C.c_double)]
 
 
+class KernelSpecC(C.Structure):
+    _fields_ = [("family", C.c_int32), ("degree", C.c_int32), ("sigma", C.c_double), ("gamma", C.c_double),
+                ("offset", C.c_double)]
+
+
+class ChainSpecC(C.Structure):
+    _fields_ = [("first", C.c_int32), ("pad_", C.c_int32), ("s1", C.c_int64), ("s2", C.c_int64),
+                ("s3", C.c_int64)]
+
+
+class ChainTablesC(C.Structure):
+    _fields_ = [("first", C.c_int32), ("degree", C.c_int32), ("in_dim", C.c_int64), ("s1", C.c_int64),
+                ("s2", C.c_int64), ("s3", C.c_int64), ("rff_w", C.c_void_p), ("rff_b", C.c_void_p),
+                ("ts_hash", C.c_void_p), ("ts_sign", C.c_void_p), ("srht_sign", C.c_void_p),
+                ("srht_rows", C.c_void_p), ("gauss_proj", C.c_void_p)]
+
+
 OPERATOR_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
 OBSERVER_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_int64)
 
@@ -164,6 +181,24 @@ _SIGS = {
     "krr_debug_i8_mma_rate": [_vp, _i, _i, _i, _i, C.POINTER(_d)],
     "krr_debug_tmem_ld_rate": [_vp, _i, _i, C.POINTER(_d)],
     "krr_debug_i8_trace": [_vp, _vp, _i],
+    # SURVEY 8f4
+    "krr_set_data_kernel": [_vp, _vp, _i64, _i64, C.POINTER(KernelSpecC)],
+    "krr_tensorsketch_realize": [C.c_uint64, _i64, _i64, _i, _vp, _vp],
+    "krr_srht_realize": [C.c_uint64, _i64, _i64, _vp, _vp],
+    "krr_gaussmap_realize": [C.c_uint64, _i64, _i64, _vp],
+    "krr_chain_apply": [_vp, C.POINTER(ChainTablesC), _vp, _i64, _vp],
+    "krr_chain_build": [_vp, C.POINTER(ChainTablesC)],
+    "krr_chain_build_seeded": [_vp, C.POINTER(ChainSpecC), C.c_uint64],
+    "krr_chain_scaled_to": [C.POINTER(ChainSpecC), _i64, C.POINTER(ChainSpecC)],
+    "krr_train_ex": [_vp, _vp, _i64, _i64, _vp, _i64, C.POINTER(KernelSpecC), C.POINTER(ChainSpecC), _d, _d,
+                     C.c_uint64, _d, _i, _vp, _vp, _vp, C.POINTER(_i64), _vp],
+    "krr_adaptive_build_ex": [_vp, C.POINTER(ChainSpecC), _d, _d, _i64, _i64, C.c_uint64, _vp, _i, C.POINTER(_i),
+                              C.POINTER(_i64), C.POINTER(_i), C.POINTER(_i)],
+    "krr_rf_baseline_train_ex": [_vp, C.POINTER(ChainTablesC), _vp, _i64, _d, _vp],
+    "krr_rf_baseline_predict_ex": [_vp, C.POINTER(ChainTablesC), _vp, _i64, _vp, _i64, _vp],
+    "krr_model_save_ex": [C.c_char_p, C.POINTER(KernelSpecC), _d, C.c_uint64, _vp, _i64, _vp, _i64, _i64, _vp,
+                          _i64],
+    "krr_model_kernel": [C.c_char_p, C.POINTER(KernelSpecC)],
 }
 
 

@@ -30,7 +30,13 @@ ExpConsts make_exp_consts(double scale) {
     int64_t bits;
     std::memcpy(&bits, &d2max, sizeof(bits));
     c.hi_under = int(bits >> 32);
-    c.pad_ = 0;
+    c.degree = 0;
+    return c;
+}
+
+ExpConsts make_poly_consts(int degree) {
+    ExpConsts c{};
+    c.degree = degree;
     return c;
 }
 

@@ -26,11 +26,13 @@ struct ExpConsts {
     double neg_scale; // -scale (mode 0)
     double a1, a2, a3, a4, a5;  // (ln2/64)^m / m!
     int hi_under;     // d2 high word above this -> result 0
-    int pad_;
+    int degree;       // mode 2 (polynomial kernel): the exponent q
 };
 
 // Host-side construction (long double for the constants).
 ExpConsts make_exp_consts(double scale);
+// Mode 2 (polynomial kernel): only `degree` is used.
+ExpConsts make_poly_consts(int degree);
 // Host-side table 2^(j/64), j = 0..63, correctly rounded to double.
 void make_exp_table(double* tab64);
 
@@ -59,13 +61,25 @@ __device__ __forceinline__ double gauss_exp_table(double d2, const ExpConsts& c,
     return hi > c.hi_under ? 0.0 : r;
 }
 
+// Polynomial kernel entry ipow(p, q) (kernels.cpp:10-14: r = p, then q-1 times r *= p),
+// p = gamma x_i.x_j + c arriving from the same tensor-core contraction as d2 (the operands
+// are the augmented inputs [sqrt(gamma) x, sqrt(c)], kernels.cpp:56-62).
+__device__ __forceinline__ double poly_ipow(double p, const ExpConsts& c) {
+    double r = p;
+    for (int i = 1; i < c.degree; ++i) r = __dmul_rn(r, p);
+    return r;
+}
+
+// The K1 epilogue: MODE 0/1 Gaussian (libdevice / table exp), MODE 2 polynomial.
 template <int MODE>
 __device__ __forceinline__ double gauss_exp(double d2, const ExpConsts& c,
                                             const double* __restrict__ tab) {
     if constexpr (MODE == 0) {
         return gauss_exp_libdevice(d2, c);
-    } else {
+    } else if constexpr (MODE == 1) {
         return gauss_exp_table(d2, c, tab);
+    } else {
+        return poly_ipow(d2, c);
     }
 }
 

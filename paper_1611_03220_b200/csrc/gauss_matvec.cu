@@ -38,6 +38,8 @@
 //              datapath (split-warp microbenchmark: 37.0 TFLOP/s combined = DMMA
 //              alone), so the only way to fill the latency-bound exp epilogue's idle
 //              pipe cycles is another warp's DMMAs on the same SM sub-partition.
+#include <type_traits>
+
 #include "common.cuh"
 #include "gauss_exp.cuh"
 #include "kernels.cuh"
@@ -517,11 +519,12 @@ __global__ void __launch_bounds__(256, 1) gauss_matvec_grouped_kernel(const Matv
     for (int i = tid; i < A.st; i += 256) dst[i] = rowacc[i];
 }
 
-// out_i = sum_x part[x][i] (owned slots only) + (1 + lambda) v_i  (diag, rank 0)
+// out_i = sum_x part[x][i] (owned slots only) + (K_ii + lambda) v_i  (diag, rank 0);
+// K_ii = 1 for the Gaussian kernel (kernels.cpp:81), kdiag[i] for the polynomial kernel.
 __global__ void matvec_finish_kernel(const double* __restrict__ part, int ns_count, int64_t n_pad,
                                      int64_t n, int st, const uint8_t* __restrict__ owned,
                                      const double* __restrict__ v, double lambda, int add_diag,
-                                     double* __restrict__ out) {
+                                     const double* __restrict__ kdiag, double* __restrict__ out) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_pad;
          i += int64_t(gridDim.x) * blockDim.x) {
         if (i >= n) {
@@ -534,7 +537,7 @@ __global__ void matvec_finish_kernel(const double* __restrict__ part, int ns_cou
             if (!owned || owned[int64_t(x) * ns_count + y]) s += part[int64_t(x) * n_pad + i];
         if (add_diag) {
             const double vi = v[i];
-            s = (s + vi) + lambda * vi;
+            s = (s + (kdiag ? kdiag[i] * vi : vi)) + lambda * vi;
         }
         out[i] = s;
     }
@@ -607,13 +610,22 @@ void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part
     // The resident shape pays one pipeline drain per column tile: only worth it for
     // long I sweeps (super-tiles of >= 1024 rows).
     const bool res = p.resident && p.st >= 1024 && gauss_matvec_resident_ok(p.st, p.dp);
-    if (res && p.grouped && !p.warps16 && grouped_smem_bytes(p.st, p.dp) <= size_t(MAX_SMEM)) {
-        exp_mode == 0 ? launch_grouped<0>(a, p.num_tiles, stream) : launch_grouped<1>(a, p.num_tiles, stream);
-    } else if (exp_mode == 0) {
-        p.warps16 ? launch_ms<0, 4>(a, p.num_tiles, res, stream) : launch_ms<0, 8>(a, p.num_tiles, res, stream);
-    } else {
-        p.warps16 ? launch_ms<1, 4>(a, p.num_tiles, res, stream) : launch_ms<1, 8>(a, p.num_tiles, res, stream);
-    }
+    const bool grouped = res && p.grouped && !p.warps16 && grouped_smem_bytes(p.st, p.dp) <= size_t(MAX_SMEM);
+    auto dispatch = [&](auto mode) {
+        constexpr int M = decltype(mode)::value;
+        if (grouped)
+            launch_grouped<M>(a, p.num_tiles, stream);
+        else if (p.warps16)
+            launch_ms<M, 4>(a, p.num_tiles, res, stream);
+        else
+            launch_ms<M, 8>(a, p.num_tiles, res, stream);
+    };
+    if (exp_mode == 2)
+        dispatch(std::integral_constant<int, 2>{});
+    else if (exp_mode == 0)
+        dispatch(std::integral_constant<int, 0>{});
+    else
+        dispatch(std::integral_constant<int, 1>{});
     KRR_LAUNCH_CHECK();
 }
 
@@ -621,7 +633,7 @@ void matvec_finish_launch(const GaussMatvecPlan& p, const double* part, const do
                           double lambda, int add_diag, double* out, cudaStream_t stream) {
     const int64_t blocks = std::min<int64_t>((p.n_pad + 255) / 256, 148 * 8);
     matvec_finish_kernel<<<unsigned(blocks), 256, 0, stream>>>(part, p.ns, p.n_pad, p.n, p.st,
-                                                                p.owned, v, lambda, add_diag, out);
+                                                                p.owned, v, lambda, add_diag, p.kdiag, out);
     KRR_LAUNCH_CHECK();
 }
 

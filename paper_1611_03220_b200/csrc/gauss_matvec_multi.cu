@@ -48,7 +48,7 @@ struct MultiArgs {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <int T>
+template <int T, int MODE>
 __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) {
     constexpr int NTT = T / 8;  // n8 tiles of the RHS dimension
     extern __shared__ __align__(16) double smem[];
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
                 for (int ns = 0; ns < 4; ++ns)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        double x = gauss_exp<1>(acc[ms][ns][h], A.ec, tab);
+                        double x = gauss_exp<MODE>(acc[ms][ns][h], A.ec, tab);
                         if (dtile) x = (wn * 32 + ns * 8 + 2 * t4 + h > il) ? x : 0.0;
                         e[ns][h] = x;
                     }
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
 __global__ void matmat_finish_kernel(const double* __restrict__ part, int ns_count, int64_t n_pad, int64_t n,
                                      int st, int T, const uint8_t* __restrict__ owned,
                                      const double* __restrict__ v, double lambda, int add_diag,
-                                     double* __restrict__ out) {
+                                     const double* __restrict__ kdiag, double* __restrict__ out) {
     const int64_t total = n_pad * T;
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
          k += int64_t(gridDim.x) * blockDim.x) {
@@ -269,7 +269,7 @@ __global__ void matmat_finish_kernel(const double* __restrict__ part, int ns_cou
             if (!owned || owned[int64_t(x) * ns_count + y]) s += part[int64_t(x) * n_pad * T + k];
         if (add_diag) {
             const double vi = v[k];
-            s = (s + vi) + lambda * vi;
+            s = (s + (kdiag ? kdiag[i] * vi : vi)) + lambda * vi;
         }
         out[k] = s;
     }
@@ -280,17 +280,17 @@ size_t matmat_smem(int) {
     return sizeof(double) * (size_t(NSTAGE) * STAGE_DOUBLES + 2 * BM * T + 4 * BM * T + 64);
 }
 
-template <int T>
+template <int T, int MODE>
 void launch_matmat(const MultiArgs& a, int64_t ntiles, cudaStream_t stream) {
     const size_t smem = matmat_smem<T>(a.st);
-    KRR_CUDA(cudaFuncSetAttribute(gauss_matmat_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KRR_CUDA(cudaFuncSetAttribute(gauss_matmat_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
-    gauss_matmat_kernel<T><<<unsigned(ntiles), NT, smem, stream>>>(a);
+    gauss_matmat_kernel<T, MODE><<<unsigned(ntiles), NT, smem, stream>>>(a);
 }
 
 }  // namespace
 
-void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, double* part,
+void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, double* part, int mode,
                          cudaStream_t stream) {
     if (p.num_tiles == 0) return;
     MultiArgs a;
@@ -305,9 +305,9 @@ void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, doubl
     a.st = p.st;
     a.ec = p.ec;
     if (T == 8) {
-        launch_matmat<8>(a, p.num_tiles, stream);
+        mode == 2 ? launch_matmat<8, 2>(a, p.num_tiles, stream) : launch_matmat<8, 1>(a, p.num_tiles, stream);
     } else if (T == 16) {
-        launch_matmat<16>(a, p.num_tiles, stream);
+        mode == 2 ? launch_matmat<16, 2>(a, p.num_tiles, stream) : launch_matmat<16, 1>(a, p.num_tiles, stream);
     } else {
         fail(KRR_ERR_INVALID_ARGUMENT, "gauss_matmat: T must be 8 or 16");
     }
@@ -318,7 +318,7 @@ void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const do
                           double lambda, int add_diag, double* out, cudaStream_t stream) {
     const int64_t blocks = std::min<int64_t>((p.n_pad * T + 255) / 256, 148 * 8);
     matmat_finish_kernel<<<unsigned(blocks), 256, 0, stream>>>(part, p.ns, p.n_pad, p.n, p.st, T, p.owned, v,
-                                                               lambda, add_diag, out);
+                                                               lambda, add_diag, p.kdiag, out);
     KRR_LAUNCH_CHECK();
 }
 

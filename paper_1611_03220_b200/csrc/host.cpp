@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <numbers>
 #include <random>
 #include <stdexcept>
@@ -111,6 +112,60 @@ void rff_realize(uint64_t master_seed, int64_t d, int64_t s, double sigma, doubl
     for (int64_t i = 0; i < s; ++i)
         for (int64_t j = 0; j < d; ++j) W[i * d + j] = freq(gen);
     for (int64_t i = 0; i < s; ++i) b[i] = phase(gen);
+}
+
+uint64_t stage_seed(uint64_t master, int stage) { return master + uint64_t(stage + 1) * kStageSeedStride; }
+
+int64_t next_pow2(int64_t m) {
+    int64_t p = 1;
+    while (p < m) p <<= 1;
+    return p;
+}
+
+void tensorsketch_realize(uint64_t seed, int64_t in_dim, int64_t s, int degree, uint32_t* hash, double* sign) {
+    if (s < 1) throw std::invalid_argument("TensorSketchMap: need at least one feature");
+    if (degree < 1) throw std::invalid_argument("TensorSketchMap: degree must be >= 1");
+    std::mt19937_64 gen(seed);
+    std::uniform_int_distribution<uint32_t> bucket(0, uint32_t(s - 1));
+    std::uniform_int_distribution<int> coin(0, 1);
+    for (int q = 0; q < degree; ++q) {
+        uint32_t* h = hash + int64_t(q) * in_dim;
+        double* g = sign + int64_t(q) * in_dim;
+        for (int64_t j = 0; j < in_dim; ++j) h[j] = bucket(gen);
+        for (int64_t j = 0; j < in_dim; ++j) g[j] = coin(gen) ? 1.0 : -1.0;
+    }
+}
+
+void srht_realize(uint64_t seed, int64_t in_dim, int64_t s, double* sign, int64_t* rows) {
+    if (s < 1) throw std::invalid_argument("SrhtMap: need at least one feature");
+    if (in_dim < 1) throw std::invalid_argument("SrhtMap: input dimension must be positive");
+    const int64_t P = next_pow2(in_dim);
+    std::mt19937_64 gen(seed);
+    std::uniform_int_distribution<int> coin(0, 1);
+    std::uniform_int_distribution<int64_t> pick(0, P - 1);
+    for (int64_t i = 0; i < P; ++i) sign[i] = coin(gen) ? 1.0 : -1.0;
+    for (int64_t i = 0; i < s; ++i) rows[i] = pick(gen);
+}
+
+void gaussmap_realize(uint64_t seed, int64_t in_dim, int64_t s, double* proj) {
+    if (s < 1) throw std::invalid_argument("GaussianMap: need at least one feature");
+    std::mt19937_64 gen(seed);
+    std::normal_distribution<double> normal(0.0, 1.0);
+    for (int64_t i = 0; i < s * in_dim; ++i) proj[i] = normal(gen);
+}
+
+void fft_twiddles(int64_t P, bool inverse, double* out) {
+    for (int64_t len = 2; len <= P; len <<= 1) {
+        const double ang = (inverse ? 2.0 : -2.0) * std::numbers::pi / double(len);
+        const std::complex<double> step = std::polar(1.0, ang);
+        std::complex<double> w(1.0, 0.0);
+        double* o = out + 2 * (len / 2 - 1);
+        for (int64_t j = 0; j < len / 2; ++j) {
+            o[2 * j] = w.real();
+            o[2 * j + 1] = w.imag();
+            w *= step;
+        }
+    }
 }
 
 void rlsc_encode(const int32_t* classes, int64_t n, int32_t num_classes, double* Y) {

@@ -24,6 +24,7 @@ struct GaussMatvecPlan {
     bool warps16 = false;            // 16 warps x (32 x 32) instead of 8 warps x (64 x 32)
     bool grouped = true;             // two phase-offset warp groups (resident shape only)
     ExpConsts ec{};
+    const double* kdiag = nullptr;   // polynomial kernel: K_ii per row (nullptr: K_ii = 1)
 };
 size_t gauss_matvec_smem_bytes(int st);
 bool gauss_matvec_resident_ok(int st, int dp);
@@ -34,7 +35,7 @@ void matvec_finish_launch(const GaussMatvecPlan& p, const double* part, const do
 
 // K1T: OUT = (K + lambda I) V for T in {8, 16} interleaved right-hand sides (n_pad x T),
 // part is NS x n_pad x T.
-void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, double* part,
+void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, double* part, int mode,
                          cudaStream_t stream);
 void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const double* v, int T,
                           double lambda, int add_diag, double* out, cudaStream_t stream);
@@ -70,6 +71,27 @@ void build_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad,
 void cross_matvec_launch(const double* Xq, int64_t m, const double* X, int64_t n, int64_t d,
                          const double* c, int64_t t, double scale, double* out,
                          cudaStream_t stream);
+
+// ---------------------------------------------------------------- SURVEY 8f4 (sketch.cu)
+// Polynomial-kernel operands L = R = [sqrt(gamma) x, sqrt(c), 0...] (rows >= n zero) and
+// kdiag_i = ipow(|xa_i|^2, degree) (nullable; R nullable).
+void poly_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, int dp, double sg, double so,
+                          int degree, double* L, double* R, double* kdiag, cudaStream_t stream);
+// predict_scores for the polynomial kernel: out (m x t) = K(Xq, X) C.
+void cross_poly_launch(const double* Xq, int64_t m, const double* X, int64_t n, int64_t d, const double* c,
+                       int64_t t, double sg, double so, int degree, double* out, cudaStream_t stream);
+// TensorSketch rows: A (m rows, stride lda, in_dim entries) -> Z (m x s).  P = s when s is a
+// power of two, else next_pow2(degree (s-1) + 1); tw_* from fft_twiddles(P).  scratch:
+// tensorsketch_scratch(P, m) double2 elements (0 -> nullptr allowed).
+size_t tensorsketch_scratch(int64_t P, int64_t m);
+void tensorsketch_launch(const uint32_t* hash, const double* sign, const double2* tw_fwd, const double2* tw_inv,
+                         int64_t in_dim, int64_t s, int64_t P, int degree, const double* A, int64_t lda, int64_t m,
+                         double* Z, double2* scratch, cudaStream_t stream);
+// SRHT rows: A (m x in_dim) -> Z (m x s); P = next_pow2(in_dim); scratch: srht_scratch(P, m) doubles.
+size_t srht_scratch(int64_t P, int64_t m);
+void srht_launch(const double* sign, const int64_t* rows, int64_t in_dim, int64_t P, int64_t s, double scale,
+                 const double* A, int64_t m, double* Z, double* scratch, cudaStream_t stream);
+void div_launch(double* z, int64_t count, double denom, cudaStream_t stream);
 
 // ---------------------------------------------------------------- vector algebra (K7)
 // All reductions are deterministic: `nb` fixed block partials then a fixed-order sum.

@@ -117,6 +117,11 @@ struct Ctx {
     bool has_data = false;
     int64_t n = 0, d = 0;
     double sigma = 1.0, scale = 0.5;
+    // kernel family: 0 Gaussian, 1 polynomial (gamma x.z + offset)^degree
+    int family = 0;
+    double gamma = 1.0, offset = 0.0;
+    int degree = 1;
+    DevMem<double> kdiag;
     Schedule sched;
     GaussMatvecPlan plan;
     DevMem<double> X, L, R, part, exp_tab;
@@ -176,13 +181,14 @@ void allreduce_sum(Ctx& c, double* buf, int64_t count) {
 // DMMA kernel on B200 (measured: d >= ~48, profiles/README.md) and the data's exponent range
 // allows it; the DMMA kernel otherwise.  Both are GPU kernels; neither is a fallback.
 bool use_i8(const Ctx& c) {
-    if (!c.i8_ready) return false;
+    if (!c.i8_ready || c.family != 0) return false;
     if (c.k1_path >= 0) return c.k1_path == 1;
     return c.d >= 48;
 }
 
 void f32_ensure(Ctx& c) {
     if (c.f32_ready) return;
+    if (c.family != 0) fail(KRR_ERR_INVALID_ARGUMENT, "fp32 precision mode serves the Gaussian kernel only");
     if (!f32_supported(c.d, int(c.sched.st)))
         fail(KRR_ERR_INVALID_ARGUMENT, "fp32 precision mode supports d <= 128 (got d = " + std::to_string(c.d) + ")");
     const int kb = f32_kb(c.d);
@@ -206,21 +212,45 @@ void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t
         gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.ejs8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
                                c.stream, c.i8_debug);
     else
-        gauss_matvec_launch(c.plan, v, c.part.get(), c.exp_mode, c.stream);
+        gauss_matvec_launch(c.plan, v, c.part.get(), c.family == 1 ? 2 : c.exp_mode, c.stream);
     if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
     matvec_finish_launch(c.plan, c.part.get(), v, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad);
 }
 
-void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
+// KernelSpec::validate (kernels.cpp:36-44).
+void validate_kernel(const krr_kernel_spec& k) {
+    if (k.family == 0) {
+        if (!(k.sigma > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: sigma must be positive");
+    } else if (k.family == 1) {
+        if (k.degree < 1) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: degree must be at least 1");
+        if (k.offset < 0.0) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: offset must be non-negative");
+        if (!(k.gamma > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: gamma must be positive");
+    } else {
+        fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: unknown kernel family");
+    }
+}
+
+krr_kernel_spec gaussian_spec(double sigma) {
+    krr_kernel_spec k{};
+    k.family = 0;
+    k.sigma = sigma;
+    return k;
+}
+
+void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_spec& ks) {
     if (n < 1 || d < 1) fail(KRR_ERR_INVALID_ARGUMENT, "krr_set_data: n and d must be positive");
-    if (!(sigma > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: sigma must be positive");
+    validate_kernel(ks);
     c.set_device();
     c.has_data = false;
     c.n = n;
     c.d = d;
-    c.sigma = sigma;
-    c.scale = 1.0 / (2.0 * sigma * sigma);  // kernels.cpp:79
+    c.family = ks.family;
+    c.sigma = ks.family == 0 ? ks.sigma : 1.0;
+    c.scale = 1.0 / (2.0 * c.sigma * c.sigma);  // kernels.cpp:79
+    c.gamma = ks.gamma;
+    c.offset = ks.offset;
+    c.degree = ks.degree;
     c.sched = make_schedule(n, c.world, c.rank);
     const int dp = int(((d + 2) + 3) / 4 * 4);
     const int64_t n_pad = c.sched.n_pad;
@@ -229,7 +259,13 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
                              c.stream));
     c.L.ensure(size_t(n_pad * dp));
     c.R.ensure(size_t(n_pad * dp));
-    build_operands_launch(c.X.get(), n, d, n_pad, dp, c.L.get(), c.R.get(), c.stream);
+    if (c.family == 0) {
+        build_operands_launch(c.X.get(), n, d, n_pad, dp, c.L.get(), c.R.get(), c.stream);
+    } else {
+        c.kdiag.ensure(size_t(n_pad));
+        poly_operands_launch(c.X.get(), n, d, n_pad, dp, std::sqrt(c.gamma), std::sqrt(c.offset), c.degree,
+                             c.L.get(), c.R.get(), c.kdiag.get(), c.stream);
+    }
     const int64_t ntiles = int64_t(c.sched.tiles.size() / 2);
     c.tiles.ensure(size_t(std::max<int64_t>(1, ntiles)));
     if (ntiles)
@@ -266,10 +302,11 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, double sigma) {
     p.dp = dp;
     p.st = int(c.sched.st);
     p.ns = int(c.sched.ns);
-    p.ec = make_exp_consts(c.scale);
+    p.ec = c.family == 0 ? make_exp_consts(c.scale) : make_poly_consts(c.degree);
+    p.kdiag = c.family == 1 ? c.kdiag.get() : nullptr;
     c.i8_ready = false;
     c.f32_ready = false;
-    if (i8_supported(d, int(c.sched.st))) {
+    if (c.family == 0 && i8_supported(d, int(c.sched.st))) {
         c.kp8 = i8_kp(d);
         c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
         c.ex8.ensure(size_t(n_pad));
@@ -297,6 +334,7 @@ void sketch_alloc(Ctx& c, int64_t n, int64_t s) {
 
 void rff_build(Ctx& c, const double* W, const double* b, int64_t s) {
     require_data(c);
+    if (c.family != 0) fail(KRR_ERR_INVALID_ARGUMENT, "realize_chain: random Fourier features serve the Gaussian kernel");
     if (s < 1) fail(KRR_ERR_INVALID_ARGUMENT, "ChainSpec: s1 must be at least 1");
     c.set_device();
     sketch_alloc(c, c.n, s);
@@ -534,7 +572,7 @@ void ensure_batched(Ctx& c, int T) {
 
 // out (n_pad x T) = (K + lambda I) v (n_pad x T), replicated on all ranks.
 void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
-    gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.stream);
+    gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.family == 1 ? 2 : 1, c.stream);
     matmat_finish_launch(c.plan, c.bpart.get(), v, T, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad * T);
 }
@@ -1077,7 +1115,7 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
 }
 
 int krr_set_data(krr_ctx* ctx, const double* X, int64_t n, int64_t d, double sigma) {
-    return guard([&] { krr::set_data(*krr::as_ctx(ctx), X, n, d, sigma); });
+    return guard([&] { krr::set_data(*krr::as_ctx(ctx), X, n, d, krr::gaussian_spec(sigma)); });
 }
 
 int krr_kernel_matvec_device(krr_ctx* ctx, double lambda, const double* dV, int64_t t,
@@ -1141,8 +1179,12 @@ int krr_predict_scores(krr_ctx* ctx, const double* Xq, int64_t m, const double* 
                                  c.stream));
         KRR_CUDA(cudaMemcpyAsync(cc.get(), C, sizeof(double) * size_t(c.n * t), cudaMemcpyHostToDevice,
                                  c.stream));
-        krr::cross_matvec_launch(q.get(), m, c.X.get(), c.n, c.d, cc.get(), t, c.scale, o.get(),
-                                 c.stream);
+        if (c.family == 1)
+            krr::cross_poly_launch(q.get(), m, c.X.get(), c.n, c.d, cc.get(), t, std::sqrt(c.gamma),
+                                   std::sqrt(c.offset), c.degree, o.get(), c.stream);
+        else
+            krr::cross_matvec_launch(q.get(), m, c.X.get(), c.n, c.d, cc.get(), t, c.scale, o.get(),
+                                     c.stream);
         KRR_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * size_t(m * t), cudaMemcpyDeviceToHost,
                                  c.stream));
         c.sync();
@@ -1178,20 +1220,16 @@ void rf_features_dev(Ctx& c, const double* Xdev, int64_t m, const double* W, con
 }  // namespace
 }  // namespace krr
 
-int krr_rf_baseline_train(krr_ctx* ctx, const double* W, const double* b, int64_t s, const double* Y, int64_t t,
-                          double lambda, double* w_out) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        krr::require_data(c);
-        if (!(lambda > 0.0)) krr::fail(KRR_ERR_NON_POSITIVE_LAMBDA, "baseline: lambda must be positive");
-        if (s < 1) krr::fail(KRR_ERR_INVALID_ARGUMENT, "ChainSpec: s1 must be at least 1");
-        if (t < 1) krr::fail(KRR_ERR_DIMENSION_MISMATCH, "baseline: Y needs at least one column");
-        if (c.world != 1) krr::fail(KRR_ERR_STATE, "the random-features baseline is single-rank");
-        c.set_device();
+namespace krr {
+namespace {
+// w = (Z^T Z + lambda I)^{-1} Z^T Y for a device Z (n x s row-major): the solve half of
+// train_random_features_baseline (solver.cpp:175-193).
+void rf_baseline_solve(Ctx& c, DevMem<double>& Z, int64_t s, const double* Y, int64_t t, double lambda,
+                       double* w_out) {
+    {
         const int64_t n = c.n;
-        krr::DevMem<double> Z, G, Yd, Rm, work;
+        krr::DevMem<double> G, Yd, Rm, work;
         krr::DevMem<int> info;
-        krr::rf_features_dev(c, c.X.get(), n, W, b, s, Z);
         // G = Z^T Z + lambda I (lower): Z row-major n x s == col-major Z^T (s x n)
         G.ensure(size_t(s * s));
         const double one = 1.0, zero = 0.0;
@@ -1237,6 +1275,25 @@ int krr_rf_baseline_train(krr_ctx* ctx, const double* W, const double* b, int64_
         c.sync();
         for (int64_t k = 0; k < s; ++k)
             for (int64_t j = 0; j < t; ++j) w_out[k * t + j] = wcm[size_t(j * s + k)];
+    }
+}
+}  // namespace
+}  // namespace krr
+
+int krr_rf_baseline_train(krr_ctx* ctx, const double* W, const double* b, int64_t s, const double* Y, int64_t t,
+                          double lambda, double* w_out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (!(lambda > 0.0)) krr::fail(KRR_ERR_NON_POSITIVE_LAMBDA, "baseline: lambda must be positive");
+        if (s < 1) krr::fail(KRR_ERR_INVALID_ARGUMENT, "ChainSpec: s1 must be at least 1");
+        if (t < 1) krr::fail(KRR_ERR_DIMENSION_MISMATCH, "baseline: Y needs at least one column");
+        if (c.world != 1) krr::fail(KRR_ERR_STATE, "the random-features baseline is single-rank");
+        if (c.family != 0) krr::fail(KRR_ERR_INVALID_ARGUMENT, "realize_chain: random Fourier features serve the Gaussian kernel");
+        c.set_device();
+        krr::DevMem<double> Z;
+        krr::rf_features_dev(c, c.X.get(), c.n, W, b, s, Z);
+        krr::rf_baseline_solve(c, Z, s, Y, t, lambda, w_out);
     });
 }
 
@@ -1415,7 +1472,7 @@ int krr_train(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const double*
         if (!(lambda > 0.0)) fail(KRR_ERR_NON_POSITIVE_LAMBDA, "train: lambda must be positive");
         if (s < 1) fail(KRR_ERR_INVALID_ARGUMENT, "ChainSpec: s1 must be at least 1");
         const double lp = lambda_p > 0.0 ? lambda_p : lambda;                           // solver.cpp:102
-        krr::set_data(c, X, n, d, sigma);
+        krr::set_data(c, X, n, d, krr::gaussian_spec(sigma));
         std::vector<double> W(static_cast<size_t>(s * d)), b(static_cast<size_t>(s));
         krr::rff_realize(master_seed, d, s, sigma, W.data(), b.data());
         cudaEvent_t ev[4];
@@ -1512,7 +1569,7 @@ int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0,
 
 int krr_model_save(const char* path, double sigma, double lambda, uint64_t seed, const double* label_map,
                    int64_t nlabels, const double* X, int64_t n, int64_t d, const double* C, int64_t t) {
-    return guard([&] { krr::model_save(path, sigma, lambda, seed, label_map, nlabels, X, n, d, C, t); });
+    return guard([&] { krr::model_save(path, 0, sigma, 0.0, 0.0, 0, lambda, seed, label_map, nlabels, X, n, d, C, t); });
 }
 
 int krr_model_info(const char* path, int64_t* n, int64_t* d, int64_t* t, int64_t* nlabels, double* sigma,
@@ -1689,6 +1746,422 @@ int krr_debug_tmem_ld_rate(krr_ctx* ctx, int warps, int reps, double* bytes_per_
         if (warps < 1 || warps > 32 || reps < 1) fail(KRR_ERR_INVALID_ARGUMENT, "warps in [1, 32], reps >= 1");
         c.set_device();
         *bytes_per_clk = krr::tmem_ld_rate(warps, reps, c.stream);
+    });
+}
+
+}  // extern "C"
+
+// ============================================================================= SURVEY 8f4
+// Kernel families and sketch chains: realize_chain (sketches.cpp:213-242) with the host's
+// libstdc++ draws, SketchChain::apply_rows (sketches.cpp:194-211) on the device.
+namespace krr {
+namespace {
+
+constexpr int kInvalid = KRR_ERR_INVALID_ARGUMENT;
+
+struct ChainOwned {
+    std::vector<double> w, b, ts_sign, srht_sign, proj;
+    std::vector<uint32_t> ts_hash;
+    std::vector<int64_t> srht_rows;
+    krr_chain_tables t{};
+};
+
+void validate_chain(const krr_chain_spec& sp) {  // ChainSpec::validate (sketches.cpp:155-165)
+    if (sp.first != 0 && sp.first != 1) fail(kInvalid, "ChainSpec: unknown first stage");
+    if (sp.s1 < 1) fail(kInvalid, "ChainSpec: s1 must be at least 1");
+    if (sp.s2 < 0 || sp.s3 < 0) fail(kInvalid, "ChainSpec: stage sizes must be non-negative");
+    int64_t prev = sp.s1;
+    if (sp.s2 > 0) {
+        if (sp.s2 > prev) fail(kInvalid, "ChainSpec: stage sizes must be non-increasing");
+        prev = sp.s2;
+    }
+    if (sp.s3 > 0 && sp.s3 > prev) fail(kInvalid, "ChainSpec: stage sizes must be non-increasing");
+}
+
+int64_t chain_out_dim(int64_t s1, int64_t s2, int64_t s3) { return s3 > 0 ? s3 : (s2 > 0 ? s2 : s1); }
+
+krr_chain_spec chain_scaled_to(const krr_chain_spec& sp, int64_t target) {  // sketches.cpp:173-192
+    validate_chain(sp);
+    if (target < 1) fail(kInvalid, "ChainSpec: target size must be at least 1");
+    const double factor = double(target) / double(chain_out_dim(sp.s1, sp.s2, sp.s3));
+    auto scale = [&](int64_t v) { return std::max<int64_t>(target, int64_t(std::ceil(double(v) * factor))); };
+    krr_chain_spec o = sp;
+    o.s1 = scale(sp.s1);
+    if (sp.s2 > 0) o.s2 = scale(sp.s2);
+    if (sp.s3 > 0) o.s3 = scale(sp.s3);
+    if (o.s3 > 0)
+        o.s3 = target;
+    else if (o.s2 > 0)
+        o.s2 = target;
+    else
+        o.s1 = target;
+    validate_chain(o);
+    return o;
+}
+
+void check_family(const Ctx& c, int first) {  // sketches.cpp:217-220
+    if (first == 0 && c.family != 0) fail(kInvalid, "realize_chain: random Fourier features serve the Gaussian kernel");
+    if (first == 1 && c.family != 1) fail(kInvalid, "realize_chain: TensorSketch serves the polynomial kernel");
+}
+
+void realize_chain_host(const Ctx& c, const krr_chain_spec& sp, uint64_t master, ChainOwned& o) {
+    validate_chain(sp);
+    check_family(c, sp.first);
+    krr_chain_tables& t = o.t;
+    t = krr_chain_tables{};
+    t.first = sp.first;
+    t.s1 = sp.s1;
+    t.s2 = sp.s2;
+    t.s3 = sp.s3;
+    if (sp.first == 0) {
+        t.in_dim = c.d;
+        o.w.resize(size_t(sp.s1 * c.d));
+        o.b.resize(size_t(sp.s1));
+        rff_realize(master, c.d, sp.s1, c.sigma, o.w.data(), o.b.data());  // stage_seed(master, 0) inside
+        t.rff_w = o.w.data();
+        t.rff_b = o.b.data();
+    } else {
+        t.in_dim = c.d + 1;  // augmented representation (sketches.cpp:229)
+        t.degree = c.degree;
+        o.ts_hash.resize(size_t(c.degree * t.in_dim));
+        o.ts_sign.resize(size_t(c.degree * t.in_dim));
+        tensorsketch_realize(stage_seed(master, 0), t.in_dim, sp.s1, c.degree, o.ts_hash.data(), o.ts_sign.data());
+        t.ts_hash = o.ts_hash.data();
+        t.ts_sign = o.ts_sign.data();
+    }
+    int64_t prev = sp.s1;
+    if (sp.s2 > 0) {
+        o.srht_sign.resize(size_t(next_pow2(prev)));
+        o.srht_rows.resize(size_t(sp.s2));
+        srht_realize(stage_seed(master, 1), prev, sp.s2, o.srht_sign.data(), o.srht_rows.data());
+        t.srht_sign = o.srht_sign.data();
+        t.srht_rows = o.srht_rows.data();
+        prev = sp.s2;
+    }
+    if (sp.s3 > 0) {
+        o.proj.resize(size_t(sp.s3 * prev));
+        gaussmap_realize(stage_seed(master, 2), prev, sp.s3, o.proj.data());
+        t.gauss_proj = o.proj.data();
+    }
+}
+
+void check_tables(const Ctx& c, const krr_chain_tables& t) {
+    validate_chain(krr_chain_spec{t.first, 0, t.s1, t.s2, t.s3});
+    check_family(c, t.first);
+    if (t.first == 0) {
+        if (t.in_dim != c.d) fail(KRR_ERR_DIMENSION_MISMATCH, "RffMap: input dimension mismatch");
+        if (!t.rff_w || !t.rff_b) fail(kInvalid, "chain tables: RFF tables missing");
+    } else {
+        if (t.in_dim != c.d + 1) fail(KRR_ERR_DIMENSION_MISMATCH, "TensorSketchMap: input dimension mismatch");
+        if (t.degree != c.degree) fail(kInvalid, "chain tables: TensorSketch degree differs from the kernel's");
+        if (!t.ts_hash || !t.ts_sign) fail(kInvalid, "chain tables: TensorSketch tables missing");
+        for (int64_t i = 0; i < int64_t(t.degree) * t.in_dim; ++i)
+            if (int64_t(t.ts_hash[i]) >= t.s1) fail(kInvalid, "TensorSketchMap: hash bucket out of range");
+    }
+    if (t.s2 > 0) {
+        if (!t.srht_sign || !t.srht_rows) fail(kInvalid, "chain tables: SRHT tables missing");
+        const int64_t P = next_pow2(t.s1);
+        for (int64_t i = 0; i < t.s2; ++i)
+            if (t.srht_rows[i] < 0 || t.srht_rows[i] >= P) fail(kInvalid, "SrhtMap: sampled row out of range");
+    }
+    if (t.s3 > 0 && !t.gauss_proj) fail(kInvalid, "chain tables: Gaussian projection missing");
+}
+
+template <typename T>
+void upload(DevMem<T>& dst, const T* src, size_t count, cudaStream_t st) {
+    dst.ensure(std::max<size_t>(1, count));
+    if (count) KRR_CUDA(cudaMemcpyAsync(dst.get(), src, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+}
+
+// Zout (m x out_dim, row-major) = SketchChain::apply_rows of the device rows Xrows (m x d).
+void chain_apply_dev(Ctx& c, const krr_chain_tables& t, const double* Xrows, int64_t m, DevMem<double>& Zout) {
+    check_tables(c, t);
+    const int64_t out = chain_out_dim(t.s1, t.s2, t.s3);
+    Zout.ensure(size_t(std::max<int64_t>(1, m * out)));
+    if (m == 0) return;
+    DevMem<double> z1, z2;
+    DevMem<double>& d1 = (t.s2 == 0 && t.s3 == 0) ? Zout : z1;
+    if (t.first == 0) {
+        rf_features_dev(c, Xrows, m, t.rff_w, t.rff_b, t.s1, d1);  // K2
+    } else {
+        const int dp = c.plan.dp;
+        DevMem<double> A;
+        A.ensure(size_t(m * dp));
+        poly_operands_launch(Xrows, m, c.d, m, dp, std::sqrt(c.gamma), std::sqrt(c.offset), c.degree, A.get(),
+                             nullptr, nullptr, c.stream);
+        DevMem<uint32_t> h;
+        DevMem<double> g;
+        upload(h, t.ts_hash, size_t(t.degree * t.in_dim), c.stream);
+        upload(g, t.ts_sign, size_t(t.degree * t.in_dim), c.stream);
+        const bool p2 = (t.s1 & (t.s1 - 1)) == 0;  // sketches.cpp:79-82
+        const int64_t P = p2 ? t.s1 : next_pow2(int64_t(t.degree) * (t.s1 - 1) + 1);
+        std::vector<double> tw(size_t(2 * std::max<int64_t>(1, P - 1)));
+        DevMem<double2> twf, twi, scr;
+        fft_twiddles(P, false, tw.data());
+        upload(twf, reinterpret_cast<const double2*>(tw.data()), size_t(P - 1), c.stream);
+        c.sync();  // tw is reused for the inverse table
+        fft_twiddles(P, true, tw.data());
+        upload(twi, reinterpret_cast<const double2*>(tw.data()), size_t(P - 1), c.stream);
+        const size_t ns = tensorsketch_scratch(P, m);
+        if (ns) scr.ensure(ns);
+        d1.ensure(size_t(m * t.s1));
+        tensorsketch_launch(h.get(), g.get(), twf.get(), twi.get(), t.in_dim, t.s1, P, t.degree, A.get(), dp, m,
+                            d1.get(), ns ? scr.get() : nullptr, c.stream);
+        c.sync();
+    }
+    DevMem<double>* cur = &d1;
+    int64_t prev = t.s1;
+    if (t.s2 > 0) {
+        DevMem<double>& d2 = t.s3 == 0 ? Zout : z2;
+        const int64_t P = next_pow2(prev);
+        DevMem<double> sg, scr;
+        DevMem<int64_t> rows;
+        upload(sg, t.srht_sign, size_t(P), c.stream);
+        upload(rows, t.srht_rows, size_t(t.s2), c.stream);
+        const size_t ns = srht_scratch(P, m);
+        if (ns) scr.ensure(ns);
+        d2.ensure(size_t(m * t.s2));
+        srht_launch(sg.get(), rows.get(), prev, P, t.s2, 1.0 / std::sqrt(double(t.s2)), cur->get(), m, d2.get(),
+                    ns ? scr.get() : nullptr, c.stream);
+        c.sync();
+        cur = &d2;
+        prev = t.s2;
+    }
+    if (t.s3 > 0) {
+        DevMem<double> pj;
+        upload(pj, t.gauss_proj, size_t(t.s3 * prev), c.stream);
+        const double one = 1.0, zero = 0.0;
+        cublas_check(cublasSetStream(c.blas, c.stream), "cublasSetStream");
+        // Z3^T (s3 x m, col-major) = proj (s3 x prev, row-major == col-major prev x s3, op T) . Z2^T
+        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, int(t.s3), int(m), int(prev), &one, pj.get(),
+                                 int(prev), cur->get(), int(prev), &zero, Zout.get(), int(t.s3)),
+                     "cublasDgemm(chain Gaussian stage)");
+        div_launch(Zout.get(), m * t.s3, std::sqrt(double(t.s3)), c.stream);
+        c.sync();
+    }
+}
+
+// krr_rff_build generalised: the context's own rows [z0, z1) -> resident sketch Z.
+void chain_build(Ctx& c, const krr_chain_tables& t) {
+    require_data(c);
+    c.set_device();
+    check_tables(c, t);
+    sketch_alloc(c, c.n, chain_out_dim(t.s1, t.s2, t.s3));
+    chain_apply_dev(c, t, c.X.get() + c.z0 * c.d, c.z1 - c.z0, c.Z);
+    c.sync();
+    c.has_sketch = true;
+}
+
+void adaptive_dev(Ctx& c, const krr_chain_spec& tmpl, double lambda, double lambda_p, int64_t s0, int64_t s_max,
+                  uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
+                  int64_t* final_size, int* passed, int* jitter_used) {
+    require_data(c);
+    if (s0 < 1) fail(kInvalid, "adaptive_build: s0 must be at least 1");
+    if (s_max < s0) fail(kInvalid, "adaptive_build: s_max must be >= s0");
+    validate_chain(tmpl);
+    check_family(c, tmpl.first);
+    const double lp = lambda_p > 0.0 ? lambda_p : lambda;
+    int64_t s = s0;
+    int nh = 0;
+    bool ok = false;
+    for (int attempt = 0;; ++attempt) {
+        const uint64_t seed = master_seed + uint64_t(attempt) * kAttemptSeedStride;
+        ChainOwned o;
+        realize_chain_host(c, chain_scaled_to(tmpl, s), seed, o);
+        chain_build(c, o.t);
+        const krr_quality_report rep = quality_test_dev(c, lambda);
+        if (history && nh < max_history) history[nh] = rep;
+        ++nh;
+        if (final_size) *final_size = s;
+        if (rep.passed) {
+            ok = true;
+            break;
+        }
+        if (s >= s_max) break;
+        s = std::min(2 * s, s_max);
+    }
+    if (n_history) *n_history = nh;
+    if (passed) *passed = ok ? 1 : 0;
+    precond_build(c, lp, jitter_used);
+}
+
+}  // namespace
+}  // namespace krr
+
+extern "C" {
+
+int krr_set_data_kernel(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const krr_kernel_spec* kernel) {
+    return guard([&] {
+        if (!kernel) fail(KRR_ERR_INVALID_ARGUMENT, "null kernel spec");
+        krr::set_data(*krr::as_ctx(ctx), X, n, d, *kernel);
+    });
+}
+
+int krr_tensorsketch_realize(uint64_t seed, int64_t in_dim, int64_t s, int degree, uint32_t* hash, double* sign) {
+    return guard([&] { krr::tensorsketch_realize(seed, in_dim, s, degree, hash, sign); });
+}
+
+int krr_srht_realize(uint64_t seed, int64_t in_dim, int64_t s, double* sign, int64_t* rows) {
+    return guard([&] { krr::srht_realize(seed, in_dim, s, sign, rows); });
+}
+
+int krr_gaussmap_realize(uint64_t seed, int64_t in_dim, int64_t s, double* proj) {
+    return guard([&] { krr::gaussmap_realize(seed, in_dim, s, proj); });
+}
+
+int krr_chain_apply(krr_ctx* ctx, const krr_chain_tables* tables, const double* Xq, int64_t m, double* Z) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (!tables) fail(KRR_ERR_INVALID_ARGUMENT, "null chain tables");
+        if (m < 0) fail(KRR_ERR_DIMENSION_MISMATCH, "chain apply: bad shapes");
+        c.set_device();
+        krr::DevMem<double> q, z;
+        krr::upload(q, Xq, size_t(m * c.d), c.stream);
+        krr::chain_apply_dev(c, *tables, q.get(), m, z);
+        const int64_t out = krr::chain_out_dim(tables->s1, tables->s2, tables->s3);
+        if (m > 0)
+            KRR_CUDA(cudaMemcpyAsync(Z, z.get(), sizeof(double) * size_t(m * out), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
+int krr_chain_build(krr_ctx* ctx, const krr_chain_tables* tables) {
+    return guard([&] {
+        if (!tables) fail(KRR_ERR_INVALID_ARGUMENT, "null chain tables");
+        krr::chain_build(*krr::as_ctx(ctx), *tables);
+    });
+}
+
+int krr_chain_build_seeded(krr_ctx* ctx, const krr_chain_spec* spec, uint64_t master_seed) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (!spec) fail(KRR_ERR_INVALID_ARGUMENT, "null chain spec");
+        krr::ChainOwned o;
+        krr::realize_chain_host(c, *spec, master_seed, o);
+        krr::chain_build(c, o.t);
+    });
+}
+
+int krr_chain_scaled_to(const krr_chain_spec* spec, int64_t target, krr_chain_spec* out) {
+    return guard([&] {
+        if (!spec || !out) fail(KRR_ERR_INVALID_ARGUMENT, "null chain spec");
+        *out = krr::chain_scaled_to(*spec, target);
+    });
+}
+
+int krr_train_ex(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const double* Y, int64_t t,
+                 const krr_kernel_spec* kernel, const krr_chain_spec* chain, double lambda, double lambda_p,
+                 uint64_t master_seed, double tau, int max_iter, double* C, krr_rhs_stats* stats,
+                 double* residual_history, int64_t* total_matvecs, double* phase_ms) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (!kernel || !chain) fail(KRR_ERR_INVALID_ARGUMENT, "null kernel or chain spec");
+        if (n < 1) fail(KRR_ERR_INVALID_ARGUMENT, "train: dataset is empty");          // solver.cpp:97
+        if (!(lambda > 0.0)) fail(KRR_ERR_NON_POSITIVE_LAMBDA, "train: lambda must be positive");
+        const double lp = lambda_p > 0.0 ? lambda_p : lambda;                           // solver.cpp:102
+        krr::validate_chain(*chain);
+        krr::set_data(c, X, n, d, *kernel);
+        krr::ChainOwned o;
+        krr::realize_chain_host(c, *chain, master_seed, o);
+        cudaEvent_t ev[4];
+        for (auto& e : ev) KRR_CUDA(cudaEventCreate(&e));
+        KRR_CUDA(cudaEventRecord(ev[0], c.stream));
+        krr::chain_build(c, o.t);
+        KRR_CUDA(cudaEventRecord(ev[1], c.stream));
+        krr::precond_build(c, lp, nullptr);
+        KRR_CUDA(cudaEventRecord(ev[2], c.stream));
+        krr::solve_gaussian(c, lambda, Y, t, tau, max_iter, 1, C, stats, residual_history, total_matvecs);
+        KRR_CUDA(cudaEventRecord(ev[3], c.stream));
+        KRR_CUDA(cudaEventSynchronize(ev[3]));
+        if (phase_ms) {
+            float a = 0, b = 0, cc = 0, tot = 0;
+            KRR_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+            KRR_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+            KRR_CUDA(cudaEventElapsedTime(&cc, ev[2], ev[3]));
+            KRR_CUDA(cudaEventElapsedTime(&tot, ev[0], ev[3]));
+            phase_ms[0] = a;
+            phase_ms[1] = b;
+            phase_ms[2] = cc;
+            phase_ms[3] = tot;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int krr_adaptive_build_ex(krr_ctx* ctx, const krr_chain_spec* chain_template, double lambda, double lambda_p,
+                          int64_t s0, int64_t s_max, uint64_t master_seed, krr_quality_report* history,
+                          int max_history, int* n_history, int64_t* final_size, int* passed, int* jitter_used) {
+    return guard([&] {
+        if (!chain_template) fail(KRR_ERR_INVALID_ARGUMENT, "null chain spec");
+        krr::adaptive_dev(*krr::as_ctx(ctx), *chain_template, lambda, lambda_p, s0, s_max, master_seed, history,
+                          max_history, n_history, final_size, passed, jitter_used);
+    });
+}
+
+int krr_rf_baseline_train_ex(krr_ctx* ctx, const krr_chain_tables* tables, const double* Y, int64_t t,
+                             double lambda, double* w_out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (!tables) fail(KRR_ERR_INVALID_ARGUMENT, "null chain tables");
+        if (!(lambda > 0.0)) krr::fail(KRR_ERR_NON_POSITIVE_LAMBDA, "baseline: lambda must be positive");
+        if (t < 1) krr::fail(KRR_ERR_DIMENSION_MISMATCH, "baseline: Y needs at least one column");
+        if (c.world != 1) krr::fail(KRR_ERR_STATE, "the random-features baseline is single-rank");
+        c.set_device();
+        krr::DevMem<double> Z;
+        krr::chain_apply_dev(c, *tables, c.X.get(), c.n, Z);
+        krr::rf_baseline_solve(c, Z, krr::chain_out_dim(tables->s1, tables->s2, tables->s3), Y, t, lambda, w_out);
+    });
+}
+
+int krr_rf_baseline_predict_ex(krr_ctx* ctx, const krr_chain_tables* tables, const double* Xq, int64_t m,
+                               const double* w, int64_t t, double* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        krr::require_data(c);
+        if (!tables) fail(KRR_ERR_INVALID_ARGUMENT, "null chain tables");
+        if (t < 1 || m < 0) krr::fail(KRR_ERR_DIMENSION_MISMATCH, "baseline predict: bad shapes");
+        c.set_device();
+        if (m == 0) return;
+        const int64_t s = krr::chain_out_dim(tables->s1, tables->s2, tables->s3);
+        krr::DevMem<double> q, Zq, wd, o;
+        krr::upload(q, Xq, size_t(m * c.d), c.stream);
+        krr::chain_apply_dev(c, *tables, q.get(), m, Zq);
+        krr::upload(wd, w, size_t(s * t), c.stream);
+        o.ensure(size_t(m * t));
+        const double one = 1.0, zero = 0.0;
+        krr::cublas_check(cublasSetStream(c.blas, c.stream), "cublasSetStream");
+        krr::cublas_check(cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, int(t), int(m), int(s), &one, wd.get(), int(t),
+                                      Zq.get(), int(s), &zero, o.get(), int(t)),
+                          "cublasDgemm(Zq w)");
+        KRR_CUDA(cudaMemcpyAsync(out, o.get(), sizeof(double) * size_t(m * t), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
+int krr_model_save_ex(const char* path, const krr_kernel_spec* kernel, double lambda, uint64_t seed,
+                      const double* label_map, int64_t nlabels, const double* X, int64_t n, int64_t d,
+                      const double* C, int64_t t) {
+    return guard([&] {
+        if (!kernel) fail(KRR_ERR_INVALID_ARGUMENT, "null kernel spec");
+        krr::validate_kernel(*kernel);
+        krr::model_save(path, kernel->family, kernel->sigma, kernel->gamma, kernel->offset, kernel->degree, lambda,
+                        seed, label_map, nlabels, X, n, d, C, t);
+    });
+}
+
+int krr_model_kernel(const char* path, krr_kernel_spec* kernel) {
+    return guard([&] {
+        if (!kernel) fail(KRR_ERR_INVALID_ARGUMENT, "null kernel spec");
+        const krr::ModelMeta m = krr::model_info(path);
+        *kernel = krr_kernel_spec{};
+        kernel->family = m.family;
+        kernel->sigma = m.sigma;
+        kernel->gamma = m.gamma;
+        kernel->offset = m.offset;
+        kernel->degree = m.degree;
     });
 }
 

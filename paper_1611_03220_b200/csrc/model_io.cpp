@@ -6,6 +6,7 @@
 // C (n x t fp64, row-major), host byte order.  The metadata for a Gaussian model is
 //   {"d":D,"kernel":{"family":"gaussian","sigma":S},"label_map":[...],"lambda":L,"n":N,
 //    "seed":SEED,"t":T,"tool_version":"0.1.0"}
+// and a polynomial model's kernel object is {"degree":Q,"family":"polynomial","gamma":G,"offset":C}.
 // with doubles in nlohmann's shortest-round-trip format (dtoa_impl::format_buffer: fixed
 // notation for decimal exponents in (-4, 15], ".0" appended to integral values, otherwise
 // d.ddde±XX with at least two exponent digits).  load_model's checks are kept: bad magic,
@@ -226,10 +227,22 @@ ModelMeta read_meta(std::ifstream& in, const std::string& path) {
     if (!kobj) io_fail("model file: bad metadata: kernel");
     auto fam = std::get_if<std::string>(&at(**kobj, "family").v);
     if (!fam) io_fail("model file: bad metadata: kernel family");
-    if (*fam == "polynomial")
-        io_fail("model file: polynomial kernel — the B200 path serves the Gaussian kernel only");
-    if (*fam != "gaussian") io_fail("model file: unknown kernel family '" + *fam + "'");
-    m.sigma = num(at(**kobj, "sigma"));
+    // kernel_from_json (io.cpp:82-90) -> KernelSpec::gaussian / ::polynomial, which validate.
+    if (*fam == "gaussian") {
+        m.family = 0;
+        m.sigma = num(at(**kobj, "sigma"));
+        if (!(m.sigma > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: sigma must be positive");
+    } else if (*fam == "polynomial") {
+        m.family = 1;
+        m.gamma = num(at(**kobj, "gamma"));
+        m.offset = num(at(**kobj, "offset"));
+        m.degree = int(unum(at(**kobj, "degree")));
+        if (m.degree < 1) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: degree must be at least 1");
+        if (m.offset < 0.0) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: offset must be non-negative");
+        if (!(m.gamma > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "KernelSpec: gamma must be positive");
+    } else {
+        io_fail("model file: unknown kernel family '" + *fam + "'");
+    }
     m.lambda = num(at(o, "lambda"));
     m.seed = unum(at(o, "seed"));
     auto lm = std::get_if<std::shared_ptr<JArr>>(&at(o, "label_map").v);
@@ -247,12 +260,17 @@ ModelMeta read_meta(std::ifstream& in, const std::string& path) {
 
 namespace krr {
 
-void model_save(const char* path, double sigma, double lambda, uint64_t seed, const double* label_map,
-                int64_t nlabels, const double* X, int64_t n, int64_t d, const double* C, int64_t t) {
+void model_save(const char* path, int family, double sigma, double gamma, double offset, int degree, double lambda,
+                uint64_t seed, const double* label_map, int64_t nlabels, const double* X, int64_t n, int64_t d,
+                const double* C, int64_t t) {
     if (!path) fail(KRR_ERR_INVALID_ARGUMENT, "model file: null path");
     if (n < 1 || d < 0 || t < 1 || nlabels < 0) fail(KRR_ERR_DIMENSION_MISMATCH, "model file: bad shapes");
-    std::string meta = "{\"d\":" + std::to_string(d) + ",\"kernel\":{\"family\":\"gaussian\",\"sigma\":" +
-                       json_double(sigma) + "},\"label_map\":[";
+    // kernel_to_json (io.cpp:73-80); nlohmann orders object keys alphabetically.
+    const std::string kernel =
+        family == 0 ? "{\"family\":\"gaussian\",\"sigma\":" + json_double(sigma) + "}"
+                    : "{\"degree\":" + std::to_string(degree) + ",\"family\":\"polynomial\",\"gamma\":" +
+                          json_double(gamma) + ",\"offset\":" + json_double(offset) + "}";
+    std::string meta = "{\"d\":" + std::to_string(d) + ",\"kernel\":" + kernel + ",\"label_map\":[";
     for (int64_t i = 0; i < nlabels; ++i) meta += (i ? "," : "") + json_double(label_map[i]);
     meta += "],\"lambda\":" + json_double(lambda) + ",\"n\":" + std::to_string(n) + ",\"seed\":" +
             std::to_string(seed) + ",\"t\":" + std::to_string(t) + ",\"tool_version\":\"" + kToolVersion + "\"}";
