@@ -70,7 +70,23 @@ __device__ __forceinline__ double poly_ipow(double p, const ExpConsts& c) {
     return r;
 }
 
-// The K1 epilogue: MODE 0/1 Gaussian (libdevice / table exp), MODE 2 polynomial.
+// The same product chain with the degree known at compile time: straight-line code the
+// scheduler interleaves across a tile's accumulators (a runtime-trip-count loop per element
+// serialises the dependent DMULs and measured 1.5x slower than the Gaussian epilogue).
+template <int Q>
+__device__ __forceinline__ double poly_ipow_fixed(double p) {
+    double r = p;
+#pragma unroll
+    for (int i = 1; i < Q; ++i) r = __dmul_rn(r, p);
+    return r;
+}
+
+// K1 epilogue modes: 0/1 Gaussian (libdevice / table exp); 2 polynomial, runtime degree;
+// 10 + q polynomial of compile-time degree q (q = 1..4).
+constexpr int kPolyModeBase = 10;
+constexpr int kPolyMaxFixed = 4;
+inline int poly_mode(int degree) { return degree <= kPolyMaxFixed ? kPolyModeBase + degree : 2; }
+
 template <int MODE>
 __device__ __forceinline__ double gauss_exp(double d2, const ExpConsts& c,
                                             const double* __restrict__ tab) {
@@ -78,6 +94,8 @@ __device__ __forceinline__ double gauss_exp(double d2, const ExpConsts& c,
         return gauss_exp_libdevice(d2, c);
     } else if constexpr (MODE == 1) {
         return gauss_exp_table(d2, c, tab);
+    } else if constexpr (MODE >= kPolyModeBase) {
+        return poly_ipow_fixed<MODE - kPolyModeBase>(d2);
     } else {
         return poly_ipow(d2, c);
     }

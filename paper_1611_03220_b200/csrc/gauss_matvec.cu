@@ -622,6 +622,14 @@ void gauss_matvec_launch(const GaussMatvecPlan& p, const double* v, double* part
     };
     if (exp_mode == 2)
         dispatch(std::integral_constant<int, 2>{});
+    else if (exp_mode == kPolyModeBase + 1)
+        dispatch(std::integral_constant<int, kPolyModeBase + 1>{});
+    else if (exp_mode == kPolyModeBase + 2)
+        dispatch(std::integral_constant<int, kPolyModeBase + 2>{});
+    else if (exp_mode == kPolyModeBase + 3)
+        dispatch(std::integral_constant<int, kPolyModeBase + 3>{});
+    else if (exp_mode == kPolyModeBase + 4)
+        dispatch(std::integral_constant<int, kPolyModeBase + 4>{});
     else if (exp_mode == 0)
         dispatch(std::integral_constant<int, 0>{});
     else

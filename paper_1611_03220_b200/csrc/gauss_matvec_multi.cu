@@ -18,6 +18,8 @@
 //
 // Layout: V, OUT and part are row-major with T interleaved columns (element (i, c) at
 // i*T + c); rows >= n are zero.
+#include <type_traits>
+
 #include "common.cuh"
 #include "gauss_exp.cuh"
 #include "kernels.cuh"
@@ -304,10 +306,21 @@ void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, doubl
     a.dp = p.dp;
     a.st = p.st;
     a.ec = p.ec;
+    auto by_mode = [&](auto tv) {
+        constexpr int TT = decltype(tv)::value;
+        switch (mode) {
+            case 2: launch_matmat<TT, 2>(a, p.num_tiles, stream); break;
+            case kPolyModeBase + 1: launch_matmat<TT, kPolyModeBase + 1>(a, p.num_tiles, stream); break;
+            case kPolyModeBase + 2: launch_matmat<TT, kPolyModeBase + 2>(a, p.num_tiles, stream); break;
+            case kPolyModeBase + 3: launch_matmat<TT, kPolyModeBase + 3>(a, p.num_tiles, stream); break;
+            case kPolyModeBase + 4: launch_matmat<TT, kPolyModeBase + 4>(a, p.num_tiles, stream); break;
+            default: launch_matmat<TT, 1>(a, p.num_tiles, stream);
+        }
+    };
     if (T == 8) {
-        mode == 2 ? launch_matmat<8, 2>(a, p.num_tiles, stream) : launch_matmat<8, 1>(a, p.num_tiles, stream);
+        by_mode(std::integral_constant<int, 8>{});
     } else if (T == 16) {
-        mode == 2 ? launch_matmat<16, 2>(a, p.num_tiles, stream) : launch_matmat<16, 1>(a, p.num_tiles, stream);
+        by_mode(std::integral_constant<int, 16>{});
     } else {
         fail(KRR_ERR_INVALID_ARGUMENT, "gauss_matmat: T must be 8 or 16");
     }

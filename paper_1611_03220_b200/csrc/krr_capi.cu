@@ -212,7 +212,7 @@ void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t
         gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.ejs8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
                                c.stream, c.i8_debug);
     else
-        gauss_matvec_launch(c.plan, v, c.part.get(), c.family == 1 ? 2 : c.exp_mode, c.stream);
+        gauss_matvec_launch(c.plan, v, c.part.get(), c.family == 1 ? poly_mode(c.degree) : c.exp_mode, c.stream);
     if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
     matvec_finish_launch(c.plan, c.part.get(), v, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad);
@@ -572,7 +572,7 @@ void ensure_batched(Ctx& c, int T) {
 
 // out (n_pad x T) = (K + lambda I) v (n_pad x T), replicated on all ranks.
 void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
-    gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.family == 1 ? 2 : 1, c.stream);
+    gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.family == 1 ? poly_mode(c.degree) : 1, c.stream);
     matmat_finish_launch(c.plan, c.bpart.get(), v, T, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad * T);
 }

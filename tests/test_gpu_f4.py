@@ -15,6 +15,7 @@ POLY_CASES = [  # n, d, gamma, offset, degree
     (700, 16, 0.05, 1.0, 3),
     (1500, 9, 0.3, 0.0, 4),
     (2100, 40, 0.02, 0.5, 1),
+    (300, 4, 0.3, 0.2, 6),  # degree > 4: the runtime-degree epilogue
 ]
 
 
@@ -42,17 +43,17 @@ def test_poly_matvec_matches_oracle(krr, oracle, ctx, n, d, g, c, q):
     assert np.all(np.abs(got - want) <= 1e-12 * scale * q + 1e-300), np.max(np.abs(got - want) / scale)
 
 
-@pytest.mark.parametrize("t", [2, 8, 16])
-def test_poly_matmat_matches_oracle(krr, oracle, ctx, t):
+@pytest.mark.parametrize("t,q", [(2, 2), (8, 3), (16, 2), (16, 5)])
+def test_poly_matmat_matches_oracle(krr, oracle, ctx, t, q):
     """Multi-column operator (K1T for t in {8, 16}) with the polynomial epilogue."""
     n, d = 900, 7
     x = oracle.random_matrix(n, d, 21)
     v = oracle.random_matrix(n, t, 22)
-    op = krr.KernelOperator(x, _pk(krr, 0.5, 1.5, 2), 0.1, ctx=ctx)
+    op = krr.KernelOperator(x, _pk(krr, 0.5, 1.5, q), 0.1, ctx=ctx)
     got = op.matmat(v)
-    k = oracle.poly_gram(x, 0.5, 1.5, 2)
+    k = oracle.poly_gram(x, 0.5, 1.5, q)
     want = k @ v + 0.1 * v
-    assert np.max(np.abs(got - want) / (np.abs(k) @ np.abs(v) + 0.1 * np.abs(v))) <= 2e-12
+    assert np.max(np.abs(got - want) / (np.abs(k) @ np.abs(v) + 0.1 * np.abs(v))) <= 1e-12 * q
 
 
 def test_poly_predict_matches_oracle(krr, oracle, ctx):
