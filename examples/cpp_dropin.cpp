@@ -141,6 +141,43 @@ int main() {
         check(std::sqrt(fn / nn) <= 2e-6, "fp32 mode within 2e-6");
         check(krr_set_precision(ctx, 16) == KRR_ERR_INVALID_ARGUMENT, "precision 16 rejected");
     }
+    // polynomial kernel + TensorSketch -> SRHT chain through krr_train_ex; the
+    // true residual of the returned c through the device polynomial operator
+    {
+        const int64_t n = 500, d = 4;
+        auto x = random_matrix(n, d, 21);
+        for (auto& v : x) v *= 0.5;
+        const auto y = random_matrix(n, 1, 22);
+        krr_kernel_spec k{};
+        k.family = 1;
+        k.gamma = 1.0;
+        k.offset = 0.5;
+        k.degree = 2;
+        krr_chain_spec ch{};
+        ch.first = 1;
+        ch.s1 = 64;
+        ch.s2 = 32;
+        std::vector<double> c(static_cast<size_t>(n));
+        krr_rhs_stats st{};
+        int64_t total = 0;
+        must(krr_train_ex(ctx, x.data(), n, d, y.data(), 1, &k, &ch, 0.05, -1.0, 3, 1e-9, 300, c.data(), &st,
+                          nullptr, &total, nullptr),
+             "train_ex polynomial");
+        std::vector<double> kc(static_cast<size_t>(n));
+        must(krr_kernel_matvec(ctx, 0.05, c.data(), 1, kc.data()), "polynomial matvec");
+        double rn = 0, yn = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            rn += (y[size_t(i)] - kc[size_t(i)]) * (y[size_t(i)] - kc[size_t(i)]);
+            yn += y[size_t(i)] * y[size_t(i)];
+        }
+        check(st.converged == 1 && std::sqrt(rn) <= 1e-7 * std::sqrt(yn), "polynomial train residual within tau");
+        krr_chain_spec bad = ch;
+        bad.first = 0;
+        check(krr_chain_build_seeded(ctx, &bad, 0) == KRR_ERR_INVALID_ARGUMENT, "RFF chain on a polynomial kernel rejected");
+        krr_chain_spec half{};
+        must(krr_chain_scaled_to(&ch, 16, &half), "scaled_to");
+        check(half.s1 == 32 && half.s2 == 16, "ChainSpec::scaled_to(16) of {64, 32}");
+    }
     // error mapping: lambda <= 0 -> NonPositiveLambda; sigma <= 0 -> invalid_argument
     {
         double dummy[4] = {0, 0, 0, 0};
