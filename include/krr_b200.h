@@ -82,7 +82,11 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
  *   "k1_warps" 8|16, "k1_grouped" 1|0  DMMA mat-vec shape (defaults 8, 1)
  *   "batched_rhs" 1|0  multi-RHS solves / mat-mats through the batched kernel (default 1)
  *   "exp_mode"    1|0  table exp (default) | libdevice exp in the Gaussian epilogue
- *   "i8_debug"    bits  profiling only (K1-I8: 1 skip MMAs, 2 skip exp, 4 clock trace) */
+ *   "i8_debug"    bits  profiling only (K1-I8: 1 skip MMAs, 2 skip exp, 4 clock trace)
+ *   "emulate_world" W, "emulate_rank" r   test only, single-rank contexts: the next
+ *                         krr_set_data builds rank r of W's K1 schedule (tiles, owned slots,
+ *                         diagonal on rank 0) with no collective, so K v returns that rank's
+ *                         partial — the multi-rank K1 checked on one GPU (sum over r = K v) */
 int krr_set_option(krr_ctx* ctx, const char* key, double value);
 /* Arithmetic of the fused mat-vec (SURVEY §8b krr_set_precision; north-star "optional fp32
  * mode, reported separately"): 64 = fp64, oracle-matching (default); 32 = fp32-accuracy K1

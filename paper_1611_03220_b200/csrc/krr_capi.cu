@@ -109,6 +109,11 @@ struct Ctx {
     cusolverDnHandle_t sol = nullptr;
     ncclComm_t comm = nullptr;
     int exp_mode = 1;
+    // Test-only single-GPU emulation of rank `emu_rank` of `emu_world` for the K1 / K1T
+    // kernels (the B200_PROFILING rule: with fewer GPUs than ranks, emulate the ranks): the
+    // schedule, owned slots and diagonal term of that rank, no collective — K v returns the
+    // rank's partial sum.  Applied at krr_set_data; a single-rank context only.
+    int emu_world = 1, emu_rank = 0;
     bool k1_resident = true;
     bool k1_warps16 = false;
     bool k1_grouped = true;
@@ -162,6 +167,9 @@ struct Ctx {
     int* hactive = nullptr;
 
     void set_device() const { KRR_CUDA(cudaSetDevice(device)); }
+    // the (world, rank) the K1 schedule is built for
+    int k1_world() const { return world > 1 ? world : emu_world; }
+    int k1_rank() const { return world > 1 ? rank : emu_rank; }
     void sync() const { KRR_CUDA(cudaStreamSynchronize(stream)); }
 };
 
@@ -214,7 +222,7 @@ void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t
     else
         gauss_matvec_launch(c.plan, v, c.part.get(), c.family == 1 ? poly_mode(c.degree) : c.exp_mode, c.stream);
     if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
-    matvec_finish_launch(c.plan, c.part.get(), v, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
+    matvec_finish_launch(c.plan, c.part.get(), v, lambda, c.k1_rank() == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad);
 }
 
@@ -251,7 +259,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_sp
     c.gamma = ks.gamma;
     c.offset = ks.offset;
     c.degree = ks.degree;
-    c.sched = make_schedule(n, c.world, c.rank);
+    c.sched = make_schedule(n, c.k1_world(), c.k1_rank());
     const int dp = int(((d + 2) + 3) / 4 * 4);
     const int64_t n_pad = c.sched.n_pad;
     c.X.ensure(size_t(n * d));
@@ -271,7 +279,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_sp
     if (ntiles)
         KRR_CUDA(cudaMemcpyAsync(c.tiles.get(), c.sched.tiles.data(), sizeof(int2) * size_t(ntiles),
                                  cudaMemcpyHostToDevice, c.stream));
-    if (c.world > 1) {
+    if (c.k1_world() > 1) {
         c.owned.ensure(c.sched.owned.size());
         KRR_CUDA(cudaMemcpyAsync(c.owned.get(), c.sched.owned.data(), c.sched.owned.size(),
                                  cudaMemcpyHostToDevice, c.stream));
@@ -295,7 +303,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_sp
     p.R = c.R.get();
     p.tiles = c.tiles.get();
     p.num_tiles = ntiles;
-    p.owned = c.world > 1 ? c.owned.get() : nullptr;
+    p.owned = c.k1_world() > 1 ? c.owned.get() : nullptr;
     p.exp_tab = c.exp_tab.get();
     p.n = n;
     p.n_pad = n_pad;
@@ -573,7 +581,7 @@ void ensure_batched(Ctx& c, int T) {
 // out (n_pad x T) = (K + lambda I) v (n_pad x T), replicated on all ranks.
 void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
     gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.family == 1 ? poly_mode(c.degree) : 1, c.stream);
-    matmat_finish_launch(c.plan, c.bpart.get(), v, T, lambda, c.rank == 0 ? 1 : 0, out, c.stream);
+    matmat_finish_launch(c.plan, c.bpart.get(), v, T, lambda, c.k1_rank() == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad * T);
 }
 
@@ -1076,6 +1084,13 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
             c.batched = value != 0.0;
         } else if (k == "exp_mode") {
             c.exp_mode = value != 0.0 ? 1 : 0;
+        } else if (k == "emulate_world" || k == "emulate_rank") {
+            if (c.world != 1) fail(KRR_ERR_STATE, "rank emulation is for single-rank contexts");
+            const int iv = int(value);
+            if (double(iv) != value || iv < 0 || (k == "emulate_world" && iv < 1))
+                fail(KRR_ERR_INVALID_ARGUMENT, k + " must be a non-negative integer (world >= 1)");
+            (k == "emulate_world" ? c.emu_world : c.emu_rank) = iv;
+            c.has_data = false;  // the schedule is rebuilt by the next krr_set_data
         } else {
             fail(KRR_ERR_INVALID_ARGUMENT, "unknown option '" + k + "'");
         }
@@ -1108,6 +1123,10 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
             *value = c.exp_mode;
         } else if (k == "batched_rhs") {
             *value = c.batched ? 1.0 : 0.0;
+        } else if (k == "emulate_world") {
+            *value = c.emu_world;
+        } else if (k == "emulate_rank") {
+            *value = c.emu_rank;
         } else {
             fail(KRR_ERR_INVALID_ARGUMENT, "unknown option '" + k + "'");
         }
