@@ -282,3 +282,30 @@ def test_poly_model_file_round_trip(krr, oracle, ctx, tmp_path):
     assert np.array_equal(back.x, x) and np.array_equal(back.c, cmat)
     xq = oracle.random_matrix(5, 3, 9)
     assert rel(krr.predict_scores(back, xq, ctx=ctx), oracle.poly_cross(xq, x, 0.01, 1.0, 3) @ cmat) <= 1e-12
+
+
+@pytest.mark.parametrize("first,s1,s2,s3,q", [("TensorSketch", 1, 0, 0, 3), ("TensorSketch", 2, 1, 1, 2),
+                                              ("TensorSketch", 3, 0, 0, 5), ("RandomFourier", 1, 1, 1, 0),
+                                              ("RandomFourier", 5, 3, 0, 0)])
+def test_chain_degenerate_sizes(krr, oracle, ctx, first, s1, s2, s3, q):
+    """Tiny stages (P = 1 transforms, one-row SRHT, one-column Gaussian map) and a single row."""
+    kern = krr.KernelSpec.gaussian(1.1) if first == "RandomFourier" else _pk(krr, 0.6, 0.2, q)
+    chain = krr.realize_chain(krr.ChainSpec(first, s1, s2, s3), kern, 3, 11)
+    for m in (1, 9):
+        x = oracle.random_matrix(m, 3, 12 + m)
+        got = chain.apply_rows(x, ctx=ctx)
+        want = oracle.chain_apply_rows(_oracle_tables(chain), x)
+        assert got.shape == want.shape == (m, s3 or s2 or s1)
+        if first == "TensorSketch" and s3 == 0:
+            assert np.array_equal(got, want)
+        else:
+            assert rel(got, want) <= 1e-13
+
+
+def test_poly_degree_one_is_linear_kernel(krr, oracle, ctx):
+    """q = 1: K = gamma X X' + c (the diagonal included)."""
+    x = oracle.random_matrix(257, 6, 3)
+    v = oracle.random_vector(257, 4)
+    got = krr.KernelOperator(x, _pk(krr, 0.5, 2.0, 1), 0.0, ctx=ctx)(v)
+    want = (0.5 * x @ x.T + 2.0) @ v
+    assert rel(got, want) <= 1e-13
