@@ -382,6 +382,10 @@ int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, d
 /* TMEM read throughput (tcgen05.ld.32x32b.x16 + wait in a loop), `warps` warps on every
  * SM; returns bytes per clock per SM. */
 int krr_debug_tmem_ld_rate(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk);
+/* TMEM load bandwidth of `warps` warps while one more warp issues back-to-back kind::i8 MMAs
+ * (M 128, N 64, K 96 B) into other TMEM columns; *mma_cycles = the MMA's cycles / instruction
+ * meanwhile (tools/mma_rate.py). */
+int krr_debug_tmem_ld_under_mma(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk, double* mma_cycles);
 /* K1-I8 profiling trace (set_option("i8_debug", 4) before a mat-vec): clock64 stamps of
  * CTA 0, 16 per tile for the first 64 tiles. */
 int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count);

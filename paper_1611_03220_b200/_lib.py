@@ -180,6 +180,7 @@ _SIGS = {
     "krr_debug_bf16_gemm": [_vp, _vp, _vp, _vp, _i, _i],
     "krr_debug_i8_mma_rate": [_vp, _i, _i, _i, _i, C.POINTER(_d)],
     "krr_debug_tmem_ld_rate": [_vp, _i, _i, C.POINTER(_d)],
+    "krr_debug_tmem_ld_under_mma": [_vp, _i, _i, C.POINTER(_d), C.POINTER(_d)],
     "krr_debug_i8_trace": [_vp, _vp, _i],
     # SURVEY 8f4
     "krr_set_data_kernel": [_vp, _vp, _i64, _i64, C.POINTER(KernelSpecC)],

@@ -119,7 +119,8 @@ struct I8Args {
     int64_t n_pad;
     int st;
     int debug;  // profiling only: bit 0 skips the MMAs, bit 1 the exp phase (results invalid),
-                // bit 2 records a clock64 trace of CTA 0 (i8_read_trace)
+                // bit 2 records a clock64 trace of CTA 0 (i8_read_trace), bit 4 drops the exp
+                // polynomial (4 FP64 ops / pair fewer; results invalid)
     I8Consts ec;
 };
 
@@ -140,7 +141,7 @@ __device__ __forceinline__ double magic_pack(int32_t a, int32_t b) {
 // 1.5 * 2^52 + 2^31 and that constant times (1 + 2^-28), both exact integers < 2^53
 constexpr double M2 = 6755401588539392.0 + 25165832.0;  // M1 = 1.5 * 2^52 + 2^31, M2 = M1 (1 + 2^-28)
 
-template <bool MASK>
+template <bool MASK, bool CHEAP = false>
 __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts& ec, const double* __restrict__ tab,
                                           const double* __restrict__ cd_sq, const double* __restrict__ cd_v,
                                           const int* __restrict__ cd_e, double* __restrict__ scr,
@@ -168,14 +169,19 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
         for (int b = 0; b < BW; ++b) t2[b] = y[b] + shifter;
 #pragma unroll
         for (int b = 0; b < BW; ++b) f[b] = y[b] - (t2[b] - shifter);
+        if constexpr (CHEAP) {  // profiling only (i8_debug 16): 4 fewer FP64 ops, wrong values
 #pragma unroll
-        for (int b = 0; b < BW; ++b) q[b] = fma(f[b], ec.a5, ec.a4);
+            for (int b = 0; b < BW; ++b) q[b] = ec.a1;
+        } else {
 #pragma unroll
-        for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a3);
+            for (int b = 0; b < BW; ++b) q[b] = fma(f[b], ec.a5, ec.a4);
 #pragma unroll
-        for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a2);
+            for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a3);
 #pragma unroll
-        for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a1);
+            for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a2);
+#pragma unroll
+            for (int b = 0; b < BW; ++b) q[b] = fma(q[b], f[b], ec.a1);
+        }
 #pragma unroll
         for (int b = 0; b < BW; ++b) {
             q[b] = q[b] * f[b];
@@ -304,45 +310,52 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc = tc::idesc_i8(TI, TJ);
-            const uint32_t aBase = tc::smem_u32(sA);
-            int bq = 0;
-            for (int it = 0; it < nTI; ++it) {
-                tc::mbar_wait_sleep(a_full, uint32_t(it & 1));
+        // The whole warp runs the (warp-uniform) schedule and waits, so the descriptors stay in
+        // uniform registers; one elected lane issues each group's MMAs and their commits.  (A
+        // single-thread `if (lane == 0)` region made ptxas wrap every tcgen05.mma in an
+        // ELECT / R2UR waterfall loop of ~10 dependent instructions.)
+        const uint32_t idesc = tc::idesc_i8(TI, TJ);
+        const uint32_t aBase = tc::smem_u32(sA);
+        int bq = 0;
+        for (int it = 0; it < nTI; ++it) {
+            tc::mbar_wait_sleep(a_full, uint32_t(it & 1));
+            tc::fence_after();
+            for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
+                const int s = bq % NSTB;
+                I8_TRACE(lane == 0, bq, 8);
+                tc::mbar_wait_sleep(b_full + s, uint32_t((bq / NSTB) & 1));
                 tc::fence_after();
-                for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
-                    const int s = bq % NSTB;
-                    I8_TRACE(true, bq, 8);
-                    tc::mbar_wait_sleep(b_full + s, uint32_t((bq / NSTB) & 1));
-                    tc::fence_after();
-                    I8_TRACE(true, bq, 9);
-                    // Descriptors differ only in the start-address field (16-byte units):
-                    // two bases plus compile-time offsets in the fully unrolled sequence.
-                    const uint64_t dA0 = tc::smem_desc(aBase, 128, sbo);
-                    const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB + s * C::B_BYTES), 128, sbo);
+                I8_TRACE(lane == 0, bq, 9);
+                // Descriptors differ only in the start-address field (16-byte units):
+                // two bases plus compile-time offsets in the fully unrolled sequence.
+                const uint64_t dA0 = tc::smem_desc(aBase, 128, sbo);
+                const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB + s * C::B_BYTES), 128, sbo);
 #pragma unroll
-                    for (int c = NGRP - 1; c >= 0; --c) {
-                        if (bq > 0) {
-                            tc::mbar_wait_sleep(g_empty + c, uint32_t((bq - 1) & 1));
-                            tc::fence_after();
-                        }
-                        if (c == 7 || c == 4 || c == 0) I8_TRACE(true, bq, c == 7 ? 10 : (c == 4 ? 11 : 12));
+                for (int c = NGRP - 1; c >= 0; --c) {
+                    if (bq > 0) {
+                        tc::mbar_wait_sleep(g_empty + c, uint32_t((bq - 1) & 1));
+                        tc::fence_after();
+                    }
+                    if (c == 7 || c == 4 || c == 0) I8_TRACE(lane == 0, bq, c == 7 ? 10 : (c == 4 ? 11 : 12));
+                    if (tc::elect_one()) {
                         if (!(A.debug & 1))
 #pragma unroll
-                        for (int p = 0; p <= c; ++p)
+                            for (int p = 0; p <= c; ++p)
 #pragma unroll
-                            for (int ks = 0; ks < ksteps; ++ks)
-                                tc::mma_i8(tmem_base + uint32_t(c * TJ),
-                                           dA0 + uint64_t((p * TI * kp + ks * 256) >> 4),
-                                           dB0 + uint64_t(((c - p) * TJ * kp + ks * 256) >> 4), idesc,
-                                           (p == 0 && ks == 0) ? 0u : 1u);
+                                for (int ks = 0; ks < ksteps; ++ks)
+                                    tc::mma_i8(tmem_base + uint32_t(c * TJ),
+                                               dA0 + uint64_t((p * TI * kp + ks * 256) >> 4),
+                                               dB0 + uint64_t(((c - p) * TJ * kp + ks * 256) >> 4), idesc,
+                                               (p == 0 && ks == 0) ? 0u : 1u);
                         tc::mma_commit(g_full + c);
                     }
-                    tc::mma_commit(b_empty + s);
+                    __syncwarp();
                 }
-                tc::mma_commit(a_empty);
+                if (tc::elect_one()) tc::mma_commit(b_empty + s);
+                __syncwarp();
             }
+            if (tc::elect_one()) tc::mma_commit(a_empty);
+            __syncwarp();
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -374,15 +387,18 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 int32_t bint[CPT];
                 double lo[CPT], T[CPT];
                 auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
-                    tc::mbar_wait(g_full + ca + 1, ph);
-                    tc::mbar_wait(g_full + ca, ph);
+                    tc::mbar_wait_sleep(g_full + ca + 1, ph);
+                    I8_TRACE(etid == 0 && ca == 0, tq, 15);
+                    tc::mbar_wait_sleep(g_full + ca, ph);
                     tc::fence_after();
+                    I8_TRACE(etid == 0 && ca == 0, tq, 13);
                     // all loads of the stage in flight before one wait (TMEM load latency
                     // under load is ~250 clk; one round trip per stage, not per 8 columns)
                     uint32_t gl[CPT], gh[CPT];
                     tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ), gl);
                     tc::tmem_ld16(taddr + uint32_t(ca * TJ), gh);
                     tc::tmem_wait_ld();
+                    I8_TRACE(etid == 0 && ca == 0, tq, 14);
 #pragma unroll
                     for (int k = 0; k < CPT; ++k) fn(k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
                     tc::fence_before();
@@ -424,6 +440,9 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
                     exp_phase<true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
                                          rowacc, lane, colOff, mask_row);
+                } else if (A.debug & 16) {
+                    exp_phase<false, true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i,
+                                           v_i, rowacc, lane, colOff, 0);
                 } else {
                     exp_phase<false>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
                                           rowacc, lane, colOff, 0);

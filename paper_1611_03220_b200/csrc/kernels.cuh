@@ -168,7 +168,8 @@ void bf16_probe_launch(const uint16_t* A, const uint16_t* B, float* C, int K, in
 double i8_mma_rate(int N, int reps, int kbytes, int mode, cudaStream_t stream);
 double tmem_ld_rate(int warps, int reps, cudaStream_t stream);
 double i8_tile_order_rate(int order, int tiles, cudaStream_t stream);
-double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream);
+double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream, double* mma_cycles = nullptr, int nwork = 4);
+double tmem_ld_under_mma(int warps, int reps, cudaStream_t stream, double* mma_cycles);
 double i8_mma_rate_pair(int N, int reps, cudaStream_t stream);
 void debug_exp_launch(const double* d2, int64_t n, const ExpConsts& ec, const double* tab,
                       int mode, double* out, cudaStream_t stream);

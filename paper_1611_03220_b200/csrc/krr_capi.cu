@@ -1739,6 +1739,28 @@ int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, d
             *cycles_per_mma = krr::fp64_under_mma((mode - 8) >> 1, (mode - 8) & 1, std::max(64, reps), c.stream);
             return;
         }
+        if (mode >= 13 && mode <= 16) {  // 13 FFMA, 14 FFMA + MMA, 15 IMAD, 16 IMAD + MMA (lane-ops/clk/SM)
+            c.set_device();
+            *cycles_per_mma = krr::fp64_under_mma(2 + ((mode - 13) >> 1), (mode - 13) & 1, std::max(64, reps), c.stream);
+            return;
+        }
+        if (mode >= 17 && mode <= 24 && mode != 23) {  // MMA cycles / instr beside 17 DADD, 18 DFMA, 19 FFMA,
+            if (mode == 24) mode = 23;  // 20 IMAD, 21 idle, 22 LDS.128, 24 -> op 6 (FFMA off the MMA's SMSP)
+            c.set_device();
+            krr::fp64_under_mma(mode - 17, 1, std::max(64, reps), c.stream, cycles_per_mma);
+            return;
+        }
+        if (mode >= 26 && mode <= 29) {  // DFMA lane-ops/clk/SM with 16 worker warps: 26 alone, 27 + MMA;
+            c.set_device();               // 28 / 29: the same with 8 worker warps
+            const int nw = mode <= 27 ? 16 : 8;
+            *cycles_per_mma = krr::fp64_under_mma(1, (mode - 26) & 1, std::max(64, reps), c.stream, nullptr, nw);
+            return;
+        }
+        if (mode == 25) {  // MMA cycles / instr beside FFMA on the MMA warp's own SMSP only (op 7)
+            c.set_device();
+            krr::fp64_under_mma(7, 1, std::max(64, reps), c.stream, cycles_per_mma);
+            return;
+        }
         if (mode == 6 || mode == 7) {  // in-situ K1-I8 tile order (N = 64, kp = 96), reps = tiles
             c.set_device();
             *cycles_per_mma = krr::i8_tile_order_rate(mode - 6, std::max(1, reps), c.stream);
@@ -1756,6 +1778,15 @@ int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count) {
         Ctx& c = *krr::as_ctx(ctx);
         c.set_device();
         krr::i8_read_trace(out, count);
+    });
+}
+
+int krr_debug_tmem_ld_under_mma(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk, double* mma_cycles) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (warps < 1 || warps > 16 || reps < 1) fail(KRR_ERR_INVALID_ARGUMENT, "warps in [1, 16], reps >= 1");
+        c.set_device();
+        *bytes_per_clk = krr::tmem_ld_under_mma(warps, reps, c.stream, mma_cycles);
     });
 }
 

@@ -72,6 +72,18 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint
         "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
+// One lane of a converged warp (the lowest active one: the same lane every call, so the
+// tcgen05.commit that tracks a thread's MMAs is issued by the thread that issued them).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void mma_commit(void* mbar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                      smem_u32(mbar))

@@ -198,14 +198,14 @@ __global__ void __launch_bounds__(128) i8_tile_order_kernel(int tiles, long long
 // back-to-back tcgen05.mma kind::i8 (M = 128, N = 64, K = 32, SS) until they finish.
 // Returns cycles of the FP64 loop (max over SMs).
 template <int OP, bool MMA>
-__global__ void __launch_bounds__(256) fp64_under_mma_kernel(int iters, long long* out, double* sink) {
+__global__ void __launch_bounds__(1024) fp64_under_mma_kernel(int iters, long long* out, double* sink) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t mbar;
     __shared__ uint32_t tbase;
     __shared__ volatile int stop;
     __shared__ long long tmax;
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < (128 + 64) * 96; i += 256) sm[i] = 0;
+    for (int i = tid; i < (128 + 64) * 96; i += blockDim.x) sm[i] = 0;
     tc::fence_proxy_async();
     if (tid == 0) {
         tc::mbar_init(&mbar, 1);
@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(256) fp64_under_mma_kernel(int iters, long lon
         const uint64_t da = tc::smem_desc(tc::smem_u32(sm), 128, 96 * 8);
         const uint64_t db = tc::smem_desc(tc::smem_u32(sm + 128 * 96), 128, 96 * 8);
         int r = 0;
+        const long long m0 = clock64();
         while (!stop && r < (1 << 22)) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) tc::mma_i8(tmem + uint32_t(u * 64), da, db, idesc, 1u);
@@ -232,24 +233,71 @@ __global__ void __launch_bounds__(256) fp64_under_mma_kernel(int iters, long lon
                 tc::mbar_wait(&mbar, uint32_t(((r >> 6) - 1) & 1));
             }
         }
-    } else if (warp >= 4) {
-        double a[8];
+        // MMA cycles per instruction while the other warps ran (completed batches only)
+        if (r >= 64) out[gridDim.x + blockIdx.x] = (long long)(double(clock64() - m0) / double(r & ~63) * 1000.0);
+    } else if (warp >= 4 && !(OP == 6 && warp == 4) && !(OP == 7 && warp != 4)) {
+        // OP 0 DADD, 1 DFMA (FP64 pipe); 2 FFMA (FP32), 3 IMAD (integer): 8 chains per thread;
+        // OP 6: FFMA on the three SM sub-partitions the MMA warp does not use (warps 5-7);
+        // OP 7: FFMA on the MMA warp's sub-partition only (warp 4)
+        // OP 4: idle workers (sleep for ~iters x 32 clk) — the MMA-alone baseline of this harness
+        if constexpr (OP == 4) {
+            const long long s0 = clock64();
+            while (clock64() - s0 < (long long)iters * 32) __nanosleep(200);
+            const long long s1 = clock64();
+            atomicMax(reinterpret_cast<unsigned long long*>(&tmax), (unsigned long long)(s1 - s0));
+            __syncwarp();
+            if (tid == 128) stop = 1;
+            tc::fence_before();
+            __syncthreads();
+            if (tid == 0) out[blockIdx.x] = tmax;
+            if (warp == 0) tc::tmem_dealloc(tmem, 512);
+            return;
+        }
+        if constexpr (OP == 5) {  // shared-memory reads (LDS.128, conflict-free) beside the MMAs
+            const uint4* src = reinterpret_cast<const uint4*>(sm);
+            uint32_t x = 0;
+            const long long s0 = clock64();
+            for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = 1.0 + 1e-3 * (i + tid);
-        const double b = 1e-9, c = 0.999999;
+                for (int i = 0; i < 8; ++i) {
+                    const uint4 q = src[((it * 8 + i) * 32 + (tid & 31)) & 1023];
+                    x ^= q.x ^ q.y ^ q.z ^ q.w;
+                }
+            }
+            const long long s1 = clock64();
+            if (x == 0x9876u) sink[0] = double(x);
+            atomicMax(reinterpret_cast<unsigned long long*>(&tmax), (unsigned long long)(s1 - s0));
+            __syncwarp();
+            if (tid == 128) stop = 1;
+            tc::fence_before();
+            __syncthreads();
+            if (tid == 0) out[blockIdx.x] = tmax;
+            if (warp == 0) tc::tmem_dealloc(tmem, 512);
+            return;
+        }
+        using T = std::conditional_t<(OP <= 1), double,
+                                     std::conditional_t<(OP == 2 || OP >= 6), float, uint32_t>>;
+        T a[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = T(1.0 + 1e-3 * (i + tid));
+        const T b = OP == 3 ? T(12345) : T(1e-9), c = OP == 3 ? T(2654435761u) : T(0.999999);
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = OP == 0 ? a[i] + b : fma(a[i], c, b);
+            for (int i = 0; i < 8; ++i) {
+                if constexpr (OP == 0) a[i] = a[i] + b;
+                else if constexpr (OP == 3) a[i] = a[i] * c + b;
+                else a[i] = fma(a[i], c, b);
+            }
         }
         const long long t1 = clock64();
         double s = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s += a[i];
+        for (int i = 0; i < 8; ++i) s += double(a[i]);
         if (s == 1234.5) sink[0] = s;
         atomicMax(reinterpret_cast<unsigned long long*>(&tmax), (unsigned long long)(t1 - t0));
         __syncwarp();
-        if (tid == 128) stop = 1;
+        if (tid == (OP == 6 ? 160 : 128)) stop = 1;
     }
     tc::fence_before();
     __syncthreads();
@@ -349,6 +397,71 @@ __global__ void tmem_ld_rate_kernel(int reps, long long* out, unsigned* sink) {
     if (warp == 0) tc::tmem_dealloc(tbase, 512);
 }
 
+// TMEM loads (tcgen05.ld.32x32b.x16 + wait) by `warps` warps from columns [256, 512) while
+// one more warp issues back-to-back kind::i8 MMAs (M = 128, N = 64, K = 96 B) into columns
+// [0, 256): does the accumulator traffic of the MMAs slow the loads (and vice versa)?
+// out[b] = load cycles, out[148 + b] = MMA cycles / instruction x 1000.
+__global__ void tmem_ld_under_mma_kernel(int reps, int warps, long long* out, unsigned* sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tbase;
+    __shared__ volatile int stop;
+    __shared__ long long tmax;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (128 + 64) * 96; i += blockDim.x) sm[i] = 0;
+    tc::fence_proxy_async();
+    if (tid == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::mbar_fence_init();
+        stop = 0;
+        tmax = 0;
+    }
+    if (warp == 0) tc::tmem_alloc(&tbase, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tbase;
+    if (warp == warps) {
+        if ((tid & 31) == 0) {
+            const uint32_t idesc = tc::idesc_i8(128, 64);
+            const uint64_t da = tc::smem_desc(tc::smem_u32(sm), 128, 96 * 8);
+            const uint64_t db = tc::smem_desc(tc::smem_u32(sm + 128 * 96), 128, 96 * 8);
+            int r = 0;
+            const long long m0 = clock64();
+            while (!stop && r < (1 << 22)) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) tc::mma_i8(tmem + uint32_t((u & 3) * 64), da, db, idesc, 1u);
+                r += 8;
+                if ((r & 63) == 0) {
+                    tc::mma_commit(&mbar);
+                    tc::mbar_wait(&mbar, uint32_t(((r >> 6) - 1) & 1));
+                }
+            }
+            if (r >= 64) out[gridDim.x + blockIdx.x] = (long long)(double(clock64() - m0) / double(r & ~63) * 1000.0);
+        }
+    } else {
+        const uint32_t taddr = tmem + (uint32_t((warp & 3) * 32) << 16) + 256u;
+        unsigned x = 0;
+        const long long t0 = clock64();
+        for (int r = 0; r < reps; ++r) {
+            uint32_t v[16];
+            tc::tmem_ld16(taddr + uint32_t(((r * 16) + (warp >> 2) * 64) & 255), v);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x ^= v[j];
+        }
+        const long long t1 = clock64();
+        atomicMax(reinterpret_cast<unsigned long long*>(&tmax), (unsigned long long)(t1 - t0));
+        if (x == 0x12345u) sink[0] = x;
+        __syncwarp();
+        if (warp == 0 && (tid & 31) == 0) stop = 1;
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) out[blockIdx.x] = tmax;
+    if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
 }  // namespace
 
 double i8_mma_rate(int N, int reps, int kbytes, int mode, cudaStream_t stream) {
@@ -405,30 +518,48 @@ double i8_tile_order_rate(int order, int tiles, cudaStream_t stream) {
     return mx / (double(tiles) * 108.0);
 }
 
-double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream) {
+double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream, double* mma_cycles, int nwork) {
     long long* d = nullptr;
     double* sink = nullptr;
-    KRR_CUDA(cudaMalloc(&d, 148 * sizeof(long long)));
+    KRR_CUDA(cudaMalloc(&d, 2 * 148 * sizeof(long long)));
+    KRR_CUDA(cudaMemsetAsync(d, 0, 2 * 148 * sizeof(long long), stream));
     KRR_CUDA(cudaMalloc(&sink, sizeof(double)));
     const size_t smem = size_t(128 + 64) * 96;
     auto run = [&](auto kern) {
         KRR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<148, 256, smem, stream>>>(iters, d, sink);
+        kern<<<148, 32 * (4 + nwork), smem, stream>>>(iters, d, sink);
     };
-    if (op == 0 && mma) run(fp64_under_mma_kernel<0, true>);
-    else if (op == 0) run(fp64_under_mma_kernel<0, false>);
-    else if (mma) run(fp64_under_mma_kernel<1, true>);
-    else run(fp64_under_mma_kernel<1, false>);
+    switch (op * 2 + (mma ? 1 : 0)) {
+        case 0: run(fp64_under_mma_kernel<0, false>); break;
+        case 1: run(fp64_under_mma_kernel<0, true>); break;
+        case 2: run(fp64_under_mma_kernel<1, false>); break;
+        case 3: run(fp64_under_mma_kernel<1, true>); break;
+        case 4: run(fp64_under_mma_kernel<2, false>); break;
+        case 5: run(fp64_under_mma_kernel<2, true>); break;
+        case 6: run(fp64_under_mma_kernel<3, false>); break;
+        case 7: run(fp64_under_mma_kernel<3, true>); break;
+        case 9: run(fp64_under_mma_kernel<4, true>); break;
+        case 10: run(fp64_under_mma_kernel<5, false>); break;
+        case 11: run(fp64_under_mma_kernel<5, true>); break;
+        case 13: run(fp64_under_mma_kernel<6, true>); break;
+        default: run(fp64_under_mma_kernel<7, true>); break;
+    }
     KRR_LAUNCH_CHECK();
-    long long h[148];
+    long long h[2 * 148];
     KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
     KRR_CUDA(cudaStreamSynchronize(stream));
     cudaFree(d);
     cudaFree(sink);
     double mx = 0;
-    for (long long v : h) mx = std::max(mx, double(v));
-    // FP64 lane-ops per clock per SM: 4 warps x 32 lanes x 8 chains x iters / cycles
-    return 4.0 * 32 * 8 * double(iters) / mx;
+    for (int i = 0; i < 148; ++i) mx = std::max(mx, double(h[i]));
+    if (mma_cycles) {
+        double sum = 0;
+        for (int i = 148; i < 2 * 148; ++i) sum += double(h[i]) / 1000.0;
+        *mma_cycles = sum / 148.0;
+    }
+    // FP64 lane-ops per clock per SM: 4 warps x 32 lanes x 8 chains x iters / cycles (op 5: LDS
+    // bytes per clock per SM: 4 warps x 32 lanes x 8 x 16 B x iters / cycles)
+    return (op == 5 ? 16.0 : 1.0) * double(nwork) * 32 * 8 * double(iters) / mx;
 }
 
 double i8_mma_rate_pair(int N, int reps, cudaStream_t stream) {
@@ -465,7 +596,7 @@ double tmem_ld_rate(int warps, int reps, cudaStream_t stream) {
     cudaFree(d);
     cudaFree(sink);
     double mx = 0;
-    for (long long v : h) mx = std::max(mx, double(v));
+    for (int i = 0; i < 148; ++i) mx = std::max(mx, double(h[i]));
     // bytes per clock per SM: warps x reps x (32 lanes x 16 columns x 4 B) / cycles
     return double(warps) * reps * 2048.0 / mx;
 }
@@ -502,4 +633,30 @@ void i8_probe_launch(const int8_t* A, const int8_t* B, int32_t* C, int K, int N,
     KRR_LAUNCH_CHECK();
 }
 
+}  // namespace krr
+
+namespace krr {
+// TMEM load bandwidth (B/clk/SM) of `warps` warps beside back-to-back INT8 MMAs; *mma_cycles
+// receives the MMA's cycles per instruction meanwhile.
+double tmem_ld_under_mma(int warps, int reps, cudaStream_t stream, double* mma_cycles) {
+    long long* d = nullptr;
+    unsigned* sink = nullptr;
+    KRR_CUDA(cudaMalloc(&d, 2 * 148 * sizeof(long long)));
+    KRR_CUDA(cudaMemsetAsync(d, 0, 2 * 148 * sizeof(long long), stream));
+    KRR_CUDA(cudaMalloc(&sink, sizeof(unsigned)));
+    const size_t smem = size_t(128 + 64) * 96;
+    KRR_CUDA(cudaFuncSetAttribute(tmem_ld_under_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    tmem_ld_under_mma_kernel<<<148, 32 * (warps + 1), smem, stream>>>(reps, warps, d, sink);
+    KRR_LAUNCH_CHECK();
+    long long h[2 * 148];
+    KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d);
+    cudaFree(sink);
+    double mx = 0, sum = 0;
+    for (int i = 0; i < 148; ++i) mx = std::max(mx, double(h[i]));
+    for (int i = 148; i < 2 * 148; ++i) sum += double(h[i]) / 1000.0;
+    if (mma_cycles) *mma_cycles = sum / 148.0;
+    return double(warps) * reps * 2048.0 / mx;
+}
 }  // namespace krr

@@ -27,8 +27,9 @@ buf = np.zeros(64 * 16, dtype=np.int64)
 _lib.check(_lib.LIB.krr_debug_i8_trace(ctx.handle, buf.ctypes.data_as(C.c_void_p), buf.size))
 t = buf.reshape(64, 16)
 t0 = t[0, 0]
-names = ["start", "st6", "st4", "st2", "st0", "cd", "exp", "bar", "m:bfull?", "m:bfull", "m:g7", "m:g4", "m:g0"]
+names = ["start", "st6", "st4", "st2", "st0", "cd", "exp", "bar", "m:bfull?", "m:bfull", "m:g7", "m:g4", "m:g0",
+         "g0full", "g0ld", "g1full"]
 print("tile " + " ".join(f"{nm:>8s}" for nm in names))
 for q in range(1, 40):
     row = t[q]
-    print(f"{q:4d} " + " ".join(f"{(row[i] - t[q, 0]):8d}" for i in range(13)), f" dt={t[q + 1, 0] - t[q, 0]}")
+    print(f"{q:4d} " + " ".join(f"{(row[i] - t[q, 0]):8d}" for i in range(16)), f" dt={t[q + 1, 0] - t[q, 0]}")

@@ -35,11 +35,27 @@ for n in (64, 128, 256):
     macs_per_sm = 128 * n * 32
     print(json.dumps({"pair_cta_group2": True, "M": 256, "N": n, "cycles_per_mma": round(cyc.value, 2),
                       "mac_per_clk_per_sm": round(macs_per_sm / cyc.value, 1)}), flush=True)
-for mode, name in ((8, "DADD"), (9, "DADD+MMA"), (10, "DFMA"), (11, "DFMA+MMA")):
+for mode, name in ((8, "DADD"), (9, "DADD+MMA"), (10, "DFMA"), (11, "DFMA+MMA"), (13, "FFMA"), (14, "FFMA+MMA"),
+                   (15, "IMAD"), (16, "IMAD+MMA")):
     r = C.c_double()
     _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, 64, 20000, 96, mode, C.byref(r)))
     print(json.dumps({"fp64_under_mma": name, "fp64_lane_ops_per_clk_per_sm": round(r.value, 2)}), flush=True)
+for mode, name in ((21, "idle"), (17, "DADD"), (18, "DFMA"), (19, "FFMA"), (20, "IMAD"), (22, "LDS.128"),
+                   (24, "FFMA, other 3 SMSPs"), (25, "FFMA, MMA warp SMSP only")):
+    r = C.c_double()
+    _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, 64, 20000, 96, mode, C.byref(r)))
+    print(json.dumps({"mma_beside": name, "mma_cycles_per_instr": round(r.value, 2)}), flush=True)
 for warps in (1, 4, 8, 16):
     bpc = C.c_double()
     _lib.check(_lib.LIB.krr_debug_tmem_ld_rate(ctx.handle, warps, 4096, C.byref(bpc)))
     print(json.dumps({"tmem_ld_warps": warps, "bytes_per_clk_per_sm": round(bpc.value, 1)}), flush=True)
+
+for warps in (4, 8, 16):
+    bpc, mc = C.c_double(), C.c_double()
+    _lib.check(_lib.LIB.krr_debug_tmem_ld_under_mma(ctx.handle, warps, 4096, C.byref(bpc), C.byref(mc)))
+    print(json.dumps({"tmem_ld_under_mma_warps": warps, "bytes_per_clk_per_sm": round(bpc.value, 1),
+                      "mma_cycles_per_instr": round(mc.value, 2)}), flush=True)
+for mode, name in ((26, "DFMA 16 warps"), (27, "DFMA 16 warps + MMA"), (28, "DFMA 8 warps"), (29, "DFMA 8 warps + MMA")):
+    r = C.c_double()
+    _lib.check(_lib.LIB.krr_debug_i8_mma_rate(ctx.handle, 64, 20000, 96, mode, C.byref(r)))
+    print(json.dumps({"fp64_warps": name, "fp64_lane_ops_per_clk_per_sm": round(r.value, 2)}), flush=True)
