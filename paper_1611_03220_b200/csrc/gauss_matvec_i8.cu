@@ -99,7 +99,7 @@ struct Cfg {
     static constexpr size_t OFF_COLSCR = OFF_SCR + size_t(NEPI) * CPT * SCR_LD * 8;
     static constexpr size_t OFF_TAB = OFF_COLSCR + 2 * 4 * TJ * 8;
     static constexpr size_t OFF_BARS = OFF_TAB + TAB * TAB_REP * 8;
-    static constexpr int NBARS = 2 + 2 * NSTB + 2 * NCD + 2 * NGRP;
+    static constexpr int NBARS = 2 + 2 * NSTB + 2 * NCD + 2 * NGRP + 1;
     static constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
 };
 
@@ -120,7 +120,8 @@ struct I8Args {
     int st;
     int debug;  // profiling only: bit 0 skips the MMAs, bit 1 the exp phase (results invalid),
                 // bit 2 records a clock64 trace of CTA 0 (i8_read_trace), bit 4 drops the exp
-                // polynomial (4 FP64 ops / pair fewer; results invalid)
+                // polynomial (4 FP64 ops / pair fewer; results invalid); bit 5 = overlap mode
+                // (valid results: a tile's MMAs may run during the previous tile's exp phase)
     I8Consts ec;
 };
 
@@ -244,7 +245,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
     uint64_t* cd_empty = cd_full + NCD;
     uint64_t* g_full = cd_empty + NCD;
     uint64_t* g_empty = g_full + NGRP;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_empty + NGRP);
+    uint64_t* epi_done = g_empty + NGRP;  // the exp phase of a tile is over (MMA time-multiplexing)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int2 tile = A.tiles[blockIdx.x];
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
             tc::mbar_init(g_full + g, 1);
             tc::mbar_init(g_empty + g, NEPI);
         }
+        tc::mbar_init(epi_done, NEPI);
         tc::mbar_fence_init();
     }
     for (int i = tid; i < TAB * TAB_REP; i += NTHR) tab[i] = g_tab64[i / TAB_REP];
@@ -330,6 +333,12 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 // two bases plus compile-time offsets in the fully unrolled sequence.
                 const uint64_t dA0 = tc::smem_desc(aBase, 128, sbo);
                 const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB + s * C::B_BYTES), 128, sbo);
+                // Time-multiplexed with the epilogue: no MMA of this tile while the epilogue's
+                // FP64 exp phase of the previous tile runs.  Measured: INT8 MMAs throttle the
+                // FP64 pipe ~4x (probe) to ~8x (in situ), so FP64 work overlapped with MMAs is
+                // nearly wasted; serialising the exp phase is 6 % faster (d = 54 and 90).  The
+                // drain (TMEM loads, integer combination) still overlaps the MMAs.
+                if (!(A.debug & 32) && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
 #pragma unroll
                 for (int c = NGRP - 1; c >= 0; --c) {
                     if (bq > 0) {
@@ -449,7 +458,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 }
                 I8_TRACE(etid == 0, tq, 6);
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(cd_empty + cs);
+                if (lane == 0) {
+                    tc::mbar_arrive(cd_empty + cs);
+                    tc::mbar_arrive(epi_done);
+                }
                 epi_bar();
                 I8_TRACE(etid == 0, tq, 7);
                 if (etid < TJ) {
