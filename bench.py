@@ -326,8 +326,8 @@ def main():
                     "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2x bf16 on B200)"
                                    if "bf16_tflops" in peaks else "2 x 2.25 PF nominal bf16 (no MEASURED_PEAKS.json)",
                     "fp64_equivalent": fp64_view,
-                    "note": "FP64 epilogue and INT8 MMAs share SM execution resources and shared-memory "
-                            "bandwidth on B200 (profiles/README.md), so MMA and epilogue time add"}
+                    "note": "INT8 MMAs throttle the FP64 pipe ~4-8x on B200 (profiles/README.md), so the "
+                            "kernel time-multiplexes each SM: tensor-core phase, then the FP64 exp phase"}
     else:
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
                     "frac": achieved / peak_dmma, "traffic": traffic,
