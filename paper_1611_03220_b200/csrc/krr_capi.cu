@@ -92,6 +92,30 @@ struct DevMem {
     T* get() const { return p; }
 };
 
+// A set of CUDA events destroyed on scope exit (error paths included).
+struct Events {
+    std::vector<cudaEvent_t> e;
+    explicit Events(size_t n) : e(n, nullptr) {
+        try {
+            for (auto& x : e) KRR_CUDA(cudaEventCreate(&x));
+        } catch (...) {
+            release();
+            throw;
+        }
+    }
+    Events(const Events&) = delete;
+    Events& operator=(const Events&) = delete;
+    ~Events() { release(); }
+    void release() {
+        for (auto& x : e)
+            if (x) {
+                cudaEventDestroy(x);
+                x = nullptr;
+            }
+    }
+    cudaEvent_t operator[](size_t i) const { return e[i]; }
+};
+
 struct PinnedScalars {
     double* p = nullptr;
     explicit PinnedScalars(size_t count = 16) { KRR_CUDA(cudaMallocHost(&p, count * sizeof(double))); }
@@ -1494,8 +1518,7 @@ int krr_train(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const double*
         krr::set_data(c, X, n, d, krr::gaussian_spec(sigma));
         std::vector<double> W(static_cast<size_t>(s * d)), b(static_cast<size_t>(s));
         krr::rff_realize(master_seed, d, s, sigma, W.data(), b.data());
-        cudaEvent_t ev[4];
-        for (auto& e : ev) KRR_CUDA(cudaEventCreate(&e));
+        krr::Events ev(4);
         KRR_CUDA(cudaEventRecord(ev[0], c.stream));
         krr::rff_build(c, W.data(), b.data(), s);
         KRR_CUDA(cudaEventRecord(ev[1], c.stream));
@@ -1516,7 +1539,6 @@ int krr_train(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const double*
             phase_ms[2] = c3;
             phase_ms[3] = tot;
         }
-        for (auto& e : ev) cudaEventDestroy(e);
     });
 }
 
@@ -1549,40 +1571,6 @@ int krr_quality_test(krr_ctx* ctx, double lambda, krr_quality_report* out) {
         Ctx& c = *krr::as_ctx(ctx);
         krr::require_data(c);
         *out = krr::quality_test_dev(c, lambda);
-    });
-}
-
-int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0, int64_t s_max,
-                       uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
-                       int64_t* final_size, int* passed, int* jitter_used) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        krr::require_data(c);
-        if (s0 < 1) fail(KRR_ERR_INVALID_ARGUMENT, "adaptive_build: s0 must be at least 1");
-        if (s_max < s0) fail(KRR_ERR_INVALID_ARGUMENT, "adaptive_build: s_max must be >= s0");
-        const double lp = lambda_p > 0.0 ? lambda_p : lambda;
-        int64_t s = s0;
-        int nh = 0;
-        bool ok = false;
-        for (int attempt = 0;; ++attempt) {
-            const uint64_t seed = master_seed + uint64_t(attempt) * krr::kAttemptSeedStride;
-            std::vector<double> W(static_cast<size_t>(s * c.d)), b(static_cast<size_t>(s));
-            krr::rff_realize(seed, c.d, s, c.sigma, W.data(), b.data());
-            krr::rff_build(c, W.data(), b.data(), s);
-            const krr_quality_report rep = krr::quality_test_dev(c, lambda);
-            if (history && nh < max_history) history[nh] = rep;
-            ++nh;
-            if (final_size) *final_size = s;
-            if (rep.passed) {
-                ok = true;
-                break;
-            }
-            if (s >= s_max) break;
-            s = std::min(2 * s, s_max);
-        }
-        if (n_history) *n_history = nh;
-        if (passed) *passed = ok ? 1 : 0;
-        krr::precond_build(c, lp, jitter_used);
     });
 }
 
@@ -1628,8 +1616,7 @@ int krr_bench_matvec(krr_ctx* ctx, double lambda, int steps, double* total_ms, d
                                      cudaMemcpyHostToDevice, c.stream));
             c.sync();
         }
-        std::vector<cudaEvent_t> ev(size_t(2 * steps + 2));
-        for (auto& e : ev) KRR_CUDA(cudaEventCreate(&e));
+        krr::Events ev(size_t(2 * steps + 2));
         KRR_CUDA(cudaEventRecord(ev[0], c.stream));
         for (int k = 0; k < steps; ++k)
             krr::matvec_dev(c, c.vin.get(), c.vout.get(), lambda, ev[size_t(2 + 2 * k)],
@@ -1646,7 +1633,6 @@ int krr_bench_matvec(krr_ctx* ctx, double lambda, int steps, double* total_ms, d
         }
         *total_ms = tot;
         *k1_ms = k1 / steps;
-        for (auto& e : ev) cudaEventDestroy(e);
     });
 }
 
@@ -2115,8 +2101,7 @@ int krr_train_ex(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const doub
         krr::set_data(c, X, n, d, *kernel);
         krr::ChainOwned o;
         krr::realize_chain_host(c, *chain, master_seed, o);
-        cudaEvent_t ev[4];
-        for (auto& e : ev) KRR_CUDA(cudaEventCreate(&e));
+        krr::Events ev(4);
         KRR_CUDA(cudaEventRecord(ev[0], c.stream));
         krr::chain_build(c, o.t);
         KRR_CUDA(cudaEventRecord(ev[1], c.stream));
@@ -2136,7 +2121,6 @@ int krr_train_ex(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const doub
             phase_ms[2] = cc;
             phase_ms[3] = tot;
         }
-        for (auto& e : ev) cudaEventDestroy(e);
     });
 }
 
@@ -2147,6 +2131,18 @@ int krr_adaptive_build_ex(krr_ctx* ctx, const krr_chain_spec* chain_template, do
         if (!chain_template) fail(KRR_ERR_INVALID_ARGUMENT, "null chain spec");
         krr::adaptive_dev(*krr::as_ctx(ctx), *chain_template, lambda, lambda_p, s0, s_max, master_seed, history,
                           max_history, n_history, final_size, passed, jitter_used);
+    });
+}
+
+int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0, int64_t s_max,
+                       uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
+                       int64_t* final_size, int* passed, int* jitter_used) {
+    return guard([&] {
+        krr_chain_spec rff{};  // the RandomFourier single-stage template (scaled_to(s) gives s1 = s)
+        rff.first = 0;
+        rff.s1 = std::max<int64_t>(1, s0);
+        krr::adaptive_dev(*krr::as_ctx(ctx), rff, lambda, lambda_p, s0, s_max, master_seed, history, max_history,
+                          n_history, final_size, passed, jitter_used);
     });
 }
 
