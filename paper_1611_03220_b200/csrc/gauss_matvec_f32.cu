@@ -166,24 +166,26 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_f32_kernel(const F32Args
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_bf16(TI, TJ);
-            const uint32_t aBase = tc::smem_u32(sA);
-            int bq = 0;
-            for (int it = 0; it < nTI; ++it) {
-                tc::mbar_wait_sleep(a_full, uint32_t(it & 1));
+        // converged warp, one elect.sync lane issues (no per-MMA ELECT/R2UR waterfall loop; the
+        // same change made K1-I8 3 % faster, gauss_matvec_i8.cu)
+        constexpr uint32_t idesc = tc::idesc_bf16(TI, TJ);
+        const uint32_t aBase = tc::smem_u32(sA);
+        int bq = 0;
+        for (int it = 0; it < nTI; ++it) {
+            tc::mbar_wait_sleep(a_full, uint32_t(it & 1));
+            tc::fence_after();
+            for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
+                const int s = bq % NSTB, buf = bq % NACC;
+                if (bq >= NACC) tc::mbar_wait_sleep(t_empty + buf, uint32_t(((bq / NACC) - 1) & 1));
+                tc::mbar_wait_sleep(b_full + s, uint32_t((bq / NSTB) & 1));
                 tc::fence_after();
-                for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
-                    const int s = bq % NSTB, buf = bq % NACC;
-                    if (bq >= NACC) tc::mbar_wait_sleep(t_empty + buf, uint32_t(((bq / NACC) - 1) & 1));
-                    tc::mbar_wait_sleep(b_full + s, uint32_t((bq / NSTB) & 1));
-                    tc::fence_after();
-                    const uint64_t dA0 = tc::smem_desc(aBase, 128, sbo);
-                    const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB + s * C::B_BYTES), 128, sbo);
-                    const uint32_t d = tmem_base + uint32_t(buf * TJ);
-                    // small products first (fp32 accumulation), then the leading one
-                    constexpr int PP[6] = {2, 1, 0, 1, 0, 0};
-                    constexpr int QQ[6] = {0, 1, 2, 0, 1, 0};
+                const uint64_t dA0 = tc::smem_desc(aBase, 128, sbo);
+                const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB + s * C::B_BYTES), 128, sbo);
+                const uint32_t d = tmem_base + uint32_t(buf * TJ);
+                // small products first (fp32 accumulation), then the leading one
+                constexpr int PP[6] = {2, 1, 0, 1, 0, 0};
+                constexpr int QQ[6] = {0, 1, 2, 0, 1, 0};
+                if (tc::elect_one()) {
 #pragma unroll
                     for (int m = 0; m < 6; ++m)
 #pragma unroll
@@ -194,8 +196,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_f32_kernel(const F32Args
                     tc::mma_commit(b_empty + s);
                     tc::mma_commit(t_full + buf);
                 }
-                tc::mma_commit(a_empty);
+                __syncwarp();
             }
+            if (tc::elect_one()) tc::mma_commit(a_empty);
+            __syncwarp();
         }
     } else {
         // ------------------------------------------------------------ epilogue
