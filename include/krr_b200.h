@@ -76,7 +76,7 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
 
 /* Tuning / diagnostic knobs (no reference equivalent):
  *   "k1_path"     -1|0|1  fused mat-vec kernel: auto (default: INT8-slice tensor-core kernel
- *                         for d >= 48 when the data's exponent range allows, else FP64 DMMA) |
+ *                         where faster: 27 <= d <= 32, 44 <= d <= 96, when the data's exponent range allows, else FP64 DMMA) |
  *                         FP64 DMMA | tcgen05 INT8 slices
  *   "k1_resident" 1|0  keep the column tile of the DMMA mat-vec in shared memory (default 1)
  *   "k1_warps" 8|16, "k1_grouped" 1|0  DMMA mat-vec shape (defaults 8, 1)

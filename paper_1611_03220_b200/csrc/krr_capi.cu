@@ -215,7 +215,11 @@ void allreduce_sum(Ctx& c, double* buf, int64_t count) {
 bool use_i8(const Ctx& c) {
     if (!c.i8_ready || c.family != 0) return false;
     if (c.k1_path >= 0) return c.k1_path == 1;
-    return c.d >= 48;
+    // Cost model from the measured crossover (n = 65536, profiles/r1_k1_crossover_n65536.log):
+    // the DMMA K1 grows ~linearly in d, K1-I8 steps with the slice width kp = 32 / 64 / 96.
+    const double dmma_ms = 4.40 + 0.1405 * double(c.d);
+    const double i8_ms = c.kp8 <= 32 ? 8.04 : (c.kp8 <= 64 ? 10.43 : 11.9);
+    return i8_ms < dmma_ms;
 }
 
 void f32_ensure(Ctx& c) {
