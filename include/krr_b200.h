@@ -83,6 +83,8 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
  *   "batched_rhs" 1|0  multi-RHS solves / mat-mats through the batched kernel (default 1)
  *   "exp_mode"    1|0  table exp (default) | libdevice exp in the Gaussian epilogue
  *   "i8_debug"    bits  profiling only (K1-I8: 1 skip MMAs, 2 skip exp, 4 clock trace)
+ *   "pcg_graph"   1|0  single-RHS device PCG as one CUDA graph (conditional WHILE node, device-side
+ *                         stop / breakdown decision; default 1) | host-driven loop; same iterates
  *   "emulate_world" W, "emulate_rank" r   test only, single-rank contexts: the next
  *                         krr_set_data builds rank r of W's K1 schedule (tiles, owned slots,
  *                         diagonal on rank 0) with no collective, so K v returns that rank's

@@ -588,6 +588,7 @@ int i8_kp(int64_t d) { return int((d + 31) / 32 * 32); }
 
 bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp,
                        double kscale, uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream) {
+    ensure_table(stream);  // here (it synchronises once) so graph-captured launches never need to
     const int kp = i8_kp(d);
     const double ks = i8_kscale(kscale);
     const unsigned wblocks = unsigned(std::min<int64_t>((n_pad + 7) / 8, 148 * 16));

@@ -108,6 +108,11 @@ void pcg_update_xr_launch(const double* pap_part, int nb, const double* rz, doub
 void pcg_update_p_launch(const double* rz_part, int nb, const double* rz_old, double* rz_out,
                          double* p, const double* z, int64_t n, cudaStream_t stream);
 void copy_launch(double* dst, const double* src, int64_t n, cudaStream_t stream);
+// Graph-resident PCG loop (krr_capi.cu pcg_graph): the device-side stop decision and the
+// rz double-buffer copy.
+void pcg_control_launch(const double* scal, int* ctl, double* hist, double* final_rel, double norm_y, double tau,
+                        int max_iter, cudaGraphConditionalHandle cond, cudaStream_t stream);
+void scalar_copy_launch(double* dst, const double* src, cudaStream_t stream);
 // Gather column c of an n x t row-major matrix into a contiguous vector (and back).
 void gather_col_launch(const double* M, int64_t n, int64_t t, int64_t c, double* out,
                        cudaStream_t stream);

@@ -185,6 +185,11 @@ struct Ctx {
 
     // batched multi-RHS state (n_pad x T interleaved blocks)
     bool batched = true;
+    // single-RHS PCG with device operators runs as one CUDA graph: a conditional WHILE node whose
+    // body is one iteration and a device-side stop decision (no host round trip per iteration)
+    bool pcg_graph = true;
+    DevMem<int> ctl;
+    DevMem<double> dhist;
     DevMem<double> bx, br, bz, bp, bap, by, bin, bout, bpart, bred, bscal, bW, bY;
     DevMem<int> bactive;
     std::unique_ptr<PinnedScalars> hscalT;
@@ -527,8 +532,88 @@ struct PcgOut {
 
 // Vectors live in c.vx/vr/vz/vp/vap (length >= n, zero beyond n).  y is a device
 // vector of length n (zero-padded to the buffer length).  The solution is left in c.vx.
+// The graph-resident PCG loop: the same kernels in the same order as pcg_core's host loop
+// (bitwise-identical iterates), captured once into the body of a conditional WHILE node; a
+// one-thread control kernel makes solver.cpp:37-52's stop / breakdown decision on the device.
+// Single rank, no host observer.  Precondition: the caller ran the prologue (x = 0, r = y,
+// z = M r, p = z, scal[2] = r'z) and norm_y > 0.
+void pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double norm_y, double tau, int max_iter,
+                    double* hist, PcgOut& out) {
+    if (c.precision == 32) f32_ensure(c);  // one-off preparation synchronises: not inside the capture
+    const int nb = vec_blocks(n);
+    double* red = c.red.get();
+    double* pap_part = red;
+    double* rr_part = red + 1024;
+    double* rz_part = red + 2048;
+    double* scal = c.scal.get();
+    c.ctl.ensure(4);
+    c.dhist.ensure(size_t(std::max(1, max_iter)));
+    KRR_CUDA(cudaMemsetAsync(c.ctl.get(), 0, 4 * sizeof(int), c.stream));
+    double* z = M ? c.vz.get() : c.vr.get();
+
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    struct Cleanup {
+        cudaGraph_t& g;
+        cudaGraphExec_t& e;
+        ~Cleanup() {
+            if (e) cudaGraphExecDestroy(e);
+            if (g) cudaGraphDestroy(g);
+        }
+    } cleanup{g, exec};
+    KRR_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle cond;
+    KRR_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    KRR_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    KRR_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    try {
+        A(c.vp.get(), c.vap.get());
+        dot_partial_launch(c.vp.get(), c.vap.get(), n, pap_part, nb, c.stream);
+        pcg_update_xr_launch(pap_part, nb, scal + 2, c.vx.get(), c.vr.get(), c.vp.get(), c.vap.get(), n, rr_part,
+                             scal, c.stream);
+        sum_partials_launch(rr_part, nb, scal + 4, c.stream);
+        pcg_control_launch(scal, c.ctl.get(), c.dhist.get(), scal + 6, norm_y, tau, max_iter, cond, c.stream);
+        // (after a stop the rest of the body still runs once; it touches only z, p and r'z)
+        if (M) (*M)(c.vr.get(), z);
+        dot_partial_launch(c.vr.get(), z, n, rz_part, nb, c.stream);
+        pcg_update_p_launch(rz_part, nb, scal + 2, scal + 3, c.vp.get(), z, n, c.stream);
+        scalar_copy_launch(scal + 2, scal + 3, c.stream);
+    } catch (...) {
+        cudaGraph_t dummy = nullptr;
+        cudaStreamEndCapture(c.stream, &dummy);
+        throw;
+    }
+    KRR_CUDA(cudaStreamEndCapture(c.stream, &body));
+    KRR_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    KRR_CUDA(cudaGraphLaunch(exec, c.stream));
+    int hctl[4];
+    double* hs = c.hscal->p;
+    KRR_CUDA(cudaMemcpyAsync(hctl, c.ctl.get(), sizeof(hctl), cudaMemcpyDeviceToHost, c.stream));
+    KRR_CUDA(cudaMemcpyAsync(hs + 6, scal + 6, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const int its = hctl[0];
+    if (hist && its > 0) {
+        KRR_CUDA(cudaMemcpyAsync(hist, c.dhist.get(), sizeof(double) * size_t(hctl[1] == 3 ? its - 1 : its),
+                                 cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    }
+    if (hctl[1] == 3) fail(KRR_ERR_BREAKDOWN, "pcg_solve: p'Ap <= 0, operator is not positive definite");
+    out.iterations = its;
+    out.final_residual = hs[6];
+    out.converged = hctl[1] == 1 ? 1 : 0;
+}
+
+// device_ops: A and M only enqueue device work on c.stream (no host callbacks, no host
+// synchronisation) — the precondition for the graph-resident loop.
 PcgOut pcg_core(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, const double* y, double tau,
-                int max_iter, double* hist, const HostObserver* obs) {
+                int max_iter, double* hist, const HostObserver* obs, bool device_ops) {
     if (!(tau > 0.0)) fail(KRR_ERR_INVALID_ARGUMENT, "pcg_solve: tau must be positive");
     if (max_iter < 1) fail(KRR_ERR_INVALID_ARGUMENT, "pcg_solve: max_iter must be at least 1");
     const int nb = vec_blocks(n);
@@ -559,6 +644,10 @@ PcgOut pcg_core(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, const double*
     copy_launch(c.vp.get(), z, n, c.stream);  // p = z
     dot_partial_launch(c.vr.get(), z, n, rz_part, nb, c.stream);
     sum_partials_launch(rz_part, nb, scal + 2, c.stream);
+    if (device_ops && c.pcg_graph && !obs && c.world == 1) {
+        pcg_graph_loop(c, n, A, M, norm_y, tau, max_iter, hist, out);
+        return out;
+    }
     int cur = 0;
     for (int it = 1; it <= max_iter; ++it) {
         A(c.vp.get(), c.vap.get());
@@ -950,7 +1039,7 @@ void solve_gaussian(Ctx& c, double lambda, const double* Y, int64_t t, double ta
             KRR_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(double) * v->count, c.stream));
         gather_col_launch(c.mat_a.get(), n, t, j, c.vy.get(), c.stream);
         const PcgOut o = pcg_core(c, n, A, use_precond ? &M : nullptr, c.vy.get(), tau, max_iter,
-                                  hist ? hist + j * max_iter : nullptr, nullptr);
+                                  hist ? hist + j * max_iter : nullptr, nullptr, true);
         scatter_col_launch(c.vx.get(), n, t, j, c.mat_b.get(), c.stream);
         stats[j].iterations = o.iterations;
         stats[j].converged = o.converged;
@@ -1112,6 +1201,8 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
             c.batched = value != 0.0;
         } else if (k == "exp_mode") {
             c.exp_mode = value != 0.0 ? 1 : 0;
+        } else if (k == "pcg_graph") {
+            c.pcg_graph = value != 0.0;
         } else if (k == "emulate_world" || k == "emulate_rank") {
             if (c.world != 1) fail(KRR_ERR_STATE, "rank emulation is for single-rank contexts");
             const int iv = int(value);
@@ -1151,6 +1242,8 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
             *value = c.exp_mode;
         } else if (k == "batched_rhs") {
             *value = c.batched ? 1.0 : 0.0;
+        } else if (k == "pcg_graph") {
+            *value = c.pcg_graph ? 1.0 : 0.0;
         } else if (k == "emulate_world") {
             *value = c.emu_world;
         } else if (k == "emulate_rank") {
@@ -1499,7 +1592,7 @@ int krr_pcg_solve_operator(krr_ctx* ctx, int64_t n, krr_operator_cb apply_a, voi
         KRR_CUDA(cudaMemcpyAsync(c.vy.get(), y, sizeof(double) * size_t(n), cudaMemcpyHostToDevice,
                                  c.stream));
         const krr::PcgOut o = krr::pcg_core(c, n, A, apply_m ? &M : nullptr, c.vy.get(), tau, max_iter,
-                                            residual_history, observer ? &obs : nullptr);
+                                            residual_history, observer ? &obs : nullptr, false);
         KRR_CUDA(cudaMemcpyAsync(x, c.vx.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
                                  c.stream));
         c.sync();

@@ -116,6 +116,36 @@ __global__ void pcg_update_p_kernel(const double* __restrict__ rz_part, int nb,
         p[i] = z[i] + beta * p[i];
 }
 
+// Device-side PCG control for the graph-resident loop (one thread): the stop/breakdown
+// decisions solver.cpp:37-52 makes on the host, from the scalars the iteration left in scal.
+// ctl: [0] iterations so far, [1] status (0 running, 1 converged, 2 max_iter, 3 breakdown).
+__global__ void pcg_control_kernel(const double* __restrict__ scal, int* __restrict__ ctl,
+                                   double* __restrict__ hist, double* __restrict__ final_rel, double norm_y,
+                                   double tau, int max_iter, cudaGraphConditionalHandle cond) {
+    const int it = ctl[0] + 1;
+    ctl[0] = it;
+    const double pap = scal[0];
+    if (!(pap > 0.0)) {
+        ctl[1] = 3;
+        cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    const double rel = sqrt(scal[4]) / norm_y;
+    hist[it - 1] = rel;
+    *final_rel = rel;
+    if (rel <= tau) {
+        ctl[1] = 1;
+        cudaGraphSetConditional(cond, 0);
+    } else if (it >= max_iter) {
+        ctl[1] = 2;
+        cudaGraphSetConditional(cond, 0);
+    } else {
+        cudaGraphSetConditional(cond, 1);
+    }
+}
+
+__global__ void scalar_copy_kernel(double* __restrict__ dst, const double* __restrict__ src) { *dst = *src; }
+
 __global__ void copy_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -341,6 +371,17 @@ void pcg_update_xr_launch(const double* pap_part, int nb, const double* rz, doub
 void pcg_update_p_launch(const double* rz_part, int nb, const double* rz_old, double* rz_out,
                          double* p, const double* z, int64_t n, cudaStream_t stream) {
     pcg_update_p_kernel<<<nb, kVecThreads, 0, stream>>>(rz_part, nb, rz_old, rz_out, p, z, n);
+    KRR_LAUNCH_CHECK();
+}
+
+void pcg_control_launch(const double* scal, int* ctl, double* hist, double* final_rel, double norm_y, double tau,
+                        int max_iter, cudaGraphConditionalHandle cond, cudaStream_t stream) {
+    pcg_control_kernel<<<1, 1, 0, stream>>>(scal, ctl, hist, final_rel, norm_y, tau, max_iter, cond);
+    KRR_LAUNCH_CHECK();
+}
+
+void scalar_copy_launch(double* dst, const double* src, cudaStream_t stream) {
+    scalar_copy_kernel<<<1, 1, 0, stream>>>(dst, src);
     KRR_LAUNCH_CHECK();
 }
 

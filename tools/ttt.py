@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--oracle-iters", type=int, default=0)
     ap.add_argument("--n", type=int, default=0, help="override n (sub-sampled config)")
     ap.add_argument("--precision", type=int, default=64, help="64 (fp64, default) or 32 (optional fp32 mode)")
+    ap.add_argument("--pcg-graph", type=int, default=1, help="1: graph-resident PCG loop (default), 0: host loop")
     args = ap.parse_args()
     od = ROOT / "gpurun_out"
     od.mkdir(exist_ok=True)
@@ -42,6 +43,7 @@ def main():
                               chain=krr.ChainSpec(s1=s), seed=0)
         ctx = krr.Context(0)
         ctx.set_precision(args.precision)
+        ctx.set_option("pcg_graph", args.pcg_graph)
         res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), sc, ctx=ctx)
         out = {"config": cfg, "precision": args.precision, "n": n, "d": d, "t": t, "sigma": sigma, "lambda": lam, "s": s,
                "tau": args.tau, "max_iter": args.max_iter, "gen_s": gen_s,
@@ -70,7 +72,8 @@ def main():
         print(json.dumps({k2: v for k2, v in out.items() if k2 != "per_rhs"}), flush=True)
         print(json.dumps({"iterations": [r["iterations"] for r in out["per_rhs"]],
                           "final_residual": [r["final_residual"] for r in out["per_rhs"]]}), flush=True)
-        tag = ("_n" + str(n) if args.n else "") + ("_fp32" if args.precision == 32 else "")
+        tag = ("_n" + str(n) if args.n else "") + ("_fp32" if args.precision == 32 else "") + \
+            ("_hostloop" if not args.pcg_graph else "")
         (od / f"ttt_{cfg}{tag}.json").write_text(json.dumps(out, indent=1))
 
 
