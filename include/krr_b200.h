@@ -204,8 +204,9 @@ typedef struct krr_kernel_spec {
  * contract the augmented inputs [sqrt(gamma) x, sqrt(offset)] (kernels.cpp:56-62) on the
  * FP64 tensor path and raise p_ij to the degree in the epilogue (ipow, kernels.cpp:10-14);
  * K_ii = ipow(|xa_i|^2) is applied by the finish kernel (kernels.cpp:89-99 keeps the
- * diagonal, unlike the Gaussian K_ii = 1).  The INT8 / fp32 K1 paths serve the Gaussian
- * kernel only (polynomial: K1 is always the DMMA kernel; precision 32 is rejected). */
+ * diagonal, unlike the Gaussian K_ii = 1).  The polynomial kernel runs on the DMMA K1 or on
+ * K1-I8 (INT8 slices, p = gamma x.z + c formed in the epilogue; auto for d >= 55); the fp32
+ * mode is Gaussian-only (precision 32 is rejected). */
 int krr_set_data_kernel(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const krr_kernel_spec* kernel);
 
 /* ChainSpec (sketches.hpp:96-107): first 0 = RandomFourier (Gaussian kernel), 1 =

@@ -104,8 +104,10 @@ struct Cfg {
 };
 
 struct I8Consts {
-    double kabs;                // |kscale| = scale 64 / ln2
-    double a1, a2, a3, a4, a5;  // (ln2/64)^m / m!
+    double kabs;                // |kscale| = scale 64 / ln2 (polynomial kernel: gamma)
+    double a1, a2, a3, a4, a5;  // (ln2/64)^m / m!      (polynomial kernel: a1 = offset c)
+    int degree;                 // polynomial kernel only
+    int pad_;
 };
 
 struct I8Args {
@@ -142,11 +144,12 @@ __device__ __forceinline__ double magic_pack(int32_t a, int32_t b) {
 // 1.5 * 2^52 + 2^31 and that constant times (1 + 2^-28), both exact integers < 2^53
 constexpr double M2 = 6755401588539392.0 + 25165832.0;  // M1 = 1.5 * 2^52 + 2^31, M2 = M1 (1 + 2^-28)
 
-template <bool MASK, bool CHEAP = false>
+template <bool MASK, bool CHEAP = false, bool POLY = false>
 __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts& ec, const double* __restrict__ tab,
                                           const double* __restrict__ cd_sq, const double* __restrict__ cd_v,
                                           const int* __restrict__ cd_e, double* __restrict__ scr,
-                                          double* __restrict__ colscr_q, int nsi_hi, int nsi_lo, double sqs_i,
+                                          double* __restrict__ colscr_q, long long* __restrict__ tr,
+                                          int nsi_hi, int nsi_lo, double sqs_i,
                                           double v_i, double& rowacc, int lane, int colOff, int mask_row) {
     const double shifter = 6755399441055744.0;  // 1.5 * 2^52
     double racc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -157,6 +160,27 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
     for (int k0 = 0; k0 < CPT; k0 += BW) {
         double y[BW], t2[BW], f[BW], q[BW], e[BW];
         int kk[BW];
+        if constexpr (POLY) {
+            // polynomial kernel: p = gamma x_i.x_j + c = fma(T, gamma 2^(e_i+e_j-35), c),
+            // then ipow(p, q) as r = p, r *= p (kernels.cpp:10-14), degree-outer across the batch
+#pragma unroll
+            for (int b = 0; b < BW; ++b) {
+                const int cl = colOff + k0 + b;
+                const double nscale = __hiloint2double(nsi_hi + cd_e[cl], nsi_lo);
+                y[b] = fma(T[k0 + b], nscale, ec.a1);
+                e[b] = y[b];
+            }
+            for (int r = 1; r < ec.degree; ++r)
+#pragma unroll
+                for (int b = 0; b < BW; ++b) e[b] = __dmul_rn(e[b], y[b]);
+#pragma unroll
+            for (int b = 0; b < BW; ++b) {
+                if constexpr (MASK) e[b] = (colOff + k0 + b > mask_row) ? e[b] : 0.0;
+                racc[b] = fma(e[b], cd_v[colOff + k0 + b], racc[b]);
+                scr[(k0 + b) * SCR_LD + lane] = e[b] * v_i;
+            }
+            continue;
+        }
 #pragma unroll
         for (int b = 0; b < BW; ++b) {
             const int cl = colOff + k0 + b;
@@ -202,6 +226,7 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
             scr[(k0 + b) * SCR_LD + lane] = e[b] * v_i;  // column k, row `lane`
         }
     }
+    if (tr) tr[13] = clock64();  // profiling trace: element loop done
     rowacc += (racc[0] + racc[1]) + (racc[2] + racc[3]);
     // column sums over the warp's 32 rows: lane L sums column L % CPT over rows
     // (L / CPT) * RPL .. + RPL in 4 chains, then a butterfly over the row blocks (fixed order)
@@ -219,11 +244,12 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
     double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = CPT; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (tr) tr[14] = clock64();  // column sums done
     if (lane < CPT) colscr_q[colOff + lane] = acc;
     __syncwarp();
 }
 
-template <int KPT>
+template <int KPT, bool POLY>
 __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A) {
     using C = Cfg<KPT>;
     constexpr int kp = KPT;
@@ -381,7 +407,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
             const int64_t gi = rowBase + int64_t(it) * TI + row;
             const double sqs_i = A.sqs[gi];
             const double v_i = A.v[gi];
-            const int nsi_hi = kabs_hi + (A.ex[gi] - 34) * (1 << 20);  // |kscale| 2^(e_i - 34)
+            // |kscale| 2^(e_i - 34) (Gaussian) | gamma 2^(e_i - 35) (polynomial: x.x = 2^(e_i+e_j-35) T)
+            const int nsi_hi = kabs_hi + (A.ex[gi] - (POLY ? 35 : 34)) * (1 << 20);
             double rowacc = 0.0;
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++tq) {
                 const uint32_t ph = uint32_t(tq & 1);
@@ -397,17 +424,14 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 double lo[CPT], T[CPT];
                 auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
                     tc::mbar_wait_sleep(g_full + ca + 1, ph);
-                    I8_TRACE(etid == 0 && ca == 0, tq, 15);
                     tc::mbar_wait_sleep(g_full + ca, ph);
                     tc::fence_after();
-                    I8_TRACE(etid == 0 && ca == 0, tq, 13);
                     // all loads of the stage in flight before one wait (TMEM load latency
                     // under load is ~250 clk; one round trip per stage, not per 8 columns)
                     uint32_t gl[CPT], gh[CPT];
                     tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ), gl);
                     tc::tmem_ld16(taddr + uint32_t(ca * TJ), gh);
                     tc::tmem_wait_ld();
-                    I8_TRACE(etid == 0 && ca == 0, tq, 14);
 #pragma unroll
                     for (int k = 0; k < CPT; ++k) fn(k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
                     tc::fence_before();
@@ -439,6 +463,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 double* colscr_q = colscr + ((tq & 1) * 4 + quarter) * TJ;
                 const int colOff = half * CPT;
                 const bool masked = diag && jt < (it + 1) * (TI / TJ);
+                long long* trp = ((A.debug & 4) && blockIdx.x == 0 && etid == 0 && tq < TRACE_TILES)
+                                     ? g_trace + tq * 16 : nullptr;
                 if (A.debug & 2) {
                     double z = 0.0;
 #pragma unroll
@@ -447,13 +473,13 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 } else if (masked) {
                     // diagonal block: keep j > i (local column index vs local row index)
                     const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
-                    exp_phase<true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
+                    exp_phase<true, false, POLY>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
                                          rowacc, lane, colOff, mask_row);
                 } else if (A.debug & 16) {
-                    exp_phase<false, true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i,
+                    exp_phase<false, true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i,
                                            v_i, rowacc, lane, colOff, 0);
                 } else {
-                    exp_phase<false>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, nsi_hi, kabs_lo, sqs_i, v_i,
+                    exp_phase<false, false, POLY>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
                                           rowacc, lane, colOff, 0);
                 }
                 I8_TRACE(etid == 0, tq, 6);
@@ -546,13 +572,13 @@ __global__ void scaled_sq_kernel(const double* __restrict__ L, int64_t n_pad, in
         sqs[i] = kscale * L[i * dp + d];
 }
 
-template <int KPT>
+template <int KPT, bool POLY>
 void launch_kp(const I8Args& a, int64_t num_tiles, cudaStream_t stream) {
     constexpr size_t smem = Cfg<KPT>::SMEM;
     static_assert(smem <= 227 * 1024, "K1-I8 shared memory");
-    KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_i8_kernel<KPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KRR_CUDA(cudaFuncSetAttribute(gauss_matvec_i8_kernel<KPT, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
-    gauss_matvec_i8_kernel<KPT><<<unsigned(num_tiles), NTHR, smem, stream>>>(a);
+    gauss_matvec_i8_kernel<KPT, POLY><<<unsigned(num_tiles), NTHR, smem, stream>>>(a);
 }
 
 // kscale of the 1/64-octave table exp (the K1 constant, -scale 64 / ln2)
@@ -587,7 +613,8 @@ bool i8_supported(int64_t d, int st) {
 int i8_kp(int64_t d) { return int((d + 31) / 32 * 32); }
 
 bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp,
-                       double kscale, uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream) {
+                       double kscale, uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream,
+                       double poly_gamma) {
     ensure_table(stream);  // here (it synchronises once) so graph-captured launches never need to
     const int kp = i8_kp(d);
     const double ks = i8_kscale(kscale);
@@ -611,6 +638,10 @@ bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, con
         lo = std::min(lo, e);
         hi = std::max(hi, e);
     }
+    if (poly_gamma > 0.0) {  // polynomial kernel: gamma 2^(e_i + e_j - 35) must be a normal double
+        const int eg = std::ilogb(poly_gamma);
+        return eg + 2 * lo - 35 > -1000 && eg + 2 * hi - 35 < 1000;
+    }
     const int ek = std::ilogb(-ks);
     const double ymax = -ks * 4.0 * double(d) * std::ldexp(1.0, 2 * hi);
     return ek + 2 * lo - 34 > -1000 && ek + 2 * hi - 34 < 1000 && ymax < std::ldexp(1.0, 50);
@@ -618,7 +649,7 @@ bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, con
 
 void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const int* ejs,
                             const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
-                            int debug) {
+                            int debug, int poly_degree, double poly_gamma, double poly_offset) {
     if (p.num_tiles == 0) return;
     ensure_table(stream);
     I8Args a;
@@ -646,9 +677,17 @@ void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const in
     a.ec.a3 = c[3];
     a.ec.a4 = c[4];
     a.ec.a5 = c[5];
-    if (kp == 32) launch_kp<32>(a, p.num_tiles, stream);
-    else if (kp == 64) launch_kp<64>(a, p.num_tiles, stream);
-    else if (kp == 96) launch_kp<96>(a, p.num_tiles, stream);
+    a.ec.degree = 0;
+    a.ec.pad_ = 0;
+    const bool poly = poly_degree > 0;
+    if (poly) {  // polynomial kernel: gamma, offset, degree in the constants (8f4)
+        a.ec.kabs = poly_gamma;
+        a.ec.a1 = poly_offset;
+        a.ec.degree = poly_degree;
+    }
+    if (kp == 32) poly ? launch_kp<32, true>(a, p.num_tiles, stream) : launch_kp<32, false>(a, p.num_tiles, stream);
+    else if (kp == 64) poly ? launch_kp<64, true>(a, p.num_tiles, stream) : launch_kp<64, false>(a, p.num_tiles, stream);
+    else if (kp == 96) poly ? launch_kp<96, true>(a, p.num_tiles, stream) : launch_kp<96, false>(a, p.num_tiles, stream);
     else fail(KRR_ERR_INVALID_ARGUMENT, "K1-I8: kp must be 32, 64 or 96");
     KRR_LAUNCH_CHECK();
 }

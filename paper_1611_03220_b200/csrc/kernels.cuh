@@ -55,11 +55,14 @@ int i8_kp(int64_t d);
 // Builds the slices S, row exponents ex (and ex << 20), sq' = kscale' |x|^2 (kscale' of the
 // 1/256-octave exp); returns false when the data's exponent range would leave the range
 // the fused epilogue handles.
+// poly_gamma > 0: prepare for the polynomial kernel (the sq' terms are unused).
 bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp,
-                       double kscale, uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream);
+                       double kscale, uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream,
+                       double poly_gamma = 0.0);
+// poly_degree > 0: the polynomial kernel's epilogue (p = gamma x.z + offset, ipow) instead of exp.
 void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const int* ejs,
                             const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
-                            int debug = 0);
+                            int debug = 0, int poly_degree = 0, double poly_gamma = 0.0, double poly_offset = 0.0);
 
 // Build L / R operands from X (n x d) on the device; rows >= n and cols >= d+2 zeroed.
 void build_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, int dp,

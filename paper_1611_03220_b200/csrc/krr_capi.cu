@@ -218,8 +218,13 @@ void allreduce_sum(Ctx& c, double* buf, int64_t count) {
 // DMMA kernel on B200 (measured: d >= ~48, profiles/README.md) and the data's exponent range
 // allows it; the DMMA kernel otherwise.  Both are GPU kernels; neither is a fallback.
 bool use_i8(const Ctx& c) {
-    if (!c.i8_ready || c.family != 0) return false;
+    if (!c.i8_ready) return false;
     if (c.k1_path >= 0) return c.k1_path == 1;
+    if (c.family != 0) {  // polynomial kernel (cheaper epilogue): profiles/r1_poly_k1_crossover_n65536.log
+        const double dmma_ms = 2.1 + 0.14 * double(c.d);
+        const double i8_ms = c.kp8 <= 32 ? 7.49 : (c.kp8 <= 64 ? 9.74 : 11.4);
+        return i8_ms < dmma_ms;
+    }
     // Cost model from the measured crossover (n = 65536, profiles/r1_k1_crossover_n65536.log):
     // the DMMA K1 grows ~linearly in d, K1-I8 steps with the slice width kp = 32 / 64 / 96.
     const double dmma_ms = 4.40 + 0.1405 * double(c.d);
@@ -251,7 +256,7 @@ void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t
                                 c.stream);
     else if (use_i8(c))
         gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.ejs8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
-                               c.stream, c.i8_debug);
+                               c.stream, c.i8_debug, c.family == 1 ? c.degree : 0, c.gamma, c.offset);
     else
         gauss_matvec_launch(c.plan, v, c.part.get(), c.family == 1 ? poly_mode(c.degree) : c.exp_mode, c.stream);
     if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
@@ -347,14 +352,15 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_sp
     p.kdiag = c.family == 1 ? c.kdiag.get() : nullptr;
     c.i8_ready = false;
     c.f32_ready = false;
-    if (c.family == 0 && i8_supported(d, int(c.sched.st))) {
+    if (i8_supported(d, int(c.sched.st))) {
         c.kp8 = i8_kp(d);
         c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
         c.ex8.ensure(size_t(n_pad));
         c.ejs8.ensure(size_t(n_pad));
         c.sq8.ensure(size_t(n_pad));
-        c.i8_ready = i8_prepare_launch(c.X.get(), n, d, n_pad, c.L.get(), dp, p.ec.kscale, c.S8.get(), c.ex8.get(),
-                                       c.ejs8.get(), c.sq8.get(), c.stream);
+        c.i8_ready = i8_prepare_launch(c.X.get(), n, d, n_pad, c.L.get(), dp,
+                                       c.family == 0 ? p.ec.kscale : -1.0, c.S8.get(), c.ex8.get(), c.ejs8.get(),
+                                       c.sq8.get(), c.stream, c.family == 1 ? c.gamma : 0.0);
     }
     p.resident = c.k1_resident;
     p.warps16 = c.k1_warps16;

@@ -309,3 +309,26 @@ def test_poly_degree_one_is_linear_kernel(krr, oracle, ctx):
     got = krr.KernelOperator(x, _pk(krr, 0.5, 2.0, 1), 0.0, ctx=ctx)(v)
     want = (0.5 * x @ x.T + 2.0) @ v
     assert rel(got, want) <= 1e-13
+
+
+@pytest.mark.parametrize("n,d,g,c,q", [(700, 9, 0.3, 0.5, 2), (1300, 54, 0.02, 1.0, 3), (2000, 90, 0.01, 0.2, 4),
+                                       (500, 33, 0.1, 0.0, 1), (900, 64, 0.05, 0.7, 6)])
+def test_poly_matvec_on_int8_tensor_cores(krr, oracle, ctx, n, d, g, c, q):
+    """The polynomial kernel through K1-I8 (tcgen05 INT8 slices; p = gamma 2^(e_i+e_j-35) T + c,
+    then ipow) and through the DMMA K1: both match the oracle and each other."""
+    x = oracle.random_matrix(n, d, 13)
+    v = oracle.random_vector(n, 14)
+    k = oracle.poly_gram(x, g, c, q)
+    want = k @ v + 0.5 * v
+    scale = np.abs(k) @ np.abs(v) + 0.5 * np.abs(v)
+    got = {}
+    for path in (1, 0):
+        ctx.set_option("k1_path", path)
+        try:
+            op = krr.KernelOperator(x, _pk(krr, g, c, q), 0.5, ctx=ctx)
+            assert ctx.get_option("k1_path_effective") == path
+            got[path] = op(v)
+        finally:
+            ctx.set_option("k1_path", -1)
+        assert np.max(np.abs(got[path] - want) / scale) <= 1e-12 * q, (path, np.max(np.abs(got[path] - want) / scale))
+    assert np.max(np.abs(got[1] - got[0]) / scale) <= 2e-12 * q

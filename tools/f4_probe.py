@@ -52,7 +52,8 @@ def main():
     x = rng.normal(size=(n, d)) / np.sqrt(d)
     poly = krr.KernelSpec.polynomial(1.0 / d, 1.0, 3)
     for kern, path in [(krr.KernelSpec.gaussian(1.0), 0), (krr.KernelSpec.gaussian(1.0), -1), (poly, -1),
-                       (krr.KernelSpec.polynomial(1.0 / d, 1.0, 2), -1), (krr.KernelSpec.polynomial(1.0 / d, 1.0, 6), -1)]:
+                       (krr.KernelSpec.polynomial(1.0 / d, 1.0, 2), -1), (krr.KernelSpec.polynomial(1.0 / d, 1.0, 6), -1),
+                       (poly, 0), (krr.KernelSpec.polynomial(1.0 / d, 1.0, 6), 0)]:
         r = bench_matvec(ctx, x, kern, args.steps, path)
         rows.append(r)
         print(json.dumps(r), flush=True)

@@ -1,6 +1,6 @@
 """K1-I8 per-tile timeline of CTA 0 (clock64 stamps; i8_debug bit 2).
 
-python tools/i8_trace.py [n] [d] [extra debug bits]
+python tools/i8_trace.py [n] [d] [extra debug bits] [poly]
 """
 import ctypes as C
 import sys
@@ -15,9 +15,13 @@ from paper_1611_03220_b200 import _lib  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 90
 extra = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+poly = len(sys.argv) > 4 and sys.argv[4] == "poly"
 ctx = krr.Context(0)
 x = np.random.default_rng(0).standard_normal((n, d))
-_lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, 6.0))
+if poly:  # the polynomial kernel's epilogue (no exp) on the same K1-I8 skeleton
+    krr._set_data(ctx, x, krr.KernelSpec.polynomial(1.0 / d, 1.0, 3))
+else:
+    _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, 6.0))
 ctx.set_option("k1_path", 1)
 tot, k1 = C.c_double(), C.c_double()
 _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))
@@ -28,7 +32,7 @@ _lib.check(_lib.LIB.krr_debug_i8_trace(ctx.handle, buf.ctypes.data_as(C.c_void_p
 t = buf.reshape(64, 16)
 t0 = t[0, 0]
 names = ["start", "st6", "st4", "st2", "st0", "cd", "exp", "bar", "m:bfull?", "m:bfull", "m:g7", "m:g4", "m:g0",
-         "g0full", "g0ld", "g1full"]
+         "elem", "colsum", "-"]
 print("tile " + " ".join(f"{nm:>8s}" for nm in names))
 for q in range(1, 40):
     row = t[q]

@@ -1,0 +1,18 @@
+"""One K1T launch (multi-RHS, t = 16) at config-5 shape (d = 440) for ncu captures.
+
+python tools/one_k1t_launch.py [n]
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+
+import paper_1611_03220_b200 as krr  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+x, _ = krr.generate_config(5, n, 440, 16, 0)
+v = np.random.default_rng(0).standard_normal((n, 16))
+op = krr.KernelOperator(x, krr.KernelSpec.gaussian(20.0), 1e-5)
+out = op.matmat(v)
+print("ok", float(out[0, 0]))
