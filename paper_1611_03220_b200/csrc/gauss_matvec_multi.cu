@@ -53,6 +53,12 @@ __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync
 template <int T, int MODE>
 __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) {
     constexpr int NTT = T / 8;  // n8 tiles of the RHS dimension
+    // Row-major (row, T) tiles in shared memory with the column index XOR-swizzled by the row
+    // parity when T = 16 (rows are 128 B = all 32 banks): the fragment reads of four
+    // consecutive rows and the 8-row double2 stores then take the minimum number of
+    // wavefronts (2 and 4) instead of 4 and 8 (ncu: 23 % of the shared-memory wavefronts
+    // were bank conflicts at d = 440, t = 16).
+    auto sw = [](int row, int col) { return row * T + (T == 16 ? (col ^ ((row & 1) << 3)) : col); };
     extern __shared__ __align__(16) double smem[];
     double* stages = smem;                                  // NSTAGE * STAGE_DOUBLES
     double* vjs = stages + NSTAGE * STAGE_DOUBLES;          // BM x T
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
     for (int jt = 0; jt < nT; ++jt) {
         const int64_t J0 = colBase + int64_t(jt) * BM;
         __syncthreads();  // previous J's users of vjs / scr are done
-        for (int k = tid; k < BM * T; k += NT) vjs[k] = A.v[J0 * T + k];
+        for (int k = tid; k < BM * T; k += NT) vjs[sw(k / T, k % T)] = A.v[J0 * T + k];
         double colT[4][NTT][2];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
                 cp_async_wait<NSTAGE - 2>();
                 __syncthreads();
                 if (kc == 0)  // V_I for this tile (vis is free: last read before this barrier)
-                    for (int k = tid; k < BM * T; k += NT) vis[k] = A.v[I0 * T + k];
+                    for (int k = tid; k < BM * T; k += NT) vis[sw(k / T, k % T)] = A.v[I0 * T + k];
                 if (ps < total) {
                     issue(ps % NSTAGE);
                     advance();
@@ -194,16 +200,16 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
                     const int src = g * 4 + half * 2 + (t4 >> 1);
                     const double v0 = shfl_d(e[ns][0], src), v1 = shfl_d(e[ns][1], src);
                     const double a = (t4 & 1) ? v1 : v0;  // E[g][ns*8 + half*4 + t4]
-                    const double* vb = vjs + (wn * 32 + kk * 4 + t4) * T + g;
+                    const int vr = wn * 32 + kk * 4 + t4;
 #pragma unroll
-                    for (int nt = 0; nt < NTT; ++nt) dmma884(oi[nt][0], oi[nt][1], a, vb[nt * 8]);
+                    for (int nt = 0; nt < NTT; ++nt) dmma884(oi[nt][0], oi[nt][1], a, vjs[sw(vr, g + nt * 8)]);
                 }
 #pragma unroll
                 for (int nt = 0; nt < NTT; ++nt) {
                     double2 o2;
                     o2.x = oi[nt][0];
                     o2.y = oi[nt][1];
-                    *reinterpret_cast<double2*>(scr + (wn * BM + wm * 64 + ms * 8 + g) * T + nt * 8 + 2 * t4) = o2;
+                    *reinterpret_cast<double2*>(scr + wn * BM * T + sw(wm * 64 + ms * 8 + g, nt * 8 + 2 * t4)) = o2;
                 }
                 // columns: O_J(32 x T) += E_blk^T(32 x 8) . V_I(8 x T)
 #pragma unroll
@@ -213,10 +219,10 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
                         const int src = (kk * 4 + t4) * 4 + (g >> 1);
                         const double v0 = shfl_d(e[mt][0], src), v1 = shfl_d(e[mt][1], src);
                         const double a = (g & 1) ? v1 : v0;  // E[kk*4 + t4][mt*8 + g]
-                        const double* vb = vis + (wm * 64 + ms * 8 + kk * 4 + t4) * T + g;
+                        const int vr = wm * 64 + ms * 8 + kk * 4 + t4;
 #pragma unroll
                         for (int nt = 0; nt < NTT; ++nt)
-                            dmma884(colT[mt][nt][0], colT[mt][nt][1], a, vb[nt * 8]);
+                            dmma884(colT[mt][nt][0], colT[mt][nt][1], a, vis[sw(vr, g + nt * 8)]);
                     }
             }
             __syncthreads();
@@ -225,7 +231,8 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
                 double* dst = A.part + (int64_t(sb) * A.n_pad + I0) * T;
                 const bool first = diag ? (jt == it) : (jt == 0);
                 for (int k = tid; k < BM * T; k += NT) {
-                    const double s = ((scr[k] + scr[BM * T + k]) + scr[2 * BM * T + k]) + scr[3 * BM * T + k];
+                    const int q = sw(k / T, k % T);
+                    const double s = ((scr[q] + scr[BM * T + q]) + scr[2 * BM * T + q]) + scr[3 * BM * T + q];
                     dst[k] = first ? s : dst[k] + s;
                 }
             }
@@ -240,13 +247,14 @@ __global__ void __launch_bounds__(NT, 1) gauss_matmat_kernel(const MultiArgs A) 
                 double2 o2;
                 o2.x = colT[mt][nt][0];
                 o2.y = colT[mt][nt][1];
-                *reinterpret_cast<double2*>(scr + (wm * BM + wn * 32 + mt * 8 + g) * T + nt * 8 + 2 * t4) = o2;
+                *reinterpret_cast<double2*>(scr + wm * BM * T + sw(wn * 32 + mt * 8 + g, nt * 8 + 2 * t4)) = o2;
             }
         __syncthreads();
         {
             double* dst = A.part + (int64_t(sa) * A.n_pad + J0) * T;
             for (int k = tid; k < BM * T; k += NT) {
-                const double s = scr[k] + scr[BM * T + k];
+                const int q = sw(k / T, k % T);
+                const double s = scr[q] + scr[BM * T + q];
                 dst[k] = diag ? dst[k] + s : s;  // diag: the row partial of (jt, jt) is already there
             }
         }
