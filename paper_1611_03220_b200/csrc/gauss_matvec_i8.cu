@@ -155,7 +155,7 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
     double racc[4] = {0.0, 0.0, 0.0, 0.0};
     // four columns at a time, each step applied across the batch: independent chains
     // side by side for the scheduler (the per-pair chain is ~16 dependent FP64 ops)
-    constexpr int BW = 4;
+    constexpr int BW = 2;
 #pragma unroll
     for (int k0 = 0; k0 < CPT; k0 += BW) {
         double y[BW], t2[BW], f[BW], q[BW], e[BW];
