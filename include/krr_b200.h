@@ -189,6 +189,15 @@ int krr_rff_download(krr_ctx* ctx, double* Z);
  * build_preconditioner(z, lambda_p) (precond.hpp:28) take any sketch. */
 int krr_sketch_upload(krr_ctx* ctx, const double* Z, int64_t n, int64_t s);
 
+/* solve_regularized (solver.hpp:82-84, solver.cpp:69-94) with the reference's own signature: a
+ * caller-supplied dense K (n x n row-major, symmetric), Y n x t; A v = K v + lambda v on the
+ * device (cuBLAS DGEMV), M = the context's Woodbury preconditioner when use_precond (built for
+ * n rows).  Per-column PCG as the reference's sequential loop.  Single rank.  The on-the-fly
+ * path (krr_set_data + krr_pcg_solve) is the one that scales: K is n^2 doubles here. */
+int krr_solve_regularized_dense(krr_ctx* ctx, const double* K, int64_t n, const double* Y, int64_t t, double lambda,
+                                int use_precond, double tau, int max_iter, double* C, krr_rhs_stats* stats,
+                                double* residual_history, int64_t* total_matvecs);
+
 /* ---------------------------------------------------------------- kernel families + sketch chains */
 /* KernelSpec (kernels.hpp:15-27).  family 0 = Gaussian (sigma > 0), 1 = polynomial
  * k(x, z) = (gamma x.z + offset)^degree (gamma > 0, offset >= 0, degree >= 1);

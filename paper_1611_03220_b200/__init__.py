@@ -49,7 +49,7 @@ __all__ = [
     "KernelSpec", "Dataset", "RffMap", "TensorSketchMap", "SrhtMap", "GaussianMap", "ChainSpec", "SketchChain",
     "realize_chain", "KernelOperator",
     "Preconditioner", "build_preconditioner", "GaussianOperator", "SolverConfig", "RhsStats",
-    "PcgReport", "PcgResult", "KrrModel", "TrainResult", "pcg_solve", "solve_regularized",
+    "PcgReport", "PcgResult", "KrrModel", "TrainResult", "pcg_solve", "solve_regularized", "solve_regularized_dense",
     "train", "predict_scores", "predict_labels", "rlsc_encode", "rlsc_decode",
     "generate_config", "schedule", "Context", "device_count",
     "save_model", "load_model", "ModelFileError",
@@ -645,6 +645,39 @@ def solve_regularized(x: np.ndarray, kernel: KernelSpec, y: np.ndarray, lambda_:
             ctx.close()
     report = PcgReport([_stats_from(st, hist, j) for j in range(t)], int(tot.value), wall)
     return c, report
+
+
+def solve_regularized_dense(k: np.ndarray, y: np.ndarray, lambda_: float, preconditioner: Optional[Preconditioner],
+                            tau: float, max_iter: int, ctx: Optional[Context] = None):
+    """solve_regularized (solver.hpp:82-84, solver.cpp:69-94) with the reference's own signature:
+    a dense K (the on-the-fly `solve_regularized(x, kernel, ...)` is the scalable form).  The
+    preconditioner, if given, must have been built on the same context (pass its ctx)."""
+    k = _lib.f64(k)
+    y = _lib.f64(y)
+    y2 = y[:, None] if y.ndim == 1 else y
+    if k.ndim != 2 or k.shape[0] != k.shape[1] or y2.shape[0] != k.shape[0]:
+        raise DimensionMismatch("solve_regularized: K and Y dimensions do not match")
+    own = ctx is None
+    if preconditioner is not None:
+        ctx = preconditioner._ctx
+        own = False
+    ctx = ctx or Context()
+    try:
+        n, t = y2.shape
+        c = np.empty((n, t))
+        st = (_lib.RhsStatsC * t)()
+        hist = np.zeros((t, max(1, int(max_iter))))
+        tot = C.c_int64()
+        t0 = time.perf_counter()
+        _lib.check(_lib.LIB.krr_solve_regularized_dense(ctx.handle, _lib.ptr(k), n, _lib.ptr(y2), t, float(lambda_),
+                                                        1 if preconditioner is not None else 0, float(tau),
+                                                        int(max_iter), _lib.ptr(c), st, _lib.ptr(hist),
+                                                        C.byref(tot)))
+        wall = time.perf_counter() - t0
+    finally:
+        if own:
+            ctx.close()
+    return c, PcgReport([_stats_from(st, hist, j) for j in range(t)], int(tot.value), wall)
 
 
 def train(data: Dataset, kernel: KernelSpec, cfg: SolverConfig, ctx: Optional[Context] = None) -> TrainResult:

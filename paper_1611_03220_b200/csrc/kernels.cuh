@@ -116,6 +116,7 @@ void copy_launch(double* dst, const double* src, int64_t n, cudaStream_t stream)
 void pcg_control_launch(const double* scal, int* ctl, double* hist, double* final_rel, double norm_y, double tau,
                         int max_iter, cudaGraphConditionalHandle cond, cudaStream_t stream);
 void scalar_copy_launch(double* dst, const double* src, cudaStream_t stream);
+void add_scaled_launch(double* out, const double* v, double lambda, int64_t n, cudaStream_t stream);
 // Gather column c of an n x t row-major matrix into a contiguous vector (and back).
 void gather_col_launch(const double* M, int64_t n, int64_t t, int64_t c, double* out,
                        cudaStream_t stream);

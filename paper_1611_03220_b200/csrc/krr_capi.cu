@@ -2124,10 +2124,66 @@ void adaptive_dev(Ctx& c, const krr_chain_spec& tmpl, double lambda, double lamb
     precond_build(c, lp, jitter_used);
 }
 
+// solve_regularized (solver.cpp:69-94) on a caller-supplied dense K, the reference's own
+// signature: A v = K v + lambda v by cuBLAS DGEMV (K is symmetric, so its row-major buffer is
+// read as column-major) plus the lambda term; M = the context's Woodbury preconditioner.
+void solve_dense_dev(Ctx& c, const double* K, int64_t n, const double* Y, int64_t t, double lambda, int use_precond,
+                     double tau, int max_iter, double* C, krr_rhs_stats* stats, double* hist,
+                     int64_t* total_matvecs) {
+    if (n < 1) fail(KRR_ERR_DIMENSION_MISMATCH, "solve_regularized: K must be non-empty");
+    if (t < 1) fail(KRR_ERR_DIMENSION_MISMATCH, "solve_regularized: K and Y dimensions do not match");
+    if (!(lambda > 0.0)) fail(KRR_ERR_NON_POSITIVE_LAMBDA, "solve_regularized: lambda must be positive");
+    if (c.world != 1) fail(KRR_ERR_STATE, "the dense-K solve is single-rank");
+    if (use_precond) {
+        if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
+        if (c.pn != n) fail(KRR_ERR_DIMENSION_MISMATCH, "Preconditioner: dimension mismatch");
+    }
+    c.set_device();
+    DevMem<double> Kd;
+    upload(Kd, K, size_t(n * n), c.stream);
+    for (auto* v : {&c.vx, &c.vr, &c.vz, &c.vp, &c.vap, &c.vy}) v->ensure(size_t(n));
+    c.red.ensure(size_t(4 * 1024));
+    c.mat_a.ensure(size_t(n * t));
+    c.mat_b.ensure(size_t(n * t));
+    KRR_CUDA(cudaMemcpyAsync(c.mat_a.get(), Y, sizeof(double) * size_t(n * t), cudaMemcpyHostToDevice, c.stream));
+    cublas_check(cublasSetStream(c.blas, c.stream), "cublasSetStream");
+    const double* kd = Kd.get();
+    const DevOp A = [&c, kd, n, lambda](const double* din, double* dout) {
+        const double one = 1.0, zero = 0.0;
+        cublas_check(cublasDgemv(c.blas, CUBLAS_OP_N, int(n), int(n), &one, kd, int(n), din, 1, &zero, dout, 1),
+                     "cublasDgemv(K v)");
+        add_scaled_launch(dout, din, lambda, n, c.stream);
+    };
+    const DevOp M = precond_op(c);
+    int64_t total = 0;
+    for (int64_t j = 0; j < t; ++j) {
+        gather_col_launch(c.mat_a.get(), n, t, j, c.vy.get(), c.stream);
+        const PcgOut o = pcg_core(c, n, A, use_precond ? &M : nullptr, c.vy.get(), tau, max_iter,
+                                  hist ? hist + j * max_iter : nullptr, nullptr, true);
+        scatter_col_launch(c.vx.get(), n, t, j, c.mat_b.get(), c.stream);
+        stats[j].iterations = o.iterations;
+        stats[j].converged = o.converged;
+        stats[j].final_residual = o.final_residual;
+        total += o.iterations;
+    }
+    KRR_CUDA(cudaMemcpyAsync(C, c.mat_b.get(), sizeof(double) * size_t(n * t), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (total_matvecs) *total_matvecs = total;
+}
+
 }  // namespace
 }  // namespace krr
 
 extern "C" {
+
+int krr_solve_regularized_dense(krr_ctx* ctx, const double* K, int64_t n, const double* Y, int64_t t, double lambda,
+                                int use_precond, double tau, int max_iter, double* C, krr_rhs_stats* stats,
+                                double* residual_history, int64_t* total_matvecs) {
+    return guard([&] {
+        krr::solve_dense_dev(*krr::as_ctx(ctx), K, n, Y, t, lambda, use_precond, tau, max_iter, C, stats,
+                             residual_history, total_matvecs);
+    });
+}
 
 int krr_set_data_kernel(krr_ctx* ctx, const double* X, int64_t n, int64_t d, const krr_kernel_spec* kernel) {
     return guard([&] {

@@ -146,6 +146,12 @@ __global__ void pcg_control_kernel(const double* __restrict__ scal, int* __restr
 
 __global__ void scalar_copy_kernel(double* __restrict__ dst, const double* __restrict__ src) { *dst = *src; }
 
+// out_i = out_i + lambda v_i, rounded as the reference's `k * v + lambda * v` (no contraction)
+__global__ void add_scaled_kernel(double* __restrict__ out, const double* __restrict__ v, double lambda, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = __dadd_rn(out[i], __dmul_rn(lambda, v[i]));
+}
+
 __global__ void copy_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -377,6 +383,11 @@ void pcg_update_p_launch(const double* rz_part, int nb, const double* rz_old, do
 void pcg_control_launch(const double* scal, int* ctl, double* hist, double* final_rel, double norm_y, double tau,
                         int max_iter, cudaGraphConditionalHandle cond, cudaStream_t stream) {
     pcg_control_kernel<<<1, 1, 0, stream>>>(scal, ctl, hist, final_rel, norm_y, tau, max_iter, cond);
+    KRR_LAUNCH_CHECK();
+}
+
+void add_scaled_launch(double* out, const double* v, double lambda, int64_t n, cudaStream_t stream) {
+    add_scaled_kernel<<<grid_for(n), 256, 0, stream>>>(out, v, lambda, n);
     KRR_LAUNCH_CHECK();
 }
 

@@ -336,3 +336,31 @@ def test_rlsc_multiclass_train(krr, oracle):
     pred = krr.predict_labels(res.model, x[:200])
     want = [int(np.argmax(r)) for r in oracle.cross_gram(x[:200], x, sigma) @ ref.c]
     assert pred == want
+
+
+@pytest.mark.parametrize("pre,t", [(False, 1), (True, 1), (True, 3)])
+def test_solve_regularized_dense_matches_oracle(krr, oracle, ctx, pre, t):
+    """solve_regularized with the reference's own dense-K signature (solver.cpp:69-94).  (At
+    lambda = 1 the oracle's own summation orders stop within one iteration of each other —
+    39 / 40 — so the +-1 bar is meaningful; at lambda = 0.1 they already spread 123..125.)"""
+    n, d, sigma, lam = 800, 6, 2.0, 1.0
+    x = oracle.random_matrix(n, d, 21)
+    y = oracle.random_matrix(n, t, 22)
+    k = oracle.gram_matrix(x, sigma)
+    u = None
+    p = None
+    if pre:
+        w, b = oracle.rff_realize(0, d, 128, sigma)
+        z = oracle.rff_apply_rows(x, w, b)
+        u, _ = oracle.build_preconditioner(z, lam)
+        p = krr.build_preconditioner(z, lam, ctx=ctx)
+    c, rep = krr.solve_regularized_dense(k, y, lam, p, 1e-10, 300, ctx=ctx)
+    ref = oracle.solve_dense(k, lam, u, lam, y, 1e-10, 300)
+    for j in range(t):
+        assert rep.per_rhs[j].converged == ref.converged[j]
+        assert abs(rep.per_rhs[j].iterations - ref.iterations[j]) <= 1
+    assert rel(c, ref.c) <= 1e-8
+    with pytest.raises(krr.DimensionMismatch):
+        krr.solve_regularized_dense(k[:10, :10], y, lam, None, 1e-8, 10, ctx=ctx)
+    with pytest.raises(krr.NonPositiveLambda):
+        krr.solve_regularized_dense(k, y, 0.0, None, 1e-8, 10, ctx=ctx)
