@@ -401,6 +401,8 @@ int krr_debug_tmem_ld_under_mma(krr_ctx* ctx, int warps, int reps, double* bytes
 /* K1-I8 profiling trace (set_option("i8_debug", 4) before a mat-vec): clock64 stamps of
  * CTA 0, 16 per tile for the first 64 tiles. */
 int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count);
+/* Same for the K1T-I8 multi-RHS kernel (16 stamps per tile, first 32 tiles of CTA 0). */
+int krr_debug_i8t_trace(krr_ctx* ctx, long long* out, int count);
 
 #ifdef __cplusplus
 }

@@ -182,6 +182,7 @@ _SIGS = {
     "krr_debug_tmem_ld_rate": [_vp, _i, _i, C.POINTER(_d)],
     "krr_debug_tmem_ld_under_mma": [_vp, _i, _i, C.POINTER(_d), C.POINTER(_d)],
     "krr_debug_i8_trace": [_vp, _vp, _i],
+    "krr_debug_i8t_trace": [_vp, _vp, _i],
     "krr_solve_regularized_dense": [_vp, _vp, _i64, _vp, _i64, _d, _i, _d, _i, _vp, _vp, _vp, C.POINTER(_i64)],
     # SURVEY 8f4
     "krr_set_data_kernel": [_vp, _vp, _i64, _i64, C.POINTER(KernelSpecC)],

@@ -40,6 +40,18 @@ void gauss_matmat_launch(const GaussMatvecPlan& p, const double* v, int T, doubl
 void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const double* v, int T,
                           double lambda, int add_diag, double* out, cudaStream_t stream);
 
+// K1T-I8: T = 16 right-hand sides, tcgen05 kind::i8 dot products with K-streamed slices and
+// DMMA E.V contractions (gauss_matmat_i8.cu).  Gaussian kernel, d <= 448.
+int i8s_kp(int64_t d);
+bool i8s_supported(int64_t d, int st);
+bool i8s_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp, double kscale,
+                        uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream);
+void gauss_matmat_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const int* ejs,
+                            const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
+                            int debug = 0);
+void i8s_read_trace(long long* out, int count);
+constexpr int64_t kI8TMinD = 28;  // auto path: K1T-I8 from d = 28 (measured crossover, profiles/r1_k1t_i8_crossover.log)
+
 // K1-I8: tcgen05 kind::i8 slice path (gauss_matvec_i8.cu).  Supported for d <= 96.
 bool i8_supported(int64_t d, int st);
 // K1-F32 (optional fp32-accuracy mode, gauss_matvec_f32.cu): three bf16 parts per value on

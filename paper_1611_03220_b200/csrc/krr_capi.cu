@@ -164,6 +164,13 @@ struct Ctx {
     DevMem<uint8_t> S8;
     DevMem<int> ex8, ejs8;
     DevMem<double> sq8;
+    // K1T-I8 operands (K-chunk-major slices for the multi-RHS kernel; prepared on first use)
+    int k1t_path = -1;  // -1 auto, 0 = FP64 DMMA K1T, 1 = K1T-I8 (T = 16)
+    int i8s_state = 0;  // 0 not prepared, 1 ready, -1 exponent range unsupported
+    int kp8s = 0;
+    DevMem<uint8_t> S8s;
+    DevMem<int> ex8s, ejs8s;
+    DevMem<double> sq8s;
     // K1-F32 operands (optional fp32 mode; prepared on first use)
     int precision = 64;  // 64: fp64 (oracle-matching); 32: fp32-accuracy K1
     bool f32_ready = false;
@@ -352,6 +359,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_sp
     p.kdiag = c.family == 1 ? c.kdiag.get() : nullptr;
     c.i8_ready = false;
     c.f32_ready = false;
+    c.i8s_state = 0;
     if (i8_supported(d, int(c.sched.st))) {
         c.kp8 = i8_kp(d);
         c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
@@ -701,9 +709,34 @@ void ensure_batched(Ctx& c, int T) {
     }
 }
 
+// K1T path selection: the tcgen05 INT8-slice kernel (K1T-I8, T = 16, Gaussian) where it is
+// faster than the FP64 DMMA K1T (measured crossover, profiles/), else K1T.  Neither is a
+// fallback: both are GPU kernels parity-tested against the oracle.
+bool use_i8T(Ctx& c, int T) {
+    if (T != 16 || c.family != 0 || c.k1t_path == 0 || !i8s_supported(c.d, int(c.sched.st))) return false;
+    if (c.k1t_path < 0 && c.d < kI8TMinD) return false;
+    if (c.i8s_state == 0) {
+        const int64_t n_pad = c.plan.n_pad;
+        c.kp8s = i8s_kp(c.d);
+        c.S8s.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8s));
+        c.ex8s.ensure(size_t(n_pad));
+        c.ejs8s.ensure(size_t(n_pad));
+        c.sq8s.ensure(size_t(n_pad));
+        c.i8s_state = i8s_prepare_launch(c.X.get(), c.n, c.d, n_pad, c.L.get(), c.plan.dp, c.plan.ec.kscale,
+                                         c.S8s.get(), c.ex8s.get(), c.ejs8s.get(), c.sq8s.get(), c.stream)
+                          ? 1
+                          : -1;
+    }
+    return c.i8s_state == 1;
+}
+
 // out (n_pad x T) = (K + lambda I) v (n_pad x T), replicated on all ranks.
 void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
-    gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.family == 1 ? poly_mode(c.degree) : 1, c.stream);
+    if (use_i8T(c, T))
+        gauss_matmat_i8_launch(c.plan, c.S8s.get(), c.ex8s.get(), c.ejs8s.get(), c.sq8s.get(), v, c.bpart.get(),
+                               c.kp8s, c.stream, c.i8_debug);
+    else
+        gauss_matmat_launch(c.plan, v, T, c.bpart.get(), c.family == 1 ? poly_mode(c.degree) : 1, c.stream);
     matmat_finish_launch(c.plan, c.bpart.get(), v, T, lambda, c.k1_rank() == 0 ? 1 : 0, out, c.stream);
     allreduce_sum(c, out, c.plan.n_pad * T);
 }
@@ -1203,6 +1236,10 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
             if (value != 0.0 && value != 1.0 && value != -1.0)
                 fail(KRR_ERR_INVALID_ARGUMENT, "k1_path must be -1 (auto), 0 (dmma) or 1 (i8)");
             c.k1_path = int(value);
+        } else if (k == "k1t_path") {
+            if (value != 0.0 && value != 1.0 && value != -1.0)
+                fail(KRR_ERR_INVALID_ARGUMENT, "k1t_path must be -1 (auto), 0 (dmma) or 1 (i8)");
+            c.k1t_path = int(value);
         } else if (k == "batched_rhs") {
             c.batched = value != 0.0;
         } else if (k == "exp_mode") {
@@ -1241,6 +1278,11 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
         } else if (k == "k1_path_effective") {  // the K1 kernel a mat-vec runs now
             krr::require_data(c);
             *value = krr::use_i8(c) ? 1.0 : 0.0;
+        } else if (k == "k1t_path") {
+            *value = c.k1t_path;
+        } else if (k == "k1t_path_effective") {  // the K1T kernel a 16-column batch runs now
+            krr::require_data(c);
+            *value = krr::use_i8T(c, 16) ? 1.0 : 0.0;
         } else if (k == "i8_supported") {
             krr::require_data(c);
             *value = c.i8_ready ? 1.0 : 0.0;
@@ -1867,6 +1909,14 @@ int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count) {
         Ctx& c = *krr::as_ctx(ctx);
         c.set_device();
         krr::i8_read_trace(out, count);
+    });
+}
+
+int krr_debug_i8t_trace(krr_ctx* ctx, long long* out, int count) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        c.set_device();
+        krr::i8s_read_trace(out, count);
     });
 }
 

@@ -1,0 +1,91 @@
+"""K1T-I8 — the T = 16 multi-RHS mat-mat with tcgen05 INT8-slice dot products (K-streamed
+operands) and DMMA E.V contractions (csrc/gauss_matmat_i8.cu), vs the CPU oracle and vs the
+FP64 DMMA K1T.
+
+Reference: gram_matrix (kernels.cpp:72-88) applied column by column as solve_regularized's
+apply_a (solver.cpp:75-77).  Bar: ||dKV|| / ||KV|| <= 1e-13 (the K1 bar); the K entries are
+K1-I8's bit patterns (same slices, drain and table exp), checked bitwise.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(1, 1, 1.0, 16), (5, 4, 0.7, 16), (300, 6, 1.7, 16), (1000, 90, 6.0, 11), (2048, 440, 20.0, 16),
+         (4097, 440, 20.0, 16), (9000, 96, 8.0, 16), (20000, 440, 20.0, 16), (3000, 54, 3.0, 30)]
+
+
+@pytest.mark.parametrize("n,d,sigma,t", CASES)
+def test_i8_matmat_matches_oracle_and_dmma(krr, oracle, ctx, n, d, sigma, t):
+    x = oracle.random_matrix(n, d, 3 + n)
+    v = oracle.random_matrix(n, t, 4 + n)
+    lam = 1e-3
+    ctx.set_option("k1t_path", 1)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(sigma), lam, ctx=ctx)
+    assert ctx.get_option("k1t_path_effective") == 1
+    got = op.matmat(v)
+    ctx.set_option("k1t_path", 0)
+    assert ctx.get_option("k1t_path_effective") == 0
+    dmma = op.matmat(v)
+    for r0, r1 in {(0, min(n, 40)), (max(0, n - 40), n)}:
+        want = oracle.kernel_matvec(x, sigma, lam, v, rows=(r0, r1))
+        assert rel(got[r0:r1], want) <= 1e-13, (r0, rel(got[r0:r1], want))
+    assert rel(got, dmma) <= 1e-13, rel(got, dmma)
+
+
+def test_i8_matmat_entries_bitwise_k1_i8(krr, oracle, ctx):
+    """K V with V = identity columns: every entry is one e_ij (the E.V sums add exact zeros),
+    so K1T-I8's Gram matrix is K1-I8's bit for bit, exactly symmetric, with a unit diagonal."""
+    n, d = 300, 40
+    x = oracle.random_matrix(n, d, 11)
+    x[::7] *= 1e-2
+    x[4] = x[9]  # duplicate rows: d2 clamped at 0 where rounding makes it negative
+    ctx.set_option("k1t_path", 1)
+    ctx.set_option("k1_path", 1)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(3.0), 0.0, ctx=ctx)
+    kk = op.matmat(np.eye(n))
+    cols = list(range(0, n, 23))
+    k1 = np.column_stack([op(np.eye(n)[:, j]) for j in cols])
+    assert np.array_equal(np.diag(kk), np.ones(n))
+    assert np.array_equal(kk, kk.T)
+    assert np.array_equal(kk[:, cols], k1)
+    want = oracle.gram_matrix(x, 3.0)
+    assert np.max(np.abs(kk - want)) <= 4e-15  # entries <= 1; |x|^2 up to ~40 at d = 40
+
+
+def test_i8_matmat_rank_emulation_partials_sum(krr, oracle, ctx):
+    """Per-rank K1T-I8 partials (emulated ranks of a W = 4 job) sum to the single-rank K V."""
+    n, d, t = 9000, 90, 16
+    x = oracle.random_matrix(n, d, 21)
+    v = oracle.random_matrix(n, t, 22)
+    ctx.set_option("k1t_path", 1)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(6.0), 0.0, ctx=ctx)
+    full = op.matmat(v)
+    acc = np.zeros_like(full)
+    for r in range(4):
+        ctx.set_option("emulate_world", 4)
+        ctx.set_option("emulate_rank", r)
+        op_r = krr.GaussianOperator(x, krr.KernelSpec.gaussian(6.0), 0.0, ctx=ctx)
+        acc += op_r.matmat(v)
+    ctx.set_option("emulate_world", 1)
+    ctx.set_option("emulate_rank", 0)
+    assert rel(acc, full) <= 1e-14, rel(acc, full)
+
+
+@pytest.mark.parametrize("d,want", [(16, 0), (27, 0), (28, 1), (90, 1), (440, 1), (449, 0)])
+def test_k1t_path_auto_selection(krr, oracle, ctx, d, want):
+    """Auto K1T path: K1T-I8 from d = 28 (profiles/r1_k1t_i8_crossover.log) up to kp = 448."""
+    x = oracle.random_matrix(600, d, 3)
+    krr.GaussianOperator(x, krr.KernelSpec.gaussian(4.0), 0.0, ctx=ctx)
+    assert ctx.get_option("k1t_path") == -1
+    assert ctx.get_option("k1t_path_effective") == want
+
+
+def test_k1t_i8_not_used_for_polynomial(krr, oracle, ctx):
+    """The polynomial kernel's multi-RHS products stay on the DMMA K1T (Gaussian-only kernel)."""
+    x = oracle.random_matrix(600, 90, 3)
+    ctx.set_option("k1t_path", 1)
+    krr.KernelOperator(x, krr.KernelSpec.polynomial(1.0 / 90, 1.0, 3), 0.0, ctx=ctx)
+    assert ctx.get_option("k1t_path_effective") == 0
