@@ -21,6 +21,9 @@ roofline: dominant kernel = K1.  The default path at d = 90 is K1-I8 (tcgen05 ki
           = 2x bf16).  The same launch is also expressed as FP64-equivalent dot-product
           TFLOP/s (pairs x 2d) against the live-measured FP64 DMMA peak (krr_microbench),
           the unit of the DMMA K1 path (k1_path = 0).
+config5_pass: informational, N = 1 only (--no-config5 skips it): one (K + lambda I) V pass at
+          BASELINE config 5 (n = 524288, d = 440, t = 16) through krr_kernel_matvec with host
+          buffers, on K1T-I8 (INT8-slice dot products + DMMA E.V) and on the DMMA K1T.
 --impl reference: the CPU restatement (oracle/, all host threads) on a bounded row
           sample of the same workload — the reference itself (CPU-only, Eigen) cannot be
           built in this image.
@@ -55,6 +58,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the optional fp32-mode measurement")
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 multi-RHS pass (K1T-I8 vs DMMA K1T)")
     ap.add_argument("--time-to-tol", type=int, default=0, metavar="CFG",
                     help="also run the full train (RFF + precond + PCG) of BASELINE config CFG")
     return ap.parse_args()
@@ -288,6 +292,11 @@ def main():
                "rel_err_vs_fp64": float(np.linalg.norm(out32 - ref64) / np.linalg.norm(ref64)),
                "note": "optional fp32-accuracy mode (krr_set_precision 32); not the headline"}
 
+    # ---- BASELINE config 5's multi-RHS pass (d = 440, t = 16: K1T-I8 vs the DMMA K1T), one GPU
+    c5 = None
+    if world == 1 and not args.no_config5:
+        c5 = config5_pass(krr, _lib, local)
+
     # ---- optional time-to-tolerance (full train on the device)
     ttt = None
     if args.time_to_tol:
@@ -379,11 +388,41 @@ def main():
         line["time_to_tol"] = ttt
     if f32:
         line["fp32_mode"] = f32
+    if c5:
+        line["config5_pass"] = c5
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
     D.close()
     return 0
+
+
+def config5_pass(krr, _lib, device: int) -> dict:
+    """One (K + lambda I) V pass at BASELINE config 5 (n = 524288, d = 440, t = 16) through the
+    reference-facing krr_kernel_matvec with host buffers (64 MiB each way), K1T-I8 and DMMA K1T."""
+    n, d, t, sigma, lam, s = krr.CONFIGS[5]
+    x, y = krr.generate_config(5, n, d, t, 0)
+    v = np.ascontiguousarray(y)
+    out = {}
+    res = {"workload": "config5 (K + lambda I) V, t = 16", "n": n, "d": d, "t": t, "unit": "s per pass (e2e)",
+           "h2d_bytes_per_pass": 8 * n * t, "d2h_bytes_per_pass": 8 * n * t}
+    c5 = krr.Context(device)
+    try:
+        _lib.check(_lib.LIB.krr_set_data(c5.handle, _lib.ptr(x), n, d, sigma))
+        for name, path in (("k1t_i8", 1), ("k1t_dmma", 0)):
+            c5.set_option("k1t_path", path)
+            o = np.empty_like(v)
+            _lib.check(_lib.LIB.krr_kernel_matvec(c5.handle, lam, _lib.ptr(v), t, _lib.ptr(o)))  # warm
+            t0 = time.perf_counter()
+            _lib.check(_lib.LIB.krr_kernel_matvec(c5.handle, lam, _lib.ptr(v), t, _lib.ptr(o)))
+            res[name] = time.perf_counter() - t0
+            out[name] = o
+    finally:
+        c5.close()
+    res["rel_diff_i8_vs_dmma"] = float(np.linalg.norm(out["k1t_i8"] - out["k1t_dmma"]) /
+                                       np.linalg.norm(out["k1t_dmma"]))
+    res["rhs_gevals_per_s"] = float(n) * n * t / res["k1t_i8"] / 1e9
+    return res
 
 
 def time_to_tol(krr, ctx, cfg: int) -> dict:
