@@ -78,11 +78,16 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
  *   "k1_path"     -1|0|1  fused mat-vec kernel: auto (default: INT8-slice tensor-core kernel
  *                         where faster: 27 <= d <= 32, 44 <= d <= 96, when the data's exponent range allows, else FP64 DMMA) |
  *                         FP64 DMMA | tcgen05 INT8 slices
+ *   "k1t_path"    -1|0|1  16-column batches of multi-RHS mat-mats / batched PCG: auto (default:
+ *                         K1T-I8 — INT8-slice dot products on K-streamed operands + DMMA E.V —
+ *                         for the Gaussian kernel with 28 <= d <= 448, else the DMMA K1T) |
+ *                         DMMA K1T | K1T-I8 where supported
  *   "k1_resident" 1|0  keep the column tile of the DMMA mat-vec in shared memory (default 1)
  *   "k1_warps" 8|16, "k1_grouped" 1|0  DMMA mat-vec shape (defaults 8, 1)
  *   "batched_rhs" 1|0  multi-RHS solves / mat-mats through the batched kernel (default 1)
  *   "exp_mode"    1|0  table exp (default) | libdevice exp in the Gaussian epilogue
- *   "i8_debug"    bits  profiling only (K1-I8: 1 skip MMAs, 2 skip exp, 4 clock trace)
+ *   "i8_debug"    bits  profiling only (K1-I8: 1 skip MMAs, 2 skip exp, 4 clock trace;
+ *                         K1T-I8: 4 clock trace)
  *   "pcg_graph"   1|0  single-RHS device PCG as one CUDA graph (conditional WHILE node, device-side
  *                         stop / breakdown decision; default 1) | host-driven loop; same iterates
  *   "emulate_world" W, "emulate_rank" r   test only, single-rank contexts: the next
@@ -144,8 +149,9 @@ int krr_quality_test(krr_ctx* ctx, double lambda, krr_quality_report* out);
 int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0, int64_t s_max,
                        uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
                        int64_t* final_size, int* passed, int* jitter_used);
-/* Read a knob back: "k1_path", "exp_mode", "batched_rhs", and (after krr_set_data)
- * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now), "i8_supported",
+/* Read a knob back: "k1_path", "k1t_path", "exp_mode", "batched_rhs", and (after krr_set_data)
+ * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now), "k1t_path_effective"
+ * (the kernel a 16-column batch runs now; may prepare the K1T-I8 operands), "i8_supported",
  * and "precision" (64 | 32). */
 int krr_get_option(krr_ctx* ctx, const char* key, double* value);
 
