@@ -67,7 +67,8 @@ int krr_device_count(void);
 int krr_ctx_create(int device, krr_ctx** out);
 /* Rank `rank` of `world` (one process per GPU).  `nccl_id` is the 128-byte
  * ncclUniqueId produced by krr_nccl_unique_id on rank 0 and broadcast by the
- * caller (bench.py uses torch.distributed for that broadcast only). */
+ * caller (bench.py uses torch.distributed for that broadcast only).  world = 1 gives a
+ * one-rank communicator (the data path then needs no collective). */
 int krr_nccl_unique_id(void* out_128_bytes);
 int krr_ctx_create_dist(int device, int rank, int world, const void* nccl_id, krr_ctx** out);
 int krr_ctx_destroy(krr_ctx* ctx);
@@ -407,6 +408,9 @@ int krr_debug_tmem_ld_under_mma(krr_ctx* ctx, int warps, int reps, double* bytes
 /* K1-I8 profiling trace (set_option("i8_debug", 4) before a mat-vec): clock64 stamps of
  * CTA 0, 16 per tile for the first 64 tiles. */
 int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count);
+/* In-place ncclAllReduce (sum) of n host doubles over the context's communicator (contexts
+ * from krr_ctx_create_dist, including one-rank ones) — plumbing check of the NCCL path. */
+int krr_debug_nccl_allreduce(krr_ctx* ctx, double* buf, int64_t n);
 /* Same for the K1T-I8 multi-RHS kernel (16 stamps per tile, first 32 tiles of CTA 0). */
 int krr_debug_i8t_trace(krr_ctx* ctx, long long* out, int count);
 

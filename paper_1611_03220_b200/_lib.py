@@ -183,6 +183,7 @@ _SIGS = {
     "krr_debug_tmem_ld_under_mma": [_vp, _i, _i, C.POINTER(_d), C.POINTER(_d)],
     "krr_debug_i8_trace": [_vp, _vp, _i],
     "krr_debug_i8t_trace": [_vp, _vp, _i],
+    "krr_debug_nccl_allreduce": [_vp, _vp, _i64],
     "krr_solve_regularized_dense": [_vp, _vp, _i64, _vp, _i64, _d, _i, _d, _i, _vp, _vp, _vp, C.POINTER(_i64)],
     # SURVEY 8f4
     "krr_set_data_kernel": [_vp, _vp, _i64, _i64, C.POINTER(KernelSpecC)],
@@ -254,7 +255,7 @@ class Context:
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # world 1 + id: a one-rank NCCL communicator
             if nccl_id is None or len(nccl_id) != 128:
                 raise InvalidArgument("a 128-byte NCCL unique id is required when world > 1")
             buf = C.create_string_buffer(nccl_id, 128)

@@ -1184,11 +1184,11 @@ int krr_ctx_create_dist(int device, int rank, int world, const void* nccl_id, kr
         c->rank = rank;
         c->world = world;
         krr::ctx_init_common(*c);
-        if (world > 1) {
-            ncclUniqueId id;
-            std::memcpy(&id, nccl_id, sizeof(id));
-            krr::nccl_check(krr::nccl().commInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
-        }
+        // world == 1 with an id: a one-rank communicator (collectives are identities; the data
+        // path skips them) — lets a single-GPU box exercise the NCCL plumbing
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        krr::nccl_check(krr::nccl().commInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
         *out = reinterpret_cast<krr_ctx*>(c.release());
     });
 }
@@ -1909,6 +1909,23 @@ int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count) {
         Ctx& c = *krr::as_ctx(ctx);
         c.set_device();
         krr::i8_read_trace(out, count);
+    });
+}
+
+int krr_debug_nccl_allreduce(krr_ctx* ctx, double* buf, int64_t n) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (!c.comm) fail(KRR_ERR_STATE, "no NCCL communicator on this context (krr_ctx_create_dist)");
+        if (n < 0 || (n > 0 && !buf)) fail(KRR_ERR_INVALID_ARGUMENT, "bad buffer");
+        c.set_device();
+        if (n == 0) return;
+        krr::DevMem<double> d;
+        d.ensure(size_t(n));
+        KRR_CUDA(cudaMemcpyAsync(d.get(), buf, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c.stream));
+        krr::nccl_check(krr::nccl().allReduce(d.get(), d.get(), size_t(n), ncclDouble, ncclSum, c.comm, c.stream),
+                        "ncclAllReduce");
+        KRR_CUDA(cudaMemcpyAsync(buf, d.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
     });
 }
 
