@@ -70,6 +70,9 @@ constexpr int NCD = 3;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
+#ifndef I8_EARLY_DONE
+#define I8_EARLY_DONE 1  // arrive on epi_done after the exp element loop (1) or after the column sums (0)
+#endif
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int KP_MAX = 96;
 constexpr int SCR_LD = 33;  // transpose scratch row stride (doubles): conflict-free both ways
@@ -150,7 +153,8 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
                                           const int* __restrict__ cd_e, double* __restrict__ scr,
                                           double* __restrict__ colscr_q, long long* __restrict__ tr,
                                           int nsi_hi, int nsi_lo, double sqs_i,
-                                          double v_i, double& rowacc, int lane, int colOff, int mask_row) {
+                                          double v_i, double& rowacc, int lane, int colOff, int mask_row,
+                                          uint64_t* fp64_done) {
     const double shifter = 6755399441055744.0;  // 1.5 * 2^52
     double racc[4] = {0.0, 0.0, 0.0, 0.0};
     // four columns at a time, each step applied across the batch: independent chains
@@ -228,6 +232,13 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
     }
     if (tr) tr[13] = clock64();  // profiling trace: element loop done
     rowacc += (racc[0] + racc[1]) + (racc[2] + racc[3]);
+    // The FP64-heavy part of the tile is over: release the tensor core now, so the next tile's
+    // first MMA groups overlap the column-sum transposes below (shared-memory traffic and one
+    // DADD per pair) instead of waiting for them.
+    if (fp64_done) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(fp64_done);
+    }
     // column sums over the warp's 32 rows: lane L sums column L % CPT over rows
     // (L / CPT) * RPL .. + RPL in 4 chains, then a butterfly over the row blocks (fixed order)
     __syncwarp();
@@ -465,6 +476,9 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 const bool masked = diag && jt < (it + 1) * (TI / TJ);
                 long long* trp = ((A.debug & 4) && blockIdx.x == 0 && etid == 0 && tq < TRACE_TILES)
                                      ? g_trace + tq * 16 : nullptr;
+                // epi_done is arrived inside exp_phase (after its FP64 element loop) unless the
+                // exp phase is skipped (profiling) or I8_EARLY_DONE = 0
+                uint64_t* early = (I8_EARLY_DONE && !(A.debug & 2)) ? epi_done : nullptr;
                 if (A.debug & 2) {
                     double z = 0.0;
 #pragma unroll
@@ -474,19 +488,19 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     // diagonal block: keep j > i (local column index vs local row index)
                     const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
                     exp_phase<true, false, POLY>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
-                                         rowacc, lane, colOff, mask_row);
+                                         rowacc, lane, colOff, mask_row, early);
                 } else if (A.debug & 16) {
                     exp_phase<false, true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i,
-                                           v_i, rowacc, lane, colOff, 0);
+                                           v_i, rowacc, lane, colOff, 0, early);
                 } else {
                     exp_phase<false, false, POLY>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
-                                          rowacc, lane, colOff, 0);
+                                          rowacc, lane, colOff, 0, early);
                 }
                 I8_TRACE(etid == 0, tq, 6);
                 __syncwarp();
                 if (lane == 0) {
                     tc::mbar_arrive(cd_empty + cs);
-                    tc::mbar_arrive(epi_done);
+                    if (!early) tc::mbar_arrive(epi_done);
                 }
                 epi_bar();
                 I8_TRACE(etid == 0, tq, 7);
