@@ -434,13 +434,16 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 int32_t bint[CPT];
                 double lo[CPT], T[CPT];
                 auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
+                    // both loads of the stage in flight before one wait (TMEM load latency under
+                    // load is ~250 clk); group ca + 1 completes first (issue order 7 -> 0), so its
+                    // load overlaps the wait for group ca — on the tile's last stage that wait is
+                    // the exposed tail before the exp phase
+                    uint32_t gl[CPT], gh[CPT];
                     tc::mbar_wait_sleep(g_full + ca + 1, ph);
+                    tc::fence_after();
+                    tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ), gl);
                     tc::mbar_wait_sleep(g_full + ca, ph);
                     tc::fence_after();
-                    // all loads of the stage in flight before one wait (TMEM load latency
-                    // under load is ~250 clk; one round trip per stage, not per 8 columns)
-                    uint32_t gl[CPT], gh[CPT];
-                    tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ), gl);
                     tc::tmem_ld16(taddr + uint32_t(ca * TJ), gh);
                     tc::tmem_wait_ld();
 #pragma unroll
