@@ -56,8 +56,7 @@ constexpr int NEPI = 16;   // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;    // columns per epilogue thread
 constexpr int NTHR = 32 * (2 + NEPI);
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int NSTG = 2;                 // K-chunk stages in their own region
-constexpr int NRING = NSTG;
+constexpr int NSTG = 2;                 // K-chunk ring stages
 constexpr int A_CH = P * TI * 32;       // 32 KB
 constexpr int B_CH = P * TJ * 32;       // 16 KB
 constexpr int STG_BYTES = A_CH + B_CH;  // 48 KB
@@ -78,7 +77,7 @@ constexpr size_t OFF_VJ = OFF_VI + size_t(TI) * TR * 8;
 constexpr size_t OFF_CD = OFF_VJ + size_t(TJ) * TR * 8;
 constexpr size_t OFF_TAB = OFF_CD + size_t(NCD) * CD_BYTES;
 constexpr size_t OFF_BARS = OFF_TAB + size_t(TAB) * TAB_REP * 8;
-constexpr int NBARS = 2 * NRING + 2 * NCD + 2 * NGRP + 1;
+constexpr int NBARS = 2 * NSTG + 2 * NCD + 2 * NGRP + 1;
 constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
 static_assert(SMEM <= 227 * 1024, "K1T-I8 shared memory");
 
@@ -137,8 +136,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
     double* tab = reinterpret_cast<double*>(smem + OFF_TAB);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BARS);
     uint64_t* s_full = bars;
-    uint64_t* s_empty = s_full + NRING;
-    uint64_t* cd_full = s_empty + NRING;
+    uint64_t* s_empty = s_full + NSTG;
+    uint64_t* cd_full = s_empty + NSTG;
     uint64_t* cd_empty = cd_full + NCD;
     uint64_t* g_full = cd_empty + NCD;
     uint64_t* g_empty = g_full + NGRP;
@@ -156,7 +155,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
     const int64_t g8 = A.n_pad / 8;  // 8-row groups per K chunk
 
     if (tid == 0) {
-        for (int s = 0; s < NRING; ++s) {
+        for (int s = 0; s < NSTG; ++s) {
             tc::mbar_init(s_full + s, 1);
             tc::mbar_init(s_empty + s, 1);
         }
@@ -182,7 +181,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             int bq = 0;
-            int uses[NRING] = {};
+            int uses[NSTG] = {};
             for (int it = 0; it < nTI; ++it) {
                 const int64_t r0 = rowBase + int64_t(it) * TI;
                 for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
@@ -194,7 +193,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     tc::bulk_g2s(cd, A.sqs + c0, TJ * 8, cd_full + cs);
                     tc::bulk_g2s(cd + TJ * 8, A.ejs + c0, TJ * 4, cd_full + cs);
                     for (int ks = 0; ks < KS; ++ks) {
-                        const int s = ks % NRING;
+                        const int s = ks % NSTG;
                         if (ks == 0) MI8_TRACE(true, bq, 12);
                         if (uses[s] > 0) tc::mbar_wait_sleep(s_empty + s, uint32_t((uses[s] - 1) & 1));
                         ++uses[s];
@@ -214,14 +213,14 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
         // ------------------------------------------------------------ MMA issuer
         const uint32_t idesc = tc::idesc_i8(TI, TJ);
         int bq = 0;
-        int uses[NRING] = {};
+        int uses[NSTG] = {};
         for (int it = 0; it < nTI; ++it) {
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
                 // time-multiplexed with the previous tile's FP64 phase (exp + DMMA)
                 if (MI8_TMUX && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
                 MI8_TRACE(lane == 0, bq, 8);
                 for (int ks = 0; ks < KS; ++ks) {
-                    const int s = ks % NRING;
+                    const int s = ks % NSTG;
                     tc::mbar_wait_sleep(s_full + s, uint32_t(uses[s] & 1));
                     ++uses[s];
                     if (ks == 0 || ks == KS / 2 || ks == KS - 1) MI8_TRACE(lane == 0, bq, ks == 0 ? 9 : (ks == KS - 1 ? 11 : 10));
