@@ -151,7 +151,8 @@ int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0,
                        uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
                        int64_t* final_size, int* passed, int* jitter_used);
 /* Read a knob back: "k1_path", "k1t_path", "exp_mode", "batched_rhs", and (after krr_set_data)
- * "k1_path_effective" (0 DMMA / 1 I8: the kernel a mat-vec runs now), "k1t_path_effective"
+ * "k1_path_effective" (0 DMMA / 1 I8 / 2 column 0 of a 16-column K1T-I8 pass, d >= 160: the
+ * kernel a mat-vec runs now), "k1t_path_effective"
  * (the kernel a 16-column batch runs now; may prepare the K1T-I8 operands), "i8_supported",
  * and "precision" (64 | 32). */
 int krr_get_option(krr_ctx* ctx, const char* key, double* value);

@@ -50,6 +50,7 @@ void gauss_matmat_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const in
                             const double* sqs, const double* v, double* part, int kp, cudaStream_t stream,
                             int debug = 0);
 void i8s_read_trace(long long* out, int count);
+constexpr int64_t kI8T1MinD = 160;  // single-RHS K v through K1T-I8 from d = 160 (when K1-I8 does not apply)
 constexpr int64_t kI8TMinD = 28;  // auto path: K1T-I8 from d = 28 (measured crossover, profiles/r1_k1t_i8_crossover.log)
 
 // K1-I8: tcgen05 kind::i8 slice path (gauss_matvec_i8.cu).  Supported for d <= 96.

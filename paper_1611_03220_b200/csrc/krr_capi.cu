@@ -254,6 +254,50 @@ void f32_ensure(Ctx& c) {
 }
 
 // out (n_pad) = (K + lambda I) v, v zero-padded to n_pad.  Replicated on all ranks.
+void ensure_batched(Ctx& c, int T) {
+    const size_t nt = size_t(c.plan.n_pad) * size_t(T);
+    for (auto* v : {&c.bx, &c.br, &c.bz, &c.bp, &c.bap, &c.by, &c.bin, &c.bout}) v->ensure(nt);
+    c.bpart.ensure(size_t(c.sched.ns) * nt);
+    c.bred.ensure(size_t(3) * 148 * 4 * 16);
+    c.bscal.ensure(128);
+    c.bactive.ensure(16);
+    if (!c.hscalT) {
+        c.hscalT = std::make_unique<PinnedScalars>(128);
+        KRR_CUDA(cudaMallocHost(&c.hactive, 16 * sizeof(int)));
+    }
+}
+
+// K1T path selection: the tcgen05 INT8-slice kernel (K1T-I8, T = 16, Gaussian) where it is
+// faster than the FP64 DMMA K1T (measured crossover, profiles/), else K1T.  Neither is a
+// fallback: both are GPU kernels parity-tested against the oracle.
+bool use_i8T(Ctx& c, int T) {
+    if (T != 16 || c.family != 0 || c.k1t_path == 0 || !i8s_supported(c.d, int(c.sched.st))) return false;
+    if (c.k1t_path < 0 && c.d < kI8TMinD) return false;
+    if (c.i8s_state == 0) {
+        const int64_t n_pad = c.plan.n_pad;
+        c.kp8s = i8s_kp(c.d);
+        c.S8s.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8s));
+        c.ex8s.ensure(size_t(n_pad));
+        c.ejs8s.ensure(size_t(n_pad));
+        c.sq8s.ensure(size_t(n_pad));
+        c.i8s_state = i8s_prepare_launch(c.X.get(), c.n, c.d, n_pad, c.L.get(), c.plan.dp, c.plan.ec.kscale,
+                                         c.S8s.get(), c.ex8s.get(), c.ejs8s.get(), c.sq8s.get(), c.stream)
+                          ? 1
+                          : -1;
+    }
+    return c.i8s_state == 1;
+}
+
+// Single right-hand sides with large d (where K1-I8 does not apply): one real column of a
+// 16-column K1T-I8 pass beats the FP64 DMMA K1 from d ~ 160 (profiles/r1_k1_single_large_d.log:
+// d = 192 27 vs 34 ms, d = 440 43 vs 75 ms at n = 65536).  Prepared outside graph capture.
+bool use_i8T1(Ctx& c) {
+    if (c.precision != 64 || c.family != 0 || c.k1_path == 0 || c.d < kI8T1MinD || use_i8(c)) return false;
+    if (!use_i8T(c, 16)) return false;
+    ensure_batched(c, 16);
+    return true;
+}
+
 void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t k1a = nullptr,
                 cudaEvent_t k1b = nullptr) {
     if (c.precision == 32) f32_ensure(c);
@@ -264,7 +308,19 @@ void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t
     else if (use_i8(c))
         gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.ejs8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
                                c.stream, c.i8_debug, c.family == 1 ? c.degree : 0, c.gamma, c.offset);
-    else
+    else if (use_i8T1(c)) {
+        // v as column 0 of a zero-padded 16-column block through K1T-I8 (+ its finish, lambda,
+        // all-reduce), column 0 back out
+        pad_cols_launch(v, c.n, 1, 0, c.plan.n_pad, 16, c.bin.get(), c.stream);
+        gauss_matmat_i8_launch(c.plan, c.S8s.get(), c.ex8s.get(), c.ejs8s.get(), c.sq8s.get(), c.bin.get(),
+                               c.bpart.get(), c.kp8s, c.stream, c.i8_debug);
+        if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
+        matmat_finish_launch(c.plan, c.bpart.get(), c.bin.get(), 16, lambda, c.k1_rank() == 0 ? 1 : 0, c.bout.get(),
+                             c.stream);
+        allreduce_sum(c, c.bout.get(), c.plan.n_pad * 16);
+        unpad_cols_launch(c.bout.get(), c.n, 1, 0, 16, out, c.stream);
+        return;
+    } else
         gauss_matvec_launch(c.plan, v, c.part.get(), c.family == 1 ? poly_mode(c.degree) : c.exp_mode, c.stream);
     if (k1b) KRR_CUDA(cudaEventRecord(k1b, c.stream));
     matvec_finish_launch(c.plan, c.part.get(), v, lambda, c.k1_rank() == 0 ? 1 : 0, out, c.stream);
@@ -554,6 +610,7 @@ struct PcgOut {
 void pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double norm_y, double tau, int max_iter,
                     double* hist, PcgOut& out) {
     if (c.precision == 32) f32_ensure(c);  // one-off preparation synchronises: not inside the capture
+    use_i8T1(c);                            // (same for the large-d single-column K1T-I8 route)
     const int nb = vec_blocks(n);
     double* red = c.red.get();
     double* pap_part = red;
@@ -696,39 +753,6 @@ PcgOut pcg_core(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, const double*
 // ---------------------------------------------------------------- batched multi-RHS (t > 1)
 int batch_width(int64_t t) { return t <= 8 ? 8 : 16; }
 
-void ensure_batched(Ctx& c, int T) {
-    const size_t nt = size_t(c.plan.n_pad) * size_t(T);
-    for (auto* v : {&c.bx, &c.br, &c.bz, &c.bp, &c.bap, &c.by, &c.bin, &c.bout}) v->ensure(nt);
-    c.bpart.ensure(size_t(c.sched.ns) * nt);
-    c.bred.ensure(size_t(3) * 148 * 4 * 16);
-    c.bscal.ensure(128);
-    c.bactive.ensure(16);
-    if (!c.hscalT) {
-        c.hscalT = std::make_unique<PinnedScalars>(128);
-        KRR_CUDA(cudaMallocHost(&c.hactive, 16 * sizeof(int)));
-    }
-}
-
-// K1T path selection: the tcgen05 INT8-slice kernel (K1T-I8, T = 16, Gaussian) where it is
-// faster than the FP64 DMMA K1T (measured crossover, profiles/), else K1T.  Neither is a
-// fallback: both are GPU kernels parity-tested against the oracle.
-bool use_i8T(Ctx& c, int T) {
-    if (T != 16 || c.family != 0 || c.k1t_path == 0 || !i8s_supported(c.d, int(c.sched.st))) return false;
-    if (c.k1t_path < 0 && c.d < kI8TMinD) return false;
-    if (c.i8s_state == 0) {
-        const int64_t n_pad = c.plan.n_pad;
-        c.kp8s = i8s_kp(c.d);
-        c.S8s.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8s));
-        c.ex8s.ensure(size_t(n_pad));
-        c.ejs8s.ensure(size_t(n_pad));
-        c.sq8s.ensure(size_t(n_pad));
-        c.i8s_state = i8s_prepare_launch(c.X.get(), c.n, c.d, n_pad, c.L.get(), c.plan.dp, c.plan.ec.kscale,
-                                         c.S8s.get(), c.ex8s.get(), c.ejs8s.get(), c.sq8s.get(), c.stream)
-                          ? 1
-                          : -1;
-    }
-    return c.i8s_state == 1;
-}
 
 // out (n_pad x T) = (K + lambda I) v (n_pad x T), replicated on all ranks.
 void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
@@ -1277,7 +1301,7 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
             *value = c.precision;
         } else if (k == "k1_path_effective") {  // the K1 kernel a mat-vec runs now
             krr::require_data(c);
-            *value = krr::use_i8(c) ? 1.0 : 0.0;
+            *value = krr::use_i8(c) ? 1.0 : (krr::use_i8T1(c) ? 2.0 : 0.0);
         } else if (k == "k1t_path") {
             *value = c.k1t_path;
         } else if (k == "k1t_path_effective") {  // the K1T kernel a 16-column batch runs now

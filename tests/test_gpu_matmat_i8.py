@@ -89,3 +89,41 @@ def test_k1t_i8_not_used_for_polynomial(krr, oracle, ctx):
     ctx.set_option("k1t_path", 1)
     krr.KernelOperator(x, krr.KernelSpec.polynomial(1.0 / 90, 1.0, 3), 0.0, ctx=ctx)
     assert ctx.get_option("k1t_path_effective") == 0
+
+
+@pytest.mark.parametrize("n,d,sigma", [(700, 200, 12.0), (4097, 160, 10.0), (5000, 440, 20.0)])
+def test_single_rhs_large_d_through_k1t_i8(krr, oracle, ctx, n, d, sigma):
+    """d >= 160 (K1-I8 does not apply above d = 96): a single K v runs as column 0 of a
+    16-column K1T-I8 pass (k1_path_effective = 2); same bar as every K1 path."""
+    x = oracle.random_matrix(n, d, 8 + n)
+    v = oracle.random_vector(n, 9 + n)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(sigma), 1e-3, ctx=ctx)
+    assert ctx.get_option("k1_path_effective") == 2
+    got = op(v)
+    for r0, r1 in {(0, min(n, 40)), (max(0, n - 40), n)}:
+        want = oracle.kernel_matvec(x, sigma, 1e-3, v, rows=(r0, r1))
+        assert rel(got[r0:r1], want) <= 1e-13, (r0, rel(got[r0:r1], want))
+    ctx.set_option("k1_path", 0)
+    try:
+        assert ctx.get_option("k1_path_effective") == 0
+        dmma = op(v)
+    finally:
+        ctx.set_option("k1_path", -1)
+    assert rel(got, dmma) <= 1e-13
+
+
+def test_train_large_d_graph_loop_matches_oracle(krr, oracle, ctx):
+    """The graph-resident PCG loop with the large-d single-column K1T-I8 operator (prepared
+    before capture) reproduces the oracle's train.  sigma = 8 at d = 200 keeps the solve well
+    conditioned (a few tens of iterations), away from the round-off-sensitive regime where even
+    two CPU summation orders disagree on the stopping iteration."""
+    n, d, sigma, lam = 1200, 200, 8.0, 0.1
+    x = oracle.random_matrix(n, d, 31)
+    y = oracle.random_matrix(n, 1, 32)
+    cfg = krr.SolverConfig(lambda_=lam, tau=1e-8, max_iter=500, chain=krr.ChainSpec(s1=256), seed=0)
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), cfg, ctx=ctx)
+    assert ctx.get_option("k1_path_effective") == 2
+    ref = oracle.train(x, y, sigma, lam, 256, 0, 1e-8, 500)
+    st = res.report.per_rhs[0]
+    assert st.converged and abs(st.iterations - ref.iterations[0]) <= 1, (st.iterations, ref.iterations[0])
+    assert rel(res.model.c, ref.c) <= 1e-8, rel(res.model.c, ref.c)
