@@ -424,7 +424,6 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++tq) {
                 const uint32_t ph = uint32_t(tq & 1);
                 I8_TRACE(etid == 0, tq, 0);
-                double* cdst = A.part + int64_t(sa) * A.n_pad + colBase + int64_t(jt) * TJ + etid;
 
                 // ---- drain the 8 groups in MMA completion order (7 -> 0) two at a time,
                 // 16 columns per tcgen05.ld (register pressure), releasing each pair at once
@@ -505,6 +504,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 epi_bar();
                 I8_TRACE(etid == 0, tq, 7);
                 if (etid < TJ) {
+                    double* cdst = A.part + int64_t(sa) * A.n_pad + colBase + int64_t(jt) * TJ + etid;
                     // the column's running sum (owner thread, same thread every pass), read here rather
                     // than prefetched before the drain: a shorter live range (fewer spills, +0.8 %)
                     const double cprev = it > 0 ? *cdst : 0.0;
