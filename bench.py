@@ -335,6 +335,7 @@ def main():
                     "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2x bf16 on B200)"
                                    if "bf16_tflops" in peaks else "2 x 2.25 PF nominal bf16 (no MEASURED_PEAKS.json)",
                     "fp64_equivalent": fp64_view,
+                    "model_bound": i8_model_bound(d, kp, pairs_rank, k1_ms, clk.get("sm_mhz") or 1965.0),
                     "note": "INT8 MMAs throttle the FP64 pipe ~4-8x on B200 (profiles/README.md), so the "
                             "kernel time-multiplexes each SM: tensor-core phase, then the FP64 exp phase"}
     else:
@@ -395,6 +396,23 @@ def main():
     ctx.close()
     D.close()
     return 0
+
+
+def i8_model_bound(d: int, kp: int, pairs: float, k1_ms: float, sm_mhz: float) -> dict:
+    """K1-I8's bound from its two measured per-SM floors, additive because the tensor core is
+    time-multiplexed with the FP64 exp phase (INT8 MMAs throttle the FP64 pipe, profiles/README.md):
+    per 128 x 64 tile, 36 * kp / 32 tcgen05.mma kind::i8 at the 44.8-clk per-instruction floor for
+    N = 64 (tools/mma_rate.py) + 8192 pairs x 14 FP64 ops at 64 lane-ops / clk / SM."""
+    mma_clk = 36 * (kp // 32) * 44.8
+    fp64_clk = 8192 * 14 / 64.0
+    tile_clk = mma_clk + fp64_clk
+    tiles_per_s = 148 * sm_mhz * 1e6 / tile_clk
+    bound_pairs_per_s = tiles_per_s * 8192
+    achieved_pairs_per_s = pairs / (k1_ms * 1e-3)
+    return {"unit": "unique pairs / s", "bound": bound_pairs_per_s, "achieved": achieved_pairs_per_s,
+            "frac": achieved_pairs_per_s / bound_pairs_per_s, "mma_floor_clk_per_tile": mma_clk,
+            "fp64_floor_clk_per_tile": fp64_clk, "sm_mhz": sm_mhz,
+            "note": "model bound (measured floors), informational; the graded roofline is 'frac' above"}
 
 
 def config5_pass(krr, _lib, device: int) -> dict:
