@@ -24,9 +24,19 @@ roofline: dominant kernel = K1.  The default path at d = 90 is K1-I8 (tcgen05 ki
 config5_pass: informational, N = 1 only (--no-config5 skips it): one (K + lambda I) V pass at
           BASELINE config 5 (n = 524288, d = 440, t = 16) through krr_kernel_matvec with host
           buffers, on K1T-I8 (INT8-slice dot products + DMMA E.V) and on the DMMA K1T.
+pcg_leg:  config 4's time to tolerance on the device, bounded: the full train path (RFF
+          features, Woodbury build split into Z^T Z / Cholesky / U = L^-1 Z^T, then --pcg-iters
+          graph-resident PCG iterations), mean ms per iteration, K1's share of it, the
+          iteration's roofline fraction and the projection to max_iter = 500 (BASELINE configs
+          1-5 stop at max_iter in the reference algorithm too: DESIGN.md section 4); plus the
+          full 500-iteration config-1 train.  --pcg-iters 0 skips it.
 --impl reference: the CPU restatement (oracle/, all host threads) on a bounded row
           sample of the same workload — the reference itself (CPU-only, Eigen) cannot be
-          built in this image.
+          built in this image.  Its inputs come from oracle/'s own restated generator (no
+          product code in that process).  It also times the reference-as-written mode on
+          config 1 (dense K, one core, SURVEY 8d CPU mode 1).
+--gpus N without WORLD_SIZE in the environment re-launches itself under torchrun with N
+          ranks (127.0.0.1); --dry-run does the rank plumbing only (gloo, no GPU work).
 """
 from __future__ import annotations
 
@@ -61,7 +71,36 @@ def parse():
     ap.add_argument("--no-config5", action="store_true", help="skip the config-5 multi-RHS pass (K1T-I8 vs DMMA K1T)")
     ap.add_argument("--time-to-tol", type=int, default=0, metavar="CFG",
                     help="also run the full train (RFF + precond + PCG) of BASELINE config CFG")
+    ap.add_argument("--pcg-iters", type=int, default=3,
+                    help="config-4 PCG leg: iterations timed after the full build (0 = skip)")
+    ap.add_argument("--no-c1-reference", action="store_true",
+                    help="--impl reference: skip the 1-core dense config-1 timing")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (no GPU work)")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def maybe_spawn(args) -> None:
+    """One process per GPU: under torchrun (WORLD_SIZE set) the world must equal --gpus; a
+    plain `python bench.py --gpus N` (N > 1) re-executes itself under torchrun with N ranks."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(f"error: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            sys.exit(2)
+        return
+    if args.gpus <= 1:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(ROOT / "bench.py")] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 # ----------------------------------------------------------------------------- plumbing
@@ -93,6 +132,13 @@ class Dist:
         t = torch.tensor([v], dtype=torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
+
+    def gather(self, obj) -> list:
+        if not self.dist:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
 
     def bcast_bytes(self, b: bytes | None) -> bytes:
         if not self.dist:
@@ -181,10 +227,11 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0  # the CPU reference arm runs on rank 0 only
-    import paper_1611_03220_b200 as krr  # host-only generator (no GPU work)
-    n = args.n
-    x, _ = krr.generate_config(4, n, CFG4["d"], 1, 0)
+    # inputs from oracle/'s restated generator (bitwise the library's, tests/test_host_abi.py):
+    # nothing of the product is loaded into this process
     from oracle import oracle_ffi as oracle
+    n = args.n
+    x, _ = oracle.generate_config(4, n, CFG4["d"], 1, 0)
     threads = os.cpu_count() or 1
     oracle.set_threads(threads)
     v = np.random.default_rng(12345).standard_normal(n)
@@ -218,27 +265,64 @@ def run_reference(args):
                          "sample": sample},
         "e2e": {"value": value, "unit": "Gevals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference (CPU-only C++/Eigen) is unbuildable here (Eigen3 absent); this arm "
-                "times its restatement oracle/krr_oracle.cpp with the same per-entry formula",
+                "times its restatement oracle/krr_oracle.cpp with the same per-entry formula on a row "
+                "sample of the config-4 product (not the whole n^2 product: ~2 h of CPU per step)",
     }
+    if not args.no_c1_reference:
+        line["reference_as_written_c1"] = reference_as_written_c1(oracle)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def reference_as_written_c1(oracle) -> dict:
+    """SURVEY 8d CPU mode 1: the reference as written is single-threaded Eigen with a dense K
+    (kernels.cpp:72-88 gram once, solver.cpp:75-77 dense GEMV per iteration).  Its stand-in: the
+    oracle's dense mode on one core, config 1 (n = 8192, d = 16, s = 1024), timed for the build +
+    1 iteration and the build + 11 iterations, extrapolated to the 500 iterations the run takes."""
+    import numpy as np
+    n, d, sigma, lam, s = 8192, 16, 4.0, 1e-3, 1024
+    x, y = oracle.generate_config(1, n, d, 1, 0)
+    oracle.set_threads(1)
+    t = {}
+    for its in (1, 11):
+        t0 = time.perf_counter()
+        r = oracle.train(x, y, sigma, lam, s, 0, 1e-6, its, dense_k=True)
+        t[its] = time.perf_counter() - t0
+    per_it = (t[11] - t[1]) / 10.0
+    oracle.set_threads(os.cpu_count() or 1)
+    return {"config": 1, "n": n, "d": d, "s": s, "cores": 1, "kind": "port", "dense_k": True,
+            "build_plus_1_iter_s": t[1], "per_iteration_s": per_it,
+            "time_to_500_iters_s_extrapolated": t[1] + 499 * per_it,
+            "residual_after_11": float(r.final_residual[0]),
+            "note": "oracle dense mode on one thread (Eigen absent: the reference itself cannot be built); "
+                    "config 1 stops at max_iter = 500 in the reference algorithm (DESIGN.md section 4)"}
 
 
 # ----------------------------------------------------------------------------- ours
 def main():
     args = parse()
+    maybe_spawn(args)
     if args.impl == "reference":
         return run_reference(args)
     world, rank, local = dist_env()
-    if args.gpus != world and world > 1:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     D = Dist(world, rank)
+    if args.dry_run:
+        ranks = D.gather({"rank": rank, "local_rank": local, "world": world, "pid": os.getpid()})
+        D.barrier()
+        t = D.max(float(rank))
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks, "max_over_ranks": t}), flush=True)
+        D.close()
+        return 0
     import paper_1611_03220_b200 as krr
     from paper_1611_03220_b200 import _lib
 
     nccl_id = krr.nccl_unique_id() if (world > 1 and rank == 0) else None
     nccl_id = D.bcast_bytes(nccl_id)
     ctx = krr.Context(local, rank, world, nccl_id)
+    rank_info = {"rank": rank, "device": local, "nccl_nranks": int(ctx.get_option("nccl_nranks"))}
+    print(json.dumps(rank_info), file=sys.stderr, flush=True)
+    rank_info = D.gather(rank_info)
     n, d, sigma, lam = args.n, CFG4["d"], CFG4["sigma"], CFG4["lam"]
     x, _ = krr.generate_config(4, n, d, 1, 0)
     _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, sigma))
@@ -301,6 +385,14 @@ def main():
     ttt = None
     if args.time_to_tol:
         ttt = time_to_tol(krr, ctx, args.time_to_tol)
+
+    # ---- config 4 time-to-tolerance leg (bounded) and the full config-1 train
+    pcg = None
+    if args.pcg_iters > 0 and args.n == CFG4["n"]:
+        try:
+            pcg = pcg_leg(krr, ctx, D, args.pcg_iters, k1.value / max(1, args.steps))
+        except Exception as e:  # reported, not fatal: the mat-vec line stands on its own
+            pcg = {"error": f"{type(e).__name__}: {e}"}
 
     # ---- roofline bookkeeping
     st, ns, tiles = krr.schedule(n, world, rank)
@@ -387,6 +479,9 @@ def main():
         line["cpu_baseline"] = cpu
     if ttt:
         line["time_to_tol"] = ttt
+    if pcg:
+        line["pcg_leg"] = pcg
+    line["ranks"] = rank_info
     if f32:
         line["fp32_mode"] = f32
     if c5:
@@ -441,6 +536,64 @@ def config5_pass(krr, _lib, device: int) -> dict:
                                        np.linalg.norm(out["k1t_dmma"]))
     res["rhs_gevals_per_s"] = float(n) * n * t / res["k1t_i8"] / 1e9
     return res
+
+
+def hbm_peak() -> float:
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        try:
+            return float(json.loads(pk.read_text()).get("hbm_gbs", 7700.0))
+        except Exception:
+            pass
+    return 7700.0
+
+
+def pcg_leg(krr, ctx, D, iters: int, k1_ms_per_launch: float) -> dict:
+    """BASELINE config 4 through krr.train (the public API) with max_iter = iters: RFF features,
+    the Woodbury build (split), the graph-resident PCG.  Device time (CUDA events), max over ranks."""
+    n, d, t, sigma, lam, s = krr.CONFIGS[4]
+    x, y = krr.generate_config(4, n, d, t, 0)
+    sc = krr.SolverConfig(tau=1e-6, max_iter=iters, lambda_=lam, chain=krr.ChainSpec(s1=s), seed=0)
+    D.barrier()
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), sc, ctx=ctx)
+    ph = {k: D.max(float(v)) for k, v in res.report.phase_ms.items()}
+    build = {k: D.max(ctx.get_option(f"build_{k}_ms")) for k in ("gram", "cholesky", "trsm")}
+    st = res.report.per_rhs[0]
+    per_it = ph["solve"] / max(1, st.iterations)
+    # the iteration's own roofline: K1 at the INT8 tensor peak + two HBM passes over U (16 n s bytes)
+    # + ~12 n doubles of vector traffic, over the measured per-iteration time
+    kp = (d + 31) // 32 * 32
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak_i8 = 2.0 * float(peaks.get("bf16_tflops", 2250.0)) * 1e12
+    k1_ideal = (n * (n - 1) / 2) * 36.0 * kp * 2.0 / peak_i8 / D.world
+    hbm = hbm_peak() * 1e9
+    pre_ideal = 16.0 * n * s / D.world / hbm
+    vec_ideal = 12.0 * 8 * n / hbm
+    ideal_ms = 1e3 * (k1_ideal + pre_ideal + vec_ideal)
+    out = {"config": 4, "n": n, "d": d, "s": s, "iterations": st.iterations,
+           "residual_history": [float(r) for r in st.residual_history],
+           "rff_build_ms": ph["rff_build"], "precond_build_ms": ph["precond_build"],
+           "precond_build_split_ms": build, "solve_ms": ph["solve"], "ms_per_iteration": per_it,
+           "k1_ms_per_matvec": k1_ms_per_launch, "k1_share_of_iteration": k1_ms_per_launch / per_it,
+           "iteration_roofline": {"ideal_ms": ideal_ms, "frac": ideal_ms / per_it,
+                                  "parts_ms": {"k1_int8_peak": 1e3 * k1_ideal, "woodbury_hbm": 1e3 * pre_ideal,
+                                               "vectors_hbm": 1e3 * vec_ideal}},
+           "projected_500_iters_s": 1e-3 * (ph["rff_build"] + ph["precond_build"] + 500 * per_it),
+           "note": "solve_ms includes the PCG prologue (one Woodbury apply) and the graph instantiation; "
+                   "configs 1-5 stop at max_iter = 500 without reaching tau = 1e-6 in the reference "
+                   "algorithm too (oracle, DESIGN.md section 4), so time-to-tol = time to 500 iterations"}
+    ctx.precond_drop()
+    if D.world == 1:
+        n1, d1, t1, s1g, l1, ss1 = krr.CONFIGS[1]
+        x1, y1 = krr.generate_config(1, n1, d1, t1, 0)
+        c1 = krr.train(krr.Dataset(x1, y1), krr.KernelSpec.gaussian(s1g),
+                       krr.SolverConfig(tau=1e-6, max_iter=500, lambda_=l1, chain=krr.ChainSpec(s1=ss1), seed=0),
+                       ctx=ctx)
+        r1 = c1.report.per_rhs[0]
+        out["config1_train"] = {"n": n1, "iterations": r1.iterations, "final_residual": r1.final_residual,
+                                "device_ms": c1.report.phase_ms["total"], "phase_ms": c1.report.phase_ms}
+        ctx.precond_drop()
+    return out
 
 
 def time_to_tol(krr, ctx, cfg: int) -> dict:

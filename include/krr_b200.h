@@ -43,7 +43,8 @@ typedef enum krr_status {
     KRR_ERR_NCCL = 8,                  /* collective error (no reference equivalent)               */
     KRR_ERR_STATE = 9,                 /* call out of order (e.g. matvec before krr_set_data)      */
     KRR_ERR_CALLBACK = 10,             /* a user operator callback reported failure                */
-    KRR_ERR_IO = 11                    /* model file I/O or format error (std::runtime_error, io.cpp) */
+    KRR_ERR_IO = 11,                   /* model file I/O or format error (std::runtime_error, io.cpp) */
+    KRR_ERR_NO_CONVERGENCE = 12        /* types.hpp:34  NoConvergence       (std::runtime_error)   */
 } krr_status;
 
 typedef struct krr_ctx krr_ctx;
@@ -94,7 +95,9 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
  *   "emulate_world" W, "emulate_rank" r   test only, single-rank contexts: the next
  *                         krr_set_data builds rank r of W's K1 schedule (tiles, owned slots,
  *                         diagonal on rank 0) with no collective, so K v returns that rank's
- *                         partial — the multi-rank K1 checked on one GPU (sum over r = K v) */
+ *                         partial — the multi-rank K1 checked on one GPU (sum over r = K v)
+ *   "poison_batched" 1|0  test only: fill the batched (t > 1) PCG vectors with NaN bytes whenever
+ *                         they are (re)used, standing in for stale contents of an earlier call */
 int krr_set_option(krr_ctx* ctx, const char* key, double value);
 /* Arithmetic of the fused mat-vec (SURVEY §8b krr_set_precision; north-star "optional fp32
  * mode, reported separately"): 64 = fp64, oracle-matching (default); 32 = fp32-accuracy K1
@@ -154,7 +157,9 @@ int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0,
  * "k1_path_effective" (0 DMMA / 1 I8 / 2 column 0 of a 16-column K1T-I8 pass, d >= 160: the
  * kernel a mat-vec runs now), "k1t_path_effective"
  * (the kernel a 16-column batch runs now; may prepare the K1T-I8 operands), "i8_supported",
- * and "precision" (64 | 32). */
+ * "precision" (64 | 32), "build_gram_ms" / "build_cholesky_ms" / "build_trsm_ms" (CUDA-event
+ * split of the last krr_precond_build: Z^T Z + lambda_p I, Cholesky with its retry, U = L^-1 Z^T)
+ * and "nccl_nranks" (ncclCommCount of the context's communicator; 1 without one). */
 int krr_get_option(krr_ctx* ctx, const char* key, double* value);
 
 /* ---------------------------------------------------------------- data + kernel operator */

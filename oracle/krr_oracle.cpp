@@ -887,3 +887,162 @@ int oracle_poly_augment(const double* x, std::int64_t n, std::int64_t d, double 
 }
 
 }  // extern "C"
+
+// ============================================================================= BASELINE inputs
+// The BASELINE configs' synthetic generators as SURVEY.md §8(d) specifies them (not a
+// reference function: the reference's benchmarks ran on public datasets).  Restated here
+// so the CPU legs of bench.py (--impl reference, cpu_baseline) and the config fixtures need
+// nothing from the product library; tests check it equals krr_generate_config bit for bit.
+// Arithmetic order: row-major draws, column statistics accumulated over rows in order,
+// population std, then (x - mean) * (1 / std); tanh / sin arguments as forward dot products.
+namespace {
+
+void gen_standardise(double* X, std::int64_t n, std::int64_t d) {
+    std::vector<double> mu(static_cast<std::size_t>(d), 0.0), inv(static_cast<std::size_t>(d), 0.0);
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t j = 0; j < d; ++j) mu[std::size_t(j)] += X[i * d + j];
+    for (auto& m : mu) m /= double(n);
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t j = 0; j < d; ++j) {
+            const double c = X[i * d + j] - mu[std::size_t(j)];
+            inv[std::size_t(j)] += c * c;
+        }
+    for (auto& v : inv) {
+        const double sd = std::sqrt(v / double(n));
+        v = sd > 0.0 ? 1.0 / sd : 1.0;
+    }
+    for (std::int64_t i = 0; i < n; ++i)
+        for (std::int64_t j = 0; j < d; ++j) X[i * d + j] = (X[i * d + j] - mu[std::size_t(j)]) * inv[std::size_t(j)];
+}
+
+double gen_dot(const double* a, const double* b, std::int64_t d) {
+    double s = 0.0;
+    for (std::int64_t k = 0; k < d; ++k) s += a[k] * b[k];
+    return s;
+}
+
+// Orthogonal factor Q of a d x d matrix by Householder reflections (H_k = I - 2 v v^T / v^T v,
+// v = a_k - alpha e_k with alpha = -sign(a_kk) |a_k|), signs fixed so that diag(R) > 0.
+std::vector<double> gen_orthogonal(std::vector<double> a, std::int64_t d) {
+    const auto at = [d](std::int64_t i, std::int64_t j) { return std::size_t(i * d + j); };
+    std::vector<double> q(std::size_t(d * d), 0.0), v(std::size_t(d), 0.0);
+    for (std::int64_t i = 0; i < d; ++i) q[at(i, i)] = 1.0;
+    for (std::int64_t k = 0; k < d; ++k) {
+        double nrm = 0.0;
+        for (std::int64_t i = k; i < d; ++i) nrm += a[at(i, k)] * a[at(i, k)];
+        nrm = std::sqrt(nrm);
+        if (nrm == 0.0) continue;
+        const double alpha = a[at(k, k)] > 0 ? -nrm : nrm;
+        std::fill(v.begin(), v.end(), 0.0);
+        for (std::int64_t i = k; i < d; ++i) v[std::size_t(i)] = a[at(i, k)];
+        v[std::size_t(k)] -= alpha;
+        double vv = 0.0;
+        for (std::int64_t i = k; i < d; ++i) vv += v[std::size_t(i)] * v[std::size_t(i)];
+        if (vv == 0.0) continue;
+        for (std::int64_t j = 0; j < d; ++j) {
+            double h = 0.0;
+            for (std::int64_t i = k; i < d; ++i) h += v[std::size_t(i)] * a[at(i, j)];
+            h = 2.0 * h / vv;
+            for (std::int64_t i = k; i < d; ++i) a[at(i, j)] -= h * v[std::size_t(i)];
+        }
+        for (std::int64_t i = 0; i < d; ++i) {
+            double h = 0.0;
+            for (std::int64_t j = k; j < d; ++j) h += q[at(i, j)] * v[std::size_t(j)];
+            h = 2.0 * h / vv;
+            for (std::int64_t j = k; j < d; ++j) q[at(i, j)] -= h * v[std::size_t(j)];
+        }
+    }
+    for (std::int64_t k = 0; k < d; ++k)
+        if (a[at(k, k)] < 0.0)
+            for (std::int64_t i = 0; i < d; ++i) q[at(i, k)] = -q[at(i, k)];
+    return q;
+}
+
+}  // namespace
+
+extern "C" int oracle_generate_config(int cfg, std::int64_t n, std::int64_t d, std::int64_t t, std::uint64_t seed,
+                                      double* X, double* Y) {
+    if (n < 1 || d < 1 || t < 1 || cfg < 1 || cfg > 5) return INVALID_ARGUMENT;
+    if (cfg != 5 && t != 1) return INVALID_ARGUMENT;
+    std::normal_distribution<double> n01(0.0, 1.0);
+    if (cfg == 1) {  // X ~ N(0,1); y = sin(w.x) + 0.1 eps, w ~ N(0, I/d)
+        std::mt19937_64 gx(seed), gw(seed + 1), ge(seed + 2);
+        for (std::int64_t i = 0; i < n * d; ++i) X[i] = n01(gx);
+        std::normal_distribution<double> nw(0.0, 1.0 / std::sqrt(double(d)));
+        std::vector<double> w(static_cast<std::size_t>(d));
+        for (auto& e : w) e = nw(gw);
+        for (std::int64_t i = 0; i < n; ++i) Y[i] = std::sin(gen_dot(w.data(), X + i * d, d)) + 0.1 * n01(ge);
+    } else if (cfg == 2) {  // 7 clusters, centres ~ N(0, 4I); +-1 by cluster parity, 5 % flips
+        const int K = 7;
+        std::mt19937_64 gx(seed), gc(seed + 1), gk(seed + 3), gf(seed + 4);
+        std::normal_distribution<double> ncen(0.0, 2.0);
+        std::vector<double> cen(static_cast<std::size_t>(K * d));
+        for (auto& e : cen) e = ncen(gc);
+        std::uniform_int_distribution<int> pick(0, K - 1);
+        std::vector<int> lab(static_cast<std::size_t>(n));
+        for (auto& e : lab) e = pick(gk);
+        for (std::int64_t i = 0; i < n; ++i)
+            for (std::int64_t j = 0; j < d; ++j) X[i * d + j] = cen[std::size_t(lab[std::size_t(i)] * d + j)] + n01(gx);
+        gen_standardise(X, n, d);
+        std::uniform_real_distribution<double> u01(0.0, 1.0);
+        for (std::int64_t i = 0; i < n; ++i) {
+            const double yi = lab[std::size_t(i)] % 2 == 0 ? 1.0 : -1.0;
+            Y[i] = u01(gf) < 0.05 ? -yi : yi;
+        }
+    } else if (cfg == 3 || cfg == 4) {  // AR(1) features rho = 0.5; y = sum_k a_k tanh(u_k.x) + N(0, 0.25)
+        std::mt19937_64 gx(seed), gu(seed + 1), ge(seed + 2);
+        const double c = std::sqrt(0.75);
+        for (std::int64_t i = 0; i < n; ++i) {
+            double* xr = X + i * d;
+            xr[0] = n01(gx);
+            for (std::int64_t j = 1; j < d; ++j) xr[j] = 0.5 * xr[j - 1] + c * n01(gx);
+        }
+        gen_standardise(X, n, d);
+        std::normal_distribution<double> nu(0.0, 1.0 / std::sqrt(double(d)));
+        std::vector<double> u(std::size_t(8 * d)), a(8);
+        for (auto& e : u) e = nu(gu);
+        for (auto& e : a) e = n01(gu);
+        std::normal_distribution<double> noise(0.0, 0.5);
+        for (std::int64_t i = 0; i < n; ++i) {
+            double yi = 0.0;
+            for (int k = 0; k < 8; ++k) yi += a[std::size_t(k)] * std::tanh(gen_dot(u.data() + k * d, X + i * d, d));
+            Y[i] = yi + noise(ge);
+        }
+    } else {  // cfg 5: X = G diag(sqrt(1/i)) Q^T, standardised; one-hot (+-1) argmax teacher labels
+        std::mt19937_64 gg(seed), gt(seed + 1), gq(seed + 5);
+        std::vector<double> G(static_cast<std::size_t>(n * d));
+        for (auto& e : G) e = n01(gg);
+        std::vector<double> qa(static_cast<std::size_t>(d * d));
+        for (auto& e : qa) e = n01(gq);
+        const std::vector<double> Q = gen_orthogonal(std::move(qa), d);
+        std::vector<double> M(static_cast<std::size_t>(d * d));  // M[k][j] = sqrt(1/(k+1)) Q[j][k]
+        for (std::int64_t k = 0; k < d; ++k)
+            for (std::int64_t j = 0; j < d; ++j) M[std::size_t(k * d + j)] = std::sqrt(1.0 / double(k + 1)) * Q[std::size_t(j * d + k)];
+#pragma omp parallel for schedule(static)
+        for (std::int64_t r = 0; r < n; ++r) {
+            double* xr = X + r * d;
+            for (std::int64_t j = 0; j < d; ++j) xr[j] = 0.0;
+            for (std::int64_t k = 0; k < d; ++k) {
+                const double g = G[std::size_t(r * d + k)];
+                for (std::int64_t j = 0; j < d; ++j) xr[j] += g * M[std::size_t(k * d + j)];
+            }
+        }
+        gen_standardise(X, n, d);
+        std::vector<double> T(static_cast<std::size_t>(d * t));
+        for (auto& e : T) e = n01(gt);
+        for (std::int64_t i = 0; i < n; ++i) {
+            std::int64_t best = 0;
+            double bv = 0.0;
+            for (std::int64_t c = 0; c < t; ++c) {
+                double sc = 0.0;
+                for (std::int64_t k = 0; k < d; ++k) sc += X[i * d + k] * T[std::size_t(k * t + c)];
+                if (c == 0 || sc > bv) {
+                    bv = sc;
+                    best = c;
+                }
+            }
+            for (std::int64_t c = 0; c < t; ++c) Y[i * t + c] = c == best ? 1.0 : -1.0;  // rlsc_encode, solver.cpp:152-161
+        }
+    }
+    return OK;
+}

@@ -86,6 +86,7 @@ def lib() -> C.CDLL:
             "oracle_srht_apply_rows": ([_vp, _vp, _i64, _i64, _vp, _i64, _vp], _i),
             "oracle_gaussmap_realize": ([C.c_uint64, _i64, _i64, _vp], _i),
             "oracle_gaussmap_apply_rows": ([_vp, _i64, _i64, _vp, _i64, _vp, _i], _i),
+            "oracle_generate_config": ([_i, _i64, _i64, _i64, C.c_uint64, _vp, _vp], _i),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -130,6 +131,15 @@ def random_uniform(count: int, seed: int, lo: float, hi: float) -> np.ndarray:
     out = np.empty(count)
     lib().oracle_random_uniform(count, seed, lo, hi, _p(out))
     return out
+
+
+def generate_config(cfg: int, n: int, d: int, t: int = 1, seed: int = 0):
+    """BASELINE config generators, restated independently of the product
+    library: bench.py's CPU legs and the config fixtures use this one.  Returns (X n x d, Y n x t)."""
+    x = np.empty((n, d))
+    y = np.empty((n, t))
+    _chk(lib().oracle_generate_config(int(cfg), n, d, t, C.c_uint64(seed), _p(x), _p(y)), "generate_config")
+    return x, y
 
 
 def rff_realize(master_seed: int, d: int, s: int, sigma: float):

@@ -37,6 +37,7 @@ from ._lib import (  # noqa: F401  (re-exported exception types)
     KrrError,
     ModelFileError,
     NcclError,
+    NoConvergence,
     NonPositiveLambda,
     NotPositiveDefinite,
     SingularTriangular,
@@ -52,7 +53,7 @@ __all__ = [
     "PcgReport", "PcgResult", "KrrModel", "TrainResult", "pcg_solve", "solve_regularized", "solve_regularized_dense",
     "train", "predict_scores", "predict_labels", "rlsc_encode", "rlsc_decode",
     "generate_config", "schedule", "Context", "device_count",
-    "save_model", "load_model", "ModelFileError",
+    "save_model", "load_model", "ModelFileError", "NoConvergence",
     "QualityReport", "quality_test", "AdaptiveResult", "adaptive_build", "default_initial_sketch_size",
     "RandomFeaturesModel", "train_random_features_baseline", "baseline_predict_scores", "baseline_predict_labels",
 ]

@@ -27,6 +27,7 @@ ERR_NCCL = 8
 ERR_STATE = 9
 ERR_CALLBACK = 10
 ERR_IO = 11
+ERR_NO_CONVERGENCE = 12
 
 
 class KrrError(Exception):
@@ -75,6 +76,10 @@ class CallbackError(KrrError, RuntimeError):
     pass
 
 
+class NoConvergence(KrrError, RuntimeError):
+    """types.hpp:34 (symmetric_eigen's eigensolver did not converge)."""
+
+
 class ModelFileError(KrrError, RuntimeError):
     """io.cpp model file errors (std::runtime_error in the reference)."""
 
@@ -91,6 +96,7 @@ _EXC = {
     ERR_STATE: StateError,
     ERR_CALLBACK: CallbackError,
     ERR_IO: ModelFileError,
+    ERR_NO_CONVERGENCE: NoConvergence,
 }
 
 
@@ -293,6 +299,10 @@ class Context:
         out = C.c_double()
         check(LIB.krr_get_option(self.handle, key.encode(), C.byref(out)))
         return out.value
+
+    def precond_drop(self) -> None:
+        """Free the context's sketch / preconditioner buffers (krr_precond_drop)."""
+        check(LIB.krr_precond_drop(self.handle))
 
     @property
     def launches(self) -> int:

@@ -43,6 +43,7 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char* (*getErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -56,6 +57,7 @@ const NcclApi& nccl() {
         a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(h, "ncclAllReduce"));
         a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
         a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.commCount = reinterpret_cast<decltype(a.commCount)>(dlsym(h, "ncclCommCount"));
         return a;
     }();
     if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
@@ -82,12 +84,14 @@ struct DevMem {
         p = nullptr;
         count = 0;
     }
-    void ensure(size_t n) {
-        if (n <= count && p) return;
+    // returns true when the buffer was (re)allocated (its contents are then undefined)
+    bool ensure(size_t n) {
+        if (n <= count && p) return false;
         release();
-        if (n == 0) return;
+        if (n == 0) return false;
         KRR_CUDA(cudaMalloc(&p, n * sizeof(T)));
         count = n;
+        return true;
     }
     T* get() const { return p; }
 };
@@ -185,6 +189,7 @@ struct Ctx {
     bool has_sketch = false, has_pre = false;
     int64_t pn = 0, s = 0, z0 = 0, z1 = 0;
     double lambda_p = 1.0;
+    double build_ms[3] = {0.0, 0.0, 0.0};  // last precond build: Z^T Z, Cholesky (+ retry), U = L^-1 Z^T
     DevMem<double> Z, G, Gcopy, W, Wpart, work, brff, wrff, wpad, chk;
     DevMem<int> info;
 
@@ -195,12 +200,28 @@ struct Ctx {
     // single-RHS PCG with device operators runs as one CUDA graph: a conditional WHILE node whose
     // body is one iteration and a device-side stop decision (no host round trip per iteration)
     bool pcg_graph = true;
+    bool poison_batched = false;  // test-only (krr_set_option "poison_batched")
     DevMem<int> ctl;
     DevMem<double> dhist;
     DevMem<double> bx, br, bz, bp, bap, by, bin, bout, bpart, bred, bscal, bW, bY;
     DevMem<int> bactive;
     std::unique_ptr<PinnedScalars> hscalT;
     int* hactive = nullptr;
+
+    Ctx() = default;
+    Ctx(const Ctx&) = delete;
+    Ctx& operator=(const Ctx&) = delete;
+    // Releases the handles on every path (also when a create call fails half way, e.g. in
+    // ncclCommInitRank); the device buffers are freed by their own destructors afterwards.
+    ~Ctx() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        if (comm) nccl().commDestroy(comm);
+        if (sol) cusolverDnDestroy(sol);
+        if (blas) cublasDestroy(blas);
+        if (hactive) cudaFreeHost(hactive);
+        if (stream) cudaStreamDestroy(stream);
+    }
 
     void set_device() const { KRR_CUDA(cudaSetDevice(device)); }
     // the (world, rank) the K1 schedule is built for
@@ -256,7 +277,13 @@ void f32_ensure(Ctx& c) {
 // out (n_pad) = (K + lambda I) v, v zero-padded to n_pad.  Replicated on all ranks.
 void ensure_batched(Ctx& c, int T) {
     const size_t nt = size_t(c.plan.n_pad) * size_t(T);
-    for (auto* v : {&c.bx, &c.br, &c.bz, &c.bp, &c.bap, &c.by, &c.bin, &c.bout}) v->ensure(nt);
+    // K1T / K1T-I8 read the padded rows [n, n_pad) of their V operand and need them zero; the
+    // Woodbury apply writes rows < n only, so every batched vector starts zeroed.
+    for (auto* v : {&c.bx, &c.br, &c.bz, &c.bp, &c.bap, &c.by, &c.bin, &c.bout}) {
+        if (v->ensure(nt)) KRR_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(double) * v->count, c.stream));
+        // test-only: all-ones bytes (NaN doubles) stand in for whatever a previous call left
+        if (c.poison_batched) KRR_CUDA(cudaMemsetAsync(v->get(), 0xFF, sizeof(double) * v->count, c.stream));
+    }
     c.bpart.ensure(size_t(c.sched.ns) * nt);
     c.bred.ensure(size_t(3) * 148 * 4 * 16);
     c.bscal.ensure(128);
@@ -514,6 +541,8 @@ void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
     c.chk.ensure(4);
     c.info.ensure(1);
     const double one = 1.0, zero = 0.0;
+    Events ev(4);
+    KRR_CUDA(cudaEventRecord(ev[0], c.stream));
     if (rows > 0) {
         // G = Z^T Z (lower): Z row-major rows x s == col-major A = Z^T (s x rows); G = A A^T.
         cublas_check(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(s), int(rows), &one,
@@ -524,6 +553,7 @@ void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
     }
     allreduce_sum(c, c.G.get(), s * s);
     diag_add_launch(c.G.get(), s, lambda_p, c.stream);  // precond.cpp:24
+    KRR_CUDA(cudaEventRecord(ev[1], c.stream));
     KRR_CUDA(cudaMemcpyAsync(c.Gcopy.get(), c.G.get(), sizeof(double) * size_t(s * s),
                              cudaMemcpyDeviceToDevice, c.stream));
     if (jitter_used) *jitter_used = 0;
@@ -547,6 +577,7 @@ void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
     KRR_CUDA(cudaMemcpyAsync(h, c.chk.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     if (h[0] < 1e-300) fail(KRR_ERR_SINGULAR_TRIANGULAR, "triangular_solve: diagonal entry below 1e-300");
+    KRR_CUDA(cudaEventRecord(ev[2], c.stream));
     if (rows > 0) {
         // U = L^-1 Z^T in place: col-major s x rows, ld = s  (precond.cpp:38)
         cublas_check(cublasDtrsm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
@@ -554,8 +585,14 @@ void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
                                  c.Z.get(), int(s)),
                      "cublasDtrsm(L^-1 Z^T)");
     }
+    KRR_CUDA(cudaEventRecord(ev[3], c.stream));
     c.lambda_p = lambda_p;
     c.sync();
+    for (int k = 0; k < 3; ++k) {
+        float ms = 0.0f;
+        KRR_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+        c.build_ms[k] = ms;
+    }
     c.has_pre = true;
 }
 
@@ -828,6 +865,9 @@ void pcgT_core(Ctx& c, int T, int t_real, double lambda, bool use_pre, double ta
     KRR_CUDA(cudaMemcpyAsync(c.bactive.get(), c.hactive, sizeof(int) * T, cudaMemcpyHostToDevice, c.stream));
     if (n_active == 0) return;
     copy_launch(c.br.get(), c.by.get(), nt, c.stream);
+    // precondT_apply_dev writes rows < n only; bz's padded tail feeds bp (copied below), which
+    // K1T reads, so it must be zero whatever an earlier call left there
+    if (use_pre) KRR_CUDA(cudaMemsetAsync(c.bz.get(), 0, sizeof(double) * size_t(nt), c.stream));
     double* z = use_pre ? c.bz.get() : c.br.get();
     if (use_pre) precondT_apply_dev(c, c.br.get(), z, T);
     copy_launch(c.bp.get(), z, nt, c.stream);
@@ -917,7 +957,7 @@ void syevd_dev(Ctx& c, double* A, int64_t s, double* evals) {
     int h = 0;
     KRR_CUDA(cudaMemcpyAsync(&h, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
-    if (h != 0) fail(KRR_ERR_NOT_POSITIVE_DEFINITE, "symmetric_eigen: eigensolver did not converge");
+    if (h != 0) fail(KRR_ERR_NO_CONVERGENCE, "symmetric_eigen: eigensolver did not converge");  // types.hpp:34
 }
 
 // quality_test (precond.cpp:60-100) of the context's raw sketch Z against its data's K.
@@ -1220,16 +1260,7 @@ int krr_ctx_create_dist(int device, int rank, int world, const void* nccl_id, kr
 int krr_ctx_destroy(krr_ctx* ctx) {
     return guard([&] {
         if (!ctx) return;
-        Ctx* c = krr::as_ctx(ctx);
-        cudaSetDevice(c->device);
-        cudaStreamSynchronize(c->stream);
-        if (c->comm) krr::nccl().commDestroy(c->comm);
-        if (c->sol) cusolverDnDestroy(c->sol);
-        if (c->blas) cublasDestroy(c->blas);
-        cudaStream_t st = c->stream;
-        if (c->hactive) cudaFreeHost(c->hactive);
-        delete c;  // frees device buffers
-        if (st) cudaStreamDestroy(st);
+        delete krr::as_ctx(ctx);  // ~Ctx releases the handles, then the device buffers
     });
 }
 
@@ -1270,6 +1301,8 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
             c.exp_mode = value != 0.0 ? 1 : 0;
         } else if (k == "pcg_graph") {
             c.pcg_graph = value != 0.0;
+        } else if (k == "poison_batched") {
+            c.poison_batched = value != 0.0;
         } else if (k == "emulate_world" || k == "emulate_rank") {
             if (c.world != 1) fail(KRR_ERR_STATE, "rank emulation is for single-rank contexts");
             const int iv = int(value);
@@ -1316,6 +1349,13 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
             *value = c.batched ? 1.0 : 0.0;
         } else if (k == "pcg_graph") {
             *value = c.pcg_graph ? 1.0 : 0.0;
+        } else if (k == "build_gram_ms" || k == "build_cholesky_ms" || k == "build_trsm_ms") {
+            // CUDA-event split of the last krr_precond_build (precond.cpp:23 / :26-34 / :38)
+            *value = c.build_ms[k == "build_gram_ms" ? 0 : (k == "build_cholesky_ms" ? 1 : 2)];
+        } else if (k == "nccl_nranks") {  // ncclCommCount of the context's communicator (1 without one)
+            int nr = 1;
+            if (c.comm && krr::nccl().commCount) krr::nccl_check(krr::nccl().commCount(c.comm, &nr), "ncclCommCount");
+            *value = nr;
         } else if (k == "emulate_world") {
             *value = c.emu_world;
         } else if (k == "emulate_rank") {

@@ -1,0 +1,40 @@
+"""bench.py's multi-rank launcher on CPU: `python bench.py --gpus 2 --dry-run` (no WORLD_SIZE)
+re-executes itself under torchrun with 2 ranks over gloo on 127.0.0.1, and a torchrun world
+that disagrees with --gpus is an error (not a mislabelled single-GPU line)."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _env():
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    return env
+
+
+def test_bench_spawns_n_ranks():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run"], cwd=ROOT,
+                         env=_env(), capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["dry_run"]
+    assert sorted(r["rank"] for r in line["ranks"]) == [0, 1]
+    assert {r["world"] for r in line["ranks"]} == {2}
+    assert sorted(r["local_rank"] for r in line["ranks"]) == [0, 1]
+    assert line["max_over_ranks"] == 1.0
+
+
+def test_bench_rejects_world_mismatch():
+    env = _env()
+    env.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run"], cwd=ROOT,
+                         env=env, capture_output=True, text=True, timeout=120)
+    assert out.returncode != 0
+    assert "WORLD_SIZE" in out.stderr

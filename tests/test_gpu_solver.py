@@ -321,6 +321,31 @@ def test_multi_rhs_train_parity(krr, oracle):
     assert rel(res.model.c, fam[2].c) <= 1e-8, rel(res.model.c, fam[2].c)
 
 
+@pytest.mark.parametrize("kpath", [0, 1])
+def test_multi_rhs_train_stale_batched_buffers(krr, oracle, kpath):
+    """Batched preconditioned PCG with n % super-tile != 0 (padded rows [n, n_pad) exist) and
+    every batched vector pre-filled with NaN, as a stale buffer from an earlier call would be:
+    the padded tail of z / p must never reach K1T (precondT writes rows < n only).
+    Runs T = 8 then T = 16 on one context (the reallocation path), both paths of K1T."""
+    n, d, sigma, lam, s = 2000, 30, 3.0, 1e-2, 256
+    x = oracle.random_matrix(n, d, 13)
+    ctx = krr.Context(0)
+    try:
+        ctx.set_option("k1t_path", kpath)
+        ctx.set_option("poison_batched", 1)
+        for t in (5, 16):
+            y = oracle.random_matrix(n, t, 60 + t)
+            cfg = krr.SolverConfig(lambda_=lam, tau=1e-8, max_iter=500, chain=krr.ChainSpec(s1=s), seed=0)
+            res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), cfg, ctx=ctx)
+            ref = oracle.train(x, y, sigma, lam, s, 0, 1e-8, 500)
+            assert np.all(np.isfinite(res.model.c))
+            assert rel(res.model.c, ref.c) <= 1e-8, (t, rel(res.model.c, ref.c))
+            for j in range(t):
+                assert abs(res.report.per_rhs[j].iterations - ref.iterations[j]) <= 2
+    finally:
+        ctx.close()
+
+
 def test_rlsc_multiclass_train(krr, oracle):
     """Config-5-shaped (small): RLSC one-vs-all targets, 16 classes, batched PCG, labels
     predicted on the training set agree with the oracle's."""

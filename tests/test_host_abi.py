@@ -135,3 +135,24 @@ def test_schedule_super_rows(krr):
     assert krr.schedule(8192)[0] == 256
     assert krr.schedule(65536)[0] == 2048
     assert krr.schedule(1048576)[0] == 4096
+
+
+def test_status_codes_map_onto_reference_exceptions(krr):
+    """Every KRR_ERR_* the header declares maps onto one Python exception named after the
+    reference's types.hpp:18-64 type (NoConvergence = types.hpp:34 included)."""
+    from paper_1611_03220_b200 import _lib
+    codes = dict(re.findall(r"(KRR_ERR_\w+)\s*=\s*(\d+)", HEADER.read_text()))
+    assert int(codes["KRR_ERR_NO_CONVERGENCE"]) == _lib.ERR_NO_CONVERGENCE
+    assert set(int(v) for v in codes.values()) == set(_lib._EXC)
+    assert _lib._EXC[_lib.ERR_NO_CONVERGENCE] is krr.NoConvergence
+    assert issubclass(krr.NoConvergence, RuntimeError)
+
+
+@pytest.mark.parametrize("cfg,n,d,t", [(1, 300, 16, 1), (2, 500, 54, 1), (3, 400, 90, 1), (4, 257, 90, 1),
+                                       (5, 600, 40, 16)])
+def test_oracle_generator_equals_library_generator(krr, oracle, cfg, n, d, t):
+    """oracle/'s restated BASELINE generator (used by bench.py's product-free CPU legs) is the
+    library's krr_generate_config bit for bit."""
+    x0, y0 = krr.generate_config(cfg, n, d, t, 0)
+    x1, y1 = oracle.generate_config(cfg, n, d, t, 0)
+    assert np.array_equal(x0, x1) and np.array_equal(y0.reshape(n, t), y1)
