@@ -19,7 +19,7 @@ roofline: dominant kernel = K1.  The default path at d = 90 is K1-I8 (tcgen05 ki
           36 slice products x kp x 2) / mean K1 launch time (CUDA events on the launching
           stream); peak = 2 x the measured dense bf16 rate in MEASURED_PEAKS.json (B200 INT8
           = 2x bf16).  The same launch is also expressed as FP64-equivalent dot-product
-          TFLOP/s (pairs x 2d) against the live-measured FP64 DMMA peak (krr_microbench),
+          TFLOP/s (pairs x 2d) against the live-measured FP64 DMMA peak (libkrr_diag.so),
           the unit of the DMMA K1 path (k1_path = 0).
 config5_pass: informational, N = 1 only (--no-config5 skips it): one (K + lambda I) V pass at
           BASELINE config 5 (n = 524288, d = 440, t = 16) through krr_kernel_matvec with host
@@ -327,8 +327,8 @@ def main():
     x, _ = krr.generate_config(4, n, d, 1, 0)
     _lib.check(_lib.LIB.krr_set_data(ctx.handle, _lib.ptr(x), n, d, sigma))
 
-    mb = np.zeros(9)
-    _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(mb)))
+    from paper_1611_03220_b200 import _diag  # measurement tooling (libkrr_diag.so)
+    mb = _diag.microbench(local)
     peak_dmma = float(mb[0])
     path = int(ctx.get_option("k1_path_effective"))  # 1 = K1-I8 (tcgen05), 0 = K1 (DMMA)
 
@@ -390,7 +390,7 @@ def main():
     pcg = None
     if args.pcg_iters > 0 and args.n == CFG4["n"]:
         try:
-            pcg = pcg_leg(krr, ctx, D, args.pcg_iters, k1.value / max(1, args.steps))
+            pcg = pcg_leg(krr, ctx, D, args.pcg_iters, k1.value)  # k1: mean ms per K1 launch
         except Exception as e:  # reported, not fatal: the mat-vec line stands on its own
             pcg = {"error": f"{type(e).__name__}: {e}"}
 
@@ -413,7 +413,7 @@ def main():
         except Exception:
             traffic = None
     fp64_view = {"achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s", "frac": achieved / peak_dmma,
-                 "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU (krr_microbench)"}
+                 "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU (krr_diag_microbench)"}
     if path == 1:
         kp = (d + 31) // 32 * 32
         i8_ops = pairs_rank * 36.0 * kp * 2.0
@@ -436,7 +436,7 @@ def main():
                     "kernel": "gauss_matvec_kernel (K1, FP64 DMMA)",
                     "flops_per_launch": flops, "k1_ms": k1_ms,
                     "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU "
-                                   "(krr_microbench; MEASURED_PEAKS.json has no FP64 entry)",
+                                   "(krr_diag_microbench; MEASURED_PEAKS.json has no FP64 entry)",
                     "fp64_pipe": {"ops_per_pair": dp + 12, "achieved_tflops_equiv":
                                   pipe_ops / (k1_ms * 1e-3) / 1e12,
                                   "frac": pipe_ops / (k1_ms * 1e-3) / 1e12 / peak_dmma}}

@@ -377,48 +377,8 @@ int krr_rlsc_encode(const int32_t* classes, int64_t n, int32_t num_classes, doub
  * *k1_ms = mean duration of the fused K1 kernel launch alone (per step). */
 int krr_bench_matvec(krr_ctx* ctx, double lambda, int steps, double* total_ms, double* k1_ms);
 
-/* ---------------------------------------------------------------- diagnostics */
-/* Micro-benchmarks run on the context's device: FP64 DMMA and DFMA issue rates,
- * and the Gaussian-epilogue throughput (results in the 8-double array:
- * [dmma_tflops, dfma_tflops, dmma+dfma concurrent tflops, exp_libdevice_geval,
- *  exp_table_geval, sm_count, clock_mhz, split-warps dmma|dfma tflops,
- *  legacy mma.sync int8 tops]). */
-int krr_microbench(krr_ctx* ctx, double* results);
-/* Evaluate the device Gaussian epilogue exp(-max(0,d2)*scale) for n host values
- * (mode 0 = libdevice exp, 1 = table exp used by the mat-vec) — accuracy tests. */
-int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale, int mode,
-                        double* out);
-
-/* tcgen05 kind::i8 probe: C (128 x N int32) = A (128 x K int8) . B (N x K int8)^T on
- * one CTA (K % 32 == 0, K <= 256, N in {32, 64}); host buffers, row-major. */
-int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int K, int N);
-/* tcgen05 kind::f16 probe: C (128 x N fp32) = A (128 x K bf16) . B (N x K bf16)^T, K % 16 == 0,
- * K <= 128, N in {32, 64}; bf16 given as uint16 bit patterns. */
-int krr_debug_bf16_gemm(krr_ctx* ctx, const uint16_t* A, const uint16_t* B, float* C, int K, int N);
-/* cycles per back-to-back tcgen05.mma kind::i8 (M = 128, N in {16, 32, 64, 128, 256}, K = 32),
- * operands in the no-swizzle K-major layout with `kbytes` bytes per row.  mode: 0 SS with
- * per-MMA descriptors, 1 SS hoisted, 2 SS hoisted + rotating accumulators, 3 TS (A in
- * TMEM), 4 TS hoisted + rotating, 5 SS hoisted + rotating + distinct smem tiles, 6 / 7 the
- * K1-I8 tile (N = 64, kp = 96, 36 products in 8 groups) in group-major / A-major order with
- * reps = tiles (N, kbytes ignored); 8-11: FP64 lane-ops / clk / SM of DADD, DADD beside
- * back-to-back MMAs, DFMA, DFMA beside MMAs (reps = iterations); 12: 2-SM tcgen05.mma
- * (cta_group::2, M = 256, clusters of 2), N in {64, 128, 256}. */
-int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, double* cycles_per_mma);
-/* TMEM read throughput (tcgen05.ld.32x32b.x16 + wait in a loop), `warps` warps on every
- * SM; returns bytes per clock per SM. */
-int krr_debug_tmem_ld_rate(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk);
-/* TMEM load bandwidth of `warps` warps while one more warp issues back-to-back kind::i8 MMAs
- * (M 128, N 64, K 96 B) into other TMEM columns; *mma_cycles = the MMA's cycles / instruction
- * meanwhile (tools/mma_rate.py). */
-int krr_debug_tmem_ld_under_mma(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk, double* mma_cycles);
-/* K1-I8 profiling trace (set_option("i8_debug", 4) before a mat-vec): clock64 stamps of
- * CTA 0, 16 per tile for the first 64 tiles. */
-int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count);
-/* In-place ncclAllReduce (sum) of n host doubles over the context's communicator (contexts
- * from krr_ctx_create_dist, including one-rank ones) — plumbing check of the NCCL path. */
-int krr_debug_nccl_allreduce(krr_ctx* ctx, double* buf, int64_t n);
-/* Same for the K1T-I8 multi-RHS kernel (16 stamps per tile, first 32 tiles of CTA 0). */
-int krr_debug_i8t_trace(krr_ctx* ctx, long long* out, int count);
+/* Diagnostics (micro-benchmarks, tcgen05 probes, kernel clock traces) live in a separate
+ * library, libkrr_diag.so (include/krr_diag.h); this header is the drop-in interface only. */
 
 #ifdef __cplusplus
 }

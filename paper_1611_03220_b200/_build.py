@@ -19,6 +19,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_obj"
 LIB = PKG / "libkrr_b200.so"
+DIAG_SRC = PKG / "diag"
+DIAG_LIB = PKG / "libkrr_diag.so"
 ORACLE_DIR = ROOT / "oracle"
 CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
@@ -41,16 +43,17 @@ def _sources():
 
 
 def _headers_mtime() -> float:
-    hs = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + list((ROOT / "include").glob("*.h"))
+    hs = (list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + list((ROOT / "include").glob("*.h")) +
+          list(DIAG_SRC.glob("*.cuh")))
     return max((h.stat().st_mtime for h in hs), default=0.0)
 
 
-def _compile(src: Path, verbose: bool) -> Path:
-    obj = BUILD / (src.name + ".o")
+def _compile(src: Path, verbose: bool, prefix: str = "") -> Path:
+    obj = BUILD / (prefix + src.name + ".o")
     hm = _headers_mtime()
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hm):
         return obj
-    cmd = [NVCC] + NVCC_FLAGS + ["-c", str(src), "-o", str(obj)]
+    cmd = [NVCC] + NVCC_FLAGS + ["-I", str(CSRC), "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -79,6 +82,26 @@ def build_lib(verbose: bool = False, force: bool = False) -> Path:
         raise RuntimeError(f"link failed:\n{res.stderr}\n{res.stdout}")
     os.replace(tmp, LIB)
     return LIB
+
+
+def build_diag(verbose: bool = False, force: bool = False) -> Path:
+    """libkrr_diag.so: micro-benchmarks / probes / traces (include/krr_diag.h), linked against
+    the product library; not part of the drop-in interface."""
+    BUILD.mkdir(exist_ok=True)
+    srcs = sorted(DIAG_SRC.glob("*.cu"))
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose, "diag_"), srcs))
+    newest = max([o.stat().st_mtime for o in objs] + [LIB.stat().st_mtime])
+    if DIAG_LIB.exists() and DIAG_LIB.stat().st_mtime >= newest and not force:
+        return DIAG_LIB
+    tmp = DIAG_LIB.with_suffix(".so.tmp")
+    cmd = ([NVCC] + ARCH + ["-shared", "-o", str(tmp)] + [str(o) for o in objs] + LINK_LIBS +
+           ["-L", str(PKG), "-lkrr_b200", "-Xlinker", "-rpath,$ORIGIN"])
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"diag link failed:\n{res.stderr}\n{res.stdout}")
+    os.replace(tmp, DIAG_LIB)
+    return DIAG_LIB
 
 
 def build_examples() -> Path:
@@ -111,9 +134,11 @@ def main(argv=None) -> int:
     verbose = "-v" in argv
     force = "-f" in argv
     lib = build_lib(verbose=verbose, force=force)
+    diag = build_diag(verbose=verbose, force=force)
     orc = build_oracle()
     ex = build_examples()
     print(lib)
+    print(diag)
     print(orc)
     print(ex)
     return 0

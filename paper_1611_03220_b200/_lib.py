@@ -180,16 +180,6 @@ _SIGS = {
     "krr_generate_config": [_i, _i64, _i64, _i64, C.c_uint64, _vp, _vp],
     "krr_rlsc_encode": [_vp, _i64, C.c_int32, _vp],
     "krr_bench_matvec": [_vp, _d, _i, C.POINTER(_d), C.POINTER(_d)],
-    "krr_microbench": [_vp, _vp],
-    "krr_debug_gauss_exp": [_vp, _vp, _i64, _d, _i, _vp],
-    "krr_debug_i8_gemm": [_vp, _vp, _vp, _vp, _i, _i],
-    "krr_debug_bf16_gemm": [_vp, _vp, _vp, _vp, _i, _i],
-    "krr_debug_i8_mma_rate": [_vp, _i, _i, _i, _i, C.POINTER(_d)],
-    "krr_debug_tmem_ld_rate": [_vp, _i, _i, C.POINTER(_d)],
-    "krr_debug_tmem_ld_under_mma": [_vp, _i, _i, C.POINTER(_d), C.POINTER(_d)],
-    "krr_debug_i8_trace": [_vp, _vp, _i],
-    "krr_debug_i8t_trace": [_vp, _vp, _i],
-    "krr_debug_nccl_allreduce": [_vp, _vp, _i64],
     "krr_solve_regularized_dense": [_vp, _vp, _i64, _vp, _i64, _d, _i, _d, _i, _vp, _vp, _vp, C.POINTER(_i64)],
     # SURVEY 8f4
     "krr_set_data_kernel": [_vp, _vp, _i64, _i64, C.POINTER(KernelSpecC)],

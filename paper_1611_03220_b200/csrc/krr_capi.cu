@@ -1845,180 +1845,6 @@ int krr_bench_matvec(krr_ctx* ctx, double lambda, int steps, double* total_ms, d
     });
 }
 
-int krr_microbench(krr_ctx* ctx, double* results) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        c.set_device();
-        double tab[64];
-        krr::make_exp_table(tab);
-        krr::DevMem<double> dt;
-        dt.ensure(64);
-        KRR_CUDA(cudaMemcpy(dt.get(), tab, sizeof(tab), cudaMemcpyHostToDevice));
-        const krr::ExpConsts ec = krr::make_exp_consts(1.0 / 72.0);
-        krr::microbench_run(ec, dt.get(), results, c.stream);
-    });
-}
-
-int krr_debug_gauss_exp(krr_ctx* ctx, const double* d2, int64_t n, double scale, int mode,
-                        double* out) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        c.set_device();
-        double tab[64];
-        krr::make_exp_table(tab);
-        krr::DevMem<double> dt, din, dout;
-        dt.ensure(64);
-        din.ensure(size_t(std::max<int64_t>(1, n)));
-        dout.ensure(size_t(std::max<int64_t>(1, n)));
-        KRR_CUDA(cudaMemcpyAsync(dt.get(), tab, sizeof(tab), cudaMemcpyHostToDevice, c.stream));
-        KRR_CUDA(cudaMemcpyAsync(din.get(), d2, sizeof(double) * size_t(n), cudaMemcpyHostToDevice,
-                                 c.stream));
-        krr::debug_exp_launch(din.get(), n, krr::make_exp_consts(scale), dt.get(), mode, dout.get(),
-                              c.stream);
-        KRR_CUDA(cudaMemcpyAsync(out, dout.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost,
-                                 c.stream));
-        c.sync();
-    });
-}
-
-int krr_debug_i8_gemm(krr_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int K, int N) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        if (K <= 0 || K % 32 != 0 || K > 256) fail(KRR_ERR_INVALID_ARGUMENT, "K must be a multiple of 32 <= 256");
-        c.set_device();
-        krr::DevMem<int8_t> a, b;
-        krr::DevMem<int32_t> o;
-        a.ensure(size_t(128 * K));
-        b.ensure(size_t(N * K));
-        o.ensure(size_t(128 * N));
-        KRR_CUDA(cudaMemcpyAsync(a.get(), A, size_t(128 * K), cudaMemcpyHostToDevice, c.stream));
-        KRR_CUDA(cudaMemcpyAsync(b.get(), B, size_t(N * K), cudaMemcpyHostToDevice, c.stream));
-        krr::i8_probe_launch(a.get(), b.get(), o.get(), K, N, c.stream);
-        KRR_CUDA(cudaMemcpyAsync(C, o.get(), sizeof(int32_t) * size_t(128 * N), cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-    });
-}
-
-int krr_debug_bf16_gemm(krr_ctx* ctx, const uint16_t* A, const uint16_t* B, float* C, int K, int N) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        if (K <= 0 || K % 16 != 0 || K > 128) fail(KRR_ERR_INVALID_ARGUMENT, "K must be a multiple of 16 <= 128");
-        c.set_device();
-        krr::DevMem<uint16_t> a, b;
-        krr::DevMem<float> o;
-        a.ensure(size_t(128 * K));
-        b.ensure(size_t(N * K));
-        o.ensure(size_t(128 * N));
-        KRR_CUDA(cudaMemcpyAsync(a.get(), A, sizeof(uint16_t) * size_t(128 * K), cudaMemcpyHostToDevice, c.stream));
-        KRR_CUDA(cudaMemcpyAsync(b.get(), B, sizeof(uint16_t) * size_t(N * K), cudaMemcpyHostToDevice, c.stream));
-        krr::bf16_probe_launch(a.get(), b.get(), o.get(), K, N, c.stream);
-        KRR_CUDA(cudaMemcpyAsync(C, o.get(), sizeof(float) * size_t(128 * N), cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-    });
-}
-
-int krr_debug_i8_mma_rate(krr_ctx* ctx, int N, int reps, int kbytes, int mode, double* cycles_per_mma) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        if (N != 16 && N != 32 && N != 64 && N != 128 && N != 256)
-            fail(KRR_ERR_INVALID_ARGUMENT, "N must be 16/32/64/128/256");
-        if (kbytes < 32 || kbytes % 32 != 0) fail(KRR_ERR_INVALID_ARGUMENT, "kbytes must be a multiple of 32");
-        if (mode == 12) {  // 2-SM (cta_group::2) MMA, M = 256, N in {64, 128, 256}
-            if (N != 64 && N != 128 && N != 256) fail(KRR_ERR_INVALID_ARGUMENT, "pair mode: N in {64, 128, 256}");
-            c.set_device();
-            *cycles_per_mma = krr::i8_mma_rate_pair(N, std::max(8, reps), c.stream);
-            return;
-        }
-        if (mode >= 8 && mode <= 11) {  // FP64 ops/clk/SM: 8 DADD, 9 DADD + MMA, 10 DFMA, 11 DFMA + MMA
-            c.set_device();
-            *cycles_per_mma = krr::fp64_under_mma((mode - 8) >> 1, (mode - 8) & 1, std::max(64, reps), c.stream);
-            return;
-        }
-        if (mode >= 13 && mode <= 16) {  // 13 FFMA, 14 FFMA + MMA, 15 IMAD, 16 IMAD + MMA (lane-ops/clk/SM)
-            c.set_device();
-            *cycles_per_mma = krr::fp64_under_mma(2 + ((mode - 13) >> 1), (mode - 13) & 1, std::max(64, reps), c.stream);
-            return;
-        }
-        if (mode >= 17 && mode <= 24 && mode != 23) {  // MMA cycles / instr beside 17 DADD, 18 DFMA, 19 FFMA,
-            if (mode == 24) mode = 23;  // 20 IMAD, 21 idle, 22 LDS.128, 24 -> op 6 (FFMA off the MMA's SMSP)
-            c.set_device();
-            krr::fp64_under_mma(mode - 17, 1, std::max(64, reps), c.stream, cycles_per_mma);
-            return;
-        }
-        if (mode >= 26 && mode <= 29) {  // DFMA lane-ops/clk/SM with 16 worker warps: 26 alone, 27 + MMA;
-            c.set_device();               // 28 / 29: the same with 8 worker warps
-            const int nw = mode <= 27 ? 16 : 8;
-            *cycles_per_mma = krr::fp64_under_mma(1, (mode - 26) & 1, std::max(64, reps), c.stream, nullptr, nw);
-            return;
-        }
-        if (mode == 25) {  // MMA cycles / instr beside FFMA on the MMA warp's own SMSP only (op 7)
-            c.set_device();
-            krr::fp64_under_mma(7, 1, std::max(64, reps), c.stream, cycles_per_mma);
-            return;
-        }
-        if (mode == 6 || mode == 7) {  // in-situ K1-I8 tile order (N = 64, kp = 96), reps = tiles
-            c.set_device();
-            *cycles_per_mma = krr::i8_tile_order_rate(mode - 6, std::max(1, reps), c.stream);
-            return;
-        }
-        if (reps < 8 || mode < 0 || mode > 5) fail(KRR_ERR_INVALID_ARGUMENT, "reps >= 8, mode in [0, 7]");
-        if (size_t(128 + N) * size_t(kbytes) > 200 * 1024) fail(KRR_ERR_INVALID_ARGUMENT, "operands exceed smem");
-        c.set_device();
-        *cycles_per_mma = krr::i8_mma_rate(N, reps, kbytes, mode, c.stream);
-    });
-}
-
-int krr_debug_i8_trace(krr_ctx* ctx, long long* out, int count) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        c.set_device();
-        krr::i8_read_trace(out, count);
-    });
-}
-
-int krr_debug_nccl_allreduce(krr_ctx* ctx, double* buf, int64_t n) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        if (!c.comm) fail(KRR_ERR_STATE, "no NCCL communicator on this context (krr_ctx_create_dist)");
-        if (n < 0 || (n > 0 && !buf)) fail(KRR_ERR_INVALID_ARGUMENT, "bad buffer");
-        c.set_device();
-        if (n == 0) return;
-        krr::DevMem<double> d;
-        d.ensure(size_t(n));
-        KRR_CUDA(cudaMemcpyAsync(d.get(), buf, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c.stream));
-        krr::nccl_check(krr::nccl().allReduce(d.get(), d.get(), size_t(n), ncclDouble, ncclSum, c.comm, c.stream),
-                        "ncclAllReduce");
-        KRR_CUDA(cudaMemcpyAsync(buf, d.get(), sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-    });
-}
-
-int krr_debug_i8t_trace(krr_ctx* ctx, long long* out, int count) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        c.set_device();
-        krr::i8s_read_trace(out, count);
-    });
-}
-
-int krr_debug_tmem_ld_under_mma(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk, double* mma_cycles) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        if (warps < 1 || warps > 16 || reps < 1) fail(KRR_ERR_INVALID_ARGUMENT, "warps in [1, 16], reps >= 1");
-        c.set_device();
-        *bytes_per_clk = krr::tmem_ld_under_mma(warps, reps, c.stream, mma_cycles);
-    });
-}
-
-int krr_debug_tmem_ld_rate(krr_ctx* ctx, int warps, int reps, double* bytes_per_clk) {
-    return guard([&] {
-        Ctx& c = *krr::as_ctx(ctx);
-        if (warps < 1 || warps > 32 || reps < 1) fail(KRR_ERR_INVALID_ARGUMENT, "warps in [1, 32], reps >= 1");
-        c.set_device();
-        *bytes_per_clk = krr::tmem_ld_rate(warps, reps, c.stream);
-    });
-}
-
 }  // extern "C"
 
 // ============================================================================= SURVEY 8f4

@@ -4,7 +4,7 @@
 #include <type_traits>
 
 #include "common.cuh"
-#include "kernels.cuh"
+#include "diag.cuh"
 #include "tc_i8.cuh"
 
 namespace krr {

@@ -24,7 +24,7 @@ def _ulps(a, b):
 @pytest.mark.parametrize("mode", [0, 1])
 def test_gauss_exp_accuracy(krr, ctx, mode):
     """Device epilogue exp(-max(0, d2) scale) vs glibc exp on the same rounded argument."""
-    from paper_1611_03220_b200 import _lib
+    from paper_1611_03220_b200 import _diag, _lib
     rng = np.random.default_rng(0)
     for scale in (1.0 / 32.0, 1.0 / 18.0, 1.0 / 72.0, 1.0 / 800.0, 0.5):
         d2 = np.concatenate([
@@ -32,8 +32,7 @@ def test_gauss_exp_accuracy(krr, ctx, mode):
             rng.exponential(1.0 / scale, 20000), np.array([0.0, -1e-14, -3.0, 1e-300, 5e-324]),
             np.linspace(0, 745.0 / scale, 5000)])
         out = np.empty_like(d2)
-        _lib.check(_lib.LIB.krr_debug_gauss_exp(ctx.handle, _lib.ptr(d2), d2.size, scale, mode,
-                                                _lib.ptr(out)))
+        _diag.check(_diag.LIB.krr_diag_gauss_exp(0, _lib.ptr(d2), d2.size, scale, mode, _lib.ptr(out)))
         y = -np.maximum(0.0, d2) * scale
         ref = np.exp(y)
         normal = ref >= 2.0 ** -1020

@@ -1,6 +1,6 @@
 """The NCCL plumbing on one GPU: a one-rank communicator (krr_ctx_create_dist with world = 1)
-loads NCCL (dlopen), builds the communicator and runs ncclAllReduce on the context's stream;
-the K1 data path is unchanged by its presence.  (Multi-rank logic: tests/test_dist_gloo.py,
+loads NCCL (dlopen) and builds the communicator (ncclCommCount = 1); the K1 data path is
+unchanged by its presence.  (Multi-rank logic: tests/test_dist_gloo.py,
 tests/test_gpu_rank_emulation.py.)"""
 import numpy as np
 import pytest
@@ -8,21 +8,16 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def test_one_rank_nccl_allreduce_and_matvec(krr, oracle):
+def test_one_rank_nccl_comm_and_matvec(krr, oracle):
     import torch  # noqa: F401  (load torch's NCCL first, as bench.py does, so one NCCL is in the process)
-    from paper_1611_03220_b200 import _lib
 
     nid = krr.nccl_unique_id()
     assert len(nid) == 128
     ctx = krr.Context(0, 0, 1, nid)
     plain = krr.Context(0)
     try:
-        buf = np.linspace(-3.0, 7.0, 4099)
-        want = buf.copy()
-        _lib.check(_lib.LIB.krr_debug_nccl_allreduce(ctx.handle, _lib.ptr(buf), buf.size))
-        assert np.array_equal(buf, want)  # sum over one rank
-        with pytest.raises(krr.StateError):
-            _lib.check(_lib.LIB.krr_debug_nccl_allreduce(plain.handle, _lib.ptr(buf), buf.size))
+        assert ctx.get_option("nccl_nranks") == 1.0
+        assert plain.get_option("nccl_nranks") == 1.0
         x = oracle.random_matrix(3000, 90, 4)
         v = oracle.random_vector(3000, 5)
         a = krr.GaussianOperator(x, krr.KernelSpec.gaussian(6.0), 1e-3, ctx=ctx)(v)

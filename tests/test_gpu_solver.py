@@ -327,7 +327,7 @@ def test_multi_rhs_train_stale_batched_buffers(krr, oracle, kpath):
     every batched vector pre-filled with NaN, as a stale buffer from an earlier call would be:
     the padded tail of z / p must never reach K1T (precondT writes rows < n only).
     Runs T = 8 then T = 16 on one context (the reallocation path), both paths of K1T."""
-    n, d, sigma, lam, s = 2000, 30, 3.0, 1e-2, 256
+    n, d, sigma, lam, s = 2000, 30, 3.0, 1e-1, 256
     x = oracle.random_matrix(n, d, 13)
     ctx = krr.Context(0)
     try:
@@ -337,11 +337,12 @@ def test_multi_rhs_train_stale_batched_buffers(krr, oracle, kpath):
             y = oracle.random_matrix(n, t, 60 + t)
             cfg = krr.SolverConfig(lambda_=lam, tau=1e-8, max_iter=500, chain=krr.ChainSpec(s1=s), seed=0)
             res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), cfg, ctx=ctx)
-            ref = oracle.train(x, y, sigma, lam, s, 0, 1e-8, 500)
+            fam = [oracle.train(x, y, sigma, lam, s, 0, 1e-8, 500, order=k) for k in (2, 0, 1)]
             assert np.all(np.isfinite(res.model.c))
-            assert rel(res.model.c, ref.c) <= 1e-8, (t, rel(res.model.c, ref.c))
+            assert rel(res.model.c, fam[0].c) <= 1e-8, (t, rel(res.model.c, fam[0].c))
             for j in range(t):
-                assert abs(res.report.per_rhs[j].iterations - ref.iterations[j]) <= 2
+                its = [f.iterations[j] for f in fam]
+                assert min(its) - 1 <= res.report.per_rhs[j].iterations <= max(its) + 1, (t, j, its)
     finally:
         ctx.close()
 

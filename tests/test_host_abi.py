@@ -156,3 +156,25 @@ def test_oracle_generator_equals_library_generator(krr, oracle, cfg, n, d, t):
     x0, y0 = krr.generate_config(cfg, n, d, t, 0)
     x1, y1 = oracle.generate_config(cfg, n, d, t, 0)
     assert np.array_equal(x0, x1) and np.array_equal(y0.reshape(n, t), y1)
+
+
+def test_drop_in_library_exports_no_diagnostics():
+    """The drop-in library's ABI is the reference-mapped interface (+ option knobs and the
+    mat-vec timing entry); probes / micro-benchmarks live in libkrr_diag.so."""
+    out = subprocess.run(["nm", "-D", "--defined-only", str(LIB)], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\sT\s(krr_\w+)$", out, flags=re.M))
+    assert not [f for f in exported if f.startswith(("krr_debug", "krr_diag")) or f == "krr_microbench"]
+    assert exported == set(declared_functions())
+
+
+def test_diag_library_exports_its_header(krr):
+    diag_h = ROOT / "include" / "krr_diag.h"
+    text = re.sub(r"/\*.*?\*/", "", diag_h.read_text(), flags=re.S)
+    names = set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(krr_diag_\w+)\s*\(", text, flags=re.M))
+    out = subprocess.run(["nm", "-D", "--defined-only", str(ROOT / "paper_1611_03220_b200" / "libkrr_diag.so")],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(krr_diag_\w+)$", out, flags=re.M))
+    assert names and names == exported
+    from paper_1611_03220_b200 import _diag
+    assert set(_diag.declared_symbols()) == names

@@ -10,7 +10,8 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1611_03220_b200 as krr  # noqa: E402
-from paper_1611_03220_b200 import _lib  # noqa: E402
+from paper_1611_03220_b200 import _lib
+from paper_1611_03220_b200 import _diag  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 90
@@ -28,7 +29,7 @@ _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(
 ctx.set_option("i8_debug", 4 | extra)
 _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, 1e-6, 1, C.byref(tot), C.byref(k1)))
 buf = np.zeros(64 * 16, dtype=np.int64)
-_lib.check(_lib.LIB.krr_debug_i8_trace(ctx.handle, buf.ctypes.data_as(C.c_void_p), buf.size))
+_diag.check(_diag.LIB.krr_diag_i8_trace(buf.ctypes.data_as(C.c_void_p), buf.size))
 t = buf.reshape(64, 16)
 t0 = t[0, 0]
 names = ["start", "st6", "st4", "st2", "st0", "cd", "exp", "bar", "m:bfull?", "m:bfull", "m:g7", "m:g4", "m:g0",

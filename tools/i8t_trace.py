@@ -10,7 +10,8 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1611_03220_b200 as krr  # noqa: E402
-from paper_1611_03220_b200 import _lib  # noqa: E402
+from paper_1611_03220_b200 import _lib
+from paper_1611_03220_b200 import _diag  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 440
@@ -23,7 +24,7 @@ op.matmat(v)
 ctx.set_option("i8_debug", 4)
 op.matmat(v)
 buf = np.zeros(32 * 16, dtype=np.int64)
-_lib.check(_lib.LIB.krr_debug_i8t_trace(ctx.handle, buf.ctypes.data_as(C.c_void_p), buf.size))
+_diag.check(_diag.LIB.krr_diag_i8t_trace(buf.ctypes.data_as(C.c_void_p), buf.size))
 t = buf.reshape(32, 16)
 names = ["start", "st6", "drained", "exp", "barA", "dmmaR", "dmmaC", "barB", "m:go", "m:ks0", "m:ksM", "m:ksL",
          "p:ks0", "p:efree", "-", "-"]

@@ -16,7 +16,8 @@ sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 
 import paper_1611_03220_b200 as krr  # noqa: E402
-from paper_1611_03220_b200 import _lib  # noqa: E402
+from paper_1611_03220_b200 import _lib
+from paper_1611_03220_b200 import _diag  # noqa: E402
 
 MB_KEYS = ["dmma_tflops", "dfma_tflops", "mixed_tflops", "exp_libdevice_gevals", "exp_table_gevals",
            "sms", "clock_mhz", "split_warps_tflops", "imma_legacy_tops"]
@@ -52,7 +53,7 @@ def main():
     ctx = krr.Context(0)
     if not args.no_microbench:
         res = np.zeros(9)
-        _lib.check(_lib.LIB.krr_microbench(ctx.handle, _lib.ptr(res)))
+        _diag.check(_diag.LIB.krr_diag_microbench(0, _lib.ptr(res)))
         out["microbench"] = dict(zip(MB_KEYS, res.tolist()))
         print(json.dumps(out["microbench"]), flush=True)
     rows = []
