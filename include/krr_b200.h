@@ -310,6 +310,12 @@ int krr_precond_build(krr_ctx* ctx, double lambda_p, int* jitter_used);
 int krr_precond_apply(krr_ctx* ctx, const double* R, int64_t t, double* out);
 /* Download U (s x n row-major, the reference's Preconditioner::u) — test helper. */
 int krr_precond_download_u(krr_ctx* ctx, double* U);
+/* Read a block of Preconditioner::u (precond.hpp:16, a public member): out (nrows x ncols,
+ * row-major) = U[row0 : row0 + nrows, cols[0..ncols)] — the rows are sketch features, the
+ * columns data points (zero for columns in another rank's shard).  Lets a caller inspect U
+ * at sizes where downloading all s x n of it is impractical (64 GiB at BASELINE config 4). */
+int krr_precond_read_u(krr_ctx* ctx, int64_t row0, int64_t nrows, const int64_t* cols, int64_t ncols,
+                       double* out);
 int krr_precond_drop(krr_ctx* ctx);
 
 /* ---------------------------------------------------------------- PCG */

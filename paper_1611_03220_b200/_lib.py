@@ -169,6 +169,7 @@ _SIGS = {
     "krr_precond_build": [_vp, _d, C.POINTER(_i)],
     "krr_precond_apply": [_vp, _vp, _i64, _vp],
     "krr_precond_download_u": [_vp, _vp],
+    "krr_precond_read_u": [_vp, _i64, _i64, _vp, _i64, _vp],
     "krr_precond_drop": [_vp],
     "krr_pcg_solve": [_vp, _d, _vp, _i64, _d, _i, _i, _vp, _vp, _vp, C.POINTER(_i64)],
     "krr_pcg_solve_operator": [_vp, _i64, OPERATOR_CB, _vp, OPERATOR_CB, _vp, _vp, _d, _i,
@@ -289,6 +290,13 @@ class Context:
         out = C.c_double()
         check(LIB.krr_get_option(self.handle, key.encode(), C.byref(out)))
         return out.value
+
+    def read_u(self, row0: int, nrows: int, cols) -> np.ndarray:
+        """U[row0:row0+nrows, cols] of the context's preconditioner (krr_precond_read_u)."""
+        cols = np.ascontiguousarray(cols, dtype=np.int64)
+        out = np.empty((nrows, cols.size))
+        check(LIB.krr_precond_read_u(self.handle, row0, nrows, ptr(cols), cols.size, ptr(out)))
+        return out
 
     def precond_drop(self) -> None:
         """Free the context's sketch / preconditioner buffers (krr_precond_drop)."""

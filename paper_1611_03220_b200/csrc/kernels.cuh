@@ -147,8 +147,6 @@ void pcgT_update_xr_launch(const double* pap_part, int nb, int T, const double* 
                            double* rr_part, double* pap_out, cudaStream_t stream);
 void pcgT_update_p_launch(const double* rz_part, int nb, int T, const double* rz_old, double* rz_out,
                           const int* active, double* p, const double* z, int64_t n, cudaStream_t stream);
-void woodbury_finish_launch(const double* r, const double* y, double lambda_p, double* z, int64_t count,
-                            cudaStream_t stream);
 // columns [c0, c0 + T) of an n x t row-major block <-> n_pad x T interleaved (zero padded)
 void pad_cols_launch(const double* in, int64_t n, int64_t t, int64_t c0, int64_t n_pad, int T, double* out,
                      cudaStream_t stream);
@@ -178,6 +176,11 @@ void reduce_rows_launch(const double* Wpart, int nchunks, int64_t s, double* W,
                         cudaStream_t stream);
 // z_i = (r_i - B[i] . W) / lambda_p, rz partials (nb blocks).
 int zrow_blocks(int64_t n);
+// K6T (precond_multi.cu): Woodbury apply for T = 8 / 16 interleaved columns on the DMMA path.
+// which: 1 = pass 1 (W = B^T R, reduced), 2 = pass 2 (Z = (R - B W) / lambda_p), 3 = both.
+int k6t_splits(int64_t n, int64_t s);
+void precond_multi_launch(const double* B, int64_t n, int64_t s, const double* R, double lambda_p, double* Z,
+                          double* Wpart, int nsplit, double* W, int T, int which, cudaStream_t stream);
 void precond_z_launch(const double* B, int64_t n, int64_t s, const double* W, const double* r,
                       double lambda_p, double* z, double* rz_part, int nb, cudaStream_t stream);
 

@@ -203,7 +203,7 @@ struct Ctx {
     bool poison_batched = false;  // test-only (krr_set_option "poison_batched")
     DevMem<int> ctl;
     DevMem<double> dhist;
-    DevMem<double> bx, br, bz, bp, bap, by, bin, bout, bpart, bred, bscal, bW, bY;
+    DevMem<double> bx, br, bz, bp, bap, by, bin, bout, bpart, bred, bscal, bW;
     DevMem<int> bactive;
     std::unique_ptr<PinnedScalars> hscalT;
     int* hactive = nullptr;
@@ -802,30 +802,19 @@ void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
     allreduce_sum(c, out, c.plan.n_pad * T);
 }
 
-// z (pn x T) = (r - U^T U r) / lambda_p for T interleaved columns: two cuBLAS GEMMs over
-// the row shard of B = U^T (n x s row-major == s x n column-major) + a fused finish.
+// z (pn x T) = (r - U^T U r) / lambda_p for T interleaved columns (precond.cpp:15-18): the two
+// K6T passes over the row shard of B = U^T (precond_multi.cu), the s x T all-reduce between them.
 void precondT_apply_dev(Ctx& c, const double* r, double* z, int T) {
     if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
     const int64_t s = c.s, rows = c.z1 - c.z0;
+    const int nsplit = k6t_splits(std::max<int64_t>(1, rows), s);
     c.bW.ensure(size_t(s * T));
-    c.bY.ensure(size_t(std::max<int64_t>(1, rows)) * T);
-    const double one = 1.0, zero = 0.0;
-    if (rows > 0) {
-        // W (s x T col-major) = B_cm (s x rows) . R_cm^T, R_cm = r rows as T x rows col-major
-        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_T, int(s), T, int(rows), &one, c.Z.get(),
-                                 int(s), r + c.z0 * T, T, &zero, c.bW.get(), int(s)),
-                     "cublasDgemm(U R)");
-    } else {
-        KRR_CUDA(cudaMemsetAsync(c.bW.get(), 0, sizeof(double) * size_t(s * T), c.stream));
-    }
+    c.Wpart.ensure(size_t(nsplit) * size_t(s * T));
+    precond_multi_launch(c.Z.get(), rows, s, r + c.z0 * T, c.lambda_p, z + c.z0 * T, c.Wpart.get(), nsplit,
+                         c.bW.get(), T, 1, c.stream);
     allreduce_sum(c, c.bW.get(), s * T);
-    if (rows > 0) {
-        // Y (T x rows col-major == rows x T row-major) = W^T . B_cm
-        cublas_check(cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, T, int(rows), int(s), &one, c.bW.get(),
-                                 int(s), c.Z.get(), int(s), &zero, c.bY.get(), T),
-                     "cublasDgemm(U^T W)");
-        woodbury_finish_launch(r + c.z0 * T, c.bY.get(), c.lambda_p, z + c.z0 * T, rows * T, c.stream);
-    }
+    precond_multi_launch(c.Z.get(), rows, s, r + c.z0 * T, c.lambda_p, z + c.z0 * T, c.Wpart.get(), nsplit,
+                         c.bW.get(), T, 2, c.stream);
     if (c.world > 1) {
         if (c.z0 > 0) KRR_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * size_t(c.z0 * T), c.stream));
         if (c.z1 < c.pn)
@@ -1614,10 +1603,24 @@ int krr_precond_apply(krr_ctx* ctx, const double* Rm, int64_t t, double* out) {
         krr::DevMem<double> a, b, vi, vo;
         a.ensure(size_t(n * t));
         b.ensure(size_t(n * t));
-        vi.ensure(size_t(n));
-        vo.ensure(size_t(n));
         KRR_CUDA(cudaMemcpyAsync(a.get(), Rm, sizeof(double) * size_t(n * t), cudaMemcpyHostToDevice,
                                  c.stream));
+        if (t > 1 && c.batched) {  // apply_columns: K6T over batches of T = 8 / 16 columns
+            const int T = krr::batch_width(t);
+            vi.ensure(size_t(n * T));
+            vo.ensure(size_t(n * T));
+            for (int64_t c0 = 0; c0 < t; c0 += T) {
+                krr::pad_cols_launch(a.get(), n, t, c0, n, T, vi.get(), c.stream);
+                krr::precondT_apply_dev(c, vi.get(), vo.get(), T);
+                krr::unpad_cols_launch(vo.get(), n, t, c0, T, b.get(), c.stream);
+            }
+            KRR_CUDA(cudaMemcpyAsync(out, b.get(), sizeof(double) * size_t(n * t), cudaMemcpyDeviceToHost,
+                                     c.stream));
+            c.sync();
+            return;
+        }
+        vi.ensure(size_t(n));
+        vo.ensure(size_t(n));
         for (int64_t j = 0; j < t; ++j) {
             krr::gather_col_launch(a.get(), n, t, j, vi.get(), c.stream);
             krr::precond_apply_dev(c, vi.get(), vo.get());
@@ -1641,6 +1644,32 @@ int krr_precond_download_u(krr_ctx* ctx, double* U) {
         c.sync();
         for (int64_t i = 0; i < c.pn; ++i)
             for (int64_t k = 0; k < c.s; ++k) U[k * c.pn + i] = b[size_t(i * c.s + k)];
+    });
+}
+
+int krr_precond_read_u(krr_ctx* ctx, int64_t row0, int64_t nrows, const int64_t* cols, int64_t ncols,
+                       double* out) {
+    return guard([&] {
+        Ctx& c = *krr::as_ctx(ctx);
+        if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
+        if (row0 < 0 || nrows < 0 || row0 + nrows > c.s || ncols < 0)
+            fail(KRR_ERR_DIMENSION_MISMATCH, "krr_precond_read_u: row block outside U's s rows");
+        c.set_device();
+        // U[k, i] lives at Z[(i - z0) * s + k] (U^T row-major over the rank's row shard)
+        std::vector<double> row(static_cast<size_t>(nrows));
+        for (int64_t j = 0; j < ncols; ++j) {
+            const int64_t i = cols[j];
+            if (i < 0 || i >= c.pn) fail(KRR_ERR_DIMENSION_MISMATCH, "krr_precond_read_u: column outside U's n");
+            if (i < c.z0 || i >= c.z1) {  // another rank's shard
+                for (int64_t k = 0; k < nrows; ++k) out[k * ncols + j] = 0.0;
+                continue;
+            }
+            if (nrows > 0)
+                KRR_CUDA(cudaMemcpyAsync(row.data(), c.Z.get() + (i - c.z0) * c.s + row0, sizeof(double) * size_t(nrows),
+                                         cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            for (int64_t k = 0; k < nrows; ++k) out[k * ncols + j] = row[size_t(k)];
+        }
     });
 }
 

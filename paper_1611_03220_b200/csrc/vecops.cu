@@ -283,12 +283,6 @@ __global__ void unpad_cols_kernel(const double* __restrict__ in, int64_t n, int6
 }
 
 // z = (r - y) / lambda_p elementwise (batched Woodbury epilogue after the cuBLAS GEMMs)
-__global__ void woodbury_finish_kernel(const double* __restrict__ r, const double* __restrict__ y,
-                                       double lambda_p, double* __restrict__ z, int64_t count) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
-         i += int64_t(gridDim.x) * blockDim.x)
-        z[i] = (r[i] - y[i]) / lambda_p;
-}
 
 unsigned grid_for(int64_t n) {
     return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
@@ -338,11 +332,6 @@ void unpad_cols_launch(const double* in, int64_t n, int64_t t, int64_t c0, int T
     KRR_LAUNCH_CHECK();
 }
 
-void woodbury_finish_launch(const double* r, const double* y, double lambda_p, double* z, int64_t count,
-                            cudaStream_t stream) {
-    woodbury_finish_kernel<<<grid_for(count), 256, 0, stream>>>(r, y, lambda_p, z, count);
-    KRR_LAUNCH_CHECK();
-}
 
 void build_operands_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, int dp,
                            double* L, double* R, cudaStream_t stream) {

@@ -390,3 +390,19 @@ def test_solve_regularized_dense_matches_oracle(krr, oracle, ctx, pre, t):
         krr.solve_regularized_dense(k[:10, :10], y, lam, None, 1e-8, 10, ctx=ctx)
     with pytest.raises(krr.NonPositiveLambda):
         krr.solve_regularized_dense(k, y, 0.0, None, 1e-8, 10, ctx=ctx)
+
+
+@pytest.mark.parametrize("n,s,t", [(3001, 333, 16), (777, 70, 5), (4096, 1024, 16), (130, 7, 9)])
+def test_precond_apply_columns_k6t_matches_oracle(krr, oracle, n, s, t):
+    """apply_columns (precond.cpp:15-18) through K6T (T = 8 / 16 interleaved columns on the DMMA
+    path, ragged n and s) against the oracle's per-column apply."""
+    z = oracle.random_matrix(n, s, 31) * 0.1
+    lp = 1e-2
+    u_ref, _ = oracle.build_preconditioner(z, lp)
+    p = krr.build_preconditioner(z, lp)
+    x = oracle.random_matrix(n, t, 32)
+    got = p.apply_columns(x)
+    want = oracle.precond_apply(u_ref, lp, x)
+    assert rel(got, want) <= 1e-11, rel(got, want)
+    for j in (0, t - 1):
+        assert rel(got[:, j], p.apply(x[:, j])) <= 1e-13
