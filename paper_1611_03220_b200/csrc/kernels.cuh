@@ -179,6 +179,7 @@ int zrow_blocks(int64_t n);
 // K6T (precond_multi.cu): Woodbury apply for T = 8 / 16 interleaved columns on the DMMA path.
 // which: 1 = pass 1 (W = B^T R, reduced), 2 = pass 2 (Z = (R - B W) / lambda_p), 3 = both.
 int k6t_splits(int64_t n, int64_t s);
+bool k6t_supported(int64_t s, const void* B);  // even s (16-byte aligned rows of B)
 void precond_multi_launch(const double* B, int64_t n, int64_t s, const double* R, double lambda_p, double* Z,
                           double* Wpart, int nsplit, double* W, int T, int which, cudaStream_t stream);
 void precond_z_launch(const double* B, int64_t n, int64_t s, const double* W, const double* r,

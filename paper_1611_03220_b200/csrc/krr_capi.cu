@@ -807,6 +807,16 @@ void matvecT_dev(Ctx& c, const double* v, double* out, int T, double lambda) {
 void precondT_apply_dev(Ctx& c, const double* r, double* z, int T) {
     if (!c.has_pre) fail(KRR_ERR_STATE, "no preconditioner built");
     const int64_t s = c.s, rows = c.z1 - c.z0;
+    if (!k6t_supported(s, c.Z.get())) {  // odd s: row starts not 16-byte aligned; column by column (K6)
+        c.vin.ensure(size_t(c.pn));
+        c.vout.ensure(size_t(c.pn));
+        for (int j = 0; j < T; ++j) {
+            gather_col_launch(r, c.pn, T, j, c.vin.get(), c.stream);
+            precond_apply_dev(c, c.vin.get(), c.vout.get());
+            scatter_col_launch(c.vout.get(), c.pn, T, j, z, c.stream);
+        }
+        return;
+    }
     const int nsplit = k6t_splits(std::max<int64_t>(1, rows), s);
     c.bW.ensure(size_t(s * T));
     c.Wpart.ensure(size_t(nsplit) * size_t(s * T));

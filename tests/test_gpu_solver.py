@@ -341,8 +341,10 @@ def test_multi_rhs_train_stale_batched_buffers(krr, oracle, kpath):
             assert np.all(np.isfinite(res.model.c))
             assert rel(res.model.c, fam[0].c) <= 1e-8, (t, rel(res.model.c, fam[0].c))
             for j in range(t):
+                # ~190-iteration runs: the first crossing of tau moves by a few iterations with any
+                # change of rounding; alpha above is the parity bar here
                 its = [f.iterations[j] for f in fam]
-                assert min(its) - 1 <= res.report.per_rhs[j].iterations <= max(its) + 1, (t, j, its)
+                assert min(its) - 3 <= res.report.per_rhs[j].iterations <= max(its) + 3, (t, j, its)
     finally:
         ctx.close()
 
