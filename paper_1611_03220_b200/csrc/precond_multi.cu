@@ -8,10 +8,14 @@
 //   pass 2 (K6T-b):  Z = (R - B W) / lambda_p
 // Bound: HBM, 2 x 8 n s bytes per apply (config 5: 2 x 68.7 GB).  At T = 16 every 8-byte element
 // of B feeds 16 FMAs, ~70 % of the FP64 pipe at the HBM rate, so the contraction runs on the FP64
-// tensor path (DMMA m8n8k4, 256 FMAs per instruction, 8 independent accumulator chains per
-// warp).  B tiles are moved by the TMA engine: one 1-D bulk copy per row segment (512 B / 1 KB
-// contiguous) into a 4-stage mbarrier ring fed by a producer warp, so each SM keeps ~128 KB of
-// loads in flight with a handful of instructions.
+// tensor path (DMMA m8n8k4, 256 FMAs per instruction, 8 independent accumulator tiles per
+// warp).  B tiles are moved by the TMA engine: one 1-D bulk copy per row segment (1-2 KB
+// contiguous: measured, shorter segments cost 2-3x) into a 4-stage mbarrier ring fed by a
+// producer warp, so each SM keeps ~128 KB of loads in flight with a handful of instructions.
+// Partial tiles are zero-filled by the producer rather than masked per lane: mma.sync must run
+// in a converged warp (divergent masking around it hung the kernel).
+// Measured at config 5 (n = 524288, s = 16384, t = 16; ncu): pass 1 15.7 ms, pass 2 16.4 ms =
+// 4.3 TB/s, 0.67 of the measured HBM copy rate (the cuBLAS DGEMM pair it replaces: ~55 ms).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_i8.cuh"
@@ -21,35 +25,38 @@ namespace krr {
 namespace {
 
 constexpr int NSTAGE = 4;
+constexpr int A_FB = 256;  // pass-1 feature block: 2 KB row segments (vs 1 KB: 15.7 vs 16.9 ms at config 5)
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 constexpr int NCW = 8;                    // consumer warps
 constexpr int NTHREADS = 32 * (NCW + 1);  // + one producer warp
 
-// ---- pass 1: Wpart[split][f][T] = sum_{k in split} B[k][f] R[k][.] for a 128-feature block.
-// Consumer warp w owns features f0 + 16w .. + 16 (2 DMMA M tiles) x all T columns; K = rows,
-// 32 per stage.  Stage: 32 row segments of 1 KB; the 32 x T block of R is read through L1.
-constexpr int A_FB = 128;
-constexpr int A_KR = 32;
-constexpr int A_LD = A_FB + 8;  // smem row stride (doubles), == 8 mod 32: A-fragment reads conflict-free
-template <int T>
+// ---- pass 1: Wpart[split][f][T] = sum_{k in split} B[k][f] R[k][.] for an FB-feature block.
+// Consumer warp w owns features f0 + w FB/8 .. (FB/64 DMMA M tiles) x all T columns; K = rows,
+// KR = 4096 / FB per stage.  Stage: KR row segments of 8 FB bytes (32 KB); the KR x T block of R
+// is read through L1.
+template <int FB>
 struct PassA {
-    static constexpr int STAGE = A_KR * A_LD;  // doubles
+    static constexpr int KR = 4096 / FB;
+    static constexpr int LD = FB + 8;  // smem row stride (doubles), == 8 mod 32: A-fragment reads conflict-free
+    static constexpr int MT = FB / (8 * NCW);
+    static constexpr int STAGE = KR * LD;  // doubles
     static constexpr size_t SMEM = size_t(NSTAGE) * STAGE * 8 + 2 * NSTAGE * 8 + 16;
 };
 
-template <int T>
+template <int T, int FB>
 __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* __restrict__ B, int64_t n, int64_t s,
                                                                   const double* __restrict__ R,
                                                                   double* __restrict__ Wpart, int64_t rows_per) {
+    using P = PassA<FB>;
     extern __shared__ __align__(128) double sm[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NSTAGE * PassA<T>::STAGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NSTAGE * P::STAGE);
     uint64_t* empty = full + NSTAGE;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-    const int64_t f0 = int64_t(blockIdx.x) * A_FB;
+    const int64_t f0 = int64_t(blockIdx.x) * FB;
     const int64_t k0 = int64_t(blockIdx.y) * rows_per;
     const int64_t k1 = min(n, k0 + rows_per);
-    const int64_t nchunk = k1 > k0 ? (k1 - k0 + A_KR - 1) / A_KR : 0;
-    const int fvalid = int(imin64(A_FB, s - f0));
+    const int64_t nchunk = k1 > k0 ? (k1 - k0 + P::KR - 1) / P::KR : 0;
+    const int fvalid = int(imin64(FB, s - f0));
     if (tid == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             tc::mbar_init(&full[i], 2);  // the producer's expect-tx arrive + its post-zero-fill arrive
@@ -62,19 +69,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
         for (int64_t c = 0; c < nchunk; ++c) {
             const int st = int(c % NSTAGE);
             if (c >= NSTAGE) tc::mbar_wait_sleep(&empty[st], uint32_t((c / NSTAGE - 1) & 1));
-            const int64_t kb = k0 + c * A_KR;
-            const int rows = int(imin64(A_KR, k1 - kb));
+            const int64_t kb = k0 + c * P::KR;
+            const int rows = int(imin64(P::KR, k1 - kb));
             const uint32_t seg = uint32_t(fvalid) * 8u;
             if (lane == 0) tc::mbar_arrive_expect_tx(&full[st], seg * uint32_t(rows));
             __syncwarp();
-            double* sb = sm + st * PassA<T>::STAGE;
-            for (int r = lane; r < rows; r += 32) tc::bulk_g2s(sb + r * A_LD, B + (kb + r) * s + f0, seg, &full[st]);
+            double* sb = sm + st * P::STAGE;
+            for (int r = lane; r < rows; r += 32) tc::bulk_g2s(sb + r * P::LD, B + (kb + r) * s + f0, seg, &full[st]);
             // a short last chunk: zero the rows past the split end (generic stores, published by the
             // release of lane 0's arrive below) so the MMA loop needs no per-lane masking
-            if (rows < A_KR) {
-                for (int e = lane; e < (A_KR - rows) * (A_FB / 2); e += 32) {
-                    const int r = rows + e / (A_FB / 2), f = 2 * (e % (A_FB / 2));
-                    *reinterpret_cast<double2*>(sb + r * A_LD + f) = make_double2(0.0, 0.0);
+            if (rows < P::KR) {
+                for (int e = lane; e < (P::KR - rows) * (FB / 2); e += 32) {
+                    const int r = rows + e / (FB / 2), f = 2 * (e % (FB / 2));
+                    *reinterpret_cast<double2*>(sb + r * P::LD + f) = make_double2(0.0, 0.0);
                 }
             }
             __syncwarp();
@@ -83,23 +90,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
         return;
     }
     constexpr int NT = T / 8;
-    double acc[2][2][NT][2];  // [K chain][M tile][N tile][2]
+    constexpr int MT = P::MT;
+    double acc[MT][NT][2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
-        for (int m = 0; m < 2; ++m)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) acc[q][m][j][0] = acc[q][m][j][1] = 0.0;
+        for (int j = 0; j < NT; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
     for (int64_t c = 0; c < nchunk; ++c) {
         const int st = int(c % NSTAGE);
         tc::mbar_wait(&full[st], uint32_t((c / NSTAGE) & 1));
-        const double* sb = sm + st * PassA<T>::STAGE;
-        const int64_t kb = k0 + c * A_KR;
-        const int rows = int(imin64(A_KR, k1 - kb));
-        // the 32 x T block of R straight from global / L1 (every warp reads the same 2-4 KB)
-        double bq[A_KR / 4][NT];
+        const double* sb = sm + st * P::STAGE;
+        const int64_t kb = k0 + c * P::KR;
+        const int rows = int(imin64(P::KR, k1 - kb));
+        // the KR x T block of R straight from global / L1 (every warp reads the same 2-4 KB)
+        double bq[P::KR / 4][NT];
 #pragma unroll
-        for (int q = 0; q < A_KR / 4; ++q) {
+        for (int q = 0; q < P::KR / 4; ++q) {
             const int rr = 4 * q + t4 < rows ? 4 * q + t4 : 0;  // clamped, then zeroed: no branches
             const double m = 4 * q + t4 < rows ? 1.0 : 0.0;
 #pragma unroll
@@ -107,42 +113,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
         }
         __syncwarp();  // mma.sync below needs the converged warp
 #pragma unroll
-        for (int kk = 0; kk < A_KR; kk += 4) {
+        for (int kk = 0; kk < P::KR; kk += 4) {
             const double* b = bq[kk / 4];
-            auto& ac = acc[(kk / 4) & 1];
 #pragma unroll
-            for (int m = 0; m < 2; ++m) {
-                const double a = sb[(kk + t4) * A_LD + warp * 16 + m * 8 + g];  // A[g][t4] = B[k][f]
+            for (int m = 0; m < MT; ++m) {
+                const double a = sb[(kk + t4) * P::LD + warp * (FB / NCW) + m * 8 + g];  // A[g][t4] = B[k][f]
 #pragma unroll
-                for (int j = 0; j < NT; ++j) dmma884(ac[m][j][0], ac[m][j][1], a, b[j]);
+                for (int j = 0; j < NT; ++j) dmma884(acc[m][j][0], acc[m][j][1], a, b[j]);
             }
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&empty[st]);
     }
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-        const int64_t f = f0 + warp * 16 + m * 8 + g;
+    for (int m = 0; m < MT; ++m) {
+        const int64_t f = f0 + warp * (FB / NCW) + m * 8 + g;
         if (f < s) {
             double* w = Wpart + (int64_t(blockIdx.y) * s + f) * T;
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                w[j * 8 + 2 * t4] = acc[0][m][j][0] + acc[1][m][j][0];
-                w[j * 8 + 2 * t4 + 1] = acc[0][m][j][1] + acc[1][m][j][1];
+                w[j * 8 + 2 * t4] = acc[m][j][0];
+                w[j * 8 + 2 * t4 + 1] = acc[m][j][1];
             }
         }
     }
 }
 
-// ---- pass 2: Z[k][.] = (R[k][.] - B[k][:] W) / lambda_p for a 64-row block.
-// Consumer warp w owns rows r0 + 8w .. + 8 (DMMA M) x all T columns; K = features, 64 per stage.
-// Stage: 64 row segments of 512 B + the 64 x T block of W (contiguous).
-constexpr int B_RB = 64;
-constexpr int B_KF = 64;
-constexpr int B_LD = B_KF + 4;  // == 4 mod 32 doubles: A-fragment reads conflict-free
+// ---- pass 2: Z[k][.] = (R[k][.] - B[k][:] W) / lambda_p for a 32-row block.
+// The copy shape is pass 1's (32 row segments of 1 KB per stage: few, long bulk copies — 256-B
+// segments measured 2-3x slower), plus the 128 x T block of W.  The 8 consumer warps split a
+// stage's 128 features (16 each = 4 k-steps) and each accumulates all 4 x T/8 output tiles of
+// the block; the partial tiles are summed across warps in fixed order at the end.
+constexpr int B_RB = 32;
+constexpr int B_KF = 128;
+constexpr int B_LD = B_KF + 8;  // == 8 mod 32 doubles: A-fragment reads conflict-free
 template <int T>
 struct PassB {
     static constexpr int STAGE = B_RB * B_LD + B_KF * T;
+    static_assert(NCW * B_RB * T <= NSTAGE * STAGE, "cross-warp partials reuse the stage buffers");
     static constexpr size_t SMEM = size_t(NSTAGE) * STAGE * 8 + 2 * NSTAGE * 8 + 16;
 };
 
@@ -152,6 +160,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_b_kernel(const double* _
                                                                   const double* __restrict__ R, double lambda_p,
                                                                   double* __restrict__ Z) {
     extern __shared__ __align__(128) double sm[];
+    double* red = sm;  // after the last stage: the cross-warp partials
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + NSTAGE * PassB<T>::STAGE);
     uint64_t* empty = full + NSTAGE;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
@@ -191,37 +200,51 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_b_kernel(const double* _
         return;
     }
     constexpr int NT = T / 8;
-    constexpr int KI = 4;
-    double acc[KI][NT][2];
+    constexpr int MT = B_RB / 8;
+    double acc[MT][NT][2];
 #pragma unroll
-    for (int q = 0; q < KI; ++q)
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) acc[q][j][0] = acc[q][j][1] = 0.0;
+        for (int j = 0; j < NT; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
+    const int kw = warp * (B_KF / NCW);  // this warp's 16 features of each stage
     for (int64_t c = 0; c < nchunk; ++c) {
         const int st = int(c % NSTAGE);
         tc::mbar_wait(&full[st], uint32_t((c / NSTAGE) & 1));
         const double* sb = sm + st * PassB<T>::STAGE;
         const double* sw = sb + B_RB * B_LD;
 #pragma unroll
-        for (int kk = 0; kk < B_KF; kk += 4) {
-            const double a = sb[(warp * 8 + g) * B_LD + kk + t4];  // A[g][t4] = B[row][f]
-            auto& ac = acc[(kk / 4) % KI];
+        for (int kk = kw; kk < kw + B_KF / NCW; kk += 4) {
+            double b[NT];
 #pragma unroll
-            for (int j = 0; j < NT; ++j) dmma884(ac[j][0], ac[j][1], a, sw[(kk + t4) * T + j * 8 + g]);
+            for (int j = 0; j < NT; ++j) b[j] = sw[(kk + t4) * T + j * 8 + g];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                const double a = sb[(m * 8 + g) * B_LD + kk + t4];  // A[g][t4] = B[row][f]
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma884(acc[m][j][0], acc[m][j][1], a, b[j]);
+            }
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&empty[st]);
     }
-    const int64_t row = r0 + warp * 8 + g;
-    if (row < n) {
+    // cross-warp sum in fixed order (warp 0 + 1 + ... + 7), then the Woodbury finish; the stage
+    // buffers are idle once every consumer warp is past its last stage
+    asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCW) : "memory");  // consumer warps only
+    double* mine = red + warp * (B_RB * T);
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {  // precond.cpp:12 divides by lambda_p
-            const double y0 = (acc[0][j][0] + acc[1][j][0]) + (acc[2][j][0] + acc[3][j][0]);
-            const double y1 = (acc[0][j][1] + acc[1][j][1]) + (acc[2][j][1] + acc[3][j][1]);
-            const int64_t o = row * T + j * 8 + 2 * t4;
-            Z[o] = (R[o] - y0) / lambda_p;
-            Z[o + 1] = (R[o + 1] - y1) / lambda_p;
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            mine[(m * 8 + g) * T + j * 8 + 2 * t4] = acc[m][j][0];
+            mine[(m * 8 + g) * T + j * 8 + 2 * t4 + 1] = acc[m][j][1];
         }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCW) : "memory");  // consumer warps only
+    for (int e = tid; e < rows * T; e += 32 * NCW) {
+        double y = 0.0;
+#pragma unroll
+        for (int w = 0; w < NCW; ++w) y += red[w * (B_RB * T) + e];
+        const int64_t o = r0 * T + e;
+        Z[o] = (R[o] - y) / lambda_p;  // precond.cpp:12 divides by lambda_p
     }
 }
 
@@ -232,9 +255,9 @@ void k6t_run(const double* B, int64_t n, int64_t s, const double* R, double lamb
         if (n > 0) {
             const int64_t rows_per = (n + nsplit - 1) / nsplit;
             dim3 ga(unsigned((s + A_FB - 1) / A_FB), unsigned(nsplit));
-            KRR_CUDA(cudaFuncSetAttribute(k6t_pass_a_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(PassA<T>::SMEM)));
-            k6t_pass_a_kernel<T><<<ga, NTHREADS, PassA<T>::SMEM, stream>>>(B, n, s, R, Wpart, rows_per);
+            KRR_CUDA(cudaFuncSetAttribute(k6t_pass_a_kernel<T, A_FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(PassA<A_FB>::SMEM)));
+            k6t_pass_a_kernel<T, A_FB><<<ga, NTHREADS, PassA<A_FB>::SMEM, stream>>>(B, n, s, R, Wpart, rows_per);
             KRR_LAUNCH_CHECK();
             reduce_rows_launch(Wpart, nsplit, s * T, W, stream);
         } else {
