@@ -15,7 +15,7 @@
 // Partial tiles are zero-filled by the producer rather than masked per lane: mma.sync must run
 // in a converged warp (divergent masking around it hung the kernel).
 // Measured at config 5 (n = 524288, s = 16384, t = 16; ncu): pass 1 15.7 ms, pass 2 16.4 ms =
-// 4.3 TB/s, 0.67 of the measured HBM copy rate (the cuBLAS DGEMM pair it replaces: ~55 ms).
+// 4.3 TB/s, 0.67 of the measured HBM copy rate.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_i8.cuh"
