@@ -178,6 +178,11 @@ void reduce_rows_launch(const double* Wpart, int nchunks, int64_t s, double* W,
 int zrow_blocks(int64_t n);
 // K6T (precond_multi.cu): Woodbury apply for T = 8 / 16 interleaved columns on the DMMA path.
 // which: 1 = pass 1 (W = B^T R, reduced), 2 = pass 2 (Z = (R - B W) / lambda_p), 3 = both.
+// K3-I8 (gram_i8.cu): G = Z^T Z (column-major lower triangle) on tcgen05 INT8 Ozaki slices.
+int64_t gram_i8_spad(int64_t s);
+size_t gram_i8_scratch_bytes(int64_t rows, int64_t s);
+void gram_i8_launch(const double* Z, int64_t rows, int64_t s, double* G, uint8_t* scratch, int* ex,
+                    unsigned long long* maxbits, int* bad, int2* tiles, cudaStream_t stream);
 int k6t_splits(int64_t n, int64_t s);
 bool k6t_supported(int64_t s, const void* B);  // even s (16-byte aligned rows of B)
 void precond_multi_launch(const double* B, int64_t n, int64_t s, const double* R, double lambda_p, double* Z,

@@ -190,6 +190,11 @@ struct Ctx {
     int64_t pn = 0, s = 0, z0 = 0, z1 = 0;
     double lambda_p = 1.0;
     double build_ms[3] = {0.0, 0.0, 0.0};  // last precond build: Z^T Z, Cholesky (+ retry), U = L^-1 Z^T
+    // K3-I8 scratch (gram_i8.cu): one unit's slices, feature exponents, column maxima, flag, tile list
+    DevMem<uint8_t> gscr;
+    DevMem<int> gex, gbad;
+    DevMem<unsigned long long> gmax;
+    DevMem<int2> gtiles;
     DevMem<double> Z, G, Gcopy, W, Wpart, work, brff, wrff, wpad, chk;
     DevMem<int> info;
 
@@ -231,6 +236,17 @@ struct Ctx {
 };
 
 namespace {
+
+// G (s x s, column-major lower triangle) = Z^T Z over `rows` rows of Z on K3-I8.
+void gram_dev(Ctx& c, const double* Z, int64_t rows, int64_t s, double* G) {
+    const int64_t sp = gram_i8_spad(s);
+    c.gscr.ensure(gram_i8_scratch_bytes(rows, s));
+    c.gex.ensure(size_t(sp));
+    c.gmax.ensure(size_t(sp));
+    c.gbad.ensure(1);
+    c.gtiles.ensure(size_t((sp / 128) * (sp / 64)));
+    gram_i8_launch(Z, rows, s, G, c.gscr.get(), c.gex.get(), c.gmax.get(), c.gbad.get(), c.gtiles.get(), c.stream);
+}
 
 void require_data(const Ctx& c) {
     if (!c.has_data) fail(KRR_ERR_STATE, "no data set on the context (call krr_set_data first)");
@@ -543,14 +559,8 @@ void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
     const double one = 1.0, zero = 0.0;
     Events ev(4);
     KRR_CUDA(cudaEventRecord(ev[0], c.stream));
-    if (rows > 0) {
-        // G = Z^T Z (lower): Z row-major rows x s == col-major A = Z^T (s x rows); G = A A^T.
-        cublas_check(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(s), int(rows), &one,
-                                 c.Z.get(), int(s), &zero, c.G.get(), int(s)),
-                     "cublasDsyrk(Z^T Z)");
-    } else {
-        KRR_CUDA(cudaMemsetAsync(c.G.get(), 0, sizeof(double) * size_t(s * s), c.stream));
-    }
+    // G = Z^T Z (precond.cpp:23): K3-I8, column-major lower triangle (gram_i8.cu)
+    gram_dev(c, c.Z.get(), rows, s, c.G.get());
     allreduce_sum(c, c.G.get(), s * s);
     diag_add_launch(c.G.get(), s, lambda_p, c.stream);  // precond.cpp:24
     KRR_CUDA(cudaEventRecord(ev[1], c.stream));
@@ -982,9 +992,7 @@ krr_quality_report quality_test_dev(Ctx& c, double lambda) {
     DevMem<double> G, ev;
     G.ensure(size_t(s * s));
     ev.ensure(size_t(s));
-    cublas_check(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(s), int(n), &one, c.Z.get(), int(s),
-                             &zero, G.get(), int(s)),
-                 "cublasDsyrk(Z^T Z)");
+    gram_dev(c, c.Z.get(), n, s, G.get());  // Z^T Z on K3-I8 (lower triangle, what syevd reads)
     syevd_dev(c, G.get(), s, ev.get());
     std::vector<double> evh(static_cast<size_t>(s));
     KRR_CUDA(cudaMemcpyAsync(evh.data(), ev.get(), sizeof(double) * size_t(s), cudaMemcpyDeviceToHost, c.stream));

@@ -408,3 +408,28 @@ def test_precond_apply_columns_k6t_matches_oracle(krr, oracle, n, s, t):
     assert rel(got, want) <= 1e-11, rel(got, want)
     for j in (0, t - 1):
         assert rel(got[:, j], p.apply(x[:, j])) <= 1e-13
+
+
+@pytest.mark.parametrize("n,s", [(50000, 300), (1000, 2), (33, 129), (40000, 1000)])
+def test_gram_k3i8_build_matches_oracle(krr, oracle, n, s):
+    """build_preconditioner's Z^T Z on K3-I8 (tcgen05 INT8 Ozaki slices, units of 16384 rows):
+    U = L^-1 Z^T against the oracle (precond.cpp:20-40), with feature columns spanning many
+    binades and an all-zero column (per-column exponents)."""
+    rng = np.random.default_rng(n + s)
+    z = oracle.random_matrix(n, s, 77)
+    z *= np.exp2(rng.integers(-20, 20, size=s))[None, :]
+    z[:, s // 2] = 0.0
+    lp = 1e-3
+    u_ref, jit = oracle.build_preconditioner(z, lp)
+    u_alt, _ = oracle.build_preconditioner(z, lp, order=1)  # another legitimate summation order
+    floor = rel(u_alt, u_ref)
+    p = krr.build_preconditioner(z, lp)
+    assert p.jitter_used == jit
+    assert rel(p.u, u_ref) <= max(1e-11, 10 * floor), (rel(p.u, u_ref), floor)
+
+
+def test_gram_non_finite_sketch_not_positive_definite(krr):
+    z = np.ones((100, 8))
+    z[3, 5] = np.nan
+    with pytest.raises(krr.NotPositiveDefinite):
+        krr.build_preconditioner(z, 1.0)
