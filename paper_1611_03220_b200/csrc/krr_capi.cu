@@ -556,7 +556,6 @@ void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
     c.Gcopy.ensure(size_t(s * s));
     c.chk.ensure(4);
     c.info.ensure(1);
-    const double one = 1.0, zero = 0.0;
     Events ev(4);
     KRR_CUDA(cudaEventRecord(ev[0], c.stream));
     // G = Z^T Z (precond.cpp:23): K3-I8, column-major lower triangle (gram_i8.cu)
@@ -588,13 +587,8 @@ void precond_build(Ctx& c, double lambda_p, int* jitter_used) {
     c.sync();
     if (h[0] < 1e-300) fail(KRR_ERR_SINGULAR_TRIANGULAR, "triangular_solve: diagonal entry below 1e-300");
     KRR_CUDA(cudaEventRecord(ev[2], c.stream));
-    if (rows > 0) {
-        // U = L^-1 Z^T in place: col-major s x rows, ld = s  (precond.cpp:38)
-        cublas_check(cublasDtrsm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                                 CUBLAS_DIAG_NON_UNIT, int(s), int(rows), &one, c.G.get(), int(s),
-                                 c.Z.get(), int(s)),
-                     "cublasDtrsm(L^-1 Z^T)");
-    }
+    // U = L^-1 Z^T in place over the row-major Z (precond.cpp:38): K5 on DMMA (trsm.cu)
+    trsm_lower_launch(c.Z.get(), rows, s, c.G.get(), c.stream);
     KRR_CUDA(cudaEventRecord(ev[3], c.stream));
     c.lambda_p = lambda_p;
     c.sync();
