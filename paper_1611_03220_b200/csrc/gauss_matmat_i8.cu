@@ -110,17 +110,13 @@ struct MI8Args {
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NEPI * 32) : "memory"); }
 
 // the bits of the double 1.5 * 2^52 + 2^31 + (2^14 a + b)  (K1-I8's drain, exact)
-__device__ __forceinline__ double magic_pack(int32_t a, int32_t b) {
-    double r;
-    asm("{\n\t.reg .b64 base, prod;\n\t"
-        "mov.b64 base, {%2, %3};\n\t"
-        "mad.wide.s32 prod, %1, 16384, base;\n\t"
-        "mov.b64 %0, prod;\n\t}\n"
-        : "=d"(r)
-        : "r"(a), "r"(int(uint32_t(b) ^ 0x80000000u)), "r"(0x43380000));
-    return r;
-}
 constexpr double M2 = 6755401588539392.0 + 25165832.0;
+// The same with 64-bit inputs: M1 + 16384 a + b for |16384 a + b| < 2^51.  K1T-I8's chunks reach
+// kp = 448 bytes, where a group sum can reach 8 x 127^2 x 448 = 5.8e7 and b_k = 128 G_2k + G_2k+1
+// no longer fits in int32 (K1-I8, kp <= 96, stays below 1.6e9); the combination is int64 here.
+__device__ __forceinline__ double magic_pack64(int64_t a, int64_t b) {
+    return __longlong_as_double(0x4338000080000000LL + a * 16384 + b);
+}
 
 // swizzled shared-memory indices
 __device__ __forceinline__ int e_idx(int r, int c) { return r * ELD + (c ^ ((r >> 2) & 3)); }
@@ -295,7 +291,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
 
                 MI8_TRACE(etid == 0, tq, 0);
                 // ---- drain the 8 groups two at a time (K1-I8's integer combination)
-                int32_t bint[CPT];
+                int64_t bint[CPT];
                 double lo[CPT], T[CPT];
                 auto stage = [&](int ca, auto&& fn) {
                     tc::mbar_wait_sleep(g_full + ca + 1, ph);
@@ -306,7 +302,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     tc::tmem_ld16(taddr + uint32_t(ca * TJ), gh);
                     tc::tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) fn(k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
+                    for (int k = 0; k < CPT; ++k) fn(k, int64_t(int32_t(gh[k])) * 128 + int32_t(gl[k]));
                     tc::fence_before();
                     __syncwarp();
                     if (lane == 0) {
@@ -314,11 +310,11 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                         tc::mbar_arrive(g_empty + ca);
                     }
                 };
-                stage(6, [&](int k, int32_t b) { bint[k] = b; });
+                stage(6, [&](int k, int64_t b) { bint[k] = b; });
                 MI8_TRACE(etid == 0, tq, 1);
-                stage(4, [&](int k, int32_t b) { lo[k] = magic_pack(b, bint[k]); });
-                stage(2, [&](int k, int32_t b) { bint[k] = b; });
-                stage(0, [&](int k, int32_t b) { T[k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2); });
+                stage(4, [&](int k, int64_t b) { lo[k] = magic_pack64(b, bint[k]); });
+                stage(2, [&](int k, int64_t b) { bint[k] = b; });
+                stage(0, [&](int k, int64_t b) { T[k] = fma(lo[k], 0x1p-28, magic_pack64(b, bint[k]) - M2); });
 
                 MI8_TRACE(etid == 0, tq, 2);
                 // ---- exp phase: E tile (masked on the diagonal blocks) into shared memory

@@ -127,3 +127,24 @@ def test_train_large_d_graph_loop_matches_oracle(krr, oracle, ctx):
     st = res.report.per_rhs[0]
     assert st.converged and abs(st.iterations - ref.iterations[0]) <= 1, (st.iterations, ref.iterations[0])
     assert rel(res.model.c, ref.c) <= 1e-8, rel(res.model.c, ref.c)
+
+
+@pytest.mark.parametrize("d", [440, 96])
+def test_i8_matmat_worst_case_slice_sums(krr, oracle, ctx, d):
+    """Inputs whose Ozaki digits are all +-127 (x = +-(1 - 2^-53)): the group sums reach
+    8 x 127^2 x kp, which for kp = 448 overflows an int32 combination 128 G_2k + G_2k+1 — the
+    drain combines in int64 (gauss_matmat_i8.cu).  Checked against the oracle and the DMMA K1T."""
+    n, t = 512, 16
+    rng = np.random.default_rng(5)
+    x = np.where(rng.random((n, d)) < 0.9, 1.0, -1.0) * (1.0 - 2.0 ** -53)
+    x[:, 0] = 1.0 - 2.0 ** -53  # every row's max |x| sets e = 0: all digits 127
+    v = oracle.random_matrix(n, t, 8)
+    sigma, lam = 30.0, 1e-3
+    ctx.set_option("k1t_path", 1)
+    op = krr.GaussianOperator(x, krr.KernelSpec.gaussian(sigma), lam, ctx=ctx)
+    assert ctx.get_option("k1t_path_effective") == 1
+    got = op.matmat(v)
+    want = oracle.kernel_matvec(x, sigma, lam, v)
+    assert rel(got, want) <= 1e-13, rel(got, want)
+    ctx.set_option("k1t_path", 0)
+    assert rel(got, op.matmat(v)) <= 1e-13
