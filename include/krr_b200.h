@@ -97,7 +97,10 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
  *                         diagonal on rank 0) with no collective, so K v returns that rank's
  *                         partial — the multi-rank K1 checked on one GPU (sum over r = K v)
  *   "poison_batched" 1|0  test only: fill the batched (t > 1) PCG vectors with NaN bytes whenever
- *                         they are (re)used, standing in for stale contents of an earlier call */
+ *                         they are (re)used, standing in for stale contents of an earlier call
+ *   "nccl_always" 1|0  test only, contexts with a communicator: run the collectives even with
+ *                         world = 1 (identity all-reduces), so one GPU exercises the multi-rank
+ *                         data path, NCCL inside the graph-resident PCG loop included */
 int krr_set_option(krr_ctx* ctx, const char* key, double value);
 /* Arithmetic of the fused mat-vec (SURVEY §8b krr_set_precision; north-star "optional fp32
  * mode, reported separately"): 64 = fp64, oracle-matching (default); 32 = fp32-accuracy K1

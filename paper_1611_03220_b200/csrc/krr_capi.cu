@@ -206,6 +206,10 @@ struct Ctx {
     // body is one iteration and a device-side stop decision (no host round trip per iteration)
     bool pcg_graph = true;
     bool poison_batched = false;  // test-only (krr_set_option "poison_batched")
+    // test-only (krr_set_option "nccl_always"): run the collectives even on a one-rank
+    // communicator (an identity all-reduce), so a single GPU exercises the multi-rank data path,
+    // including NCCL kernels captured inside the graph-resident PCG loop
+    bool nccl_always = false;
     DevMem<int> ctl;
     DevMem<double> dhist;
     DevMem<double> bx, br, bz, bp, bap, by, bin, bout, bpart, bred, bscal, bW;
@@ -253,7 +257,7 @@ void require_data(const Ctx& c) {
 }
 
 void allreduce_sum(Ctx& c, double* buf, int64_t count) {
-    if (c.world <= 1) return;
+    if (c.world <= 1 && !(c.nccl_always && c.comm)) return;
     nccl_check(nccl().allReduce(buf, buf, size_t(count), ncclDouble, ncclSum, c.comm, c.stream),
                "ncclAllReduce");
 }
@@ -646,7 +650,7 @@ struct PcgOut {
 // The graph-resident PCG loop: the same kernels in the same order as pcg_core's host loop
 // (bitwise-identical iterates), captured once into the body of a conditional WHILE node; a
 // one-thread control kernel makes solver.cpp:37-52's stop / breakdown decision on the device.
-// Single rank, no host observer.  Precondition: the caller ran the prologue (x = 0, r = y,
+// No host observer (any world size).  Precondition: the caller ran the prologue (x = 0, r = y,
 // z = M r, p = z, scal[2] = r'z) and norm_y > 0.
 void pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double norm_y, double tau, int max_iter,
                     double* hist, PcgOut& out) {
@@ -756,7 +760,10 @@ PcgOut pcg_core(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, const double*
     copy_launch(c.vp.get(), z, n, c.stream);  // p = z
     dot_partial_launch(c.vr.get(), z, n, rz_part, nb, c.stream);
     sum_partials_launch(rz_part, nb, scal + 2, c.stream);
-    if (device_ops && c.pcg_graph && !obs && c.world == 1) {
+    // multi-rank too: the NCCL all-reduces are captured into the loop body (relaxed capture), and
+    // every stop decision is made from all-reduced (rank-identical) vectors, so all ranks run the
+    // same number of iterations without a host round trip
+    if (device_ops && c.pcg_graph && !obs) {
         pcg_graph_loop(c, n, A, M, norm_y, tau, max_iter, hist, out);
         return out;
     }
@@ -1304,6 +1311,9 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
             c.pcg_graph = value != 0.0;
         } else if (k == "poison_batched") {
             c.poison_batched = value != 0.0;
+        } else if (k == "nccl_always") {
+            if (!c.comm && value != 0.0) fail(KRR_ERR_STATE, "nccl_always needs a communicator (krr_ctx_create_dist)");
+            c.nccl_always = value != 0.0;
         } else if (k == "emulate_world" || k == "emulate_rank") {
             if (c.world != 1) fail(KRR_ERR_STATE, "rank emulation is for single-rank contexts");
             const int iv = int(value);
