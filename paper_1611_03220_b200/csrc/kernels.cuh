@@ -183,6 +183,8 @@ int64_t gram_i8_spad(int64_t s);
 size_t gram_i8_scratch_bytes(int64_t rows, int64_t s);
 void gram_i8_launch(const double* Z, int64_t rows, int64_t s, double* G, uint8_t* scratch, int* ex,
                     unsigned long long* maxbits, int* bad, int2* tiles, cudaStream_t stream);
+// K4 (cholesky.cu): in-place Cholesky of the column-major lower triangle; *info = 1 + first bad pivot.
+void cholesky_launch(double* G, int64_t s, int* info, cudaStream_t stream);
 // K5 (trsm.cu): U^T = Z L^-T in place (U = L^-1 Z^T), L column-major lower, on DMMA.
 void trsm_lower_launch(double* Z, int64_t n, int64_t s, const double* L, cudaStream_t stream);
 int k6t_splits(int64_t n, int64_t s);

@@ -524,22 +524,15 @@ void sketch_upload(Ctx& c, const double* Z, int64_t n, int64_t s) {
     c.has_sketch = true;
 }
 
-// Returns true when the factorisation succeeded (finite, positive pivots).
+// Returns true when the factorisation succeeded (finite, positive pivots): K4 (cholesky.cu).
 bool try_potrf(Ctx& c, int64_t s) {
-    // Non-finite input (e.g. Z'Z overflowed to inf) can slip through potrf's pivot test.
+    // Non-finite input (e.g. Z'Z overflowed to inf) must fail like LLT on the reference's G.
     diag_check_launch(c.G.get(), s, c.chk.get(), c.stream);
     double h[2];
     KRR_CUDA(cudaMemcpyAsync(h, c.chk.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     if (h[1] != 0.0) return false;
-    int lwork = 0;
-    cusolver_check(cusolverDnDpotrf_bufferSize(c.sol, CUBLAS_FILL_MODE_LOWER, int(s), c.G.get(),
-                                               int(s), &lwork),
-                   "potrf_bufferSize");
-    c.work.ensure(size_t(std::max(1, lwork)));
-    cusolver_check(cusolverDnDpotrf(c.sol, CUBLAS_FILL_MODE_LOWER, int(s), c.G.get(), int(s),
-                                    c.work.get(), lwork, c.info.get()),
-                   "cusolverDnDpotrf");
+    cholesky_launch(c.G.get(), s, c.info.get(), c.stream);
     int hinfo = 0;
     KRR_CUDA(cudaMemcpyAsync(&hinfo, c.info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     diag_check_launch(c.G.get(), s, c.chk.get(), c.stream);

@@ -433,3 +433,17 @@ def test_gram_non_finite_sketch_not_positive_definite(krr):
     z[3, 5] = np.nan
     with pytest.raises(krr.NotPositiveDefinite):
         krr.build_preconditioner(z, 1.0)
+
+
+def test_cholesky_jitter_retry_matches_oracle(krr, oracle):
+    """precond.cpp:27-34 on the native K4 Cholesky: duplicated sketch columns with a negligible
+    lambda_p make the second pivot exactly 0, the factorisation fails, and the single retry with
+    1e-12 trace(G) / s on the diagonal succeeds — the same on the device and in the oracle."""
+    z0 = oracle.random_matrix(300, 40, 91)
+    z = np.concatenate([z0, z0[:, :3]], axis=1)  # columns 40..42 duplicate 0..2
+    lp = 1e-300
+    u_ref, jit = oracle.build_preconditioner(z, lp)
+    assert jit
+    p = krr.build_preconditioner(z, lp)
+    assert p.jitter_used
+    assert rel(p.u, u_ref) <= 1e-6, rel(p.u, u_ref)  # jittered, badly conditioned factor
