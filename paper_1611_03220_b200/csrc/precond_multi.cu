@@ -14,8 +14,10 @@
 // producer warp, so each SM keeps ~128 KB of loads in flight with a handful of instructions.
 // Partial tiles are zero-filled by the producer rather than masked per lane: mma.sync must run
 // in a converged warp (divergent masking around it hung the kernel).
-// Measured at config 5 (n = 524288, s = 16384, t = 16; ncu): pass 1 15.7 ms, pass 2 16.4 ms =
-// 4.3 TB/s, 0.67 of the measured HBM copy rate.
+// Measured at config 5 (n = 524288, s = 16384, t = 16; ncu): pass 1 15.0 ms, pass 2 16.4 ms =
+// 4.4 TB/s, 0.68 of the measured HBM copy rate, with the DMMA sub-pipe ~53 % busy.  The FP64
+// datapath caps this kernel near 0.8: at the full copy rate (22 B/clk/SM = 2.8 elements) 16
+// FMAs per element need 69 % of the 64 FMA/clk/SM that DMMA and DFMA share.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_i8.cuh"
@@ -25,7 +27,7 @@ namespace krr {
 namespace {
 
 constexpr int NSTAGE = 4;
-constexpr int A_FB = 256;  // pass-1 feature block: 2 KB row segments (vs 1 KB: 15.7 vs 16.9 ms at config 5)
+constexpr int A_FB = 256;  // pass-1 feature block: 2 KB row segments (1 KB: 16.9 ms, 2 KB: 15.0 ms, 4 KB: 15.0 ms at config 5)
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 constexpr int NCW = 8;                    // consumer warps
 constexpr int NTHREADS = 32 * (NCW + 1);  // + one producer warp
@@ -40,7 +42,8 @@ struct PassA {
     static constexpr int LD = FB + 8;  // smem row stride (doubles), == 8 mod 32: A-fragment reads conflict-free
     static constexpr int MT = FB / (8 * NCW);
     static constexpr int STAGE = KR * LD;  // doubles
-    static constexpr size_t SMEM = size_t(NSTAGE) * STAGE * 8 + 2 * NSTAGE * 8 + 16;
+    static constexpr int NST = 6;          // ring depth: ~192 KB of loads in flight per SM
+    static constexpr size_t SMEM = size_t(NST) * STAGE * 8 + 2 * NST * 8 + 16;
 };
 
 template <int T, int FB>
@@ -49,8 +52,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
                                                                   double* __restrict__ Wpart, int64_t rows_per) {
     using P = PassA<FB>;
     extern __shared__ __align__(128) double sm[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NSTAGE * P::STAGE);
-    uint64_t* empty = full + NSTAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + P::NST * P::STAGE);
+    uint64_t* empty = full + P::NST;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
     const int64_t f0 = int64_t(blockIdx.x) * FB;
     const int64_t k0 = int64_t(blockIdx.y) * rows_per;
@@ -58,7 +61,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
     const int64_t nchunk = k1 > k0 ? (k1 - k0 + P::KR - 1) / P::KR : 0;
     const int fvalid = int(imin64(FB, s - f0));
     if (tid == 0) {
-        for (int i = 0; i < NSTAGE; ++i) {
+        for (int i = 0; i < P::NST; ++i) {
             tc::mbar_init(&full[i], 2);  // the producer's expect-tx arrive + its post-zero-fill arrive
             tc::mbar_init(&empty[i], NCW);
         }
@@ -67,8 +70,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
     __syncthreads();
     if (warp == NCW) {  // producer
         for (int64_t c = 0; c < nchunk; ++c) {
-            const int st = int(c % NSTAGE);
-            if (c >= NSTAGE) tc::mbar_wait_sleep(&empty[st], uint32_t((c / NSTAGE - 1) & 1));
+            const int st = int(c % P::NST);
+            if (c >= P::NST) tc::mbar_wait_sleep(&empty[st], uint32_t((c / P::NST - 1) & 1));
             const int64_t kb = k0 + c * P::KR;
             const int rows = int(imin64(P::KR, k1 - kb));
             const uint32_t seg = uint32_t(fvalid) * 8u;
@@ -97,8 +100,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
     for (int64_t c = 0; c < nchunk; ++c) {
-        const int st = int(c % NSTAGE);
-        tc::mbar_wait(&full[st], uint32_t((c / NSTAGE) & 1));
+        const int st = int(c % P::NST);
+        tc::mbar_wait(&full[st], uint32_t((c / P::NST) & 1));
         const double* sb = sm + st * P::STAGE;
         const int64_t kb = k0 + c * P::KR;
         const int rows = int(imin64(P::KR, k1 - kb));
