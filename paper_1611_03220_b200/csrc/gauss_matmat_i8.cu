@@ -291,30 +291,41 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
 
                 MI8_TRACE(etid == 0, tq, 0);
                 // ---- drain the 8 groups two at a time (K1-I8's integer combination)
-                int64_t bint[CPT];
-                double lo[CPT], T[CPT];
-                auto stage = [&](int ca, auto&& fn) {
-                    tc::mbar_wait_sleep(g_full + ca + 1, ph);
-                    tc::mbar_wait_sleep(g_full + ca, ph);
-                    tc::fence_after();
-                    uint32_t gl[CPT], gh[CPT];
-                    tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ), gl);
-                    tc::tmem_ld16(taddr + uint32_t(ca * TJ), gh);
+                // two 8-column halves, each through all four stages: the int64 partials of one
+                // half only stay live (register pressure); the groups are released after the second
+                int64_t bint[CPT / 2];
+                double lo[CPT / 2], T[CPT];
+                auto stage = [&](int ca, int h, auto&& fn) {
+                    if (h == 0) {
+                        tc::mbar_wait_sleep(g_full + ca + 1, ph);
+                        tc::mbar_wait_sleep(g_full + ca, ph);
+                        tc::fence_after();
+                    }
+                    uint32_t gl[CPT / 2], gh[CPT / 2];
+                    tc::tmem_ld8(taddr + uint32_t((ca + 1) * TJ + h * (CPT / 2)), gl);
+                    tc::tmem_ld8(taddr + uint32_t(ca * TJ + h * (CPT / 2)), gh);
                     tc::tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) fn(k, int64_t(int32_t(gh[k])) * 128 + int32_t(gl[k]));
-                    tc::fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tc::mbar_arrive(g_empty + ca + 1);
-                        tc::mbar_arrive(g_empty + ca);
+                    for (int k = 0; k < CPT / 2; ++k) fn(k, int64_t(int32_t(gh[k])) * 128 + int32_t(gl[k]));
+                    if (h == 1) {
+                        tc::fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tc::mbar_arrive(g_empty + ca + 1);
+                            tc::mbar_arrive(g_empty + ca);
+                        }
                     }
                 };
-                stage(6, [&](int k, int64_t b) { bint[k] = b; });
-                MI8_TRACE(etid == 0, tq, 1);
-                stage(4, [&](int k, int64_t b) { lo[k] = magic_pack64(b, bint[k]); });
-                stage(2, [&](int k, int64_t b) { bint[k] = b; });
-                stage(0, [&](int k, int64_t b) { T[k] = fma(lo[k], 0x1p-28, magic_pack64(b, bint[k]) - M2); });
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    stage(6, h, [&](int k, int64_t b) { bint[k] = b; });
+                    if (h == 0) MI8_TRACE(etid == 0, tq, 1);
+                    stage(4, h, [&](int k, int64_t b) { lo[k] = magic_pack64(b, bint[k]); });
+                    stage(2, h, [&](int k, int64_t b) { bint[k] = b; });
+                    stage(0, h, [&](int k, int64_t b) {
+                        T[h * (CPT / 2) + k] = fma(lo[k], 0x1p-28, magic_pack64(b, bint[k]) - M2);
+                    });
+                }
 
                 MI8_TRACE(etid == 0, tq, 2);
                 // ---- exp phase: E tile (masked on the diagonal blocks) into shared memory
