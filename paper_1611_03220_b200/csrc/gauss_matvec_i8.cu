@@ -70,6 +70,9 @@ constexpr int NCD = 3;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
+#ifndef I8_HALF_DRAIN
+#define I8_HALF_DRAIN 0  // drain each thread's 16 columns as two 8-column halves (A/B experiment)
+#endif
 #ifndef I8_EARLY_DONE
 #define I8_EARLY_DONE 1  // arrive on epi_done after the exp element loop (1) or after the column sums (0)
 #endif
@@ -427,6 +430,46 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
 
                 // ---- drain the 8 groups in MMA completion order (7 -> 0) two at a time,
                 // 16 columns per tcgen05.ld (register pressure), releasing each pair at once
+#if I8_HALF_DRAIN
+                // two 8-column halves, each through all four stages (fewer live registers); the
+                // groups are released after the second half (the next tile's MMAs wait for the exp
+                // phase anyway: time-multiplexed)
+                int32_t bint[CPT / 2];
+                double lo[CPT / 2], T[CPT];
+                auto stage = [&](int ca, int h, auto&& fn) {
+                    uint32_t gl[CPT / 2], gh[CPT / 2];
+                    if (h == 0) {
+                        tc::mbar_wait_sleep(g_full + ca + 1, ph);
+                        tc::fence_after();
+                    }
+                    tc::tmem_ld8(taddr + uint32_t((ca + 1) * TJ + h * (CPT / 2)), gl);
+                    if (h == 0) {
+                        tc::mbar_wait_sleep(g_full + ca, ph);
+                        tc::fence_after();
+                    }
+                    tc::tmem_ld8(taddr + uint32_t(ca * TJ + h * (CPT / 2)), gh);
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < CPT / 2; ++k) fn(k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
+                    if (h == 1) {
+                        tc::fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tc::mbar_arrive(g_empty + ca + 1);
+                            tc::mbar_arrive(g_empty + ca);
+                        }
+                    }
+                };
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    stage(6, h, [&](int k, int32_t b) { bint[k] = b; });
+                    stage(4, h, [&](int k, int32_t b) { lo[k] = magic_pack(b, bint[k]); });
+                    stage(2, h, [&](int k, int32_t b) { bint[k] = b; });
+                    stage(0, h, [&](int k, int32_t b) {
+                        T[h * (CPT / 2) + k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);
+                    });
+                }
+#else
                 int32_t bint[CPT];
                 double lo[CPT], T[CPT];
                 auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
@@ -460,6 +503,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 stage(0, [&](int k, int32_t b) {
                     T[k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
                 });
+
+#endif
 
                 // ---- exp, row sums, column sums
                 I8_TRACE(etid == 0, tq, 4);

@@ -24,7 +24,8 @@ def main():
     if r.returncode:
         raise SystemExit(r.stderr)
     spills = sorted({l.strip() for l in r.stderr.splitlines() if "spill" in l})
-    objs = [str(o) for o in sorted(B.BUILD.glob("*.o")) if o.name != srcp.name + ".o"] + [str(obj)]
+    # the product library's objects only (libkrr_diag.so's diag_*.o are a separate library)
+    objs = [str(B.BUILD / (p.name + ".o")) for p in B._sources() if p.name != srcp.name] + [str(obj)]
     lib = out / f"libkrr_{name}.so"
     r = subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", str(lib)] + objs + B.LINK_LIBS, capture_output=True, text=True)
     if r.returncode:
