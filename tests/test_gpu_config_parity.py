@@ -76,3 +76,24 @@ def test_config_build_block_matches_oracle(krr, cfg):
         assert rel(ky[rows[:want.shape[0]]], want) <= 1e-13
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("lam", [3e-2, 1e-2])
+def test_config1_shape_converging_full_solve(krr, oracle, lam):
+    """The north-star bar on a BASELINE-shaped solve that converges: config 1's generator and
+    sketch (n = 8192, d = 16, sigma = 4, s = 1024 RFF, tau = 1e-6) with lambda raised from 1e-3
+    (where the reference algorithm stalls at max_iter) to 3e-2 / 1e-2 (~200 / ~430 iterations).
+    Iterations within +-1 of the oracle's three summation orders; alpha within 1e-8 of the
+    Eigen-like order when the counts match (else within the order-to-order spread)."""
+    n, d, t, sigma, _, s = krr.CONFIGS[1]
+    x, y = krr.generate_config(1, n, d, t, 0)
+    fam = [oracle.train(x, y, sigma, lam, s, 0, 1e-6, 500, order=k) for k in (2, 0, 1)]
+    cfg = krr.SolverConfig(lambda_=lam, tau=1e-6, max_iter=500, chain=krr.ChainSpec(s1=s), seed=0)
+    res = krr.train(krr.Dataset(x, y), krr.KernelSpec.gaussian(sigma), cfg)
+    st = res.report.per_rhs[0]
+    its = [f.iterations[0] for f in fam]
+    assert st.converged and all(f.converged[0] for f in fam)
+    assert min(its) - 1 <= st.iterations <= max(its) + 1, (st.iterations, its)
+    spread = max(rel(f.c, fam[0].c) for f in fam[1:])
+    bar = 1e-8 if st.iterations == its[0] else max(1e-8, 4 * spread, 10 * 1e-6)
+    assert rel(res.model.c, fam[0].c) <= bar, (rel(res.model.c, fam[0].c), st.iterations, its, spread)
