@@ -447,3 +447,18 @@ def test_cholesky_jitter_retry_matches_oracle(krr, oracle):
     p = krr.build_preconditioner(z, lp)
     assert p.jitter_used
     assert rel(p.u, u_ref) <= 1e-6, rel(p.u, u_ref)  # jittered, badly conditioned factor
+
+
+@pytest.mark.parametrize("n,s", [(1, 1), (2, 1), (1, 3), (5, 2), (130, 129), (7, 200), (64, 64), (129, 65)])
+def test_build_tiny_and_ragged_shapes(krr, oracle, n, s):
+    """The native build (K3-I8 Gram, K4 Cholesky, K5 TRSM) on degenerate and ragged shapes:
+    single rows / features, n < s (rank-deficient Gram), partial tiles, panels and blocks."""
+    z = oracle.random_matrix(n, s, 5 + n + s)
+    lp = 0.3
+    u_ref, jit = oracle.build_preconditioner(z, lp)
+    u_alt, _ = oracle.build_preconditioner(z, lp, order=1)
+    p = krr.build_preconditioner(z, lp)
+    assert p.jitter_used == jit
+    assert rel(p.u, u_ref) <= max(1e-12, 10 * rel(u_alt, u_ref)), rel(p.u, u_ref)
+    x = oracle.random_vector(n, 9)
+    assert rel(p.apply(x), oracle.precond_apply(u_ref, lp, x)) <= 1e-12
