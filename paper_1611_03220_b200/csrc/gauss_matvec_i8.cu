@@ -70,6 +70,12 @@ constexpr int NCD = 3;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
+#ifndef I8_T_SMEM
+#define I8_T_SMEM 0  // drain writes T to the warp's transpose scratch, the exp loop reads it back (A/B)
+#endif
+#ifndef I8_BW
+#define I8_BW 2      // columns per exp batch
+#endif
 #ifndef I8_HALF_DRAIN
 #define I8_HALF_DRAIN 0  // drain each thread's 16 columns as two 8-column halves (A/B experiment)
 #endif
@@ -160,9 +166,19 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
                                           uint64_t* fp64_done) {
     const double shifter = 6755399441055744.0;  // 1.5 * 2^52
     double racc[4] = {0.0, 0.0, 0.0, 0.0};
+    static_assert(I8_BW <= 4, "row-sum chains");
     // four columns at a time, each step applied across the batch: independent chains
     // side by side for the scheduler (the per-pair chain is ~16 dependent FP64 ops)
-    constexpr int BW = 2;
+    constexpr int BW = I8_BW;
+    // T of column k: registers, or (I8_T_SMEM) this lane's slot of the transpose scratch, which the
+    // element loop overwrites with e v_i for the same column right after reading it
+    auto tval = [&](int k) {
+#if I8_T_SMEM
+        return scr[k * SCR_LD + lane];
+#else
+        return T[k];
+#endif
+    };
 #pragma unroll
     for (int k0 = 0; k0 < CPT; k0 += BW) {
         double y[BW], t2[BW], f[BW], q[BW], e[BW];
@@ -174,7 +190,7 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
             for (int b = 0; b < BW; ++b) {
                 const int cl = colOff + k0 + b;
                 const double nscale = __hiloint2double(nsi_hi + cd_e[cl], nsi_lo);
-                y[b] = fma(T[k0 + b], nscale, ec.a1);
+                y[b] = fma(tval(k0 + b), nscale, ec.a1);
                 e[b] = y[b];
             }
             for (int r = 1; r < ec.degree; ++r)
@@ -192,7 +208,7 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
         for (int b = 0; b < BW; ++b) {
             const int cl = colOff + k0 + b;
             const double nscale = __hiloint2double(nsi_hi + cd_e[cl], nsi_lo);
-            y[b] = fma(T[k0 + b], nscale, sqs_i + cd_sq[cl]);
+            y[b] = fma(tval(k0 + b), nscale, sqs_i + cd_sq[cl]);
             // y <= 0 (d2 >= 0): y > 0 (rounding, near-duplicate rows) has a non-negative high
             // word; clamping it to 0 leaves a positive denormal, whose exp is 1 exactly.
             y[b] = __hiloint2double(min(__double2hiint(y[b]), 0), __double2loint(y[b]));
@@ -501,7 +517,11 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 stage(2, [&](int k, int32_t b) { bint[k] = b; });                    // b1
                 I8_TRACE(etid == 0, tq, 3);
                 stage(0, [&](int k, int32_t b) {
+#if I8_T_SMEM
+                    scr[k * SCR_LD + lane] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
+#else
                     T[k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
+#endif
                 });
 
 #endif
@@ -526,7 +546,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 if (A.debug & 2) {
                     double z = 0.0;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) z += T[k];
+                    for (int k = 0; k < CPT; ++k) z += I8_T_SMEM ? scr[k * SCR_LD + lane] : T[k];
                     rowacc += z;
                 } else if (masked) {
                     // diagonal block: keep j > i (local column index vs local row index)
