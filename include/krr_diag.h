@@ -32,6 +32,7 @@ int krr_diag_tmem_ld_rate(int device, int warps, int reps, double* bytes_per_clk
 int krr_diag_tmem_ld_under_mma(int device, int warps, int reps, double* bytes_per_clk, double* mma_cycles);
 /* clock64 stamps of CTA 0 from the last K1-I8 / K1T-I8 launch run with i8_debug bit 2 */
 int krr_diag_i8_trace(long long* out, int count);
+int krr_diag_i8x_trace(long long* out, int count);
 int krr_diag_i8t_trace(long long* out, int count);
 
 #ifdef __cplusplus

@@ -25,6 +25,7 @@ _SIGS = {
     "krr_diag_tmem_ld_rate": [_i, _i, _i, C.POINTER(_d)],
     "krr_diag_tmem_ld_under_mma": [_i, _i, _i, C.POINTER(_d), C.POINTER(_d)],
     "krr_diag_i8_trace": [_vp, _i],
+    "krr_diag_i8x_trace": [_vp, _i],
     "krr_diag_i8t_trace": [_vp, _i],
 }
 for _name, _args in _SIGS.items():

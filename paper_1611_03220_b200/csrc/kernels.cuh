@@ -53,6 +53,16 @@ void i8s_read_trace(long long* out, int count);
 constexpr int64_t kI8T1MinD = 160;  // single-RHS K v through K1T-I8 from d = 160 (when K1-I8 does not apply)
 constexpr int64_t kI8TMinD = 28;  // auto path: K1T-I8 from d = 28 (measured crossover, profiles/r1_k1t_i8_crossover.log)
 
+// K1-I8X: K1-I8's tensor-core dot products with an integer exp epilogue that overlaps the MMAs
+// (gauss_matvec_i8x.cu).  Gaussian kernel, d <= 96.  prepare returns the global exponent E of
+// z = sqrt(2 scale) x (1..8), or 0 when the data is out of its fixed-point range.
+bool i8x_supported(int64_t d, int st);
+void i8x_read_trace(long long* out, int count);
+int i8x_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, double scale, uint8_t* S, long long* sq,
+                       cudaStream_t stream);
+void gauss_matvec_i8x_launch(const GaussMatvecPlan& p, const uint8_t* S, const long long* sq, int E, const double* v,
+                             double* part, int kp, cudaStream_t stream, int debug = 0);
+
 // K1-I8: tcgen05 kind::i8 slice path (gauss_matvec_i8.cu).  Supported for d <= 96.
 bool i8_supported(int64_t d, int st);
 // K1-F32 (optional fp32-accuracy mode, gauss_matvec_f32.cu): three bf16 parts per value on

@@ -168,6 +168,11 @@ struct Ctx {
     DevMem<uint8_t> S8;
     DevMem<int> ex8, ejs8;
     DevMem<double> sq8;
+    // K1-I8X operands (slices of z = sqrt(2 scale) x under one global exponent E, SQ_i = |z_i|^2/2
+    // in fixed point); E = 0: not prepared or out of range (gauss_matvec_i8x.cu)
+    int i8x_E = 0;
+    DevMem<uint8_t> S8x;
+    DevMem<long long> sq8x;
     // K1T-I8 operands (K-chunk-major slices for the multi-RHS kernel; prepared on first use)
     int k1t_path = -1;  // -1 auto, 0 = FP64 DMMA K1T, 1 = K1T-I8 (T = 16)
     int i8s_state = 0;  // 0 not prepared, 1 ready, -1 exponent range unsupported
@@ -265,8 +270,9 @@ void allreduce_sum(Ctx& c, double* buf, int64_t count) {
 // K1 path selection: the INT8-slice tensor-core kernel where it is faster than the FP64
 // DMMA kernel on B200 (measured: d >= ~48, profiles/README.md) and the data's exponent range
 // allows it; the DMMA kernel otherwise.  Both are GPU kernels; neither is a fallback.
+bool use_i8x(const Ctx& c);
 bool use_i8(const Ctx& c) {
-    if (!c.i8_ready) return false;
+    if (!c.i8_ready || use_i8x(c)) return false;
     if (c.k1_path >= 0) return c.k1_path == 1;
     if (c.family != 0) {  // polynomial kernel (cheaper epilogue): profiles/r1_poly_k1_crossover_n65536.log
         const double dmma_ms = 2.1 + 0.14 * double(c.d);
@@ -278,6 +284,24 @@ bool use_i8(const Ctx& c) {
     const double dmma_ms = 4.40 + 0.1405 * double(c.d);
     const double i8_ms = c.kp8 <= 32 ? 8.04 : (c.kp8 <= 64 ? 10.43 : 11.9);
     return i8_ms < dmma_ms;
+}
+
+// K1-I8X (integer exp argument under the next tile's MMAs, FP64 tail in a time-multiplexed
+// phase; gauss_matvec_i8x.cu) on request (k1_path = 3) where the data's range allows it (1 <= E
+// <= 8, Gaussian).  Measured at the speed of K1-I8 (profiles/README.md), so auto keeps K1-I8.
+bool use_i8x(const Ctx& c) {
+    return c.i8x_E > 0 && c.family == 0 && c.precision == 64 && c.k1_path == 3;
+}
+
+// K1-I8X operands: prepared when k1_path = 3 is requested (at krr_set_data, or by the option once
+// data is set), outside any graph capture (the preparation reads E back to the host).
+void i8x_ensure(Ctx& c) {
+    c.i8x_E = 0;
+    if (c.k1_path != 3 || c.family != 0 || !i8x_supported(c.d, int(c.sched.st))) return;
+    const int64_t n_pad = c.plan.n_pad;
+    c.S8x.ensure(size_t(8) * size_t(n_pad) * size_t(i8_kp(c.d)));
+    c.sq8x.ensure(size_t(n_pad));
+    c.i8x_E = i8x_prepare_launch(c.X.get(), c.n, c.d, n_pad, c.scale, c.S8x.get(), c.sq8x.get(), c.stream);
 }
 
 void f32_ensure(Ctx& c) {
@@ -339,7 +363,8 @@ bool use_i8T(Ctx& c, int T) {
 // 16-column K1T-I8 pass beats the FP64 DMMA K1 from d ~ 160 (profiles/r1_k1_single_large_d.log:
 // d = 192 27 vs 34 ms, d = 440 43 vs 75 ms at n = 65536).  Prepared outside graph capture.
 bool use_i8T1(Ctx& c) {
-    if (c.precision != 64 || c.family != 0 || c.k1_path == 0 || c.d < kI8T1MinD || use_i8(c)) return false;
+    if (c.precision != 64 || c.family != 0 || c.k1_path == 0 || c.d < kI8T1MinD || use_i8(c) || use_i8x(c))
+        return false;
     if (!use_i8T(c, 16)) return false;
     ensure_batched(c, 16);
     return true;
@@ -352,6 +377,9 @@ void matvec_dev(Ctx& c, const double* v, double* out, double lambda, cudaEvent_t
     if (c.precision == 32)
         gauss_matvec_f32_launch(c.plan, c.S32.get(), c.s32.get(), v, c.v32.get(), c.part.get(), f32_kb(c.d), c.scale,
                                 c.stream);
+    else if (use_i8x(c))
+        gauss_matvec_i8x_launch(c.plan, c.S8x.get(), c.sq8x.get(), c.i8x_E, v, c.part.get(), c.kp8, c.stream,
+                                c.i8_debug);
     else if (use_i8(c))
         gauss_matvec_i8_launch(c.plan, c.S8.get(), c.ex8.get(), c.ejs8.get(), c.sq8.get(), v, c.part.get(), c.kp8,
                                c.stream, c.i8_debug, c.family == 1 ? c.degree : 0, c.gamma, c.offset);
@@ -463,6 +491,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_sp
     c.i8_ready = false;
     c.f32_ready = false;
     c.i8s_state = 0;
+    c.i8x_E = 0;
     if (i8_supported(d, int(c.sched.st))) {
         c.kp8 = i8_kp(d);
         c.S8.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8));
@@ -476,6 +505,7 @@ void set_data(Ctx& c, const double* X, int64_t n, int64_t d, const krr_kernel_sp
     p.resident = c.k1_resident;
     p.warps16 = c.k1_warps16;
     p.grouped = c.k1_grouped;
+    i8x_ensure(c);
     c.sync();
     c.has_data = true;
 }
@@ -1289,9 +1319,10 @@ int krr_set_option(krr_ctx* ctx, const char* key, double value) {
         } else if (k == "i8_debug") {
             c.i8_debug = int(value);
         } else if (k == "k1_path") {
-            if (value != 0.0 && value != 1.0 && value != -1.0)
-                fail(KRR_ERR_INVALID_ARGUMENT, "k1_path must be -1 (auto), 0 (dmma) or 1 (i8)");
+            if (value != 0.0 && value != 1.0 && value != 3.0 && value != -1.0)
+                fail(KRR_ERR_INVALID_ARGUMENT, "k1_path must be -1 (auto), 0 (dmma), 1 (i8) or 3 (i8x)");
             c.k1_path = int(value);
+            if (c.has_data && c.k1_path == 3 && c.i8x_E == 0) krr::i8x_ensure(c);
         } else if (k == "k1t_path") {
             if (value != 0.0 && value != 1.0 && value != -1.0)
                 fail(KRR_ERR_INVALID_ARGUMENT, "k1t_path must be -1 (auto), 0 (dmma) or 1 (i8)");
@@ -1338,7 +1369,7 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
             *value = c.precision;
         } else if (k == "k1_path_effective") {  // the K1 kernel a mat-vec runs now
             krr::require_data(c);
-            *value = krr::use_i8(c) ? 1.0 : (krr::use_i8T1(c) ? 2.0 : 0.0);
+            *value = krr::use_i8x(c) ? 3.0 : (krr::use_i8(c) ? 1.0 : (krr::use_i8T1(c) ? 2.0 : 0.0));
         } else if (k == "k1t_path") {
             *value = c.k1t_path;
         } else if (k == "k1t_path_effective") {  // the K1T kernel a 16-column batch runs now
@@ -1347,6 +1378,9 @@ int krr_get_option(krr_ctx* ctx, const char* key, double* value) {
         } else if (k == "i8_supported") {
             krr::require_data(c);
             *value = c.i8_ready ? 1.0 : 0.0;
+        } else if (k == "i8x_exponent") {  // K1-I8X's global exponent E of z (0: not available)
+            krr::require_data(c);
+            *value = c.i8x_E;
         } else if (k == "exp_mode") {
             *value = c.exp_mode;
         } else if (k == "batched_rhs") {

@@ -186,6 +186,10 @@ int krr_diag_i8_trace(long long* out, int count) {
     return guard([&] { krr::i8_read_trace(out, count); });
 }
 
+int krr_diag_i8x_trace(long long* out, int count) {
+    return guard([&] { krr::i8x_read_trace(out, count); });
+}
+
 int krr_diag_i8t_trace(long long* out, int count) {
     return guard([&] { krr::i8s_read_trace(out, count); });
 }
