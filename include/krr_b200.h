@@ -77,9 +77,10 @@ int krr_ctx_destroy(krr_ctx* ctx);
 int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
 
 /* Tuning / diagnostic knobs (no reference equivalent):
- *   "k1_path"     -1|0|1  fused mat-vec kernel: auto (default: INT8-slice tensor-core kernel
+ *   "k1_path"     -1|0|1|3  fused mat-vec kernel: auto (default: INT8-slice tensor-core kernel
  *                         where faster: 27 <= d <= 32, 44 <= d <= 96, when the data's exponent range allows, else FP64 DMMA) |
- *                         FP64 DMMA | tcgen05 INT8 slices
+ *                         FP64 DMMA | tcgen05 INT8 slices | K1-I8X (INT8 slices, exact integer exp argument;
+ *                         Gaussian, d <= 96, |x| sqrt(2 scale) < 256; otherwise the request runs the auto choice)
  *   "k1t_path"    -1|0|1  16-column batches of multi-RHS mat-mats / batched PCG: auto (default:
  *                         K1T-I8 — INT8-slice dot products on K-streamed operands + DMMA E.V —
  *                         for the Gaussian kernel with 28 <= d <= 448, else the DMMA K1T) |
@@ -157,8 +158,9 @@ int krr_adaptive_build(krr_ctx* ctx, double lambda, double lambda_p, int64_t s0,
                        uint64_t master_seed, krr_quality_report* history, int max_history, int* n_history,
                        int64_t* final_size, int* passed, int* jitter_used);
 /* Read a knob back: "k1_path", "k1t_path", "exp_mode", "batched_rhs", and (after krr_set_data)
- * "k1_path_effective" (0 DMMA / 1 I8 / 2 column 0 of a 16-column K1T-I8 pass, d >= 160: the
- * kernel a mat-vec runs now), "k1t_path_effective"
+ * "k1_path_effective" (0 DMMA / 1 I8 / 2 column 0 of a 16-column K1T-I8 pass, d >= 160 / 3 K1-I8X:
+ * the kernel a mat-vec runs now), "i8x_exponent" (K1-I8X's global exponent E, 0 when not prepared
+ * or out of range), "k1t_path_effective"
  * (the kernel a 16-column batch runs now; may prepare the K1T-I8 operands), "i8_supported",
  * "precision" (64 | 32), "build_gram_ms" / "build_cholesky_ms" / "build_trsm_ms" (CUDA-event
  * split of the last krr_precond_build: Z^T Z + lambda_p I, Cholesky with its retry, U = L^-1 Z^T)

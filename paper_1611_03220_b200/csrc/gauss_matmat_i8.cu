@@ -68,7 +68,8 @@ constexpr int TAB_REP = 16;
 constexpr int YMIN_K = -1022 * TAB;
 constexpr int KP_MAX = 448;
 #ifndef MI8_TMUX
-#define MI8_TMUX 0  // time-multiplex the tensor core with the FP64 phase (1) or overlap them (0)
+#define MI8_TMUX 0  // time-multiplex the tensor core with the FP64 phase (1), overlap them (0), or run the
+                    // DMMA contraction of tile t after tile t+1's MMAs, exp still overlapped (2)
 #endif
 
 constexpr size_t OFF_E = size_t(NSTG) * STG_BYTES;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
         for (int it = 0; it < nTI; ++it) {
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
                 // time-multiplexed with the previous tile's FP64 phase (exp + DMMA)
-                if (MI8_TMUX && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
+                if (MI8_TMUX == 1 && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
                 MI8_TRACE(lane == 0, bq, 8);
                 for (int ks = 0; ks < KS; ++ks) {
                     const int s = ks % NSTG;
@@ -260,6 +261,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
         const bool rows_role = ew < 8;              // warps 0-7: E . V_J; 8-15: E^T . V_I
         const int jb = ew - 8;                       // column role: 8-column block of the tile
         int tq = 0;
+        int ntiles_cta = 0;  // tiles of this CTA (the MMA warp's order)
+        for (int it2 = 0; it2 < nTI; ++it2) ntiles_cta += nTJ - (diag ? it2 * (TI / TJ) : 0);
         for (int it = 0; it < nTI; ++it) {
             const int64_t i0 = rowBase + int64_t(it) * TI;
             const int64_t gi = i0 + row;
@@ -386,6 +389,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                 MI8_TRACE(etid == 0, tq, 4);
 
                 // ---- FP64 tensor phase
+                if (MI8_TMUX == 2 && tq + 1 < ntiles_cta) tc::mbar_wait(g_full + 0, uint32_t((tq + 1) & 1));
                 if (rows_role) {
                     // O_I rows 16 ew .. 16 ew + 15 (+)= E . V_J
 #pragma unroll 4
