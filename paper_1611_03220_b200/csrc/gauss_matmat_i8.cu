@@ -67,6 +67,12 @@ constexpr int TAB = 64;
 constexpr int TAB_REP = 16;
 constexpr int YMIN_K = -1022 * TAB;
 constexpr int KP_MAX = 448;
+#ifndef MI8_SLICEBAR
+#define MI8_SLICEBAR 0  // 1: per-slice ring barriers: slice q of a stage is refilled as soon as group q (its last reader) completes
+#endif
+#ifndef MI8_BIGCOPY
+#define MI8_BIGCOPY 0  // 1: two copies of the slices laid out so one ring stage is 2 bulk copies (A 32 KB, B 16 KB)
+#endif
 #ifndef MI8_TMUX
 #define MI8_TMUX 0  // time-multiplex the tensor core with the FP64 phase (1), overlap them (0), or run the
                     // DMMA contraction of tile t after tile t+1's MMAs, exp still overlapped (2)
@@ -78,7 +84,7 @@ constexpr size_t OFF_VJ = OFF_VI + size_t(TI) * TR * 8;
 constexpr size_t OFF_CD = OFF_VJ + size_t(TJ) * TR * 8;
 constexpr size_t OFF_TAB = OFF_CD + size_t(NCD) * CD_BYTES;
 constexpr size_t OFF_BARS = OFF_TAB + size_t(TAB) * TAB_REP * 8;
-constexpr int NBARS = 2 * NSTG + 2 * NCD + 2 * NGRP + 1;
+constexpr int NBARS = 2 * NSTG * P + 2 * NCD + 2 * NGRP + 1;
 constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
 static_assert(SMEM <= 227 * 1024, "K1T-I8 shared memory");
 
@@ -103,7 +109,7 @@ struct MI8Args {
     int64_t n_pad;
     int st;
     int ks;  // kp / 32
-    int debug;
+    int debug;  // profiling (results invalid unless 0 / 4): 1 no MMAs, 2 no exp arithmetic, 4 trace, 8 no DMMA
     double kabs;
     double a1, a2, a3, a4, a5;
 };
@@ -132,9 +138,9 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
     uint8_t* sCD = smem + OFF_CD;
     double* tab = reinterpret_cast<double*>(smem + OFF_TAB);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BARS);
-    uint64_t* s_full = bars;
-    uint64_t* s_empty = s_full + NSTG;
-    uint64_t* cd_full = s_empty + NSTG;
+    uint64_t* s_full = bars;              // [NSTG][P] (MI8_SLICEBAR) or [NSTG]
+    uint64_t* s_empty = s_full + NSTG * P;
+    uint64_t* cd_full = s_empty + NSTG * P;
     uint64_t* cd_empty = cd_full + NCD;
     uint64_t* g_full = cd_empty + NCD;
     uint64_t* g_empty = g_full + NGRP;
@@ -152,7 +158,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
     const int64_t g8 = A.n_pad / 8;  // 8-row groups per K chunk
 
     if (tid == 0) {
-        for (int s = 0; s < NSTG; ++s) {
+        for (int s = 0; s < NSTG * P; ++s) {
             tc::mbar_init(s_full + s, 1);
             tc::mbar_init(s_empty + s, 1);
         }
@@ -192,15 +198,37 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     for (int ks = 0; ks < KS; ++ks) {
                         const int s = ks % NSTG;
                         if (ks == 0) MI8_TRACE(true, bq, 12);
+                        uint8_t* st = sStg + s * STG_BYTES;
+                        if (MI8_SLICEBAR && !MI8_BIGCOPY) {
+                            // slice q (A and B) as soon as the previous chunk in this stage released it
+                            for (int q = P - 1; q >= 0; --q) {
+                                uint64_t* full = s_full + s * P + q;
+                                if (uses[s] > 0) tc::mbar_wait_sleep(s_empty + s * P + q, uint32_t((uses[s] - 1) & 1));
+                                tc::mbar_arrive_expect_tx(full, uint32_t((TI + TJ) * 32));
+                                const uint8_t* base = A.S + (int64_t(q) * KS + ks) * g8 * 256;
+                                tc::bulk_g2s(st + q * (TI * 32), base + (r0 >> 3) * 256, uint32_t(TI * 32), full);
+                                tc::bulk_g2s(st + A_CH + q * (TJ * 32), base + (c0 >> 3) * 256, uint32_t(TJ * 32), full);
+                            }
+                            ++uses[s];
+                            continue;
+                        }
                         if (uses[s] > 0) tc::mbar_wait_sleep(s_empty + s, uint32_t((uses[s] - 1) & 1));
                         ++uses[s];
                         tc::mbar_arrive_expect_tx(s_full + s, uint32_t(STG_BYTES));
-                        uint8_t* st = sStg + s * STG_BYTES;
-                        for (int p = 0; p < P; ++p) {
-                            const uint8_t* base = A.S + (int64_t(p) * KS + ks) * g8 * 256;
-                            tc::bulk_g2s(st + p * (TI * 32), base + (r0 >> 3) * 256, uint32_t(TI * 32), s_full + s);
-                            tc::bulk_g2s(st + A_CH + p * (TJ * 32), base + (c0 >> 3) * 256, uint32_t(TJ * 32),
-                                         s_full + s);
+                        if (MI8_BIGCOPY) {
+                            // [ks][n_pad/128][p][128 x 32 B] and [ks][n_pad/64][p][64 x 32 B] copies
+                            const uint8_t* sa = A.S + (int64_t(ks) * (A.n_pad / TI) + (r0 / TI)) * A_CH;
+                            const uint8_t* sb = A.S + int64_t(KS) * A.n_pad * P * 32 +
+                                                (int64_t(ks) * (A.n_pad / TJ) + (c0 / TJ)) * B_CH;
+                            tc::bulk_g2s(st, sa, uint32_t(A_CH), s_full + s);
+                            tc::bulk_g2s(st + A_CH, sb, uint32_t(B_CH), s_full + s);
+                        } else {
+                            for (int p = 0; p < P; ++p) {
+                                const uint8_t* base = A.S + (int64_t(p) * KS + ks) * g8 * 256;
+                                tc::bulk_g2s(st + p * (TI * 32), base + (r0 >> 3) * 256, uint32_t(TI * 32), s_full + s);
+                                tc::bulk_g2s(st + A_CH + p * (TJ * 32), base + (c0 >> 3) * 256, uint32_t(TJ * 32),
+                                             s_full + s);
+                            }
                         }
                     }
                 }
@@ -218,7 +246,9 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                 MI8_TRACE(lane == 0, bq, 8);
                 for (int ks = 0; ks < KS; ++ks) {
                     const int s = ks % NSTG;
-                    tc::mbar_wait_sleep(s_full + s, uint32_t(uses[s] & 1));
+                    constexpr bool SB = MI8_SLICEBAR && !MI8_BIGCOPY;
+                    const uint32_t ph = uint32_t(uses[s] & 1);
+                    if (!SB) tc::mbar_wait_sleep(s_full + s, ph);
                     ++uses[s];
                     if (ks == 0 || ks == KS / 2 || ks == KS - 1) MI8_TRACE(lane == 0, bq, ks == 0 ? 9 : (ks == KS - 1 ? 11 : 10));
                     tc::fence_after();
@@ -232,18 +262,43 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                             tc::mbar_wait_sleep(g_empty + c, uint32_t((bq - 1) & 1));
                             tc::fence_after();
                         }
+                        if (SB && c == NGRP - 1) {
+                            // the first group reads every slice of the chunk: wait for each pair (p, 7 - p)
+#pragma unroll
+                            for (int p = 0; p <= c; ++p) {
+                                if (p < 4) {
+                                    tc::mbar_wait_sleep(s_full + s * P + p, ph);
+                                    tc::mbar_wait_sleep(s_full + s * P + (c - p), ph);
+                                    tc::fence_after();
+                                }
+                                if (tc::elect_one() && !(A.debug & 1))
+                                    tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4),
+                                               dB0 + uint64_t(((c - p) * TJ * 32) >> 4), idesc,
+                                               (ks == 0 && p == 0) ? 0u : 1u);
+                                __syncwarp();
+                            }
+                            if (tc::elect_one()) {
+                                if (last) tc::mma_commit(g_full + c);
+                                tc::mma_commit(s_empty + s * P + c);  // group c: last reader of slice c
+                            }
+                            __syncwarp();
+                            continue;
+                        }
                         if (tc::elect_one()) {
 #pragma unroll
                             for (int p = 0; p <= c; ++p)
-                                tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4),
+                                if (!(A.debug & 1)) tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4),
                                            dB0 + uint64_t(((c - p) * TJ * 32) >> 4), idesc,
                                            (ks == 0 && p == 0) ? 0u : 1u);
                             if (last) tc::mma_commit(g_full + c);
+                            if (SB) tc::mma_commit(s_empty + s * P + c);  // group c: last reader of slice c
                         }
                         __syncwarp();
                     }
-                    if (tc::elect_one()) tc::mma_commit(s_empty + s);
-                    __syncwarp();
+                    if (!SB) {
+                        if (tc::elect_one()) tc::mma_commit(s_empty + s);
+                        __syncwarp();
+                    }
                 }
             }
         }
@@ -339,6 +394,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                 const int colOff = half * CPT;
                 const bool masked = diag && jt < (it + 1) * (TI / TJ);
                 const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
+                if (A.debug & 2) {  // profiling: no exp arithmetic (results invalid)
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) sE[e_idx(row, colOff + k)] = T[k];
+                } else
 #pragma unroll
                 for (int k0 = 0; k0 < CPT; k0 += 2) {
                     double y[2], t2[2], f[2], q[2];
@@ -393,7 +452,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                 if (rows_role) {
                     // O_I rows 16 ew .. 16 ew + 15 (+)= E . V_J
 #pragma unroll 4
-                    for (int kk = 0; kk < TJ / 4; ++kk) {
+                    for (int kk = 0; kk < ((A.debug & 8) ? 0 : TJ / 4); ++kk) {
                         const int k0 = kk * 4;
                         double af[2], bf[2];
 #pragma unroll
@@ -413,7 +472,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     // O_J (columns jb*8 .. +7) = E^T . V_I over the tile's 128 rows
                     double cacc[2][2] = {};
 #pragma unroll 4
-                    for (int kk = 0; kk < TI / 4; ++kk) {
+                    for (int kk = 0; kk < ((A.debug & 8) ? 0 : TI / 4); ++kk) {
                         const int r0 = kk * 4;
                         const double a = sE[e_idx(r0 + t4, jb * 8 + g)];
                         double bf[2];
@@ -523,10 +582,21 @@ __global__ void slice_s_kernel(const double* __restrict__ X, int64_t n, int64_t 
         double w = scalbn(x, 7 - ex[row]);  // u * 2^7, |u| < 1 (as K1-I8)
         const int64_t off =
             (int64_t(k >> 5) * (n_pad >> 3) + (row >> 3)) * 256 + ((k >> 4) & 1) * 128 + (row & 7) * 16 + (k & 15);
+        // MI8_BIGCOPY: A copy [ks][n_pad/128][p][16][2][8][16], B copy [ks][n_pad/64][p][8][2][8][16]
+        const int64_t in_a = (int64_t(k >> 5) * (n_pad / TI) + row / TI) * (P * TI * 32) + ((row % TI) >> 3) * 256 +
+                             ((k >> 4) & 1) * 128 + (row & 7) * 16 + (k & 15);
+        const int64_t in_b = int64_t(ks_n) * n_pad * P * 32 +
+                             (int64_t(k >> 5) * (n_pad / TJ) + row / TJ) * (P * TJ * 32) + ((row % TJ) >> 3) * 256 +
+                             ((k >> 4) & 1) * 128 + (row & 7) * 16 + (k & 15);
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const double a = trunc(w);
-            S[int64_t(p) * ks_n * n_pad * 32 + off] = uint8_t(int8_t(int(a)));
+            if (MI8_BIGCOPY) {
+                S[in_a + p * (TI * 32)] = uint8_t(int8_t(int(a)));
+                S[in_b + p * (TJ * 32)] = uint8_t(int8_t(int(a)));
+            } else {
+                S[int64_t(p) * ks_n * n_pad * 32 + off] = uint8_t(int8_t(int(a)));
+            }
             w = (w - a) * 128.0;
         }
     }
@@ -546,6 +616,8 @@ void i8s_read_trace(long long* out, int count) {
 }
 
 int i8s_kp(int64_t d) { return int((d + 31) / 32 * 32); }
+
+size_t i8s_slice_bytes(int64_t n_pad, int64_t d) { return size_t(MI8_BIGCOPY ? 16 : 8) * size_t(n_pad) * size_t(i8s_kp(d)); }
 
 bool i8s_supported(int64_t d, int st) { return i8s_kp(d) <= KP_MAX && st % TI == 0 && st >= TI; }
 

@@ -43,6 +43,7 @@ void matmat_finish_launch(const GaussMatvecPlan& p, const double* part, const do
 // K1T-I8: T = 16 right-hand sides, tcgen05 kind::i8 dot products with K-streamed slices and
 // DMMA E.V contractions (gauss_matmat_i8.cu).  Gaussian kernel, d <= 448.
 int i8s_kp(int64_t d);
+size_t i8s_slice_bytes(int64_t n_pad, int64_t d);  // bytes of the K-chunk-major slice buffer
 bool i8s_supported(int64_t d, int st);
 bool i8s_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, const double* L, int dp, double kscale,
                         uint8_t* S, int* ex, int* ejs, double* sqs, cudaStream_t stream);

@@ -347,7 +347,7 @@ bool use_i8T(Ctx& c, int T) {
     if (c.i8s_state == 0) {
         const int64_t n_pad = c.plan.n_pad;
         c.kp8s = i8s_kp(c.d);
-        c.S8s.ensure(size_t(8) * size_t(n_pad) * size_t(c.kp8s));
+        c.S8s.ensure(i8s_slice_bytes(n_pad, c.d));
         c.ex8s.ensure(size_t(n_pad));
         c.ejs8s.ensure(size_t(n_pad));
         c.sq8s.ensure(size_t(n_pad));
