@@ -67,6 +67,9 @@ constexpr int TAB = 64;
 constexpr int TAB_REP = 16;
 constexpr int YMIN_K = -1022 * TAB;
 constexpr int KP_MAX = 448;
+#ifndef MI8_PROFILE
+#define MI8_PROFILE 0  // 1: compile the profiling modes (debug bits 1 / 2 / 8; A/B builds only: they cost ~6 % in the hot loops)
+#endif
 #ifndef MI8_SLICEBAR
 #define MI8_SLICEBAR 0  // 1: per-slice ring barriers: slice q of a stage is refilled as soon as group q (its last reader) completes
 #endif
@@ -109,7 +112,7 @@ struct MI8Args {
     int64_t n_pad;
     int st;
     int ks;  // kp / 32
-    int debug;  // profiling (results invalid unless 0 / 4): 1 no MMAs, 2 no exp arithmetic, 4 trace, 8 no DMMA
+    int debug;  // bit 2: trace; with MI8_PROFILE (results invalid): 1 no MMAs, 2 no exp arithmetic, 8 no DMMA
     double kabs;
     double a1, a2, a3, a4, a5;
 };
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                                     tc::mbar_wait_sleep(s_full + s * P + (c - p), ph);
                                     tc::fence_after();
                                 }
-                                if (tc::elect_one() && !(A.debug & 1))
+                                if (tc::elect_one() && !(MI8_PROFILE && (A.debug & 1)))
                                     tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4),
                                                dB0 + uint64_t(((c - p) * TJ * 32) >> 4), idesc,
                                                (ks == 0 && p == 0) ? 0u : 1u);
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                         if (tc::elect_one()) {
 #pragma unroll
                             for (int p = 0; p <= c; ++p)
-                                if (!(A.debug & 1)) tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4),
+                                if (!(MI8_PROFILE && (A.debug & 1))) tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4),
                                            dB0 + uint64_t(((c - p) * TJ * 32) >> 4), idesc,
                                            (ks == 0 && p == 0) ? 0u : 1u);
                             if (last) tc::mma_commit(g_full + c);
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                 const int colOff = half * CPT;
                 const bool masked = diag && jt < (it + 1) * (TI / TJ);
                 const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
-                if (A.debug & 2) {  // profiling: no exp arithmetic (results invalid)
+                if (MI8_PROFILE && (A.debug & 2)) {  // profiling: no exp arithmetic (results invalid)
 #pragma unroll
                     for (int k = 0; k < CPT; ++k) sE[e_idx(row, colOff + k)] = T[k];
                 } else
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                 if (rows_role) {
                     // O_I rows 16 ew .. 16 ew + 15 (+)= E . V_J
 #pragma unroll 4
-                    for (int kk = 0; kk < ((A.debug & 8) ? 0 : TJ / 4); ++kk) {
+                    for (int kk = 0; kk < ((MI8_PROFILE && (A.debug & 8)) ? 0 : TJ / 4); ++kk) {
                         const int k0 = kk * 4;
                         double af[2], bf[2];
 #pragma unroll
@@ -472,7 +475,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     // O_J (columns jb*8 .. +7) = E^T . V_I over the tile's 128 rows
                     double cacc[2][2] = {};
 #pragma unroll 4
-                    for (int kk = 0; kk < ((A.debug & 8) ? 0 : TI / 4); ++kk) {
+                    for (int kk = 0; kk < ((MI8_PROFILE && (A.debug & 8)) ? 0 : TI / 4); ++kk) {
                         const int r0 = kk * 4;
                         const double a = sE[e_idx(r0 + t4, jb * 8 + g)];
                         double bf[2];
