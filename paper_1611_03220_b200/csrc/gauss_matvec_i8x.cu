@@ -576,15 +576,13 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8x_kernel(const XArgs A
 }
 
 // ---- operand preparation
-__device__ unsigned long long g_absmax;
-
-__global__ void absmax_kernel(const double* __restrict__ X, int64_t total) {
+__global__ void absmax_kernel(const double* __restrict__ X, int64_t total, unsigned long long* __restrict__ out) {
     double m = 0.0;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x)
         m = fmax(m, fabs(X[i]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(&g_absmax, static_cast<unsigned long long>(__double_as_longlong(m)));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
 // the 8 digits of u = fl(c x) 2^-E, rounded to nearest (exact in fp64): |a_0| <= 127, |a_p| <= 64
@@ -700,15 +698,19 @@ bool i8x_supported(int64_t d, int st) { return i8_kp(d) <= KP_MAX && st % TI == 
 int i8x_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, double scale, uint8_t* S, long long* sq,
                        cudaStream_t stream) {
     ensure_xtable(stream);  // (synchronises once) so graph-captured launches never need to
-    const unsigned long long zero = 0;
-    KRR_CUDA(cudaMemcpyToSymbolAsync(g_absmax, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, stream));
+    // max |x| (the bits of non-negative doubles order like the values) in a per-call scratch word,
+    // so contexts preparing concurrently on one device do not share it
+    unsigned long long* dmax = nullptr;
+    KRR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dmax), sizeof(unsigned long long), stream));
+    KRR_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), stream));
     const int64_t total = n * d;
     if (total > 0) {
-        absmax_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 8)), 256, 0, stream>>>(X, total);
+        absmax_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 8)), 256, 0, stream>>>(X, total, dmax);
         KRR_LAUNCH_CHECK();
     }
     unsigned long long bits = 0;
-    KRR_CUDA(cudaMemcpyFromSymbolAsync(&bits, g_absmax, sizeof(bits), 0, cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaMemcpyAsync(&bits, dmax, sizeof(bits), cudaMemcpyDeviceToHost, stream));
+    KRR_CUDA(cudaFreeAsync(dmax, stream));
     KRR_CUDA(cudaStreamSynchronize(stream));
     double xmax = 0.0;
     std::memcpy(&xmax, &bits, sizeof(xmax));
@@ -717,7 +719,8 @@ int i8x_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, dou
     const double zmax = std::fma(xmax, c, xmax * c_lo);  // = max_ik |z_ik|: the rounding is monotonic
     if (!std::isfinite(zmax)) return 0;
     int E = std::max(1, zmax > 0.0 ? std::ilogb(zmax) + 1 : 1);
-    while (zmax >= std::ldexp(127.5 / 128.0, E)) ++E;  // the rounded leading digit stays <= 127
+    // the rounded leading digit stays <= 127 (with a margin for the per-element fma rounding)
+    while (zmax * (1.0 + 0x1p-40) >= std::ldexp(127.5 / 128.0, E)) ++E;
     if (E > 8) return 0;  // |z| >= 128: out of K1-I8X's fixed-point range (K1-I8 / DMMA serve it)
     const int kp = i8_kp(d);
     const int64_t st = n_pad * kp;
