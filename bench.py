@@ -16,7 +16,8 @@ e2e     = same metric through the reference-facing C-ABI call krr_kernel_matvec 
           pinned HOST buffers (H2D of v and D2H of the result inside the timed region).
 roofline: dominant kernel = K1.  The default path at d = 90 is K1-I8 (tcgen05 kind::i8
           Ozaki slices): achieved = algorithmic INT8 tensor ops per launch (unique pairs x
-          36 slice products x kp x 2) / mean K1 launch time (CUDA events on the launching
+          28 slice products x kp x 2: 7 balanced 8-bit digits, products p + q <= 6) / mean K1
+          launch time (CUDA events on the launching
           stream); peak = 2 x the measured dense bf16 rate in MEASURED_PEAKS.json (B200 INT8
           = 2x bf16).  The same launch is also expressed as FP64-equivalent dot-product
           TFLOP/s (pairs x 2d) against the live-measured FP64 DMMA peak (libkrr_diag.so),
@@ -102,6 +103,10 @@ def maybe_spawn(args) -> None:
     sys.stdout.flush()
     os.execv(sys.executable, cmd)
 
+
+# INT8 slice products per pair of K1-I8 / K1T-I8 (tc_i8.cuh:balanced_digits8: 7 balanced 8-bit
+# digits, products p + q <= 6; round 1 used 8 truncated 7-bit digits and 36 products)
+I8_PRODUCTS = 28
 
 # ----------------------------------------------------------------------------- plumbing
 def dist_env():
@@ -416,7 +421,7 @@ def main():
                  "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU (krr_diag_microbench)"}
     if path == 1:
         kp = (d + 31) // 32 * 32
-        i8_ops = pairs_rank * 36.0 * kp * 2.0
+        i8_ops = pairs_rank * I8_PRODUCTS * kp * 2.0
         i8_achieved = i8_ops / (k1_ms * 1e-3) / 1e12
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
         peak_i8 = 2.0 * float(peaks.get("bf16_tflops", 2250.0))
@@ -496,9 +501,9 @@ def main():
 def i8_model_bound(d: int, kp: int, pairs: float, k1_ms: float, sm_mhz: float) -> dict:
     """K1-I8's bound from its two measured per-SM floors, additive because the tensor core is
     time-multiplexed with the FP64 exp phase (INT8 MMAs throttle the FP64 pipe, profiles/README.md):
-    per 128 x 64 tile, 36 * kp / 32 tcgen05.mma kind::i8 at the 44.8-clk per-instruction floor for
+    per 128 x 64 tile, 28 * kp / 32 tcgen05.mma kind::i8 at the 44.8-clk per-instruction floor for
     N = 64 (tools/mma_rate.py) + 8192 pairs x 14 FP64 ops at 64 lane-ops / clk / SM."""
-    mma_clk = 36 * (kp // 32) * 44.8
+    mma_clk = I8_PRODUCTS * (kp // 32) * 44.8
     fp64_clk = 8192 * 14 / 64.0
     tile_clk = mma_clk + fp64_clk
     tiles_per_s = 148 * sm_mhz * 1e6 / tile_clk
@@ -565,7 +570,7 @@ def pcg_leg(krr, ctx, D, iters: int, k1_ms_per_launch: float) -> dict:
     kp = (d + 31) // 32 * 32
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak_i8 = 2.0 * float(peaks.get("bf16_tflops", 2250.0)) * 1e12
-    k1_ideal = (n * (n - 1) / 2) * 36.0 * kp * 2.0 / peak_i8 / D.world
+    k1_ideal = (n * (n - 1) / 2) * I8_PRODUCTS * kp * 2.0 / peak_i8 / D.world
     hbm = hbm_peak() * 1e9
     pre_ideal = 16.0 * n * s / D.world / hbm
     vec_ideal = 12.0 * 8 * n / hbm

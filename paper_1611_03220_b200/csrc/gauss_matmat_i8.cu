@@ -1,16 +1,16 @@
 // K1T-I8 — fused symmetric Gaussian mat-mat  OUT = (K + lambda I) V  for T = 16 interleaved
 // right-hand sides (BASELINE config 5: n = 524288, d = 440, t = 16 one-vs-all RLSC targets),
 // K never stored.  The dot products run on the 5th-generation tensor cores exactly as in
-// K1-I8 (gauss_matvec_i8.cu: tcgen05.mma kind::i8 on 8 Ozaki slices of 7 bits, 36 products in
-// 8 TMEM groups, the same integer drain and table exp), so every K_ij is K1-I8's bit pattern;
+// K1-I8 (gauss_matvec_i8.cu: tcgen05.mma kind::i8 on 7 Ozaki slices of balanced 8-bit digits, 28
+// products in 7 TMEM groups, the same integer drain and table exp), so every K_ij is K1-I8's bit pattern;
 // the E . V contractions run on the FP64 tensor path (DMMA m8n8k4):
 //     rows:     O_I (128 x 16) += E (128 x 64)   . V_J (64 x 16)    (accumulated over a pass)
 //     columns:  O_J (64 x 16)   = E^T (64 x 128) . V_I (128 x 16)   (one J tile)
 //
 // Differences from K1-I8, both forced by d = 440:
-//  * K-streamed operands.  The I tile's slices (8 x 128 x 448 B = 448 KB) cannot stay
+//  * K-streamed operands.  The I tile's slices (7 x 128 x 448 B = 392 KB) cannot stay
 //    resident, so both operands stream through a 2-stage ring of 32-byte K chunks
-//    (8 slices x (128 + 64) rows x 32 B = 48 KB per stage), one bulk copy (TMA engine) per
+//    (7 slices x (128 + 64) rows x 32 B = 42 KB per stage), one bulk copy (TMA engine) per
 //    slice and operand.  The MMAs are then shared-memory-bandwidth bound: (128 + 64) x 32 B
 //    of SS operand reads per MMA plus the TMA fills, ~57 clk per MMA (a 3rd stage and an
 //    L2 prefetch one tile ahead were measured slower, profiles/README.md).  The slices use a K-chunk-major global layout
@@ -47,8 +47,8 @@ namespace krr {
 
 namespace {
 
-constexpr int P = 8;       // slices
-constexpr int NGRP = 8;    // groups c = p + q in [0, 7]
+constexpr int P = 7;       // slices (balanced 8-bit digits, tc_i8.cuh:balanced_digits8)
+constexpr int NGRP = 7;    // groups c = p + q in [0, 6]
 constexpr int TI = 128;    // I tile rows (MMA M, TMEM lanes)
 constexpr int TJ = 64;     // J tile columns (MMA N)
 constexpr int TR = 16;     // right-hand sides
@@ -57,9 +57,9 @@ constexpr int CPT = 16;    // columns per epilogue thread
 constexpr int NTHR = 32 * (2 + NEPI);
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int NSTG = 2;                 // K-chunk ring stages
-constexpr int A_CH = P * TI * 32;       // 32 KB
-constexpr int B_CH = P * TJ * 32;       // 16 KB
-constexpr int STG_BYTES = A_CH + B_CH;  // 48 KB
+constexpr int A_CH = P * TI * 32;       // 28 KB
+constexpr int B_CH = P * TJ * 32;       // 14 KB
+constexpr int STG_BYTES = A_CH + B_CH;  // 42 KB
 constexpr int ELD = 68;                 // E tile row stride (doubles), = 4 (mod 16)
 constexpr int NCD = 2;                  // column-data stages (sq', e_j << 20)
 constexpr int CD_BYTES = TJ * 8 + TJ * 4;
@@ -74,7 +74,7 @@ constexpr int KP_MAX = 448;
 #define MI8_SLICEBAR 0  // 1: per-slice ring barriers: slice q of a stage is refilled as soon as group q (its last reader) completes
 #endif
 #ifndef MI8_BIGCOPY
-#define MI8_BIGCOPY 0  // 1: two copies of the slices laid out so one ring stage is 2 bulk copies (A 32 KB, B 16 KB)
+#define MI8_BIGCOPY 0  // 1: two copies of the slices laid out so one ring stage is 2 bulk copies (A 28 KB, B 14 KB)
 #endif
 #ifndef MI8_TMUX
 #define MI8_TMUX 0  // time-multiplex the tensor core with the FP64 phase (1), overlap them (0), or run the
@@ -119,14 +119,17 @@ struct MI8Args {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NEPI * 32) : "memory"); }
 
-// the bits of the double 1.5 * 2^52 + 2^31 + (2^14 a + b)  (K1-I8's drain, exact)
-constexpr double M2 = 6755401588539392.0 + 25165832.0;
-// The same with 64-bit inputs: M1 + 16384 a + b for |16384 a + b| < 2^51.  K1T-I8's chunks reach
-// kp = 448 bytes, where a group sum can reach 8 x 127^2 x 448 = 5.8e7 and b_k = 128 G_2k + G_2k+1
-// no longer fits in int32 (K1-I8, kp <= 96, stays below 1.6e9); the combination is int64 here.
-__device__ __forceinline__ double magic_pack64(int64_t a, int64_t b) {
-    return __longlong_as_double(0x4338000080000000LL + a * 16384 + b);
+// a * b + c with a 32 x 32 -> 64-bit signed product (mad.wide.s32)
+__device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
+    int64_t d;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
 }
+// K1-I8's drain (gauss_matvec_i8.cu), with int64 partials throughout: at kp = 448 a group sum
+// reaches 7 x 128^2 x 448 = 5.1e7, so 2^8 G_1 + G_2 no longer fits in int32 here.  MAGIC + V is
+// the double 1.5 * 2^52 + V (|V| < 2^51); M2 = 1.5 * 2^52 (1 + 2^-24).
+constexpr int64_t MAGIC = 0x4338000000000000LL;
+constexpr double M2 = 6755399441055744.0 + 402653184.0;
 
 // swizzled shared-memory indices
 __device__ __forceinline__ int e_idx(int r, int c) { return r * ELD + (c ^ ((r >> 2) & 3)); }
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
             const int64_t i0 = rowBase + int64_t(it) * TI;
             const int64_t gi = i0 + row;
             const double sqs_i = A.sqs[gi];
-            const int nsi_hi = kabs_hi + (A.ex[gi] - 34) * (1 << 20);
+            const int nsi_hi = kabs_hi + (A.ex[gi] - 39) * (1 << 20);  // -2 x.x = -2^(e_i+e_j-39) T
             // V_I of the pass (swizzled; the previous pass's readers are past the tile barrier)
             for (int k = etid; k < TI * TR / 2; k += NEPI * 32) {
                 const int r = (2 * k) / TR, t = (2 * k) % TR;
@@ -351,40 +354,43 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                 }
 
                 MI8_TRACE(etid == 0, tq, 0);
-                // ---- drain the 8 groups two at a time (K1-I8's integer combination)
-                // two 8-column halves, each through all four stages: the int64 partials of one
-                // half only stay live (register pressure); the groups are released after the second
-                int64_t bint[CPT / 2];
+                // ---- drain the 7 groups as (6, 5), (4, 3), (2, 1), (0) (K1-I8's integer combination:
+                // T = H + 2^-24 L, H = 2^24 G_0 + 2^16 G_1 + 2^8 G_2, L = 2^24 G_3 + 2^16 G_4 + 2^8 G_5 + G_6)
+                // in two 8-column halves, each through all four stages: the int64 partials of one half
+                // only stay live (register pressure); the groups are released after the second
+                int64_t acc[CPT / 2];
                 double lo[CPT / 2], T[CPT];
-                auto stage = [&](int ca, int h, auto&& fn) {
+                auto stage = [&](int ca, int cb, int h, auto&& fn) {  // groups ca (completes first), cb = ca - 1 or none
                     if (h == 0) {
-                        tc::mbar_wait_sleep(g_full + ca + 1, ph);
                         tc::mbar_wait_sleep(g_full + ca, ph);
+                        if (cb >= 0) tc::mbar_wait_sleep(g_full + cb, ph);
                         tc::fence_after();
                     }
-                    uint32_t gl[CPT / 2], gh[CPT / 2];
-                    tc::tmem_ld8(taddr + uint32_t((ca + 1) * TJ + h * (CPT / 2)), gl);
-                    tc::tmem_ld8(taddr + uint32_t(ca * TJ + h * (CPT / 2)), gh);
+                    uint32_t ga[CPT / 2], gb[CPT / 2];
+                    tc::tmem_ld8(taddr + uint32_t(ca * TJ + h * (CPT / 2)), ga);
+                    if (cb >= 0) tc::tmem_ld8(taddr + uint32_t(cb * TJ + h * (CPT / 2)), gb);
                     tc::tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < CPT / 2; ++k) fn(k, int64_t(int32_t(gh[k])) * 128 + int32_t(gl[k]));
+                    for (int k = 0; k < CPT / 2; ++k) fn(k, int32_t(ga[k]), int32_t(gb[k]));
                     if (h == 1) {
                         tc::fence_before();
                         __syncwarp();
                         if (lane == 0) {
-                            tc::mbar_arrive(g_empty + ca + 1);
                             tc::mbar_arrive(g_empty + ca);
+                            if (cb >= 0) tc::mbar_arrive(g_empty + cb);
                         }
                     }
                 };
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    stage(6, h, [&](int k, int64_t b) { bint[k] = b; });
+                    stage(6, 5, h, [&](int k, int32_t g6, int32_t g5) { acc[k] = mad_wide(g5, 256, int64_t(g6)); });
                     if (h == 0) MI8_TRACE(etid == 0, tq, 1);
-                    stage(4, h, [&](int k, int64_t b) { lo[k] = magic_pack64(b, bint[k]); });
-                    stage(2, h, [&](int k, int64_t b) { bint[k] = b; });
-                    stage(0, h, [&](int k, int64_t b) {
-                        T[h * (CPT / 2) + k] = fma(lo[k], 0x1p-28, magic_pack64(b, bint[k]) - M2);
+                    stage(4, 3, h, [&](int k, int32_t g4, int32_t g3) {
+                        lo[k] = __longlong_as_double(mad_wide(g3, 1 << 24, mad_wide(g4, 65536, acc[k] + MAGIC)));
+                    });
+                    stage(2, 1, h, [&](int k, int32_t g2, int32_t g1) { acc[k] = mad_wide(g1, 256, int64_t(g2)); });
+                    stage(0, -1, h, [&](int k, int32_t g0, int32_t) {
+                        T[h * (CPT / 2) + k] = fma(lo[k], 0x1p-24, __longlong_as_double(mad_wide(g0, 1 << 24, acc[k] * 256 + MAGIC)) - M2);
                     });
                 }
 
@@ -566,7 +572,9 @@ __global__ void row_exponent_s_kernel(const double* __restrict__ X, int64_t n, i
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0) {
-            const int e = m > 0.0 ? ilogb(m) + 1 : 0;
+            // |x_ik| 2^-e <= 0.498: the range of 7 balanced 8-bit digits (as K1-I8)
+            int e = m > 0.0 ? ilogb(m) + 2 : 0;
+            if (m > 0.0 && scalbn(m, -e) > 0.498) ++e;
             ex[i] = e;
             ejs[i] = e * (1 << 20);
         }
@@ -582,7 +590,8 @@ __global__ void slice_s_kernel(const double* __restrict__ X, int64_t n, int64_t 
         const int64_t row = idx / kp;
         const int k = int(idx % kp);
         const double x = (row < n && k < d) ? X[row * d + k] : 0.0;
-        double w = scalbn(x, 7 - ex[row]);  // u * 2^7, |u| < 1 (as K1-I8)
+        int a[P];
+        tc::balanced_digits8(x, ex[row], a);  // as K1-I8
         const int64_t off =
             (int64_t(k >> 5) * (n_pad >> 3) + (row >> 3)) * 256 + ((k >> 4) & 1) * 128 + (row & 7) * 16 + (k & 15);
         // MI8_BIGCOPY: A copy [ks][n_pad/128][p][16][2][8][16], B copy [ks][n_pad/64][p][8][2][8][16]
@@ -593,14 +602,12 @@ __global__ void slice_s_kernel(const double* __restrict__ X, int64_t n, int64_t 
                              ((k >> 4) & 1) * 128 + (row & 7) * 16 + (k & 15);
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const double a = trunc(w);
             if (MI8_BIGCOPY) {
-                S[in_a + p * (TI * 32)] = uint8_t(int8_t(int(a)));
-                S[in_b + p * (TJ * 32)] = uint8_t(int8_t(int(a)));
+                S[in_a + p * (TI * 32)] = uint8_t(int8_t(a[p]));
+                S[in_b + p * (TJ * 32)] = uint8_t(int8_t(a[p]));
             } else {
-                S[int64_t(p) * ks_n * n_pad * 32 + off] = uint8_t(int8_t(int(a)));
+                S[int64_t(p) * ks_n * n_pad * 32 + off] = uint8_t(int8_t(a[p]));
             }
-            w = (w - a) * 128.0;
         }
     }
 }
@@ -648,7 +655,7 @@ bool i8s_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, co
     }
     const int ek = std::ilogb(-kscale);
     const double ymax = -kscale * 4.0 * double(d) * std::ldexp(1.0, 2 * hi);
-    return ek + 2 * lo - 34 > -1000 && ek + 2 * hi - 34 < 1000 && ymax < std::ldexp(1.0, 50);
+    return ek + 2 * lo - 39 > -1000 && ek + 2 * hi - 39 < 1000 && ymax < std::ldexp(1.0, 50);
 }
 
 void gauss_matmat_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const int* ejs,

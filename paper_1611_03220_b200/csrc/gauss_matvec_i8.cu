@@ -10,18 +10,19 @@
 // and 15 FP64 operations per pair in the epilogue (vs 92 + 12 per pair for the DMMA K1
 // at d = 90).
 //
-// Decomposition (per row i, e_i = ilogb(max_k |x_ik|) + 1, u_i = x_i 2^-e_i in (-1, 1)):
-//     u_i = sum_{p<8} A_i^(p) 2^(-7(p+1)) + r_i,   A^(p) in [-127, 127],  |r_i| < 2^-56
-// (truncation, all steps exact in fp64).  Then
-//     x_i . x_j = 2^(e_i + e_j - 14) sum_c 2^(-7c) G_c,   G_c = sum_{p+q=c} A_i^(p) . A_j^(q)
-// keeping c = p + q <= 7: 36 int8 products accumulated exactly in int32 into 8 TMEM
-// groups.  The epilogue fuses the groups in integer arithmetic and converts twice:
-//     b_k = 128 G_2k + G_2k+1 (int32),  H = 2^14 b_0 + b_1,  Lo = 2^14 b_2 + b_3 (int64, exact)
-//     T = H + 2^-28 Lo  (one rounding)  =  2^21 sum_c 2^(-7c) G_c
-// via the 1.5 * 2^52 bit trick (a 64-bit integer multiply-add into the mantissa field +
-// one DADD / DFMA), so -2 x_i.x_j = -2^(e_i + e_j - 34) T.  The exp argument is formed
-// directly in units of 1/64 octave,
-//     y = kscale d2 = sq'_i + sq'_j + |kscale| 2^(e_i - 34) 2^(e_j) T,   sq' = kscale |x|^2,
+// Decomposition (per row i, e_i = ilogb(max_k |x_ik|) + 2, u_i = x_i 2^-e_i in (-1/2, 1/2)):
+//     U_i = rint(u_i 2^56) (int64),  u_i = sum_{p<7} A_i^(p) 2^(-8(p+1)) + r_i,  A^(p) in [-128, 127],  |r_i| <= 2^-57
+// (the balanced bytes of U_i, tc_i8.cuh:balanced_digits8).  Then
+//     x_i . x_j = 2^(e_i + e_j - 16) sum_c 2^(-8c) G_c,   G_c = sum_{p+q=c} A_i^(p) . A_j^(q)
+// keeping c = p + q <= 6: 28 int8 products accumulated exactly in int32 into 7 TMEM groups (the
+// dropped c >= 7 terms are zero-mean, |A| <= 128: the dot product stays at fp64 level, as with the
+// round-1 scheme of 8 truncated 7-bit digits and 36 products).  The drain fuses the groups in
+// integer arithmetic, straight into the mantissa field of 1.5 * 2^52 (mad.wide), and converts once:
+//     Hi = 2^24 G_0 + 2^16 G_1 + 2^8 G_2 + G_3,  Lo = 2^16 G_4 + 2^8 G_5 + G_6   (int64, exact)
+//     T = Hi + 2^-24 Lo  (one DADD + one DFMA, one rounding)  =  2^40 u_i . u_j
+// so -2 x_i.x_j = -2^(e_i + e_j - 39) T.  The exp argument is formed directly in units of 1/64
+// octave,
+//     y = kscale d2 = sq'_i + sq'_j + |kscale| 2^(e_i - 39) 2^(e_j) T,   sq' = kscale |x|^2,
 // with kscale = -scale 64 / ln2 (the per-column power of two is an integer add on the high
 // word), and e = 2^(k/64) (1 + q(f)), k = round(y), f = y - k, from the K1 64-entry table
 // (replicated 16x in shared memory so a warp's lookups are bank-conflict free) and a
@@ -30,11 +31,11 @@
 // Structure (one CTA per symmetric super-tile, 10 warps, tiles of M = 128 rows x N = 64
 // columns):
 //   warp 0     producer: 1-D bulk async copies (TMA engine) of the I tile (128 rows x 8
-//              slices, resident for a pass), a ring of J tiles (64 rows x 8 slices) and a
+//              slices, resident for a pass), a ring of J tiles (64 rows x 7 slices) and a
 //              ring of per-column data (sq', v, e_j << 20);
-//   warp 1     MMA issuer: one thread issues the 36 x (kp/32) tcgen05.mma of a tile group by
-//              group, c = 7 down to 0, each group into its own 64 TMEM columns (8 x 64 = all
-//              512), committing one mbarrier per group;
+//   warp 1     MMA issuer: one thread issues the 28 x (kp/32) tcgen05.mma of a tile group by
+//              group, c = 6 down to 0, each group into its own 64 TMEM columns (7 x 64 = 448 of
+//              the 512 allocated), committing one mbarrier per group;
 //   warps 2-9  epilogue: each thread owns one row (its TMEM lane) and 32 of the 64 columns.
 //              It drains the groups in completion order (tcgen05.ld) and releases each pair
 //              at once, so the next tile's MMAs start while this tile is still converting.
@@ -62,22 +63,24 @@ namespace krr {
 
 namespace {
 
-constexpr int P = 8;      // slices
-constexpr int NGRP = 8;   // groups c = p + q in [0, 7]
+constexpr int P = 7;      // slices (balanced 8-bit digits)
+constexpr int NGRP = 7;   // groups c = p + q in [0, 6]
 constexpr int TI = 128;   // I tile rows (MMA M)
 constexpr int TJ = 64;    // J tile columns (MMA N)
 constexpr int NCD = 3;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
-#ifndef I8_T_SMEM
-#define I8_T_SMEM 0  // drain writes T to the warp's transpose scratch, the exp loop reads it back (A/B)
+#ifndef I8_LATE_DRAIN
+#define I8_LATE_DRAIN 0  // 1: drain only after the tile's last group (no TMEM loads while the MMAs run)
 #endif
+#ifndef I8_MMA_LAST
+#define I8_MMA_LAST 1  // control warps last (epilogue 0-15, producer 16, MMA 17): the issue arbiter
+                       // prefers high warp ids, so the MMA warp is not starved by the epilogue on its SMSP
+#endif
+constexpr int WARP_PROD = I8_MMA_LAST ? NEPI : 0, WARP_MMA = I8_MMA_LAST ? NEPI + 1 : 1;
 #ifndef I8_BW
 #define I8_BW 2      // columns per exp batch
-#endif
-#ifndef I8_HALF_DRAIN
-#define I8_HALF_DRAIN 0  // drain each thread's 16 columns as two 8-column halves (A/B experiment)
 #endif
 #ifndef I8_EARLY_DONE
 #define I8_EARLY_DONE 1  // arrive on epi_done after the exp element loop (1) or after the column sums (0)
@@ -141,20 +144,16 @@ struct I8Args {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NEPI * 32) : "memory"); }
 
-// 64-bit pattern {lo = b ^ 2^31, hi = 0x43380000} + a * 2^14 (signed): the bits of the
-// double 1.5 * 2^52 + 2^31 + (2^14 a + b), exact for |2^14 a + b| < 2^51.
-__device__ __forceinline__ double magic_pack(int32_t a, int32_t b) {
-    double r;
-    asm("{\n\t.reg .b64 base, prod;\n\t"
-        "mov.b64 base, {%2, %3};\n\t"
-        "mad.wide.s32 prod, %1, 16384, base;\n\t"
-        "mov.b64 %0, prod;\n\t}\n"
-        : "=d"(r)
-        : "r"(a), "r"(int(uint32_t(b) ^ 0x80000000u)), "r"(0x43380000));
-    return r;
+// a * b + c with a 32 x 32 -> 64-bit signed product (mad.wide.s32)
+__device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
+    int64_t d;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
 }
-// 1.5 * 2^52 + 2^31 and that constant times (1 + 2^-28), both exact integers < 2^53
-constexpr double M2 = 6755401588539392.0 + 25165832.0;  // M1 = 1.5 * 2^52 + 2^31, M2 = M1 (1 + 2^-28)
+// the bits of 1.5 * 2^52: MAGIC + V is the double 1.5 * 2^52 + V for |V| < 2^51
+constexpr int64_t MAGIC = 0x4338000000000000LL;
+// 1.5 * 2^52 (1 + 2^-24): (1.5 2^52 + Hi) + (1.5 2^52 + Lo) 2^-24 - M2 = Hi + 2^-24 Lo, exact integers
+constexpr double M2 = 6755399441055744.0 + 402653184.0;
 
 template <bool MASK, bool CHEAP = false, bool POLY = false>
 __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts& ec, const double* __restrict__ tab,
@@ -172,13 +171,7 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
     constexpr int BW = I8_BW;
     // T of column k: registers, or (I8_T_SMEM) this lane's slot of the transpose scratch, which the
     // element loop overwrites with e v_i for the same column right after reading it
-    auto tval = [&](int k) {
-#if I8_T_SMEM
-        return scr[k * SCR_LD + lane];
-#else
-        return T[k];
-#endif
-    };
+    auto tval = [&](int k) { return T[k]; };
 #pragma unroll
     for (int k0 = 0; k0 < CPT; k0 += BW) {
         double y[BW], t2[BW], f[BW], q[BW], e[BW];
@@ -333,13 +326,13 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         tc::mbar_fence_init();
     }
     for (int i = tid; i < TAB * TAB_REP; i += NTHR) tab[i] = g_tab64[i / TAB_REP];
-    if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == WARP_MMA) tc::tmem_alloc(tmem_slot, TMEM_COLS);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp == WARP_PROD) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             int bq = 0;
@@ -367,7 +360,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == WARP_MMA) {
         // ------------------------------------------------------------ MMA issuer
         // The whole warp runs the (warp-uniform) schedule and waits, so the descriptors stay in
         // uniform registers; one elected lane issues each group's MMAs and their commits.  (A
@@ -424,7 +417,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int ew = warp - 2;            // 0..NEPI-1
+        const int ew = I8_MMA_LAST ? warp : warp - 2;  // 0..NEPI-1
         const int quarter = warp & 3;       // TMEM lane quarter this warp may access
         const int half = ew >> 2;           // which CPT of the 64 columns
         const int etid = ew * 32 + lane;
@@ -437,8 +430,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
             const int64_t gi = rowBase + int64_t(it) * TI + row;
             const double sqs_i = A.sqs[gi];
             const double v_i = A.v[gi];
-            // |kscale| 2^(e_i - 34) (Gaussian) | gamma 2^(e_i - 35) (polynomial: x.x = 2^(e_i+e_j-35) T)
-            const int nsi_hi = kabs_hi + (A.ex[gi] - (POLY ? 35 : 34)) * (1 << 20);
+            // |kscale| 2^(e_i - 39) (Gaussian: -2 x.x = -2^(e_i+e_j-39) T) | gamma 2^(e_i - 40) (polynomial)
+            const int nsi_hi = kabs_hi + (A.ex[gi] - (POLY ? 40 : 39)) * (1 << 20);
             double rowacc = 0.0;
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++tq) {
                 const uint32_t ph = uint32_t(tq & 1);
@@ -446,85 +439,50 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
 
                 // ---- drain the 8 groups in MMA completion order (7 -> 0) two at a time,
                 // 16 columns per tcgen05.ld (register pressure), releasing each pair at once
-#if I8_HALF_DRAIN
-                // two 8-column halves, each through all four stages (fewer live registers); the
-                // groups are released after the second half (the next tile's MMAs wait for the exp
-                // phase anyway: time-multiplexed)
-                int32_t bint[CPT / 2];
-                double lo[CPT / 2], T[CPT];
-                auto stage = [&](int ca, int h, auto&& fn) {
-                    uint32_t gl[CPT / 2], gh[CPT / 2];
-                    if (h == 0) {
-                        tc::mbar_wait_sleep(g_full + ca + 1, ph);
-                        tc::fence_after();
-                    }
-                    tc::tmem_ld8(taddr + uint32_t((ca + 1) * TJ + h * (CPT / 2)), gl);
-                    if (h == 0) {
-                        tc::mbar_wait_sleep(g_full + ca, ph);
-                        tc::fence_after();
-                    }
-                    tc::tmem_ld8(taddr + uint32_t(ca * TJ + h * (CPT / 2)), gh);
-                    tc::tmem_wait_ld();
-#pragma unroll
-                    for (int k = 0; k < CPT / 2; ++k) fn(k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
-                    if (h == 1) {
-                        tc::fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            tc::mbar_arrive(g_empty + ca + 1);
-                            tc::mbar_arrive(g_empty + ca);
-                        }
-                    }
-                };
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    stage(6, h, [&](int k, int32_t b) { bint[k] = b; });
-                    stage(4, h, [&](int k, int32_t b) { lo[k] = magic_pack(b, bint[k]); });
-                    stage(2, h, [&](int k, int32_t b) { bint[k] = b; });
-                    stage(0, h, [&](int k, int32_t b) {
-                        T[h * (CPT / 2) + k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);
-                    });
-                }
-#else
-                int32_t bint[CPT];
+                // Completion order 6 -> 0, drained as (6, 5), (4, 3), (2, 1), (0).  W = sum_c 2^(8(6-c)) G_c
+                // = 2^24 H + L with
+                //   L = 2^24 G_3 + 2^16 G_4 + 2^8 G_5 + G_6   (|L| < 2^47),
+                //   H = 2^24 G_0 + 2^16 G_1 + 2^8 G_2         (|H| < 2^45),
+                // each built as int64 straight into the mantissa field of 1.5 * 2^52 (mad.wide), then
+                // T = H + 2^-24 L = 2^-24 W with one DADD + one DFMA (one rounding).  Live partials stay
+                // small: one int64 (2^8 G_5 + G_6 can exceed int32 for all-128 digits), then the double
+                // L, then 2^8 G_1 + G_2 as int32.  (Pairing (6), (5, 4), (3, 2), (1, 0) measured 3 % slower.)
+                int64_t acc[CPT];
+                int32_t t12[CPT];
                 double lo[CPT], T[CPT];
-                auto stage = [&](int ca, auto&& fn) {  // groups ca (weight 128) and ca + 1
-                    // both loads of the stage in flight before one wait (TMEM load latency under
-                    // load is ~250 clk); group ca + 1 completes first (issue order 7 -> 0), so its
-                    // load overlaps the wait for group ca — on the tile's last stage that wait is
-                    // the exposed tail before the exp phase
-                    uint32_t gl[CPT], gh[CPT];
-                    tc::mbar_wait_sleep(g_full + ca + 1, ph);
-                    tc::fence_after();
-                    tc::tmem_ld16(taddr + uint32_t((ca + 1) * TJ), gl);
+                auto stage = [&](int ca, int cb, auto&& fn) {  // groups ca (completes first) and cb = ca - 1 (or none)
+                    // both loads in flight before one wait (TMEM load latency under load ~250 clk)
+                    uint32_t ga[CPT], gb[CPT];
                     tc::mbar_wait_sleep(g_full + ca, ph);
                     tc::fence_after();
-                    tc::tmem_ld16(taddr + uint32_t(ca * TJ), gh);
+                    tc::tmem_ld16(taddr + uint32_t(ca * TJ), ga);
+                    if (cb >= 0) {
+                        tc::mbar_wait_sleep(g_full + cb, ph);
+                        tc::fence_after();
+                        tc::tmem_ld16(taddr + uint32_t(cb * TJ), gb);
+                    }
                     tc::tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) fn(k, int32_t(gh[k]) * 128 + int32_t(gl[k]));
+                    for (int k = 0; k < CPT; ++k) fn(k, int32_t(ga[k]), int32_t(gb[k]));
                     tc::fence_before();
                     __syncwarp();
                     if (lane == 0) {
-                        tc::mbar_arrive(g_empty + ca + 1);
                         tc::mbar_arrive(g_empty + ca);
+                        if (cb >= 0) tc::mbar_arrive(g_empty + cb);
                     }
                 };
-                stage(6, [&](int k, int32_t b) { bint[k] = b; });                    // b3
+                if (I8_LATE_DRAIN) tc::mbar_wait_sleep(g_full + 0, ph);
+                stage(6, 5, [&](int k, int32_t g6, int32_t g5) { acc[k] = mad_wide(g5, 256, int64_t(g6)); });
                 I8_TRACE(etid == 0, tq, 1);
-                stage(4, [&](int k, int32_t b) { lo[k] = magic_pack(b, bint[k]); });  // M1 + Lo
-                I8_TRACE(etid == 0, tq, 2);
-                stage(2, [&](int k, int32_t b) { bint[k] = b; });                    // b1
-                I8_TRACE(etid == 0, tq, 3);
-                stage(0, [&](int k, int32_t b) {
-#if I8_T_SMEM
-                    scr[k * SCR_LD + lane] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
-#else
-                    T[k] = fma(lo[k], 0x1p-28, magic_pack(b, bint[k]) - M2);  // H + 2^-28 Lo
-#endif
+                stage(4, 3, [&](int k, int32_t g4, int32_t g3) {
+                    lo[k] = __longlong_as_double(mad_wide(g3, 1 << 24, mad_wide(g4, 65536, acc[k] + MAGIC)));  // 1.5 2^52 + L
                 });
-
-#endif
+                I8_TRACE(etid == 0, tq, 2);
+                stage(2, 1, [&](int k, int32_t g2, int32_t g1) { t12[k] = g1 * 256 + g2; });  // |.| < 2^30
+                I8_TRACE(etid == 0, tq, 3);
+                stage(0, -1, [&](int k, int32_t g0, int32_t) {
+                    T[k] = fma(lo[k], 0x1p-24, __longlong_as_double(mad_wide(g0, 1 << 24, mad_wide(t12[k], 256, MAGIC))) - M2);
+                });
 
                 // ---- exp, row sums, column sums
                 I8_TRACE(etid == 0, tq, 4);
@@ -546,7 +504,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 if (A.debug & 2) {
                     double z = 0.0;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) z += I8_T_SMEM ? scr[k * SCR_LD + lane] : T[k];
+                    for (int k = 0; k < CPT; ++k) z += T[k];
                     rowacc += z;
                 } else if (masked) {
                     // diagonal block: keep j > i (local column index vs local row index)
@@ -606,7 +564,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
 
     tc::fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem_base, TMEM_COLS);
+    if (warp == WARP_MMA) tc::tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
 // ---- operand preparation
@@ -621,7 +579,9 @@ __global__ void row_exponent_kernel(const double* __restrict__ X, int64_t n, int
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0) {
-            const int e = m > 0.0 ? ilogb(m) + 1 : 0;
+            // |x_ik| 2^-e <= 127/255 - 2^-56: the range of 7 balanced 8-bit digits (tc_i8.cuh)
+            int e = m > 0.0 ? ilogb(m) + 2 : 0;
+            if (m > 0.0 && scalbn(m, -e) > 0.498) ++e;
             ex[i] = e;
             ejs[i] = e * (1 << 20);
         }
@@ -636,14 +596,11 @@ __global__ void slice_kernel(const double* __restrict__ X, int64_t n, int64_t d,
         const int64_t row = idx / kp;
         const int k = int(idx % kp);
         const double x = (row < n && k < d) ? X[row * d + k] : 0.0;
-        double w = scalbn(x, 7 - ex[row]);  // u * 2^7, |u| < 1
+        int a[P];
+        tc::balanced_digits8(x, ex[row], a);
         const int64_t off = (row >> 3) * int64_t(kp) * 8 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-            const double a = trunc(w);
-            S[int64_t(p) * n_pad * kp + off] = uint8_t(int8_t(int(a)));
-            w = (w - a) * 128.0;
-        }
+        for (int p = 0; p < P; ++p) S[int64_t(p) * n_pad * kp + off] = uint8_t(int8_t(a[p]));
     }
 }
 
@@ -710,7 +667,7 @@ bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, con
     scaled_sq_kernel<<<unsigned(std::min<int64_t>((n_pad + 255) / 256, 148 * 8)), 256, 0, stream>>>(
         L, n_pad, dp, int(d), ks, sqs);
     KRR_LAUNCH_CHECK();
-    // exponent range: (1) |kscale| 2^(e_i + e_j - 34) stays a normal double;
+    // exponent range: (1) |kscale| 2^(e_i + e_j - 39) stays a normal double;
     // (2) |y| = |kscale| d2 <= |kscale| 4 d 2^(2 e_max) < 2^50 (the 1.5 * 2^52 rounding shifter)
     std::vector<int> h(static_cast<size_t>(n_pad));
     KRR_CUDA(cudaMemcpyAsync(h.data(), ex, sizeof(int) * size_t(n_pad), cudaMemcpyDeviceToHost, stream));
@@ -720,13 +677,13 @@ bool i8_prepare_launch(const double* X, int64_t n, int64_t d, int64_t n_pad, con
         lo = std::min(lo, e);
         hi = std::max(hi, e);
     }
-    if (poly_gamma > 0.0) {  // polynomial kernel: gamma 2^(e_i + e_j - 35) must be a normal double
+    if (poly_gamma > 0.0) {  // polynomial kernel: gamma 2^(e_i + e_j - 40) must be a normal double
         const int eg = std::ilogb(poly_gamma);
-        return eg + 2 * lo - 35 > -1000 && eg + 2 * hi - 35 < 1000;
+        return eg + 2 * lo - 40 > -1000 && eg + 2 * hi - 40 < 1000;
     }
     const int ek = std::ilogb(-ks);
     const double ymax = -ks * 4.0 * double(d) * std::ldexp(1.0, 2 * hi);
-    return ek + 2 * lo - 34 > -1000 && ek + 2 * hi - 34 < 1000 && ymax < std::ldexp(1.0, 50);
+    return ek + 2 * lo - 39 > -1000 && ek + 2 * hi - 39 < 1000 && ymax < std::ldexp(1.0, 50);
 }
 
 void gauss_matvec_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const int* ex, const int* ejs,

@@ -139,6 +139,23 @@ __device__ __forceinline__ void mbar_wait_sleep(void* mbar, uint32_t parity) {
         : "memory");
 }
 
+// The 7 balanced 8-bit digits of u = x 2^-e for the INT8 Ozaki slices of K1-I8 / K1T-I8, for
+// |u| <= 0.498 (7 digits in [-128, 127] span u in [-128/255, 127/255]; the callers choose e so):
+// U = rint(u 2^56) as an int64 (exact: |U| < 2^55), then its bytes from the least significant one,
+// each taken as a signed byte with the carry pushed up, so every digit is in [-128, 127] and
+//     u = sum_{p<7} a_p 2^(-8 (p + 1))   up to the rounding of U (<= 2^-57).
+// Products a_p a_q with p + q <= 6 (28 of 49) keep the dot product at fp64 level: the dropped
+// terms are zero-mean with |digit| <= 128 (paper_1611_03220_b200/intexp.py's study, profiles/).
+__device__ __forceinline__ void balanced_digits8(double x, int e, int (&a)[7]) {
+    long long U = __double2ll_rn(scalbn(x, 56 - e));
+#pragma unroll
+    for (int p = 6; p >= 0; --p) {
+        const int dgt = int(int8_t(uint8_t(uint64_t(U) & 0xFFu)));  // sign-extended low byte
+        a[p] = dgt;
+        U = (U - dgt) >> 8;
+    }
+}
+
 // 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(

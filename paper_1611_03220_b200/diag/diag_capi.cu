@@ -156,9 +156,9 @@ int krr_diag_i8_mma_rate(int device, int N, int reps, int kbytes, int mode, doub
             krr::fp64_under_mma(7, 1, std::max(64, reps), st.s, cycles_per_mma);
             return;
         }
-        if (mode == 6 || mode == 7 || mode == 30) {  // in-situ K1-I8 tile order (N = 64, kp = 96), reps = tiles;
+        if (mode == 6 || mode == 7 || mode == 30 || mode == 31) {  // 31: K1-I8's 7-slice order (84 MMAs)  // in-situ K1-I8 tile order (N = 64, kp = 96), reps = tiles;
             // 30: K1T-I8's K-chunk order and stage layout (14 chunks x 36 MMAs, one resident stage)
-            *cycles_per_mma = krr::i8_tile_order_rate(mode == 30 ? 2 : mode - 6, std::max(1, reps), st.s);
+            *cycles_per_mma = krr::i8_tile_order_rate(mode == 30 ? 2 : (mode == 31 ? 3 : mode - 6), std::max(1, reps), st.s);
             return;
         }
         if (reps < 8 || mode < 0 || mode > 5) fail(KRR_ERR_INVALID_ARGUMENT, "reps >= 8, mode in [0, 7]");

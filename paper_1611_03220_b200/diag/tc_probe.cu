@@ -161,7 +161,18 @@ __global__ void __launch_bounds__(128) i8_tile_order_kernel(int tiles, long long
         const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sm + 8 * TI * KP), 128, KP * 8);
         const long long t0 = clock64();
         for (int t = 0; t < tiles; ++t) {
-            if constexpr (ORDER == 2) {
+            if constexpr (ORDER == 3) {
+                // K1-I8's 7-slice order (balanced 8-bit digits): c = 6..0, p = 0..c, 3 K steps, 84 MMAs
+#pragma unroll
+                for (int c = 6; c >= 0; --c)
+#pragma unroll
+                    for (int p = 0; p <= c; ++p)
+#pragma unroll
+                        for (int ks = 0; ks < 3; ++ks)
+                            tc::mma_i8(tmem + uint32_t(c * TJ), dA0 + uint64_t((p * TI * KP + ks * 256) >> 4),
+                                       dB0 + uint64_t(((c - p) * TJ * KP + ks * 256) >> 4), idesc,
+                                       (p == 0 && ks == 0) ? 0u : 1u);
+            } else if constexpr (ORDER == 2) {
                 // K1T-I8's chunk order and layout: one 48 KB stage ([p][128 x 32 B] A, [p][64 x 32 B] B,
                 // LBO 128 B, SBO 256 B), 14 K chunks of 36 MMAs into the same 8 accumulators
                 const uint64_t a2 = tc::smem_desc(tc::smem_u32(sm), 128, 256);
@@ -520,7 +531,8 @@ double i8_tile_order_rate(int order, int tiles, cudaStream_t stream) {
     };
     if (order == 0) run(i8_tile_order_kernel<0>);
     else if (order == 1) run(i8_tile_order_kernel<1>);
-    else run(i8_tile_order_kernel<2>);
+    else if (order == 2) run(i8_tile_order_kernel<2>);
+    else run(i8_tile_order_kernel<3>);
     KRR_LAUNCH_CHECK();
     long long h[148];
     KRR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -528,7 +540,7 @@ double i8_tile_order_rate(int order, int tiles, cudaStream_t stream) {
     cudaFree(d);
     double mx = 0;
     for (long long v : h) mx = std::max(mx, double(v));
-    return mx / (double(tiles) * (order == 2 ? 14.0 * 36.0 : 108.0));
+    return mx / (double(tiles) * (order == 2 ? 14.0 * 36.0 : (order == 3 ? 84.0 : 108.0)));
 }
 
 double fp64_under_mma(int op, int mma, int iters, cudaStream_t stream, double* mma_cycles, int nwork) {
