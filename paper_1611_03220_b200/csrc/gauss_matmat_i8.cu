@@ -67,6 +67,11 @@ constexpr int TAB = 64;
 constexpr int TAB_REP = 16;
 constexpr int YMIN_K = -1022 * TAB;
 constexpr int KP_MAX = 448;
+#ifndef MI8_TS
+#define MI8_TS 4  // A slices 0 .. MI8_TS-1 of each K chunk copied to TMEM (tcgen05.cp) and used in TS
+                  // mode: the 64 TMEM columns the 7 accumulator groups leave free hold two chunks x 4
+                  // slices; 22 of the 28 MMAs then read only B from shared memory
+#endif
 #ifndef MI8_PROFILE
 #define MI8_PROFILE 0  // 1: compile the profiling modes (debug bits 1 / 2 / 8; A/B builds only: they cost ~6 % in the hot loops)
 #endif
@@ -90,6 +95,7 @@ constexpr size_t OFF_BARS = OFF_TAB + size_t(TAB) * TAB_REP * 8;
 constexpr int NBARS = 2 * NSTG * P + 2 * NCD + 2 * NGRP + 1;
 constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
 static_assert(SMEM <= 227 * 1024, "K1T-I8 shared memory");
+static_assert(NGRP * TJ + NSTG * MI8_TS * 8 <= TMEM_COLS, "K1T-I8 TMEM: accumulators + TS operand buffers");
 
 // profiling trace (debug bit 2): clock64 stamps of CTA 0, 16 per tile, first 32 tiles
 constexpr int MTRACE_TILES = 32;
@@ -262,6 +268,16 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     const uint64_t dA0 = tc::smem_desc(sbase, 128, 256);
                     const uint64_t dB0 = tc::smem_desc(sbase + A_CH, 128, 256);
                     const bool last = (ks == KS - 1);
+                    // TS operands of this chunk into the stage's TMEM buffer (the stage is reused only after
+                    // the chunk two back completed, so the buffer is free; tcgen05 ops of one thread run in order)
+                    const uint32_t abuf = tmem_base + uint32_t(NGRP * TJ) + uint32_t(s * MI8_TS * 8);
+                    if (!SB && MI8_TS > 0) {
+                        if (tc::elect_one())
+#pragma unroll
+                            for (int p = 0; p < MI8_TS; ++p)
+                                tc::tmem_cp_128x256b(abuf + uint32_t(p * 8), dA0 + uint64_t((p * TI * 32) >> 4));
+                        __syncwarp();
+                    }
 #pragma unroll
                     for (int c = NGRP - 1; c >= 0; --c) {
                         if (ks == 0 && bq > 0) {
@@ -292,10 +308,16 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                         }
                         if (tc::elect_one()) {
 #pragma unroll
-                            for (int p = 0; p <= c; ++p)
-                                if (!(MI8_PROFILE && (A.debug & 1))) tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4),
-                                           dB0 + uint64_t(((c - p) * TJ * 32) >> 4), idesc,
-                                           (ks == 0 && p == 0) ? 0u : 1u);
+                            for (int p = 0; p <= c; ++p) {
+                                if (MI8_PROFILE && (A.debug & 1)) continue;
+                                const uint64_t db = dB0 + uint64_t(((c - p) * TJ * 32) >> 4);
+                                if (!SB && p < MI8_TS)
+                                    tc::mma_i8_ts(tmem_base + uint32_t(c * TJ), abuf + uint32_t(p * 8), db, idesc,
+                                                  (ks == 0 && p == 0) ? 0u : 1u);
+                                else
+                                    tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * 32) >> 4), db, idesc,
+                                               (ks == 0 && p == 0) ? 0u : 1u);
+                            }
                             if (last) tc::mma_commit(g_full + c);
                             if (SB) tc::mma_commit(s_empty + s * P + c);  // group c: last reader of slice c
                         }

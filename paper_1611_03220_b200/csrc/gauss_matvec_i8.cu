@@ -71,6 +71,10 @@ constexpr int NCD = 3;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
+#ifndef I8_TS
+#define I8_TS 1  // A slices 0 .. nts-1 of the resident I tile copied to the 64 TMEM columns the 7
+                 // accumulator groups leave free (tcgen05.cp, once per pass) and used in TS mode
+#endif
 #ifndef I8_LATE_DRAIN
 #define I8_LATE_DRAIN 0  // 1: drain only after the tile's last group (no TMEM loads while the MMAs run)
 #endif
@@ -369,9 +373,26 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         const uint32_t idesc = tc::idesc_i8(TI, TJ);
         const uint32_t aBase = tc::smem_u32(sA);
         int bq = 0;
+        // TS operands: A slices p < NTS (kp / 4 TMEM columns each) at columns 448 ..
+        constexpr int COLS_A = kp / 4;
+        constexpr int NTS = I8_TS ? ((TMEM_COLS - NGRP * TJ) / COLS_A < P ? (TMEM_COLS - NGRP * TJ) / COLS_A : P) : 0;
+        const uint32_t tA = tmem_base + uint32_t(NGRP * TJ);
         for (int it = 0; it < nTI; ++it) {
             tc::mbar_wait_sleep(a_full, uint32_t(it & 1));
             tc::fence_after();
+            if (NTS > 0) {
+                // the previous pass's MMAs are complete (the producer reloaded A after a_empty), so the
+                // columns are free; tcgen05 ops of one thread run in order, so the MMAs below see the copy
+                const uint64_t dAc = tc::smem_desc(aBase, 128, sbo);
+                if (tc::elect_one())
+#pragma unroll
+                    for (int p = 0; p < NTS; ++p)
+#pragma unroll
+                        for (int ks = 0; ks < ksteps; ++ks)
+                            tc::tmem_cp_128x256b(tA + uint32_t(p * COLS_A + ks * 8),
+                                                 dAc + uint64_t((p * TI * kp + ks * 256) >> 4));
+                __syncwarp();
+            }
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
                 const int s = bq % NSTB;
                 I8_TRACE(lane == 0, bq, 8);
@@ -400,11 +421,15 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
 #pragma unroll
                             for (int p = 0; p <= c; ++p)
 #pragma unroll
-                                for (int ks = 0; ks < ksteps; ++ks)
-                                    tc::mma_i8(tmem_base + uint32_t(c * TJ),
-                                               dA0 + uint64_t((p * TI * kp + ks * 256) >> 4),
-                                               dB0 + uint64_t(((c - p) * TJ * kp + ks * 256) >> 4), idesc,
-                                               (p == 0 && ks == 0) ? 0u : 1u);
+                                for (int ks = 0; ks < ksteps; ++ks) {
+                                    const uint64_t db = dB0 + uint64_t(((c - p) * TJ * kp + ks * 256) >> 4);
+                                    if (p < NTS)
+                                        tc::mma_i8_ts(tmem_base + uint32_t(c * TJ), tA + uint32_t(p * COLS_A + ks * 8), db,
+                                                      idesc, (p == 0 && ks == 0) ? 0u : 1u);
+                                    else
+                                        tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * kp + ks * 256) >> 4),
+                                                   db, idesc, (p == 0 && ks == 0) ? 0u : 1u);
+                                }
                         tc::mma_commit(g_full + c);
                     }
                     __syncwarp();

@@ -72,6 +72,12 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint
         "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
+// smem -> TMEM copy of a 128-row x 32-byte K-major block (the A operand of one K step):
+// 128 lanes x 8 columns, ordered with the tcgen05 pipe like the MMAs the same thread issues.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 // One lane of a converged warp (the lowest active one: the same lane every call, so the
 // tcgen05.commit that tracks a thread's MMAs is issued by the thread that issued them).
 __device__ __forceinline__ bool elect_one() {
