@@ -78,12 +78,12 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
 
 /* Tuning / diagnostic knobs (no reference equivalent):
  *   "k1_path"     -1|0|1|3  fused mat-vec kernel: auto (default: INT8-slice tensor-core kernel
- *                         where faster: 27 <= d <= 32, 44 <= d <= 96, when the data's exponent range allows, else FP64 DMMA) |
+ *                         where faster: 31 <= d <= 32, 37 <= d <= 96, when the data's exponent range allows, else FP64 DMMA) |
  *                         FP64 DMMA | tcgen05 INT8 slices | K1-I8X (INT8 slices, exact integer exp argument;
  *                         Gaussian, d <= 96, |x| sqrt(2 scale) < 256; otherwise the request runs the auto choice)
  *   "k1t_path"    -1|0|1  16-column batches of multi-RHS mat-mats / batched PCG: auto (default:
  *                         K1T-I8 — INT8-slice dot products on K-streamed operands + DMMA E.V —
- *                         for the Gaussian kernel with 28 <= d <= 448, else the DMMA K1T) |
+ *                         for the Gaussian kernel with 20 <= d <= 448, else the DMMA K1T) |
  *                         DMMA K1T | K1T-I8 where supported
  *   "k1_resident" 1|0  keep the column tile of the DMMA mat-vec in shared memory (default 1)
  *   "k1_warps" 8|16, "k1_grouped" 1|0  DMMA mat-vec shape (defaults 8, 1)

@@ -52,7 +52,7 @@ void gauss_matmat_i8_launch(const GaussMatvecPlan& p, const uint8_t* S, const in
                             int debug = 0);
 void i8s_read_trace(long long* out, int count);
 constexpr int64_t kI8T1MinD = 160;  // single-RHS K v through K1T-I8 from d = 160 (when K1-I8 does not apply)
-constexpr int64_t kI8TMinD = 28;  // auto path: K1T-I8 from d = 28 (measured crossover, profiles/r1_k1t_i8_crossover.log)
+constexpr int64_t kI8TMinD = 20;  // auto path: K1T-I8 from d = 20 (measured crossover, profiles/r2_k1t_i8_crossover.log)
 
 // K1-I8X: K1-I8's tensor-core dot products with an integer exp epilogue that overlaps the MMAs
 // (gauss_matvec_i8x.cu).  Gaussian kernel, d <= 96.  prepare returns the global exponent E of

@@ -279,10 +279,11 @@ bool use_i8(const Ctx& c) {
         const double i8_ms = c.kp8 <= 32 ? 7.49 : (c.kp8 <= 64 ? 9.74 : 11.4);
         return i8_ms < dmma_ms;
     }
-    // Cost model from the measured crossover (n = 65536, profiles/r1_k1_crossover_n65536.log):
-    // the DMMA K1 grows ~linearly in d, K1-I8 steps with the slice width kp = 32 / 64 / 96.
+    // Cost model from the measured crossover (n = 65536, profiles/r2_k1_crossover_n65536.log, round 2's
+    // 28-product slices with TS-mode A operands): the DMMA K1 grows ~linearly in d, K1-I8 steps
+    // with the slice width kp = 32 / 64 / 96.
     const double dmma_ms = 4.40 + 0.1405 * double(c.d);
-    const double i8_ms = c.kp8 <= 32 ? 8.04 : (c.kp8 <= 64 ? 10.43 : 11.9);
+    const double i8_ms = c.kp8 <= 32 ? 8.62 : (c.kp8 <= 64 ? 9.57 : 10.73);
     return i8_ms < dmma_ms;
 }
 

@@ -74,9 +74,9 @@ def test_i8_matmat_rank_emulation_partials_sum(krr, oracle, ctx):
     assert rel(acc, full) <= 1e-14, rel(acc, full)
 
 
-@pytest.mark.parametrize("d,want", [(16, 0), (27, 0), (28, 1), (90, 1), (440, 1), (449, 0)])
+@pytest.mark.parametrize("d,want", [(16, 0), (19, 0), (20, 1), (90, 1), (440, 1), (449, 0)])
 def test_k1t_path_auto_selection(krr, oracle, ctx, d, want):
-    """Auto K1T path: K1T-I8 from d = 28 (profiles/r1_k1t_i8_crossover.log) up to kp = 448."""
+    """Auto K1T path: K1T-I8 from d = 20 (profiles/r2_k1t_i8_crossover.log) up to kp = 448."""
     x = oracle.random_matrix(600, d, 3)
     krr.GaussianOperator(x, krr.KernelSpec.gaussian(4.0), 0.0, ctx=ctx)
     assert ctx.get_option("k1t_path") == -1
