@@ -87,7 +87,8 @@ constexpr int WARP_PROD = I8_MMA_LAST ? NEPI : 0, WARP_MMA = I8_MMA_LAST ? NEPI 
 #define I8_BW 2      // columns per exp batch
 #endif
 #ifndef I8_EARLY_DONE
-#define I8_EARLY_DONE 1  // arrive on epi_done after the exp element loop (1) or after the column sums (0)
+#define I8_EARLY_DONE 0  // arrive on epi_done after the exp element loop (1) or after the column sums (0, round 2: the
+                         // column sums then run on an idle tensor pipe and the next drain starts earlier)
 #endif
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int KP_MAX = 96;
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                         tc::mbar_wait_sleep(g_empty + c, uint32_t((bq - 1) & 1));
                         tc::fence_after();
                     }
-                    if (c == 7 || c == 4 || c == 0) I8_TRACE(lane == 0, bq, c == 7 ? 10 : (c == 4 ? 11 : 12));
+                    if (c == NGRP - 1 || c == 4 || c == 0) I8_TRACE(lane == 0, bq, c == NGRP - 1 ? 10 : (c == 4 ? 11 : 12));
                     if (tc::elect_one()) {
                         if (!(A.debug & 1))
 #pragma unroll
@@ -480,6 +481,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     uint32_t ga[CPT], gb[CPT];
                     tc::mbar_wait_sleep(g_full + ca, ph);
                     tc::fence_after();
+                    if (ca == 0) I8_TRACE(etid == 0, tq, 15);  // the tile's last MMA group is complete
                     tc::tmem_ld16(taddr + uint32_t(ca * TJ), ga);
                     if (cb >= 0) {
                         tc::mbar_wait_sleep(g_full + cb, ph);
