@@ -419,6 +419,15 @@ def main():
             traffic = None
     fp64_view = {"achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s", "frac": achieved / peak_dmma,
                  "peak_source": "FP64 DMMA mma.sync m8n8k4 rate measured live on this GPU (krr_diag_microbench)"}
+    # roofline Gevals/s per GPU = min(P_DMMA / 2d, R_FP64 / 23) for the
+    # reference-shaped FP64 formulation (every kernel evaluation computed, DMMA dot product, 23-op
+    # libdevice-exp epilogue), with the measured peaks; value / roofline > 1 is what the symmetric
+    # tiles and the INT8 dot products buy over it
+    peak_dfma = float(mb[1])
+    s8d = min(peak_dmma * 1e12 / (2.0 * d), peak_dfma * 1e12 / 2.0 / 23.0) / 1e9 * world
+    fp64_view["survey_8d"] = {"roofline_gevals": s8d, "achieved_gevals": float(n) * n / (k1_ms * 1e-3) / 1e9,
+                              "ratio": (float(n) * n / (k1_ms * 1e-3) / 1e9) / s8d,
+                              "note": "min(P_DMMA / 2d, R_FP64 / 23) per kernel evaluation (n^2 per mat-vec)"}
     if path == 1:
         kp = (d + 31) // 32 * 32
         i8_ops = pairs_rank * I8_PRODUCTS * kp * 2.0

@@ -508,7 +508,11 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 stage(2, 1, [&](int k, int32_t g2, int32_t g1) { t12[k] = g1 * 256 + g2; });  // |.| < 2^30
                 I8_TRACE(etid == 0, tq, 3);
                 stage(0, -1, [&](int k, int32_t g0, int32_t) {
+#if I8_PROBE_NOFP64_T  // profiling only (wrong values): the last drain stage without its two FP64 ops
+                    T[k] = __longlong_as_double(mad_wide(g0, 1 << 24, mad_wide(t12[k], 256, MAGIC)) ^ __double_as_longlong(lo[k]));
+#else
                     T[k] = fma(lo[k], 0x1p-24, __longlong_as_double(mad_wide(g0, 1 << 24, mad_wide(t12[k], 256, MAGIC))) - M2);
+#endif
                 });
 
                 // ---- exp, row sums, column sums
