@@ -71,6 +71,9 @@ constexpr int NCD = 3;    // column-data stages
 constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
+#ifndef I8_PROFILE
+#define I8_PROFILE 1  // 0: compile out the profiling modes (debug bits 1, 2, 16, 32; the trace stays)
+#endif
 #ifndef I8_TS
 #define I8_TS 1  // A slices 0 .. nts-1 of the resident I tile copied to the 64 TMEM columns the 7
                  // accumulator groups leave free (tcgen05.cp, once per pass) and used in TS mode
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 // FP64 pipe ~4x (probe) to ~8x (in situ), so FP64 work overlapped with MMAs is
                 // nearly wasted; serialising the exp phase is 6 % faster (d = 54 and 90).  The
                 // drain (TMEM loads, integer combination) still overlaps the MMAs.
-                if (!(A.debug & 32) && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
+                if (!(I8_PROFILE && (A.debug & 32)) && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
 #pragma unroll
                 for (int c = NGRP - 1; c >= 0; --c) {
                     if (bq > 0) {
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     }
                     if (c == NGRP - 1 || c == 4 || c == 0) I8_TRACE(lane == 0, bq, c == NGRP - 1 ? 10 : (c == 4 ? 11 : 12));
                     if (tc::elect_one()) {
-                        if (!(A.debug & 1))
+                        if (!(I8_PROFILE && (A.debug & 1)))
 #pragma unroll
                             for (int p = 0; p <= c; ++p)
 #pragma unroll
@@ -531,8 +534,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                                      ? g_trace + tq * 16 : nullptr;
                 // epi_done is arrived inside exp_phase (after its FP64 element loop) unless the
                 // exp phase is skipped (profiling) or I8_EARLY_DONE = 0
-                uint64_t* early = (I8_EARLY_DONE && !(A.debug & 2)) ? epi_done : nullptr;
-                if (A.debug & 2) {
+                uint64_t* early = (I8_EARLY_DONE && !(I8_PROFILE && (A.debug & 2))) ? epi_done : nullptr;
+                if (I8_PROFILE && (A.debug & 2)) {
                     double z = 0.0;
 #pragma unroll
                     for (int k = 0; k < CPT; ++k) z += T[k];
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
                     exp_phase<true, false, POLY>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
                                          rowacc, lane, colOff, mask_row, early);
-                } else if (A.debug & 16) {
+                } else if (I8_PROFILE && (A.debug & 16)) {
                     exp_phase<false, true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i,
                                            v_i, rowacc, lane, colOff, 0, early);
                 } else {
