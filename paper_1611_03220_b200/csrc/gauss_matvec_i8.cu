@@ -87,11 +87,13 @@ constexpr int NTHR = 32 * (2 + NEPI);
 #endif
 constexpr int WARP_PROD = I8_MMA_LAST ? NEPI : 0, WARP_MMA = I8_MMA_LAST ? NEPI + 1 : 1;
 #ifndef I8_BW
-#define I8_BW 2      // columns per exp batch
+#define I8_BW 4      // columns per exp batch (round 2, with the int64 tail below: 4 beats 2 by 2.5 %, 8 spills)
 #endif
 #ifndef I8_EARLY_DONE
-#define I8_EARLY_DONE 0  // arrive on epi_done after the exp element loop (1) or after the column sums (0, round 2: the
-                         // column sums then run on an idle tensor pipe and the next drain starts earlier)
+#define I8_EARLY_DONE 1  // arrive on epi_done after the exp element loop (1) or after the column sums (0).  With 4-column
+                         // batches and the int64 tail, releasing the tensor core before the column-sum transposes is
+                         // 2.5 % faster again (it was 3 % slower with 2-column batches); releasing it inside the
+                         // element loop (after 8 or 12 of the 16 columns) is 17 % slower: FP64 under the MMAs
 #endif
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int KP_MAX = 96;
@@ -173,12 +175,9 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
                                           uint64_t* fp64_done) {
     const double shifter = 6755399441055744.0;  // 1.5 * 2^52
     double racc[4] = {0.0, 0.0, 0.0, 0.0};
-    static_assert(I8_BW <= 4, "row-sum chains");
     // four columns at a time, each step applied across the batch: independent chains
     // side by side for the scheduler (the per-pair chain is ~16 dependent FP64 ops)
     constexpr int BW = I8_BW;
-    // T of column k: registers, or (I8_T_SMEM) this lane's slot of the transpose scratch, which the
-    // element loop overwrites with e v_i for the same column right after reading it
     auto tval = [&](int k) { return T[k]; };
 #pragma unroll
     for (int k0 = 0; k0 < CPT; k0 += BW) {
@@ -200,7 +199,7 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
 #pragma unroll
             for (int b = 0; b < BW; ++b) {
                 if constexpr (MASK) e[b] = (colOff + k0 + b > mask_row) ? e[b] : 0.0;
-                racc[b] = fma(e[b], cd_v[colOff + k0 + b], racc[b]);
+                racc[b & 3] = fma(e[b], cd_v[colOff + k0 + b], racc[b & 3]);
                 scr[(k0 + b) * SCR_LD + lane] = e[b] * v_i;
             }
             continue;
@@ -246,7 +245,7 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
         }
 #pragma unroll
         for (int b = 0; b < BW; ++b) {
-            racc[b] = fma(e[b], cd_v[colOff + k0 + b], racc[b]);
+            racc[b & 3] = fma(e[b], cd_v[colOff + k0 + b], racc[b & 3]);
             scr[(k0 + b) * SCR_LD + lane] = e[b] * v_i;  // column k, row `lane`
         }
     }
@@ -399,7 +398,6 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
             }
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
                 const int s = bq % NSTB;
-                I8_TRACE(lane == 0, bq, 8);
                 tc::mbar_wait_sleep(b_full + s, uint32_t((bq / NSTB) & 1));
                 tc::fence_after();
                 I8_TRACE(lane == 0, bq, 9);
@@ -412,7 +410,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 // FP64 pipe ~4x (probe) to ~8x (in situ), so FP64 work overlapped with MMAs is
                 // nearly wasted; serialising the exp phase is 6 % faster (d = 54 and 90).  The
                 // drain (TMEM loads, integer combination) still overlaps the MMAs.
-                if (!(I8_PROFILE && (A.debug & 32)) && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
+                if (!(I8_PROFILE && (A.debug & 32)) && bq > 0) {
+                    tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
+                }
+                I8_TRACE(lane == 0, bq, 8);  // the previous tile's epilogue has released the tensor core
 #pragma unroll
                 for (int c = NGRP - 1; c >= 0; --c) {
                     if (bq > 0) {
@@ -473,11 +474,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 //   L = 2^24 G_3 + 2^16 G_4 + 2^8 G_5 + G_6   (|L| < 2^47),
                 //   H = 2^24 G_0 + 2^16 G_1 + 2^8 G_2         (|H| < 2^45),
                 // each built as int64 straight into the mantissa field of 1.5 * 2^52 (mad.wide), then
-                // T = H + 2^-24 L = 2^-24 W with one DADD + one DFMA (one rounding).  Live partials stay
-                // small: one int64 (2^8 G_5 + G_6 can exceed int32 for all-128 digits), then the double
-                // L, then 2^8 G_1 + G_2 as int32.  (Pairing (6), (5, 4), (3, 2), (1, 0) measured 3 % slower.)
-                int64_t acc[CPT];
-                int32_t t12[CPT];
+                // T = H + 2^-24 L = 2^-24 W with one DADD + one DFMA (one rounding).  Live partials: one
+                // int64 (2^8 G_5 + G_6 can exceed int32 for all-128 digits), then the double L, then
+                // 1.5 2^52 + 2^16 G_1 + 2^8 G_2 as int64.  (Pairing (6), (5, 4), (3, 2), (1, 0) measured 3 % slower.)
+                int64_t acc[CPT], hp[CPT];
                 double lo[CPT], T[CPT];
                 auto stage = [&](int ca, int cb, auto&& fn) {  // groups ca (completes first) and cb = ca - 1 (or none)
                     // both loads in flight before one wait (TMEM load latency under load ~250 clk)
@@ -508,13 +508,14 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     lo[k] = __longlong_as_double(mad_wide(g3, 1 << 24, mad_wide(g4, 65536, acc[k] + MAGIC)));  // 1.5 2^52 + L
                 });
                 I8_TRACE(etid == 0, tq, 2);
-                stage(2, 1, [&](int k, int32_t g2, int32_t g1) { t12[k] = g1 * 256 + g2; });  // |.| < 2^30
+                // 1.5 2^52 + 2^16 G_1 + 2^8 G_2 (|256 G_1 + G_2| < 2^30), so the tail adds 2^24 G_0 only (+2 %)
+                stage(2, 1, [&](int k, int32_t g2, int32_t g1) { hp[k] = mad_wide(g1 * 256 + g2, 256, MAGIC); });
                 I8_TRACE(etid == 0, tq, 3);
                 stage(0, -1, [&](int k, int32_t g0, int32_t) {
 #if I8_PROBE_NOFP64_T  // profiling only (wrong values): the last drain stage without its two FP64 ops
-                    T[k] = __longlong_as_double(mad_wide(g0, 1 << 24, mad_wide(t12[k], 256, MAGIC)) ^ __double_as_longlong(lo[k]));
+                    T[k] = __longlong_as_double((hp[k] + (int64_t(g0) << 24)) ^ __double_as_longlong(lo[k]));
 #else
-                    T[k] = fma(lo[k], 0x1p-24, __longlong_as_double(mad_wide(g0, 1 << 24, mad_wide(t12[k], 256, MAGIC))) - M2);
+                    T[k] = fma(lo[k], 0x1p-24, __longlong_as_double(hp[k] + (int64_t(g0) << 24)) - M2);
 #endif
                 });
 

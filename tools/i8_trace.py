@@ -32,7 +32,7 @@ buf = np.zeros(64 * 16, dtype=np.int64)
 _diag.check(_diag.LIB.krr_diag_i8_trace(buf.ctypes.data_as(C.c_void_p), buf.size))
 t = buf.reshape(64, 16)
 t0 = t[0, 0]
-names = ["start", "st65", "st43", "st21", "st0", "cd", "exp", "bar", "m:bfull?", "m:bfull", "m:g6", "m:g4", "m:g0",
+names = ["start", "st65", "st43", "st21", "st0", "cd", "exp", "bar", "m:epiw", "m:bfull", "m:g6", "m:g4", "m:g0",
          "elem", "colsum", "g0done"]
 print("tile " + " ".join(f"{nm:>8s}" for nm in names))
 for q in range(1, 40):
