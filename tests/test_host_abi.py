@@ -131,6 +131,24 @@ def test_schedule_covers_each_pair_once(krr, n, world):
     assert max(counts) - min(counts) <= 1
 
 
+def test_schedule_blocked_order_keeps_resident_ctas_on_few_super_tiles(krr):
+    """The CTAs resident at one time (a window of 148 consecutive tiles, one per SM) share
+    their column (J) super-tiles, which K1 streams once per 128-row pass — at most 24 of them,
+    66 MB at n = 1M, d = 90 (2.75 MB each), so they stay in the 126 MB L2 — and their row (I)
+    super-tiles, read once per CTA: at most 48 distinct, each HBM read serving >= 3 CTAs
+    (host.cpp make_schedule; column-major alone gave every resident CTA its own I super-tile)."""
+    st, ns, tiles = krr.schedule(1048576)
+    assert ns == 256
+    full = [tuple(t) for t in tiles if t[0] != t[1]]
+    wa = wb = 0
+    for w0 in range(0, len(full) - 148, 101):
+        win = full[w0:w0 + 148]
+        wa = max(wa, len({a for a, _ in win}))
+        wb = max(wb, len({b for _, b in win}))
+    assert wb <= 24 and wb * 2.75 < 126, wb
+    assert wa <= 48, wa
+
+
 def test_schedule_super_rows(krr):
     assert krr.schedule(8192)[0] == 256
     assert krr.schedule(65536)[0] == 2048
