@@ -78,7 +78,7 @@ int krr_ctx_launch_count(krr_ctx* ctx, int64_t* out);
 
 /* Tuning / diagnostic knobs (no reference equivalent):
  *   "k1_path"     -1|0|1|3  fused mat-vec kernel: auto (default: INT8-slice tensor-core kernel
- *                         where faster: 31 <= d <= 32, 37 <= d <= 96, when the data's exponent range allows, else FP64 DMMA) |
+ *                         where faster: 27 <= d <= 96, when the data's exponent range allows, else FP64 DMMA) |
  *                         FP64 DMMA | tcgen05 INT8 slices | K1-I8X (INT8 slices, exact integer exp argument;
  *                         Gaussian, d <= 96, |x| sqrt(2 scale) < 256; otherwise the request runs the auto choice)
  *   "k1t_path"    -1|0|1  16-column batches of multi-RHS mat-mats / batched PCG: auto (default:

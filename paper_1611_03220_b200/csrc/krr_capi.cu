@@ -279,11 +279,12 @@ bool use_i8(const Ctx& c) {
         const double i8_ms = c.kp8 <= 32 ? 7.49 : (c.kp8 <= 64 ? 9.74 : 11.4);
         return i8_ms < dmma_ms;
     }
-    // Cost model from the measured crossover (n = 65536, profiles/r2_k1_crossover_n65536.log, round 2's
-    // 28-product slices with TS-mode A operands): the DMMA K1 grows ~linearly in d, K1-I8 steps
-    // with the slice width kp = 32 / 64 / 96.
-    const double dmma_ms = 4.40 + 0.1405 * double(c.d);
-    const double i8_ms = c.kp8 <= 32 ? 8.62 : (c.kp8 <= 64 ? 9.57 : 10.73);
+    // Cost model from the measured crossover (n = 65536, profiles/r2_k1_crossover_n65536_final.log, round 2's
+    // final K1-I8: 28-product slices, TS-mode A operands, int64 tail, 4-column exp batches): the DMMA K1
+    // grows linearly in its padded width dp = 4 ceil((d + 2) / 4), K1-I8 steps with the slice width
+    // kp = 32 / 64 / 96.  K1-I8 for 27 <= d <= 96.
+    const double dmma_ms = 3.72 + 0.1439 * double((c.d + 5) / 4 * 4);
+    const double i8_ms = c.kp8 <= 32 ? 7.97 : (c.kp8 <= 64 ? 8.71 : 9.66);
     return i8_ms < dmma_ms;
 }
 

@@ -171,11 +171,11 @@ def test_set_option_rejects_unknown(krr, ctx):
         ctx.set_option("k1_path", 2)
 
 
-@pytest.mark.parametrize("d,want", [(16, 0), (24, 0), (31, 1), (36, 0), (40, 1), (47, 1), (48, 1), (90, 1), (96, 1),
-                                    (97, 0)])
+@pytest.mark.parametrize("d,want", [(16, 0), (24, 0), (26, 0), (27, 1), (31, 1), (33, 1), (36, 1), (40, 1), (90, 1),
+                                    (96, 1), (97, 0)])
 def test_k1_path_auto_selection(krr, oracle, ctx, d, want):
     """Auto path: INT8-slice tensor-core K1 where the measured cost model says it is faster
-    (31 <= d <= 32, 37 <= d <= 96), FP64 DMMA otherwise; both match the oracle."""
+    (27 <= d <= 96), FP64 DMMA otherwise; both match the oracle."""
     n = 600
     x = oracle.random_matrix(n, d, 7)
     v = oracle.random_vector(n, 8)
