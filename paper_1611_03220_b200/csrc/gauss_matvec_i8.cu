@@ -78,6 +78,11 @@ constexpr int NTHR = 32 * (2 + NEPI);
 #define I8_TS 1  // A slices 0 .. nts-1 of the resident I tile copied to the 64 TMEM columns the 7
                  // accumulator groups leave free (tcgen05.cp, once per pass) and used in TS mode
 #endif
+#ifndef I8_REUSE
+#define I8_REUSE 1  // 1: 5 accumulator slots (groups 6..2; groups 1 / 0 reuse the slots of 6 / 5 once the
+                    // epilogue has drained those), so all 7 A slices fit in TMEM (TS mode for every MMA):
+                    // +6 % (the MMA phase is no longer bound by shared-memory operand reads), bitwise unchanged
+#endif
 #ifndef I8_LATE_DRAIN
 #define I8_LATE_DRAIN 0  // 1: drain only after the tile's last group (no TMEM loads while the MMAs run)
 #endif
@@ -86,6 +91,10 @@ constexpr int NTHR = 32 * (2 + NEPI);
                        // prefers high warp ids, so the MMA warp is not starved by the epilogue on its SMSP
 #endif
 constexpr int WARP_PROD = I8_MMA_LAST ? NEPI : 0, WARP_MMA = I8_MMA_LAST ? NEPI + 1 : 1;
+static_assert(!(I8_REUSE && I8_LATE_DRAIN), "groups 1 / 0 wait for the drain of groups 6 / 5");
+// TMEM column slot of accumulator group c
+constexpr int NSLOT = I8_REUSE ? 5 : 7;
+__host__ __device__ constexpr int gslot(int c) { return I8_REUSE ? (c >= 2 ? c - 2 : c + 3) : c; }
 #ifndef I8_BW
 #define I8_BW 4      // columns per exp batch (round 2, with the int64 tail below: 4 beats 2 by 2.5 %, 8 spills)
 #endif
@@ -376,10 +385,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         const uint32_t idesc = tc::idesc_i8(TI, TJ);
         const uint32_t aBase = tc::smem_u32(sA);
         int bq = 0;
-        // TS operands: A slices p < NTS (kp / 4 TMEM columns each) at columns 448 ..
+        // TS operands: A slices p < NTS (kp / 4 TMEM columns each) after the accumulator slots
         constexpr int COLS_A = kp / 4;
-        constexpr int NTS = I8_TS ? ((TMEM_COLS - NGRP * TJ) / COLS_A < P ? (TMEM_COLS - NGRP * TJ) / COLS_A : P) : 0;
-        const uint32_t tA = tmem_base + uint32_t(NGRP * TJ);
+        constexpr int NTS = I8_TS ? ((TMEM_COLS - NSLOT * TJ) / COLS_A < P ? (TMEM_COLS - NSLOT * TJ) / COLS_A : P) : 0;
+        const uint32_t tA = tmem_base + uint32_t(NSLOT * TJ);
         for (int it = 0; it < nTI; ++it) {
             tc::mbar_wait_sleep(a_full, uint32_t(it & 1));
             tc::fence_after();
@@ -416,8 +425,14 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 I8_TRACE(lane == 0, bq, 8);  // the previous tile's epilogue has released the tensor core
 #pragma unroll
                 for (int c = NGRP - 1; c >= 0; --c) {
-                    if (bq > 0) {
-                        tc::mbar_wait_sleep(g_empty + c, uint32_t((bq - 1) & 1));
+                    if (I8_REUSE && c < 2) {
+                        // slot of group 6 / 5 of this tile: wait for the epilogue's drain of it
+                        tc::mbar_wait_sleep(g_empty + (c == 1 ? 6 : 5), uint32_t(bq & 1));
+                        tc::fence_after();
+                    } else if (bq > 0) {
+                        // the previous tile's drain of the group that last used this slot
+                        const int prev = I8_REUSE ? (c == 6 ? 1 : (c == 5 ? 0 : c)) : c;
+                        tc::mbar_wait_sleep(g_empty + prev, uint32_t((bq - 1) & 1));
                         tc::fence_after();
                     }
                     if (c == NGRP - 1 || c == 4 || c == 0) I8_TRACE(lane == 0, bq, c == NGRP - 1 ? 10 : (c == 4 ? 11 : 12));
@@ -429,10 +444,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                                 for (int ks = 0; ks < ksteps; ++ks) {
                                     const uint64_t db = dB0 + uint64_t(((c - p) * TJ * kp + ks * 256) >> 4);
                                     if (p < NTS)
-                                        tc::mma_i8_ts(tmem_base + uint32_t(c * TJ), tA + uint32_t(p * COLS_A + ks * 8), db,
+                                        tc::mma_i8_ts(tmem_base + uint32_t(gslot(c) * TJ), tA + uint32_t(p * COLS_A + ks * 8), db,
                                                       idesc, (p == 0 && ks == 0) ? 0u : 1u);
                                     else
-                                        tc::mma_i8(tmem_base + uint32_t(c * TJ), dA0 + uint64_t((p * TI * kp + ks * 256) >> 4),
+                                        tc::mma_i8(tmem_base + uint32_t(gslot(c) * TJ), dA0 + uint64_t((p * TI * kp + ks * 256) >> 4),
                                                    db, idesc, (p == 0 && ks == 0) ? 0u : 1u);
                                 }
                         tc::mma_commit(g_full + c);
@@ -485,11 +500,11 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                     tc::mbar_wait_sleep(g_full + ca, ph);
                     tc::fence_after();
                     if (ca == 0) I8_TRACE(etid == 0, tq, 15);  // the tile's last MMA group is complete
-                    tc::tmem_ld16(taddr + uint32_t(ca * TJ), ga);
+                    tc::tmem_ld16(taddr + uint32_t(gslot(ca) * TJ), ga);
                     if (cb >= 0) {
                         tc::mbar_wait_sleep(g_full + cb, ph);
                         tc::fence_after();
-                        tc::tmem_ld16(taddr + uint32_t(cb * TJ), gb);
+                        tc::tmem_ld16(taddr + uint32_t(gslot(cb) * TJ), gb);
                     }
                     tc::tmem_wait_ld();
 #pragma unroll
