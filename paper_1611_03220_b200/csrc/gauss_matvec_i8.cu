@@ -525,7 +525,6 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 I8_TRACE(etid == 0, tq, 2);
                 // 1.5 2^52 + 2^16 G_1 + 2^8 G_2 (|256 G_1 + G_2| < 2^30), so the tail adds 2^24 G_0 only (+2 %)
                 stage(2, 1, [&](int k, int32_t g2, int32_t g1) { hp[k] = mad_wide(g1 * 256 + g2, 256, MAGIC); });
-
                 I8_TRACE(etid == 0, tq, 3);
                 stage(0, -1, [&](int k, int32_t g0, int32_t) {
 #if I8_PROBE_NOFP64_T  // profiling only (wrong values): the last drain stage without its two FP64 ops
