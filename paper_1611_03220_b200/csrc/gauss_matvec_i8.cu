@@ -72,7 +72,8 @@ constexpr int NEPI = 16;  // epilogue warps (4 per TMEM lane quarter)
 constexpr int CPT = 16;   // columns per epilogue thread (one tcgen05.ld x16 per group)
 constexpr int NTHR = 32 * (2 + NEPI);
 #ifndef I8_PROFILE
-#define I8_PROFILE 1  // 0: compile out the profiling modes (debug bits 1, 2, 16, 32; the trace stays)
+#define I8_PROFILE 0  // 1: compile in the profiling modes (debug bits 1, 2, 16, 32; the trace is always there);
+                      // build them with tools/build_variant.py ... -DI8_PROFILE=1 (the lean build is 1-2 % faster)
 #endif
 #ifndef I8_TS
 #define I8_TS 1  // A slices 0 .. nts-1 of the resident I tile copied to the 64 TMEM columns the 7
@@ -96,7 +97,8 @@ static_assert(!(I8_REUSE && I8_LATE_DRAIN), "groups 1 / 0 wait for the drain of 
 constexpr int NSLOT = I8_REUSE ? 5 : 7;
 __host__ __device__ constexpr int gslot(int c) { return I8_REUSE ? (c >= 2 ? c - 2 : c + 3) : c; }
 #ifndef I8_BW
-#define I8_BW 4      // columns per exp batch (round 2, with the int64 tail below: 4 beats 2 by 2.5 %, 8 spills)
+#define I8_BW 8      // columns per exp batch: with the int64 tail, 4 beat 2 by 2.5 %; with all A slices in TMEM and
+                     // the lean build, 8 beats 4 by 1-2 % (4 row-sum chains either way: bitwise the same K v)
 #endif
 #ifndef I8_EARLY_DONE
 #define I8_EARLY_DONE 1  // arrive on epi_done after the exp element loop (1) or after the column sums (0).  With 4-column
