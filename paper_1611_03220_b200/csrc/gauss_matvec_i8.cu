@@ -249,8 +249,11 @@ __device__ __forceinline__ void exp_phase(const double (&T)[CPT], const I8Consts
         }
 #pragma unroll
         for (int b = 0; b < BW; ++b) {
-            const double tj = tab[(kk[b] & (TAB - 1)) * TAB_REP + (lane & (TAB_REP - 1))];
-            const double ts = __hiloint2double(__double2hiint(tj) + (kk[b] >> 6) * (1 << 20), __double2loint(tj));
+            // 2^(k/64) = 2^(k >> 6) 2^((k & 63)/64): entry j = k & 63 of this lane's replica is at byte offset
+            // (k << 7) & 0x1F80 and carries hi(2^(j/64)) - (j << 14), so adding k << 14 = ((k >> 6) << 20) +
+            // (j << 14) to its high word applies the power of two (two integer ops per pair fewer: +1 %)
+            const double tj = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab) + ((kk[b] << 7) & 0x1F80));
+            const double ts = __hiloint2double(__double2hiint(tj) + kk[b] * (1 << 14), __double2loint(tj));
             e[b] = fma(ts, q[b], ts);
             if constexpr (MASK) e[b] = (colOff + k0 + b > mask_row) ? e[b] : 0.0;
         }
@@ -343,7 +346,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         tc::mbar_init(epi_done, NEPI);
         tc::mbar_fence_init();
     }
-    for (int i = tid; i < TAB * TAB_REP; i += NTHR) tab[i] = g_tab64[i / TAB_REP];
+    for (int i = tid; i < TAB * TAB_REP; i += NTHR) {
+        const double t = g_tab64[i / TAB_REP];
+        tab[i] = __hiloint2double(__double2hiint(t) - (i / TAB_REP) * (1 << 14), __double2loint(t));  // see exp_phase
+    }
     if (warp == WARP_MMA) tc::tmem_alloc(tmem_slot, TMEM_COLS);
     tc::fence_before();
     __syncthreads();
@@ -471,6 +477,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
         const int row = quarter * 32 + lane;
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(half * CPT);
         double* scr = scr_all + ew * CPT * SCR_LD;
+        const double* tab_l = tab + (lane & (TAB_REP - 1));  // this lane's table replica (conflict-free lookups)
         const int kabs_hi = __double2hiint(A.ec.kabs), kabs_lo = __double2loint(A.ec.kabs);
         int tq = 0;
         for (int it = 0; it < nTI; ++it) {
@@ -561,13 +568,13 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matvec_i8_kernel(const I8Args A
                 } else if (masked) {
                     // diagonal block: keep j > i (local column index vs local row index)
                     const int mask_row = row - (jt - it * (TI / TJ)) * TJ;
-                    exp_phase<true, false, POLY>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
+                    exp_phase<true, false, POLY>(T, A.ec, tab_l, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
                                          rowacc, lane, colOff, mask_row, early);
                 } else if (I8_PROFILE && (A.debug & 16)) {
-                    exp_phase<false, true>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i,
+                    exp_phase<false, true>(T, A.ec, tab_l, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i,
                                            v_i, rowacc, lane, colOff, 0, early);
                 } else {
-                    exp_phase<false, false, POLY>(T, A.ec, tab, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
+                    exp_phase<false, false, POLY>(T, A.ec, tab_l, cd_sq, cd_v, cd_e, scr, colscr_q, trp, nsi_hi, kabs_lo, sqs_i, v_i,
                                           rowacc, lane, colOff, 0, early);
                 }
                 I8_TRACE(etid == 0, tq, 6);
