@@ -274,10 +274,10 @@ bool use_i8x(const Ctx& c);
 bool use_i8(const Ctx& c) {
     if (!c.i8_ready || use_i8x(c)) return false;
     if (c.k1_path >= 0) return c.k1_path == 1;
-    if (c.family != 0) {  // polynomial kernel (cheaper epilogue): profiles/r1_poly_k1_crossover_n65536.log
-        const double dmma_ms = 2.1 + 0.14 * double(c.d);
-        const double i8_ms = c.kp8 <= 32 ? 7.49 : (c.kp8 <= 64 ? 9.74 : 11.4);
-        return i8_ms < dmma_ms;
+    if (c.family != 0) {  // polynomial kernel (cheaper epilogue): profiles/r2_poly_k1_crossover_n65536.log
+        const double dmma_ms = 2.22 + 0.1408 * double(c.d);
+        const double i8_ms = c.kp8 <= 32 ? 6.91 : (c.kp8 <= 64 ? 7.36 : 7.75);
+        return i8_ms < dmma_ms;  // K1-I8 for 37 <= d <= 96
     }
     // Cost model from the measured crossover (n = 65536, profiles/r2_k1_crossover_n65536_final.log, round 2's
     // final K1-I8: 28-product slices, TS-mode A operands, int64 tail, 4-column exp batches): the DMMA K1

@@ -332,3 +332,17 @@ def test_poly_matvec_on_int8_tensor_cores(krr, oracle, ctx, n, d, g, c, q):
             ctx.set_option("k1_path", -1)
         assert np.max(np.abs(got[path] - want) / scale) <= 1e-12 * q, (path, np.max(np.abs(got[path] - want) / scale))
     assert np.max(np.abs(got[1] - got[0]) / scale) <= 2e-12 * q
+
+
+@pytest.mark.parametrize("d,want", [(16, 0), (32, 0), (36, 0), (40, 1), (64, 1), (90, 1), (97, 0)])
+def test_poly_auto_path_follows_the_measured_crossover(krr, oracle, ctx, d, want):
+    """Auto path for the polynomial kernel: K1-I8 for 37 <= d <= 96 (krr_capi.cu use_i8, cost model from
+    profiles/r2_poly_k1_crossover_n65536.log), the DMMA K1 otherwise; both within the oracle's bar."""
+    n, g, c, q = 700, 1.0 / d, 1.0, 3
+    x = oracle.random_matrix(n, d, 3 + d)
+    v = oracle.random_vector(n, 4 + d)
+    op = krr.KernelOperator(x, _pk(krr, g, c, q), 0.5, ctx=ctx)
+    assert ctx.get_option("k1_path_effective") == want
+    k = oracle.poly_gram(x, g, c, q)
+    scale = np.abs(k) @ np.abs(v) + 0.5 * np.abs(v)
+    assert np.max(np.abs(op(v) - (k @ v + 0.5 * v)) / scale) <= 1e-12 * q

@@ -12,7 +12,7 @@ from paper_1611_03220_b200 import _lib  # noqa: E402
 
 n = 65536
 ctx = krr.Context(0)
-for d in (8, 16, 24, 32, 40, 48, 64, 90):
+for d in [int(a) for a in sys.argv[1:]] or (8, 16, 24, 32, 40, 48, 64, 90):
     x = np.random.default_rng(d).standard_normal((n, d)) / np.sqrt(d)
     row = {"d": d}
     for path in (0, 1):
