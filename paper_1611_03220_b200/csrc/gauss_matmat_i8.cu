@@ -72,6 +72,9 @@ constexpr int TAB = 64;
 constexpr int TAB_REP = 16;
 constexpr int YMIN_K = -1022 * TAB;
 constexpr int KP_MAX = 448;
+#ifndef MI8_BW
+#define MI8_BW 2  // columns per exp batch
+#endif
 #ifndef MI8_TS
 #define MI8_TS 4  // A slices 0 .. MI8_TS-1 of each K chunk copied to TMEM (tcgen05.cp) and used in TS
                   // mode: the 64 TMEM columns the 7 accumulator groups leave free hold two chunks x 4
@@ -190,7 +193,10 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
         tc::mbar_init(epi_done, NEPI);
         tc::mbar_fence_init();
     }
-    for (int i = tid; i < TAB * TAB_REP; i += NTHR) tab[i] = A.tab64[i / TAB_REP];
+    for (int i = tid; i < TAB * TAB_REP; i += NTHR) {  // entry j carries hi(2^(j/64)) - (j << 14) (K1-I8's table)
+        const double t = A.tab64[i / TAB_REP];
+        tab[i] = __hiloint2double(__double2hiint(t) - (i / TAB_REP) * (1 << 14), __double2loint(t));
+    }
     if (warp == WARP_MMA) tc::tmem_alloc(tmem_slot, TMEM_COLS);
     tc::fence_before();
     __syncthreads();
@@ -340,6 +346,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
         const int ew = MI8_MMA_LAST ? warp : warp - 2;  // 0..15
         const int quarter = warp & 3;  // TMEM lane quarter
         const int half = ew >> 2;      // which 16 of the 64 columns (exp phase)
+        const double* tab_l = tab + (lane & (TAB_REP - 1));  // this lane's table replica
         const int etid = ew * 32 + lane;
         const int row = quarter * 32 + lane;
         const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(half * CPT);
@@ -435,38 +442,39 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     for (int k = 0; k < CPT; ++k) sE[e_idx(row, colOff + k)] = T[k];
                 } else
 #pragma unroll
-                for (int k0 = 0; k0 < CPT; k0 += 2) {
-                    double y[2], t2[2], f[2], q[2];
-                    int kk[2];
+                for (int k0 = 0; k0 < CPT; k0 += MI8_BW) {
+                    double y[MI8_BW], t2[MI8_BW], f[MI8_BW], q[MI8_BW];
+                    int kk[MI8_BW];
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) {
+                    for (int b = 0; b < MI8_BW; ++b) {
                         const int cl = colOff + k0 + b;
                         const double nscale = __hiloint2double(nsi_hi + cd_e[cl], kabs_lo);
                         y[b] = fma(T[k0 + b], nscale, sqs_i + cd_sq[cl]);
                         y[b] = __hiloint2double(min(__double2hiint(y[b]), 0), __double2loint(y[b]));
                     }
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) t2[b] = y[b] + shifter;
+                    for (int b = 0; b < MI8_BW; ++b) t2[b] = y[b] + shifter;
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) f[b] = y[b] - (t2[b] - shifter);
+                    for (int b = 0; b < MI8_BW; ++b) f[b] = y[b] - (t2[b] - shifter);
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) q[b] = fma(f[b], A.a5, A.a4);
+                    for (int b = 0; b < MI8_BW; ++b) q[b] = fma(f[b], A.a5, A.a4);
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) q[b] = fma(q[b], f[b], A.a3);
+                    for (int b = 0; b < MI8_BW; ++b) q[b] = fma(q[b], f[b], A.a3);
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) q[b] = fma(q[b], f[b], A.a2);
+                    for (int b = 0; b < MI8_BW; ++b) q[b] = fma(q[b], f[b], A.a2);
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) q[b] = fma(q[b], f[b], A.a1);
+                    for (int b = 0; b < MI8_BW; ++b) q[b] = fma(q[b], f[b], A.a1);
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) {
+                    for (int b = 0; b < MI8_BW; ++b) {
                         q[b] = q[b] * f[b];
                         kk[b] = max(__double2loint(t2[b]), YMIN_K);
                     }
 #pragma unroll
-                    for (int b = 0; b < 2; ++b) {
-                        const double tj = tab[(kk[b] & (TAB - 1)) * TAB_REP + (lane & (TAB_REP - 1))];
-                        const double ts =
-                            __hiloint2double(__double2hiint(tj) + (kk[b] >> 6) * (1 << 20), __double2loint(tj));
+                    for (int b = 0; b < MI8_BW; ++b) {
+                        // K1-I8's lookup: byte offset (k << 7) & 0x1F80 in this lane's replica, k << 14 on the high word
+                        const double tj = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab_l) +
+                                                                           ((kk[b] << 7) & 0x1F80));
+                        const double ts = __hiloint2double(__double2hiint(tj) + kk[b] * (1 << 14), __double2loint(tj));
                         double e = fma(ts, q[b], ts);
                         const int cl = colOff + k0 + b;
                         if (masked) e = (cl > mask_row) ? e : 0.0;
