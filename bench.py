@@ -25,6 +25,9 @@ roofline: dominant kernel = K1.  The default path at d = 90 is K1-I8 (tcgen05 ki
 config5_pass: informational, N = 1 only (--no-config5 skips it): one (K + lambda I) V pass at
           BASELINE config 5 (n = 524288, d = 440, t = 16) through krr_kernel_matvec with host
           buffers, on K1T-I8 (INT8-slice dot products + DMMA E.V) and on the DMMA K1T.
+rank_split: informational, N = 1 only (--no-rank-split skips it): the config-4 K1 work split of
+          2 / 4 / 8 ranks, each rank's share timed on this GPU one rank at a time (rank emulation),
+          and the compute-side strong-scaling efficiency it allows; the all-reduce is modelled.
 pcg_leg:  config 4's time to tolerance on the device, bounded: the full train path (RFF
           features, Woodbury build split into Z^T Z / Cholesky / U = L^-1 Z^T, then --pcg-iters
           graph-resident PCG iterations), mean ms per iteration, K1's share of it, the
@@ -70,6 +73,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the optional fp32-mode measurement")
     ap.add_argument("--no-config5", action="store_true", help="skip the config-5 multi-RHS pass (K1T-I8 vs DMMA K1T)")
+    ap.add_argument("--no-rank-split", action="store_true",
+                    help="skip the emulated 2/4/8-rank K1 work split (N = 1 only)")
     ap.add_argument("--time-to-tol", type=int, default=0, metavar="CFG",
                     help="also run the full train (RFF + precond + PCG) of BASELINE config CFG")
     ap.add_argument("--pcg-iters", type=int, default=3,
@@ -386,6 +391,14 @@ def main():
     if world == 1 and not args.no_config5:
         c5 = config5_pass(krr, _lib, local)
 
+    # ---- the K1 work split of 2 / 4 / 8 ranks, emulated on this GPU (N = 1 only)
+    split = None
+    if world == 1 and not args.no_rank_split and args.n == CFG4["n"]:
+        try:
+            split = rank_split(krr, _lib, x, sigma, lam, local, k1.value)
+        except Exception as e:  # informational leg: reported, not fatal
+            split = {"error": f"{type(e).__name__}: {e}"}
+
     # ---- optional time-to-tolerance (full train on the device)
     ttt = None
     if args.time_to_tol:
@@ -500,6 +513,8 @@ def main():
         line["fp32_mode"] = f32
     if c5:
         line["config5_pass"] = c5
+    if split:
+        line["rank_split"] = split
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -550,6 +565,40 @@ def config5_pass(krr, _lib, device: int) -> dict:
                                        np.linalg.norm(out["k1t_dmma"]))
     res["rhs_gevals_per_s"] = float(n) * n * t / res["k1t_i8"] / 1e9
     return res
+
+
+def rank_split(krr, _lib, x, sigma: float, lam: float, device: int, k1_full_ms: float,
+               worlds=(2, 4, 8)) -> dict:
+    """The config-4 K1 work split of W ranks, measured on this one GPU (rank emulation: rank r of W
+    runs exactly its share of the symmetric super-tile schedule — its tiles, its owned slots, the
+    diagonal on rank 0 — with no collective; B200_PROFILING: fewer GPUs than ranks -> emulate the
+    ranks one at a time, never concurrently).  Per W: every rank's K1 time (CUDA events), and the
+    compute-side strong-scaling efficiency k1_full / (W * max_r k1_r) that the driver's N-GPU run
+    can reach before the all-reduce, whose cost is modelled, not measured (one GPU here)."""
+    n, d = x.shape
+    out = {"method": "emulated ranks, one at a time on one B200 (emulate_world / emulate_rank); "
+                     "the all-reduce of n doubles per mat-vec is a model at 700 GB/s NVLink bus bandwidth",
+           "k1_full_ms": k1_full_ms}
+    c = krr.Context(device)
+    try:
+        for W in worlds:
+            c.set_option("emulate_world", W)
+            per = []
+            for r in range(W):
+                c.set_option("emulate_rank", r)
+                _lib.check(_lib.LIB.krr_set_data(c.handle, _lib.ptr(x), n, d, sigma))
+                tot, k1 = C.c_double(), C.c_double()
+                _lib.check(_lib.LIB.krr_bench_matvec(c.handle, lam, 1, C.byref(tot), C.byref(k1)))  # warm
+                _lib.check(_lib.LIB.krr_bench_matvec(c.handle, lam, 1, C.byref(tot), C.byref(k1)))
+                per.append(k1.value)
+            ar_ms = 2.0 * (W - 1) / W * 8.0 * n / 700e9 * 1e3
+            out[str(W)] = {"k1_ms_per_rank": per, "max_ms": max(per), "mean_ms": sum(per) / W,
+                           "compute_efficiency": k1_full_ms / (W * max(per)),
+                           "allreduce_model_ms": ar_ms,
+                           "projected_efficiency": k1_full_ms / (W * (max(per) + ar_ms))}
+    finally:
+        c.close()
+    return out
 
 
 def hbm_peak() -> float:
