@@ -41,3 +41,27 @@ def test_rank_emulation_rejects_bad_values(krr, ctx):
         ctx.set_option("emulate_rank", -1)
     with pytest.raises(krr.InvalidArgument):
         ctx.set_option("emulate_rank", 0.5)
+
+
+@pytest.mark.parametrize("n,d,world", [(5000, 90, 3), (40000, 90, 8)])
+def test_rank_partials_fp32_mode(krr, oracle, ctx, n, d, world):
+    """The optional fp32 mode (K1-F32) on the multi-rank schedule: bench.py also measures it at
+    N > 1, so rank r's partial must follow the same owned-slot / diagonal rules."""
+    x = oracle.random_matrix(n, d, 7)
+    v = oracle.random_matrix(n, 1, 8)
+    kern = krr.KernelSpec.gaussian(6.0)
+    ctx.set_precision(32)
+    try:
+        full = krr.KernelOperator(x, kern, 1e-3, ctx=ctx).matmat(v)
+        acc = np.zeros_like(full)
+        ctx.set_option("emulate_world", world)
+        for r in range(world):
+            ctx.set_option("emulate_rank", r)
+            acc += krr.KernelOperator(x, kern, 1e-3, ctx=ctx).matmat(v)
+    finally:
+        ctx.set_option("emulate_world", 1)
+        ctx.set_option("emulate_rank", 0)
+        ctx.set_precision(64)
+    # per-rank partials are fp32-accurate sums; their fp64 sum matches the one-rank result to
+    # the fp32 mode's own accuracy
+    assert rel(acc, full) <= 1e-6, rel(acc, full)
