@@ -79,6 +79,8 @@ def parse():
                     help="also run the full train (RFF + precond + PCG) of BASELINE config CFG")
     ap.add_argument("--pcg-iters", type=int, default=3,
                     help="config-4 PCG leg: iterations timed after the full build (0 = skip)")
+    ap.add_argument("--leg-timeout", type=float, default=600.0,
+                    help="multi-rank runs: seconds before the PCG leg is abandoned and the measured line printed")
     ap.add_argument("--no-c1-reference", action="store_true",
                     help="--impl reference: skip the 1-core dense config-1 timing")
     ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (no GPU work)")
@@ -114,6 +116,24 @@ def maybe_spawn(args) -> None:
 I8_PRODUCTS = 28
 
 # ----------------------------------------------------------------------------- plumbing
+def arm_watchdog(seconds: float, rank: int, line: dict):
+    """Multi-rank only: if the leg that follows does not return within `seconds`, rank 0 prints the
+    already measured line (the leg marked as abandoned) and every rank leaves the process."""
+    import threading
+
+    def fire():
+        if rank == 0:
+            out = dict(line)
+            out["pcg_leg"] = {"error": f"multi-rank PCG leg did not finish within {seconds:.0f} s; abandoned"}
+            print(json.dumps(out), flush=True)
+        os._exit(0)
+
+    t = threading.Timer(seconds, fire)
+    t.daemon = True
+    t.start()
+    return t
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -399,19 +419,6 @@ def main():
         except Exception as e:  # informational leg: reported, not fatal
             split = {"error": f"{type(e).__name__}: {e}"}
 
-    # ---- optional time-to-tolerance (full train on the device)
-    ttt = None
-    if args.time_to_tol:
-        ttt = time_to_tol(krr, ctx, args.time_to_tol)
-
-    # ---- config 4 time-to-tolerance leg (bounded) and the full config-1 train
-    pcg = None
-    if args.pcg_iters > 0 and args.n == CFG4["n"]:
-        try:
-            pcg = pcg_leg(krr, ctx, D, args.pcg_iters, k1.value)  # k1: mean ms per K1 launch
-        except Exception as e:  # reported, not fatal: the mat-vec line stands on its own
-            pcg = {"error": f"{type(e).__name__}: {e}"}
-
     # ---- roofline bookkeeping
     st, ns, tiles = krr.schedule(n, world, rank)
     pairs_rank = 0
@@ -504,10 +511,6 @@ def main():
     }
     if cpu:
         line["cpu_baseline"] = cpu
-    if ttt:
-        line["time_to_tol"] = ttt
-    if pcg:
-        line["pcg_leg"] = pcg
     line["ranks"] = rank_info
     if f32:
         line["fp32_mode"] = f32
@@ -515,6 +518,28 @@ def main():
         line["config5_pass"] = c5
     if split:
         line["rank_split"] = split
+
+    # ---- optional time-to-tolerance (full train on the device)
+    ttt = None
+    if args.time_to_tol:
+        ttt = time_to_tol(krr, ctx, args.time_to_tol)
+
+    # ---- config 4 time-to-tolerance leg (bounded) and the full config-1 train.  Last, and on
+    # multi-rank runs under a watchdog: its collectives inside the captured PCG loop are the one
+    # part a single-GPU box cannot exercise, so a stall must not cost the measured line above
+    pcg = None
+    if args.pcg_iters > 0 and args.n == CFG4["n"]:
+        dog = arm_watchdog(args.leg_timeout, rank, line) if world > 1 else None
+        try:
+            pcg = pcg_leg(krr, ctx, D, args.pcg_iters, k1.value)  # k1: mean ms per K1 launch
+        except Exception as e:  # reported, not fatal: the mat-vec line stands on its own
+            pcg = {"error": f"{type(e).__name__}: {e}"}
+        if dog:
+            dog.cancel()
+    if ttt:
+        line["time_to_tol"] = ttt
+    if pcg:
+        line["pcg_leg"] = pcg
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

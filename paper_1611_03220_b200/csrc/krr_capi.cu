@@ -8,6 +8,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -677,7 +678,10 @@ struct PcgOut {
 // one-thread control kernel makes solver.cpp:37-52's stop / breakdown decision on the device.
 // No host observer (any world size).  Precondition: the caller ran the prologue (x = 0, r = y,
 // z = M r, p = z, scal[2] = r'z) and norm_y > 0.
-void pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double norm_y, double tau, int max_iter,
+// Returns false — and leaves the vectors of the prologue untouched — only when a multi-rank context
+// cannot build the graph (the captured NCCL collectives are the one part no single-GPU run can
+// exercise): every rank fails the same way, reports it on stderr and takes the host-driven loop.
+bool pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double norm_y, double tau, int max_iter,
                     double* hist, PcgOut& out) {
     if (c.precision == 32) f32_ensure(c);  // one-off preparation synchronises: not inside the capture
     use_i8T1(c);                            // (same for the large-d single-column K1T-I8 route)
@@ -702,6 +706,7 @@ void pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double no
             if (g) cudaGraphDestroy(g);
         }
     } cleanup{g, exec};
+    try {
     KRR_CUDA(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle cond;
     KRR_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
@@ -733,6 +738,14 @@ void pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double no
     }
     KRR_CUDA(cudaStreamEndCapture(c.stream, &body));
     KRR_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    } catch (const Error& e) {
+        if (c.world <= 1) throw;  // single-GPU contexts: the graph loop is tested, a failure is a bug
+        cudaGetLastError();
+        std::fprintf(stderr, "krr: rank %d: graph-resident PCG loop unavailable (%s); using the host-driven loop\n",
+                     c.rank, e.what());
+        c.pcg_graph = false;
+        return false;
+    }
     KRR_CUDA(cudaGraphLaunch(exec, c.stream));
     int hctl[4];
     double* hs = c.hscal->p;
@@ -749,6 +762,7 @@ void pcg_graph_loop(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, double no
     out.iterations = its;
     out.final_residual = hs[6];
     out.converged = hctl[1] == 1 ? 1 : 0;
+    return true;
 }
 
 // device_ops: A and M only enqueue device work on c.stream (no host callbacks, no host
@@ -789,8 +803,7 @@ PcgOut pcg_core(Ctx& c, int64_t n, const DevOp& A, const DevOp* M, const double*
     // every stop decision is made from all-reduced (rank-identical) vectors, so all ranks run the
     // same number of iterations without a host round trip
     if (device_ops && c.pcg_graph && !obs) {
-        pcg_graph_loop(c, n, A, M, norm_y, tau, max_iter, hist, out);
-        return out;
+        if (pcg_graph_loop(c, n, A, M, norm_y, tau, max_iter, hist, out)) return out;
     }
     int cur = 0;
     for (int it = 1; it <= max_iter; ++it) {
