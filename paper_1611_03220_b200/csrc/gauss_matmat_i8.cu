@@ -61,7 +61,13 @@ constexpr int NTHR = 32 * (2 + NEPI);
 #endif
 constexpr int WARP_PROD = MI8_MMA_LAST ? NEPI : 0, WARP_MMA = MI8_MMA_LAST ? NEPI + 1 : 1;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int NSTG = 2;                 // K-chunk ring stages
+#ifndef MI8_NSTG
+#define MI8_NSTG 2  // K-chunk ring stages (3 needs MI8_TAB_REP = 8 to fit the 227 KB)
+#endif
+#ifndef MI8_TAB_REP
+#define MI8_TAB_REP 16
+#endif
+constexpr int NSTG = MI8_NSTG;          // K-chunk ring stages
 constexpr int A_CH = P * TI * 32;       // 28 KB
 constexpr int B_CH = P * TJ * 32;       // 14 KB
 constexpr int STG_BYTES = A_CH + B_CH;  // 42 KB
@@ -69,7 +75,7 @@ constexpr int ELD = 68;                 // E tile row stride (doubles), = 4 (mod
 constexpr int NCD = 2;                  // column-data stages (sq', e_j << 20)
 constexpr int CD_BYTES = TJ * 8 + TJ * 4;
 constexpr int TAB = 64;
-constexpr int TAB_REP = 16;
+constexpr int TAB_REP = MI8_TAB_REP;
 constexpr int YMIN_K = -1022 * TAB;
 constexpr int KP_MAX = 448;
 #ifndef MI8_BW
@@ -103,7 +109,7 @@ constexpr size_t OFF_BARS = OFF_TAB + size_t(TAB) * TAB_REP * 8;
 constexpr int NBARS = 2 * NSTG * P + 2 * NCD + 2 * NGRP + 1;
 constexpr size_t SMEM = OFF_BARS + NBARS * 8 + 16;
 static_assert(SMEM <= 227 * 1024, "K1T-I8 shared memory");
-static_assert(NGRP * TJ + NSTG * MI8_TS * 8 <= TMEM_COLS, "K1T-I8 TMEM: accumulators + TS operand buffers");
+static_assert(NGRP * TJ + 2 * MI8_TS * 8 <= TMEM_COLS, "K1T-I8 TMEM: accumulators + TS operand buffers");
 
 // profiling trace (debug bit 2): clock64 stamps of CTA 0, 16 per tile, first 32 tiles
 constexpr int MTRACE_TILES = 32;
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
     if (warp == WARP_PROD) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
-            int bq = 0;
+            int bq = 0, cc = 0;  // cc: running K-chunk count (ring position)
             int uses[NSTG] = {};
             for (int it = 0; it < nTI; ++it) {
                 const int64_t r0 = rowBase + int64_t(it) * TI;
@@ -218,8 +224,8 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     uint8_t* cd = sCD + cs * CD_BYTES;
                     tc::bulk_g2s(cd, A.sqs + c0, TJ * 8, cd_full + cs);
                     tc::bulk_g2s(cd + TJ * 8, A.ejs + c0, TJ * 4, cd_full + cs);
-                    for (int ks = 0; ks < KS; ++ks) {
-                        const int s = ks % NSTG;
+                    for (int ks = 0; ks < KS; ++ks, ++cc) {
+                        const int s = cc % NSTG;
                         if (ks == 0) MI8_TRACE(true, bq, 12);
                         uint8_t* st = sStg + s * STG_BYTES;
                         if (MI8_SLICEBAR && !MI8_BIGCOPY) {
@@ -260,15 +266,15 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
     } else if (warp == WARP_MMA) {
         // ------------------------------------------------------------ MMA issuer
         const uint32_t idesc = tc::idesc_i8(TI, TJ);
-        int bq = 0;
+        int bq = 0, cc = 0;
         int uses[NSTG] = {};
         for (int it = 0; it < nTI; ++it) {
             for (int jt = diag ? it * (TI / TJ) : 0; jt < nTJ; ++jt, ++bq) {
                 // time-multiplexed with the previous tile's FP64 phase (exp + DMMA)
                 if (MI8_TMUX == 1 && bq > 0) tc::mbar_wait_sleep(epi_done, uint32_t((bq - 1) & 1));
                 MI8_TRACE(lane == 0, bq, 8);
-                for (int ks = 0; ks < KS; ++ks) {
-                    const int s = ks % NSTG;
+                for (int ks = 0; ks < KS; ++ks, ++cc) {
+                    const int s = cc % NSTG;
                     constexpr bool SB = MI8_SLICEBAR && !MI8_BIGCOPY;
                     const uint32_t ph = uint32_t(uses[s] & 1);
                     if (!SB) tc::mbar_wait_sleep(s_full + s, ph);
@@ -279,10 +285,15 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     const uint64_t dA0 = tc::smem_desc(sbase, 128, 256);
                     const uint64_t dB0 = tc::smem_desc(sbase + A_CH, 128, 256);
                     const bool last = (ks == KS - 1);
-                    // TS operands of this chunk into the stage's TMEM buffer (the stage is reused only after
-                    // the chunk two back completed, so the buffer is free; tcgen05 ops of one thread run in order)
-                    const uint32_t abuf = tmem_base + uint32_t(NGRP * TJ) + uint32_t(s * MI8_TS * 8);
+                    // TS operands of this chunk into one of two TMEM buffers, free once the chunk two back
+                    // completed: with a 2-stage ring the stage's own refill implies that; a deeper ring
+                    // waits for that chunk's s_empty commit here (mma -> cp is not a pipelined tcgen05 pair)
+                    const uint32_t abuf = tmem_base + uint32_t(NGRP * TJ) + uint32_t((cc & 1) * MI8_TS * 8);
                     if (!SB && MI8_TS > 0) {
+                        if (NSTG > 2 && cc >= 2) {
+                            tc::mbar_wait_sleep(s_empty + (cc - 2) % NSTG, uint32_t(((cc - 2) / NSTG) & 1));
+                            tc::fence_after();
+                        }
                         if (tc::elect_one())
 #pragma unroll
                             for (int p = 0; p < MI8_TS; ++p)
@@ -473,7 +484,7 @@ __global__ void __launch_bounds__(NTHR, 1) gauss_matmat_i8_kernel(const MI8Args 
                     for (int b = 0; b < MI8_BW; ++b) {
                         // K1-I8's lookup: byte offset (k << 7) & 0x1F80 in this lane's replica, k << 14 on the high word
                         const double tj = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab_l) +
-                                                                           ((kk[b] << 7) & 0x1F80));
+                                                                           ((kk[b] * (TAB_REP * 8)) & ((TAB - 1) * TAB_REP * 8)));
                         const double ts = __hiloint2double(__double2hiint(tj) + kk[b] * (1 << 14), __double2loint(tj));
                         double e = fma(ts, q[b], ts);
                         const int cl = colOff + k0 + b;
