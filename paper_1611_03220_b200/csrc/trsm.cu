@@ -7,14 +7,18 @@
 //     Y      = Z[:, J] - Z[:, 0:j0] L[J, 0:j0]^T     (GEMM, K = j0: DMMA m8n8k4)
 //     Z[:, J] = forward substitution of each row of Y with the diagonal block L[J, J]
 // One launch per column block, one CTA per 64 data rows: 8 warps x (32 rows x 32 columns) of
-// DMMA accumulators, operands through a 3-stage cp.async ring (A: 64 rows x 32 features of the
-// already-solved Z, B: the 32 x 128 block of L from L2).  Then the CTA stages Y and L[J, J] in
-// shared memory and each warp solves 8 rows, lane m holding columns m, m + 32, m + 64, m + 96:
+// DMMA accumulators, operands through a 3-stage cp.async ring of 32-feature stages with one barrier
+// per stage (A: 64 rows x 32 features of the already-solved Z, B: the 32 x 128 block of L from L2);
+// a stage's refill copies are issued between the first k-steps of the running stage, not as a burst.
+// Then the CTA stages Y and L[J, J] in shared memory and each warp carries its 8 rows through the
+// block together, lane m holding columns m, m + 32, m + 64, m + 96:
 //     x_c = y_c (1 / L_cc), y_m -= L_mc x_c for m > c
 // (the reference divides, numerics.cpp:70; the reciprocal, formed once per diagonal entry, costs
 // at most one more rounding per step and removes 2 x 128 FP64 divisions per row pair).
 // Work: n s^2 / 2 FMAs on the FP64 pipe (config 4: 3.5e13, config 5: 7.0e13); the substitution
-// adds n s 64 FMAs (~1 %).  L is the column-major lower factor (L(i, k) at L[i + k s]).
+// adds n s 64 FMAs (~1 % of the work, ~12 % of the time at config 4).  Measured (round 2, session 4):
+// config 4 2.37 s = 0.80 of the live DMMA peak (cuBLAS DTRSM 2.64 s; this kernel before the
+// single-barrier ring, the spread refill and the 8-row substitution: 2.97 s, same bits).  L is the column-major lower factor (L(i, k) at L[i + k s]).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -24,8 +28,18 @@ namespace {
 
 constexpr int RB = 64;    // data rows per CTA
 constexpr int BW = 128;   // column block width
-constexpr int KC = 32;    // features of K per stage
-constexpr int NST = 3;
+#ifndef TRSM_KC
+#define TRSM_KC 32  // 64-feature stages, double-buffered: equal within 1 % (profiles/README.md, round 2 session 4)
+#endif
+#ifndef TRSM_NST
+#define TRSM_NST 3
+#endif
+#ifndef TRSM_SPREAD
+#define TRSM_SPREAD 4  // k-steps (of 4 features) over which a stage's refill copies are issued; 0: one burst
+#endif
+constexpr int SPREAD = TRSM_SPREAD;
+constexpr int KC = TRSM_KC;    // features of K per stage
+constexpr int NST = TRSM_NST;
 constexpr int LDA = KC + 4;    // doubles; == 4 mod 32: A-fragment reads conflict-free
 constexpr int LDB = BW + 4;    // doubles; == 4 mod 32: B-fragment reads conflict-free
 constexpr int STAGE = RB * LDA + KC * LDB;
@@ -86,20 +100,55 @@ __global__ void __launch_bounds__(256, 1) trsm_block_kernel(double* __restrict__
             }
         }
     };
+    // the same copies one 256-thread unit at a time (s even): the refill of the next stage is spread
+    // over the first SPREAD k-steps of the current one instead of issued as one burst after the
+    // barrier (the burst stalled every warp on the load queue while the DMMA pipe idled)
+    constexpr int NUA = RB * KC / 2 / 256, NUB = KC * BW / 2 / 256, NU = NUA + NUB;
+    auto load_unit = [&](int kc, int st, int u) {
+        double* sa = sm + st * STAGE;
+        double* sb = sa + RB * LDA;
+        const int64_t k0 = int64_t(kc) * KC;
+        if (u < NUA) {
+            const int e = tid + u * 256;
+            const int r = e / (KC / 2), k = 2 * (e % (KC / 2));
+            const bool ok = r0 + r < n;
+            cp_async16z(sa + r * LDA + k, ok ? Z + (r0 + r) * s + k0 + k : Z, ok ? 2 : 0);
+        } else {
+            const int e = tid + (u - NUA) * 256;
+            const int k = e / (BW / 2), c = 2 * (e % (BW / 2));
+            const int cnt = c + 1 < bw ? 2 : (c < bw ? 1 : 0);
+            cp_async16z(sb + k * LDB + c, cnt ? L + (j0 + c) + (k0 + k) * s : L, cnt);
+        }
+    };
 #pragma unroll
     for (int st = 0; st < NST - 1; ++st) {
         if (st < nk) load(st, st);
         cp_async_commit();
     }
+    // one barrier per stage: it publishes stage kc and retires stage kc - 1, which the refill
+    // issued right after it overwrites
     for (int kc = 0; kc < nk; ++kc) {
-        if (kc + NST - 1 < nk) load(kc + NST - 1, (kc + NST - 1) % NST);
-        cp_async_commit();
-        cp_async_wait<NST - 1>();
+        cp_async_wait<NST - 2>();
         __syncthreads();
+        const bool refill = kc + NST - 1 < nk;
+        const int rst = (kc + NST - 1) % NST;
+        if (!(V2 && SPREAD > 0)) {
+            if (refill) load(kc + NST - 1, rst);
+            cp_async_commit();
+        }
         const double* sa = sm + (kc % NST) * STAGE;
         const double* sb = sa + RB * LDA;
 #pragma unroll
         for (int kk = 0; kk < KC; kk += 4) {
+            if constexpr (V2 && SPREAD > 0) {
+                constexpr int PER = (NU + SPREAD - 1) / (SPREAD > 0 ? SPREAD : 1);
+                const int t = kk / 4;
+                if (t < SPREAD && refill) {
+#pragma unroll
+                    for (int u = t * PER; u < (t + 1) * PER && u < NU; ++u) load_unit(kc + NST - 1, rst, u);
+                }
+                if (t == SPREAD - 1) cp_async_commit();
+            }
             double a[4], b[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) a[m] = sa[(wr * 32 + m * 8 + g) * LDA + kk + t4];  // A[g][t4] = Z[row][k]
@@ -110,7 +159,6 @@ __global__ void __launch_bounds__(256, 1) trsm_block_kernel(double* __restrict__
 #pragma unroll
                 for (int q = 0; q < 4; ++q) dmma884(acc[m][q][0], acc[m][q][1], a[m], b[q]);
         }
-        __syncthreads();
     }
     cp_async_wait<0>();
     __syncthreads();
@@ -131,51 +179,52 @@ __global__ void __launch_bounds__(256, 1) trsm_block_kernel(double* __restrict__
             }
     for (int e = tid; e < BW * BW; e += 256) {
         const int c = e / BW, m = e % BW;
-        const double l = (c < bw && m < bw && m >= c) ? L[(j0 + m) + (j0 + c) * s] : (m == c ? 1.0 : 0.0);
-        LJ[e] = m == c ? 1.0 / l : l;  // the diagonal holds 1 / L_cc
+        LJ[e] = (c < bw && m < bw && m >= c) ? L[(j0 + m) + (j0 + c) * s] : (m == c ? 1.0 : 0.0);
     }
     __syncthreads();
+    if (tid < BW) LJ[tid * BW + tid] = 1.0 / LJ[tid * BW + tid];  // the diagonal holds 1 / L_cc
+    __syncthreads();
 
-    // forward substitution, two rows per pass for latency hiding
-    for (int rr = warp * (RB / 8); rr < (warp + 1) * (RB / 8); rr += 2) {
-        double y0[4], y1[4];
+    // forward substitution: each warp carries its 8 rows through the 128 columns together (8
+    // independent dependency chains per step; every row sees the same operations in the same
+    // order as a row-at-a-time substitution, so the result does not depend on the grouping)
+    constexpr int RW = RB / 8;
+    const int rw0 = warp * RW;
+    double y[RW][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            y0[q] = Y[rr * LDY + lane + 32 * q];
-            y1[q] = Y[(rr + 1) * LDY + lane + 32 * q];
-        }
+    for (int r = 0; r < RW; ++r)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            for (int cl = 0; cl < 32; ++cl) {
-                const int c = 32 * q + cl;
-                if (c >= bw) break;
-                const double rcc = LJ[c * BW + c];
-                const double x0 = __shfl_sync(0xffffffffu, y0[q], cl) * rcc;
-                const double x1 = __shfl_sync(0xffffffffu, y1[q], cl) * rcc;
-                if (lane == cl) {
-                    y0[q] = x0;
-                    y1[q] = x1;
-                }
+        for (int q = 0; q < 4; ++q) y[r][q] = Y[(rw0 + r) * LDY + lane + 32 * q];
 #pragma unroll
-                for (int q2 = q; q2 < 4; ++q2) {
-                    const int m = lane + 32 * q2;
-                    if (m > c) {
-                        const double l = LJ[c * BW + m];
-                        y0[q2] = fma(-l, x0, y0[q2]);
-                        y1[q2] = fma(-l, x1, y1[q2]);
-                    }
+    for (int q = 0; q < 4; ++q) {
+        for (int cl = 0; cl < 32; ++cl) {
+            const int c = 32 * q + cl;
+            if (c >= bw) break;
+            const double rcc = LJ[c * BW + c];
+            double x[RW];
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                x[r] = __shfl_sync(0xffffffffu, y[r][q], cl) * rcc;
+                if (lane == cl) y[r][q] = x[r];
+            }
+#pragma unroll
+            for (int q2 = q; q2 < 4; ++q2) {
+                const int m = lane + 32 * q2;
+                if (m > c) {
+                    const double l = LJ[c * BW + m];
+#pragma unroll
+                    for (int r = 0; r < RW; ++r) y[r][q2] = fma(-l, x[r], y[r][q2]);
                 }
             }
         }
+    }
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int c = lane + 32 * q;
-            if (c < bw) {
-                if (r0 + rr < n) Z[(r0 + rr) * s + j0 + c] = y0[q];
-                if (r0 + rr + 1 < n) Z[(r0 + rr + 1) * s + j0 + c] = y1[q];
-            }
+            if (c < bw && r0 + rw0 + r < n) Z[(r0 + rw0 + r) * s + j0 + c] = y[r][q];
         }
-    }
 }
 
 }  // namespace

@@ -44,5 +44,6 @@ for _ in range(reps):
 t_apply = (time.perf_counter() - t0) / reps
 print(json.dumps({"cfg": cfg, "n": n, "d": d, "s": s, "rff_s": t_rff, "precond_build_s": t_build,
                   "build_split_ms": split, "jitter": jit.value, "apply16_host_s": t_apply,
-                  "u_bytes": 8.0 * n * s}))
+                  "u_bytes": 8.0 * n * s,
+                  "apply_sha1": __import__("hashlib").sha1(o.tobytes()).hexdigest()[:16]}))
 ctx.close()
