@@ -14,10 +14,18 @@
 // producer warp, so each SM keeps ~128 KB of loads in flight with a handful of instructions.
 // Partial tiles are zero-filled by the producer rather than masked per lane: mma.sync must run
 // in a converged warp (divergent masking around it hung the kernel).
-// Measured at config 5 (n = 524288, s = 16384, t = 16; ncu): pass 1 15.0 ms, pass 2 16.4 ms =
-// 4.4 TB/s, 0.68 of the measured HBM copy rate, with the DMMA sub-pipe ~53 % busy.  The FP64
-// datapath caps this kernel near 0.8: at the full copy rate (22 B/clk/SM = 2.8 elements) 16
-// FMAs per element need 69 % of the 64 FMA/clk/SM that DMMA and DFMA share.
+// Measured at config 5 (n = 524288, s = 16384, t = 16; ncu, round 2 session 4): pass 1 14.2 ms, pass 2
+// 14.8 ms = 4.7-4.8 TB/s, 0.72-0.74 of the measured HBM copy rate (round-2 start: 15.0 + 16.4 ms).
+// What the probes say (K6T_PROBE, profiles/README.md): pass 1's copy pipeline alone streams U at
+// 6.9 TB/s, so pass 1 is bound by its consumers (LDS + DMMA at ~55 % of the FP64 tensor rate with
+// 2-4 warps per sub-partition; 16 consumer warps instead of 8: -4 %); pass 2's copy pipeline alone
+// ran at 4.3 TB/s with 32-row CTAs because every CTA also pulls the whole W (2 MB) through L2 — a
+// third of its ingest — so 64-row CTAs (W re-read half as often, two 84 KB stages): -10 %.  The
+// FP64 datapath caps the kernel near 0.8 in any case: at the full copy rate (22 B/clk/SM = 2.8
+// elements) 16 FMAs per element need 69 % of the 64 FMA/clk/SM that DMMA and DFMA share.
+// Shared-memory strides are == 4 (mod 16) doubles and W carries an XOR column swizzle, so every
+// fragment read is conflict-free (ncu before: 2 and 2.7 wavefronts per LDS.64 too many; fixing it
+// did not change the time: the LSU pipe was at 25 / 45 %).
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_i8.cuh"
@@ -26,11 +34,37 @@ namespace krr {
 
 namespace {
 
+#ifndef K6T_PROBE
+#define K6T_PROBE 0  // A/B builds only (results invalid): 1 = no DMMA (copy pipeline + operand reads), 2 = no operand reads either
+#endif
+// W (s x T) is stored with the column XOR-swizzled by the feature row, so that pass 2's DMMA B
+// fragments (4 consecutive feature rows x 8 columns per load, rows 8 T bytes apart) read
+// conflict-free from the linearly copied chunk: T = 16: col ^ ((f & 3) << 2); T = 8: col ^ ((f & 2) << 1)
+template <int T>
+__host__ __device__ __forceinline__ int w_swz(int64_t f) {
+    return T == 16 ? int((f & 3) << 2) : int((f & 2) << 1);
+}
+#ifndef K6T_RB
+#define K6T_RB 64  // pass-2 rows per CTA: 64 rows x 2 stages re-read W half as often as 32 x 4 (-10 %, same bits)
+#endif
+#ifndef K6T_NSTB
+#define K6T_NSTB 2
+#endif
+__device__ __forceinline__ void k6t_mma(double& d0, double& d1, double a, double b) {
+    if (K6T_PROBE == 0) dmma884(d0, d1, a, b);
+    else if (K6T_PROBE == 1) { d0 += a; d1 += b; }
+}
+
 constexpr int NSTAGE = 4;
 constexpr int A_FB = 256;  // pass-1 feature block: 2 KB row segments (1 KB: 16.9 ms, 2 KB: 15.0 ms, 4 KB: 15.0 ms at config 5)
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
-constexpr int NCW = 8;                    // consumer warps
-constexpr int NTHREADS = 32 * (NCW + 1);  // + one producer warp
+#ifndef K6T_NCWA
+#define K6T_NCWA 16  // pass 1: 16 consumer warps (8: 4 % slower; each warp owns its features, so W does not depend on it)
+#endif
+constexpr int NCWA = K6T_NCWA;              // pass-1 consumer warps
+constexpr int NTHREADS_A = 32 * (NCWA + 1);  // + one producer warp
+constexpr int NCW = 8;                      // pass-2 consumer warps (they split K: the count fixes the summation order)
+constexpr int NTHREADS = 32 * (NCW + 1);
 
 // ---- pass 1: Wpart[split][f][T] = sum_{k in split} B[k][f] R[k][.] for an FB-feature block.
 // Consumer warp w owns features f0 + w FB/8 .. (FB/64 DMMA M tiles) x all T columns; K = rows,
@@ -39,15 +73,16 @@ constexpr int NTHREADS = 32 * (NCW + 1);  // + one producer warp
 template <int FB>
 struct PassA {
     static constexpr int KR = 4096 / FB;
-    static constexpr int LD = FB + 8;  // smem row stride (doubles), == 8 mod 32: A-fragment reads conflict-free
-    static constexpr int MT = FB / (8 * NCW);
+    static constexpr int LD = FB + 4;  // smem row stride (doubles), == 4 mod 16: the 4 feature rows of a half-warp's
+                                       // A-fragment read (8 consecutive doubles each) fall in distinct bank groups
+    static constexpr int MT = FB / (8 * NCWA);
     static constexpr int STAGE = KR * LD;  // doubles
     static constexpr int NST = 6;          // ring depth: ~192 KB of loads in flight per SM
     static constexpr size_t SMEM = size_t(NST) * STAGE * 8 + 2 * NST * 8 + 16;
 };
 
 template <int T, int FB>
-__global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* __restrict__ B, int64_t n, int64_t s,
+__global__ void __launch_bounds__(NTHREADS_A, 1) k6t_pass_a_kernel(const double* __restrict__ B, int64_t n, int64_t s,
                                                                   const double* __restrict__ R,
                                                                   double* __restrict__ Wpart, int64_t rows_per) {
     using P = PassA<FB>;
@@ -63,12 +98,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
     if (tid == 0) {
         for (int i = 0; i < P::NST; ++i) {
             tc::mbar_init(&full[i], 2);  // the producer's expect-tx arrive + its post-zero-fill arrive
-            tc::mbar_init(&empty[i], NCW);
+            tc::mbar_init(&empty[i], NCWA);
         }
         tc::mbar_fence_init();
     }
     __syncthreads();
-    if (warp == NCW) {  // producer
+    if (warp == NCWA) {  // producer
         for (int64_t c = 0; c < nchunk; ++c) {
             const int st = int(c % P::NST);
             if (c >= P::NST) tc::mbar_wait_sleep(&empty[st], uint32_t((c / P::NST - 1) & 1));
@@ -120,9 +155,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
             const double* b = bq[kk / 4];
 #pragma unroll
             for (int m = 0; m < MT; ++m) {
-                const double a = sb[(kk + t4) * P::LD + warp * (FB / NCW) + m * 8 + g];  // A[g][t4] = B[k][f]
+                const double a = sb[(kk + t4) * P::LD + warp * (FB / NCWA) + m * 8 + g];  // A[g][t4] = B[k][f]
 #pragma unroll
-                for (int j = 0; j < NT; ++j) dmma884(acc[m][j][0], acc[m][j][1], a, b[j]);
+                for (int j = 0; j < NT; ++j) k6t_mma(acc[m][j][0], acc[m][j][1], a, b[j]);
             }
         }
         __syncwarp();
@@ -130,13 +165,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
     }
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
-        const int64_t f = f0 + warp * (FB / NCW) + m * 8 + g;
+        const int64_t f = f0 + warp * (FB / NCWA) + m * 8 + g;
         if (f < s) {
             double* w = Wpart + (int64_t(blockIdx.y) * s + f) * T;
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                w[j * 8 + 2 * t4] = acc[m][j][0];
-                w[j * 8 + 2 * t4 + 1] = acc[m][j][1];
+                const int col = (j * 8 + 2 * t4) ^ w_swz<T>(f);  // the pair stays adjacent (bits 2-3 flip)
+                w[col] = acc[m][j][0];
+                w[col + 1] = acc[m][j][1];
             }
         }
     }
@@ -147,14 +183,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_a_kernel(const double* _
 // segments measured 2-3x slower), plus the 128 x T block of W.  The 8 consumer warps split a
 // stage's 128 features (16 each = 4 k-steps) and each accumulates all 4 x T/8 output tiles of
 // the block; the partial tiles are summed across warps in fixed order at the end.
-constexpr int B_RB = 32;
+constexpr int B_RB = K6T_RB;
 constexpr int B_KF = 128;
-constexpr int B_LD = B_KF + 8;  // == 8 mod 32 doubles: A-fragment reads conflict-free
+constexpr int B_LD = B_KF + 4;  // == 4 mod 16 doubles: the 4 rows of a half-warp's A-fragment read fall in distinct bank groups
+constexpr int NSTB = K6T_NSTB;  // pass-2 ring stages
 template <int T>
 struct PassB {
     static constexpr int STAGE = B_RB * B_LD + B_KF * T;
-    static_assert(NCW * B_RB * T <= NSTAGE * STAGE, "cross-warp partials reuse the stage buffers");
-    static constexpr size_t SMEM = size_t(NSTAGE) * STAGE * 8 + 2 * NSTAGE * 8 + 16;
+    static_assert(NCW * B_RB * T <= NSTB * STAGE, "cross-warp partials reuse the stage buffers");
+    static constexpr size_t SMEM = size_t(NSTB) * STAGE * 8 + 2 * NSTB * 8 + 16;
 };
 
 template <int T>
@@ -164,14 +201,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_b_kernel(const double* _
                                                                   double* __restrict__ Z) {
     extern __shared__ __align__(128) double sm[];
     double* red = sm;  // after the last stage: the cross-warp partials
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NSTAGE * PassB<T>::STAGE);
-    uint64_t* empty = full + NSTAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NSTB * PassB<T>::STAGE);
+    uint64_t* empty = full + NSTB;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
     const int64_t r0 = int64_t(blockIdx.x) * B_RB;
     const int rows = int(imin64(B_RB, n - r0));
     const int64_t nchunk = (s + B_KF - 1) / B_KF;
     if (tid == 0) {
-        for (int i = 0; i < NSTAGE; ++i) {
+        for (int i = 0; i < NSTB; ++i) {
             tc::mbar_init(&full[i], 2);  // the producer's expect-tx arrive + its post-zero-fill arrive
             tc::mbar_init(&empty[i], NCW);
         }
@@ -180,8 +217,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_b_kernel(const double* _
     __syncthreads();
     if (warp == NCW) {  // producer
         for (int64_t c = 0; c < nchunk; ++c) {
-            const int st = int(c % NSTAGE);
-            if (c >= NSTAGE) tc::mbar_wait_sleep(&empty[st], uint32_t((c / NSTAGE - 1) & 1));
+            const int st = int(c % NSTB);
+            if (c >= NSTB) tc::mbar_wait_sleep(&empty[st], uint32_t((c / NSTB - 1) & 1));
             const int64_t fb = c * B_KF;
             const int fv = int(imin64(B_KF, s - fb));
             const uint32_t seg = uint32_t(fv) * 8u;
@@ -211,20 +248,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k6t_pass_b_kernel(const double* _
         for (int j = 0; j < NT; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
     const int kw = warp * (B_KF / NCW);  // this warp's 16 features of each stage
     for (int64_t c = 0; c < nchunk; ++c) {
-        const int st = int(c % NSTAGE);
-        tc::mbar_wait(&full[st], uint32_t((c / NSTAGE) & 1));
+        const int st = int(c % NSTB);
+        tc::mbar_wait(&full[st], uint32_t((c / NSTB) & 1));
         const double* sb = sm + st * PassB<T>::STAGE;
         const double* sw = sb + B_RB * B_LD;
 #pragma unroll
         for (int kk = kw; kk < kw + B_KF / NCW; kk += 4) {
             double b[NT];
 #pragma unroll
-            for (int j = 0; j < NT; ++j) b[j] = sw[(kk + t4) * T + j * 8 + g];
+            for (int j = 0; j < NT; ++j) b[j] = sw[(kk + t4) * T + ((j * 8 + g) ^ w_swz<T>(t4))];  // kk % 4 == 0
 #pragma unroll
             for (int m = 0; m < MT; ++m) {
                 const double a = sb[(m * 8 + g) * B_LD + kk + t4];  // A[g][t4] = B[row][f]
 #pragma unroll
-                for (int j = 0; j < NT; ++j) dmma884(acc[m][j][0], acc[m][j][1], a, b[j]);
+                for (int j = 0; j < NT; ++j) k6t_mma(acc[m][j][0], acc[m][j][1], a, b[j]);
             }
         }
         __syncwarp();
@@ -260,7 +297,7 @@ void k6t_run(const double* B, int64_t n, int64_t s, const double* R, double lamb
             dim3 ga(unsigned((s + A_FB - 1) / A_FB), unsigned(nsplit));
             KRR_CUDA(cudaFuncSetAttribute(k6t_pass_a_kernel<T, A_FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(PassA<A_FB>::SMEM)));
-            k6t_pass_a_kernel<T, A_FB><<<ga, NTHREADS, PassA<A_FB>::SMEM, stream>>>(B, n, s, R, Wpart, rows_per);
+            k6t_pass_a_kernel<T, A_FB><<<ga, NTHREADS_A, PassA<A_FB>::SMEM, stream>>>(B, n, s, R, Wpart, rows_per);
             KRR_LAUNCH_CHECK();
             reduce_rows_launch(Wpart, nsplit, s * T, W, stream);
         } else {
