@@ -1,7 +1,8 @@
-"""Small Woodbury build + applies for compute-sanitizer runs (memcheck / racecheck / synccheck):
-K3-I8 Gram, K4 Cholesky, K5 TRSM (several column blocks, ragged last block), K6 and K6T.
+"""Small Woodbury builds + applies checked against numpy (K3-I8 Gram, K4 Cholesky, K5 TRSM over
+several column blocks with a ragged last block, K6 and K6T): a quick stand-alone check, and the
+workload for compute-sanitizer where that tool is available (it is closed on this GPU pool).
 
-  compute-sanitizer --tool memcheck python tools/sanitize_build.py
+  python tools/sanitize_build.py
 """
 import sys
 from pathlib import Path
