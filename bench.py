@@ -365,19 +365,23 @@ def main():
     tot, k1 = C.c_double(), C.c_double()
     if args.warmup > 0:
         _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, lam, args.warmup, C.byref(tot), C.byref(k1)))
+    import torch
+    torch.cuda.set_device(local)  # torch shares the device's primary context with the library
     D.barrier()
+    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = ctx.launches
+    # K steps timed on the device (CUDA events on the context's stream, synchronised on both sides)
     _lib.check(_lib.LIB.krr_bench_matvec(ctx.handle, lam, args.steps, C.byref(tot), C.byref(k1)))
     launches = ctx.launches - launches0
+    torch.cuda.synchronize()
     clk = clocks.stop()
     D.barrier()
     total_ms = D.max(tot.value)
     k1_ms = k1.value
 
     # ---- e2e through the reference-facing C-ABI call with pinned host buffers
-    import torch
     hv = torch.from_numpy(np.random.default_rng(7).standard_normal(n)).pin_memory()
     ho = torch.empty(n, dtype=torch.float64).pin_memory()
     _lib.check(_lib.LIB.krr_kernel_matvec(ctx.handle, lam, hv.data_ptr(), 1, ho.data_ptr()))  # warm
