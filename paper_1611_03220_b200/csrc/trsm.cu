@@ -40,6 +40,7 @@ constexpr int BW = 128;   // column block width
 constexpr int SPREAD = TRSM_SPREAD;
 constexpr int KC = TRSM_KC;    // features of K per stage
 constexpr int NST = TRSM_NST;
+static_assert(NST >= 2 && KC % 4 == 0 && SPREAD <= KC / 4, "K5: ring depth / stage width / refill spread");
 constexpr int LDA = KC + 4;    // doubles; == 4 mod 32: A-fragment reads conflict-free
 constexpr int LDB = BW + 4;    // doubles; == 4 mod 32: B-fragment reads conflict-free
 constexpr int STAGE = RB * LDA + KC * LDB;
