@@ -286,10 +286,10 @@ def run_reference(args):
               f"oracle/krr_oracle.cpp on {threads} threads")
     line = {
         "impl": "reference", "metric": "kernel-matvec Gevals/s (n=1M, fp64)", "value": value,
-        "unit": "Gevals/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "unit": "Gevals/s", "n_gpus": args.gpus, "gpus_used": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE config 4 generator, seed 0)",
-        "config": {"workload": "config4 kernel mat-vec", "n": n, "d": CFG4["d"], "sigma": CFG4["sigma"],
+        "config": {"workload": "config4 (K + lambda I) v, K on the fly", "n": n, "d": CFG4["d"], "sigma": CFG4["sigma"],
                    "lambda": CFG4["lam"], "rows_per_step": rows},
         "cpu_baseline": {"value": value, "unit": "Gevals/s", "cores": threads, "kind": "port",
                          "sample": sample},
