@@ -38,3 +38,33 @@ def test_bench_rejects_world_mismatch():
                          env=env, capture_output=True, text=True, timeout=120)
     assert out.returncode != 0
     assert "WORLD_SIZE" in out.stderr
+
+
+def test_reference_arm_line_and_no_product_code():
+    """`bench.py --impl reference` (the CPU restatement on the host cores): one JSON line with the
+    product arm's metric / unit / workload, n_gpus mirroring the launch, a cpu_baseline block — and
+    libkrr_b200.so is never mapped into that process."""
+    code = (
+        "import sys, runpy\n"
+        f"sys.argv = [{str(ROOT / 'bench.py')!r}, '--impl', 'reference', '--n', '4096', '--steps', '1', "
+        "'--warmup', '1', '--no-c1-reference']\n"
+        "try:\n"
+        f"    runpy.run_path({str(ROOT / 'bench.py')!r}, run_name='__main__')\n"
+        "except SystemExit:\n"
+        "    pass\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "print('MAPPED_PRODUCT', 'libkrr_b200' in maps, 'MAPPED_ORACLE', 'liboracle' in maps)\n"
+    )
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=_env(), capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = lines[0]
+    assert line["impl"] == "reference" and line["n_gpus"] == 1 and line["gpus_used"] == 0
+    assert line["metric"] == "kernel-matvec Gevals/s (n=1M, fp64)" and line["unit"] == "Gevals/s"
+    assert line["higher_is_better"] is True and line["value"] > 0
+    assert line["config"]["workload"].startswith("config4") and line["config"]["n"] == 4096
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert "MAPPED_PRODUCT False MAPPED_ORACLE True" in out.stdout
