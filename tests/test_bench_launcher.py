@@ -68,3 +68,22 @@ def test_reference_arm_line_and_no_product_code():
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert "MAPPED_PRODUCT False MAPPED_ORACLE True" in out.stdout
+
+
+def test_multi_rank_watchdog_prints_the_measured_line():
+    """A stalled multi-rank PCG leg must not cost the measured mat-vec line: the watchdog prints it
+    (leg marked abandoned) from rank 0 and ends the process with status 0."""
+    code = (
+        "import sys, time, json\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import bench\n"
+        "bench.arm_watchdog(0.3, 0, {'metric': 'm', 'value': 1.0})\n"
+        "time.sleep(30)\n"
+        "print('NOT REACHED')\n"
+    )
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=_env(), capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "NOT REACHED" not in out.stdout
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][0])
+    assert line["value"] == 1.0 and "abandoned" in line["pcg_leg"]["error"]
